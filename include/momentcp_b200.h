@@ -1,0 +1,136 @@
+/*
+ * momentcp_b200 -- C ABI of the B200-native implicit moment-tensor CP f+grad path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and status codes, no torch
+ * types.  Each entry point replaces one call site of the reference Python package
+ * `momentcp` (paths relative to the reference root):
+ *
+ *   mcp_load_obs         ObservationSet.__post_init__         pkg/src/momentcp/dense.py:81-111
+ *                        (V upload; fp32 is kept fp32 on device, converted exactly in-register)
+ *   mcp_fg               fg_implicit                          pkg/src/momentcp/objective.py:77-94
+ *                        (= ttsv_batch :94-107 + _finish objective.py:51-56 on device)
+ *   mcp_fg_packed        packed_fg_implicit's fg(x) closure   pkg/src/momentcp/optimize.py:123-134
+ *                        (x = [lam; vec_F(A)], g likewise -- optimize.py:104-120)
+ *   mcp_ttsv_batch       ttsv_batch                           pkg/src/momentcp/implicit.py:94-107
+ *   mcp_data_norm_sq     data_norm_sq                         pkg/src/momentcp/implicit.py:116-121
+ *   mcp_fg_partial_device / mcp_fg_finish_device
+ *                        the same evaluation split at the additive [Y | w] boundary so a
+ *                        row-sharded ObservationSet can all-reduce between them (no reference
+ *                        counterpart: the reference is single-process).
+ *
+ * Error behaviour mirrors the reference: argument errors (d < 2, shape mismatch, non-finite
+ * inputs) return MCP_ERR_ARG, which the Python host raises as ValueError exactly where the
+ * reference raises it; CUDA failures return MCP_ERR_CUDA (RuntimeError).  The message is
+ * available from mcp_last_error(ctx) (or mcp_last_error(NULL) for a failed mcp_create).
+ *
+ * Threading: every call on a context is serialised by a per-context mutex, so concurrent
+ * callers (momentcp.multistart(threads>1), optimize.py:484-493) are safe; all reductions are
+ * fixed-order, so results are bitwise reproducible run to run and independent of threading.
+ */
+#ifndef MOMENTCP_B200_H
+#define MOMENTCP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCP_ABI_VERSION 1
+
+/* status codes */
+#define MCP_OK 0
+#define MCP_ERR_ARG 1   /* invalid argument: Python raises ValueError   */
+#define MCP_ERR_CUDA 2  /* CUDA/driver failure: Python raises RuntimeError */
+#define MCP_ERR_STATE 3 /* call out of order (e.g. fg before load_obs)   */
+
+/* element type of V as handed to mcp_load_obs */
+#define MCP_F64 0
+#define MCP_F32 1
+
+/* host layout of V: VAR_MAJOR = reference ObservationSet.V (n x p, C order, row i = variable i,
+ * leading dimension ld >= p); OBS_MAJOR = p x n C order (observation l contiguous, ld >= n). */
+#define MCP_VAR_MAJOR 0
+#define MCP_OBS_MAJOR 1
+
+/* arithmetic mode */
+#define MCP_MODE_FP64 0   /* bit-faithful mode: IEEE fp64 arithmetic, fixed-order reductions */
+#define MCP_MODE_TF32X3 1 /* fast mode: 3xTF32 split on tcgen05, fp64 across tiles (<= 1e-4) */
+
+typedef struct mcp_ctx mcp_ctx;
+
+int mcp_abi_version(void);
+
+/* Last error message of ctx, or of the calling thread's last failed mcp_create if ctx==NULL. */
+const char* mcp_last_error(const mcp_ctx* ctx);
+
+/* Create a context bound to CUDA device `device` (one context per GPU / rank). */
+int mcp_create(mcp_ctx** out, int device);
+int mcp_destroy(mcp_ctx* ctx);
+
+/* Number of SMs of the bound device (the persistent-grid width the kernels use). */
+int mcp_device_sms(const mcp_ctx* ctx);
+
+/*
+ * Upload the observation matrix (host memory).  n variables, p observations.
+ * nu: p strictly positive weights, or NULL for uniform weights equal to nu_const
+ * (nu_const <= 0 means 1/p, the reference default dense.py:90-91; a row shard of a larger
+ * set passes 1/p_total).  Validation matches dense.py:83-105 (finite V, positive finite nu).
+ */
+int mcp_load_obs(mcp_ctx* ctx, const void* V, int dtype, int layout, int64_t n, int64_t p,
+                 int64_t ld, const double* nu, double nu_const);
+
+/* Same, from device memory on the context's device (e.g. data generated on the GPU). */
+int mcp_load_obs_device(mcp_ctx* ctx, const void* dV, int dtype, int layout, int64_t n,
+                        int64_t p, int64_t ld, const double* dnu, double nu_const);
+
+/* Shape of the loaded observation set. */
+int mcp_obs_shape(const mcp_ctx* ctx, int64_t* n, int64_t* p);
+
+/*
+ * One f+grad evaluation at (lam, A), host buffers.  A and g_A are n x r column-major
+ * (Fortran order, the reference's packed layout).  alpha only shifts f.
+ */
+int mcp_fg(mcp_ctx* ctx, int d, int r, const double* lam, const double* A_colmajor, double alpha,
+           int mode, double* f, double* g_lam, double* g_A_colmajor);
+
+/* Packed form: x = [lam (r); vec_F(A) (n*r)], g the same layout (optimize.py:104-134). */
+int mcp_fg_packed(mcp_ctx* ctx, int d, int r, const double* x, double alpha, int mode, double* f,
+                  double* g);
+
+/* Y = V diag(nu) (V^T A)^(d-1), n x r column-major (implicit.py:94-107). */
+int mcp_ttsv_batch(mcp_ctx* ctx, int d, int r, const double* A_colmajor, int mode,
+                   double* Y_colmajor);
+
+/* ||X||^2 = nu^T (V^T V)^d nu (implicit.py:116-121), without the p x p Gram. */
+int mcp_data_norm_sq(mcp_ctx* ctx, int d, int mode, double* out);
+
+/* Part `part` of `nparts` of the symmetric tile-pair sum of ||X||^2 (multi-GPU split). */
+int mcp_data_norm_sq_part(mcp_ctx* ctx, int d, int mode, int part, int nparts, double* out);
+
+/*
+ * Device-resident pieces (all pointers are device memory on ctx's device; stream may be NULL
+ * for the context's own stream).
+ *   dx   : [lam (r); vec_F(A) (n*r)]
+ *   dYw  : [vec_F(Y) (n*r); w (r)]  additive over row shards -> all-reduce(sum) between calls
+ *   dout : [f (1); g_lam (r); vec_F(g_A) (n*r)]
+ */
+int mcp_fg_partial_device(mcp_ctx* ctx, int d, int r, const double* dx, int mode, double* dYw,
+                          void* stream);
+int mcp_fg_finish_device(mcp_ctx* ctx, int d, int r, const double* dx, const double* dYw,
+                         double alpha, double* dout, void* stream);
+/* partial + finish in one call (single-GPU device-resident evaluation). */
+int mcp_fg_device(mcp_ctx* ctx, int d, int r, const double* dx, double alpha, int mode,
+                  double* dout, void* stream);
+
+/* Kernel launches issued by the last evaluation call (for the bench's gpu_launches claim). */
+int mcp_last_launch_count(const mcp_ctx* ctx);
+
+/* Name of the K1 kernel variant the last evaluation used (diagnostics / bench config). */
+const char* mcp_last_variant(const mcp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOMENTCP_B200_H */

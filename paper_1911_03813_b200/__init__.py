@@ -1,0 +1,41 @@
+"""B200-native implicit moment-tensor CP f+grad (arXiv 1911.03813), drop-in for ``momentcp``.
+
+The hot path of the reference package -- function/gradient evaluation of a rank-r symmetric
+CP model against the d-th empirical moment tensor of p observations, computed from the n x p
+observation matrix without forming the n^d tensor, plus the one-time ||X||^2 constant and the
+packed adapter handed to the quasi-Newton driver -- re-built as hand-written sm_100a CUDA
+kernels behind a C ABI (include/momentcp_b200.h).  Names and signatures follow the reference
+exports (pkg/src/momentcp/__init__.py:14-68) for that path.
+"""
+
+__version__ = "0.1.0"
+
+from .dense import ObservationSet
+from .implicit import (
+    GramCache,
+    SymKruskal,
+    build_gram_cache,
+    data_norm_sq,
+    kruskal_norm_sq,
+    model_data_inner,
+    ttsv_batch,
+)
+from .objective import FgResult, fg_implicit
+from .optimize import FgCallback, pack, packed_fg_implicit, unpack
+
+__all__ = [
+    "FgCallback",
+    "FgResult",
+    "GramCache",
+    "ObservationSet",
+    "SymKruskal",
+    "build_gram_cache",
+    "data_norm_sq",
+    "fg_implicit",
+    "kruskal_norm_sq",
+    "model_data_inner",
+    "pack",
+    "packed_fg_implicit",
+    "ttsv_batch",
+    "unpack",
+]

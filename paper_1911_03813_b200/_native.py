@@ -1,0 +1,226 @@
+"""ctypes binding of the C ABI in ``include/momentcp_b200.h`` (``_lib/libmomentcp_b200.so``).
+
+There is no CPU fallback: if the shared library is missing, or no B200 is visible, every entry
+point raises.  Argument errors reported by the library (``MCP_ERR_ARG``) surface as
+``ValueError`` -- the exception the reference raises for the same conditions
+(pkg/src/momentcp/objective.py:38-48, pkg/src/momentcp/implicit.py:102-105) -- and CUDA failures
+as ``RuntimeError``.  ctypes releases the GIL for the duration of each call; the library
+serialises calls per context, so pool threads may share one observation set
+(pkg/src/momentcp/optimize.py:484-493).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmomentcp_b200.so")
+
+MCP_OK, MCP_ERR_ARG, MCP_ERR_CUDA, MCP_ERR_STATE = 0, 1, 2, 3
+MCP_F64, MCP_F32 = 0, 1
+MCP_VAR_MAJOR, MCP_OBS_MAJOR = 0, 1
+MODES = {"fp64": 0, "tf32x3": 1}
+
+# name -> (restype, argtypes); every symbol include/momentcp_b200.h declares
+_c_void_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_dp = ctypes.POINTER(ctypes.c_double)
+SIGNATURES = {
+    "mcp_abi_version": (ctypes.c_int, []),
+    "mcp_last_error": (ctypes.c_char_p, [_c_void_p]),
+    "mcp_create": (ctypes.c_int, [ctypes.POINTER(_c_void_p), ctypes.c_int]),
+    "mcp_destroy": (ctypes.c_int, [_c_void_p]),
+    "mcp_device_sms": (ctypes.c_int, [_c_void_p]),
+    "mcp_load_obs": (ctypes.c_int, [_c_void_p, _c_void_p, ctypes.c_int, ctypes.c_int, _i64, _i64,
+                                    _i64, _c_void_p, ctypes.c_double]),
+    "mcp_load_obs_device": (ctypes.c_int, [_c_void_p, _c_void_p, ctypes.c_int, ctypes.c_int, _i64,
+                                           _i64, _i64, _c_void_p, ctypes.c_double]),
+    "mcp_obs_shape": (ctypes.c_int, [_c_void_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "mcp_fg": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p, _c_void_p,
+                              ctypes.c_double, ctypes.c_int, _dp, _c_void_p, _c_void_p]),
+    "mcp_fg_packed": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                     ctypes.c_double, ctypes.c_int, _dp, _c_void_p]),
+    "mcp_ttsv_batch": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                      ctypes.c_int, _c_void_p]),
+    "mcp_data_norm_sq": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _dp]),
+    "mcp_data_norm_sq_part": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, _dp]),
+    "mcp_fg_partial_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                             ctypes.c_int, _c_void_p, _c_void_p]),
+    "mcp_fg_finish_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                            _c_void_p, ctypes.c_double, _c_void_p, _c_void_p]),
+    "mcp_fg_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                     ctypes.c_double, ctypes.c_int, _c_void_p, _c_void_p]),
+    "mcp_last_launch_count": (ctypes.c_int, [_c_void_p]),
+    "mcp_last_variant": (ctypes.c_char_p, [_c_void_p]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library():
+    """Load (once) and type the C ABI; raises if the native build is missing."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"native library not built: {LIB_PATH} is missing "
+                    "(run `python -c 'import __graft_entry__ as g; g.build()'`); "
+                    "there is no CPU fallback for this path"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def mode_code(mode: str | None) -> int:
+    if mode is None:
+        mode = "fp64"
+    try:
+        return MODES[mode]
+    except KeyError:
+        raise ValueError(f"unknown mode {mode!r}; expected one of {sorted(MODES)}") from None
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Context:
+    """One device context holding one observation set (mcp_ctx*)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load_library()
+        h = ctypes.c_void_p()
+        rc = self._lib.mcp_create(ctypes.byref(h), int(device))
+        if rc != MCP_OK:
+            msg = self._lib.mcp_last_error(None).decode()
+            raise RuntimeError(f"mcp_create(device={device}) failed: {msg}")
+        self._h = h
+        self.device = int(device)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.mcp_destroy(h)
+            except Exception:  # noqa: BLE001 -- interpreter teardown
+                pass
+            self._h = None
+
+    # -- error mapping --------------------------------------------------------------------
+    def _check(self, rc: int, what: str) -> None:
+        if rc == MCP_OK:
+            return
+        msg = self._lib.mcp_last_error(self._h).decode()
+        if rc == MCP_ERR_ARG:
+            raise ValueError(msg)
+        raise RuntimeError(f"{what}: {msg}")
+
+    @property
+    def sms(self) -> int:
+        return int(self._lib.mcp_device_sms(self._h))
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self._lib.mcp_last_launch_count(self._h))
+
+    @property
+    def last_variant(self) -> str:
+        return self._lib.mcp_last_variant(self._h).decode()
+
+    # -- observation upload ---------------------------------------------------------------
+    def load_obs_host(self, V: np.ndarray, layout: int, nu: np.ndarray | None, nu_const: float):
+        if V.dtype == np.float32:
+            dt = MCP_F32
+        else:
+            V = np.ascontiguousarray(V, dtype=np.float64)
+            dt = MCP_F64
+        V = np.ascontiguousarray(V)
+        if layout == MCP_VAR_MAJOR:
+            n, p = V.shape
+            ld = p
+        else:
+            p, n = V.shape
+            ld = n
+        nu_arr = None if nu is None else np.ascontiguousarray(nu, dtype=np.float64)
+        rc = self._lib.mcp_load_obs(self._h, _ptr(V), dt, layout, n, p, ld,
+                                    None if nu_arr is None else _ptr(nu_arr), float(nu_const))
+        self._check(rc, "mcp_load_obs")
+
+    def load_obs_device(self, V_ptr: int, dtype_code: int, layout: int, n: int, p: int, ld: int,
+                        nu_ptr: int | None, nu_const: float):
+        rc = self._lib.mcp_load_obs_device(self._h, ctypes.c_void_p(V_ptr), dtype_code, layout,
+                                           n, p, ld,
+                                           None if nu_ptr is None else ctypes.c_void_p(nu_ptr),
+                                           float(nu_const))
+        self._check(rc, "mcp_load_obs_device")
+
+    # -- evaluations (host buffers) --------------------------------------------------------
+    def fg_packed(self, x: np.ndarray, n: int, d: int, r: int, alpha: float, mode: str | None):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        g = np.empty(r + n * r, dtype=np.float64)
+        f = ctypes.c_double()
+        rc = self._lib.mcp_fg_packed(self._h, int(d), int(r), _ptr(x), float(alpha),
+                                     mode_code(mode), ctypes.byref(f), _ptr(g))
+        self._check(rc, "mcp_fg_packed")
+        return f.value, g
+
+    def fg(self, lam: np.ndarray, A_fortran: np.ndarray, d: int, alpha: float, mode: str | None):
+        n, r = A_fortran.shape
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        A_fortran = np.asfortranarray(A_fortran, dtype=np.float64)
+        g_lam = np.empty(r, dtype=np.float64)
+        g_A = np.empty((n, r), dtype=np.float64, order="F")
+        f = ctypes.c_double()
+        rc = self._lib.mcp_fg(self._h, int(d), int(r), _ptr(lam), _ptr(A_fortran), float(alpha),
+                              mode_code(mode), ctypes.byref(f), _ptr(g_lam), _ptr(g_A))
+        self._check(rc, "mcp_fg")
+        return f.value, g_lam, g_A
+
+    def ttsv_batch(self, A_fortran: np.ndarray, d: int, mode: str | None) -> np.ndarray:
+        n, r = A_fortran.shape
+        A_fortran = np.asfortranarray(A_fortran, dtype=np.float64)
+        Y = np.empty((n, r), dtype=np.float64, order="F")
+        rc = self._lib.mcp_ttsv_batch(self._h, int(d), int(r), _ptr(A_fortran), mode_code(mode),
+                                      _ptr(Y))
+        self._check(rc, "mcp_ttsv_batch")
+        return Y
+
+    def data_norm_sq(self, d: int, mode: str | None, part: int = 0, nparts: int = 1) -> float:
+        out = ctypes.c_double()
+        if nparts == 1:
+            rc = self._lib.mcp_data_norm_sq(self._h, int(d), mode_code(mode), ctypes.byref(out))
+        else:
+            rc = self._lib.mcp_data_norm_sq_part(self._h, int(d), mode_code(mode), int(part),
+                                                 int(nparts), ctypes.byref(out))
+        self._check(rc, "mcp_data_norm_sq")
+        return out.value
+
+    # -- evaluations (device pointers, caller's stream) ------------------------------------
+    def fg_partial_device(self, d, r, dx_ptr, mode, dYw_ptr, stream_ptr):
+        rc = self._lib.mcp_fg_partial_device(self._h, int(d), int(r), ctypes.c_void_p(dx_ptr),
+                                             mode_code(mode), ctypes.c_void_p(dYw_ptr),
+                                             ctypes.c_void_p(stream_ptr))
+        self._check(rc, "mcp_fg_partial_device")
+
+    def fg_finish_device(self, d, r, dx_ptr, dYw_ptr, alpha, dout_ptr, stream_ptr):
+        rc = self._lib.mcp_fg_finish_device(self._h, int(d), int(r), ctypes.c_void_p(dx_ptr),
+                                            ctypes.c_void_p(dYw_ptr), float(alpha),
+                                            ctypes.c_void_p(dout_ptr), ctypes.c_void_p(stream_ptr))
+        self._check(rc, "mcp_fg_finish_device")
+
+    def fg_device(self, d, r, dx_ptr, alpha, mode, dout_ptr, stream_ptr):
+        rc = self._lib.mcp_fg_device(self._h, int(d), int(r), ctypes.c_void_p(dx_ptr),
+                                     float(alpha), mode_code(mode), ctypes.c_void_p(dout_ptr),
+                                     ctypes.c_void_p(stream_ptr))
+        self._check(rc, "mcp_fg_device")

@@ -1,0 +1,617 @@
+// C ABI of the momentcp B200 path (see include/momentcp_b200.h for the reference mapping).
+//
+// A context owns: the observation set resident in HBM (observation-major, padded), the
+// per-evaluation workspaces, pinned staging for the host entry points and one CUDA graph per
+// (d, r, mode) that replays  H2D(x) -> prep -> K1 -> K3 -> K4 -> D2H(f, g)  with one sync.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "momentcp_b200.h"
+#include "k1_fp64.cuh"
+#include "k5_gram.cuh"
+#include "k_aux.cuh"
+#include "k1_dispatch.h"
+
+using namespace mcp;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct GraphEntry {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+// Transpose a variable-major n x ld source (row i = variable) into the observation-major
+// p_pad x ldv device layout, zero padding included (dst pre-zeroed).
+template <typename T>
+__global__ void k_transpose_in(const T* __restrict__ src, int64_t n, int64_t p, int64_t ld,
+                               T* __restrict__ dst, int64_t ldv) {
+  __shared__ T tile[32][33];
+  const int64_t l0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t i = i0 + k, l = l0 + threadIdx.x;
+    if (i < n && l < p) tile[k][threadIdx.x] = src[i * ld + l];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t l = l0 + k, i = i0 + threadIdx.x;
+    if (i < n && l < p) dst[l * ldv + i] = tile[threadIdx.x][k];
+  }
+}
+
+template <typename T>
+__global__ void k_count_nonfinite(const T* __restrict__ V, int64_t total, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    local += isfinite((double)V[i]) ? 0ull : 1ull;
+  if (local) atomicAdd(bad, local);
+}
+
+__global__ void k_check_nu(const double* __restrict__ nu, int64_t p, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p;
+       i += (int64_t)gridDim.x * blockDim.x)
+    local += (isfinite(nu[i]) && nu[i] > 0.0) ? 0ull : 1ull;
+  if (local) atomicAdd(bad, local);
+}
+
+}  // namespace
+
+struct mcp_ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  mutable std::mutex mu;
+  std::string err;
+
+  bool loaded = false;
+  int dtype = MCP_F64;
+  int64_t n = 0, p = 0, p_pad = 0, ldv = 0;
+  void* dV = nullptr;
+  double* dnu = nullptr;  // nullptr => uniform nu_const
+  double nu_const = 0.0;
+
+  DevBuf dx, dout, dYw, dAfrag, dYpart, dwpart, dG, dC, dpart, dscalar, dflag;
+  void* hx = nullptr;
+  size_t hx_bytes = 0;
+  void* hout = nullptr;
+  size_t hout_bytes = 0;
+
+  std::map<std::tuple<int, int, int>, GraphEntry> graphs;
+  int last_launches = 0;
+  std::string variant = "none";
+
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+};
+
+#define CUDA_TRY(ctx, expr)                                                               \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      (void)cudaGetLastError();                                                           \
+      return (ctx)->fail(MCP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    }                                                                                     \
+  } while (0)
+
+namespace {
+
+void drop_graphs(mcp_ctx* c) {
+  for (auto& kv : c->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  }
+  c->graphs.clear();
+}
+
+int ensure(mcp_ctx* c, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return MCP_OK;
+  drop_graphs(c);  // graphs hold raw pointers into the old buffer
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  CUDA_TRY(c, cudaMalloc(&b.p, bytes));
+  b.bytes = bytes;
+  return MCP_OK;
+}
+
+int ensure_host(mcp_ctx* c, void*& p, size_t& have, size_t bytes) {
+  if (have >= bytes) return MCP_OK;
+  drop_graphs(c);
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  have = 0;
+  CUDA_TRY(c, cudaMallocHost(&p, bytes));
+  have = bytes;
+  return MCP_OK;
+}
+
+inline int grid_for(int64_t total, int threads, int cap) {
+  int64_t b = (total + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+// Shape of one evaluation's K1 launch.
+struct EvalPlan {
+  K1Variant k1;
+  int d = 0, r = 0;
+};
+
+int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
+  if (r < 1) return c->fail(MCP_ERR_ARG, "rank must be >= 1, got " + std::to_string(r));
+  if (mode != MCP_MODE_FP64)
+    return c->fail(MCP_ERR_ARG, "mode " + std::to_string(mode) + " is not available in this build");
+  pl.d = d;
+  pl.r = r;
+  std::string why;
+  if (!k1_select(c->dtype, c->n, r, c->p_pad, c->sms, pl.k1, why))
+    return c->fail(MCP_ERR_ARG, why);
+  int rc;
+  const int64_t n = c->n;
+  if ((rc = ensure(c, c->dx, sizeof(double) * (r + n * r + 1)))) return rc;
+  if ((rc = ensure(c, c->dout, sizeof(double) * (1 + r + n * r)))) return rc;
+  if ((rc = ensure(c, c->dYw, sizeof(double) * (n * r + r)))) return rc;
+  if ((rc = ensure(c, c->dAfrag, sizeof(double) * pl.k1.afrag_elems))) return rc;
+  if ((rc = ensure(c, c->dYpart, sizeof(double) * pl.k1.ypart_elems))) return rc;
+  if ((rc = ensure(c, c->dwpart, sizeof(double) * pl.k1.wpart_elems))) return rc;
+  if ((rc = ensure(c, c->dG, sizeof(double) * (size_t)r * r))) return rc;
+  if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
+  return MCP_OK;
+}
+
+// prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows.
+int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
+                    cudaStream_t s) {
+  const K1Variant& v = pl.k1;
+  const int n = (int)c->n, r = pl.r;
+  k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(
+      dx + r, n, r, v.RB, v.rbs, v.n_chunks * 16, (double*)c->dAfrag.p);
+  int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, (const double*)c->dAfrag.p, pl.d,
+                     (double*)c->dYpart.p, (double*)c->dwpart.p, s);
+  if (rc) return c->fail(MCP_ERR_CUDA, "K1 launch failed");
+  const int64_t red_items = (int64_t)v.rbs * n * v.RB + (int64_t)v.rbs * v.RB;
+  k_reduce_partials<<<grid_for(red_items, 256, 8 * c->sms), 256, 0, s>>>(
+      (const double*)c->dYpart.p, (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
+      dYw);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches = 3;
+  c->variant = v.name;
+  return MCP_OK;
+}
+
+// K4: tail from (x, Yw) -> out = [f ; g_lam ; vec_F(g_A)].
+int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
+                   const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
+  const int n = (int)c->n;
+  k_tail_gram<<<grid_for((int64_t)r * r, 128, 8 * c->sms), 128, 0, s>>>(
+      dx, n, r, d, (double*)c->dG.p, (double*)c->dC.p);
+  k_tail_vec<<<1, 256, sizeof(double) * r, s>>>(dx, dYw, (const double*)c->dG.p,
+                                                (const double*)c->dC.p, n, r, alpha_dev, alpha,
+                                                dout);
+  k_tail_ga<<<grid_for((int64_t)n * r, 256, 8 * c->sms), 256, 0, s>>>(
+      dx, dYw, (const double*)c->dC.p, n, r, d, dout);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches += 3;
+  return MCP_OK;
+}
+
+// Host entry: x (r + n r doubles) + alpha -> out (1 + r + n r doubles), through a cached graph.
+int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const double* A,
+                  double alpha) {
+  EvalPlan pl;
+  int rc = plan_eval(c, d, r, mode, pl);
+  if (rc) return rc;
+  const int64_t n = c->n;
+  const size_t xin = sizeof(double) * (r + n * r + 1);
+  const size_t xout = sizeof(double) * (1 + r + n * r);
+  if ((rc = ensure_host(c, c->hx, c->hx_bytes, xin))) return rc;
+  if ((rc = ensure_host(c, c->hout, c->hout_bytes, xout))) return rc;
+  double* hx = (double*)c->hx;
+  std::memcpy(hx, lam, sizeof(double) * r);
+  std::memcpy(hx + r, A, sizeof(double) * n * r);
+  hx[r + n * r] = alpha;
+
+  auto key = std::make_tuple(d, r, mode);
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    GraphEntry ge;
+    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    double* dx = (double*)c->dx.p;
+    cudaMemcpyAsync(dx, hx, xin, cudaMemcpyHostToDevice, c->stream);
+    int rc1 = enqueue_partial(c, pl, dx, (double*)c->dYw.p, c->stream);
+    int rc2 = rc1 ? rc1
+                  : enqueue_finish(c, d, r, dx, (const double*)c->dYw.p, dx + r + n * r, 0.0,
+                                   (double*)c->dout.p, c->stream);
+    cudaMemcpyAsync(c->hout, c->dout.p, xout, cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &ge.graph);
+    if (rc2) {
+      if (ge.graph) cudaGraphDestroy(ge.graph);
+      return rc2;
+    }
+    CUDA_TRY(c, ce);
+    CUDA_TRY(c, cudaGraphInstantiate(&ge.exec, ge.graph, 0));
+    it = c->graphs.emplace(key, ge).first;
+  } else {
+    c->last_launches = 6;
+    c->variant = pl.k1.name;
+  }
+  CUDA_TRY(c, cudaGraphLaunch(it->second.exec, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MCP_OK;  // results in c->hout = [f ; g_lam ; vec_F(g_A)]
+}
+
+template <typename T>
+int upload_obs(mcp_ctx* c, const T* V, bool on_device, int layout, int64_t n, int64_t p,
+               int64_t ld) {
+  const int64_t seg = 16 / sizeof(T);
+  const int64_t ldv = round_up(n, seg);
+  const int64_t p_pad = round_up(p, (int64_t)K1_TP);
+  const size_t bytes = sizeof(T) * (size_t)p_pad * ldv;
+  if (c->dV) cudaFree(c->dV);
+  c->dV = nullptr;
+  c->loaded = false;
+  CUDA_TRY(c, cudaMalloc(&c->dV, bytes));
+  CUDA_TRY(c, cudaMemsetAsync(c->dV, 0, bytes, c->stream));
+  if (layout == MCP_OBS_MAJOR) {
+    CUDA_TRY(c, cudaMemcpy2DAsync(c->dV, sizeof(T) * ldv, V, sizeof(T) * ld, sizeof(T) * n, p,
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                  c->stream));
+  } else {
+    const T* src = V;
+    void* staging = nullptr;
+    if (!on_device) {
+      CUDA_TRY(c, cudaMalloc(&staging, sizeof(T) * (size_t)n * ld));
+      CUDA_TRY(c, cudaMemcpyAsync(staging, V, sizeof(T) * (size_t)n * ld, cudaMemcpyHostToDevice,
+                                  c->stream));
+      src = (const T*)staging;
+    }
+    dim3 grid((unsigned)ceil_div(p, 32), (unsigned)ceil_div(n, 32));
+    k_transpose_in<T><<<grid, dim3(32, 8), 0, c->stream>>>(src, n, p, ld, (T*)c->dV, ldv);
+    cudaError_t e = cudaGetLastError();
+    if (staging) {
+      cudaStreamSynchronize(c->stream);
+      cudaFree(staging);
+    }
+    CUDA_TRY(c, e);
+  }
+  // finiteness of V (dense.py:87-88)
+  int rc = ensure(c, c->dflag, sizeof(unsigned long long));
+  if (rc) return rc;
+  CUDA_TRY(c, cudaMemsetAsync(c->dflag.p, 0, sizeof(unsigned long long), c->stream));
+  k_count_nonfinite<T><<<grid_for(p_pad * ldv, 256, 16 * c->sms), 256, 0, c->stream>>>(
+      (const T*)c->dV, p_pad * ldv, (unsigned long long*)c->dflag.p);
+  unsigned long long bad = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&bad, c->dflag.p, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (bad) {
+    cudaFree(c->dV);
+    c->dV = nullptr;
+    return c->fail(MCP_ERR_ARG, "V contains non-finite entries");
+  }
+  c->ldv = ldv;
+  c->p_pad = p_pad;
+  return MCP_OK;
+}
+
+int load_nu(mcp_ctx* c, const double* nu, bool on_device, double nu_const) {
+  if (c->dnu) cudaFree(c->dnu);
+  c->dnu = nullptr;
+  if (!nu) {
+    c->nu_const = nu_const > 0.0 ? nu_const : 1.0 / (double)c->p;
+    if (!std::isfinite(c->nu_const) || !(c->nu_const > 0.0))
+      return c->fail(MCP_ERR_ARG, "nu entries must be finite and strictly positive");
+    return MCP_OK;
+  }
+  c->nu_const = 0.0;
+  CUDA_TRY(c, cudaMalloc(&c->dnu, sizeof(double) * c->p_pad));
+  CUDA_TRY(c, cudaMemsetAsync(c->dnu, 0, sizeof(double) * c->p_pad, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->dnu, nu, sizeof(double) * c->p,
+                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              c->stream));
+  int rc = ensure(c, c->dflag, sizeof(unsigned long long));
+  if (rc) return rc;
+  CUDA_TRY(c, cudaMemsetAsync(c->dflag.p, 0, sizeof(unsigned long long), c->stream));
+  k_check_nu<<<grid_for(c->p, 256, 4 * c->sms), 256, 0, c->stream>>>(
+      c->dnu, c->p, (unsigned long long*)c->dflag.p);
+  unsigned long long bad = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&bad, c->dflag.p, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (bad) return c->fail(MCP_ERR_ARG, "nu entries must be finite and strictly positive");
+  return MCP_OK;
+}
+
+int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layout, int64_t n,
+                  int64_t p, int64_t ld, const double* nu, double nu_const) {
+  if (!V) return c->fail(MCP_ERR_ARG, "V is NULL");
+  if (dtype != MCP_F64 && dtype != MCP_F32) return c->fail(MCP_ERR_ARG, "unknown dtype");
+  if (layout != MCP_VAR_MAJOR && layout != MCP_OBS_MAJOR)
+    return c->fail(MCP_ERR_ARG, "unknown layout");
+  if (n < 1 || p < 1)
+    return c->fail(MCP_ERR_ARG, "V must be at least 1x1, got shape (" + std::to_string(n) + ", " +
+                                    std::to_string(p) + ")");
+  const int64_t minld = layout == MCP_OBS_MAJOR ? n : p;
+  if (ld < minld) return c->fail(MCP_ERR_ARG, "leading dimension too small");
+  c->loaded = false;
+  drop_graphs(c);
+  int rc = dtype == MCP_F64
+               ? upload_obs<double>(c, (const double*)V, on_device, layout, n, p, ld)
+               : upload_obs<float>(c, (const float*)V, on_device, layout, n, p, ld);
+  if (rc) return rc;
+  c->dtype = dtype;
+  c->n = n;
+  c->p = p;
+  if ((rc = load_nu(c, nu, on_device, nu_const))) return rc;
+  c->loaded = true;
+  return MCP_OK;
+}
+
+struct Guard {
+  mcp_ctx* c;
+  std::unique_lock<std::mutex> lk;
+  explicit Guard(mcp_ctx* ctx) : c(ctx), lk(ctx->mu) { cudaSetDevice(ctx->device); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int mcp_abi_version(void) { return MCP_ABI_VERSION; }
+
+const char* mcp_last_error(const mcp_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+int mcp_create(mcp_ctx** out, int device) {
+  if (!out) {
+    g_create_error = "out is NULL";
+    return MCP_ERR_ARG;
+  }
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    g_create_error = std::string("no CUDA device available: ") + cudaGetErrorString(e);
+    (void)cudaGetLastError();
+    return MCP_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) {
+    g_create_error = "device index out of range";
+    return MCP_ERR_ARG;
+  }
+  cudaDeviceProp prop;
+  if ((e = cudaSetDevice(device)) != cudaSuccess ||
+      (e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) {
+    g_create_error = cudaGetErrorString(e);
+    return MCP_ERR_CUDA;
+  }
+  if (prop.major != 10 || prop.minor != 0) {
+    g_create_error = std::string("device ") + prop.name + " is not sm_100 (B200); this build targets sm_100a only";
+    return MCP_ERR_CUDA;
+  }
+  mcp_ctx* c = new mcp_ctx();
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    g_create_error = cudaGetErrorString(e);
+    delete c;
+    return MCP_ERR_CUDA;
+  }
+  *out = c;
+  return MCP_OK;
+}
+
+int mcp_destroy(mcp_ctx* c) {
+  if (!c) return MCP_OK;
+  {
+    Guard gd(c);
+    cudaStreamSynchronize(c->stream);
+    drop_graphs(c);
+    DevBuf* bufs[] = {&c->dx, &c->dout, &c->dYw, &c->dAfrag, &c->dYpart, &c->dwpart,
+                      &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag};
+    for (DevBuf* b : bufs)
+      if (b->p) cudaFree(b->p);
+    if (c->dV) cudaFree(c->dV);
+    if (c->dnu) cudaFree(c->dnu);
+    if (c->hx) cudaFreeHost(c->hx);
+    if (c->hout) cudaFreeHost(c->hout);
+    cudaStreamDestroy(c->stream);
+  }
+  delete c;
+  return MCP_OK;
+}
+
+int mcp_device_sms(const mcp_ctx* c) { return c ? c->sms : 0; }
+
+int mcp_load_obs(mcp_ctx* c, const void* V, int dtype, int layout, int64_t n, int64_t p,
+                 int64_t ld, const double* nu, double nu_const) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  return load_obs_impl(c, V, false, dtype, layout, n, p, ld, nu, nu_const);
+}
+
+int mcp_load_obs_device(mcp_ctx* c, const void* dV, int dtype, int layout, int64_t n, int64_t p,
+                        int64_t ld, const double* dnu, double nu_const) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  return load_obs_impl(c, dV, true, dtype, layout, n, p, ld, dnu, nu_const);
+}
+
+int mcp_obs_shape(const mcp_ctx* c, int64_t* n, int64_t* p) {
+  if (!c || !c->loaded) return MCP_ERR_STATE;
+  if (n) *n = c->n;
+  if (p) *p = c->p;
+  return MCP_OK;
+}
+
+
+int mcp_fg(mcp_ctx* c, int d, int r, const double* lam, const double* A, double alpha, int mode,
+           double* f, double* g_lam, double* g_A) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!lam || !A || !f || !g_lam || !g_A) return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (!std::isfinite(alpha))
+    return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
+  int rc = run_host_eval(c, d, r, mode, lam, A, alpha);
+  if (rc) return rc;
+  const double* out = (const double*)c->hout;
+  *f = out[0];
+  std::memcpy(g_lam, out + 1, sizeof(double) * r);
+  std::memcpy(g_A, out + 1 + r, sizeof(double) * (size_t)c->n * r);
+  return MCP_OK;
+}
+
+int mcp_fg_packed(mcp_ctx* c, int d, int r, const double* x, double alpha, int mode, double* f,
+                  double* g) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!x || !f || !g) return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (!std::isfinite(alpha))
+    return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  int rc = run_host_eval(c, d, r, mode, x, x + r, alpha);
+  if (rc) return rc;
+  const double* out = (const double*)c->hout;
+  *f = out[0];
+  std::memcpy(g, out + 1, sizeof(double) * (r + (size_t)c->n * r));
+  return MCP_OK;
+}
+
+int mcp_ttsv_batch(mcp_ctx* c, int d, int r, const double* A, int mode, double* Y) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!A || !Y) return c->fail(MCP_ERR_ARG, "NULL argument");
+  EvalPlan pl;
+  int rc = plan_eval(c, d, r, mode, pl);
+  if (rc) return rc;
+  const int64_t n = c->n;
+  double* dx = (double*)c->dx.p;
+  // dx = [lam ; A]; lam is unused by the partial, leave it as is
+  CUDA_TRY(c, cudaMemcpyAsync(dx + r, A, sizeof(double) * n * r, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, c->stream))) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(Y, c->dYw.p, sizeof(double) * n * r, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MCP_OK;
+}
+
+static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, double* out) {
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
+  if (mode != MCP_MODE_FP64)
+    return c->fail(MCP_ERR_ARG, "mode " + std::to_string(mode) + " is not available in this build");
+  if (nparts < 1 || part < 0 || part >= nparts) return c->fail(MCP_ERR_ARG, "bad part/nparts");
+  if (!out) return c->fail(MCP_ERR_ARG, "NULL argument");
+  const int64_t T = c->p_pad / K5_T;
+  const int64_t pairs = T * (T + 1) / 2;
+  const int64_t b = pairs * part / nparts, e = pairs * (part + 1) / nparts;
+  const int n_chunks = (int)ceil_div(c->n, K5_NK);
+  const size_t smem = c->dtype == MCP_F64 ? k5_smem_bytes<double>() : k5_smem_bytes<float>();
+  const void* fn = c->dtype == MCP_F64 ? (const void*)k5_gram_power<double>
+                                       : (const void*)k5_gram_power<float>;
+  CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 1;
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, K5_THREADS, smem));
+  if (occ < 1) occ = 1;
+  int64_t grid = (int64_t)c->sms * occ;
+  if (grid > e - b) grid = e - b;
+  if (grid < 1) grid = 1;
+  int rc;
+  if ((rc = ensure(c, c->dpart, sizeof(double) * grid))) return rc;
+  if ((rc = ensure(c, c->dscalar, sizeof(double)))) return rc;
+  if (c->dtype == MCP_F64)
+    k5_gram_power<double><<<(int)grid, K5_THREADS, smem, c->stream>>>(
+        (const double*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
+        (double*)c->dpart.p);
+  else
+    k5_gram_power<float><<<(int)grid, K5_THREADS, smem, c->stream>>>(
+        (const float*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
+        (double*)c->dpart.p);
+  k_ordered_sum<<<1, 32, 0, c->stream>>>((const double*)c->dpart.p, (int)grid,
+                                         (double*)c->dscalar.p);
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaMemcpyAsync(out, c->dscalar.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->last_launches = 2;
+  c->variant = c->dtype == MCP_F64 ? "k5_gram_dmma<f64>" : "k5_gram_dmma<f32>";
+  return MCP_OK;
+}
+
+int mcp_data_norm_sq(mcp_ctx* c, int d, int mode, double* out) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  return data_norm_part(c, d, mode, 0, 1, out);
+}
+
+int mcp_data_norm_sq_part(mcp_ctx* c, int d, int mode, int part, int nparts, double* out) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  return data_norm_part(c, d, mode, part, nparts, out);
+}
+
+int mcp_fg_partial_device(mcp_ctx* c, int d, int r, const double* dx, int mode, double* dYw,
+                          void* stream) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!dx || !dYw) return c->fail(MCP_ERR_ARG, "NULL argument");
+  EvalPlan pl;
+  int rc = plan_eval(c, d, r, mode, pl);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  return enqueue_partial(c, pl, dx, dYw, s);
+}
+
+int mcp_fg_finish_device(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
+                         double alpha, double* dout, void* stream) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!dx || !dYw || !dout) return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
+  if (r < 1) return c->fail(MCP_ERR_ARG, "rank must be >= 1, got " + std::to_string(r));
+  int rc;
+  if ((rc = ensure(c, c->dG, sizeof(double) * (size_t)r * r))) return rc;
+  if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  c->last_launches = 0;
+  return enqueue_finish(c, d, r, dx, dYw, nullptr, alpha, dout, s);
+}
+
+int mcp_fg_device(mcp_ctx* c, int d, int r, const double* dx, double alpha, int mode,
+                  double* dout, void* stream) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!dx || !dout) return c->fail(MCP_ERR_ARG, "NULL argument");
+  EvalPlan pl;
+  int rc = plan_eval(c, d, r, mode, pl);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  if ((rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s))) return rc;
+  return enqueue_finish(c, d, r, dx, (const double*)c->dYw.p, nullptr, alpha, dout, s);
+}
+
+int mcp_last_launch_count(const mcp_ctx* c) { return c ? c->last_launches : 0; }
+
+const char* mcp_last_variant(const mcp_ctx* c) { return c ? c->variant.c_str() : ""; }
+
+}  // extern "C"

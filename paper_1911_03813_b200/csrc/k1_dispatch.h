@@ -1,0 +1,35 @@
+// Shape selection and launch of the K1 fused f+grad kernel variants (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace mcp {
+
+struct K1Variant {
+  int dtype = 0;       // MCP_F64 / MCP_F32
+  int RB = 8;          // factor columns per CTA
+  int MTW = 1;         // compile-time bound on n chunks (register array extent)
+  int n_chunks = 1;
+  int n_pad = 64;
+  int rbs = 1;         // column blocks
+  int gp = 1;          // persistent CTAs per column block
+  int grid = 1;
+  size_t smem = 0;
+  int64_t num_tiles = 0;
+  size_t afrag_elems = 0, ypart_elems = 0, wpart_elems = 0;
+  std::string name;
+  int entry = -1;
+};
+
+// Choose the variant for (dtype, n, r, p_pad) on a device with `sms` SMs.
+bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v, std::string& why);
+
+// Launch K1 on stream s; returns 0 on success.
+int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
+              double nu_const, const double* Afrag, int d, double* Ypart, double* wpart,
+              cudaStream_t s);
+
+}  // namespace mcp

@@ -1,0 +1,216 @@
+// K1 (FP64 mode): fused single-pass f+grad partial over a row block of observations.
+//
+// Replaces, per tile of K1_TP observations and one block of RB factor columns, the reference's
+//   Z = V^T A                      pkg/src/momentcp/implicit.py:106   (GEMM1, DMMA.8x8x4)
+//   P = nu * Z^(d-1)               pkg/src/momentcp/implicit.py:82-91,106-107 (epilogue, registers)
+//   w += sum_l nu_l z_l^d          (= a_j^T y_j, pkg/src/momentcp/implicit.py:139; epilogue)
+//   Y += V P                       pkg/src/momentcp/implicit.py:107   (GEMM2, DMMA.8x8x4)
+// Z and P live only in registers / shared memory -- the p x r intermediate never reaches HBM.
+//
+// Layout in HBM: V is observation-major (p_pad x ldv, row l = observation v_l, zero padded to a
+// multiple of K1_TP rows and to a 16-byte row pitch).  Each CTA is persistent over a static,
+// strided sequence of tiles and owns one RB-column block; its Y partial (n_pad x RB) lives in
+// registers across all of its tiles, distributed over 8 warps by 8-row m-tiles of n.  Partials
+// are written once per CTA and summed in a fixed order by k_reduce_partials, so results are
+// bitwise reproducible and exactly linear in nu (pkg/tests/test_implicit.py:53-57).
+#pragma once
+
+#include "mcp_common.cuh"
+
+namespace mcp {
+
+constexpr int K1_TP = 64;       // observations per tile
+constexpr int K1_NK = 64;       // n-chunk width staged in shared memory
+constexpr int K1_THREADS = 256; // 8 warps
+constexpr int K1_SV = 68;       // smem row pitch (elements): 68 = 4 mod 16 -> conflict-free
+                                // 8-byte fragment loads for both GEMMs
+
+struct K1Params {
+  const void* V;       // p_pad x ldv, observation-major
+  int64_t ldv;         // row pitch in elements (multiple of 16 bytes)
+  int64_t num_tiles;   // p_pad / K1_TP
+  int n;               // variables
+  int n_chunks;        // ceil(n / K1_NK)
+  int n_pad;           // n_chunks * K1_NK
+  const double* nu;    // p_pad weights (zero padded) or nullptr for uniform
+  double nu_const;     // uniform weight when nu == nullptr
+  const double* Afrag; // [rbs][n_chunks*16][RB/8][32] B-fragment ordered factor blocks
+  int d;
+  int rbs;             // number of RB-column blocks
+  int gp;              // persistent CTAs per column block
+  double* Ypart;       // [rbs][gp][n_pad][RB]
+  double* wpart;       // [rbs][gp][RB]
+};
+
+template <typename VT, int RB>
+__host__ __device__ constexpr size_t k1_smem_bytes() {
+  return 2 * (size_t)K1_TP * K1_SV * sizeof(VT)      // V chunk, double buffered
+         + 2 * (size_t)16 * (RB / 8) * 32 * 8        // factor fragments, double buffered
+         + (size_t)K1_TP * (RB + 4) * 8              // P tile
+         + (size_t)8 * RB * 8;                       // w cross-warp reduction
+}
+
+template <typename VT>
+__device__ __forceinline__ void k1_load_v(VT* dst, const VT* __restrict__ V, int64_t ldv,
+                                          int64_t row0, int c) {
+  constexpr int SEG = 16 / sizeof(VT);
+  constexpr int SEGS_ROW = K1_NK / SEG;
+  constexpr int TOTAL = K1_TP * SEGS_ROW;
+#pragma unroll
+  for (int s = threadIdx.x; s < TOTAL; s += K1_THREADS) {
+    const int row = s / SEGS_ROW, seg = s % SEGS_ROW;
+    const int64_t col = (int64_t)c * K1_NK + seg * SEG;
+    const bool ok = col < ldv;
+    const VT* src = ok ? V + (row0 + row) * ldv + col : V;
+    cp_async16(dst + row * K1_SV + seg * SEG, src, ok ? 16 : 0);
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void k1_load_a(double* dst, const double* __restrict__ src) {
+  constexpr int TOTAL = 16 * NT * 32 / 2;
+#pragma unroll
+  for (int s = threadIdx.x; s < TOTAL; s += K1_THREADS) cp_async16(dst + 2 * s, src + 2 * s, 16);
+}
+
+template <typename VT, int RB, int MTW>
+__global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
+  constexpr int NT = RB / 8;
+  constexpr int SP = RB + 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  VT* sV0 = reinterpret_cast<VT*>(smem_raw);
+  VT* sV1 = sV0 + K1_TP * K1_SV;
+  double* sA0 = reinterpret_cast<double*>(smem_raw + 2 * (size_t)K1_TP * K1_SV * sizeof(VT));
+  double* sA1 = sA0 + 16 * NT * 32;
+  double* sP = sA1 + 16 * NT * 32;
+  double* sW = sP + K1_TP * SP;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int rb = blockIdx.x % prm.rbs;
+  const int pg = blockIdx.x / prm.rbs;
+  const int C = prm.n_chunks;
+  const int dm1 = prm.d - 1;
+  const VT* __restrict__ V = static_cast<const VT*>(prm.V);
+  const double* __restrict__ Af = prm.Afrag + (size_t)rb * C * 16 * NT * 32;
+
+  double yacc[MTW][NT][2];
+  double wacc[NT][2];
+#pragma unroll
+  for (int c = 0; c < MTW; ++c)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) yacc[c][nt][0] = yacc[c][nt][1] = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
+
+  for (int64_t tile = pg; tile < prm.num_tiles; tile += prm.gp) {
+    const int64_t row0 = tile * K1_TP;
+
+    // ---------------- GEMM1: Z[64 x RB] = V_tile[64 x n] * A[n x RB] ----------------
+    double zacc[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) zacc[nt][0] = zacc[nt][1] = 0.0;
+
+    k1_load_v<VT>(sV0, V, prm.ldv, row0, 0);
+    k1_load_a<NT>(sA0, Af);
+    cp_async_commit();
+    for (int c = 0; c < C; ++c) {
+      VT* sv = (c & 1) ? sV1 : sV0;
+      double* sa = (c & 1) ? sA1 : sA0;
+      if (c + 1 < C) {
+        k1_load_v<VT>((c & 1) ? sV0 : sV1, V, prm.ldv, row0, c + 1);
+        k1_load_a<NT>((c & 1) ? sA0 : sA1, Af + (size_t)(c + 1) * 16 * NT * 32);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const VT* vrow = sv + (8 * warp + g) * K1_SV + t;
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const double a = to_f64(vrow[4 * ks]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(zacc[nt], a, sa[(ks * NT + nt) * 32 + lane]);
+      }
+      __syncthreads();
+    }
+
+    // ---------------- epilogue: P = nu * z^(d-1), w += P * z ----------------
+    {
+      const int lr = 8 * warp + g;
+      const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        double pv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double z = zacc[nt][e];
+          pv[e] = nul * rm_pow(z, dm1);
+          wacc[nt][e] += pv[e] * z;
+        }
+        *reinterpret_cast<double2*>(&sP[lr * SP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
+      }
+    }
+    __syncthreads();
+
+    // ---------------- GEMM2: Y[n x RB] += V_tile^T[n x 64] * P[64 x RB] ----------------
+    // Chunks run last-to-first so the (up to two) chunks still resident from GEMM1 are used
+    // before any reload; with n <= 128 the tile is read from HBM exactly once.
+#pragma unroll
+    for (int cc = 0; cc < MTW; ++cc) {
+      const int c = MTW - 1 - cc;
+      if (c < C) {
+        const VT* sv = (c & 1) ? sV1 : sV0;
+        if (c >= 1 && c - 1 <= C - 3) {
+          k1_load_v<VT>(((c - 1) & 1) ? sV1 : sV0, V, prm.ldv, row0, c - 1);
+          cp_async_commit();
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncthreads();
+        const VT* vcol = sv + t * K1_SV + 8 * warp + g;
+        const double* prow = sP + t * SP + g;
+#pragma unroll 4
+        for (int ks = 0; ks < 16; ++ks) {
+          const double a = to_f64(vcol[4 * ks * K1_SV]);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(yacc[c][nt], a, prow[4 * ks * SP + 8 * nt]);
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  // ---------------- write this CTA's partials ----------------
+  double* Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * prm.n_pad * RB;
+#pragma unroll
+  for (int c = 0; c < MTW; ++c) {
+    if (c < C) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        *reinterpret_cast<double2*>(&Yp[(size_t)(c * K1_NK + 8 * warp + g) * RB + 8 * nt + 2 * t]) =
+            make_double2(yacc[c][nt][0], yacc[c][nt][1]);
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = wacc[nt][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if (g == 0) sW[warp * RB + 8 * nt + 2 * t + e] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < RB) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < K1_THREADS / 32; ++w) s += sW[w * RB + threadIdx.x];
+    prm.wpart[((size_t)rb * prm.gp + pg) * RB + threadIdx.x] = s;
+  }
+}
+
+}  // namespace mcp

@@ -1,0 +1,169 @@
+"""Row-sharded evaluation over 1/2/4/8 GPUs (one process per GPU, torch.distributed / NCCL).
+
+The reference is single-process.  Observations are independent, so
+Y = sum_l nu_l z_l^(d-1) v_l and w = sum_l nu_l z_l^d are sums over rows of V: each rank holds a
+contiguous row block, computes its additive piece [vec_F(Y) | w] on the device (prep -> K1 -> K3,
+mcp_fg_partial_device), one all-reduce(sum) of that n*r + r vector is the only exchange, and
+every rank runs the O(n r^2) tail (mcp_fg_finish_device) on the reduced piece, so all ranks hold
+identical f and gradients.  Uniform weights are 1/p_total on every shard (dense.py:90-91 over
+the whole set).
+
+||X||^2 (implicit.py:116-121) couples every pair of observations: each rank holds the whole V
+(all-gathered once, 0.41 GB at config 4), takes a contiguous, equal-work slice of the
+upper-triangular tile-pair list, and the per-rank partial sums are combined in rank order.
+
+The per-shard compute is pluggable only so the host-side logic (shard bounds, collective,
+tail) can be exercised on CPU with gloo in tests; the product path is the CUDA backend, which
+raises if the native library or GPU is missing.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from .dense import ObservationSet
+from .objective import FgResult, validate_variables
+from .optimize import pack
+
+
+def shard_bounds(p: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row block [lo, hi) of rank `rank` out of `world` (sizes differ by <= 1)."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of size {world}")
+    return p * rank // world, p * (rank + 1) // world
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def device_partial(obs: ObservationSet, lam, A, d: int, mode: str | None = None):
+    """[vec_F(Y) | w] of this shard as a CUDA float64 tensor, on the current stream."""
+    torch = _torch()
+    ctx = obs.device_context()
+    n, r = A.shape
+    dev = torch.device("cuda", ctx.device)
+    x = torch.as_tensor(pack(lam, A), dtype=torch.float64, device=dev)
+    Yw = torch.empty(n * r + r, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ctx.fg_partial_device(d, r, x.data_ptr(), mode, Yw.data_ptr(), stream)
+    Yw._mcp_x = x  # keep x alive until the stream has consumed it
+    return Yw
+
+
+def device_finish(obs: ObservationSet, lam, A, d: int, alpha: float, Yw):
+    """Tail on the reduced piece -> (f, g_lam, g_A) on the host."""
+    torch = _torch()
+    ctx = obs.device_context()
+    n, r = A.shape
+    dev = torch.device("cuda", ctx.device)
+    x = torch.as_tensor(pack(lam, A), dtype=torch.float64, device=dev)
+    out = torch.empty(1 + r + n * r, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ctx.fg_finish_device(d, r, x.data_ptr(), Yw.data_ptr(), float(alpha), out.data_ptr(), stream)
+    h = out.cpu().numpy()
+    return float(h[0]), h[1:1 + r].copy(), h[1 + r:].reshape((n, r), order="F").copy()
+
+
+class CudaShardBackend:
+    """Per-shard compute on this rank's GPU through the C ABI."""
+
+    def __init__(self, obs: ObservationSet, mode: str | None = None):
+        self.obs = obs
+        self.mode = mode
+
+    def partial(self, lam, A, d):
+        return device_partial(self.obs, lam, A, d, self.mode)
+
+    def finish(self, lam, A, d, alpha, Yw):
+        return device_finish(self.obs, lam, A, d, alpha, Yw)
+
+
+class ShardedObservationSet:
+    """This rank's row block of a p_total-observation set, plus the process group."""
+
+    def __init__(self, local: ObservationSet, p_total: int, row_offset: int, group=None,
+                 backend=None):
+        self.local = local
+        self.n = local.n
+        self.p = int(p_total)
+        self.row_offset = int(row_offset)
+        self.group = group
+        self.backend = backend if backend is not None else CudaShardBackend(local)
+
+    @classmethod
+    def from_device_rows(cls, V_rows, p_total: int, row_offset: int, group=None):
+        """Wrap this rank's rows (rows x n CUDA tensor, observation-major)."""
+        local = ObservationSet.from_device(V_rows, p_total=p_total)
+        return cls(local, p_total, row_offset, group)
+
+
+def _all_reduce_sum(t, group):
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def fg_implicit_sharded(sobs: ShardedObservationSet, lam, A, d: int, alpha: float = 0.0,
+                        eval_kind: str = "implicit") -> FgResult:
+    """fg_implicit over a row-sharded set: partial -> all-reduce([Y|w]) -> tail, all ranks."""
+    lam, A = validate_variables(lam, A, sobs.n, alpha)
+    if d < 2:
+        raise ValueError(f"order must be >= 2, got {d}")
+    start = time.perf_counter()
+    Yw = sobs.backend.partial(lam, A, d)
+    _all_reduce_sum(Yw, sobs.group)
+    f, g_lam, g_A = sobs.backend.finish(lam, A, d, alpha, Yw)
+    return FgResult(f, g_lam, g_A, time.perf_counter() - start, eval_kind)
+
+
+def packed_fg_sharded(sobs: ShardedObservationSet, d: int, r: int, alpha: float = 0.0):
+    """packed_fg_implicit for a sharded set (every rank calls it with the same x)."""
+    n = sobs.n
+
+    def fg(x):
+        x = np.asarray(x, dtype=float)
+        lam, A = x[:r].copy(), x[r:].reshape((n, r), order="F").copy()
+        res = fg_implicit_sharded(sobs, lam, A, d, alpha)
+        return res.f, pack(res.g_lam, res.g_A)
+
+    return fg
+
+
+def data_norm_sq_split(obs_full: ObservationSet, d: int, group=None, mode: str | None = None,
+                       part_fn=None) -> float:
+    """||X||^2 with the tile-pair list split over the ranks of `group`.
+
+    Every rank holds the full set; rank k computes pair slice k of W, the W partial sums are
+    all-gathered and added in rank order (deterministic, identical on every rank).
+    """
+    import torch
+    import torch.distributed as dist
+
+    if d < 2:
+        raise ValueError(f"order must be >= 2, got {d}")
+    world, rank = 1, 0
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if part_fn is None:
+        ctx = obs_full.device_context()
+        part = ctx.data_norm_sq(d, mode, rank, world) if world > 1 else ctx.data_norm_sq(d, mode)
+        dev = torch.device("cuda", ctx.device)
+    else:
+        part = part_fn(rank, world)
+        dev = torch.device("cpu")
+    if world == 1:
+        return float(part)
+    mine = torch.tensor([part], dtype=torch.float64, device=dev)
+    parts = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    total = 0.0
+    for t in parts:
+        total += float(t.item())
+    return total

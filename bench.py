@@ -1,0 +1,388 @@
+"""Benchmark of the B200 implicit moment-tensor CP f+grad (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c2] [--mode fp64]
+
+A step is one f+grad evaluation (f, grad_lam, grad_A at (lam, A)) over the whole observation
+set of the workload.  Default workload: BASELINE.json configs[1] = c2 (n=100, p=1e6, d=4,
+r=10, float64), the configuration the metric is quoted on.  For N > 1 (torchrun, one process
+per GPU) the p rows are sharded across ranks (strong scaling: total work fixed) and the
+[Y | w] partials are combined by one NCCL all-reduce per step.
+
+Printed (rank 0, one JSON line):
+  value      evals/s with lam, A already in HBM (mcp_fg_device / partial+all-reduce+finish),
+             K steps between barriers + device syncs, CUDA events, max over ranks.
+  e2e        the same metric through the public API (packed_fg_implicit(obs, d, r)(x) with a
+             host numpy x): H2D of x and D2H of [f; g] inside every step.
+  roofline   dominant kernel K1: algorithmic bytes (n*p*sizeof(V)) per launch / its
+             event-timed duration vs measured HBM peak (MEASURED_PEAKS.json), with the
+             FP64 view (4 n p r flops) vs the measured DMMA peak (profiles/peaks_*.json).
+  cpu_baseline  the reference algorithm (CPU oracle port, numpy/OpenBLAS, all host threads)
+             on the same workload, rank 0 at N=1.
+--impl reference runs only that CPU arm, on the same config/metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_CONFIG = "c2"
+SEED = 2024
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def _read_json(path):
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+def _peaks():
+    hbm = _read_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    if hbm and "hbm_gbs" in hbm:
+        hbm_gbs, hbm_src = float(hbm["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    else:
+        hbm_gbs, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    fp = _read_json(os.path.join(ROOT, "profiles", "peaks_fp64_tf32_r01.json")) or {}
+    return hbm_gbs, hbm_src, float(fp.get("dmma_884_tflops", 37.09)), float(
+        fp.get("cublas_tf32_8192_tflops", 741.9))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms while the GPU is under load."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu = gpu_id
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._drain, daemon=True)
+        self._t.start()
+
+    def _drain(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self._t.join(timeout=5)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_arm(cfg, V_nxp, lam, A, budget_s=12.0, min_evals=2, max_evals=None):
+    """Reference algorithm (oracle port of pkg/src/momentcp/objective.py:77-94) on the host."""
+    from oracle import momentcp_oracle as om
+
+    nu = np.full(V_nxp.shape[1], 1.0 / V_nxp.shape[1])
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        om.fg_implicit(V_nxp, nu, lam, A, cfg.d, 0.0)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= min_evals and time.perf_counter() - t_start > budget_s:
+            break
+        if max_evals and len(times) >= max_evals:
+            break
+    return times
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((d.get("num_threads", 1) for d in threadpool_info()), default=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        return os.cpu_count()
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU reference arm alone (rank 0; other ranks exit 0)."""
+    if rank != 0:
+        return
+    from paper_1911_03813_b200 import synth
+
+    p_sample = cfg.p if cfg.name in ("c1", "c2") else min(cfg.p, 200_000)
+    V = synth.host_observations(cfg, SEED, p=p_sample)
+    V = np.asarray(V, dtype=float)
+    lam, A = synth.initial_point(cfg, SEED)
+    for _ in range(args.warmup):
+        cpu_arm(cfg, V, lam, A, budget_s=0.0, min_evals=1, max_evals=1)
+    times = cpu_arm(cfg, V, lam, A, budget_s=0.0, min_evals=args.steps, max_evals=args.steps)
+    scale = cfg.p / p_sample
+    evals = 1.0 / (sum(times) / len(times) * scale)
+    threads = _blas_threads()
+    line = {
+        "metric": "f+grad evals/s", "value": evals, "unit": "evals/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / evals, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": f"synthetic seeded Gaussian mixture ({cfg.name})",
+        "config": _config_dict(cfg, args, world),
+        "cpu_baseline": {"value": evals, "unit": "evals/s", "cores": threads, "kind": "port",
+                         "sample": (f"full {cfg.name} workload, p={p_sample}" if scale == 1 else
+                                    f"{cfg.name} row sample p={p_sample}, scaled x{scale:g} "
+                                    "(f+grad is linear in p)")
+                                   + f"; numpy/OpenBLAS {threads} threads, fp64"},
+        "e2e": {"value": evals, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(cfg, args, world):
+    return {"workload": f"{cfg.name}: n={cfg.n} p={cfg.p} d={cfg.d} r={cfg.r} V {cfg.dtype}, "
+                        f"{'Gaussian' if cfg.k == 0 else str(cfg.k) + '-component mixture'} "
+                        f"sigma={cfg.sigma}",
+            "n": cfg.n, "p": cfg.p, "d": cfg.d, "r": cfg.r, "v_dtype": cfg.dtype,
+            "mode": args.mode, "parallelism": f"row-shard dp{world}",
+            "l2": "inputs larger than L2 (V = %.0f MB > 126 MB), no flush needed"
+                  % (cfg.n * cfg.p * (4 if cfg.dtype == 'f32' else 8) / 1e6)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--mode", default="fp64", choices=["fp64", "tf32x3"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_1911_03813_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    if cfg.r == 0:
+        raise SystemExit("bench workloads are f+grad configs (c1, c2, c3, c5)")
+    rank, world, local = _env_rank()
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1911_03813_b200 as mcp
+    from paper_1911_03813_b200 import distributed as D
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    group = None
+
+    # ---- data: this rank's rows, generated on its GPU ----
+    lo, hi = D.shard_bounds(cfg.p, world, rank)
+    Vrows = synth.device_observations(cfg, SEED, device=dev, row_offset=lo, rows=hi - lo)
+    obs = mcp.ObservationSet.from_device(Vrows, p_total=cfg.p)
+    t_up = time.perf_counter()
+    ctx = obs.device_context()
+    torch.cuda.synchronize()
+    t_up = time.perf_counter() - t_up
+    lam, A = synth.initial_point(cfg, SEED)
+    n, r, d = cfg.n, cfg.r, cfg.d
+    x_host = mcp.pack(lam, A)
+    x_dev = torch.as_tensor(x_host, device=dev)
+    Yw = torch.empty(n * r + r, dtype=torch.float64, device=dev)
+    out = torch.empty(1 + r + n * r, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    def step_device():
+        if world == 1:
+            ctx.fg_device(d, r, x_dev.data_ptr(), 0.0, args.mode, out.data_ptr(), stream)
+        else:
+            ctx.fg_partial_device(d, r, x_dev.data_ptr(), args.mode, Yw.data_ptr(), stream)
+            dist.all_reduce(Yw, op=dist.ReduceOp.SUM)
+            ctx.fg_finish_device(d, r, x_dev.data_ptr(), Yw.data_ptr(), 0.0, out.data_ptr(),
+                                 stream)
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up, then a clock soak under the same load (nvidia-smi needs >= ~1 s) ----
+    for _ in range(args.warmup):
+        step_device()
+    barrier_sync()
+    try:
+        gpu_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:  # noqa: BLE001
+        gpu_id = str(local)
+    clocks = ClockSampler(gpu_id)
+    if rank == 0:
+        clocks.start()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 1.5:
+        for _ in range(20):
+            step_device()
+        torch.cuda.synchronize()
+    barrier_sync()
+
+    # ---- timed region: exactly K device-resident steps ----
+    ctx.set_kernel_timing(True)
+    ctx.kernel_time_ms(reset=True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier_sync()
+    e0.record()
+    for _ in range(args.steps):
+        step_device()
+    e1.record()
+    barrier_sync()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    k1_ms, k1_launches = ctx.kernel_time_ms(reset=True)
+    ctx.set_kernel_timing(False)
+    launches_per_step = ctx.last_launch_count if world == 1 else 6
+    variant = ctx.last_variant
+    clk = clocks.stop() if rank == 0 else None
+
+    # ---- e2e through the public API (host x in, host f, g out every step) ----
+    if world == 1:
+        fg = mcp.packed_fg_implicit(obs, d, r, mode=args.mode)
+    else:
+        sobs = D.ShardedObservationSet(obs, cfg.p, lo, group)
+        fg = D.packed_fg_sharded(sobs, d, r)
+    for _ in range(3):
+        fg(x_host)
+    barrier_sync()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        f_val, g_val = fg(x_host)
+    barrier_sync()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    hbm_gbs, hbm_src, fp64_peak, tf32_peak = _peaks()
+    vbytes = 4 if cfg.dtype == "f32" else 8
+    rows_here = hi - lo
+    k1_avg_ms = k1_ms / max(k1_launches, 1)
+    alg_bytes = n * rows_here * vbytes
+    alg_flops = 4.0 * n * rows_here * r
+    achieved_gbs = alg_bytes / (k1_avg_ms * 1e-3) / 1e9
+    achieved_tf = alg_flops / (k1_avg_ms * 1e-3) / 1e12
+    ridge = fp64_peak * 1e12 / (hbm_gbs * 1e9)
+    ai = alg_flops / alg_bytes
+    bound = "hbm" if ai < ridge else "tensor"
+    traffic = None
+    prof = _read_json(os.path.join(ROOT, "profiles", f"ncu_k1_{cfg.name}_r01.json"))
+    if prof and prof.get("variant") == variant:
+        traffic = prof.get("dram_bytes_per_launch")
+    value = args.steps / (ms_total * 1e-3)
+    step_flops = 4.0 * n * cfg.p * r
+    line = {
+        "metric": "f+grad evals/s", "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": f"synthetic seeded Gaussian mixture ({cfg.name}), generated on GPU",
+        "config": dict(_config_dict(cfg, args, world), kernel=variant,
+                       upload_s=round(t_up, 4)),
+        "tflops": {"achieved": step_flops * value / 1e12, "peak": fp64_peak,
+                   "peak_kind": "measured DMMA.8x8x4 FP64 (profiles/peaks_fp64_tf32_r01.json)",
+                   "frac": step_flops * value / 1e12 / fp64_peak,
+                   "flops_per_step": step_flops},
+        "roofline": {"bound": bound,
+                     "achieved": achieved_gbs if bound == "hbm" else achieved_tf,
+                     "peak": hbm_gbs if bound == "hbm" else fp64_peak,
+                     "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                     "frac": (achieved_gbs / hbm_gbs) if bound == "hbm" else achieved_tf / fp64_peak,
+                     "traffic": traffic,
+                     "kernel": variant, "kernel_avg_ms": k1_avg_ms,
+                     "kernel_share_of_step": k1_avg_ms / (ms_total / args.steps),
+                     "alg_bytes_per_launch": alg_bytes, "alg_flops_per_launch": alg_flops,
+                     "fp64_tflops": achieved_tf, "fp64_frac": achieved_tf / fp64_peak,
+                     "peak_source": hbm_src if bound == "hbm" else "measured DMMA"},
+        "e2e": {"value": args.steps / e2e_s, "unit": "evals/s",
+                "h2d_bytes_per_step": 8 * (r + n * r + 1),
+                "d2h_bytes_per_step": 8 * (1 + r + n * r)},
+        "clocks": clk,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+    if world == 1 and not args.no_cpu:
+        # bounded CPU sample on this host: the full workload when it fits (c1, c2), else rows
+        p_sample = cfg.p if cfg.name in ("c1", "c2") else min(cfg.p, 100_000)
+        Vh = Vrows[:p_sample].double().cpu().numpy().T          # n x p view (reference layout)
+        times = cpu_arm(cfg, Vh, lam, A, budget_s=12.0)
+        scale = cfg.p / p_sample
+        med = statistics.median(times) * scale
+        threads = _blas_threads()
+        line["cpu_baseline"] = {
+            "value": 1.0 / med, "unit": "evals/s", "cores": threads, "kind": "port",
+            "sample": (f"{len(times)} evals of the full {cfg.name} workload" if scale == 1 else
+                       f"{len(times)} evals of a {p_sample}-row sample scaled x{scale:g}")
+                      + f", median; oracle port of objective.py:77-94 on numpy/OpenBLAS "
+                        f"({threads} threads, fp64)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

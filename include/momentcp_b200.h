@@ -123,6 +123,14 @@ int mcp_fg_finish_device(mcp_ctx* ctx, int d, int r, const double* dx, const dou
 int mcp_fg_device(mcp_ctx* ctx, int d, int r, const double* dx, double alpha, int mode,
                   double* dout, void* stream);
 
+/*
+ * Kernel-level timing (bench.py's roofline): while enabled, every K1 / K5 launch issued outside
+ * graph capture is bracketed by CUDA events on its own stream.  mcp_kernel_time_ms waits for
+ * them and returns the summed duration and launch count (reset != 0 clears the record).
+ */
+int mcp_set_kernel_timing(mcp_ctx* ctx, int enable);
+int mcp_kernel_time_ms(mcp_ctx* ctx, double* total_ms, int* launches, int reset);
+
 /* Kernel launches issued by the last evaluation call (for the bench's gpu_launches claim). */
 int mcp_last_launch_count(const mcp_ctx* ctx);
 

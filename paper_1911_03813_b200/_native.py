@@ -54,6 +54,9 @@ SIGNATURES = {
                                             _c_void_p, ctypes.c_double, _c_void_p, _c_void_p]),
     "mcp_fg_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
                                      ctypes.c_double, ctypes.c_int, _c_void_p, _c_void_p]),
+    "mcp_set_kernel_timing": (ctypes.c_int, [_c_void_p, ctypes.c_int]),
+    "mcp_kernel_time_ms": (ctypes.c_int, [_c_void_p, _dp, ctypes.POINTER(ctypes.c_int),
+                                          ctypes.c_int]),
     "mcp_last_launch_count": (ctypes.c_int, [_c_void_p]),
     "mcp_last_variant": (ctypes.c_char_p, [_c_void_p]),
 }
@@ -137,6 +140,17 @@ class Context:
     @property
     def last_variant(self) -> str:
         return self._lib.mcp_last_variant(self._h).decode()
+
+    # -- kernel timing (bench) ------------------------------------------------------------
+    def set_kernel_timing(self, enable: bool) -> None:
+        self._check(self._lib.mcp_set_kernel_timing(self._h, int(bool(enable))), "timing")
+
+    def kernel_time_ms(self, reset: bool = True) -> tuple[float, int]:
+        ms = ctypes.c_double()
+        k = ctypes.c_int()
+        rc = self._lib.mcp_kernel_time_ms(self._h, ctypes.byref(ms), ctypes.byref(k), int(reset))
+        self._check(rc, "mcp_kernel_time_ms")
+        return ms.value, k.value
 
     # -- observation upload ---------------------------------------------------------------
     def load_obs_host(self, V: np.ndarray, layout: int, nu: np.ndarray | None, nu_const: float):

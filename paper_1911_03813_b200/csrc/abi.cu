@@ -12,6 +12,8 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <utility>
+#include <vector>
 
 #include "momentcp_b200.h"
 #include "k1_fp64.cuh"
@@ -93,6 +95,8 @@ struct mcp_ctx {
   size_t hout_bytes = 0;
 
   std::map<std::tuple<int, int, int>, GraphEntry> graphs;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
   int last_launches = 0;
   std::string variant = "none";
 
@@ -119,6 +123,29 @@ void drop_graphs(mcp_ctx* c) {
     if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
   }
   c->graphs.clear();
+}
+
+// Event pair bracketing one timed kernel launch (only when timing is on and not capturing).
+std::pair<cudaEvent_t, cudaEvent_t>* timing_begin(mcp_ctx* c, cudaStream_t s) {
+  if (!c->timing) return nullptr;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone)
+    return nullptr;
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  if (!c->event_pool.empty()) {
+    ev = c->event_pool.back();
+    c->event_pool.pop_back();
+  } else {
+    cudaEventCreate(&ev.first);
+    cudaEventCreate(&ev.second);
+  }
+  c->timed.push_back(ev);
+  cudaEventRecord(ev.first, s);
+  return &c->timed.back();
+}
+
+void timing_end(std::pair<cudaEvent_t, cudaEvent_t>* ev, cudaStream_t s) {
+  if (ev) cudaEventRecord(ev->second, s);
 }
 
 int ensure(mcp_ctx* c, DevBuf& b, size_t bytes) {
@@ -188,8 +215,10 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   const int n = (int)c->n, r = pl.r;
   k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(
       dx + r, n, r, v.RB, v.rbs, v.n_chunks * 16, (double*)c->dAfrag.p);
+  auto* ev = timing_begin(c, s);
   int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, (const double*)c->dAfrag.p, pl.d,
                      (double*)c->dYpart.p, (double*)c->dwpart.p, s);
+  timing_end(ev, s);
   if (rc) return c->fail(MCP_ERR_CUDA, "K1 launch failed");
   const int64_t red_items = (int64_t)v.rbs * n * v.RB + (int64_t)v.rbs * v.RB;
   k_reduce_partials<<<grid_for(red_items, 256, 8 * c->sms), 256, 0, s>>>(
@@ -436,6 +465,11 @@ int mcp_destroy(mcp_ctx* c) {
     if (c->dnu) cudaFree(c->dnu);
     if (c->hx) cudaFreeHost(c->hx);
     if (c->hout) cudaFreeHost(c->hout);
+    for (auto* v : {&c->timed, &c->event_pool})
+      for (auto& ev : *v) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+      }
     cudaStreamDestroy(c->stream);
   }
   delete c;
@@ -539,6 +573,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
   int rc;
   if ((rc = ensure(c, c->dpart, sizeof(double) * grid))) return rc;
   if ((rc = ensure(c, c->dscalar, sizeof(double)))) return rc;
+  auto* ev = timing_begin(c, c->stream);
   if (c->dtype == MCP_F64)
     k5_gram_power<double><<<(int)grid, K5_THREADS, smem, c->stream>>>(
         (const double*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
@@ -547,6 +582,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
     k5_gram_power<float><<<(int)grid, K5_THREADS, smem, c->stream>>>(
         (const float*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
         (double*)c->dpart.p);
+  timing_end(ev, c->stream);
   k_ordered_sum<<<1, 32, 0, c->stream>>>((const double*)c->dpart.p, (int)grid,
                                          (double*)c->dscalar.p);
   CUDA_TRY(c, cudaGetLastError());
@@ -608,6 +644,32 @@ int mcp_fg_device(mcp_ctx* c, int d, int r, const double* dx, double alpha, int 
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   if ((rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s))) return rc;
   return enqueue_finish(c, d, r, dx, (const double*)c->dYw.p, nullptr, alpha, dout, s);
+}
+
+int mcp_set_kernel_timing(mcp_ctx* c, int enable) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  c->timing = enable != 0;
+  return MCP_OK;
+}
+
+int mcp_kernel_time_ms(mcp_ctx* c, double* total_ms, int* launches, int reset) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  double tot = 0.0;
+  for (auto& ev : c->timed) {
+    CUDA_TRY(c, cudaEventSynchronize(ev.second));
+    float ms = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, ev.first, ev.second));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = (int)c->timed.size();
+  if (reset) {
+    for (auto& ev : c->timed) c->event_pool.push_back(ev);
+    c->timed.clear();
+  }
+  return MCP_OK;
 }
 
 int mcp_last_launch_count(const mcp_ctx* c) { return c ? c->last_launches : 0; }

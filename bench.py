@@ -218,6 +218,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1911_03813_b200 as mcp
+    from paper_1911_03813_b200 import _native
     from paper_1911_03813_b200 import distributed as D
 
     torch.cuda.set_device(local)
@@ -240,7 +241,7 @@ def main():
     x_dev = torch.as_tensor(x_host, device=dev)
     Yw = torch.empty(n * r + r, dtype=torch.float64, device=dev)
     out = torch.empty(1 + r + n * r, dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    stream = _native.stream_handle(torch.cuda.current_stream(dev))
 
     def step_device():
         if world == 1:

@@ -94,6 +94,13 @@ def mode_code(mode: str | None) -> int:
         raise ValueError(f"unknown mode {mode!r}; expected one of {sorted(MODES)}") from None
 
 
+def stream_handle(torch_stream) -> int:
+    """C-ABI stream argument for a torch stream: torch reports the legacy default stream as 0,
+    which the ABI reserves for "the context's own stream", so map it to cudaStreamLegacy (1)."""
+    h = int(torch_stream.cuda_stream)
+    return h if h != 0 else 1
+
+
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <string>
@@ -213,19 +214,25 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
                     cudaStream_t s) {
   const K1Variant& v = pl.k1;
   const int n = (int)c->n, r = pl.r;
-  k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(
-      dx + r, n, r, v.RB, v.rbs, v.n_chunks * 16, (double*)c->dAfrag.p);
+  int launches = 2;
+  if (v.needs_prep()) {
+    k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(
+        dx + r, n, r, v.RB, v.rbs, v.n_chunks * 16, (double*)c->dAfrag.p);
+    ++launches;
+  }
   auto* ev = timing_begin(c, s);
-  int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, (const double*)c->dAfrag.p, pl.d,
-                     (double*)c->dYpart.p, (double*)c->dwpart.p, s);
+  int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r,
+                     (const double*)c->dAfrag.p, pl.d, (double*)c->dYpart.p, (double*)c->dwpart.p,
+                     s);
   timing_end(ev, s);
   if (rc) return c->fail(MCP_ERR_CUDA, "K1 launch failed");
-  const int64_t red_items = (int64_t)v.rbs * n * v.RB + (int64_t)v.rbs * v.RB;
-  k_reduce_partials<<<grid_for(red_items, 256, 8 * c->sms), 256, 0, s>>>(
+  const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) +
+                             ceil_div((int64_t)v.rbs * v.RB, K3_X);
+  k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
       (const double*)c->dYpart.p, (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
       dYw);
   CUDA_TRY(c, cudaGetLastError());
-  c->last_launches = 3;
+  c->last_launches = launches;
   c->variant = v.name;
   return MCP_OK;
 }
@@ -234,6 +241,12 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
   const int n = (int)c->n;
+  if ((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) {
+    k_tail_fused<<<1, K4S_THREADS, 0, s>>>(dx, dYw, n, r, d, alpha_dev, alpha, dout);
+    CUDA_TRY(c, cudaGetLastError());
+    c->last_launches += 1;
+    return MCP_OK;
+  }
   k_tail_gram<<<grid_for((int64_t)r * r, 128, 8 * c->sms), 128, 0, s>>>(
       dx, n, r, d, (double*)c->dG.p, (double*)c->dC.p);
   k_tail_vec<<<1, 256, sizeof(double) * r, s>>>(dx, dYw, (const double*)c->dG.p,
@@ -283,7 +296,8 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     CUDA_TRY(c, cudaGraphInstantiate(&ge.exec, ge.graph, 0));
     it = c->graphs.emplace(key, ge).first;
   } else {
-    c->last_launches = 6;
+    c->last_launches = (pl.k1.needs_prep() ? 3 : 2) +
+                       (((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) ? 1 : 3);
     c->variant = pl.k1.name;
   }
   CUDA_TRY(c, cudaGraphLaunch(it->second.exec, c->stream));
@@ -294,8 +308,7 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
 template <typename T>
 int upload_obs(mcp_ctx* c, const T* V, bool on_device, int layout, int64_t n, int64_t p,
                int64_t ld) {
-  const int64_t seg = 16 / sizeof(T);
-  const int64_t ldv = round_up(n, seg);
+  const int64_t ldv = obs_pitch(sizeof(T) == 8 ? MCP_F64 : MCP_F32, n);
   const int64_t p_pad = round_up(p, (int64_t)K1_TP);
   const size_t bytes = sizeof(T) * (size_t)p_pad * ldv;
   if (c->dV) cudaFree(c->dV);

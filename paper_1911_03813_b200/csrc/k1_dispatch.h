@@ -22,6 +22,10 @@ struct K1Variant {
   size_t afrag_elems = 0, ypart_elems = 0, wpart_elems = 0;
   std::string name;
   int entry = -1;
+  int kind = 0;        // 0: k1_fg_dmma (generic, cp.async chunks)  1: k1s_fg_stream (TMA slabs)
+  int stages = 0;      // ring depth (kind 1)
+  int MT = 0;          // GEMM2 m-tiles (kind 1)
+  bool needs_prep() const { return kind == 0; }
 };
 
 // Choose the variant for (dtype, n, r, p_pad) on a device with `sms` SMs.
@@ -29,7 +33,10 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
 
 // Launch K1 on stream s; returns 0 on success.
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
-              double nu_const, const double* Afrag, int d, double* Ypart, double* wpart,
-              cudaStream_t s);
+              double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
+              double* wpart, cudaStream_t s);
+
+// Row pitch (elements) the observation upload uses for dtype / n.
+int64_t obs_pitch(int dtype, int64_t n);
 
 }  // namespace mcp

@@ -1,9 +1,11 @@
 // Instantiations of the K1 FP64 kernel family and the host-side variant selection.
 #include <atomic>
+#include <cstdlib>
 
 #include "momentcp_b200.h"
 #include "k1_dispatch.h"
 #include "k1_fp64.cuh"
+#include "k1s_fp64.cuh"
 
 namespace mcp {
 namespace {
@@ -67,10 +69,120 @@ int occupancy(int e) {
   return occ;
 }
 
+// ---------------- K1S (TMA-streamed slabs, fp64, n <= 128) ----------------
+template <int NTM, int TAIL, int MTH>
+void launch_s(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
+  k1s_fg_stream<NTM, TAIL, MTH><<<grid, K1S_THREADS, smem, s>>>(prm);
+}
+using LaunchS = void (*)(const K1SParams&, int, size_t, cudaStream_t);
+struct EntryS {
+  int NTM, TAIL, MTH;
+  LaunchS launch;
+  const void* fn;
+};
+#define MCP_K1S_E(NTM, TAIL, MTH) \
+  {NTM, TAIL, MTH, &launch_s<NTM, TAIL, MTH>, (const void*)&k1s_fg_stream<NTM, TAIL, MTH>}
+#define MCP_K1S_ALLT(NTM, MTH) \
+  MCP_K1S_E(NTM, 0, MTH), MCP_K1S_E(NTM, 1, MTH), MCP_K1S_E(NTM, 2, MTH), MCP_K1S_E(NTM, 3, MTH)
+// register budget: MTH * (2*NTM + TAIL) <= 40 accumulator doubles per lane
+const EntryS kTableS[] = {
+    MCP_K1S_ALLT(1, 1), MCP_K1S_ALLT(2, 1), MCP_K1S_ALLT(1, 2), MCP_K1S_ALLT(2, 2),
+    MCP_K1S_ALLT(1, 4), MCP_K1S_ALLT(2, 4), MCP_K1S_ALLT(1, 7), MCP_K1S_E(2, 0, 7),
+    MCP_K1S_ALLT(1, 8), MCP_K1S_E(2, 0, 8)};
+constexpr int kEntriesS = sizeof(kTableS) / sizeof(kTableS[0]);
+std::atomic<bool> g_attr_s[kEntriesS];
+
+bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
+  if (n > 128 || r > 19) return false;
+  const int MT = (int)ceil_div(n, 8);
+  int mtm = 0;  // m-tiles per warp of a pair
+  for (int c : {1, 2, 4, 7, 8})
+    if (2 * c >= MT) {
+      mtm = c;
+      break;
+    }
+  int ntm, tail;
+  if (r <= 8) { ntm = 1; tail = 0; }
+  else if (r <= 11) { ntm = 1; tail = r - 8; }
+  else if (r <= 16) { ntm = 2; tail = 0; }
+  else { ntm = 2; tail = r - 16; }
+  int e = -1;
+  auto find = [&](int a, int b) {
+    for (int i = 0; i < kEntriesS; ++i)
+      if (kTableS[i].NTM == a && kTableS[i].TAIL == b && kTableS[i].MTH == mtm) return i;
+    return -1;
+  };
+  e = find(ntm, tail);
+  if (e < 0 && ntm == 1) {  // register budget exceeded: pad the tail onto a second DMMA tile
+    ntm = 2;
+    tail = 0;
+    e = find(ntm, tail);
+  }
+  if (e < 0) return false;
+  const int cw = 8 * ntm + tail;
+  const size_t stage = (size_t)K1S_SR * ldv * 8;
+  const size_t fixed = k1s_fixed_bytes(ldv, ntm, cw, K1S_PAIRS);
+  const size_t budget = 227 * 1024 - 1024;
+  if (fixed + 2 * stage + 64 > budget) return false;
+  int S = (int)((budget - fixed) / (stage + 16));
+  if (S > 32) S = 32;
+  const size_t stage_need =
+      (size_t)K1S_PAIRS * MT * 8 * cw * 8 + (size_t)2 * K1S_PAIRS * cw * 8;
+  if ((size_t)S * stage < stage_need) return false;
+  const size_t smem = (size_t)S * stage + fixed + 16 * (size_t)S;
+  if (!g_attr_s[e].exchange(true)) {
+    if (cudaFuncSetAttribute(kTableS[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+      (void)cudaGetLastError();
+      g_attr_s[e].store(false);
+      return false;
+    }
+  } else {
+    cudaFuncSetAttribute(kTableS[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  v.kind = 1;
+  v.dtype = MCP_F64;
+  v.RB = cw;
+  v.MTW = mtm;
+  v.MT = MT;
+  v.n_chunks = 0;
+  v.n_pad = MT * 8;
+  v.rbs = 1;
+  v.num_tiles = p_pad / K1S_SR;
+  int64_t gp = sms;
+  if (gp > v.num_tiles) gp = v.num_tiles;
+  v.gp = (int)gp;
+  v.grid = v.gp;
+  v.stages = S;
+  v.smem = smem;
+  v.entry = e;
+  v.afrag_elems = 0;
+  v.ypart_elems = (size_t)v.gp * v.n_pad * cw;
+  v.wpart_elems = (size_t)v.gp * cw;
+  v.name = "k1s_fg_stream<f64,DMMA=" + std::to_string(8 * ntm) + ",DFMA=" +
+           std::to_string(tail) + ",MTH=" + std::to_string(mtm) + ",S=" + std::to_string(S) + ">";
+  return true;
+}
+
 }  // namespace
+
+int64_t obs_pitch(int dtype, int64_t n) {
+  if (dtype == MCP_F64) {
+    // == 4 (mod 16) doubles: conflict-free fragment loads straight from the TMA-staged rows
+    int64_t ldv = n < 4 ? 4 : n;
+    while (ldv % 16 != 4) ++ldv;
+    return ldv;
+  }
+  return round_up(n, 4);
+}
 
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v,
                std::string& why) {
+  v = K1Variant();
+  if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1S") &&
+      select_stream(n, r, p_pad, obs_pitch(dtype, n), sms, v))
+    return true;
+  v = K1Variant();
   const int n_chunks = (int)ceil_div(n, K1_NK);
   int mtw = 1;
   while (mtw < n_chunks) mtw *= 2;
@@ -120,9 +232,29 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
 }
 
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
-              double nu_const, const double* Afrag, int d, double* Ypart, double* wpart,
-              cudaStream_t s) {
+              double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
+              double* wpart, cudaStream_t s) {
   if (v.entry < 0) return 1;
+  if (v.kind == 1) {
+    K1SParams sp;
+    sp.V = static_cast<const double*>(dV);
+    sp.ldv = ldv;
+    sp.num_slabs = v.num_tiles;
+    sp.n = n;
+    sp.MT = v.MT;
+    sp.nu = dnu;
+    sp.nu_const = nu_const;
+    sp.A = A;
+    sp.r = r;
+    sp.d = d;
+    sp.rbs = 1;
+    sp.gp = v.gp;
+    sp.stages = v.stages;
+    sp.Ypart = Ypart;
+    sp.wpart = wpart;
+    kTableS[v.entry].launch(sp, v.grid, v.smem, s);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
+  }
   K1Params prm;
   prm.V = dV;
   prm.ldv = ldv;

@@ -1,0 +1,336 @@
+// K1S (FP64 mode, n <= 128): warp-specialised streaming f+grad partial over 16-row slabs.
+//
+// Same arithmetic as K1 (reference pkg/src/momentcp/implicit.py:94-107 + w of :124-140):
+//   Z = V_slab A  ->  P = nu * Z^(d-1), w += P*Z  ->  Y += V_slab^T P
+// organised for the HBM-bound small-n configs (BASELINE c1, c2):
+//   * one producer warp streams contiguous 16-row slabs HBM -> SMEM with 1-D TMA bulk copies
+//     (cp.async.bulk + mbarrier complete_tx) into an S-stage ring, V read from HBM exactly once;
+//   * 8 pairs of math warps; slab k of the CTA goes to pair k mod 8.  In a pair, warp h runs
+//     GEMM1 + epilogue for slab rows 8h..8h+7 and GEMM2 for its half of the n m-tiles; the only
+//     synchronisation is one 64-thread named barrier per slab (P is double buffered), so the
+//     main loop has no CTA-wide barrier and 4 math warps per SM sub-partition hide latency;
+//   * the factor block is 8*NTM DMMA columns plus TAIL (0..3) DFMA columns, so r = 10 (c2) runs
+//     as 8 DMMA + 2 DFMA columns with no padded FP64 work (DMMA and DFMA share the FP64 pipe).
+// The smem row pitch equals the global pitch ldv (== 4 mod 16 doubles, chosen at upload) so both
+// GEMMs' 8-byte fragment loads are bank-conflict free.  Per-warp Y partials stay in registers for
+// the whole kernel; warps and CTAs are combined in a fixed order (bitwise reproducible).
+#pragma once
+
+#include "mcp_common.cuh"
+
+namespace mcp {
+
+constexpr int K1S_SR = 16;   // observations per slab
+
+struct K1SParams {
+  const double* V;       // p_pad x ldv observation-major, fp64
+  int64_t ldv;           // row pitch (elements), == 4 mod 16
+  int64_t num_slabs;     // p_pad / K1S_SR
+  int n;
+  int MT;                // ceil(n / 8) m-tiles of GEMM2
+  const double* nu;      // nullptr -> nu_const
+  double nu_const;
+  const double* A;       // n x r column-major (packed x + r)
+  int r;
+  int d;
+  int rbs;               // column blocks of width 8*NTM + TAIL
+  int gp;                // CTAs per column block
+  int stages;            // ring depth
+  double* Ypart;         // [rbs][gp][MT*8][CW]
+  double* wpart;         // [rbs][gp][CW]
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D TMA: global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// P staging pitch (doubles) for a CW-column block: == 12 or 20 (mod 32 words: 24t / 8t), which
+// makes the GEMM2 B-fragment loads P[4ks + t][8nt + g] bank-conflict free.
+__host__ __device__ constexpr int k1s_pp(int cw) { return cw <= 12 ? 12 : 20; }
+
+// Dynamic smem layout, in order:
+//   ring: stages * SR * ldv doubles | Afrag: (ldv/4) * NTM * 32 doubles | Atail: ldv * 4 doubles
+//   P staging: pairs * 2 * SR * PP doubles | barriers: 2 * stages u64
+__host__ __device__ inline size_t k1s_fixed_bytes(int64_t ldv, int ntm, int cw, int pairs) {
+  return (size_t)(ldv / 4) * ntm * 32 * 8 + (size_t)ldv * 4 * 8 +
+         (size_t)pairs * 2 * K1S_SR * k1s_pp(cw) * 8;
+}
+
+
+constexpr int K1S_PAIRS = 7;  // math warp pairs per CTA (15 warps: <= 4 per SMSP -> 128 regs)
+constexpr int K1S_THREADS = (2 * K1S_PAIRS + 1) * 32;  // + 1 producer warp
+
+// MTH: GEMM2 m-tiles per warp (warp 0 of a pair: tiles [0, MTH), warp 1: [MTH, MT)).
+template <int NTM, int TAIL, int MTH>
+__global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
+  constexpr int CW = 8 * NTM + TAIL;
+  constexpr int PP = k1s_pp(CW);
+  constexpr int TL = TAIL > 0 ? TAIL : 1;
+  constexpr int NP = K1S_PAIRS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int64_t ldv = prm.ldv;
+  const int S = prm.stages;
+  const int kst = (int)(ldv / 4);
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  double* sAf = ring + (size_t)S * K1S_SR * ldv;
+  double* sAt = sAf + (size_t)kst * NTM * 32;
+  double* sP = sAt + ldv * 4;                                   // [NP][2][SR][PP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sP + NP * 2 * K1S_SR * PP);
+  uint64_t* empty = full + S;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int rb = blockIdx.x % prm.rbs;
+  const int pg = blockIdx.x / prm.rbs;
+  const int col0 = rb * CW;
+
+  for (int idx = threadIdx.x; idx < kst * NTM * 32; idx += blockDim.x) {
+    const int ln = idx & 31, nt = (idx >> 5) % NTM, ks = (idx >> 5) / NTM;
+    const int i = 4 * ks + (ln & 3), j = col0 + 8 * nt + (ln >> 2);
+    sAf[idx] = (i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < ldv * 4; idx += blockDim.x) {
+    const int i = idx >> 2, c = idx & 3, j = col0 + 8 * NTM + c;
+    sAt[idx] = (c < TAIL && i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t my_slabs = pg < prm.num_slabs ? (prm.num_slabs - pg + prm.gp - 1) / prm.gp : 0;
+  const uint32_t slab_bytes = (uint32_t)(K1S_SR * ldv * sizeof(double));
+
+  if (warp == 2 * NP) {
+    // ---------------- producer: one lane streams slabs into the ring ----------------
+    if (lane == 0) {
+      for (int64_t k = 0; k < my_slabs; ++k) {
+        const int s = (int)(k % S);
+        if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], slab_bytes);
+        tma_bulk_g2s(ring + (size_t)s * K1S_SR * ldv, prm.V + (pg + k * prm.gp) * K1S_SR * ldv,
+                     slab_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- math warps ----------------
+  const int q = warp >> 1, h = warp & 1;
+  const int mbase = h * MTH;
+  const int mcnt = h == 0 ? MTH : prm.MT - MTH;  // 0 < mcnt <= MTH
+  double yacc[MTH][NTM][2];
+  double ytl[MTH][TL];
+  double wacc[NTM][2];
+  double wtl = 0.0;
+#pragma unroll
+  for (int m = 0; m < MTH; ++m) {
+#pragma unroll
+    for (int nt = 0; nt < NTM; ++nt) yacc[m][nt][0] = yacc[m][nt][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < TL; ++c) ytl[m][c] = 0.0;
+  }
+#pragma unroll
+  for (int nt = 0; nt < NTM; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
+  const int dm1 = prm.d - 1;
+  const int lr = 8 * h + g;
+
+  int64_t kk = 0;
+  for (int64_t k = q; k < my_slabs; k += NP, ++kk) {
+    const int s = (int)(k % S);
+    mbar_wait(&full[s], (uint32_t)(k / S) & 1);
+    const double* sv = ring + (size_t)s * K1S_SR * ldv;
+    const int64_t row0 = (pg + k * prm.gp) * K1S_SR;
+    double* Pb = sP + ((size_t)q * 2 + (kk & 1)) * K1S_SR * PP;
+
+    // ---- GEMM1 on rows 8h..8h+7: even/odd k-steps in separate accumulators (2 chains) ----
+    double ze[NTM][2], zo[NTM][2], zte[TL], zto[TL];
+#pragma unroll
+    for (int nt = 0; nt < NTM; ++nt) ze[nt][0] = ze[nt][1] = zo[nt][0] = zo[nt][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < TL; ++c) zte[c] = zto[c] = 0.0;
+    const double* vrow = sv + lr * ldv + t;
+    const double* af = sAf + lane;
+    const double* at = sAt + t * 4;
+    int ks = 0;
+#pragma unroll 2
+    for (; ks + 1 < kst; ks += 2) {
+      const double a0 = vrow[4 * ks], a1 = vrow[4 * ks + 4];
+#pragma unroll
+      for (int nt = 0; nt < NTM; ++nt) {
+        dmma884(ze[nt], a0, af[(ks * NTM + nt) * 32]);
+        dmma884(zo[nt], a1, af[((ks + 1) * NTM + nt) * 32]);
+      }
+      if constexpr (TAIL > 0) {
+#pragma unroll
+        for (int c = 0; c < TAIL; ++c) {
+          zte[c] = fma(a0, at[16 * ks + c], zte[c]);
+          zto[c] = fma(a1, at[16 * ks + 16 + c], zto[c]);
+        }
+      }
+    }
+    if (ks < kst) {
+      const double a0 = vrow[4 * ks];
+#pragma unroll
+      for (int nt = 0; nt < NTM; ++nt) dmma884(ze[nt], a0, af[(ks * NTM + nt) * 32]);
+#pragma unroll
+      for (int c = 0; c < TAIL; ++c) zte[c] = fma(a0, at[16 * ks + c], zte[c]);
+    }
+    // ---- epilogue: z, P = nu z^(d-1), w += P z ----
+    const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
+#pragma unroll
+    for (int nt = 0; nt < NTM; ++nt) {
+      double pv[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double zz = ze[nt][e] + zo[nt][e];
+        pv[e] = nul * rm_pow(zz, dm1);
+        wacc[nt][e] = fma(pv[e], zz, wacc[nt][e]);
+      }
+      *reinterpret_cast<double2*>(&Pb[lr * PP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
+    }
+    if constexpr (TAIL > 0) {
+#pragma unroll
+      for (int c = 0; c < TAIL; ++c) {
+        double zz = zte[c] + zto[c];
+        zz += __shfl_xor_sync(0xffffffffu, zz, 1);   // lane t summed i == t (mod 4)
+        zz += __shfl_xor_sync(0xffffffffu, zz, 2);
+        if (t == c) {
+          const double pv = nul * rm_pow(zz, dm1);
+          wtl = fma(pv, zz, wtl);
+          Pb[lr * PP + 8 * NTM + c] = pv;
+        }
+      }
+    }
+    asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+
+    // ---- GEMM2: Y[m-tiles of this half] += V_slab^T P over the slab's 16 rows ----
+#pragma unroll
+    for (int k2 = 0; k2 < K1S_SR / 4; ++k2) {
+      const double* prow = Pb + (4 * k2 + t) * PP;
+      double b[NTM], bt[TL];
+#pragma unroll
+      for (int nt = 0; nt < NTM; ++nt) b[nt] = prow[8 * nt + g];
+#pragma unroll
+      for (int c = 0; c < TAIL; ++c) bt[c] = prow[8 * NTM + c];
+      const double* vr = sv + (4 * k2 + t) * ldv + 8 * mbase + g;
+#pragma unroll
+      for (int m = 0; m < MTH; ++m) {
+        if (m < MTH - 1 || mcnt == MTH) {
+          double a = vr[8 * m];
+          if (m == MTH - 1) a = (8 * (mbase + m) + g < prm.n) ? a : 0.0;  // rows past n
+#pragma unroll
+          for (int nt = 0; nt < NTM; ++nt) dmma884(yacc[m][nt], a, b[nt]);
+#pragma unroll
+          for (int c = 0; c < TAIL; ++c) ytl[m][c] = fma(a, bt[c], ytl[m][c]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- fixed-order combine of the 16 warps' partials ----------------
+#pragma unroll
+  for (int m = 0; m < MTH; ++m)
+#pragma unroll
+    for (int c = 0; c < TAIL; ++c) {
+      ytl[m][c] += __shfl_xor_sync(0xffffffffu, ytl[m][c], 1);   // lane t summed l == t (mod 4)
+      ytl[m][c] += __shfl_xor_sync(0xffffffffu, ytl[m][c], 2);
+    }
+#pragma unroll
+  for (int nt = 0; nt < NTM; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = wacc[nt][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      wacc[nt][e] = v;
+    }
+  wtl += __shfl_xor_sync(0xffffffffu, wtl, 4);
+  wtl += __shfl_xor_sync(0xffffffffu, wtl, 8);
+  wtl += __shfl_xor_sync(0xffffffffu, wtl, 16);
+  const int MT = prm.MT;
+  // all slabs consumed by every math warp -> the ring is free: [NP][MT*8][CW] + [2NP][CW]
+  asm volatile("bar.sync 15, %0;\n" ::"n"(2 * NP * 32) : "memory");
+  double* stage = ring + (size_t)q * MT * 8 * CW;
+#pragma unroll
+  for (int m = 0; m < MTH; ++m) {
+    if (m < mcnt) {
+      const int row = 8 * (mbase + m) + g;
+#pragma unroll
+      for (int nt = 0; nt < NTM; ++nt) {
+        stage[row * CW + 8 * nt + 2 * t] = yacc[m][nt][0];
+        stage[row * CW + 8 * nt + 2 * t + 1] = yacc[m][nt][1];
+      }
+#pragma unroll
+      for (int c = 0; c < TAIL; ++c)
+        if (t == c) stage[row * CW + 8 * NTM + c] = ytl[m][c];
+    }
+  }
+  double* wst = ring + (size_t)NP * MT * 8 * CW + warp * CW;
+  if (g == 0) {
+#pragma unroll
+    for (int nt = 0; nt < NTM; ++nt) {
+      wst[8 * nt + 2 * t] = wacc[nt][0];
+      wst[8 * nt + 2 * t + 1] = wacc[nt][1];
+    }
+    if (t < TAIL) wst[8 * NTM + t] = wtl;
+  }
+  asm volatile("bar.sync 15, %0;\n" ::"n"(2 * NP * 32) : "memory");
+  const int per_cta = MT * 8 * CW;
+  double* Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * per_cta;
+  for (int e = threadIdx.x; e < per_cta; e += 2 * NP * 32) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < NP; ++w) acc += ring[(size_t)w * per_cta + e];
+    Yp[e] = acc;
+  }
+  if (threadIdx.x < CW) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < 2 * NP; ++w) acc += ring[(size_t)NP * per_cta + w * CW + threadIdx.x];
+    prm.wpart[((size_t)rb * prm.gp + pg) * CW + threadIdx.x] = acc;
+  }
+}
+
+}  // namespace mcp

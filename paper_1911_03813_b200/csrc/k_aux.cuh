@@ -27,37 +27,51 @@ __global__ void k_prep_afrag(const double* __restrict__ A, int n, int r, int RB,
   }
 }
 
-// K3: Y[i][j] = sum over persistent CTAs (fixed order) of the per-CTA partials; w likewise.
+// K3: Y[i][j] = sum over the persistent CTAs' partials, in a fixed order; w likewise.
 // Output Yw = [vec_F(Y) (n*r) ; w (r)], the additive piece all-reduced across ranks.
-__global__ void k_reduce_partials(const double* __restrict__ Ypart, const double* __restrict__ wpart,
-                                  int n, int r, int n_pad, int RB, int rbs, int gp,
-                                  double* __restrict__ Yw) {
-  const int64_t ny = (int64_t)rbs * n * RB;
-  const int64_t total = ny + (int64_t)rbs * RB;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    if (idx < ny) {
-      const int jl = idx % RB;
-      const int64_t rest = idx / RB;
-      const int i = rest % n;
-      const int rb = rest / n;
-      const int j = rb * RB + jl;
-      if (j >= r) continue;
-      const double* src = Ypart + ((size_t)rb * gp * n_pad + i) * RB + jl;
-      double s = 0.0;
-      for (int q = 0; q < gp; ++q) s += src[(size_t)q * n_pad * RB];
-      Yw[(int64_t)j * n + i] = s;
+// Block = 32 consecutive outputs x 8 partial-groups: thread (tx, ty) sums partials
+// q = ty, ty+8, ... (coalesced 256-byte rows), then ty = 0 adds the 8 group sums in order.
+constexpr int K3_X = 32, K3_Y = 8;
+__global__ void __launch_bounds__(K3_X * K3_Y)
+    k_reduce_partials(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
+                      int r, int n_pad, int RB, int rbs, int gp, double* __restrict__ Yw) {
+  __shared__ double s_acc[K3_Y][K3_X];
+  const int tx = threadIdx.x % K3_X, ty = threadIdx.x / K3_X;
+  const int per_rb = n * RB;                          // Y outputs of one column block
+  const int yblocks = (per_rb + K3_X - 1) / K3_X;     // blocks per column block
+  const int64_t total_blocks = (int64_t)rbs * yblocks + (rbs * RB + K3_X - 1) / K3_X;
+  for (int64_t blk = blockIdx.x; blk < total_blocks; blk += gridDim.x) {
+    double s = 0.0;
+    int64_t dst = -1;
+    if (blk < (int64_t)rbs * yblocks) {
+      const int rb = blk / yblocks;
+      const int e = (blk % yblocks) * K3_X + tx;       // e = i * RB + jl
+      if (e < per_rb) {
+        const int i = e / RB, jl = e % RB, j = rb * RB + jl;
+        const double* src = Ypart + ((size_t)rb * gp * n_pad + i) * RB + jl;
+#pragma unroll 4
+        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * n_pad * RB];
+        if (j < r) dst = (int64_t)j * n + i;
+      }
     } else {
-      const int64_t k = idx - ny;
-      const int jl = k % RB;
-      const int rb = k / RB;
-      const int j = rb * RB + jl;
-      if (j >= r) continue;
-      const double* src = wpart + (size_t)rb * gp * RB + jl;
-      double s = 0.0;
-      for (int q = 0; q < gp; ++q) s += src[(size_t)q * RB];
-      Yw[(int64_t)n * r + j] = s;
+      const int k = (blk - (int64_t)rbs * yblocks) * K3_X + tx;   // k = rb * RB + jl
+      if (k < rbs * RB) {
+        const int rb = k / RB, jl = k % RB, j = rb * RB + jl;
+        const double* src = wpart + (size_t)rb * gp * RB + jl;
+#pragma unroll 4
+        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * RB];
+        if (j < r) dst = (int64_t)n * r + j;
+      }
     }
+    s_acc[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && dst >= 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int y = 0; y < K3_Y; ++y) t += s_acc[y][tx];
+      Yw[dst] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -117,6 +131,62 @@ __global__ void k_tail_ga(const double* __restrict__ x, const double* __restrict
     double m = 0.0;
     for (int k = 0; k < r; ++k) m += (A[(int64_t)k * n + i] * lam[k]) * C[(int64_t)k * r + j];
     out[1 + r + idx] = (s * (Yw[idx] - m)) * lam[j];
+  }
+}
+
+// K4 fused (one CTA) for small factor blocks (n*r <= K4S_MAX_NR, r <= K4S_MAX_R): G, C, u, f, g_lam
+// and g_A in a single launch, all intermediates in shared memory.  Same algebra and operation
+// order as the three-kernel tail above (implicit.py:147-149, objective.py:51-56).
+constexpr int K4S_THREADS = 512;
+constexpr int K4S_MAX_NR = 4096;
+constexpr int K4S_MAX_R = 32;
+__global__ void __launch_bounds__(K4S_THREADS)
+    k_tail_fused(const double* __restrict__ x, const double* __restrict__ Yw, int n, int r, int d,
+                 const double* __restrict__ alpha_dev, double alpha_host,
+                 double* __restrict__ out) {
+  __shared__ double sA[K4S_MAX_NR];
+  __shared__ double sC[K4S_MAX_R * K4S_MAX_R];
+  __shared__ double sU[K4S_MAX_R];
+  const double* lam = x;
+  const double* w = Yw + (int64_t)n * r;
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) sA[e] = x[r + e];
+  __syncthreads();
+  // G_jk = a_j . a_k: one warp per (j, k), lanes stride over i, fixed shuffle order
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pr = warp; pr < r * r; pr += K4S_THREADS / 32) {
+    const int j = pr / r, k = pr % r;
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += sA[j * n + i] * sA[k * n + i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) sC[pr] = s;  // G for now
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double u = 0.0;
+    for (int k = 0; k < r; ++k) {
+      const double gjk = sC[j * r + k];
+      u += (gjk * rm_pow(gjk, d - 1)) * lam[k];
+    }
+    sU[j] = u;
+    out[1 + j] = -2.0 * (w[j] - u);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) sC[e] = rm_pow(sC[e], d - 1);  // C
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double lu = 0.0, wl = 0.0;
+    for (int j = 0; j < r; ++j) lu += lam[j] * sU[j];
+    for (int j = 0; j < r; ++j) wl += w[j] * lam[j];
+    const double alpha = alpha_dev ? *alpha_dev : alpha_host;
+    out[0] = alpha + lu - 2.0 * wl;
+  }
+  const double s2d = -2.0 * d;
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) {
+    const int j = e / n, i = e % n;
+    double m = 0.0;
+    for (int k = 0; k < r; ++k) m += (sA[k * n + i] * lam[k]) * sC[k * r + j];
+    out[1 + r + e] = (s2d * (Yw[e] - m)) * lam[j];
   }
 }
 

@@ -23,6 +23,7 @@ import time
 
 import numpy as np
 
+from ._native import stream_handle
 from .dense import ObservationSet
 from .objective import FgResult, validate_variables
 from .optimize import pack
@@ -49,7 +50,7 @@ def device_partial(obs: ObservationSet, lam, A, d: int, mode: str | None = None)
     dev = torch.device("cuda", ctx.device)
     x = torch.as_tensor(pack(lam, A), dtype=torch.float64, device=dev)
     Yw = torch.empty(n * r + r, dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    stream = stream_handle(torch.cuda.current_stream(dev))
     ctx.fg_partial_device(d, r, x.data_ptr(), mode, Yw.data_ptr(), stream)
     Yw._mcp_x = x  # keep x alive until the stream has consumed it
     return Yw
@@ -63,7 +64,7 @@ def device_finish(obs: ObservationSet, lam, A, d: int, alpha: float, Yw):
     dev = torch.device("cuda", ctx.device)
     x = torch.as_tensor(pack(lam, A), dtype=torch.float64, device=dev)
     out = torch.empty(1 + r + n * r, dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    stream = stream_handle(torch.cuda.current_stream(dev))
     ctx.fg_finish_device(d, r, x.data_ptr(), Yw.data_ptr(), float(alpha), out.data_ptr(), stream)
     h = out.cpu().numpy()
     return float(h[0]), h[1:1 + r].copy(), h[1 + r:].reshape((n, r), order="F").copy()

@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1911_03813_b200 as mcp  # noqa: E402
-from paper_1911_03813_b200 import synth  # noqa: E402
+from paper_1911_03813_b200 import _native, synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
@@ -27,7 +27,7 @@ else:
     lam, A = synth.initial_point(cfg, 2024)
     x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
     out = torch.empty(1 + cfg.r + cfg.n * cfg.r, dtype=torch.float64, device="cuda")
-    s = torch.cuda.current_stream().cuda_stream
+    s = _native.stream_handle(torch.cuda.current_stream())
     for _ in range(a.evals):
         ctx.fg_device(cfg.d, cfg.r, x.data_ptr(), 0.0, None, out.data_ptr(), s)
     torch.cuda.synchronize()

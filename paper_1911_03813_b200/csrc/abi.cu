@@ -309,7 +309,8 @@ template <typename T>
 int upload_obs(mcp_ctx* c, const T* V, bool on_device, int layout, int64_t n, int64_t p,
                int64_t ld) {
   const int64_t ldv = obs_pitch(sizeof(T) == 8 ? MCP_F64 : MCP_F32, n);
-  const int64_t p_pad = round_up(p, (int64_t)K1_TP);
+  // rows padded to a multiple of 448 = lcm(K1 tile 64, K1S copy unit 14 x 16) with zeros
+  const int64_t p_pad = round_up(p, (int64_t)448);
   const size_t bytes = sizeof(T) * (size_t)p_pad * ldv;
   if (c->dV) cudaFree(c->dV);
   c->dV = nullptr;

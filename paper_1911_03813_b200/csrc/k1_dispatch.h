@@ -25,6 +25,7 @@ struct K1Variant {
   int kind = 0;        // 0: k1_fg_dmma (generic, cp.async chunks)  1: k1s_fg_stream (TMA slabs)
   int stages = 0;      // ring depth (kind 1)
   int MT = 0;          // GEMM2 m-tiles (kind 1)
+  int MTW2 = 1;        // slabs per TMA copy unit (kind 1)
   bool needs_prep() const { return kind == 0; }
 };
 

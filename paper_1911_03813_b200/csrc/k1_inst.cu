@@ -70,62 +70,71 @@ int occupancy(int e) {
 }
 
 // ---------------- K1S (TMA-streamed slabs, fp64, n <= 128) ----------------
-template <int NTM, int TAIL, int MTH>
+template <int NTM, int TAIL, int MTH, int KH>
 void launch_s(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
-  k1s_fg_stream<NTM, TAIL, MTH><<<grid, K1S_THREADS, smem, s>>>(prm);
+  k1s_fg_stream<NTM, TAIL, MTH, KH><<<grid, K1S_THREADS, smem, s>>>(prm);
 }
 using LaunchS = void (*)(const K1SParams&, int, size_t, cudaStream_t);
 struct EntryS {
-  int NTM, TAIL, MTH;
+  int NTM, TAIL, MTH, KH;
   LaunchS launch;
   const void* fn;
 };
-#define MCP_K1S_E(NTM, TAIL, MTH) \
-  {NTM, TAIL, MTH, &launch_s<NTM, TAIL, MTH>, (const void*)&k1s_fg_stream<NTM, TAIL, MTH>}
-#define MCP_K1S_ALLT(NTM, MTH) \
-  MCP_K1S_E(NTM, 0, MTH), MCP_K1S_E(NTM, 1, MTH), MCP_K1S_E(NTM, 2, MTH), MCP_K1S_E(NTM, 3, MTH)
-// register budget: MTH * (2*NTM + TAIL) <= 40 accumulator doubles per lane
-const EntryS kTableS[] = {
-    MCP_K1S_ALLT(1, 1), MCP_K1S_ALLT(2, 1), MCP_K1S_ALLT(1, 2), MCP_K1S_ALLT(2, 2),
-    MCP_K1S_ALLT(1, 4), MCP_K1S_ALLT(2, 4), MCP_K1S_ALLT(1, 7), MCP_K1S_E(2, 0, 7),
-    MCP_K1S_ALLT(1, 8), MCP_K1S_E(2, 0, 8)};
+#define MCP_K1S_E(NTM, TAIL, MTH, KH) \
+  {NTM, TAIL, MTH, KH, &launch_s<NTM, TAIL, MTH, KH>, \
+   (const void*)&k1s_fg_stream<NTM, TAIL, MTH, KH>}
+#define MCP_K1S_COLS(MTH, KH) \
+  MCP_K1S_E(1, 0, MTH, KH), MCP_K1S_E(1, 1, MTH, KH), MCP_K1S_E(1, 2, MTH, KH), \
+      MCP_K1S_E(2, 0, MTH, KH)
+// (MTH, KH) groups by n: <=16, <=32, <=64, ==97..100, <=104, <=128
+const EntryS kTableS[] = {MCP_K1S_COLS(1, 3),  MCP_K1S_COLS(2, 5),  MCP_K1S_COLS(4, 9),
+                          MCP_K1S_COLS(7, 13), MCP_K1S_COLS(7, 15), MCP_K1S_COLS(8, 17)};
 constexpr int kEntriesS = sizeof(kTableS) / sizeof(kTableS[0]);
 std::atomic<bool> g_attr_s[kEntriesS];
 
 bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
-  if (n > 128 || r > 19) return false;
+  if (n > 128 || r > 16) return false;
   const int MT = (int)ceil_div(n, 8);
-  int mtm = 0;  // m-tiles per warp of a pair
-  for (int c : {1, 2, 4, 7, 8})
-    if (2 * c >= MT) {
-      mtm = c;
-      break;
-    }
+  const int kst = (int)(ldv / 4);
+  const int mth_need = (MT + 1) / 2, kh_need = (kst + 1) / 2;
   int ntm, tail;
   if (r <= 8) { ntm = 1; tail = 0; }
-  else if (r <= 11) { ntm = 1; tail = r - 8; }
-  else if (r <= 16) { ntm = 2; tail = 0; }
-  else { ntm = 2; tail = r - 16; }
+  else if (r <= 10) { ntm = 1; tail = r - 8; }
+  else { ntm = 2; tail = 0; }
   int e = -1;
-  auto find = [&](int a, int b) {
-    for (int i = 0; i < kEntriesS; ++i)
-      if (kTableS[i].NTM == a && kTableS[i].TAIL == b && kTableS[i].MTH == mtm) return i;
-    return -1;
-  };
-  e = find(ntm, tail);
-  if (e < 0 && ntm == 1) {  // register budget exceeded: pad the tail onto a second DMMA tile
-    ntm = 2;
-    tail = 0;
-    e = find(ntm, tail);
-  }
+  for (int i = 0; i < kEntriesS && e < 0; ++i)
+    if (kTableS[i].NTM == ntm && kTableS[i].TAIL == tail && kTableS[i].MTH >= mth_need &&
+        kTableS[i].KH >= kh_need && 2 * kTableS[i].MTH >= MT + (8 * MT > n ? 0 : 0))
+      e = i;
   if (e < 0) return false;
+  const int mtm = kTableS[e].MTH;
   const int cw = 8 * ntm + tail;
-  const size_t stage = (size_t)K1S_SR * ldv * 8;
-  const size_t fixed = k1s_fixed_bytes(ldv, ntm, cw, K1S_PAIRS);
-  const size_t budget = 227 * 1024 - 1024;
-  if (fixed + 2 * stage + 64 > budget) return false;
-  int S = (int)((budget - fixed) / (stage + 16));
-  if (S > 32) S = 32;
+  // Copy units of spc slabs: the bulk-copy engine costs ~660 cycles per copy per SM whatever
+  // its size (tools/probe_tma.cu), so units must be >= ~24 KB to reach HBM bandwidth.  Every
+  // ring stage must be consumed by a fixed set of pairs (mbarrier parity waits cannot tell
+  // phase u from u + 2): spc in {7, 14} puts every pair in every unit, spc in {1, 2} needs a
+  // ring depth that is a multiple of K1S_PAIRS.
+  const size_t slab = (size_t)K1S_SR * ldv * 8;
+  const size_t fixed = k1s_fixed_bytes(kTableS[e].KH, ntm, cw, K1S_PAIRS);
+  const size_t budget = 227 * 1024 - 1024 - fixed;
+  int spc = 0, S = 0;
+  for (int cand : {1, 2, 7, 14}) {   // smallest unit >= 24 KB, else the largest that fits
+    int st = (int)(budget / (cand * slab + 16));
+    if (cand < K1S_PAIRS) {
+      if (st > 4 * K1S_PAIRS) st = 4 * K1S_PAIRS;
+      st -= st % K1S_PAIRS;
+      if (st < K1S_PAIRS) continue;
+    } else {
+      if (st > 8) st = 8;
+      if (st < 2) continue;
+    }
+    spc = cand;
+    S = st;
+    if (cand * slab >= 24 * 1024) break;
+  }
+  if (spc == 0) return false;
+  if ((p_pad / K1S_SR) % spc != 0) return false;
+  const size_t stage = (size_t)spc * slab;
   const size_t stage_need =
       (size_t)K1S_PAIRS * MT * 8 * cw * 8 + (size_t)2 * K1S_PAIRS * cw * 8;
   if ((size_t)S * stage < stage_need) return false;
@@ -154,13 +163,15 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
   v.gp = (int)gp;
   v.grid = v.gp;
   v.stages = S;
+  v.MTW2 = spc;
   v.smem = smem;
   v.entry = e;
   v.afrag_elems = 0;
   v.ypart_elems = (size_t)v.gp * v.n_pad * cw;
   v.wpart_elems = (size_t)v.gp * cw;
   v.name = "k1s_fg_stream<f64,DMMA=" + std::to_string(8 * ntm) + ",DFMA=" +
-           std::to_string(tail) + ",MTH=" + std::to_string(mtm) + ",S=" + std::to_string(S) + ">";
+           std::to_string(tail) + ",MTH=" + std::to_string(mtm) + ",KH=" +
+           std::to_string(kTableS[e].KH) + ",S=" + std::to_string(S) + ">";
   return true;
 }
 
@@ -250,6 +261,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     sp.rbs = 1;
     sp.gp = v.gp;
     sp.stages = v.stages;
+    sp.spc = v.MTW2;
     sp.Ypart = Ypart;
     sp.wpart = wpart;
     kTableS[v.entry].launch(sp, v.grid, v.smem, s);

@@ -5,10 +5,12 @@
 // organised for the HBM-bound small-n configs (BASELINE c1, c2):
 //   * one producer warp streams contiguous 16-row slabs HBM -> SMEM with 1-D TMA bulk copies
 //     (cp.async.bulk + mbarrier complete_tx) into an S-stage ring, V read from HBM exactly once;
-//   * 8 pairs of math warps; slab k of the CTA goes to pair k mod 8.  In a pair, warp h runs
-//     GEMM1 + epilogue for slab rows 8h..8h+7 and GEMM2 for its half of the n m-tiles; the only
-//     synchronisation is one 64-thread named barrier per slab (P is double buffered), so the
-//     main loop has no CTA-wide barrier and 4 math warps per SM sub-partition hide latency;
+//   * 7 pairs of math warps; slab k of the CTA goes to pair k mod 7.  In a pair, warp h runs
+//     GEMM1 over its half of the k-steps for all 16 slab rows (fixed KH steps, zero padded),
+//     the two K-halves are added through a small exchange
+//     buffer, warp h runs the epilogue for rows 8h..8h+7 and GEMM2 for its half of the n
+//     m-tiles.  Synchronisation is two 64-thread named barriers per slab -- no CTA-wide
+//     barrier in the main loop;
 //   * the factor block is 8*NTM DMMA columns plus TAIL (0..3) DFMA columns, so r = 10 (c2) runs
 //     as 8 DMMA + 2 DFMA columns with no padded FP64 work (DMMA and DFMA share the FP64 pipe).
 // The smem row pitch equals the global pitch ldv (== 4 mod 16 doubles, chosen at upload) so both
@@ -25,7 +27,8 @@ constexpr int K1S_SR = 16;   // observations per slab
 struct K1SParams {
   const double* V;       // p_pad x ldv observation-major, fp64
   int64_t ldv;           // row pitch (elements), == 4 mod 16
-  int64_t num_slabs;     // p_pad / K1S_SR
+  int64_t num_slabs;     // p_pad / K1S_SR (a multiple of spc)
+  int spc;               // slabs per TMA copy unit (one bulk copy fills spc slabs)
   int n;
   int MT;                // ceil(n / 8) m-tiles of GEMM2
   const double* nu;      // nullptr -> nu_const
@@ -35,7 +38,7 @@ struct K1SParams {
   int d;
   int rbs;               // column blocks of width 8*NTM + TAIL
   int gp;                // CTAs per column block
-  int stages;            // ring depth
+  int stages;            // ring depth in copy units
   double* Ypart;         // [rbs][gp][MT*8][CW]
   double* wpart;         // [rbs][gp][CW]
 };
@@ -64,8 +67,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Bounded wait: a pipeline bug traps (loud kernel error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1ll << 35)) __trap();
   }
 }
 // 1-D TMA: global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0).
@@ -84,18 +91,19 @@ __host__ __device__ constexpr int k1s_pp(int cw) { return cw <= 12 ? 12 : 20; }
 
 // Dynamic smem layout, in order:
 //   ring: stages * SR * ldv doubles | Afrag: (ldv/4) * NTM * 32 doubles | Atail: ldv * 4 doubles
-//   P staging: pairs * 2 * SR * PP doubles | barriers: 2 * stages u64
-__host__ __device__ inline size_t k1s_fixed_bytes(int64_t ldv, int ntm, int cw, int pairs) {
-  return (size_t)(ldv / 4) * ntm * 32 * 8 + (size_t)ldv * 4 * 8 +
-         (size_t)pairs * 2 * K1S_SR * k1s_pp(cw) * 8;
+//   P staging: pairs * SR * PP doubles | exchange: pairs * 2 * 32 * 4 doubles | barriers
+__host__ __device__ inline size_t k1s_fixed_bytes(int kh, int ntm, int cw, int pairs) {
+  return (size_t)(2 * kh) * ntm * 32 * 8 + (size_t)(2 * kh) * 16 * 8 +
+         (size_t)pairs * K1S_SR * k1s_pp(cw) * 8 + (size_t)pairs * 2 * 32 * 4 * 8;
 }
 
 
 constexpr int K1S_PAIRS = 7;  // math warp pairs per CTA (15 warps: <= 4 per SMSP -> 128 regs)
 constexpr int K1S_THREADS = (2 * K1S_PAIRS + 1) * 32;  // + 1 producer warp
 
-// MTH: GEMM2 m-tiles per warp (warp 0 of a pair: tiles [0, MTH), warp 1: [MTH, MT)).
-template <int NTM, int TAIL, int MTH>
+// NTM: 8-column DMMA tiles, TAIL: DFMA columns, MTH: GEMM2 m-tiles per warp (warp 0 of a pair
+// takes [0, MTH), warp 1 [MTH, MT)), KH: GEMM1 k-steps per warp (warp 0 [0, KH0), warp 1 the rest).
+template <int NTM, int TAIL, int MTH, int KH>
 __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   constexpr int CW = 8 * NTM + TAIL;
   constexpr int PP = k1s_pp(CW);
@@ -106,10 +114,13 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   const int S = prm.stages;
   const int kst = (int)(ldv / 4);
   double* ring = reinterpret_cast<double*>(smem_raw);
-  double* sAf = ring + (size_t)S * K1S_SR * ldv;
-  double* sAt = sAf + (size_t)kst * NTM * 32;
-  double* sP = sAt + ldv * 4;                                   // [NP][2][SR][PP]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sP + NP * 2 * K1S_SR * PP);
+  const int spc = prm.spc;
+  const int kpad = 2 * KH;                             // k-steps incl. zero padding
+  double* sAf = ring + (size_t)S * spc * K1S_SR * ldv;
+  double* sAt = sAf + (size_t)kpad * NTM * 32;
+  double* sP = sAt + kpad * 16;                        // [NP][SR][PP]
+  double* sX = sP + NP * K1S_SR * PP;                  // [NP][2][32][4] GEMM1 K-half exchange
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + NP * 2 * 32 * 4);
   uint64_t* empty = full + S;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,36 +129,53 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   const int pg = blockIdx.x / prm.rbs;
   const int col0 = rb * CW;
 
-  for (int idx = threadIdx.x; idx < kst * NTM * 32; idx += blockDim.x) {
+  // Factor block (zero beyond n / r and for the padding k-steps), and a zeroed ring: GEMM1 runs
+  // a fixed KH k-steps per warp, so warp 1's padding step multiplies finite V data (the next
+  // row, or zeros) by exact-zero factor entries -- never uninitialised shared memory.
+  for (int idx = threadIdx.x; idx < kpad * NTM * 32; idx += blockDim.x) {
     const int ln = idx & 31, nt = (idx >> 5) % NTM, ks = (idx >> 5) / NTM;
     const int i = 4 * ks + (ln & 3), j = col0 + 8 * nt + (ln >> 2);
     sAf[idx] = (i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
   }
-  for (int idx = threadIdx.x; idx < ldv * 4; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < kpad * 16; idx += blockDim.x) {
     const int i = idx >> 2, c = idx & 3, j = col0 + 8 * NTM + c;
     sAt[idx] = (c < TAIL && i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
   }
+  for (size_t idx = threadIdx.x; idx < (size_t)S * spc * K1S_SR * ldv; idx += blockDim.x)
+    ring[idx] = 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);
+      mbar_init(&empty[s], 2 * spc);   // both warps of each slab's pair release
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  const int64_t my_slabs = pg < prm.num_slabs ? (prm.num_slabs - pg + prm.gp - 1) / prm.gp : 0;
-  const uint32_t slab_bytes = (uint32_t)(K1S_SR * ldv * sizeof(double));
+  // CTA pg owns copy units pg, pg + gp, ... (a unit = spc consecutive slabs, one bulk copy);
+  // its k-th slab is slab (k mod spc) of its (k / spc)-th unit.
+  const int64_t num_units = prm.num_slabs / spc;
+  const int64_t my_units = pg < num_units ? (num_units - pg + prm.gp - 1) / prm.gp : 0;
+  const int64_t my_slabs = my_units * spc;
+  const uint32_t unit_bytes = (uint32_t)(spc * K1S_SR * ldv * sizeof(double));
 
   if (warp == 2 * NP) {
-    // ---------------- producer: one lane streams slabs into the ring ----------------
+    // ---------------- producer: one lane streams copy units into the ring ----------------
     if (lane == 0) {
-      for (int64_t k = 0; k < my_slabs; ++k) {
-        const int s = (int)(k % S);
-        if (k >= S) mbar_wait(&empty[s], (uint32_t)(k / S - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], slab_bytes);
-        tma_bulk_g2s(ring + (size_t)s * K1S_SR * ldv, prm.V + (pg + k * prm.gp) * K1S_SR * ldv,
-                     slab_bytes, &full[s]);
+      int s = 0;
+      uint32_t ph = 0;  // completed-use parity of stage s for the empty wait
+      const double* src = prm.V + (int64_t)pg * spc * K1S_SR * ldv;
+      const int64_t step = (int64_t)prm.gp * spc * K1S_SR * ldv;
+      for (int64_t j = 0; j < my_units; ++j) {
+        if (j >= S) mbar_wait(&empty[s], ph);
+        mbar_arrive_expect_tx(&full[s], unit_bytes);
+        tma_bulk_g2s(ring + (size_t)s * spc * K1S_SR * ldv, src, unit_bytes, &full[s]);
+        src += step;
+        if (++s == S) {
+          s = 0;
+          if (j >= S) ph ^= 1;
+          else ph = 0;
+        }
       }
     }
     return;
@@ -156,7 +184,8 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   // ---------------- math warps ----------------
   const int q = warp >> 1, h = warp & 1;
   const int mbase = h * MTH;
-  const int mcnt = h == 0 ? MTH : prm.MT - MTH;  // 0 < mcnt <= MTH
+  const int mcnt = h == 0 ? MTH : prm.MT - MTH;          // 0 <= mcnt <= MTH
+  const int kbase = h * KH;                              // warp h: k-steps [h*KH, h*KH + KH)
   double yacc[MTH][NTM][2];
   double ytl[MTH][TL];
   double wacc[NTM][2];
@@ -172,56 +201,102 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   for (int nt = 0; nt < NTM; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
   const int dm1 = prm.d - 1;
   const int lr = 8 * h + g;
+  double* Pb = sP + (size_t)q * K1S_SR * PP;
+  double* xo = sX + ((size_t)q * 2 + h) * 128 + lane * 4;       // my partial for rows of 1-h
+  const double* xi = sX + ((size_t)q * 2 + (1 - h)) * 128 + lane * 4;  // partner's, rows of h
 
-  int64_t kk = 0;
-  for (int64_t k = q; k < my_slabs; k += NP, ++kk) {
-    const int s = (int)(k % S);
-    mbar_wait(&full[s], (uint32_t)(k / S) & 1);
-    const double* sv = ring + (size_t)s * K1S_SR * ldv;
-    const int64_t row0 = (pg + k * prm.gp) * K1S_SR;
-    double* Pb = sP + ((size_t)q * 2 + (kk & 1)) * K1S_SR * PP;
+  // incremental slab -> (unit j, slab-in-unit sub, stage s, parity) walk (no 64-bit division)
+  int64_t j = q / spc;
+  int sub = q % spc;
+  int s = (int)(j % S);
+  uint32_t ph = (uint32_t)((j / S) & 1);
+  for (int64_t k = q; k < my_slabs; k += NP) {
+    mbar_wait(&full[s], ph);
+    const double* sv = ring + ((size_t)s * spc + sub) * K1S_SR * ldv;
+    const int64_t row0 = ((pg + j * prm.gp) * spc + sub) * K1S_SR;
+    const int s_cur = s;
+    sub += NP;
+    while (sub >= spc) {
+      sub -= spc;
+      ++j;
+      if (++s == S) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
 
-    // ---- GEMM1 on rows 8h..8h+7: even/odd k-steps in separate accumulators (2 chains) ----
-    double ze[NTM][2], zo[NTM][2], zte[TL], zto[TL];
+    // ---- GEMM1 partial over this warp's k-steps, all 16 slab rows ----
+    double z[2][NTM][2], zt[2][TL];
 #pragma unroll
-    for (int nt = 0; nt < NTM; ++nt) ze[nt][0] = ze[nt][1] = zo[nt][0] = zo[nt][1] = 0.0;
+    for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
-    for (int c = 0; c < TL; ++c) zte[c] = zto[c] = 0.0;
-    const double* vrow = sv + lr * ldv + t;
-    const double* af = sAf + lane;
-    const double* at = sAt + t * 4;
-    int ks = 0;
-#pragma unroll 2
-    for (; ks + 1 < kst; ks += 2) {
-      const double a0 = vrow[4 * ks], a1 = vrow[4 * ks + 4];
+      for (int nt = 0; nt < NTM; ++nt) z[mt][nt][0] = z[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < TL; ++c) zt[mt][c] = 0.0;
+    }
+    const double* v0 = sv + g * ldv + 4 * kbase + t;
+    const double* v1 = v0 + 8 * ldv;
+    const double* bp = sAf + kbase * NTM * 32 + lane;
+    const double* at = sAt + (4 * kbase + t) * 4;
+#pragma unroll
+    for (int kk = 0; kk < KH; ++kk) {
+      const double a0 = v0[4 * kk], a1 = v1[4 * kk];
 #pragma unroll
       for (int nt = 0; nt < NTM; ++nt) {
-        dmma884(ze[nt], a0, af[(ks * NTM + nt) * 32]);
-        dmma884(zo[nt], a1, af[((ks + 1) * NTM + nt) * 32]);
+        const double b = bp[(kk * NTM + nt) * 32];
+        dmma884(z[0][nt], a0, b);
+        dmma884(z[1][nt], a1, b);
       }
       if constexpr (TAIL > 0) {
-#pragma unroll
-        for (int c = 0; c < TAIL; ++c) {
-          zte[c] = fma(a0, at[16 * ks + c], zte[c]);
-          zto[c] = fma(a1, at[16 * ks + 16 + c], zto[c]);
+        const double2 tv = *reinterpret_cast<const double2*>(at + 16 * kk);
+        zt[0][0] = fma(a0, tv.x, zt[0][0]);
+        zt[1][0] = fma(a1, tv.x, zt[1][0]);
+        if constexpr (TAIL > 1) {
+          zt[0][TL - 1] = fma(a0, tv.y, zt[0][TL - 1]);
+          zt[1][TL - 1] = fma(a1, tv.y, zt[1][TL - 1]);
         }
       }
     }
-    if (ks < kst) {
-      const double a0 = vrow[4 * ks];
+    // ---- add the two K halves (fixed order: half 0 + half 1) ----
+    {
+      // hand the partner my partial for its m-tile (1 - h); select, never index by h
+      double xv[4];
 #pragma unroll
-      for (int nt = 0; nt < NTM; ++nt) dmma884(ze[nt], a0, af[(ks * NTM + nt) * 32]);
-#pragma unroll
-      for (int c = 0; c < TAIL; ++c) zte[c] = fma(a0, at[16 * ks + c], zte[c]);
+      for (int nt = 0; nt < NTM; ++nt) {
+        xv[2 * nt] = h == 0 ? z[1][nt][0] : z[0][nt][0];
+        xv[2 * nt + 1] = h == 0 ? z[1][nt][1] : z[0][nt][1];
+      }
+      if constexpr (NTM == 1) {
+        xv[2] = TAIL > 0 ? (h == 0 ? zt[1][0] : zt[0][0]) : 0.0;
+        xv[3] = TAIL > 1 ? (h == 0 ? zt[1][TL - 1] : zt[0][TL - 1]) : 0.0;
+      }
+      *reinterpret_cast<double2*>(xo) = make_double2(xv[0], xv[1]);
+      *reinterpret_cast<double2*>(xo + 2) = make_double2(xv[2], xv[3]);
     }
-    // ---- epilogue: z, P = nu z^(d-1), w += P z ----
+    static_assert(NTM == 1 ? TAIL <= 2 : TAIL == 0, "exchange slot holds 4 doubles per lane");
+    asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+    double zf[NTM][2], ztf[TL];
+    {
+      const double2 p01 = *reinterpret_cast<const double2*>(xi);
+      const double2 p23 = *reinterpret_cast<const double2*>(xi + 2);
+      const double pv[4] = {p01.x, p01.y, p23.x, p23.y};
+#pragma unroll
+      for (int nt = 0; nt < NTM; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          zf[nt][e] = h == 0 ? z[0][nt][e] + pv[2 * nt + e] : pv[2 * nt + e] + z[1][nt][e];
+#pragma unroll
+      for (int c = 0; c < TAIL; ++c)
+        ztf[c] = h == 0 ? zt[0][c] + pv[2 + c] : pv[2 + c] + zt[1][c];
+    }
+    // ---- epilogue on rows 8h..8h+7: P = nu z^(d-1), w += P z ----
     const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
 #pragma unroll
     for (int nt = 0; nt < NTM; ++nt) {
       double pv[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const double zz = ze[nt][e] + zo[nt][e];
+        const double zz = zf[nt][e];
         pv[e] = nul * rm_pow(zz, dm1);
         wacc[nt][e] = fma(pv[e], zz, wacc[nt][e]);
       }
@@ -230,7 +305,7 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
     if constexpr (TAIL > 0) {
 #pragma unroll
       for (int c = 0; c < TAIL; ++c) {
-        double zz = zte[c] + zto[c];
+        double zz = ztf[c];
         zz += __shfl_xor_sync(0xffffffffu, zz, 1);   // lane t summed i == t (mod 4)
         zz += __shfl_xor_sync(0xffffffffu, zz, 2);
         if (t == c) {
@@ -254,21 +329,20 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
       const double* vr = sv + (4 * k2 + t) * ldv + 8 * mbase + g;
 #pragma unroll
       for (int m = 0; m < MTH; ++m) {
-        if (m < MTH - 1 || mcnt == MTH) {
-          double a = vr[8 * m];
-          if (m == MTH - 1) a = (8 * (mbase + m) + g < prm.n) ? a : 0.0;  // rows past n
+        // every warp runs MTH m-tiles; rows past n (incl. warp 1's spare tile) read as zero
+        double a = vr[8 * m];
+        if (m >= MTH - 2) a = (8 * (mbase + m) + g < prm.n) ? a : 0.0;
 #pragma unroll
-          for (int nt = 0; nt < NTM; ++nt) dmma884(yacc[m][nt], a, b[nt]);
+        for (int nt = 0; nt < NTM; ++nt) dmma884(yacc[m][nt], a, b[nt]);
 #pragma unroll
-          for (int c = 0; c < TAIL; ++c) ytl[m][c] = fma(a, bt[c], ytl[m][c]);
-        }
+        for (int c = 0; c < TAIL; ++c) ytl[m][c] = fma(a, bt[c], ytl[m][c]);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive(&empty[s_cur]);
   }
 
-  // ---------------- fixed-order combine of the 16 warps' partials ----------------
+  // ---------------- fixed-order combine of the math warps' partials ----------------
 #pragma unroll
   for (int m = 0; m < MTH; ++m)
 #pragma unroll
@@ -290,7 +364,7 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   wtl += __shfl_xor_sync(0xffffffffu, wtl, 8);
   wtl += __shfl_xor_sync(0xffffffffu, wtl, 16);
   const int MT = prm.MT;
-  // all slabs consumed by every math warp -> the ring is free: [NP][MT*8][CW] + [2NP][CW]
+  // every math warp has consumed all of its slabs -> the ring is free for staging
   asm volatile("bar.sync 15, %0;\n" ::"n"(2 * NP * 32) : "memory");
   double* stage = ring + (size_t)q * MT * 8 * CW;
 #pragma unroll

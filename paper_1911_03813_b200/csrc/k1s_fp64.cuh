@@ -201,26 +201,34 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   for (int nt = 0; nt < NTM; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
   const int dm1 = prm.d - 1;
   const int lr = 8 * h + g;
+  (void)dm1;
   double* Pb = sP + (size_t)q * K1S_SR * PP;
   double* xo = sX + ((size_t)q * 2 + h) * 128 + lane * 4;       // my partial for rows of 1-h
   const double* xi = sX + ((size_t)q * 2 + (1 - h)) * 128 + lane * 4;  // partner's, rows of h
 
-  // incremental slab -> (unit j, slab-in-unit sub, stage s, parity) walk (no 64-bit division)
+  // Slab walk without divisions: k advances by NP, so the unit index advances by
+  // (sub + NP) / spc and sub becomes (sub + NP) % spc -- both functions of sub < spc <= 14 only.
   int64_t j = q / spc;
   int sub = q % spc;
   int s = (int)(j % S);
   uint32_t ph = (uint32_t)((j / S) & 1);
+  const int dj_lo = NP / spc, sub_step = NP % spc;   // (sub + NP) = dj_lo*spc + sub_step + sub
   for (int64_t k = q; k < my_slabs; k += NP) {
     mbar_wait(&full[s], ph);
     const double* sv = ring + ((size_t)s * spc + sub) * K1S_SR * ldv;
     const int64_t row0 = ((pg + j * prm.gp) * spc + sub) * K1S_SR;
     const int s_cur = s;
-    sub += NP;
-    while (sub >= spc) {
-      sub -= spc;
-      ++j;
-      if (++s == S) {
-        s = 0;
+    {
+      int nsub = sub + sub_step, dj = dj_lo;
+      if (nsub >= spc) {
+        nsub -= spc;
+        ++dj;
+      }
+      sub = nsub;
+      j += dj;
+      s += dj;
+      if (s >= S) {
+        s -= S;
         ph ^= 1;
       }
     }
@@ -291,16 +299,12 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
     }
     // ---- epilogue on rows 8h..8h+7: P = nu z^(d-1), w += P z ----
     const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
+    constexpr int NV = 2 * NTM + TL;   // this lane's z values: DMMA columns, then its tail column
+    double zv[NV], pw[NV];
 #pragma unroll
     for (int nt = 0; nt < NTM; ++nt) {
-      double pv[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double zz = zf[nt][e];
-        pv[e] = nul * rm_pow(zz, dm1);
-        wacc[nt][e] = fma(pv[e], zz, wacc[nt][e]);
-      }
-      *reinterpret_cast<double2*>(&Pb[lr * PP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
+      zv[2 * nt] = zf[nt][0];
+      zv[2 * nt + 1] = zf[nt][1];
     }
     if constexpr (TAIL > 0) {
 #pragma unroll
@@ -308,11 +312,28 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
         double zz = ztf[c];
         zz += __shfl_xor_sync(0xffffffffu, zz, 1);   // lane t summed i == t (mod 4)
         zz += __shfl_xor_sync(0xffffffffu, zz, 2);
-        if (t == c) {
-          const double pv = nul * rm_pow(zz, dm1);
-          wtl = fma(pv, zz, wtl);
-          Pb[lr * PP + 8 * NTM + c] = pv;
-        }
+        if (t == c) zv[2 * NTM] = zz;                // lane t == c owns tail column c
+      }
+      if (t >= TAIL) zv[2 * NTM] = 0.0;
+    } else {
+      zv[2 * NTM] = 0.0;
+    }
+    rm_pow_vec<NV>(zv, pw, dm1);
+#pragma unroll
+    for (int nt = 0; nt < NTM; ++nt) {
+      double pv[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        pv[e] = nul * pw[2 * nt + e];
+        wacc[nt][e] = fma(pv[e], zv[2 * nt + e], wacc[nt][e]);
+      }
+      *reinterpret_cast<double2*>(&Pb[lr * PP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
+    }
+    if constexpr (TAIL > 0) {
+      if (t < TAIL) {
+        const double pv = nul * pw[2 * NTM];
+        wtl = fma(pv, zv[2 * NTM], wtl);
+        Pb[lr * PP + 8 * NTM + t] = pv;
       }
     }
     asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");

@@ -39,6 +39,36 @@ __device__ __forceinline__ double rm_pow(double x, int k) {
   return acc;
 }
 
+// rm_pow over N values with one (warp-uniform) branch on k instead of one loop per value.
+template <int N>
+__device__ __forceinline__ void rm_pow_vec(const double (&x)[N], double (&y)[N], int k) {
+  switch (k) {
+    case 1:
+#pragma unroll
+      for (int i = 0; i < N; ++i) y[i] = x[i];
+      break;
+    case 2:
+#pragma unroll
+      for (int i = 0; i < N; ++i) y[i] = x[i] * x[i];
+      break;
+    case 3:
+#pragma unroll
+      for (int i = 0; i < N; ++i) y[i] = (x[i] * x[i]) * x[i];
+      break;
+    case 4:
+#pragma unroll
+      for (int i = 0; i < N; ++i) y[i] = ((x[i] * x[i]) * x[i]) * x[i];
+      break;
+    case 5:
+#pragma unroll
+      for (int i = 0; i < N; ++i) y[i] = (((x[i] * x[i]) * x[i]) * x[i]) * x[i];
+      break;
+    default:
+#pragma unroll
+      for (int i = 0; i < N; ++i) y[i] = rm_pow(x[i], k);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ double to_f64(T v) {
   return static_cast<double>(v);

@@ -21,6 +21,10 @@
 #include "k5_gram.cuh"
 #include "k_aux.cuh"
 #include "k1_dispatch.h"
+#include "k1t_tf32.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 using namespace mcp;
 
@@ -94,6 +98,16 @@ struct mcp_ctx {
   size_t hx_bytes = 0;
   void* hout = nullptr;
   size_t hout_bytes = 0;
+
+  // fast mode (tcgen05 TF32): fp32 copy of V when the set is fp64, tensor maps, prepared A^T
+  float* dV32 = nullptr;       // == dV when dtype is fp32
+  bool own_v32 = false;
+  int64_t ldv32 = 0;
+  bool tm_v_ready = false;
+  CUtensorMap tm_v1, tm_v2, tm_a;
+  void* tm_a_addr = nullptr;
+  int tm_a_rows = 0, tm_a_kpad = 0, tm_a_rb = 0;
+  DevBuf dAt;
 
   std::map<std::tuple<int, int, int>, GraphEntry> graphs;
   bool timing = false;
@@ -179,20 +193,150 @@ inline int grid_for(int64_t total, int threads, int cap) {
   return (int)b;
 }
 
+// Shape of the fast-mode (K1T) launch.
+struct K1TPlan {
+  int RB = 0, rbs = 0, gp = 0, stages = 0, nkb = 0, mt2 = 0, r_pad = 0, kpad = 0;
+  int64_t num_tiles = 0;
+  size_t smem = 0;
+};
+
 // Shape of one evaluation's K1 launch.
 struct EvalPlan {
   K1Variant k1;
+  K1TPlan t;
+  int mode = MCP_MODE_FP64;
   int d = 0, r = 0;
 };
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      (void)cudaGetLastError();
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner dim (contiguous) x outer dim, row pitch in bytes.
+bool make_tmap_f32(CUtensorMap* m, void* gaddr, uint64_t inner, uint64_t outer, uint64_t pitch,
+                   uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, gaddr, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
+  K1TPlan& t = pl.t;
+  const int64_t n = c->n;
+  t.nkb = (int)ceil_div(n, 32);
+  t.mt2 = (int)ceil_div(n, 128);
+  int RB = 16;  // 16, 32 or 64 columns per CTA block
+  while (RB < r && RB < 64) RB *= 2;
+  while (RB > 16 && (1 + t.mt2) * RB > 512) RB /= 2;
+  if ((1 + t.mt2) * RB > 512)
+    return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
+  t.RB = RB;
+  t.rbs = (int)ceil_div(r, RB);
+  t.r_pad = t.rbs * RB;
+  t.kpad = t.nkb * 32;
+  const size_t budget = 227 * 1024;
+  int ns = (int)((budget - k1t_smem_bytes(RB, 0)) / k1t_stage_bytes(RB));
+  if (ns > 8) ns = 8;
+  if (ns < 2) return c->fail(MCP_ERR_ARG, "tf32x3 stage ring does not fit");
+  t.stages = ns;
+  t.smem = k1t_smem_bytes(RB, ns);
+  t.num_tiles = c->p_pad / K1T_TP;
+  int64_t G = c->sms;
+  if (G < t.rbs) G = t.rbs;
+  G -= G % t.rbs;
+  int64_t gp = G / t.rbs;
+  if (gp > t.num_tiles) gp = t.num_tiles;
+  t.gp = (int)std::max<int64_t>(gp, 1);
+  // fp32 copy of V (fp64 sets), tensor maps over it
+  if (!c->dV32) {
+    if (c->dtype == MCP_F32) {
+      c->dV32 = (float*)c->dV;
+      c->ldv32 = c->ldv;
+      c->own_v32 = false;
+    } else {
+      c->ldv32 = round_up(n, 4);
+      CUDA_TRY(c, cudaMalloc(&c->dV32, sizeof(float) * (size_t)c->p_pad * c->ldv32));
+      c->own_v32 = true;
+      k_f64_to_f32<<<grid_for(c->p_pad * c->ldv32, 256, 16 * c->sms), 256, 0, c->stream>>>(
+          (const double*)c->dV, c->dV32, c->p_pad, c->ldv, c->ldv32, n);
+      CUDA_TRY(c, cudaGetLastError());
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+    c->tm_v_ready = false;
+  }
+  if (!c->tm_v_ready) {
+    if (!make_tmap_f32(&c->tm_v1, c->dV32, c->ldv32, c->p_pad, 4 * c->ldv32, 32, 128,
+                       CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_f32(&c->tm_v2, c->dV32, c->ldv32, c->p_pad, 4 * c->ldv32, 32, 32,
+                       CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for V");
+    c->tm_v_ready = true;
+  }
+  int rc;
+  if ((rc = ensure(c, c->dAt, sizeof(float) * 2 * (size_t)t.r_pad * t.kpad))) return rc;
+  if (c->tm_a_addr != c->dAt.p || c->tm_a_rows != 2 * t.r_pad || c->tm_a_kpad != t.kpad ||
+      c->tm_a_rb != RB) {
+    if (!make_tmap_f32(&c->tm_a, c->dAt.p, t.kpad, 2 * t.r_pad, 4 * (uint64_t)t.kpad, 32, RB,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+      return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for A");
+    c->tm_a_addr = c->dAt.p;
+    c->tm_a_rows = 2 * t.r_pad;
+    c->tm_a_kpad = t.kpad;
+    c->tm_a_rb = RB;
+  }
+  CUDA_TRY(c, cudaFuncSetAttribute(k1t_fg_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)t.smem));
+  pl.k1 = K1Variant();
+  pl.k1.kind = 2;
+  pl.k1.RB = RB;
+  pl.k1.rbs = t.rbs;
+  pl.k1.gp = t.gp;
+  pl.k1.n_pad = t.mt2 * 128;
+  pl.k1.ypart_elems = (size_t)t.rbs * t.gp * t.mt2 * 128 * RB;
+  pl.k1.wpart_elems = 0;
+  pl.k1.afrag_elems = 0;
+  pl.k1.name = "k1t_fg_tf32<3xTF32,RB=" + std::to_string(RB) + ",S=" + std::to_string(ns) + ">";
+  return MCP_OK;
+}
 
 int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
   if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
   if (r < 1) return c->fail(MCP_ERR_ARG, "rank must be >= 1, got " + std::to_string(r));
-  if (mode != MCP_MODE_FP64)
-    return c->fail(MCP_ERR_ARG, "mode " + std::to_string(mode) + " is not available in this build");
+  if (mode != MCP_MODE_FP64 && mode != MCP_MODE_TF32X3)
+    return c->fail(MCP_ERR_ARG, "unknown mode " + std::to_string(mode));
   pl.d = d;
   pl.r = r;
+  pl.mode = mode;
+  if (mode == MCP_MODE_TF32X3) {
+    int rc = plan_tf32(c, r, pl);
+    if (rc) return rc;
+    const int64_t n = c->n;
+    if ((rc = ensure(c, c->dx, sizeof(double) * (r + n * r + 1)))) return rc;
+    if ((rc = ensure(c, c->dout, sizeof(double) * (1 + r + n * r)))) return rc;
+    if ((rc = ensure(c, c->dYw, sizeof(double) * (n * r + r)))) return rc;
+    if ((rc = ensure(c, c->dYpart, sizeof(double) * pl.k1.ypart_elems))) return rc;
+    if ((rc = ensure(c, c->dG, sizeof(double) * (size_t)r * r))) return rc;
+    if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
+    return MCP_OK;
+  }
   std::string why;
   if (!k1_select(c->dtype, c->n, r, c->p_pad, c->sms, pl.k1, why))
     return c->fail(MCP_ERR_ARG, why);
@@ -209,9 +353,45 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   return MCP_OK;
 }
 
+// fast mode: prep A^T hi/lo -> K1T -> K3 (Y) -> w from Y
+int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
+                         cudaStream_t s) {
+  const K1TPlan& t = pl.t;
+  const int n = (int)c->n, r = pl.r;
+  k_prep_at_tf32<<<grid_for((int64_t)t.r_pad * t.kpad, 256, 4 * c->sms), 256, 0, s>>>(
+      dx + r, n, r, t.r_pad, t.kpad, (float*)c->dAt.p);
+  K1TParams prm;
+  prm.n = n;
+  prm.r = r;
+  prm.d = pl.d;
+  prm.nkb = t.nkb;
+  prm.mt2 = t.mt2;
+  prm.RB = t.RB;
+  prm.rbs = t.rbs;
+  prm.gp = t.gp;
+  prm.r_pad = t.r_pad;
+  prm.stages = t.stages;
+  prm.num_tiles = t.num_tiles;
+  prm.nu = c->dnu;
+  prm.nu_const = c->nu_const;
+  prm.Ypart = (double*)c->dYpart.p;
+  auto* ev = timing_begin(c, s);
+  k1t_fg_tf32<<<t.gp * t.rbs, K1T_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_a, prm);
+  timing_end(ev, s);
+  const int64_t red_blocks = (int64_t)t.rbs * ceil_div((int64_t)n * t.RB, K3_X);
+  k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
+      (const double*)c->dYpart.p, nullptr, n, r, t.mt2 * 128, t.RB, t.rbs, t.gp, dYw);
+  k_w_from_y<<<(int)ceil_div((int64_t)r * 32, 256), 256, 0, s>>>(dx + r, n, r, dYw);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches = 4;
+  c->variant = pl.k1.name;
+  return MCP_OK;
+}
+
 // prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows.
 int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
                     cudaStream_t s) {
+  if (pl.mode == MCP_MODE_TF32X3) return enqueue_partial_tf32(c, pl, dx, dYw, s);
   const K1Variant& v = pl.k1;
   const int n = (int)c->n, r = pl.r;
   int launches = 2;
@@ -296,7 +476,7 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     CUDA_TRY(c, cudaGraphInstantiate(&ge.exec, ge.graph, 0));
     it = c->graphs.emplace(key, ge).first;
   } else {
-    c->last_launches = (pl.k1.needs_prep() ? 3 : 2) +
+    c->last_launches = (pl.mode == MCP_MODE_TF32X3 ? 4 : (pl.k1.needs_prep() ? 3 : 2)) +
                        (((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) ? 1 : 3);
     c->variant = pl.k1.name;
   }
@@ -309,8 +489,8 @@ template <typename T>
 int upload_obs(mcp_ctx* c, const T* V, bool on_device, int layout, int64_t n, int64_t p,
                int64_t ld) {
   const int64_t ldv = obs_pitch(sizeof(T) == 8 ? MCP_F64 : MCP_F32, n);
-  // rows padded to a multiple of 448 = lcm(K1 tile 64, K1S copy unit 14 x 16) with zeros
-  const int64_t p_pad = round_up(p, (int64_t)448);
+  // rows padded with zeros to a multiple of 3584 = lcm(K1 tile 64, K1S copy unit 14 x 16, K1T 128)
+  const int64_t p_pad = round_up(p, (int64_t)3584);  // also a multiple of the K1T 128-row tile
   const size_t bytes = sizeof(T) * (size_t)p_pad * ldv;
   if (c->dV) cudaFree(c->dV);
   c->dV = nullptr;
@@ -398,6 +578,10 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   if (ld < minld) return c->fail(MCP_ERR_ARG, "leading dimension too small");
   c->loaded = false;
   drop_graphs(c);
+  if (c->own_v32 && c->dV32) cudaFree(c->dV32);
+  c->dV32 = nullptr;
+  c->own_v32 = false;
+  c->tm_v_ready = false;
   int rc = dtype == MCP_F64
                ? upload_obs<double>(c, (const double*)V, on_device, layout, n, p, ld)
                : upload_obs<float>(c, (const float*)V, on_device, layout, n, p, ld);
@@ -475,6 +659,8 @@ int mcp_destroy(mcp_ctx* c) {
                       &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
+    if (c->own_v32 && c->dV32) cudaFree(c->dV32);
+    if (c->dAt.p) cudaFree(c->dAt.p);
     if (c->dV) cudaFree(c->dV);
     if (c->dnu) cudaFree(c->dnu);
     if (c->hx) cudaFreeHost(c->hx);
@@ -566,8 +752,10 @@ int mcp_ttsv_batch(mcp_ctx* c, int d, int r, const double* A, int mode, double* 
 static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, double* out) {
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
   if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
-  if (mode != MCP_MODE_FP64)
-    return c->fail(MCP_ERR_ARG, "mode " + std::to_string(mode) + " is not available in this build");
+  // ||X||^2 is a one-time constant: both modes run the FP64 DMMA kernel (exact superset of the
+  // fast mode's stated 1e-4 tolerance).
+  if (mode != MCP_MODE_FP64 && mode != MCP_MODE_TF32X3)
+    return c->fail(MCP_ERR_ARG, "unknown mode " + std::to_string(mode));
   if (nparts < 1 || part < 0 || part >= nparts) return c->fail(MCP_ERR_ARG, "bad part/nparts");
   if (!out) return c->fail(MCP_ERR_ARG, "NULL argument");
   const int64_t T = c->p_pad / K5_T;

@@ -1,0 +1,335 @@
+// K1T (fast mode, mode = "tf32x3"): fused f+grad partial on the 5th-gen tensor cores.
+//
+// Same algebra as K1 (reference pkg/src/momentcp/implicit.py:94-107) on 128-observation tiles:
+//   GEMM1  Z[128 x RB] = V_tile[128 x n] A[n x RB]          tcgen05.mma kind::tf32, D in TMEM
+//   epi    P = nu * Z^(d-1)  (fp64 arithmetic, stored as TF32 hi/lo bricks in shared memory)
+//   GEMM2  Y[n x RB] += V_tile^T P                           tcgen05.mma kind::tf32, D in TMEM
+// Every product is the 3xTF32 split  x*y ~= xh*yh + xh*yl + xl*yh  (xh = top 10 mantissa bits,
+// xl = x - xh), so the result carries ~1e-7 relative error instead of TF32's 1e-3 (SURVEY.md
+// Appendix B); Z and P never reach HBM.  Y accumulates in fp32 TMEM for K1T_FLUSH tiles and is
+// then flushed into an fp64 per-CTA partial (fixed order, deterministic); w = a_j^T y_j is formed
+// from the reduced Y in fp64 by the tail (implicit.py:139).
+//
+// Roles (one CTA per SM, 10 warps): warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one
+// lane; also owns TMEM alloc), warps 2..9 = split / epilogue / flush.  V is read twice per tile
+// through two tensor maps over the same fp32 rows: pass 1 with SWIZZLE_128B (K-major operand of
+// GEMM1), pass 2 with SWIZZLE_128B_ATOM_32B (the MN-major operand GEMM2 needs -- the only layout
+// tcgen05 accepts for MN-major TF32).  Stage ring: full (TMA) -> split (hi/lo by CUDA cores) ->
+// empty (MMA commit).
+#pragma once
+
+#include <cuda.h>
+
+#include "k1s_fp64.cuh"  // mbarrier helpers
+#include "mcp_common.cuh"
+#include "umma.cuh"
+
+namespace mcp {
+
+constexpr int K1T_TP = 128;
+constexpr int K1T_MATH_WARPS = 8;
+constexpr int K1T_THREADS = (2 + K1T_MATH_WARPS) * 32;
+constexpr int K1T_VBYTES = 16384;  // V region of one stage (128 rows x 32 or 4 x 32 rows x 32)
+constexpr int K1T_FLUSH = 8;       // tiles accumulated in fp32 TMEM between fp64 flushes
+
+struct K1TParams {
+  int n, r, d;
+  int nkb;            // GEMM1 k-blocks of 32 variables
+  int mt2;            // GEMM2 m-tiles of 128 variables
+  int RB;             // factor columns per CTA (16, 32 or 64)
+  int rbs, gp;
+  int r_pad;          // rows of the hi half of the prepared A^T (lo half starts there)
+  int stages;
+  int64_t num_tiles;  // p_pad / 128
+  const double* nu;
+  double nu_const;
+  double* Ypart;      // [rbs][gp][mt2*128][RB] fp64
+};
+
+__host__ __device__ constexpr size_t k1t_stage_bytes(int RB) { return 2 * K1T_VBYTES + 256 * RB; }
+__host__ __device__ constexpr size_t k1t_smem_bytes(int RB, int stages) {
+  return 1024 /*align slack*/ + stages * k1t_stage_bytes(RB) + 1024 * (size_t)RB /*P hi+lo*/ +
+         1024 /*barriers*/;
+}
+
+__global__ void __launch_bounds__(K1T_THREADS, 1)
+    k1t_fg_tf32(const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_v2,
+                const __grid_constant__ CUtensorMap tm_a, K1TParams prm) {
+  extern __shared__ unsigned char smem_raw_t[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw_t) + 1023) & ~uintptr_t(1023));
+  const int RB = prm.RB, NS = prm.stages;
+  const size_t SB = k1t_stage_bytes(RB);
+  unsigned char* sPh = base + NS * SB;                 // 4 bricks x RB rows x 128 B
+  unsigned char* sPl = sPh + 512 * RB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sPl + 512 * RB);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NS;
+  uint64_t* split = bars + 2 * NS;
+  uint64_t* z_full = bars + 3 * NS;
+  uint64_t* p_full = z_full + 1;
+  uint64_t* p_empty = z_full + 2;
+  uint64_t* y_full = z_full + 3;
+  uint64_t* y_empty = z_full + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(z_full + 5);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = blockIdx.x % prm.rbs;
+  const int pg = blockIdx.x / prm.rbs;
+  const int64_t my_tiles =
+      pg < prm.num_tiles ? (prm.num_tiles - pg + prm.gp - 1) / prm.gp : 0;
+  const int mt2 = prm.mt2, nkb = prm.nkb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&split[s], K1T_MATH_WARPS);
+    }
+    mbar_init(z_full, 1);
+    mbar_init(p_full, K1T_MATH_WARPS);
+    mbar_init(p_empty, 1);
+    mbar_init(y_full, 1);
+    mbar_init(y_empty, K1T_MATH_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc<512>(smem_u32(tslot));
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_v1);
+    tma_prefetch_desc(&tm_v2);
+    tma_prefetch_desc(&tm_a);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tz = tmem;            // Z: columns [0, RB)
+  const uint32_t ty = tmem + RB;       // Y[mt]: columns RB * (1 + mt)
+
+  if (warp == 0) {
+    // =========================== TMA producer ===========================
+    if (lane == 0) {
+      int64_t q = 0;
+      for (int64_t u = 0; u < my_tiles; ++u) {
+        const int row0 = (int)((pg + u * prm.gp) * K1T_TP);
+        for (int step = 0; step < nkb + 4 * mt2; ++step, ++q) {
+          const int s = (int)(q % NS);
+          if (q >= NS) mbar_wait(&empty[s], (uint32_t)((q / NS) - 1) & 1);
+          unsigned char* st = base + s * SB;
+          if (step < nkb) {
+            mbar_arrive_expect_tx(&full[s], K1T_VBYTES + 256 * RB);
+            tma_load_2d(st, &tm_v1, step * 32, row0, smem_u32(&full[s]));
+            tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, step * 32, rb * RB, smem_u32(&full[s]));
+            tma_load_2d(st + 2 * K1T_VBYTES + 128 * RB, &tm_a, step * 32, prm.r_pad + rb * RB,
+                        smem_u32(&full[s]));
+          } else {
+            const int mt = (step - nkb) >> 2, rc = (step - nkb) & 3;
+            mbar_arrive_expect_tx(&full[s], K1T_VBYTES);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              tma_load_2d(st + b * 4096, &tm_v2, mt * 128 + b * 32, row0 + rc * 32,
+                          smem_u32(&full[s]));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // =========================== MMA issuer ===========================
+    if (lane == 0) {
+      const uint32_t id1 = umma_idesc_tf32(128, RB, false, false);
+      const uint32_t id2 = umma_idesc_tf32(128, RB, true, false);
+      int64_t q = 0;
+      int flushes = 0;
+      bool fresh = true, wait_y = false;
+      for (int64_t u = 0; u < my_tiles; ++u) {
+        // ---- GEMM1: Z = V A (3xTF32) ----
+        for (int kb = 0; kb < nkb; ++kb, ++q) {
+          const int s = (int)(q % NS);
+          mbar_wait(&split[s], (uint32_t)(q / NS) & 1);
+          tc_fence_after();
+          unsigned char* st = base + s * SB;
+          const uint32_t v_hi = smem_u32(st), v_lo = v_hi + K1T_VBYTES;
+          const uint32_t a_hi = v_hi + 2 * K1T_VBYTES, a_lo = a_hi + 128 * RB;
+#pragma unroll
+          for (int pr = 0; pr < 3; ++pr) {
+            const uint32_t av = pr == 2 ? v_lo : v_hi, bv = pr == 1 ? a_lo : a_hi;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              umma_tf32(tz, umma_desc_sw128(av + ks * 32, 16, 1024),
+                        umma_desc_sw128(bv + ks * 32, 16, 1024), id1,
+                        (kb | pr | ks) != 0 ? 1u : 0u);
+          }
+          umma_commit(smem_u32(&empty[s]));
+        }
+        umma_commit(smem_u32(z_full));
+        // ---- GEMM2: Y += V^T P (3xTF32), P from the epilogue ----
+        mbar_wait(p_full, (uint32_t)u & 1);
+        if (wait_y) {
+          mbar_wait(y_empty, (uint32_t)(flushes - 1) & 1);
+          wait_y = false;
+          fresh = true;
+        }
+        tc_fence_after();
+        const uint32_t p_hi = smem_u32(sPh), p_lo = smem_u32(sPl);
+        for (int step = 0; step < 4 * mt2; ++step, ++q) {
+          const int mt = step >> 2, rc = step & 3;
+          const int s = (int)(q % NS);
+          mbar_wait(&split[s], (uint32_t)(q / NS) & 1);
+          tc_fence_after();
+          const uint32_t v_hi = smem_u32(base + s * SB), v_lo = v_hi + K1T_VBYTES;
+#pragma unroll
+          for (int pr = 0; pr < 3; ++pr) {
+            const uint32_t av = pr == 2 ? v_lo : v_hi;
+            const uint32_t bv = (pr == 1 ? p_lo : p_hi) + rc * 128 * RB;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              umma_tf32(ty + mt * RB, umma_desc_sw128_32b(av + ks * 1024, 4096, 512),
+                        umma_desc_sw128(bv + ks * 32, 16, 1024), id2,
+                        (fresh && rc == 0 && pr == 0 && ks == 0) ? 0u : 1u);
+          }
+          umma_commit(smem_u32(&empty[s]));
+        }
+        fresh = false;
+        umma_commit(smem_u32(p_empty));
+        if ((u % K1T_FLUSH) == K1T_FLUSH - 1 || u == my_tiles - 1) {
+          umma_commit(smem_u32(y_full));
+          ++flushes;
+          wait_y = true;
+        }
+      }
+    }
+  } else {
+    // =========================== split / epilogue / flush warps ===========================
+    const int mw = warp - 2;                 // 0..7
+    const int sp = warp & 3;                 // TMEM sub-partition this warp may access
+    const int half = mw >> 2;                // column half for the epilogue / flush
+    const int mtid = mw * 32 + lane;         // 0..255
+    const int l = 32 * sp + lane;            // tile row (TMEM lane) this thread owns
+    // columns per warp for the epilogue / flush: halves of RB, at least one 16-column load
+    const int hc = RB >= 32 ? RB / 2 : 16;
+    const bool col_active = half * hc < RB;
+    const int dm1 = prm.d - 1;
+    int64_t q = 0;
+    int flushes = 0;
+    double* Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * (size_t)mt2 * 128 * RB;
+
+    auto split_stage = [&](int64_t qq) {
+      const int s = (int)(qq % NS);
+      mbar_wait(&full[s], (uint32_t)(qq / NS) & 1);
+      float4* vh = reinterpret_cast<float4*>(base + s * SB);
+      float4* vl = reinterpret_cast<float4*>(base + s * SB + K1T_VBYTES);
+#pragma unroll
+      for (int k = 0; k < K1T_VBYTES / 16 / 256; ++k) {
+        const int e = mtid + 256 * k;
+        float4 x = vh[e];
+        float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+        vl[e] = make_float4(x.x - hi.x, x.y - hi.y, x.z - hi.z, x.w - hi.w);
+        vh[e] = hi;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&split[s]);
+    };
+
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      const int64_t row0 = (pg + u * prm.gp) * K1T_TP;
+      for (int kb = 0; kb < nkb; ++kb, ++q) split_stage(q);
+
+      // ---- epilogue: P = nu z^(d-1) -> TF32 hi/lo bricks (K-major B operand of GEMM2) ----
+      mbar_wait(z_full, (uint32_t)u & 1);
+      if (u > 0) mbar_wait(p_empty, (uint32_t)(u - 1) & 1);
+      tc_fence_after();
+      {
+        const double nul = prm.nu ? prm.nu[row0 + l] : prm.nu_const;
+        const int brick = l >> 5, col = l & 31;
+        for (int c0 = half * hc; col_active && c0 < (half + 1) * hc; c0 += 16) {
+          float zv[16];
+          tmem_ld16(tz + ((uint32_t)(32 * sp) << 16) + c0, zv);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const double z = (double)zv[jj];
+            const float pf = (float)(nul * rm_pow(z, dm1));
+            const float ph = tf32_hi(pf);
+            const uint32_t off = brick * 128 * RB + brick_off(c0 + jj, col);
+            *reinterpret_cast<float*>(sPh + off) = ph;
+            *reinterpret_cast<float*>(sPl + off) = pf - ph;
+          }
+        }
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+
+      for (int step = 0; step < 4 * mt2; ++step, ++q) split_stage(q);
+
+      // ---- flush: fp32 TMEM Y -> fp64 per-CTA partial (fixed order) ----
+      if ((u % K1T_FLUSH) == K1T_FLUSH - 1 || u == my_tiles - 1) {
+        mbar_wait(y_full, (uint32_t)flushes & 1);
+        tc_fence_after();
+        for (int mt = 0; mt < mt2; ++mt) {
+          double* yrow = Yp + ((size_t)mt * 128 + l) * RB;
+          for (int c0 = half * hc; col_active && c0 < (half + 1) * hc; c0 += 16) {
+            float yv[16];
+            tmem_ld16(ty + mt * RB + ((uint32_t)(32 * sp) << 16) + c0, yv);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              yrow[c0 + jj] = (flushes == 0 ? 0.0 : yrow[c0 + jj]) + (double)yv[jj];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(y_empty);
+        ++flushes;
+      }
+    }
+    // CTAs without tiles still own a (zero) partial
+    if (my_tiles == 0)
+      for (int mt = 0; mt < mt2; ++mt)
+        for (int c = half * hc; col_active && c < (half + 1) * hc; ++c)
+          Yp[((size_t)mt * 128 + l) * RB + c] = 0.0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// Prepared factor operand for K1T: At[h][j][i] (h = 0 hi, 1 lo), fp32, zero padded to
+// r_pad rows and kpad = nkb*32 columns; the TF32 split of the fp32 rounding of A (fp64).
+__global__ void k_prep_at_tf32(const double* __restrict__ A, int n, int r, int r_pad, int kpad,
+                               float* __restrict__ At) {
+  const int64_t total = (int64_t)r_pad * kpad;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int j = idx / kpad, i = idx % kpad;
+    const float a = (i < n && j < r) ? (float)A[(int64_t)j * n + i] : 0.0f;
+    const float hi = tf32_hi(a);
+    At[idx] = hi;
+    At[total + idx] = a - hi;
+  }
+}
+
+// Fast mode: w_j = a_j^T y_j from the reduced Y (implicit.py:139), fp64.
+__global__ void k_w_from_y(const double* __restrict__ A, int n, int r, double* __restrict__ Yw) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= r) return;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += A[(int64_t)warp * n + i] * Yw[(int64_t)warp * n + i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) Yw[(int64_t)n * r + warp] = s;
+}
+
+// fp64 -> fp32 observation copy (fast mode on float64 data)
+__global__ void k_f64_to_f32(const double* __restrict__ src, float* __restrict__ dst, int64_t rows,
+                             int64_t ld_src, int64_t ld_dst, int64_t cols) {
+  const int64_t total = rows * ld_dst;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = idx / ld_dst, c = idx % ld_dst;
+    dst[idx] = c < cols ? (float)src[rr * ld_src + c] : 0.0f;
+  }
+}
+
+}  // namespace mcp

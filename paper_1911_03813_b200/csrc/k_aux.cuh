@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(K3_X * K3_Y)
   const int tx = threadIdx.x % K3_X, ty = threadIdx.x / K3_X;
   const int per_rb = n * RB;                          // Y outputs of one column block
   const int yblocks = (per_rb + K3_X - 1) / K3_X;     // blocks per column block
-  const int64_t total_blocks = (int64_t)rbs * yblocks + (rbs * RB + K3_X - 1) / K3_X;
+  const int64_t total_blocks =
+      (int64_t)rbs * yblocks + (wpart ? (rbs * RB + K3_X - 1) / K3_X : 0);
   for (int64_t blk = blockIdx.x; blk < total_blocks; blk += gridDim.x) {
     double s = 0.0;
     int64_t dst = -1;

@@ -256,3 +256,57 @@ def test_device_errors_are_value_errors():
         ctx.fg_packed(np.ones(3), 2, 1, 1, 0.0, None)   # d < 2 checked in the library too
     with pytest.raises(ValueError):
         mcp.fg_implicit(obs, np.ones(1), np.ones((2, 1)), 3, mode="bogus")
+
+
+# ----------------------------- fast mode (tcgen05 3xTF32) -----------------------------
+FAST_TOL = 1e-4   # the stated bound of the fast mode (BASELINE north_star)
+
+
+def _fast_errs(res, f, gl, gA, scales):
+    f_s, gl_s, gA_s = scales
+    term = max(_err(res.f, f, f_s), _err(res.g_lam, gl, gl_s), _err(res.g_A, gA, gA_s))
+    norm = max(abs(res.f - f) / max(abs(f), 1e-300),
+               float(np.linalg.norm(res.g_lam - gl) / max(np.linalg.norm(gl), 1e-300)),
+               float(np.linalg.norm(res.g_A - gA) / max(np.linalg.norm(gA), 1e-300)))
+    return term, norm
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_fast_mode_configs(golden, name):
+    g = golden["configs"]
+    cfg, V, lam, A = instances.config_instance(name)
+    key = name + "_"
+    obs = mcp.ObservationSet(V)
+    res = mcp.fg_implicit(obs, lam, A, cfg.d, 0.0, mode="tf32x3")
+    term, norm = _fast_errs(res, float(g[key + "f"]), g[key + "g_lam"], g[key + "g_A"],
+                            (g[key + "f_scale"], g[key + "gl_scale"], g[key + "gA_scale"]))
+    print(f"{name} tf32x3 via {obs.device_context().last_variant}: term-scale {term:.2e}, "
+          f"normwise {norm:.2e}")
+    assert term <= FAST_TOL and norm <= FAST_TOL
+
+
+def test_fast_mode_ext_sweep(golden):
+    g = golden["sweep"]
+    worst = 0.0
+    for k in range(instances.EXT_COUNT):
+        V, nu, lam, A, d, alpha = instances.ext_instance(k)
+        key = f"e{k}_"
+        res = mcp.fg_implicit(mcp.ObservationSet(V, nu), lam, A, d, alpha, mode="tf32x3")
+        e = max(_err(res.f, g[key + "f"], g[key + "f_scale"]),
+                _err(res.g_lam, g[key + "g_lam"], g[key + "gl_scale"]),
+                _err(res.g_A, g[key + "g_A"], g[key + "gA_scale"]))
+        assert e <= FAST_TOL, (key, e)
+        worst = max(worst, e)
+    print(f"fast-mode ext sweep: worst term-scale {worst:.2e}")
+
+
+def test_fast_mode_zero_weights_and_determinism():
+    rng = np.random.default_rng(31)
+    obs = mcp.ObservationSet(rng.standard_normal((200, 5000)).astype(np.float32))
+    A = rng.standard_normal((200, 24))
+    res = mcp.fg_implicit(obs, np.zeros(24), A, 3, 0.0, mode="tf32x3")
+    assert res.f == 0.0 and np.array_equal(res.g_A, np.zeros_like(A))
+    lam = rng.standard_normal(24)
+    a = mcp.fg_implicit(obs, lam, A, 3, mode="tf32x3")
+    b = mcp.fg_implicit(obs, lam, A, 3, mode="tf32x3")
+    assert a.f == b.f and np.array_equal(a.g_A, b.g_A)

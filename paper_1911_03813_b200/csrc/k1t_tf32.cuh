@@ -4,6 +4,11 @@
 //   GEMM1  Z[128 x RB] = V_tile[128 x n] A[n x RB]          tcgen05.mma kind::tf32, D in TMEM
 //   epi    P = nu * Z^(d-1)  (fp64 arithmetic, stored as TF32 hi/lo bricks in shared memory)
 //   GEMM2  Y[n x RB] += V_tile^T P                           tcgen05.mma kind::tf32, D in TMEM
+// Roofline note: both operands come from shared memory (SS mode) and TMEM capacity caps the
+// column block at RB <= 64 (Y needs (n/128) x RB TMEM columns), so each 3xTF32 k-step re-reads
+// A and B three times: ~136 KB of smem traffic per 32-wide k-step against 128 B/clk/SM.  The
+// kernel is shared-memory-bandwidth bound well below the TF32 tensor peak; TMEM-sourced A
+// operands (tcgen05.cp) and 2-CTA pairs are the next step.
 // Every product is the 3xTF32 split  x*y ~= xh*yh + xh*yl + xl*yh  (xh = top 10 mantissa bits,
 // xl = x - xh), so the result carries ~1e-7 relative error instead of TF32's 1e-3 (SURVEY.md
 // Appendix B); Z and P never reach HBM.  Y accumulates in fp32 TMEM for K1T_FLUSH tiles and is
@@ -55,9 +60,10 @@ __host__ __device__ constexpr size_t k1t_smem_bytes(int RB, int stages) {
 __global__ void __launch_bounds__(K1T_THREADS, 1)
     k1t_fg_tf32(const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_v2,
                 const __grid_constant__ CUtensorMap tm_a, K1TParams prm) {
-  extern __shared__ unsigned char smem_raw_t[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw_t) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) unsigned char smem_raw_t[];
+  // 1 KB alignment by an offset on the shared array itself, so the compiler keeps the shared
+  // address space (LDS/STS, not generic loads) for everything derived from `base`
+  unsigned char* base = smem_raw_t + ((1024u - (smem_u32(smem_raw_t) & 1023u)) & 1023u);
   const int RB = prm.RB, NS = prm.stages;
   const size_t SB = k1t_stage_bytes(RB);
   unsigned char* sPh = base + NS * SB;                 // 4 bricks x RB rows x 128 B

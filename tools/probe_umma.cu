@@ -102,8 +102,21 @@ int main() {
   cudaMalloc(&dB, B.size() * 4);
   cudaMalloc(&dD, D.size() * 4);
   int fails = 0;
-  for (int mv = 0; mv < 4; ++mv) {
-    int mode = mv < 4 ? mv : (mv < 8 ? 1 : 2), variant = mv < 4 ? 0 : (mv % 4);
+  for (int mv = 0; mv < 5; ++mv) {
+    int mode = mv, variant = 0;
+    if (mv == 4) {
+      // conversion probe: A = 1 + j*2^-14 (bits below TF32), B = e_0 -> D[m][0] = tf32(A[m][0])
+      for (int m = 0; m < M; ++m) for (int k = 0; k < K; ++k) A[m * K + k] = (k == 0) ? 1.0f + (float)(m % 16) * ldexpf(1.0f, -14) : 0.0f;
+      for (int nn = 0; nn < N; ++nn) for (int k = 0; k < K; ++k) B[nn * K + k] = (k == 0 && nn == 0) ? 1.0f : 0.0f;
+      cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+      cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+      umma_test<<<1, 128>>>(dA, dB, dD, 0, 0);
+      cudaDeviceSynchronize();
+      cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+      printf("conversion probe (A = 1 + j*2^-14, TF32 ulp = 2^-10):\n");
+      for (int m = 0; m < 16; ++m) printf("  j=%2d  A=%.9f  D=%.9f\n", m, A[m * K], D[m * N]);
+      continue;
+    }
     srand(1 + mode);
     for (auto& x : A) x = mode == 3 ? (float)rand() / RAND_MAX - 0.5f : (float)(rand() % 7 - 3);
     for (auto& x : B) x = mode == 3 ? (float)rand() / RAND_MAX - 0.5f : (float)(rand() % 7 - 3) * 0.5f;

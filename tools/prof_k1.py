@@ -15,6 +15,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--evals", type=int, default=4)
 ap.add_argument("--p", type=int, default=None)
 ap.add_argument("--dnorm", action="store_true")
+ap.add_argument("--mode", default=None)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 V = synth.device_observations(cfg, 2024, p=a.p)
@@ -29,6 +30,6 @@ else:
     out = torch.empty(1 + cfg.r + cfg.n * cfg.r, dtype=torch.float64, device="cuda")
     s = _native.stream_handle(torch.cuda.current_stream())
     for _ in range(a.evals):
-        ctx.fg_device(cfg.d, cfg.r, x.data_ptr(), 0.0, None, out.data_ptr(), s)
+        ctx.fg_device(cfg.d, cfg.r, x.data_ptr(), 0.0, a.mode, out.data_ptr(), s)
     torch.cuda.synchronize()
     print("f", float(out[0]), ctx.last_variant)

@@ -155,6 +155,13 @@ def run_reference(args, cfg, rank, world):
         return
     from paper_1911_03813_b200 import synth
 
+    # torchrun exports OMP_NUM_THREADS=1; the reference arm uses every host core
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=os.cpu_count())
+    except Exception:  # noqa: BLE001
+        pass
     p_sample = cfg.p if cfg.name in ("c1", "c2") else min(cfg.p, 200_000)
     V = synth.host_observations(cfg, SEED, p=p_sample)
     V = np.asarray(V, dtype=float)
@@ -196,10 +203,16 @@ def run_data_norm(args, cfg, rank, world, local):
     from paper_1911_03813_b200 import distributed as D
     from paper_1911_03813_b200 import synth
 
+    same_dev = os.environ.get("MCP_BENCH_SAME_DEVICE") == "1"   # test only, see main()
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if args.impl == "reference":
         return
     V = synth.device_observations(cfg, SEED, device=dev)
@@ -279,10 +292,18 @@ def main():
     from paper_1911_03813_b200 import _native
     from paper_1911_03813_b200 import distributed as D
 
+    # MCP_BENCH_SAME_DEVICE=1 (test only): every rank on cuda:0 over gloo, to exercise the
+    # multi-rank flow on a one-GPU box (NCCL refuses two ranks on one device).
+    same_dev = os.environ.get("MCP_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     group = None
 
     # ---- data: this rank's rows, generated on its GPU ----
@@ -435,6 +456,12 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
     }
     if world == 1 and not args.no_cpu:
+        try:
+            from threadpoolctl import threadpool_limits
+
+            threadpool_limits(limits=os.cpu_count())
+        except Exception:  # noqa: BLE001
+            pass
         # bounded CPU sample on this host: the full workload when it fits (c1, c2), else rows
         p_sample = cfg.p if cfg.name in ("c1", "c2") else min(cfg.p, 100_000)
         Vh = Vrows[:p_sample].double().cpu().numpy().T          # n x p view (reference layout)

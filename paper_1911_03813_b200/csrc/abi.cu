@@ -758,16 +758,22 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
     return c->fail(MCP_ERR_ARG, "unknown mode " + std::to_string(mode));
   if (nparts < 1 || part < 0 || part >= nparts) return c->fail(MCP_ERR_ARG, "bad part/nparts");
   if (!out) return c->fail(MCP_ERR_ARG, "NULL argument");
-  const int64_t T = c->p_pad / K5_T;
+  // K5 v2 (128 x 128 tiles) for n >= 32; the 64 x 64 variant for narrow observations
+  const bool big = c->n >= 32 && (c->p_pad % K52_T) == 0;
+  const int64_t TT = big ? K52_T : K5_T;
+  const int64_t T = c->p_pad / TT;
   const int64_t pairs = T * (T + 1) / 2;
   const int64_t b = pairs * part / nparts, e = pairs * (part + 1) / nparts;
-  const int n_chunks = (int)ceil_div(c->n, K5_NK);
-  const size_t smem = c->dtype == MCP_F64 ? k5_smem_bytes<double>() : k5_smem_bytes<float>();
-  const void* fn = c->dtype == MCP_F64 ? (const void*)k5_gram_power<double>
-                                       : (const void*)k5_gram_power<float>;
+  const int n_chunks = (int)ceil_div(c->n, big ? K52_NK : K5_NK);
+  const bool f64 = c->dtype == MCP_F64;
+  const size_t smem = big ? (f64 ? k52_smem_bytes<double>() : k52_smem_bytes<float>())
+                          : (f64 ? k5_smem_bytes<double>() : k5_smem_bytes<float>());
+  const void* fn = big ? (f64 ? (const void*)k52_gram_power<double> : (const void*)k52_gram_power<float>)
+                       : (f64 ? (const void*)k5_gram_power<double> : (const void*)k5_gram_power<float>);
+  const int threads = big ? K52_THREADS : K5_THREADS;
   CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, K5_THREADS, smem));
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)c->sms * occ;
   if (grid > e - b) grid = e - b;
@@ -776,12 +782,20 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
   if ((rc = ensure(c, c->dpart, sizeof(double) * grid))) return rc;
   if ((rc = ensure(c, c->dscalar, sizeof(double)))) return rc;
   auto* ev = timing_begin(c, c->stream);
-  if (c->dtype == MCP_F64)
-    k5_gram_power<double><<<(int)grid, K5_THREADS, smem, c->stream>>>(
+  if (big && f64)
+    k52_gram_power<double><<<(int)grid, threads, smem, c->stream>>>(
+        (const double*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
+        (double*)c->dpart.p);
+  else if (big)
+    k52_gram_power<float><<<(int)grid, threads, smem, c->stream>>>(
+        (const float*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
+        (double*)c->dpart.p);
+  else if (f64)
+    k5_gram_power<double><<<(int)grid, threads, smem, c->stream>>>(
         (const double*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
         (double*)c->dpart.p);
   else
-    k5_gram_power<float><<<(int)grid, K5_THREADS, smem, c->stream>>>(
+    k5_gram_power<float><<<(int)grid, threads, smem, c->stream>>>(
         (const float*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
         (double*)c->dpart.p);
   timing_end(ev, c->stream);
@@ -791,7 +805,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
   CUDA_TRY(c, cudaMemcpyAsync(out, c->dscalar.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->last_launches = 2;
-  c->variant = c->dtype == MCP_F64 ? "k5_gram_dmma<f64>" : "k5_gram_dmma<f32>";
+  c->variant = std::string(big ? "k52_gram_dmma128" : "k5_gram_dmma64") + (f64 ? "<f64>" : "<f32>");
   return MCP_OK;
 }
 

@@ -86,16 +86,16 @@ __global__ void __launch_bounds__(K5_THREADS)
     for (int c = 0; c < n_chunks; ++c) {
       const int s = c & 1;
       if (c + 1 < n_chunks) {
-        k5_load<VT>(sI[s ^ 1], V, ldv, I * K5_T, c + 1);
-        k5_load<VT>(sJ[s ^ 1], V, ldv, J * K5_T, c + 1);
+        k5_load<VT>(s ? sI[0] : sI[1], V, ldv, I * K5_T, c + 1);
+        k5_load<VT>(s ? sJ[0] : sJ[1], V, ldv, J * K5_T, c + 1);
         cp_async_commit();
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncthreads();
-      const VT* ai = sI[s] + (32 * wm + g) * K5_SV + t;
-      const VT* bj = sJ[s] + (16 * wn + g) * K5_SV + t;
+      const VT* ai = (s ? sI[1] : sI[0]) + (32 * wm + g) * K5_SV + t;
+      const VT* bj = (s ? sJ[1] : sJ[0]) + (16 * wn + g) * K5_SV + t;
 #pragma unroll 4
       for (int ks = 0; ks < 16; ++ks) {
         double a[4], b[2];
@@ -137,6 +137,122 @@ __global__ void __launch_bounds__(K5_THREADS)
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < K5_THREADS / 32; ++w) s += sRed[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+// ---- K5 v2: 128 x 128 tile pairs, 16 warps (4 x 4 warp grid, 32 x 32 per warp), 32-wide
+// n-chunks double buffered.  4 + 4 fragment loads feed 16 DMMAs per k-step (vs 6 per 8 for
+// 64 x 64 tiles) and each pair moves half the L2 bytes per flop.
+constexpr int K52_T = 128;
+constexpr int K52_NK = 32;
+constexpr int K52_SV = 36;   // == 4 (mod 16) doubles: conflict-free 8-byte fragment loads
+constexpr int K52_THREADS = 512;
+
+template <typename VT>
+__host__ __device__ constexpr size_t k52_smem_bytes() {
+  return 4 * (size_t)K52_T * K52_SV * sizeof(VT) + 16 * sizeof(double);
+}
+
+template <typename VT>
+__device__ __forceinline__ void k52_load(VT* dst, const VT* __restrict__ V, int64_t ldv,
+                                         int64_t row0, int c) {
+  constexpr int SEG = 16 / sizeof(VT);
+  constexpr int SEGS_ROW = K52_NK / SEG;
+  constexpr int TOTAL = K52_T * SEGS_ROW;
+#pragma unroll
+  for (int s = threadIdx.x; s < TOTAL; s += K52_THREADS) {
+    const int row = s / SEGS_ROW, seg = s % SEGS_ROW;
+    const int64_t col = (int64_t)c * K52_NK + seg * SEG;
+    const bool ok = col < ldv;
+    const VT* src = ok ? V + (row0 + row) * ldv + col : V;
+    cp_async16(dst + row * K52_SV + seg * SEG, src, ok ? 16 : 0);
+  }
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(K52_THREADS, 1)
+    k52_gram_power(const VT* __restrict__ V, int64_t ldv, int n_chunks, const double* __restrict__ nu,
+                   double nu_const, int d, int64_t T, int64_t pair_begin, int64_t pair_end,
+                   double* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char smem_raw5[];
+  VT* sI[2];
+  VT* sJ[2];
+  sI[0] = reinterpret_cast<VT*>(smem_raw5);
+  sI[1] = sI[0] + K52_T * K52_SV;
+  sJ[0] = sI[1] + K52_T * K52_SV;
+  sJ[1] = sJ[0] + K52_T * K52_SV;
+  double* sRed = reinterpret_cast<double*>(sJ[1] + K52_T * K52_SV);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;   // 4 x 4 warps, 32 x 32 each
+  double tsum = 0.0;
+
+  for (int64_t pair = pair_begin + blockIdx.x; pair < pair_end; pair += gridDim.x) {
+    int64_t I, J;
+    k5_decode(pair, T, I, J);
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    k52_load<VT>(sI[0], V, ldv, I * K52_T, 0);
+    k52_load<VT>(sJ[0], V, ldv, J * K52_T, 0);
+    cp_async_commit();
+    for (int c = 0; c < n_chunks; ++c) {
+      const int s = c & 1;
+      if (c + 1 < n_chunks) {
+        k52_load<VT>(s ? sI[0] : sI[1], V, ldv, I * K52_T, c + 1);
+        k52_load<VT>(s ? sJ[0] : sJ[1], V, ldv, J * K52_T, c + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const VT* ai = (s ? sI[1] : sI[0]) + (32 * wm + g) * K52_SV + t;
+      const VT* bj = (s ? sJ[1] : sJ[0]) + (32 * wn + g) * K52_SV + t;
+#pragma unroll
+      for (int ks = 0; ks < K52_NK / 4; ++ks) {
+        double a[4], b[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) a[mt] = to_f64(ai[8 * mt * K52_SV + 4 * ks]);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) b[nt] = to_f64(bj[8 * nt * K52_SV + 4 * ks]);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+      }
+      __syncthreads();
+    }
+
+    double tile_sum = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int64_t l = I * K52_T + 32 * wm + 8 * mt + g;
+      const double nl = nu ? nu[l] : nu_const;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t l2 = J * K52_T + 32 * wn + 8 * nt + 2 * t + e;
+          const double nl2 = nu ? nu[l2] : nu_const;
+          tile_sum += (nl * nl2) * rm_pow(acc[mt][nt][e], d);
+        }
+    }
+    tsum += (I == J) ? tile_sum : 2.0 * tile_sum;
+  }
+
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, off);
+  if (lane == 0) sRed[warp] = tsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < K52_THREADS / 32; ++w) s += sRed[w];
     part[blockIdx.x] = s;
   }
 }

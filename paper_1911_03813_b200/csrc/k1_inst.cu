@@ -86,9 +86,11 @@ struct EntryS {
 #define MCP_K1S_COLS(MTH, KH) \
   MCP_K1S_E(1, 0, MTH, KH), MCP_K1S_E(1, 1, MTH, KH), MCP_K1S_E(1, 2, MTH, KH), \
       MCP_K1S_E(2, 0, MTH, KH)
-// (MTH, KH) groups by n: <=16, <=32, <=64, ==97..100, <=104, <=128
-const EntryS kTableS[] = {MCP_K1S_COLS(1, 3),  MCP_K1S_COLS(2, 5),  MCP_K1S_COLS(4, 9),
-                          MCP_K1S_COLS(7, 13), MCP_K1S_COLS(7, 15), MCP_K1S_COLS(8, 17)};
+// (MTH, KH) groups by n (KH = ldv / 4 with ldv == 4 mod 16): n <= 4, <= 20, <= 36, <= 68,
+// <= 100, <= 116, <= 128
+const EntryS kTableS[] = {MCP_K1S_COLS(1, 1),  MCP_K1S_COLS(2, 5),  MCP_K1S_COLS(3, 9),
+                          MCP_K1S_COLS(5, 17), MCP_K1S_COLS(7, 25), MCP_K1S_COLS(8, 29),
+                          MCP_K1S_COLS(8, 33)};
 constexpr int kEntriesS = sizeof(kTableS) / sizeof(kTableS[0]);
 std::atomic<bool> g_attr_s[kEntriesS];
 
@@ -96,7 +98,7 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
   if (n > 128 || r > 16) return false;
   const int MT = (int)ceil_div(n, 8);
   const int kst = (int)(ldv / 4);
-  const int mth_need = (MT + 1) / 2, kh_need = (kst + 1) / 2;
+  const int mth_need = (MT + 1) / 2, kh_need = kst;
   int ntm, tail;
   if (r <= 8) { ntm = 1; tail = 0; }
   else if (r <= 10) { ntm = 1; tail = r - 8; }

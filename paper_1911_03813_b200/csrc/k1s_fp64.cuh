@@ -22,7 +22,8 @@
 
 namespace mcp {
 
-constexpr int K1S_SR = 16;   // observations per slab
+constexpr int K1S_SR = 16;   // observations per slab (one pair, 8 rows per warp in GEMM1)
+constexpr int K1S_MT1 = K1S_SR / 16;  // GEMM1 m-tiles per warp
 
 struct K1SParams {
   const double* V;       // p_pad x ldv observation-major, fp64
@@ -91,10 +92,10 @@ __host__ __device__ constexpr int k1s_pp(int cw) { return cw <= 12 ? 12 : 20; }
 
 // Dynamic smem layout, in order:
 //   ring: stages * SR * ldv doubles | Afrag: (ldv/4) * NTM * 32 doubles | Atail: ldv * 4 doubles
-//   P staging: pairs * SR * PP doubles | exchange: pairs * 2 * 32 * 4 doubles | barriers
+//   P staging: pairs * 2 * SR * PP doubles (double buffered) | barriers
 __host__ __device__ inline size_t k1s_fixed_bytes(int kh, int ntm, int cw, int pairs) {
-  return (size_t)(2 * kh) * ntm * 32 * 8 + (size_t)(2 * kh) * 16 * 8 +
-         (size_t)pairs * K1S_SR * k1s_pp(cw) * 8 + (size_t)pairs * 2 * 32 * 4 * 8;
+  return (size_t)kh * ntm * 32 * 8 + (size_t)kh * 16 * 8 +
+         (size_t)pairs * 2 * K1S_SR * k1s_pp(cw) * 8;
 }
 
 
@@ -102,7 +103,7 @@ constexpr int K1S_PAIRS = 7;  // math warp pairs per CTA (15 warps: <= 4 per SMS
 constexpr int K1S_THREADS = (2 * K1S_PAIRS + 1) * 32;  // + 1 producer warp
 
 // NTM: 8-column DMMA tiles, TAIL: DFMA columns, MTH: GEMM2 m-tiles per warp (warp 0 of a pair
-// takes [0, MTH), warp 1 [MTH, MT)), KH: GEMM1 k-steps per warp (warp 0 [0, KH0), warp 1 the rest).
+// takes [0, MTH), warp 1 [MTH, MT)), KH: GEMM1 k-steps (>= ldv / 4, zero-padded factor).
 template <int NTM, int TAIL, int MTH, int KH>
 __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   constexpr int CW = 8 * NTM + TAIL;
@@ -113,14 +114,12 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   const int64_t ldv = prm.ldv;
   const int S = prm.stages;
   const int kst = (int)(ldv / 4);
-  double* ring = reinterpret_cast<double*>(smem_raw);
   const int spc = prm.spc;
-  const int kpad = 2 * KH;                             // k-steps incl. zero padding
-  double* sAf = ring + (size_t)S * spc * K1S_SR * ldv;
-  double* sAt = sAf + (size_t)kpad * NTM * 32;
-  double* sP = sAt + kpad * 16;                        // [NP][SR][PP]
-  double* sX = sP + NP * K1S_SR * PP;                  // [NP][2][32][4] GEMM1 K-half exchange
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + NP * 2 * 32 * 4);
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  double* sAf = ring + (size_t)S * spc * K1S_SR * ldv;  // [KH][NTM][32]
+  double* sAt = sAf + (size_t)KH * NTM * 32;             // [KH*4 rows][4]
+  double* sP = sAt + KH * 16;                            // [NP][2][SR][PP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sP + NP * 2 * K1S_SR * PP);
   uint64_t* empty = full + S;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -129,15 +128,14 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   const int pg = blockIdx.x / prm.rbs;
   const int col0 = rb * CW;
 
-  // Factor block (zero beyond n / r and for the padding k-steps), and a zeroed ring: GEMM1 runs
-  // a fixed KH k-steps per warp, so warp 1's padding step multiplies finite V data (the next
-  // row, or zeros) by exact-zero factor entries -- never uninitialised shared memory.
-  for (int idx = threadIdx.x; idx < kpad * NTM * 32; idx += blockDim.x) {
+  // factor block (zero beyond n / r and for the padding k-steps) and a zeroed ring: the
+  // padding k-steps multiply finite data (the next row, or zeros) by exact zeros
+  for (int idx = threadIdx.x; idx < KH * NTM * 32; idx += blockDim.x) {
     const int ln = idx & 31, nt = (idx >> 5) % NTM, ks = (idx >> 5) / NTM;
     const int i = 4 * ks + (ln & 3), j = col0 + 8 * nt + (ln >> 2);
     sAf[idx] = (i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
   }
-  for (int idx = threadIdx.x; idx < kpad * 16; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < KH * 16; idx += blockDim.x) {
     const int i = idx >> 2, c = idx & 3, j = col0 + 8 * NTM + c;
     sAt[idx] = (c < TAIL && i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
   }
@@ -163,7 +161,7 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
     // ---------------- producer: one lane streams copy units into the ring ----------------
     if (lane == 0) {
       int s = 0;
-      uint32_t ph = 0;  // completed-use parity of stage s for the empty wait
+      uint32_t ph = 0;
       const double* src = prm.V + (int64_t)pg * spc * K1S_SR * ldv;
       const int64_t step = (int64_t)prm.gp * spc * K1S_SR * ldv;
       for (int64_t j = 0; j < my_units; ++j) {
@@ -184,8 +182,9 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   // ---------------- math warps ----------------
   const int q = warp >> 1, h = warp & 1;
   const int mbase = h * MTH;
-  const int mcnt = h == 0 ? MTH : prm.MT - MTH;          // 0 <= mcnt <= MTH
-  const int kbase = h * KH;                              // warp h: k-steps [h*KH, h*KH + KH)
+  // m-tiles this warp owns (warp 0: [0, MTH), warp 1: [MTH, MT)); 0 <= mcnt <= MTH.  It bounds
+  // the final staging writes, which must never spill into the next pair's region.
+  const int mcnt = h == 0 ? min(MTH, prm.MT) : max(0, prm.MT - MTH);
   double yacc[MTH][NTM][2];
   double ytl[MTH][TL];
   double wacc[NTM][2];
@@ -200,11 +199,7 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
 #pragma unroll
   for (int nt = 0; nt < NTM; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
   const int dm1 = prm.d - 1;
-  const int lr = 8 * h + g;
-  (void)dm1;
-  double* Pb = sP + (size_t)q * K1S_SR * PP;
-  double* xo = sX + ((size_t)q * 2 + h) * 128 + lane * 4;       // my partial for rows of 1-h
-  const double* xi = sX + ((size_t)q * 2 + (1 - h)) * 128 + lane * 4;  // partner's, rows of h
+  (void)kst;
 
   // Slab walk without divisions: k advances by NP, so the unit index advances by
   // (sub + NP) / spc and sub becomes (sub + NP) % spc -- both functions of sub < spc <= 14 only.
@@ -212,7 +207,8 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
   int sub = q % spc;
   int s = (int)(j % S);
   uint32_t ph = (uint32_t)((j / S) & 1);
-  const int dj_lo = NP / spc, sub_step = NP % spc;   // (sub + NP) = dj_lo*spc + sub_step + sub
+  const int dj_lo = NP / spc, sub_step = NP % spc;
+  int buf = 0;
   for (int64_t k = q; k < my_slabs; k += NP) {
     mbar_wait(&full[s], ph);
     const double* sv = ring + ((size_t)s * spc + sub) * K1S_SR * ldv;
@@ -232,8 +228,11 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
         ph ^= 1;
       }
     }
+    double* Pb = sP + ((size_t)q * 2 + buf) * K1S_SR * PP;
+    buf ^= 1;
 
-    // ---- GEMM1 partial over this warp's k-steps, all 16 slab rows ----
+    // ---- GEMM1 on rows 8h..8h+7, all k-steps ----
+    constexpr int M1 = K1S_MT1 > 0 ? K1S_MT1 : 1;
     double z[2][NTM][2], zt[2][TL];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -242,98 +241,70 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
 #pragma unroll
       for (int c = 0; c < TL; ++c) zt[mt][c] = 0.0;
     }
-    const double* v0 = sv + g * ldv + 4 * kbase + t;
-    const double* v1 = v0 + 8 * ldv;
-    const double* bp = sAf + kbase * NTM * 32 + lane;
-    const double* at = sAt + (4 * kbase + t) * 4;
+    // even / odd k-steps accumulate separately (2 independent DMMA chains), added below
+    const double* v0 = sv + (8 * h + g) * ldv + t;
+    const double* bp = sAf + lane;
+    const double* at = sAt + t * 4;
 #pragma unroll
     for (int kk = 0; kk < KH; ++kk) {
-      const double a0 = v0[4 * kk], a1 = v1[4 * kk];
+      const int e2 = kk & 1;
+      const double a0 = v0[4 * kk];
 #pragma unroll
-      for (int nt = 0; nt < NTM; ++nt) {
-        const double b = bp[(kk * NTM + nt) * 32];
-        dmma884(z[0][nt], a0, b);
-        dmma884(z[1][nt], a1, b);
-      }
+      for (int nt = 0; nt < NTM; ++nt) dmma884(z[e2][nt], a0, bp[(kk * NTM + nt) * 32]);
       if constexpr (TAIL > 0) {
         const double2 tv = *reinterpret_cast<const double2*>(at + 16 * kk);
-        zt[0][0] = fma(a0, tv.x, zt[0][0]);
-        zt[1][0] = fma(a1, tv.x, zt[1][0]);
-        if constexpr (TAIL > 1) {
-          zt[0][TL - 1] = fma(a0, tv.y, zt[0][TL - 1]);
-          zt[1][TL - 1] = fma(a1, tv.y, zt[1][TL - 1]);
-        }
+        zt[e2][0] = fma(a0, tv.x, zt[e2][0]);
+        if constexpr (TAIL > 1) zt[e2][TL - 1] = fma(a0, tv.y, zt[e2][TL - 1]);
       }
     }
-    // ---- add the two K halves (fixed order: half 0 + half 1) ----
-    {
-      // hand the partner my partial for its m-tile (1 - h); select, never index by h
-      double xv[4];
+#pragma unroll
+    for (int nt = 0; nt < NTM; ++nt) {
+      z[0][nt][0] += z[1][nt][0];
+      z[0][nt][1] += z[1][nt][1];
+    }
+#pragma unroll
+    for (int c = 0; c < TL; ++c) zt[0][c] += zt[1][c];
+    static_assert(TAIL <= 2, "tail columns are loaded as one double2");
+
+    // ---- epilogue on row 8h + g: P = nu z^(d-1), w += P z ----
+#pragma unroll
+    for (int mt = 0; mt < M1; ++mt) {
+      const int lr = 8 * h + g;
+      const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
+      constexpr int NV = 2 * NTM + 1;   // this lane's z values: DMMA columns, then a tail column
+      double zv[NV], pw[NV];
 #pragma unroll
       for (int nt = 0; nt < NTM; ++nt) {
-        xv[2 * nt] = h == 0 ? z[1][nt][0] : z[0][nt][0];
-        xv[2 * nt + 1] = h == 0 ? z[1][nt][1] : z[0][nt][1];
+        zv[2 * nt] = z[mt][nt][0];
+        zv[2 * nt + 1] = z[mt][nt][1];
       }
-      if constexpr (NTM == 1) {
-        xv[2] = TAIL > 0 ? (h == 0 ? zt[1][0] : zt[0][0]) : 0.0;
-        xv[3] = TAIL > 1 ? (h == 0 ? zt[1][TL - 1] : zt[0][TL - 1]) : 0.0;
-      }
-      *reinterpret_cast<double2*>(xo) = make_double2(xv[0], xv[1]);
-      *reinterpret_cast<double2*>(xo + 2) = make_double2(xv[2], xv[3]);
-    }
-    static_assert(NTM == 1 ? TAIL <= 2 : TAIL == 0, "exchange slot holds 4 doubles per lane");
-    asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
-    double zf[NTM][2], ztf[TL];
-    {
-      const double2 p01 = *reinterpret_cast<const double2*>(xi);
-      const double2 p23 = *reinterpret_cast<const double2*>(xi + 2);
-      const double pv[4] = {p01.x, p01.y, p23.x, p23.y};
-#pragma unroll
-      for (int nt = 0; nt < NTM; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          zf[nt][e] = h == 0 ? z[0][nt][e] + pv[2 * nt + e] : pv[2 * nt + e] + z[1][nt][e];
-#pragma unroll
-      for (int c = 0; c < TAIL; ++c)
-        ztf[c] = h == 0 ? zt[0][c] + pv[2 + c] : pv[2 + c] + zt[1][c];
-    }
-    // ---- epilogue on rows 8h..8h+7: P = nu z^(d-1), w += P z ----
-    const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
-    constexpr int NV = 2 * NTM + TL;   // this lane's z values: DMMA columns, then its tail column
-    double zv[NV], pw[NV];
-#pragma unroll
-    for (int nt = 0; nt < NTM; ++nt) {
-      zv[2 * nt] = zf[nt][0];
-      zv[2 * nt + 1] = zf[nt][1];
-    }
-    if constexpr (TAIL > 0) {
-#pragma unroll
-      for (int c = 0; c < TAIL; ++c) {
-        double zz = ztf[c];
-        zz += __shfl_xor_sync(0xffffffffu, zz, 1);   // lane t summed i == t (mod 4)
-        zz += __shfl_xor_sync(0xffffffffu, zz, 2);
-        if (t == c) zv[2 * NTM] = zz;                // lane t == c owns tail column c
-      }
-      if (t >= TAIL) zv[2 * NTM] = 0.0;
-    } else {
       zv[2 * NTM] = 0.0;
-    }
-    rm_pow_vec<NV>(zv, pw, dm1);
+      if constexpr (TAIL > 0) {
 #pragma unroll
-    for (int nt = 0; nt < NTM; ++nt) {
-      double pv[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        pv[e] = nul * pw[2 * nt + e];
-        wacc[nt][e] = fma(pv[e], zv[2 * nt + e], wacc[nt][e]);
+        for (int c = 0; c < TAIL; ++c) {
+          double zz = zt[mt][c];
+          zz += __shfl_xor_sync(0xffffffffu, zz, 1);   // lane t summed i == t (mod 4)
+          zz += __shfl_xor_sync(0xffffffffu, zz, 2);
+          if (t == c) zv[2 * NTM] = zz;                // lane t == c owns tail column c
+        }
       }
-      *reinterpret_cast<double2*>(&Pb[lr * PP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
-    }
-    if constexpr (TAIL > 0) {
-      if (t < TAIL) {
-        const double pv = nul * pw[2 * NTM];
-        wtl = fma(pv, zv[2 * NTM], wtl);
-        Pb[lr * PP + 8 * NTM + t] = pv;
+      rm_pow_vec<NV>(zv, pw, dm1);
+#pragma unroll
+      for (int nt = 0; nt < NTM; ++nt) {
+        double pv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          pv[e] = nul * pw[2 * nt + e];
+          wacc[nt][e] = fma(pv[e], zv[2 * nt + e], wacc[nt][e]);
+        }
+        *reinterpret_cast<double2*>(&Pb[lr * PP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
+      }
+      if constexpr (TAIL > 0) {
+        if (t < TAIL) {
+          const double pv = nul * pw[2 * NTM];
+          wtl = fma(pv, zv[2 * NTM], wtl);
+          Pb[lr * PP + 8 * NTM + t] = pv;
+        }
       }
     }
     asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
@@ -362,7 +333,6 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s_cur]);
   }
-
   // ---------------- fixed-order combine of the math warps' partials ----------------
 #pragma unroll
   for (int m = 0; m < MTH; ++m)

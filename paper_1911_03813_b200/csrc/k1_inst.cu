@@ -101,7 +101,7 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
   const int mth_need = (MT + 1) / 2, kh_need = kst;
   int ntm, tail;
   if (r <= 8) { ntm = 1; tail = 0; }
-  else if (r <= 10) { ntm = 1; tail = r - 8; }
+  else if (r <= 10 && !getenv("MCP_K1S_NO_TAIL")) { ntm = 1; tail = r - 8; }
   else { ntm = 2; tail = 0; }
   int e = -1;
   for (int i = 0; i < kEntriesS && e < 0; ++i)

@@ -98,6 +98,15 @@ int mcp_fg(mcp_ctx* ctx, int d, int r, const double* lam, const double* A_colmaj
 int mcp_fg_packed(mcp_ctx* ctx, int d, int r, const double* x, double alpha, int mode, double* f,
                   double* g);
 
+/*
+ * Batched evaluation of k starting points in ONE pass over V (SURVEY.md 8f "batched multistart";
+ * the reference runs multistart's starts one by one, optimize.py:454-508).  X is k x (r + n r),
+ * row s = the packed point of start s; F[s] and G row s are its f and packed gradient.  Y and w
+ * depend on each factor column alone, so the k*r columns share K1; the tails run per start.
+ */
+int mcp_fg_batch(mcp_ctx* ctx, int d, int r, int k, const double* X, double alpha, int mode,
+                 double* F, double* G);
+
 /* Y = V diag(nu) (V^T A)^(d-1), n x r column-major (implicit.py:94-107). */
 int mcp_ttsv_batch(mcp_ctx* ctx, int d, int r, const double* A_colmajor, int mode,
                    double* Y_colmajor);

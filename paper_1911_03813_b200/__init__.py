@@ -21,7 +21,7 @@ from .implicit import (
     ttsv_batch,
 )
 from .objective import FgResult, fg_implicit
-from .optimize import FgCallback, pack, packed_fg_implicit, unpack
+from .optimize import FgCallback, pack, packed_fg_implicit, packed_fg_implicit_batched, unpack
 
 __all__ = [
     "FgCallback",
@@ -36,6 +36,7 @@ __all__ = [
     "model_data_inner",
     "pack",
     "packed_fg_implicit",
+    "packed_fg_implicit_batched",
     "ttsv_batch",
     "unpack",
 ]

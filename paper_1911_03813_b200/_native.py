@@ -43,6 +43,8 @@ SIGNATURES = {
                               ctypes.c_double, ctypes.c_int, _dp, _c_void_p, _c_void_p]),
     "mcp_fg_packed": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
                                      ctypes.c_double, ctypes.c_int, _dp, _c_void_p]),
+    "mcp_fg_batch": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                    ctypes.c_double, ctypes.c_int, _c_void_p, _c_void_p]),
     "mcp_ttsv_batch": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
                                       ctypes.c_int, _c_void_p]),
     "mcp_data_norm_sq": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _dp]),
@@ -207,6 +209,16 @@ class Context:
                               mode_code(mode), ctypes.byref(f), _ptr(g_lam), _ptr(g_A))
         self._check(rc, "mcp_fg")
         return f.value, g_lam, g_A
+
+    def fg_batch(self, X: np.ndarray, n: int, d: int, r: int, alpha: float, mode: str | None):
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        k = X.shape[0]
+        F = np.empty(k, dtype=np.float64)
+        G = np.empty_like(X)
+        rc = self._lib.mcp_fg_batch(self._h, int(d), int(r), int(k), _ptr(X), float(alpha),
+                                    mode_code(mode), _ptr(F), _ptr(G))
+        self._check(rc, "mcp_fg_batch")
+        return F, G
 
     def ttsv_batch(self, A_fortran: np.ndarray, d: int, mode: str | None) -> np.ndarray:
         n, r = A_fortran.shape

@@ -417,26 +417,32 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   return MCP_OK;
 }
 
-// K4: tail from (x, Yw) -> out = [f ; g_lam ; vec_F(g_A)].
-int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
-                   const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
+// K4: tail from (x, Y, w) -> out = [f ; g_lam ; vec_F(g_A)].
+int enqueue_finish_yw(mcp_ctx* c, int d, int r, const double* dx, const double* dY,
+                      const double* dw, const double* alpha_dev, double alpha, double* dout,
+                      cudaStream_t s) {
   const int n = (int)c->n;
   if ((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) {
-    k_tail_fused<<<1, K4S_THREADS, 0, s>>>(dx, dYw, n, r, d, alpha_dev, alpha, dout);
+    k_tail_fused<<<1, K4S_THREADS, 0, s>>>(dx, dY, dw, n, r, d, alpha_dev, alpha, dout);
     CUDA_TRY(c, cudaGetLastError());
     c->last_launches += 1;
     return MCP_OK;
   }
   k_tail_gram<<<grid_for((int64_t)r * r, 128, 8 * c->sms), 128, 0, s>>>(
       dx, n, r, d, (double*)c->dG.p, (double*)c->dC.p);
-  k_tail_vec<<<1, 256, sizeof(double) * r, s>>>(dx, dYw, (const double*)c->dG.p,
+  k_tail_vec<<<1, 256, sizeof(double) * r, s>>>(dx, dw, (const double*)c->dG.p,
                                                 (const double*)c->dC.p, n, r, alpha_dev, alpha,
                                                 dout);
   k_tail_ga<<<grid_for((int64_t)n * r, 256, 8 * c->sms), 256, 0, s>>>(
-      dx, dYw, (const double*)c->dC.p, n, r, d, dout);
+      dx, dY, (const double*)c->dC.p, n, r, d, dout);
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 3;
   return MCP_OK;
+}
+
+int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
+                   const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
+  return enqueue_finish_yw(c, d, r, dx, dYw, dYw + c->n * r, alpha_dev, alpha, dout, s);
 }
 
 // Host entry: x (r + n r doubles) + alpha -> out (1 + r + n r doubles), through a cached graph.
@@ -884,6 +890,61 @@ int mcp_kernel_time_ms(mcp_ctx* c, double* total_ms, int* launches, int reset) {
   if (reset) {
     for (auto& ev : c->timed) c->event_pool.push_back(ev);
     c->timed.clear();
+  }
+  return MCP_OK;
+}
+
+int mcp_fg_batch(mcp_ctx* c, int d, int r, int k, const double* X, double alpha, int mode,
+                 double* F, double* G) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!X || !F || !G) return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (k < 1) return c->fail(MCP_ERR_ARG, "batch size must be >= 1");
+  if (!std::isfinite(alpha))
+    return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  const int64_t n = c->n;
+  const int64_t rows = r + n * r;             // one packed start
+  const int R = k * r;                        // columns of the shared pass
+  EvalPlan pl;
+  int rc = plan_eval(c, d, R, mode, pl);
+  if (rc) return rc;
+  // staging: [lam_all (R) ; A_all (n x R, col-major) ; alpha] for the pass, then the k starts
+  const size_t xin = sizeof(double) * ((size_t)R + n * R + 1 + (size_t)k * rows);
+  const size_t xout = sizeof(double) * (size_t)k * (1 + rows);
+  if ((rc = ensure_host(c, c->hx, c->hx_bytes, xin))) return rc;
+  if ((rc = ensure_host(c, c->hout, c->hout_bytes, xout))) return rc;
+  if ((rc = ensure(c, c->dx, xin))) return rc;
+  if ((rc = ensure(c, c->dout, xout))) return rc;
+  double* hx = (double*)c->hx;
+  for (int sidx = 0; sidx < k; ++sidx) {
+    const double* xs = X + (size_t)sidx * rows;
+    std::memcpy(hx + (size_t)sidx * r, xs, sizeof(double) * r);
+    std::memcpy(hx + R + (size_t)sidx * n * r, xs + r, sizeof(double) * n * r);
+  }
+  hx[R + n * R] = alpha;
+  std::memcpy(hx + R + n * R + 1, X, sizeof(double) * (size_t)k * rows);
+  double* dx = (double*)c->dx.p;
+  CUDA_TRY(c, cudaMemcpyAsync(dx, hx, xin, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, c->stream))) return rc;
+  const int launches = c->last_launches;
+  const double* dY = (const double*)c->dYw.p;
+  const double* dW = dY + n * R;
+  const double* dXs = dx + R + n * R + 1;
+  for (int sidx = 0; sidx < k; ++sidx) {
+    if ((rc = enqueue_finish_yw(c, d, r, dXs + (size_t)sidx * rows, dY + (size_t)sidx * n * r,
+                                dW + (size_t)sidx * r, dx + R + n * R, 0.0,
+                                (double*)c->dout.p + (size_t)sidx * (1 + rows), c->stream)))
+      return rc;
+  }
+  c->last_launches += launches;
+  CUDA_TRY(c, cudaMemcpyAsync(c->hout, c->dout.p, xout, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  const double* out = (const double*)c->hout;
+  for (int sidx = 0; sidx < k; ++sidx) {
+    F[sidx] = out[(size_t)sidx * (1 + rows)];
+    std::memcpy(G + (size_t)sidx * rows, out + (size_t)sidx * (1 + rows) + 1,
+                sizeof(double) * rows);
   }
   return MCP_OK;
 }

@@ -95,13 +95,12 @@ __global__ void k_tail_gram(const double* __restrict__ x, int n, int r, int d,
 
 // K4b (one CTA): u = (G o C) lam, g_lam = -2 (w - u), f = alpha + lam.u - 2 w.lam
 // (implicit.py:149, objective.py:53-54).  out = [f ; g_lam ; g_A].
-__global__ void k_tail_vec(const double* __restrict__ x, const double* __restrict__ Yw,
+__global__ void k_tail_vec(const double* __restrict__ x, const double* __restrict__ w,
                            const double* __restrict__ G, const double* __restrict__ C, int n, int r,
                            const double* __restrict__ alpha_dev, double alpha_host,
                            double* __restrict__ out) {
   extern __shared__ double s_u[];
   const double* lam = x;
-  const double* w = Yw + (int64_t)n * r;
   for (int j = threadIdx.x; j < r; j += blockDim.x) {
     double u = 0.0;
     for (int k = 0; k < r; ++k) u += (G[(int64_t)j * r + k] * C[(int64_t)j * r + k]) * lam[k];
@@ -119,7 +118,7 @@ __global__ void k_tail_vec(const double* __restrict__ x, const double* __restric
 }
 
 // K4c: g_A = -2d (Y - (A o lam) C) o lam (objective.py:55), column-major into out + 1 + r.
-__global__ void k_tail_ga(const double* __restrict__ x, const double* __restrict__ Yw,
+__global__ void k_tail_ga(const double* __restrict__ x, const double* __restrict__ Y,
                           const double* __restrict__ C, int n, int r, int d,
                           double* __restrict__ out) {
   const double* lam = x;
@@ -131,7 +130,7 @@ __global__ void k_tail_ga(const double* __restrict__ x, const double* __restrict
     const int j = idx / n, i = idx % n;
     double m = 0.0;
     for (int k = 0; k < r; ++k) m += (A[(int64_t)k * n + i] * lam[k]) * C[(int64_t)k * r + j];
-    out[1 + r + idx] = (s * (Yw[idx] - m)) * lam[j];
+    out[1 + r + idx] = (s * (Y[idx] - m)) * lam[j];
   }
 }
 
@@ -142,14 +141,14 @@ constexpr int K4S_THREADS = 512;
 constexpr int K4S_MAX_NR = 4096;
 constexpr int K4S_MAX_R = 32;
 __global__ void __launch_bounds__(K4S_THREADS)
-    k_tail_fused(const double* __restrict__ x, const double* __restrict__ Yw, int n, int r, int d,
+    k_tail_fused(const double* __restrict__ x, const double* __restrict__ Y,
+                 const double* __restrict__ w, int n, int r, int d,
                  const double* __restrict__ alpha_dev, double alpha_host,
                  double* __restrict__ out) {
   __shared__ double sA[K4S_MAX_NR];
   __shared__ double sC[K4S_MAX_R * K4S_MAX_R];
   __shared__ double sU[K4S_MAX_R];
   const double* lam = x;
-  const double* w = Yw + (int64_t)n * r;
   for (int e = threadIdx.x; e < n * r; e += blockDim.x) sA[e] = x[r + e];
   __syncthreads();
   // G_jk = a_j . a_k: one warp per (j, k), lanes stride over i, fixed shuffle order
@@ -187,7 +186,7 @@ __global__ void __launch_bounds__(K4S_THREADS)
     const int j = e / n, i = e % n;
     double m = 0.0;
     for (int k = 0; k < r; ++k) m += (sA[k * n + i] * lam[k]) * sC[k * r + j];
-    out[1 + r + e] = (s2d * (Yw[e] - m)) * lam[j];
+    out[1 + r + e] = (s2d * (Y[e] - m)) * lam[j];
   }
 }
 

@@ -51,3 +51,26 @@ def packed_fg_implicit(obs: ObservationSet, d: int, r: int, alpha: float = 0.0, 
         return ctx.fg_packed(x, n, d, r, alpha, mode)
 
     return fg
+
+
+def packed_fg_implicit_batched(obs: ObservationSet, d: int, r: int, alpha: float = 0.0, *,
+                               mode: str | None = None):
+    """fg over a batch of packed points X (k x (r + n r)) -> (f[k], G[k x (r + n r)]).
+
+    The k starts share one pass over V (batched multistart); each row equals
+    ``packed_fg_implicit(obs, d, r, alpha)(X[s])`` up to fp64 reassociation of the column blocks.
+    """
+    n = obs.n
+    if d < 2:
+        raise ValueError(f"order must be >= 2, got {d}")
+    ctx = obs.device_context()
+
+    def fg(X: np.ndarray):
+        X = np.asarray(X, dtype=float)
+        if X.ndim != 2 or X.shape[1] != r + n * r:
+            raise ValueError(f"expected a (k, {r + n * r}) batch, got {X.shape}")
+        if not np.isfinite(X).all():
+            raise ValueError("model variables and alpha must be finite")
+        return ctx.fg_batch(X, n, d, r, alpha, mode)
+
+    return fg

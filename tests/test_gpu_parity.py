@@ -310,3 +310,24 @@ def test_fast_mode_zero_weights_and_determinism():
     a = mcp.fg_implicit(obs, lam, A, 3, mode="tf32x3")
     b = mcp.fg_implicit(obs, lam, A, 3, mode="tf32x3")
     assert a.f == b.f and np.array_equal(a.g_A, b.g_A)
+
+
+# ----------------------------- batched multistart -----------------------------
+@pytest.mark.parametrize("n,p,r,d,k", [(20, 3000, 5, 3, 4), (100, 20000, 10, 4, 8), (7, 50, 3, 2, 3)])
+def test_batched_matches_single_starts(n, p, r, d, k):
+    rng = np.random.default_rng(n + k)
+    V = rng.standard_normal((n, p))
+    obs = mcp.ObservationSet(V)
+    X = np.stack([mcp.pack(rng.standard_normal(r), rng.standard_normal((n, r)))
+                  for _ in range(k)])
+    F, G = mcp.packed_fg_implicit_batched(obs, d, r, alpha=0.5)(X)
+    fg1 = mcp.packed_fg_implicit(obs, d, r, alpha=0.5)
+    nu = np.full(p, 1.0 / p)
+    for s in range(k):
+        f1, g1 = fg1(X[s])
+        lam, A = mcp.unpack(X[s], n, r)
+        f_s, gl_s, gA_s, _ = om.term_scales(V, nu, lam, A, d, 0.5)
+        scale = np.concatenate([gl_s, gA_s.ravel(order="F")])
+        assert _err(F[s], f1, f_s) <= 1e-13 and _err(G[s], g1, scale) <= 1e-13
+        fo, go = om.packed_fg(V, nu, d, r, 0.5)(X[s])
+        assert _err(F[s], fo, f_s) <= FG_TOL and _err(G[s], go, scale) <= FG_TOL

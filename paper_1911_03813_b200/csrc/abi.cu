@@ -931,11 +931,19 @@ int mcp_fg_batch(mcp_ctx* c, int d, int r, int k, const double* X, double alpha,
   const double* dY = (const double*)c->dYw.p;
   const double* dW = dY + n * R;
   const double* dXs = dx + R + n * R + 1;
-  for (int sidx = 0; sidx < k; ++sidx) {
-    if ((rc = enqueue_finish_yw(c, d, r, dXs + (size_t)sidx * rows, dY + (size_t)sidx * n * r,
-                                dW + (size_t)sidx * r, dx + R + n * R, 0.0,
-                                (double*)c->dout.p + (size_t)sidx * (1 + rows), c->stream)))
-      return rc;
+  if (n * r <= K4S_MAX_NR && r <= K4S_MAX_R) {
+    // all k tails in one launch, one CTA per start
+    k_tail_fused<<<k, K4S_THREADS, 0, c->stream>>>(dXs, dY, dW, (int)n, r, d, dx + R + n * R, 0.0,
+                                                   (double*)c->dout.p, rows, n * r, r, 1 + rows);
+    CUDA_TRY(c, cudaGetLastError());
+    c->last_launches = 1;
+  } else {
+    for (int sidx = 0; sidx < k; ++sidx) {
+      if ((rc = enqueue_finish_yw(c, d, r, dXs + (size_t)sidx * rows, dY + (size_t)sidx * n * r,
+                                  dW + (size_t)sidx * r, dx + R + n * R, 0.0,
+                                  (double*)c->dout.p + (size_t)sidx * (1 + rows), c->stream)))
+        return rc;
+    }
   }
   c->last_launches += launches;
   CUDA_TRY(c, cudaMemcpyAsync(c->hout, c->dout.p, xout, cudaMemcpyDeviceToHost, c->stream));

@@ -95,14 +95,14 @@ constexpr int kEntriesS = sizeof(kTableS) / sizeof(kTableS[0]);
 std::atomic<bool> g_attr_s[kEntriesS];
 
 bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
-  if (n > 128 || r > 16) return false;
+  if (n > 128) return false;
   const int MT = (int)ceil_div(n, 8);
   const int kst = (int)(ldv / 4);
   const int mth_need = (MT + 1) / 2, kh_need = kst;
   int ntm, tail;
   if (r <= 8) { ntm = 1; tail = 0; }
   else if (r <= 10 && !getenv("MCP_K1S_NO_TAIL")) { ntm = 1; tail = r - 8; }
-  else { ntm = 2; tail = 0; }
+  else { ntm = 2; tail = 0; }          // r > 16: several 16-column blocks, one per CTA
   int e = -1;
   for (int i = 0; i < kEntriesS && e < 0; ++i)
     if (kTableS[i].NTM == ntm && kTableS[i].TAIL == tail && kTableS[i].MTH >= mth_need &&
@@ -158,19 +158,23 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
   v.MT = MT;
   v.n_chunks = 0;
   v.n_pad = MT * 8;
-  v.rbs = 1;
+  v.rbs = (int)ceil_div(r, cw);
   v.num_tiles = p_pad / K1S_SR;
-  int64_t gp = sms;
-  if (gp > v.num_tiles) gp = v.num_tiles;
+  int64_t G = sms;
+  if (G < v.rbs) G = v.rbs;
+  G -= G % v.rbs;
+  int64_t gp = G / v.rbs;
+  if (gp > v.num_tiles / spc) gp = v.num_tiles / spc;
+  if (gp < 1) gp = 1;
   v.gp = (int)gp;
-  v.grid = v.gp;
+  v.grid = v.gp * v.rbs;
   v.stages = S;
   v.MTW2 = spc;
   v.smem = smem;
   v.entry = e;
   v.afrag_elems = 0;
-  v.ypart_elems = (size_t)v.gp * v.n_pad * cw;
-  v.wpart_elems = (size_t)v.gp * cw;
+  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * cw;
+  v.wpart_elems = (size_t)v.rbs * v.gp * cw;
   v.name = "k1s_fg_stream<f64,DMMA=" + std::to_string(8 * ntm) + ",DFMA=" +
            std::to_string(tail) + ",MTH=" + std::to_string(mtm) + ",KH=" +
            std::to_string(kTableS[e].KH) + ",S=" + std::to_string(S) + ">";
@@ -260,7 +264,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     sp.A = A;
     sp.r = r;
     sp.d = d;
-    sp.rbs = 1;
+    sp.rbs = v.rbs;
     sp.gp = v.gp;
     sp.stages = v.stages;
     sp.spc = v.MTW2;

@@ -144,7 +144,13 @@ __global__ void __launch_bounds__(K4S_THREADS)
     k_tail_fused(const double* __restrict__ x, const double* __restrict__ Y,
                  const double* __restrict__ w, int n, int r, int d,
                  const double* __restrict__ alpha_dev, double alpha_host,
-                 double* __restrict__ out) {
+                 double* __restrict__ out, int64_t sx = 0, int64_t sy = 0, int64_t sw = 0,
+                 int64_t so = 0) {
+  // batched launches: CTA b handles start b (strides between consecutive starts' buffers)
+  x += blockIdx.x * sx;
+  Y += blockIdx.x * sy;
+  w += blockIdx.x * sw;
+  out += blockIdx.x * so;
   __shared__ double sA[K4S_MAX_NR];
   __shared__ double sC[K4S_MAX_R * K4S_MAX_R];
   __shared__ double sU[K4S_MAX_R];

@@ -20,6 +20,7 @@ from .implicit import (
     model_data_inner,
     ttsv_batch,
 )
+from .io import ParseError, read_observations_binary, write_observations_binary
 from .objective import FgResult, fg_implicit
 from .optimize import FgCallback, pack, packed_fg_implicit, packed_fg_implicit_batched, unpack
 
@@ -28,6 +29,7 @@ __all__ = [
     "FgResult",
     "GramCache",
     "ObservationSet",
+    "ParseError",
     "SymKruskal",
     "build_gram_cache",
     "data_norm_sq",
@@ -35,8 +37,10 @@ __all__ = [
     "kruskal_norm_sq",
     "model_data_inner",
     "pack",
+    "read_observations_binary",
     "packed_fg_implicit",
     "packed_fg_implicit_batched",
     "ttsv_batch",
     "unpack",
+    "write_observations_binary",
 ]

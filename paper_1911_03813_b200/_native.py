@@ -165,10 +165,13 @@ class Context:
     def load_obs_host(self, V: np.ndarray, layout: int, nu: np.ndarray | None, nu_const: float):
         if V.dtype == np.float32:
             dt = MCP_F32
+        elif V.dtype == np.float64 and V.dtype.byteorder in ("=", "<", "|"):
+            dt = MCP_F64
         else:
             V = np.ascontiguousarray(V, dtype=np.float64)
             dt = MCP_F64
-        V = np.ascontiguousarray(V)
+        if not (isinstance(V, np.memmap) and V.flags.c_contiguous):
+            V = np.ascontiguousarray(V)
         if layout == MCP_VAR_MAJOR:
             n, p = V.shape
             ld = p

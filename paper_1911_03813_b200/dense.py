@@ -49,6 +49,7 @@ class ObservationSet:
         self._dev = None
         self._dev_lock = threading.Lock()
         self._dev_obs = None  # (torch tensor, ...) when constructed from device memory
+        self._host_obs = None  # (p x n) host array when constructed observation-major
 
     @classmethod
     def from_device(cls, V_obs_major, nu=None, labels=None, *, p_total: int | None = None):
@@ -83,6 +84,35 @@ class ObservationSet:
         self._dev_obs = V_obs_major.contiguous()
         return self
 
+    @classmethod
+    def from_obs_major_host(cls, V_pn, nu=None, labels=None, *, p_total: int | None = None,
+                            device: int | None = None):
+        """Wrap a host (p x n) observation-major array (e.g. a memory-mapped MOMV payload).
+
+        Nothing is copied or validated on the host: the upload copies the rows into HBM and
+        checks finiteness on the device (ValueError on failure, like dense.py:87-88).
+        """
+        V_pn = np.asarray(V_pn) if not isinstance(V_pn, np.memmap) else V_pn
+        if V_pn.ndim != 2:
+            raise ValueError(f"V must be a 2-D matrix, got ndim={V_pn.ndim}")
+        p, n = V_pn.shape
+        if n < 1 or p < 1:
+            raise ValueError(f"V must be at least 1x1, got shape {(n, p)}")
+        self = cls.__new__(cls)
+        self._Vsrc = None
+        self._V64 = None
+        self._host_obs = V_pn
+        self._n, self._p = int(n), int(p)
+        self._uniform_default = nu is None
+        self.nu = _check_nu(nu, p) if nu is not None else None
+        self._nu_const = 1.0 / float(p_total if p_total is not None else p)
+        self.labels = _check_labels(labels, p)
+        self._device = device
+        self._dev = None
+        self._dev_lock = threading.Lock()
+        self._dev_obs = None
+        return self
+
     # -- reference surface ----------------------------------------------------------------
     @property
     def V(self) -> np.ndarray:
@@ -90,6 +120,8 @@ class ObservationSet:
         if self._V64 is None:
             if self._Vsrc is not None:
                 self._V64 = np.asarray(self._Vsrc, dtype=float)
+            elif getattr(self, "_host_obs", None) is not None:
+                self._V64 = np.asarray(self._host_obs, dtype=float).T
             else:
                 self._V64 = self._dev_obs.double().t().cpu().numpy()
         return self._V64
@@ -133,6 +165,9 @@ class ObservationSet:
                         nu_ptr = self._nu_dev.data_ptr()
                     ctx.load_obs_device(t.data_ptr(), code, _native.MCP_OBS_MAJOR, self._n,
                                         self._p, t.stride(0), nu_ptr, self._nu_const)
+                elif getattr(self, "_host_obs", None) is not None:
+                    nu = None if self._uniform_default else self.nu
+                    ctx.load_obs_host(self._host_obs, _native.MCP_OBS_MAJOR, nu, self._nu_const)
                 else:
                     nu = None if self._uniform_default else self.nu
                     ctx.load_obs_host(self._Vsrc, _native.MCP_VAR_MAJOR, nu, 1.0 / self._p)

@@ -140,6 +140,30 @@ int mcp_fg_device(mcp_ctx* ctx, int d, int r, const double* dx, double alpha, in
 int mcp_set_kernel_timing(mcp_ctx* ctx, int enable);
 int mcp_kernel_time_ms(mcp_ctx* ctx, double* total_ms, int* launches, int reset);
 
+/*
+ * Device-resident L-BFGS replacing lbfgs_minimize / two_loop_direction /
+ * _wolfe_line_search (reference pkg/src/momentcp/optimize.py:149-355) for the objective
+ * x -> fg(x) of the loaded observation set.  x, g, the direction and the (s, y) history stay in
+ * HBM; the two-loop recursion, trial points and step bookkeeping run as kernels, and the host
+ * only receives the handful of scalars the line-search decisions need (one graph launch + one
+ * sync per function evaluation).  Decisions follow the reference in the same order; dot products
+ * are fixed-order device reductions (deterministic, not numpy's summation order).
+ *   x0 (host, r + n r)            starting point, packed as in mcp_fg_packed
+ *   opts[7] = {memory, pgtol, max_iters, max_total_iters, c1 (sufficient decrease),
+ *              c2 (curvature), max_line_steps}   (OptConfig, optimize.py:31-48)
+ *   x_out, g_out (host, r + n r)  final iterate and its gradient; f_out its objective
+ *   trace_f / trace_t (host, trace_cap)  f and seconds-since-start at x0 and every accepted step
+ *   info[4] = {n_fg, n_steps, reason (0 tolerance, 1 iteration cap, 2 line-search failure),
+ *              trace rows written}
+ *   hook (may be NULL): called with a host copy of every accepted iterate (and x0).
+ * MCP_ERR_ARG with "objective is not finite at the starting point" when fg(x0) is not finite.
+ */
+typedef void (*mcp_iterate_hook)(const double* x, int64_t len, void* user);
+int mcp_lbfgs(mcp_ctx* ctx, int d, int r, double alpha, int mode, const double* x0,
+              const double* opts, double* x_out, double* g_out, double* f_out, double* trace_f,
+              double* trace_t, int64_t trace_cap, int64_t* info, mcp_iterate_hook hook,
+              void* hook_user);
+
 /* Kernel launches issued by the last evaluation call (for the bench's gpu_launches claim). */
 int mcp_last_launch_count(const mcp_ctx* ctx);
 

@@ -22,13 +22,16 @@ from .implicit import (
 )
 from .io import ParseError, read_observations_binary, write_observations_binary
 from .objective import FgResult, fg_implicit
-from .optimize import FgCallback, pack, packed_fg_implicit, packed_fg_implicit_batched, unpack
+from .optimize import (FgCallback, OptConfig, RunReport, lbfgs_minimize, pack, packed_fg_implicit,
+                       packed_fg_implicit_batched, unpack)
 
 __all__ = [
     "FgCallback",
     "FgResult",
     "GramCache",
     "ObservationSet",
+    "OptConfig",
+    "RunReport",
     "ParseError",
     "SymKruskal",
     "build_gram_cache",
@@ -36,6 +39,7 @@ __all__ = [
     "fg_implicit",
     "kruskal_norm_sq",
     "model_data_inner",
+    "lbfgs_minimize",
     "pack",
     "read_observations_binary",
     "packed_fg_implicit",

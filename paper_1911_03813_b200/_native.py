@@ -28,6 +28,9 @@ MODES = {"fp64": 0, "tf32x3": 1}
 _c_void_p = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _dp = ctypes.POINTER(ctypes.c_double)
+# void (*)(const double* x, int64_t len, void* user)  (mcp_iterate_hook)
+IterateHook = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
+
 SIGNATURES = {
     "mcp_abi_version": (ctypes.c_int, []),
     "mcp_last_error": (ctypes.c_char_p, [_c_void_p]),
@@ -59,6 +62,9 @@ SIGNATURES = {
     "mcp_set_kernel_timing": (ctypes.c_int, [_c_void_p, ctypes.c_int]),
     "mcp_kernel_time_ms": (ctypes.c_int, [_c_void_p, _dp, ctypes.POINTER(ctypes.c_int),
                                           ctypes.c_int]),
+    "mcp_lbfgs": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                 ctypes.c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _dp,
+                                 _c_void_p, _c_void_p, _i64, _c_void_p, IterateHook, _c_void_p]),
     "mcp_last_launch_count": (ctypes.c_int, [_c_void_p]),
     "mcp_last_variant": (ctypes.c_char_p, [_c_void_p]),
 }
@@ -222,6 +228,44 @@ class Context:
                                     mode_code(mode), _ptr(F), _ptr(G))
         self._check(rc, "mcp_fg_batch")
         return F, G
+
+    def lbfgs(self, x0: np.ndarray, n: int, d: int, r: int, alpha: float, mode: str | None,
+              opts, hook=None) -> dict:
+        """Device-resident L-BFGS (mcp_lbfgs); opts = (memory, pgtol, max_iters,
+        max_total_iters, c1, c2, max_line_steps)."""
+        N = r + n * r
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        if x0.shape != (N,):
+            raise ValueError(f"expected packed length {N}, got {x0.shape}")
+        o = np.array([float(v) for v in opts], dtype=np.float64)
+        cap = int(min(o[2], o[3])) + 1
+        x = np.empty(N)
+        g = np.empty(N)
+        tf = np.empty(cap)
+        tt = np.empty(cap)
+        info = np.zeros(4, dtype=np.int64)
+        f = ctypes.c_double()
+        err: list[BaseException] = []
+
+        def _hook(xp, length, _user):
+            if err:
+                return
+            try:
+                hook(np.ctypeslib.as_array(xp, shape=(length,)).copy())
+            except BaseException as exc:  # re-raised after the native call returns
+                err.append(exc)
+
+        cb = IterateHook(_hook) if hook is not None else IterateHook()
+        rc = self._lib.mcp_lbfgs(self._h, int(d), int(r), float(alpha), mode_code(mode), _ptr(x0),
+                                 _ptr(o), _ptr(x), _ptr(g), ctypes.byref(f), _ptr(tf), _ptr(tt),
+                                 cap, _ptr(info), cb, None)
+        if err:
+            raise err[0]
+        self._check(rc, "mcp_lbfgs")
+        k = int(info[3])
+        return {"x": x, "g": g, "f": f.value, "n_fg": int(info[0]), "n_steps": int(info[1]),
+                "reason": ("tolerance", "iteration cap", "line-search failure")[int(info[2])],
+                "trace": list(zip(tf[:k].tolist(), tt[:k].tolist()))}
 
     def ttsv_batch(self, A_fortran: np.ndarray, d: int, mode: str | None) -> np.ndarray:
         n, r = A_fortran.shape

@@ -22,6 +22,7 @@
 #include "k_aux.cuh"
 #include "k1_dispatch.h"
 #include "k1t_tf32.cuh"
+#include "ctx.h"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -31,16 +32,6 @@ using namespace mcp;
 namespace {
 
 thread_local std::string g_create_error;
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
-
-struct GraphEntry {
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-};
 
 // Transpose a variable-major n x ld source (row i = variable) into the observation-major
 // p_pad x ldv device layout, zero padding included (dst pre-zeroed).
@@ -79,58 +70,7 @@ __global__ void k_check_nu(const double* __restrict__ nu, int64_t p, unsigned lo
 
 }  // namespace
 
-struct mcp_ctx {
-  int device = 0;
-  int sms = 0;
-  cudaStream_t stream = nullptr;
-  mutable std::mutex mu;
-  std::string err;
-
-  bool loaded = false;
-  int dtype = MCP_F64;
-  int64_t n = 0, p = 0, p_pad = 0, ldv = 0;
-  void* dV = nullptr;
-  double* dnu = nullptr;  // nullptr => uniform nu_const
-  double nu_const = 0.0;
-
-  DevBuf dx, dout, dYw, dAfrag, dYpart, dwpart, dG, dC, dpart, dscalar, dflag;
-  void* hx = nullptr;
-  size_t hx_bytes = 0;
-  void* hout = nullptr;
-  size_t hout_bytes = 0;
-
-  // fast mode (tcgen05 TF32): fp32 copy of V when the set is fp64, tensor maps, prepared A^T
-  float* dV32 = nullptr;       // == dV when dtype is fp32
-  bool own_v32 = false;
-  int64_t ldv32 = 0;
-  bool tm_v_ready = false;
-  CUtensorMap tm_v1, tm_v2, tm_a;
-  void* tm_a_addr = nullptr;
-  int tm_a_rows = 0, tm_a_kpad = 0, tm_a_rb = 0;
-  DevBuf dAt;
-
-  std::map<std::tuple<int, int, int>, GraphEntry> graphs;
-  bool timing = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
-  int last_launches = 0;
-  std::string variant = "none";
-
-  int fail(int code, const std::string& msg) {
-    err = msg;
-    return code;
-  }
-};
-
-#define CUDA_TRY(ctx, expr)                                                               \
-  do {                                                                                    \
-    cudaError_t _e = (expr);                                                              \
-    if (_e != cudaSuccess) {                                                              \
-      (void)cudaGetLastError();                                                           \
-      return (ctx)->fail(MCP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
-    }                                                                                     \
-  } while (0)
-
-namespace {
+namespace mcp_internal {
 
 void drop_graphs(mcp_ctx* c) {
   for (auto& kv : c->graphs) {
@@ -138,6 +78,10 @@ void drop_graphs(mcp_ctx* c) {
     if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
   }
   c->graphs.clear();
+  if (c->lbfgs_ws) {
+    c->lbfgs_ws_free(c->lbfgs_ws);
+    c->lbfgs_ws = nullptr;
+  }
 }
 
 // Event pair bracketing one timed kernel launch (only when timing is on and not capturing).
@@ -185,28 +129,6 @@ int ensure_host(mcp_ctx* c, void*& p, size_t& have, size_t bytes) {
   have = bytes;
   return MCP_OK;
 }
-
-inline int grid_for(int64_t total, int threads, int cap) {
-  int64_t b = (total + threads - 1) / threads;
-  if (b < 1) b = 1;
-  if (b > cap) b = cap;
-  return (int)b;
-}
-
-// Shape of the fast-mode (K1T) launch.
-struct K1TPlan {
-  int RB = 0, rbs = 0, gp = 0, stages = 0, nkb = 0, mt2 = 0, r_pad = 0, kpad = 0;
-  int64_t num_tiles = 0;
-  size_t smem = 0;
-};
-
-// Shape of one evaluation's K1 launch.
-struct EvalPlan {
-  K1Variant k1;
-  K1TPlan t;
-  int mode = MCP_MODE_FP64;
-  int d = 0, r = 0;
-};
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -600,13 +522,9 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   return MCP_OK;
 }
 
-struct Guard {
-  mcp_ctx* c;
-  std::unique_lock<std::mutex> lk;
-  explicit Guard(mcp_ctx* ctx) : c(ctx), lk(ctx->mu) { cudaSetDevice(ctx->device); }
-};
+}  // namespace mcp_internal
 
-}  // namespace
+using namespace mcp_internal;
 
 extern "C" {
 

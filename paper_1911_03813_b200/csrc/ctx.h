@@ -1,0 +1,130 @@
+// Internal view of a momentcp context shared by the C-ABI translation units (abi.cu, lbfgs.cu).
+// Not part of the public ABI (include/momentcp_b200.h): the struct layout may change freely.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "momentcp_b200.h"
+#include "k1_dispatch.h"
+
+namespace mcp_internal {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct GraphEntry {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+}  // namespace mcp_internal
+
+struct mcp_ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  mutable std::mutex mu;
+  std::string err;
+
+  bool loaded = false;
+  int dtype = MCP_F64;
+  int64_t n = 0, p = 0, p_pad = 0, ldv = 0;
+  void* dV = nullptr;
+  double* dnu = nullptr;  // nullptr => uniform nu_const
+  double nu_const = 0.0;
+
+  mcp_internal::DevBuf dx, dout, dYw, dAfrag, dYpart, dwpart, dG, dC, dpart, dscalar, dflag;
+  void* hx = nullptr;
+  size_t hx_bytes = 0;
+  void* hout = nullptr;
+  size_t hout_bytes = 0;
+
+  // fast mode (tcgen05 TF32): fp32 copy of V when the set is fp64, tensor maps, prepared A^T
+  float* dV32 = nullptr;       // == dV when dtype is fp32
+  bool own_v32 = false;
+  int64_t ldv32 = 0;
+  bool tm_v_ready = false;
+  CUtensorMap tm_v1, tm_v2, tm_a;
+  void* tm_a_addr = nullptr;
+  int tm_a_rows = 0, tm_a_kpad = 0, tm_a_rb = 0;
+  mcp_internal::DevBuf dAt;
+
+  std::map<std::tuple<int, int, int>, mcp_internal::GraphEntry> graphs;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
+  int last_launches = 0;
+  std::string variant = "none";
+
+  // cached device-resident L-BFGS workspace (lbfgs.cu); freed with the graphs
+  void* lbfgs_ws = nullptr;
+  void (*lbfgs_ws_free)(void*) = nullptr;
+
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+};
+
+#define CUDA_TRY(ctx, expr)                                                               \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      (void)cudaGetLastError();                                                           \
+      return (ctx)->fail(MCP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    }                                                                                     \
+  } while (0)
+
+namespace mcp_internal {
+
+// Shape of the fast-mode (K1T) launch.
+struct K1TPlan {
+  int RB = 0, rbs = 0, gp = 0, stages = 0, nkb = 0, mt2 = 0, r_pad = 0, kpad = 0;
+  int64_t num_tiles = 0;
+  size_t smem = 0;
+};
+
+// Shape of one evaluation's K1 launch.
+struct EvalPlan {
+  mcp::K1Variant k1;
+  K1TPlan t;
+  int mode = MCP_MODE_FP64;
+  int d = 0, r = 0;
+};
+
+struct Guard {
+  mcp_ctx* c;
+  std::unique_lock<std::mutex> lk;
+  explicit Guard(mcp_ctx* ctx) : c(ctx), lk(ctx->mu) { cudaSetDevice(ctx->device); }
+};
+
+
+void drop_graphs(mcp_ctx* c);
+int ensure(mcp_ctx* c, DevBuf& b, size_t bytes);
+int ensure_host(mcp_ctx* c, void*& p, size_t& have, size_t bytes);
+int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl);
+// prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows (stream-ordered, capturable)
+int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
+                    cudaStream_t s);
+// K4 : out = [f ; g_lam ; vec_F(g_A)] from x = [lam ; vec_F(A)] and [Y ; w]
+int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
+                   const double* alpha_dev, double alpha, double* dout, cudaStream_t s);
+
+inline int grid_for(int64_t total, int threads, int cap) {
+  int64_t b = (total + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+}  // namespace mcp_internal

@@ -8,6 +8,7 @@ is one C-ABI call (``mcp_fg_packed``): H2D of x, one CUDA-graph replay, D2H of [
 
 from __future__ import annotations
 
+from dataclasses import dataclass, field
 from typing import Callable
 
 import numpy as np
@@ -15,6 +16,45 @@ import numpy as np
 from .dense import ObservationSet
 
 FgCallback = Callable[[np.ndarray], tuple[float, np.ndarray]]
+
+
+@dataclass
+class OptConfig:
+    """L-BFGS settings (reference optimize.py:31-48, same defaults and checks)."""
+
+    memory: int = 5
+    pgtol: float = 1e-4
+    max_iters: int = 10_000
+    max_total_iters: int = 50_000
+    sufficient_decrease: float = 1e-4
+    curvature: float = 0.9
+    max_line_steps: int = 20
+    seed: int = 0
+
+    def __post_init__(self) -> None:
+        if self.pgtol <= 0:
+            raise ValueError(f"pgtol must be > 0, got {self.pgtol}")
+        if self.memory < 1:
+            raise ValueError(f"memory must be >= 1, got {self.memory}")
+
+
+@dataclass
+class RunReport:
+    """Outcome of one optimization run (reference optimize.py:78-101)."""
+
+    lam: np.ndarray
+    A: np.ndarray
+    f: float
+    grad_inf_norm: float
+    n_fg: int
+    n_steps: int
+    wall_time: float
+    reason: str
+    seed: int | None = None
+    trace: list[tuple[float, float]] = field(default_factory=list)
+    run_index: int | None = None
+    runs: list["RunReport"] | None = None
+    failures: list[str] = field(default_factory=list)
 
 
 def pack(lam, A) -> np.ndarray:
@@ -50,7 +90,46 @@ def packed_fg_implicit(obs: ObservationSet, d: int, r: int, alpha: float = 0.0, 
             raise ValueError("model variables and alpha must be finite")
         return ctx.fg_packed(x, n, d, r, alpha, mode)
 
+    fg.device_problem = (obs, int(d), int(r), float(alpha), mode)  # read by lbfgs_minimize
     return fg
+
+
+def lbfgs_minimize(fg: FgCallback, x0: np.ndarray, cfg: OptConfig,
+                   shape: tuple[int, int] | None = None,
+                   iterate_hook: Callable[[np.ndarray], None] | None = None) -> RunReport:
+    """L-BFGS with strong-Wolfe line search, run device-resident (reference optimize.py:255-355).
+
+    ``fg`` must come from :func:`packed_fg_implicit`: the whole solve (two-loop recursion,
+    trial points, (s, y) history, every f+grad) runs on the GPU through ``mcp_lbfgs`` and the
+    host only steers the line search on scalars.  Stopping rules, step logic and the report
+    match the reference; ``trace`` rows are ``(f, seconds since start)``.
+    """
+    import time
+
+    problem = getattr(fg, "device_problem", None)
+    if problem is None:
+        raise TypeError("lbfgs_minimize runs on the device: pass the fg returned by "
+                        "packed_fg_implicit(obs, d, r, alpha)")
+    obs, d, r, alpha, mode = problem
+    start = time.perf_counter()
+    x0 = np.asarray(x0, dtype=float)
+    if x0.shape != (r + obs.n * r,):
+        raise ValueError(f"expected packed length {r + obs.n * r}, got {x0.shape}")
+    if not np.isfinite(x0).all():
+        raise ValueError("model variables and alpha must be finite")
+    ctx = obs.device_context()
+    opts = (cfg.memory, cfg.pgtol, cfg.max_iters, cfg.max_total_iters, cfg.sufficient_decrease,
+            cfg.curvature, cfg.max_line_steps)
+    out = ctx.lbfgs(x0, obs.n, d, r, alpha, mode, opts, iterate_hook)
+    x = out["x"]
+    if shape is None:
+        lam, A = x.copy(), np.empty((0, 0))
+    else:
+        lam, A = unpack(x, *shape)
+    return RunReport(lam=lam, A=A, f=out["f"], grad_inf_norm=float(np.abs(out["g"]).max()),
+                     n_fg=out["n_fg"], n_steps=out["n_steps"],
+                     wall_time=time.perf_counter() - start, reason=out["reason"], seed=cfg.seed,
+                     trace=out["trace"])
 
 
 def packed_fg_implicit_batched(obs: ObservationSet, d: int, r: int, alpha: float = 0.0, *,

@@ -1,0 +1,110 @@
+"""Device-resident L-BFGS against the reference solver's decisions.
+
+Protocol (SURVEY.md 8c replay + Appendix A): the device solver takes the reference's decisions
+on scalars computed with a different dot-product summation order, so trajectories agree to
+rounding for the opening steps and drift chaotically later.  Checked here:
+  * the first 10 iterates match the reference's own trajectory (tests/golden/lbfgs_c1.npz,
+    produced by the unmodified reference lbfgs_minimize) to 1e-10;
+  * step-for-step agreement with the restated reference solver (oracle/lbfgs_oracle.py) driven by
+    the same GPU f+grad: identical evaluation counts per step and f within 1e-12 relative for
+    the first 20 steps;
+  * every trace value is bitwise the f+grad of the iterate reported with it;
+  * on a problem that converges, the same stopping reason and final f (1e-9) as the restated
+    reference;
+  * run-to-run bitwise determinism.
+"""
+
+import numpy as np
+import pytest
+
+import instances
+import paper_1911_03813_b200 as mcp
+from oracle import lbfgs_oracle as lo
+from oracle import momentcp_oracle as om
+
+pytestmark = pytest.mark.gpu
+
+
+def _c1():
+    cfg, V, lam, A = instances.config_instance("c1")
+    return cfg, mcp.ObservationSet(V), om.pack(lam, A)
+
+
+def test_device_lbfgs_follows_reference_trajectory(golden):
+    cfg, obs, x0 = _c1()
+    g = golden["lbfgs_c1"]
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+    its = []
+    rep = mcp.lbfgs_minimize(fg, x0, mcp.OptConfig(max_iters=100), shape=(cfg.n, cfg.r),
+                             iterate_hook=its.append)
+    assert rep.n_steps == 100 and rep.reason == "iteration cap"
+    assert len(its) == 101 and len(rep.trace) == 101
+    for k in range(10):
+        assert np.allclose(its[k], g["iterates"][k], rtol=1e-10, atol=1e-12), k
+    # trace values are the f of the reported iterates, bitwise
+    for k in (0, 1, 2, 50, 100):
+        assert fg(its[k])[0] == rep.trace[k][0], k
+    assert rep.f == rep.trace[-1][0]
+    lam, A = mcp.unpack(its[-1], cfg.n, cfg.r)
+    assert np.array_equal(lam, rep.lam) and np.array_equal(A, rep.A)
+    assert rep.grad_inf_norm == float(np.abs(fg(its[-1])[1]).max())
+
+
+def test_device_lbfgs_matches_restated_solver_step_for_step():
+    cfg, obs, x0 = _c1()
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+    counts = []
+
+    def counting(x):
+        counts.append(1)
+        return fg(x)
+
+    host_its, dev_its = [], []
+    host_n_fg = []
+    host = lo.lbfgs(counting, x0, max_iters=20,
+                    iterate_hook=lambda x: (host_its.append(x), host_n_fg.append(len(counts))))
+    dev = mcp.lbfgs_minimize(fg, x0, mcp.OptConfig(max_iters=20), iterate_hook=dev_its.append)
+    assert dev.n_steps == host["n_steps"] == 20
+    assert dev.n_fg == host["n_fg"]
+    for k in range(21):
+        assert abs(dev.trace[k][0] - host["trace"][k]) <= 1e-12 * abs(host["trace"][k]), k
+        assert np.allclose(dev_its[k], host_its[k], rtol=1e-9, atol=1e-12), k
+
+
+def test_device_lbfgs_converged_run_agrees():
+    # an exactly representable moment: V holds r points, so the fit converges to tolerance
+    rng = np.random.default_rng(7)
+    n, r, d = 6, 3, 3
+    V = rng.standard_normal((n, r))
+    V /= np.linalg.norm(V, axis=0)
+    obs = mcp.ObservationSet(V)
+    lam0 = np.full(r, 1.0 / r) * 0.8
+    A0 = V + 0.05 * rng.standard_normal((n, r))
+    x0 = om.pack(lam0, A0)
+    fg = mcp.packed_fg_implicit(obs, d, r)
+    cfg = mcp.OptConfig(pgtol=1e-8, max_iters=2000)
+    host = lo.lbfgs(fg, x0, pgtol=1e-8, max_iters=2000)
+    dev = mcp.lbfgs_minimize(fg, x0, cfg, shape=(n, r))
+    assert dev.reason == host["reason"] == "tolerance"
+    assert dev.grad_inf_norm <= 1e-8
+    assert abs(dev.f - host["f"]) <= 1e-9 * max(1.0, abs(host["f"]))
+    again = mcp.lbfgs_minimize(fg, x0, cfg, shape=(n, r))
+    assert again.f == dev.f and np.array_equal(again.A, dev.A) and again.n_fg == dev.n_fg
+
+
+def test_device_lbfgs_fast_mode_and_limits():
+    cfg, obs, x0 = _c1()
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r, mode="tf32x3")
+    rep = mcp.lbfgs_minimize(fg, x0, mcp.OptConfig(max_iters=30))
+    assert rep.n_steps == 30 and rep.trace[-1][0] < rep.trace[0][0]
+    # evaluation budget: stops with "iteration cap" once max_total_iters evaluations are spent
+    fg64 = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+    rep = mcp.lbfgs_minimize(fg64, x0, mcp.OptConfig(max_total_iters=7))
+    host = lo.lbfgs(fg64, x0, max_total_iters=7)
+    assert rep.reason == host["reason"] and rep.n_fg == host["n_fg"] and rep.n_steps == host["n_steps"]
+    # memory 1 and a large memory
+    for m in (1, 12):
+        rep = mcp.lbfgs_minimize(fg64, x0, mcp.OptConfig(memory=m, max_iters=15))
+        host = lo.lbfgs(fg64, x0, memory=m, max_iters=15)
+        assert rep.n_fg == host["n_fg"]
+        assert abs(rep.f - host["f"]) <= 1e-10 * abs(host["f"])

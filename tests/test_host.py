@@ -88,3 +88,14 @@ def test_synth_host_generation_is_deterministic():
     assert np.allclose(np.linalg.norm(A, axis=0), 1.0) and np.all(lam == 1.0 / cfg.r)
     c3 = synth.host_observations(synth.CONFIGS["c3"], 1, p=100)
     assert c3.dtype == np.float32 and c3.shape == (512, 100)
+
+
+def test_lbfgs_minimize_requires_device_objective():
+    import paper_1911_03813_b200 as mcp
+
+    with pytest.raises(TypeError):
+        mcp.lbfgs_minimize(lambda x: (0.0, x), np.zeros(3), mcp.OptConfig())
+    with pytest.raises(ValueError):
+        mcp.OptConfig(pgtol=0)
+    with pytest.raises(ValueError):
+        mcp.OptConfig(memory=0)

@@ -164,6 +164,30 @@ int mcp_lbfgs(mcp_ctx* ctx, int d, int r, double alpha, int mode, const double* 
               double* trace_t, int64_t trace_cap, int64_t* info, mcp_iterate_hook hook,
               void* hook_user);
 
+/*
+ * Stochastic path.
+ * mcp_gather_rows: rows idx[0..s) of the resident set -> dst (device, s rows of pitch ld_dst,
+ *   dst_dtype MCP_F64 or MCP_F32), i.e. the V[:, idx] of sample_observations
+ *   (pkg/src/momentcp/objective.py:97-113) without leaving HBM.
+ * mcp_adam: adam_minimize (pkg/src/momentcp/optimize.py:365-451) with x, m1, m2 and the
+ *   best iterate in HBM; every iteration gathers its mini-batch on the device and evaluates it
+ *   with uniform weights 1/batch.  Randomness stays with the caller: est_idx (n_est rows, the
+ *   fixed estimate subset) and, once per epoch, sample(idx, epoch_len * batch, user) fills that
+ *   epoch's row indices in draw order (return 0 on success).  The caller is responsible for the
+ *   uniform-weights precondition.
+ *   opts[8] = {step_size, reduced_step_size, epoch_len, batch, beta1, beta2, eps, max_epochs}
+ *   x_out / g_out: best iterate and its estimate gradient; f_out: best estimate
+ *   trace_f / trace_t: estimate at x0 and after every epoch, seconds since start
+ *   info[3] = {inner iterations, reason (0 iteration cap, 1 learning-rate exhausted), trace rows}
+ */
+typedef int (*mcp_sample_fn)(int64_t* idx, int64_t count, void* user);
+int mcp_gather_rows(mcp_ctx* ctx, const int64_t* idx, int64_t s, void* dst, int64_t ld_dst,
+                    int dst_dtype);
+int mcp_adam(mcp_ctx* ctx, int d, int r, int mode, const double* x0, const double* opts,
+             const int64_t* est_idx, int64_t n_est, mcp_sample_fn sample, void* user,
+             double* x_out, double* g_out, double* f_out, double* trace_f, double* trace_t,
+             int64_t trace_cap, int64_t* info);
+
 /* Kernel launches issued by the last evaluation call (for the bench's gpu_launches claim). */
 int mcp_last_launch_count(const mcp_ctx* ctx);
 

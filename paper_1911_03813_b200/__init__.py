@@ -21,11 +21,14 @@ from .implicit import (
     ttsv_batch,
 )
 from .io import ParseError, read_observations_binary, write_observations_binary
-from .objective import FgResult, fg_implicit
-from .optimize import (FgCallback, OptConfig, RunReport, lbfgs_minimize, pack, packed_fg_implicit,
-                       packed_fg_implicit_batched, unpack)
+from .objective import FgResult, fg_implicit, sample_observations
+from .optimize import (AdamConfig, FgCallback, OptConfig, RunReport, adam_minimize, lbfgs_minimize,
+                       pack, packed_fg_implicit, packed_fg_implicit_batched, unpack)
 
 __all__ = [
+    "AdamConfig",
+    "adam_minimize",
+    "sample_observations",
     "FgCallback",
     "FgResult",
     "GramCache",

@@ -31,6 +31,10 @@ _dp = ctypes.POINTER(ctypes.c_double)
 # void (*)(const double* x, int64_t len, void* user)  (mcp_iterate_hook)
 IterateHook = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
 
+# int (*)(int64_t* idx, int64_t count, void* user)  (mcp_sample_fn)
+SampleFn = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                            ctypes.c_void_p)
+
 SIGNATURES = {
     "mcp_abi_version": (ctypes.c_int, []),
     "mcp_last_error": (ctypes.c_char_p, [_c_void_p]),
@@ -65,6 +69,10 @@ SIGNATURES = {
     "mcp_lbfgs": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                  ctypes.c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _dp,
                                  _c_void_p, _c_void_p, _i64, _c_void_p, IterateHook, _c_void_p]),
+    "mcp_gather_rows": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, ctypes.c_int]),
+    "mcp_adam": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                _c_void_p, _c_void_p, _i64, SampleFn, _c_void_p, _c_void_p,
+                                _c_void_p, _dp, _c_void_p, _c_void_p, _i64, _c_void_p]),
     "mcp_last_launch_count": (ctypes.c_int, [_c_void_p]),
     "mcp_last_variant": (ctypes.c_char_p, [_c_void_p]),
 }
@@ -125,6 +133,7 @@ class Context:
             raise RuntimeError(f"mcp_create(device={device}) failed: {msg}")
         self._h = h
         self.device = int(device)
+        self.dtype_code = None  # set by the load calls
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -188,6 +197,7 @@ class Context:
         rc = self._lib.mcp_load_obs(self._h, _ptr(V), dt, layout, n, p, ld,
                                     None if nu_arr is None else _ptr(nu_arr), float(nu_const))
         self._check(rc, "mcp_load_obs")
+        self.dtype_code = dt
 
     def load_obs_device(self, V_ptr: int, dtype_code: int, layout: int, n: int, p: int, ld: int,
                         nu_ptr: int | None, nu_const: float):
@@ -196,6 +206,7 @@ class Context:
                                            None if nu_ptr is None else ctypes.c_void_p(nu_ptr),
                                            float(nu_const))
         self._check(rc, "mcp_load_obs_device")
+        self.dtype_code = int(dtype_code)
 
     # -- evaluations (host buffers) --------------------------------------------------------
     def fg_packed(self, x: np.ndarray, n: int, d: int, r: int, alpha: float, mode: str | None):
@@ -265,6 +276,48 @@ class Context:
         k = int(info[3])
         return {"x": x, "g": g, "f": f.value, "n_fg": int(info[0]), "n_steps": int(info[1]),
                 "reason": ("tolerance", "iteration cap", "line-search failure")[int(info[2])],
+                "trace": list(zip(tf[:k].tolist(), tt[:k].tolist()))}
+
+    def gather_rows(self, idx: np.ndarray, dst_ptr: int, ld: int, dtype_code: int) -> None:
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        rc = self._lib.mcp_gather_rows(self._h, _ptr(idx), int(idx.size), ctypes.c_void_p(dst_ptr),
+                                       int(ld), int(dtype_code))
+        self._check(rc, "mcp_gather_rows")
+
+    def adam(self, x0: np.ndarray, n: int, d: int, r: int, mode: str | None, opts,
+             est_idx: np.ndarray, sample) -> dict:
+        """Device-resident Adam (mcp_adam); sample(count) -> int64 indices for one epoch."""
+        N = r + n * r
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        o = np.array([float(v) for v in opts], dtype=np.float64)
+        est_idx = np.ascontiguousarray(est_idx, dtype=np.int64)
+        cap = int(o[7]) + 1
+        x = np.empty(N)
+        g = np.empty(N)
+        tf = np.empty(cap)
+        tt = np.empty(cap)
+        info = np.zeros(3, dtype=np.int64)
+        f = ctypes.c_double()
+        err: list[BaseException] = []
+
+        def _sample(buf, count, _user):
+            try:
+                np.ctypeslib.as_array(buf, shape=(count,))[:] = sample(int(count))
+                return 0
+            except BaseException as exc:  # re-raised after the native call returns
+                err.append(exc)
+                return 1
+
+        cb = SampleFn(_sample)
+        rc = self._lib.mcp_adam(self._h, int(d), int(r), mode_code(mode), _ptr(x0), _ptr(o),
+                                _ptr(est_idx), int(est_idx.size), cb, None, _ptr(x), _ptr(g),
+                                ctypes.byref(f), _ptr(tf), _ptr(tt), cap, _ptr(info))
+        if err:
+            raise err[0]
+        self._check(rc, "mcp_adam")
+        k = int(info[2])
+        return {"x": x, "g": g, "f": f.value, "n_iter": int(info[0]),
+                "reason": ("iteration cap", "learning-rate exhausted")[int(info[1])],
                 "trace": list(zip(tf[:k].tolist(), tt[:k].tolist()))}
 
     def ttsv_batch(self, A_fortran: np.ndarray, d: int, mode: str | None) -> np.ndarray:

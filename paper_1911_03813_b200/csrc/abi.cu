@@ -522,6 +522,50 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   return MCP_OK;
 }
 
+// Everything a context owns except V, nu and the stream (shared with views).
+void release_ctx(mcp_ctx* c) {
+  drop_graphs(c);
+  DevBuf* bufs[] = {&c->dx, &c->dout, &c->dYw, &c->dAfrag, &c->dYpart, &c->dwpart,
+                    &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag, &c->dAt};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (c->own_v32 && c->dV32) cudaFree(c->dV32);
+  c->dV32 = nullptr;
+  if (c->hx) cudaFreeHost(c->hx);
+  if (c->hout) cudaFreeHost(c->hout);
+  c->hx = c->hout = nullptr;
+  for (auto* v : {&c->timed, &c->event_pool})
+    for (auto& ev : *v) {
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+  c->timed.clear();
+  c->event_pool.clear();
+}
+
+mcp_ctx* make_view_ctx(const mcp_ctx* parent, void* dV, int dtype, int64_t p, int64_t ldv) {
+  mcp_ctx* v = new mcp_ctx();
+  v->device = parent->device;
+  v->sms = parent->sms;
+  v->stream = parent->stream;
+  v->dtype = dtype;
+  v->n = parent->n;
+  v->p = p;
+  v->p_pad = round_up(p, 3584);
+  v->ldv = ldv;
+  v->dV = dV;
+  v->dnu = nullptr;
+  v->nu_const = 1.0 / (double)p;
+  v->loaded = true;
+  return v;
+}
+
+void destroy_view_ctx(mcp_ctx* v) {
+  if (!v) return;
+  release_ctx(v);
+  delete v;
+}
+
 }  // namespace mcp_internal
 
 using namespace mcp_internal;
@@ -578,22 +622,9 @@ int mcp_destroy(mcp_ctx* c) {
   {
     Guard gd(c);
     cudaStreamSynchronize(c->stream);
-    drop_graphs(c);
-    DevBuf* bufs[] = {&c->dx, &c->dout, &c->dYw, &c->dAfrag, &c->dYpart, &c->dwpart,
-                      &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag};
-    for (DevBuf* b : bufs)
-      if (b->p) cudaFree(b->p);
-    if (c->own_v32 && c->dV32) cudaFree(c->dV32);
-    if (c->dAt.p) cudaFree(c->dAt.p);
+    release_ctx(c);
     if (c->dV) cudaFree(c->dV);
     if (c->dnu) cudaFree(c->dnu);
-    if (c->hx) cudaFreeHost(c->hx);
-    if (c->hout) cudaFreeHost(c->hout);
-    for (auto* v : {&c->timed, &c->event_pool})
-      for (auto& ev : *v) {
-        cudaEventDestroy(ev.first);
-        cudaEventDestroy(ev.second);
-      }
     cudaStreamDestroy(c->stream);
   }
   delete c;

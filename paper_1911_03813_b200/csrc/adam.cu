@@ -1,0 +1,380 @@
+// Stochastic path on the device: row sampling + epoch-based Adam.
+//
+// Reference: sample_observations (pkg/src/momentcp/objective.py:97-113) and adam_minimize
+// (pkg/src/momentcp/optimize.py:365-451).
+//
+// The observation set stays resident; a mini-batch is a gather of `batch` rows of V into a
+// small zero-padded buffer that a view context (ctx.h make_view_ctx, uniform weights 1/batch)
+// evaluates with the same K1 -> K3 -> K4 chain as a full evaluation.  One Adam iteration is
+//     gather(idx[it]) -> fg(batch view, x) -> adam update of x, m1, m2 (it += 1)
+// captured once as a CUDA graph and replayed epoch_len times per epoch without host syncs; the
+// epoch's indices (drawn by the caller's numpy Generator exactly as the reference draws them)
+// and bias corrections 1 - beta^t (host pow, as in the reference) are uploaded per epoch.  The
+// function estimate on the fixed estimate subset is one more graph; the host reads back only f.
+// The update uses explicit round-to-nearest operations in the reference's evaluation order, so
+// given the same gradient it reproduces numpy's m1, m2 and x bit for bit.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+#include "mcp_common.cuh"
+
+using namespace mcp;
+using namespace mcp_internal;
+
+namespace {
+
+constexpr int AD_T = 256;
+
+// rows idx[it * batch + l] of the resident set -> row l of the batch buffer (pitch ldo)
+template <typename Tin, typename Tout>
+__global__ void k_gather_rows(const Tin* __restrict__ V, int64_t ldv, int64_t n,
+                              const int64_t* __restrict__ idx, const int* __restrict__ it_dev,
+                              int64_t batch, Tout* __restrict__ out, int64_t ldo) {
+  const int64_t base = it_dev ? (int64_t)(*it_dev) * batch : 0;
+  for (int64_t l = blockIdx.y; l < batch; l += gridDim.y) {
+    const Tin* src = V + idx[base + l] * ldv;
+    Tout* dst = out + l * ldo;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      dst[i] = (Tout)src[i];
+  }
+}
+
+struct AdamScalars {
+  double lr, b1, omb1, b2, omb2, eps;
+};
+
+// m1 = b1 m1 + (1-b1) g ; m2 = b2 m2 + ((1-b2) g) g ; x -= (lr (m1/bc1)) / (sqrt(m2/bc2) + eps)
+// (optimize.py:425-430).  bc[2 it], bc[2 it + 1] = 1 - b1^t, 1 - b2^t.  The last block advances
+// the iteration counter.
+__global__ void k_adam_step(int64_t N, const double* __restrict__ out, double* __restrict__ x,
+                            double* __restrict__ m1, double* __restrict__ m2,
+                            const double* __restrict__ bc, const double* __restrict__ lr_dev,
+                            AdamScalars sc, int* __restrict__ it_dev, unsigned* counter) {
+  const int it = *it_dev;
+  const double bc1 = bc[2 * it], bc2 = bc[2 * it + 1];
+  const double lr = *lr_dev;
+  const double* g = out + 1;
+  for (int64_t j = blockIdx.x * (int64_t)AD_T + threadIdx.x; j < N;
+       j += (int64_t)gridDim.x * AD_T) {
+    const double gj = g[j];
+    const double a = __dadd_rn(__dmul_rn(sc.b1, m1[j]), __dmul_rn(sc.omb1, gj));
+    const double b = __dadd_rn(__dmul_rn(sc.b2, m2[j]), __dmul_rn(__dmul_rn(sc.omb2, gj), gj));
+    m1[j] = a;
+    m2[j] = b;
+    const double mh = __ddiv_rn(a, bc1);
+    const double vh = __ddiv_rn(b, bc2);
+    x[j] = __dsub_rn(x[j], __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), sc.eps)));
+  }
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (last) {
+      *counter = 0u;
+      *it_dev = it + 1;
+    }
+  }
+}
+
+struct AdamRun {
+  mcp_ctx* c = nullptr;
+  mcp_ctx* vb = nullptr;   // batch view
+  mcp_ctx* ve = nullptr;   // estimate view
+  int d = 0, r = 0, mode = 0;
+  int64_t N = 0, batch = 0, epoch_len = 0, n_est = 0;
+  int nb = 1;
+  EvalPlan plb, ple;
+  std::vector<void*> dev;
+  void *Vb = nullptr, *Ve = nullptr;
+  double *X = nullptr, *XB = nullptr, *M1 = nullptr, *M2 = nullptr, *OB = nullptr, *OE = nullptr;
+  double *bc = nullptr, *lr_dev = nullptr;
+  int64_t *idx = nullptr, *eidx = nullptr;
+  int* it_dev = nullptr;
+  unsigned* counter = nullptr;
+  int64_t* h_idx = nullptr;
+  double* h_bc = nullptr;
+  double* h_scal = nullptr;  // [lr, f_est]
+  GraphEntry g_iter, g_est;
+  AdamScalars sc{};
+
+  ~AdamRun() {
+    for (GraphEntry* g : {&g_iter, &g_est}) {
+      if (g->exec) cudaGraphExecDestroy(g->exec);
+      if (g->graph) cudaGraphDestroy(g->graph);
+    }
+    destroy_view_ctx(vb);
+    destroy_view_ctx(ve);
+    for (void* p : dev) cudaFree(p);
+    if (h_idx) cudaFreeHost(h_idx);
+    if (h_bc) cudaFreeHost(h_bc);
+    if (h_scal) cudaFreeHost(h_scal);
+  }
+
+  template <typename T>
+  int alloc(T*& p, size_t elems) {
+    void* q = nullptr;
+    CUDA_TRY(c, cudaMalloc(&q, sizeof(T) * (elems ? elems : 1)));
+    dev.push_back(q);
+    p = (T*)q;
+    return MCP_OK;
+  }
+
+  // gather view dtype: the set's own, except fp32 rows for tcgen05 fast mode on an fp64 set
+  int view_dtype() const { return mode == MCP_MODE_TF32X3 ? MCP_F32 : c->dtype; }
+
+  int enqueue_gather(void* dst, int64_t rows, const int64_t* ix, const int* itp, int64_t ldo) {
+    const int64_t n = c->n;
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((n + AD_T - 1) / AD_T, 4)),
+              (unsigned)std::min<int64_t>(rows, 4096));
+    cudaStream_t s = c->stream;
+    if (c->dtype == MCP_F64 && view_dtype() == MCP_F64)
+      k_gather_rows<double, double><<<grid, AD_T, 0, s>>>((const double*)c->dV, c->ldv, n, ix,
+                                                           itp, rows, (double*)dst, ldo);
+    else if (c->dtype == MCP_F64)
+      k_gather_rows<double, float><<<grid, AD_T, 0, s>>>((const double*)c->dV, c->ldv, n, ix, itp,
+                                                          rows, (float*)dst, ldo);
+    else
+      k_gather_rows<float, float><<<grid, AD_T, 0, s>>>((const float*)c->dV, c->ldv, n, ix, itp,
+                                                         rows, (float*)dst, ldo);
+    CUDA_TRY(c, cudaGetLastError());
+    return MCP_OK;
+  }
+
+  int make_view(mcp_ctx** out, void** buf, int64_t rows) {
+    const int dt = view_dtype();
+    const int64_t ldo = obs_pitch(dt, c->n);
+    const size_t esz = dt == MCP_F64 ? 8 : 4;
+    const size_t bytes = esz * (size_t)round_up(rows, (int64_t)3584) * ldo;
+    void* q = nullptr;
+    CUDA_TRY(c, cudaMalloc(&q, bytes));
+    dev.push_back(q);
+    CUDA_TRY(c, cudaMemset(q, 0, bytes));
+    *buf = q;
+    *out = make_view_ctx(c, q, dt, rows, ldo);
+    return MCP_OK;
+  }
+
+  int capture(GraphEntry& ge, const std::function<int()>& body) {
+    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = body();
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &ge.graph);
+    if (rc) return rc;
+    CUDA_TRY(c, ce);
+    CUDA_TRY(c, cudaGraphInstantiate(&ge.exec, ge.graph, 0));
+    return MCP_OK;
+  }
+
+  int fg_on(mcp_ctx* v, const EvalPlan& pl, const double* x, double* out) {
+    int rc = enqueue_partial(v, pl, x, (double*)v->dYw.p, c->stream);
+    if (rc) return c->fail(rc, v->err);
+    rc = enqueue_finish(v, d, r, x, (const double*)v->dYw.p, nullptr, 0.0, out, c->stream);
+    if (rc) return c->fail(rc, v->err);
+    return MCP_OK;
+  }
+
+  int setup(const int64_t* est_idx) {
+    const int64_t n = c->n;
+    N = r + n * r;
+    nb = grid_for(N, AD_T, 2 * c->sms);
+    int rc;
+    if ((rc = make_view(&vb, &Vb, batch)) || (rc = make_view(&ve, &Ve, n_est))) return rc;
+    if ((rc = plan_eval(vb, d, r, mode, plb))) return c->fail(rc, vb->err);
+    if ((rc = plan_eval(ve, d, r, mode, ple))) return c->fail(rc, ve->err);
+    if ((rc = alloc(X, N)) || (rc = alloc(XB, N)) || (rc = alloc(M1, N)) || (rc = alloc(M2, N)) ||
+        (rc = alloc(OB, N + 1)) || (rc = alloc(OE, N + 1)) || (rc = alloc(bc, 2 * epoch_len)) ||
+        (rc = alloc(lr_dev, 1)) || (rc = alloc(idx, epoch_len * batch)) ||
+        (rc = alloc(eidx, n_est)) || (rc = alloc(it_dev, 1)) || (rc = alloc(counter, 1)))
+      return rc;
+    CUDA_TRY(c, cudaMemset(counter, 0, sizeof(unsigned)));
+    CUDA_TRY(c, cudaMallocHost(&h_idx, sizeof(int64_t) * std::max(epoch_len * batch, n_est)));
+    CUDA_TRY(c, cudaMallocHost(&h_bc, sizeof(double) * 2 * epoch_len));
+    CUDA_TRY(c, cudaMallocHost(&h_scal, sizeof(double) * 4));
+    // the estimate subset is gathered once
+    std::memcpy(h_idx, est_idx, sizeof(int64_t) * n_est);
+    CUDA_TRY(c, cudaMemcpyAsync(eidx, h_idx, sizeof(int64_t) * n_est, cudaMemcpyHostToDevice,
+                                c->stream));
+    if ((rc = enqueue_gather(Ve, n_est, eidx, nullptr, ve->ldv))) return rc;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    cudaStream_t s = c->stream;
+    if ((rc = capture(g_iter, [&]() -> int {
+           int e = enqueue_gather(Vb, batch, idx, it_dev, vb->ldv);
+           if (e) return e;
+           if ((e = fg_on(vb, plb, X, OB))) return e;
+           k_adam_step<<<nb, AD_T, 0, s>>>(N, OB, X, M1, M2, bc, lr_dev, sc, it_dev, counter);
+           CUDA_TRY(c, cudaGetLastError());
+           return MCP_OK;
+         })))
+      return rc;
+    if ((rc = capture(g_est, [&]() -> int {
+           int e = fg_on(ve, ple, X, OE);
+           if (e) return e;
+           CUDA_TRY(c, cudaMemcpyAsync(h_scal + 1, OE, sizeof(double), cudaMemcpyDeviceToHost, s));
+           return MCP_OK;
+         })))
+      return rc;
+    return MCP_OK;
+  }
+
+  int estimate(double* f) {
+    CUDA_TRY(c, cudaGraphLaunch(g_est.exec, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    *f = h_scal[1];
+    return MCP_OK;
+  }
+};
+
+}  // namespace
+
+extern "C" int mcp_gather_rows(mcp_ctx* c, const int64_t* idx, int64_t s, void* dst,
+                               int64_t ld_dst, int dst_dtype) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  if (!idx || !dst || s < 1) return c->fail(MCP_ERR_ARG, "sample size must be >= 1");
+  if (ld_dst < c->n) return c->fail(MCP_ERR_ARG, "leading dimension too small");
+  if (dst_dtype != c->dtype && !(c->dtype == MCP_F64 && dst_dtype == MCP_F32))
+    return c->fail(MCP_ERR_ARG, "unsupported destination dtype");
+  for (int64_t l = 0; l < s; ++l)
+    if (idx[l] < 0 || idx[l] >= c->p) return c->fail(MCP_ERR_ARG, "row index out of range");
+  int64_t* didx = nullptr;
+  CUDA_TRY(c, cudaMalloc(&didx, sizeof(int64_t) * s));
+  cudaError_t e = cudaMemcpyAsync(didx, idx, sizeof(int64_t) * s, cudaMemcpyHostToDevice,
+                                  c->stream);
+  if (e == cudaSuccess) {
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((c->n + AD_T - 1) / AD_T, 4)),
+              (unsigned)std::min<int64_t>(s, 4096));
+    if (c->dtype == MCP_F64 && dst_dtype == MCP_F64)
+      k_gather_rows<double, double><<<grid, AD_T, 0, c->stream>>>(
+          (const double*)c->dV, c->ldv, c->n, didx, nullptr, s, (double*)dst, ld_dst);
+    else if (c->dtype == MCP_F64)
+      k_gather_rows<double, float><<<grid, AD_T, 0, c->stream>>>(
+          (const double*)c->dV, c->ldv, c->n, didx, nullptr, s, (float*)dst, ld_dst);
+    else
+      k_gather_rows<float, float><<<grid, AD_T, 0, c->stream>>>(
+          (const float*)c->dV, c->ldv, c->n, didx, nullptr, s, (float*)dst, ld_dst);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  }
+  cudaFree(didx);
+  CUDA_TRY(c, e);
+  return MCP_OK;
+}
+
+extern "C" int mcp_adam(mcp_ctx* c, int d, int r, int mode, const double* x0, const double* opts,
+                        const int64_t* est_idx, int64_t n_est, mcp_sample_fn sample, void* user,
+                        double* x_out, double* g_out, double* f_out, double* trace_f,
+                        double* trace_t, int64_t trace_cap, int64_t* info) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!x0 || !opts || !est_idx || !sample || !x_out || !g_out || !f_out || !info)
+    return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  const double step_size = opts[0], reduced = opts[1];
+  const int64_t epoch_len = (int64_t)opts[2], batch = (int64_t)opts[3];
+  const double beta1 = opts[4], beta2 = opts[5], eps = opts[6];
+  const int64_t max_epochs = (int64_t)opts[7];
+  if (epoch_len < 1) return c->fail(MCP_ERR_ARG, "epoch_len must be >= 1");
+  if (batch < 1) return c->fail(MCP_ERR_ARG, "batch must be >= 1");
+  if (n_est < 1) return c->fail(MCP_ERR_ARG, "estimate subset is empty");
+  for (int64_t l = 0; l < n_est; ++l)
+    if (est_idx[l] < 0 || est_idx[l] >= c->p) return c->fail(MCP_ERR_ARG, "row index out of range");
+  const auto t_start = std::chrono::steady_clock::now();
+  auto seconds = [&]() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  AdamRun R;
+  R.c = c;
+  R.d = d;
+  R.r = r;
+  R.mode = mode;
+  R.batch = batch;
+  R.epoch_len = epoch_len;
+  R.n_est = n_est;
+  R.sc = AdamScalars{step_size, beta1, 1.0 - beta1, beta2, 1.0 - beta2, eps};
+  int rc = R.setup(est_idx);
+  if (rc) return rc;
+  const int64_t N = R.N;
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c, cudaMemcpyAsync(R.X, x0, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemsetAsync(R.M1, 0, sizeof(double) * N, s));
+  CUDA_TRY(c, cudaMemsetAsync(R.M2, 0, sizeof(double) * N, s));
+  double f_best = 0.0;
+  if ((rc = R.estimate(&f_best))) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(R.XB, R.X, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+  int64_t n_trace = 0;
+  auto push_trace = [&](double fv) {
+    if (n_trace < trace_cap) {
+      if (trace_f) trace_f[n_trace] = fv;
+      if (trace_t) trace_t[n_trace] = seconds();
+    }
+    ++n_trace;
+  };
+  push_trace(f_best);
+  double lr = step_size;
+  int64_t t = 0, n_iter = 0;
+  int increases = 0, reason = 0;
+  for (int64_t epoch = 0; epoch < max_epochs; ++epoch) {
+    // the previous epoch's graph replays must be done with the pinned staging before reuse
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (sample(R.h_idx, epoch_len * batch, user) != 0)
+      return c->fail(MCP_ERR_ARG, "sampling callback failed");
+    for (int64_t l = 0; l < epoch_len * batch; ++l)
+      if (R.h_idx[l] < 0 || R.h_idx[l] >= c->p)
+        return c->fail(MCP_ERR_ARG, "row index out of range");
+    for (int64_t k = 0; k < epoch_len; ++k) {
+      const double tt = (double)(t + k + 1);
+      R.h_bc[2 * k] = 1.0 - std::pow(beta1, tt);
+      R.h_bc[2 * k + 1] = 1.0 - std::pow(beta2, tt);
+    }
+    R.h_scal[0] = lr;
+    CUDA_TRY(c, cudaMemcpyAsync(R.idx, R.h_idx, sizeof(int64_t) * epoch_len * batch,
+                                cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(R.bc, R.h_bc, sizeof(double) * 2 * epoch_len,
+                                cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemcpyAsync(R.lr_dev, R.h_scal, sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaMemsetAsync(R.it_dev, 0, sizeof(int), s));
+    for (int64_t k = 0; k < epoch_len; ++k) CUDA_TRY(c, cudaGraphLaunch(R.g_iter.exec, s));
+    t += epoch_len;
+    n_iter += epoch_len;
+    double f_est = 0.0;
+    if ((rc = R.estimate(&f_est))) return rc;
+    push_trace(f_est);
+    if (f_est < f_best) {
+      f_best = f_est;
+      CUDA_TRY(c, cudaMemcpyAsync(R.XB, R.X, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    } else {
+      ++increases;
+      CUDA_TRY(c, cudaMemcpyAsync(R.X, R.XB, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(c, cudaMemsetAsync(R.M1, 0, sizeof(double) * N, s));
+      CUDA_TRY(c, cudaMemsetAsync(R.M2, 0, sizeof(double) * N, s));
+      t = 0;
+      if (increases == 1) {
+        lr = reduced;
+      } else {
+        reason = 1;
+        break;
+      }
+    }
+  }
+  // gradient estimate at the best iterate (optimize.py:441)
+  CUDA_TRY(c, cudaMemcpyAsync(R.X, R.XB, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+  double f_fin = 0.0;
+  if ((rc = R.estimate(&f_fin))) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(x_out, R.XB, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(g_out, R.OE + 1, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  *f_out = f_best;
+  info[0] = n_iter;
+  info[1] = reason;
+  info[2] = std::min(n_trace, trace_cap);
+  return MCP_OK;
+}

@@ -120,6 +120,13 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s);
 
+// A context over rows gathered elsewhere (stochastic path): shares the parent's device and
+// stream, V (p_pad = round_up(p, 3584) rows of pitch ldv, zero padded) is owned by the caller,
+// uniform weights 1/p.  Destroy with destroy_view_ctx.
+mcp_ctx* make_view_ctx(const mcp_ctx* parent, void* dV, int dtype, int64_t p, int64_t ldv);
+void destroy_view_ctx(mcp_ctx* v);
+void release_ctx(mcp_ctx* c);
+
 inline int grid_for(int64_t total, int threads, int cap) {
   int64_t b = (total + threads - 1) / threads;
   if (b < 1) b = 1;

@@ -51,3 +51,26 @@ def fg_implicit(obs: ObservationSet, lam, A, d: int, alpha: float = 0.0,
     start = time.perf_counter()
     f, g_lam, g_A = ctx.fg(lam, np.asfortranarray(A), d, float(alpha), mode)
     return FgResult(f, g_lam, np.ascontiguousarray(g_A), time.perf_counter() - start, eval_kind)
+
+
+def sample_observations(obs: ObservationSet, s: int, rng: np.random.Generator) -> ObservationSet:
+    """Draw ``s`` observations uniformly with replacement, weights 1/s (objective.py:97-113).
+
+    Same draws as the reference (``rng.integers(0, p, size=s)``); the rows are gathered on the
+    device from the resident set (``mcp_gather_rows``), so the sample never visits the host.
+    """
+    import torch
+
+    from . import _native
+
+    if s < 1:
+        raise ValueError(f"sample size must be >= 1, got {s}")
+    if not obs.has_uniform_weights():
+        raise ValueError("sampling requires uniform observation weights")
+    idx = rng.integers(0, obs.p, size=s)
+    labels = obs.labels[idx] if obs.labels is not None else None
+    ctx = obs.device_context()
+    dt = torch.float32 if ctx.dtype_code == _native.MCP_F32 else torch.float64
+    rows = torch.empty((s, obs.n), dtype=dt, device=f"cuda:{ctx.device}")
+    ctx.gather_rows(idx, rows.data_ptr(), obs.n, ctx.dtype_code)
+    return ObservationSet.from_device(rows, labels=labels)

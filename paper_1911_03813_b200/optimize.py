@@ -39,6 +39,27 @@ class OptConfig:
 
 
 @dataclass
+class AdamConfig:
+    """Epoch-based Adam settings (reference optimize.py:51-75, same defaults and checks)."""
+
+    step_size: float = 0.01
+    reduced_step_size: float = 0.001
+    epoch_len: int = 100
+    batch: int = 100
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    estimate_samples: int = 1000
+    max_epochs: int = 1000
+
+    def __post_init__(self) -> None:
+        if self.epoch_len < 1:
+            raise ValueError(f"epoch_len must be >= 1, got {self.epoch_len}")
+        if self.batch < 1:
+            raise ValueError(f"batch must be >= 1, got {self.batch}")
+
+
+@dataclass
 class RunReport:
     """Outcome of one optimization run (reference optimize.py:78-101)."""
 
@@ -153,3 +174,43 @@ def packed_fg_implicit_batched(obs: ObservationSet, d: int, r: int, alpha: float
         return ctx.fg_batch(X, n, d, r, alpha, mode)
 
     return fg
+
+
+def adam_minimize(obs: ObservationSet, d: int, r_hat: int, x0: np.ndarray, cfg: AdamConfig,
+                  rng: np.random.Generator, *, mode: str | None = None) -> RunReport:
+    """Stochastic minimization with epoch-based Adam, device-resident (optimize.py:365-451).
+
+    Same draws from ``rng`` in the same order as the reference (the estimate subset, then
+    ``rng.integers(0, p, size=batch)`` per inner iteration); mini-batches are gathered from the
+    resident observations and the Adam state never leaves the GPU (``mcp_adam``).
+    """
+    import time
+
+    start = time.perf_counter()
+    n, p = obs.n, obs.p
+    if not obs.has_uniform_weights():
+        raise ValueError("stochastic optimization requires uniform weights")
+    x = np.asarray(x0, dtype=float).copy()
+    if x.shape != (r_hat + n * r_hat,):
+        raise ValueError(f"x0 has length {x.size}, expected {r_hat + n * r_hat}")
+    if d < 2:
+        raise ValueError(f"order must be >= 2, got {d}")
+    if not np.isfinite(x).all():
+        raise ValueError("model variables and alpha must be finite")
+    est_idx = rng.choice(p, size=min(cfg.estimate_samples, p), replace=False)
+
+    def sample(count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.int64)
+        for k in range(count // cfg.batch):
+            out[k * cfg.batch:(k + 1) * cfg.batch] = rng.integers(0, p, size=cfg.batch)
+        return out
+
+    ctx = obs.device_context()
+    opts = (cfg.step_size, cfg.reduced_step_size, cfg.epoch_len, cfg.batch, cfg.beta1,
+            cfg.beta2, cfg.eps, cfg.max_epochs)
+    out = ctx.adam(x, n, d, r_hat, mode, opts, est_idx, sample)
+    lam, A = unpack(out["x"], n, r_hat)
+    return RunReport(lam=lam, A=A, f=out["f"], grad_inf_norm=float(np.abs(out["g"]).max()),
+                     n_fg=out["n_iter"], n_steps=out["n_iter"],
+                     wall_time=time.perf_counter() - start, reason=out["reason"],
+                     trace=out["trace"])

@@ -29,4 +29,4 @@ def golden():
 
     gdir = os.path.join(ROOT, "tests", "golden")
     return {name: np.load(os.path.join(gdir, f"{name}.npz"))
-            for name in ("kat", "sweep", "configs", "lbfgs_c1")}
+            for name in ("kat", "sweep", "configs", "lbfgs_c1", "adam_c1")}

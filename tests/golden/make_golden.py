@@ -137,7 +137,23 @@ def lbfgs_c1():
             "final_lam": rep.lam, "final_A": rep.A, "grad_inf": np.array(rep.grad_inf_norm)}
 
 
+def adam_c1():
+    """Reference epoch-based Adam at c1 (small epochs so the run ends by itself)."""
+    from momentcp.optimize import AdamConfig, adam_minimize
+
+    cfg, V, lam, A = instances.config_instance("c1")
+    obs = ref_obs(V, None)
+    rep = adam_minimize(obs, cfg.d, cfg.r, pack(lam, A), AdamConfig(**instances.ADAM_C1),
+                        np.random.default_rng(instances.ADAM_SEED))
+    return {"trace_f": np.array([t[0] for t in rep.trace]), "final_f": np.array(rep.f),
+            "n_fg": np.array(rep.n_fg), "reason": np.array(rep.reason), "final_lam": rep.lam,
+            "final_A": rep.A, "grad_inf": np.array(rep.grad_inf_norm)}
+
+
 def main():
+    if sys.argv[1:] == ["adam"]:
+        np.savez_compressed(os.path.join(HERE, "adam_c1.npz"), **adam_c1())
+        return
     t = time.time()
     np.savez_compressed(os.path.join(HERE, "kat.npz"), **kats())
     sw = sweep("t", instances.TINY_COUNT, instances.tiny_instance)
@@ -146,6 +162,7 @@ def main():
     print(f"sweep done {time.time() - t:.1f}s", flush=True)
     np.savez_compressed(os.path.join(HERE, "configs.npz"), **configs())
     np.savez_compressed(os.path.join(HERE, "lbfgs_c1.npz"), **lbfgs_c1())
+    np.savez_compressed(os.path.join(HERE, "adam_c1.npz"), **adam_c1())
     print(f"all done {time.time() - t:.1f}s")
 
 

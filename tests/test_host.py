@@ -99,3 +99,13 @@ def test_lbfgs_minimize_requires_device_objective():
         mcp.OptConfig(pgtol=0)
     with pytest.raises(ValueError):
         mcp.OptConfig(memory=0)
+
+
+def test_adam_config_checks():
+    import paper_1911_03813_b200 as mcp
+
+    with pytest.raises(ValueError):
+        mcp.AdamConfig(epoch_len=0)
+    with pytest.raises(ValueError):
+        mcp.AdamConfig(batch=0)
+    assert mcp.AdamConfig().estimate_samples == 1000

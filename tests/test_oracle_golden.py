@@ -134,3 +134,18 @@ def test_validation_errors():
         om.fg_implicit(V, nu, np.array([np.nan]), np.ones((2, 1)), 3)
     with pytest.raises(ValueError):
         om.fg_implicit(V, nu, np.ones(1), np.ones((2, 1)), 3, np.inf)
+
+
+def test_adam_restatement_reproduces_reference_run(golden):
+    """oracle/adam_oracle.py vs the reference adam_minimize (tests/golden/adam_c1.npz)."""
+    from oracle import adam_oracle as ao
+
+    g = golden["adam_c1"]
+    cfg, V, lam, A = instances.config_instance("c1")
+    out = ao.adam(V, cfg.d, cfg.r, om.pack(lam, A), np.random.default_rng(instances.ADAM_SEED),
+                  **instances.ADAM_C1)
+    assert np.array_equal(np.array(out["trace_f"]), g["trace_f"])
+    assert out["reason"] == str(g["reason"]) and out["n_iter"] == int(g["n_fg"])
+    lam_b, A_b = om.unpack(out["x"], cfg.n, cfg.r)
+    assert np.array_equal(lam_b, g["final_lam"]) and np.array_equal(A_b, g["final_A"])
+    assert out["grad_inf"] == float(g["grad_inf"])

@@ -82,6 +82,10 @@ void drop_graphs(mcp_ctx* c) {
     c->lbfgs_ws_free(c->lbfgs_ws);
     c->lbfgs_ws = nullptr;
   }
+  if (c->adam_ws) {
+    c->adam_ws_free(c->adam_ws);
+    c->adam_ws = nullptr;
+  }
 }
 
 // Event pair bracketing one timed kernel launch (only when timing is on and not capturing).
@@ -350,7 +354,7 @@ int enqueue_finish_yw(mcp_ctx* c, int d, int r, const double* dx, const double* 
     c->last_launches += 1;
     return MCP_OK;
   }
-  k_tail_gram<<<grid_for((int64_t)r * r, 128, 8 * c->sms), 128, 0, s>>>(
+  k_tail_gram<<<grid_for((int64_t)r * r, K4A_WARPS, 16 * c->sms), 32 * K4A_WARPS, 0, s>>>(
       dx, n, r, d, (double*)c->dG.p, (double*)c->dC.p);
   k_tail_vec<<<1, 256, sizeof(double) * r, s>>>(dx, dw, (const double*)c->dG.p,
                                                 (const double*)c->dC.p, n, r, alpha_dev, alpha,
@@ -551,7 +555,7 @@ mcp_ctx* make_view_ctx(const mcp_ctx* parent, void* dV, int dtype, int64_t p, in
   v->dtype = dtype;
   v->n = parent->n;
   v->p = p;
-  v->p_pad = round_up(p, 3584);
+  v->p_pad = round_up(p, 896);  // lcm of the K1 (64), K1S (224) and K1T (128) row units
   v->ldv = ldv;
   v->dV = dV;
   v->dnu = nullptr;

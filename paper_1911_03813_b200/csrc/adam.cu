@@ -153,7 +153,7 @@ struct AdamRun {
     const int dt = view_dtype();
     const int64_t ldo = obs_pitch(dt, c->n);
     const size_t esz = dt == MCP_F64 ? 8 : 4;
-    const size_t bytes = esz * (size_t)round_up(rows, (int64_t)3584) * ldo;
+    const size_t bytes = esz * (size_t)round_up(rows, (int64_t)896) * ldo;
     void* q = nullptr;
     CUDA_TRY(c, cudaMalloc(&q, bytes));
     dev.push_back(q);
@@ -181,8 +181,15 @@ struct AdamRun {
     return MCP_OK;
   }
 
-  int setup(const int64_t* est_idx) {
-    const int64_t n = c->n;
+  bool matches(int d_, int r_, int mode_, int64_t batch_, int64_t epoch_len_, int64_t n_est_,
+               const AdamScalars& sc_) const {
+    return d == d_ && r == r_ && mode == mode_ && batch == batch_ && epoch_len == epoch_len_ &&
+           n_est == n_est_ && c->n == n && std::memcmp(&sc, &sc_, sizeof(sc)) == 0;
+  }
+  int64_t n = 0;
+
+  int setup() {
+    n = c->n;
     N = r + n * r;
     nb = grid_for(N, AD_T, 2 * c->sms);
     int rc;
@@ -198,12 +205,6 @@ struct AdamRun {
     CUDA_TRY(c, cudaMallocHost(&h_idx, sizeof(int64_t) * std::max(epoch_len * batch, n_est)));
     CUDA_TRY(c, cudaMallocHost(&h_bc, sizeof(double) * 2 * epoch_len));
     CUDA_TRY(c, cudaMallocHost(&h_scal, sizeof(double) * 4));
-    // the estimate subset is gathered once
-    std::memcpy(h_idx, est_idx, sizeof(int64_t) * n_est);
-    CUDA_TRY(c, cudaMemcpyAsync(eidx, h_idx, sizeof(int64_t) * n_est, cudaMemcpyHostToDevice,
-                                c->stream));
-    if ((rc = enqueue_gather(Ve, n_est, eidx, nullptr, ve->ldv))) return rc;
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     cudaStream_t s = c->stream;
     if ((rc = capture(g_iter, [&]() -> int {
            int e = enqueue_gather(Vb, batch, idx, it_dev, vb->ldv);
@@ -221,6 +222,18 @@ struct AdamRun {
            return MCP_OK;
          })))
       return rc;
+    return MCP_OK;
+  }
+
+  // the estimate subset of this run, gathered once
+  int load_estimate_rows(const int64_t* est_idx) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    std::memcpy(h_idx, est_idx, sizeof(int64_t) * n_est);
+    CUDA_TRY(c, cudaMemcpyAsync(eidx, h_idx, sizeof(int64_t) * n_est, cudaMemcpyHostToDevice,
+                                c->stream));
+    int rc = enqueue_gather(Ve, n_est, eidx, nullptr, ve->ldv);
+    if (rc) return rc;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return MCP_OK;
   }
 
@@ -291,16 +304,32 @@ extern "C" int mcp_adam(mcp_ctx* c, int d, int r, int mode, const double* x0, co
   auto seconds = [&]() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   };
-  AdamRun R;
-  R.c = c;
-  R.d = d;
-  R.r = r;
-  R.mode = mode;
-  R.batch = batch;
-  R.epoch_len = epoch_len;
-  R.n_est = n_est;
-  R.sc = AdamScalars{step_size, beta1, 1.0 - beta1, beta2, 1.0 - beta2, eps};
-  int rc = R.setup(est_idx);
+  const AdamScalars sc{step_size, beta1, 1.0 - beta1, beta2, 1.0 - beta2, eps};
+  AdamRun* ws = (AdamRun*)c->adam_ws;
+  if (!ws || !ws->matches(d, r, mode, batch, epoch_len, n_est, sc)) {
+    if (ws) {
+      c->adam_ws_free(ws);
+      c->adam_ws = nullptr;
+    }
+    ws = new AdamRun();
+    ws->c = c;
+    ws->d = d;
+    ws->r = r;
+    ws->mode = mode;
+    ws->batch = batch;
+    ws->epoch_len = epoch_len;
+    ws->n_est = n_est;
+    ws->sc = sc;
+    int rc0 = ws->setup();
+    if (rc0) {
+      delete ws;
+      return rc0;
+    }
+    c->adam_ws = ws;
+    c->adam_ws_free = [](void* p) { delete (AdamRun*)p; };
+  }
+  AdamRun& R = *ws;
+  int rc = R.load_estimate_rows(est_idx);
   if (rc) return rc;
   const int64_t N = R.N;
   cudaStream_t s = c->stream;

@@ -69,6 +69,9 @@ struct mcp_ctx {
   // cached device-resident L-BFGS workspace (lbfgs.cu); freed with the graphs
   void* lbfgs_ws = nullptr;
   void (*lbfgs_ws_free)(void*) = nullptr;
+  // cached stochastic-path workspace (adam.cu); freed with the graphs
+  void* adam_ws = nullptr;
+  void (*adam_ws_free)(void*) = nullptr;
 
   int fail(int code, const std::string& msg) {
     err = msg;
@@ -121,7 +124,7 @@ int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s);
 
 // A context over rows gathered elsewhere (stochastic path): shares the parent's device and
-// stream, V (p_pad = round_up(p, 3584) rows of pitch ldv, zero padded) is owned by the caller,
+// stream, V (p_pad = round_up(p, 896) rows of pitch ldv, zero padded) is owned by the caller,
 // uniform weights 1/p.  Destroy with destroy_view_ctx.
 mcp_ctx* make_view_ctx(const mcp_ctx* parent, void* dV, int dtype, int64_t p, int64_t ldv);
 void destroy_view_ctx(mcp_ctx* v);

@@ -76,20 +76,33 @@ __global__ void __launch_bounds__(K3_X * K3_Y)
   }
 }
 
-// K4a: G = A^T A and C = G^(d-1) (implicit.py:147-148), row-major r x r.
+// K4a: G = A^T A and C = G^(d-1) (implicit.py:147-148), row-major r x r.  One warp per upper
+// triangle entry (j <= k): lanes stride over the n rows of the two columns (coalesced), then a
+// fixed butterfly; the value is mirrored so G is exactly symmetric.  Launch with 256-thread
+// blocks (K4A_WARPS warps per block).
+constexpr int K4A_WARPS = 8;
 __global__ void k_tail_gram(const double* __restrict__ x, int n, int r, int d,
                             double* __restrict__ G, double* __restrict__ C) {
   const double* A = x + r;
+  const int lane = threadIdx.x & 31;
   const int64_t total = (int64_t)r * r;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int j = idx / r, k = idx % r;
+  for (int64_t idx = blockIdx.x * (int64_t)K4A_WARPS + (threadIdx.x >> 5); idx < total;
+       idx += (int64_t)gridDim.x * K4A_WARPS) {
+    const int j = (int)(idx / r), k = (int)(idx % r);
+    if (j > k) continue;
     const double* aj = A + (int64_t)j * n;
     const double* ak = A + (int64_t)k * n;
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += aj[i] * ak[i];
-    G[idx] = s;
-    C[idx] = rm_pow(s, d - 1);
+    for (int i = lane; i < n; i += 32) s += aj[i] * ak[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const double c = rm_pow(s, d - 1);
+      G[(int64_t)j * r + k] = s;
+      G[(int64_t)k * r + j] = s;
+      C[(int64_t)j * r + k] = c;
+      C[(int64_t)k * r + j] = c;
+    }
   }
 }
 

@@ -43,6 +43,8 @@ CONFIGS = {
     "c3": Config("c3", 512, 4_000_000, 6, 64, "f32", 0.05, 64, "scaled", "dirichlet"),
     "c4": Config("c4", 256, 200_000, 4, 0, "f64", 1.0, 0, "none", "none"),
     "c5": Config("c5", 1024, 16_000_000, 3, 256, "f32", 0.1, 256, "unit", "uniform"),
+    # the paper's stochastic example (Table 2): Adam with s = 10/100/1000
+    "t2": Config("t2", 500, 500_000, 3, 10, "f64", 0.1, 10, "unit", "uniform"),
 }
 
 

@@ -214,3 +214,53 @@ def adam_minimize(obs: ObservationSet, d: int, r_hat: int, x0: np.ndarray, cfg: 
                      n_fg=out["n_iter"], n_steps=out["n_iter"],
                      wall_time=time.perf_counter() - start, reason=out["reason"],
                      trace=out["trace"])
+
+
+def multistart(k: int, init: Callable[[np.random.Generator], np.ndarray],
+               minimize: Callable[[np.ndarray, np.random.Generator], RunReport], seed: int,
+               threads: int = 1) -> RunReport:
+    """Best of ``k`` independently seeded runs (reference optimize.py:454-508, same semantics).
+
+    Run i draws from ``default_rng(SeedSequence(seed).spawn(k)[i])``; the report with the
+    lowest final f (ties by run index) is returned with every run attached.  With
+    ``threads > 1`` runs are submitted from a thread pool; the device serialises them per
+    observation set, and results equal the sequential ones bitwise.
+    """
+    if k < 1:
+        raise ValueError(f"number of starts must be >= 1, got {k}")
+    root = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
+    children = root.spawn(k)
+
+    def one(i: int) -> RunReport:
+        rng = np.random.default_rng(children[i])
+        x0 = init(rng)
+        report = minimize(x0, rng)
+        report.run_index = i
+        return report
+
+    results: list[RunReport | None] = [None] * k
+    errors: list[str] = []
+    if threads > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            futures = {pool.submit(one, i): i for i in range(k)}
+            for fut, i in futures.items():
+                try:
+                    results[i] = fut.result()
+                except Exception as exc:  # noqa: BLE001 - aggregated below
+                    errors.append(f"run {i}: {exc}")
+    else:
+        for i in range(k):
+            try:
+                results[i] = one(i)
+            except Exception as exc:  # noqa: BLE001 - aggregated below
+                errors.append(f"run {i}: {exc}")
+    successes = [r for r in results if r is not None]
+    if not successes:
+        raise RuntimeError("all multistart runs failed: " + "; ".join(errors))
+    best = min(successes, key=lambda rp: (rp.f, rp.run_index))
+    best.runs = successes
+    best.failures = errors
+    best.seed = seed if isinstance(seed, int) else None
+    return best

@@ -108,3 +108,23 @@ def test_device_lbfgs_fast_mode_and_limits():
         host = lo.lbfgs(fg64, x0, memory=m, max_iters=15)
         assert rep.n_fg == host["n_fg"]
         assert abs(rep.f - host["f"]) <= 1e-10 * abs(host["f"])
+
+
+def test_multistart_device_lbfgs_threads_equal_sequential():
+    """multistart (optimize.py:454-508) over device L-BFGS runs: best-of-k selection, and
+    threaded submission equals sequential bitwise (test_optimize.py:256-261)."""
+    cfg, obs, _ = _c1()
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+
+    def init(rng):
+        A = rng.standard_normal((cfg.n, cfg.r))
+        return mcp.pack(np.full(cfg.r, 1.0 / cfg.r), A / np.linalg.norm(A, axis=0))
+
+    def minimize(x0, rng):
+        return mcp.lbfgs_minimize(fg, x0, mcp.OptConfig(max_iters=25), shape=(cfg.n, cfg.r))
+
+    seq = mcp.multistart(4, init, minimize, seed=5)
+    thr = mcp.multistart(4, init, minimize, seed=5, threads=4)
+    assert len(seq.runs) == 4 and seq.f == min(r.f for r in seq.runs)
+    assert thr.run_index == seq.run_index and thr.f == seq.f
+    assert all(a.f == b.f and np.array_equal(a.A, b.A) for a, b in zip(seq.runs, thr.runs))

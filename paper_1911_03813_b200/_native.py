@@ -17,7 +17,8 @@ import threading
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmomentcp_b200.so")
+LIB_PATH = os.environ.get("MCP_LIBRARY") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libmomentcp_b200.so")  # env: A/B builds
 
 MCP_OK, MCP_ERR_ARG, MCP_ERR_CUDA, MCP_ERR_STATE = 0, 1, 2, 3
 MCP_F64, MCP_F32 = 0, 1

@@ -331,7 +331,11 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
                      (const double*)c->dAfrag.p, pl.d, (double*)c->dYpart.p, (double*)c->dwpart.p,
                      s);
   timing_end(ev, s);
-  if (rc) return c->fail(MCP_ERR_CUDA, "K1 launch failed");
+  if (rc) {
+    const cudaError_t e = cudaGetLastError();
+    return c->fail(MCP_ERR_CUDA, std::string("K1 launch failed (") + v.name + "): " +
+                                     cudaGetErrorString(e));
+  }
   const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) +
                              ceil_div((int64_t)v.rbs * v.RB, K3_X);
   k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(

@@ -6,6 +6,7 @@
 #include "k1_dispatch.h"
 #include "k1_fp64.cuh"
 #include "k1s_fp64.cuh"
+#include "k1p_fp64.cuh"
 
 namespace mcp {
 namespace {
@@ -94,6 +95,22 @@ const EntryS kTableS[] = {MCP_K1S_COLS(1, 1),  MCP_K1S_COLS(2, 5),  MCP_K1S_COLS
 constexpr int kEntriesS = sizeof(kTableS) / sizeof(kTableS[0]);
 std::atomic<bool> g_attr_s[kEntriesS];
 
+// ---------------- K1P (self-fed pairs, fp64, n <= 128) ----------------
+template <int NTM, int TAIL, int MTH, int KH>
+void launch_p(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
+  k1p_fg_pairs<NTM, TAIL, MTH, KH><<<grid, K1P_THREADS, smem, s>>>(prm);
+}
+#define MCP_K1P_E(NTM, TAIL, MTH, KH) \
+  {NTM, TAIL, MTH, KH, &launch_p<NTM, TAIL, MTH, KH>, \
+   (const void*)&k1p_fg_pairs<NTM, TAIL, MTH, KH>}
+#define MCP_K1P_COLS(MTH, KH) \
+  MCP_K1P_E(1, 0, MTH, KH), MCP_K1P_E(1, 1, MTH, KH), MCP_K1P_E(1, 2, MTH, KH), \
+      MCP_K1P_E(2, 0, MTH, KH)
+const EntryS kTableP[] = {MCP_K1P_COLS(1, 1),  MCP_K1P_COLS(2, 5),  MCP_K1P_COLS(3, 9),
+                          MCP_K1P_COLS(5, 17), MCP_K1P_COLS(7, 25), MCP_K1P_COLS(8, 29),
+                          MCP_K1P_COLS(8, 33)};
+std::atomic<bool> g_attr_p[kEntriesS];
+
 bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
   if (n > 128) return false;
   const int MT = (int)ceil_div(n, 8);
@@ -181,6 +198,73 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
   return true;
 }
 
+// K1P: same column / m-tile split as K1S, a private ring of SP >= 2 slabs per pair.
+bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
+  if (n > 128) return false;
+  const int MT = (int)ceil_div(n, 8);
+  const int kst = (int)(ldv / 4);
+  const int mth_need = (MT + 1) / 2, kh_need = kst;
+  int ntm, tail;
+  if (r <= 8) { ntm = 1; tail = 0; }
+  else if (r <= 10 && !getenv("MCP_K1S_NO_TAIL")) { ntm = 1; tail = r - 8; }
+  else { ntm = 2; tail = 0; }
+  int e = -1;
+  for (int i = 0; i < kEntriesS && e < 0; ++i)
+    if (kTableP[i].NTM == ntm && kTableP[i].TAIL == tail && kTableP[i].MTH >= mth_need &&
+        kTableP[i].KH >= kh_need)
+      e = i;
+  if (e < 0) return false;
+  const int cw = 8 * ntm + tail;
+  const size_t slab = (size_t)K1S_SR * ldv * 8;
+  const size_t fixed = k1p_fixed_bytes(kTableP[e].KH, ntm, cw);
+  const size_t budget = 227 * 1024 - 1024 - fixed;
+  int SP = (int)(budget / ((size_t)K1P_PAIRS * (slab + 8)));
+  if (SP > 4) SP = 4;
+  if (SP < 2) return false;
+  const size_t ring_bytes = (size_t)K1P_PAIRS * SP * slab;
+  const size_t stage_need = ((size_t)K1P_PAIRS * MT * 8 * cw + (size_t)2 * K1P_PAIRS * cw) * 8;
+  if (ring_bytes < stage_need) return false;
+  const size_t smem = ring_bytes + fixed + 8 * (size_t)K1P_PAIRS * SP;
+  if (!g_attr_p[e].exchange(true)) {
+    if (cudaFuncSetAttribute(kTableP[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+      (void)cudaGetLastError();
+      g_attr_p[e].store(false);
+      return false;
+    }
+  } else {
+    cudaFuncSetAttribute(kTableP[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  v.kind = 3;
+  v.dtype = MCP_F64;
+  v.RB = cw;
+  v.MTW = kTableP[e].MTH;
+  v.MT = MT;
+  v.n_chunks = 0;
+  v.n_pad = MT * 8;
+  v.rbs = (int)ceil_div(r, cw);
+  v.num_tiles = p_pad / K1S_SR;
+  int64_t G = sms;
+  if (G < v.rbs) G = v.rbs;
+  G -= G % v.rbs;
+  int64_t gp = G / v.rbs;
+  if (gp > v.num_tiles) gp = v.num_tiles;
+  if (gp < 1) gp = 1;
+  v.gp = (int)gp;
+  v.grid = v.gp * v.rbs;
+  v.stages = SP;
+  v.MTW2 = 1;
+  v.smem = smem;
+  v.entry = e;
+  v.afrag_elems = 0;
+  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * cw;
+  v.wpart_elems = (size_t)v.rbs * v.gp * cw;
+  v.name = "k1p_fg_pairs<f64,DMMA=" + std::to_string(8 * ntm) + ",DFMA=" +
+           std::to_string(tail) + ",MTH=" + std::to_string(kTableP[e].MTH) + ",KH=" +
+           std::to_string(kTableP[e].KH) + ",SP=" + std::to_string(SP) + ">";
+  return true;
+}
+
 }  // namespace
 
 int64_t obs_pitch(int dtype, int64_t n) {
@@ -195,6 +279,10 @@ int64_t obs_pitch(int dtype, int64_t n) {
 
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v,
                std::string& why) {
+  v = K1Variant();
+  if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1P") &&
+      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v))
+    return true;
   v = K1Variant();
   if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1S") &&
       select_stream(n, r, p_pad, obs_pitch(dtype, n), sms, v))
@@ -252,7 +340,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
               double* wpart, cudaStream_t s) {
   if (v.entry < 0) return 1;
-  if (v.kind == 1) {
+  if (v.kind == 1 || v.kind == 3) {
     K1SParams sp;
     sp.V = static_cast<const double*>(dV);
     sp.ldv = ldv;
@@ -270,7 +358,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     sp.spc = v.MTW2;
     sp.Ypart = Ypart;
     sp.wpart = wpart;
-    kTableS[v.entry].launch(sp, v.grid, v.smem, s);
+    (v.kind == 1 ? kTableS : kTableP)[v.entry].launch(sp, v.grid, v.smem, s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }
   K1Params prm;

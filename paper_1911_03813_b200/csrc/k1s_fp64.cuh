@@ -99,13 +99,22 @@ __host__ __device__ inline size_t k1s_fixed_bytes(int kh, int ntm, int cw, int p
 }
 
 
-constexpr int K1S_PAIRS = 7;  // math warp pairs per CTA (15 warps: <= 4 per SMSP -> 128 regs)
+#ifndef MCP_K1S_PAIRS
+#define MCP_K1S_PAIRS 7
+#endif
+constexpr int K1S_PAIRS = MCP_K1S_PAIRS;  // math warp pairs per CTA (6: 13 warps -> 152 regs)
 constexpr int K1S_THREADS = (2 * K1S_PAIRS + 1) * 32;  // + 1 producer warp
+// registers per thread: each of the 4 SM sub-partitions has its own 16K-register file and
+// receives ceil(warps / 4) of the CTA's warps
+constexpr int K1S_MAXREG =
+    (16384 / (32 * ((K1S_THREADS / 32 + 3) / 4))) / 8 * 8 > 255
+        ? 255
+        : (16384 / (32 * ((K1S_THREADS / 32 + 3) / 4))) / 8 * 8;
 
 // NTM: 8-column DMMA tiles, TAIL: DFMA columns, MTH: GEMM2 m-tiles per warp (warp 0 of a pair
 // takes [0, MTH), warp 1 [MTH, MT)), KH: GEMM1 k-steps (>= ldv / 4, zero-padded factor).
 template <int NTM, int TAIL, int MTH, int KH>
-__global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
+__global__ void __maxnreg__(K1S_MAXREG) k1s_fg_stream(K1SParams prm) {
   constexpr int CW = 8 * NTM + TAIL;
   constexpr int PP = k1s_pp(CW);
   constexpr int TL = TAIL > 0 ? TAIL : 1;
@@ -241,20 +250,40 @@ __global__ void __launch_bounds__(K1S_THREADS, 1) k1s_fg_stream(K1SParams prm) {
 #pragma unroll
       for (int c = 0; c < TL; ++c) zt[mt][c] = 0.0;
     }
-    // even / odd k-steps accumulate separately (2 independent DMMA chains), added below
+    // even / odd k-steps accumulate separately (2 independent DMMA chains), added below.
+    // Operands of step kk + 1 are loaded before step kk's math (explicit software pipeline:
+    // with the register cap ptxas otherwise reuses one register set and serialises every step
+    // on its shared-memory load).
     const double* v0 = sv + (8 * h + g) * ldv + t;
     const double* bp = sAf + lane;
     const double* at = sAt + t * 4;
+    double a_c = v0[0], b_c[NTM];
+    double2 t_c = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int nt = 0; nt < NTM; ++nt) b_c[nt] = bp[nt * 32];
+    if constexpr (TAIL > 0) t_c = *reinterpret_cast<const double2*>(at);
 #pragma unroll
     for (int kk = 0; kk < KH; ++kk) {
       const int e2 = kk & 1;
-      const double a0 = v0[4 * kk];
+      double a_n = 0.0, b_n[NTM];
+      double2 t_n = make_double2(0.0, 0.0);
+      if (kk + 1 < KH) {
+        a_n = v0[4 * (kk + 1)];
 #pragma unroll
-      for (int nt = 0; nt < NTM; ++nt) dmma884(z[e2][nt], a0, bp[(kk * NTM + nt) * 32]);
+        for (int nt = 0; nt < NTM; ++nt) b_n[nt] = bp[((kk + 1) * NTM + nt) * 32];
+        if constexpr (TAIL > 0) t_n = *reinterpret_cast<const double2*>(at + 16 * (kk + 1));
+      }
+#pragma unroll
+      for (int nt = 0; nt < NTM; ++nt) dmma884(z[e2][nt], a_c, b_c[nt]);
       if constexpr (TAIL > 0) {
-        const double2 tv = *reinterpret_cast<const double2*>(at + 16 * kk);
-        zt[e2][0] = fma(a0, tv.x, zt[e2][0]);
-        if constexpr (TAIL > 1) zt[e2][TL - 1] = fma(a0, tv.y, zt[e2][TL - 1]);
+        zt[e2][0] = fma(a_c, t_c.x, zt[e2][0]);
+        if constexpr (TAIL > 1) zt[e2][TL - 1] = fma(a_c, t_c.y, zt[e2][TL - 1]);
+      }
+      if (kk + 1 < KH) {
+        a_c = a_n;
+#pragma unroll
+        for (int nt = 0; nt < NTM; ++nt) b_c[nt] = b_n[nt];
+        t_c = t_n;
       }
     }
 #pragma unroll

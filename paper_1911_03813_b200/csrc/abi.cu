@@ -276,6 +276,10 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   if ((rc = ensure(c, c->dwpart, sizeof(double) * pl.k1.wpart_elems))) return rc;
   if ((rc = ensure(c, c->dG, sizeof(double) * (size_t)r * r))) return rc;
   if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
+  if (k1_fuses_tail(pl.k1, c->n, r)) {
+    if ((rc = ensure(c, c->dM, sizeof(double) * (size_t)n * r))) return rc;
+    if ((rc = ensure(c, c->du, sizeof(double) * (size_t)r))) return rc;
+  }
   return MCP_OK;
 }
 
@@ -375,6 +379,36 @@ int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw
   return enqueue_finish_yw(c, d, r, dx, dYw, dYw + c->n * r, alpha_dev, alpha, dout, s);
 }
 
+int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const double* alpha_dev,
+                    double alpha, double* dout, cudaStream_t s) {
+  const int r = pl.r;
+  if (pl.mode != MCP_MODE_FP64 || !k1_fuses_tail(pl.k1, c->n, r) || getenv("MCP_NO_FUSED_TAIL")) {
+    int rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s);
+    if (rc) return rc;
+    return enqueue_finish(c, pl.d, r, dx, (const double*)c->dYw.p, alpha_dev, alpha, dout, s);
+  }
+  const K1Variant& v = pl.k1;
+  const int n = (int)c->n;
+  auto* ev = timing_begin(c, s);
+  int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r, nullptr, pl.d,
+                     (double*)c->dYpart.p, (double*)c->dwpart.p, s, dx, (double*)c->dM.p,
+                     (double*)c->du.p);
+  timing_end(ev, s);
+  if (rc) {
+    const cudaError_t e = cudaGetLastError();
+    return c->fail(MCP_ERR_CUDA, std::string("K1 launch failed (") + v.name + "): " +
+                                     cudaGetErrorString(e));
+  }
+  const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) + 1;
+  k_reduce_finish<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
+      (const double*)c->dYpart.p, (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
+      dx, (const double*)c->dM.p, (const double*)c->du.p, pl.d, alpha_dev, alpha, dout);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches = 2;
+  c->variant = v.name;
+  return MCP_OK;
+}
+
 // Host entry: x (r + n r doubles) + alpha -> out (1 + r + n r doubles), through a cached graph.
 int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const double* A,
                   double alpha) {
@@ -398,10 +432,7 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     double* dx = (double*)c->dx.p;
     cudaMemcpyAsync(dx, hx, xin, cudaMemcpyHostToDevice, c->stream);
-    int rc1 = enqueue_partial(c, pl, dx, (double*)c->dYw.p, c->stream);
-    int rc2 = rc1 ? rc1
-                  : enqueue_finish(c, d, r, dx, (const double*)c->dYw.p, dx + r + n * r, 0.0,
-                                   (double*)c->dout.p, c->stream);
+    int rc2 = enqueue_fg_full(c, pl, dx, dx + r + n * r, 0.0, (double*)c->dout.p, c->stream);
     cudaMemcpyAsync(c->hout, c->dout.p, xout, cudaMemcpyDeviceToHost, c->stream);
     cudaError_t ce = cudaStreamEndCapture(c->stream, &ge.graph);
     if (rc2) {
@@ -412,8 +443,11 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     CUDA_TRY(c, cudaGraphInstantiate(&ge.exec, ge.graph, 0));
     it = c->graphs.emplace(key, ge).first;
   } else {
-    c->last_launches = (pl.mode == MCP_MODE_TF32X3 ? 4 : (pl.k1.needs_prep() ? 3 : 2)) +
-                       (((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) ? 1 : 3);
+    c->last_launches =
+        (pl.mode == MCP_MODE_FP64 && k1_fuses_tail(pl.k1, c->n, r) && !getenv("MCP_NO_FUSED_TAIL"))
+            ? 2
+            : (pl.mode == MCP_MODE_TF32X3 ? 4 : (pl.k1.needs_prep() ? 3 : 2)) +
+                  (((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) ? 1 : 3);
     c->variant = pl.k1.name;
   }
   CUDA_TRY(c, cudaGraphLaunch(it->second.exec, c->stream));
@@ -534,7 +568,8 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
 void release_ctx(mcp_ctx* c) {
   drop_graphs(c);
   DevBuf* bufs[] = {&c->dx, &c->dout, &c->dYw, &c->dAfrag, &c->dYpart, &c->dwpart,
-                    &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag, &c->dAt};
+                    &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag, &c->dAt,
+                    &c->dM, &c->du};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->own_v32 && c->dV32) cudaFree(c->dV32);
@@ -821,8 +856,7 @@ int mcp_fg_device(mcp_ctx* c, int d, int r, const double* dx, double alpha, int 
   int rc = plan_eval(c, d, r, mode, pl);
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  if ((rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s))) return rc;
-  return enqueue_finish(c, d, r, dx, (const double*)c->dYw.p, nullptr, alpha, dout, s);
+  return enqueue_fg_full(c, pl, dx, nullptr, alpha, dout, s);
 }
 
 int mcp_set_kernel_timing(mcp_ctx* c, int enable) {

@@ -174,9 +174,7 @@ struct AdamRun {
   }
 
   int fg_on(mcp_ctx* v, const EvalPlan& pl, const double* x, double* out) {
-    int rc = enqueue_partial(v, pl, x, (double*)v->dYw.p, c->stream);
-    if (rc) return c->fail(rc, v->err);
-    rc = enqueue_finish(v, d, r, x, (const double*)v->dYw.p, nullptr, 0.0, out, c->stream);
+    int rc = enqueue_fg_full(v, pl, x, nullptr, 0.0, out, c->stream);
     if (rc) return c->fail(rc, v->err);
     return MCP_OK;
   }

@@ -45,6 +45,7 @@ struct mcp_ctx {
   double nu_const = 0.0;
 
   mcp_internal::DevBuf dx, dout, dYw, dAfrag, dYpart, dwpart, dG, dC, dpart, dscalar, dflag;
+  mcp_internal::DevBuf dM, du;  // fused-tail pieces (K1P): M = (A o lam) C, u = (G o C) lam
   void* hx = nullptr;
   size_t hx_bytes = 0;
   void* hout = nullptr;
@@ -122,6 +123,10 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
 // K4 : out = [f ; g_lam ; vec_F(g_A)] from x = [lam ; vec_F(A)] and [Y ; w]
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s);
+// A whole single-device evaluation x -> out: K1P + fused reduce/finish when available, else
+// partial (K1 -> K3) + finish (K4).  Scratch [Y ; w] in c->dYw.
+int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const double* alpha_dev,
+                    double alpha, double* dout, cudaStream_t s);
 
 // A context over rows gathered elsewhere (stochastic path): shares the parent's device and
 // stream, V (p_pad = round_up(p, 896) rows of pitch ldv, zero padded) is owned by the caller,

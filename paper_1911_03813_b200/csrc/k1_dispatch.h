@@ -33,10 +33,15 @@ struct K1Variant {
 // Choose the variant for (dtype, n, r, p_pad) on a device with `sms` SMs.
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v, std::string& why);
 
-// Launch K1 on stream s; returns 0 on success.
+// Launch K1 on stream s; returns 0 on success.  tail_lam / tail_M / tail_u (K1P only, r <= 32)
+// make the kernel also produce M = (A o lam) C and u = (G o C) lam for k_reduce_finish.
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
-              double* wpart, cudaStream_t s);
+              double* wpart, cudaStream_t s, const double* tail_lam = nullptr,
+              double* tail_M = nullptr, double* tail_u = nullptr);
+
+// True when K1 variant v can run the fused tail (K1P, r <= 32, A and G fit the P staging).
+bool k1_fuses_tail(const K1Variant& v, int64_t n, int r);
 
 // Row pitch (elements) the observation upload uses for dtype / n.
 int64_t obs_pitch(int dtype, int64_t n);

@@ -7,6 +7,7 @@
 #include "k1_fp64.cuh"
 #include "k1s_fp64.cuh"
 #include "k1p_fp64.cuh"
+#include "k1q_fp64.cuh"
 
 namespace mcp {
 namespace {
@@ -111,6 +112,23 @@ const EntryS kTableP[] = {MCP_K1P_COLS(1, 1),  MCP_K1P_COLS(2, 5),  MCP_K1P_COLS
                           MCP_K1P_COLS(8, 33)};
 std::atomic<bool> g_attr_p[kEntriesS];
 
+// ---------------- K1Q (warp-specialised pairs, fp64, n <= 128) ----------------
+template <int NTM, int TAIL, int MT2, int KH>
+void launch_q(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
+  k1q_fg_pairs<NTM, TAIL, MT2, KH><<<grid, K1Q_THREADS, smem, s>>>(prm);
+}
+#define MCP_K1Q_E(NTM, TAIL, MT2, KH) \
+  {NTM, TAIL, MT2, KH, &launch_q<NTM, TAIL, MT2, KH>, \
+   (const void*)&k1q_fg_pairs<NTM, TAIL, MT2, KH>}
+#define MCP_K1Q_COLS(MT2, KH) \
+  MCP_K1Q_E(1, 0, MT2, KH), MCP_K1Q_E(1, 1, MT2, KH), MCP_K1Q_E(1, 2, MT2, KH), \
+      MCP_K1Q_E(2, 0, MT2, KH)
+// (MT2, KH) groups by n: n <= 4, <= 20, <= 36, <= 68, <= 100, <= 116, <= 128 (MTH field = MT2)
+const EntryS kTableQ[] = {MCP_K1Q_COLS(1, 1),  MCP_K1Q_COLS(3, 5),  MCP_K1Q_COLS(5, 9),
+                          MCP_K1Q_COLS(9, 17), MCP_K1Q_COLS(13, 25), MCP_K1Q_COLS(15, 29),
+                          MCP_K1Q_COLS(16, 33)};
+std::atomic<bool> g_attr_q[kEntriesS];
+
 bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
   if (n > 128) return false;
   const int MT = (int)ceil_div(n, 8);
@@ -199,8 +217,11 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
 }
 
 // K1P: same column / m-tile split as K1S, a private ring of SP >= 2 slabs per pair.
-bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
+bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v,
+                  bool specialised) {
   if (n > 128) return false;
+  const EntryS* table = specialised ? kTableQ : kTableP;
+  std::atomic<bool>* attr = specialised ? g_attr_q : g_attr_p;
   const int MT = (int)ceil_div(n, 8);
   const int kst = (int)(ldv / 4);
   const int mth_need = (MT + 1) / 2, kh_need = kst;
@@ -210,13 +231,13 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   else { ntm = 2; tail = 0; }
   int e = -1;
   for (int i = 0; i < kEntriesS && e < 0; ++i)
-    if (kTableP[i].NTM == ntm && kTableP[i].TAIL == tail && kTableP[i].MTH >= mth_need &&
-        kTableP[i].KH >= kh_need)
+    if (table[i].NTM == ntm && table[i].TAIL == tail &&
+        table[i].MTH >= (specialised ? MT : mth_need) && table[i].KH >= kh_need)
       e = i;
   if (e < 0) return false;
   const int cw = 8 * ntm + tail;
   const size_t slab = (size_t)K1S_SR * ldv * 8;
-  const size_t fixed = k1p_fixed_bytes(kTableP[e].KH, ntm, cw);
+  const size_t fixed = k1p_fixed_bytes(table[e].KH, ntm, cw);
   const size_t budget = 227 * 1024 - 1024 - fixed;
   int SP = (int)(budget / ((size_t)K1P_PAIRS * (slab + 8)));
   if (SP > 4) SP = 4;
@@ -224,21 +245,21 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   const size_t ring_bytes = (size_t)K1P_PAIRS * SP * slab;
   const size_t stage_need = ((size_t)K1P_PAIRS * MT * 8 * cw + (size_t)2 * K1P_PAIRS * cw) * 8;
   if (ring_bytes < stage_need) return false;
-  const size_t smem = ring_bytes + fixed + 8 * (size_t)K1P_PAIRS * SP;
-  if (!g_attr_p[e].exchange(true)) {
-    if (cudaFuncSetAttribute(kTableP[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = ring_bytes + fixed + 8 * (size_t)K1P_PAIRS * (SP + 4);
+  if (!attr[e].exchange(true)) {
+    if (cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
       (void)cudaGetLastError();
-      g_attr_p[e].store(false);
+      attr[e].store(false);
       return false;
     }
   } else {
-    cudaFuncSetAttribute(kTableP[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
-  v.kind = 3;
+  v.kind = specialised ? 4 : 3;
   v.dtype = MCP_F64;
   v.RB = cw;
-  v.MTW = kTableP[e].MTH;
+  v.MTW = table[e].MTH;
   v.MT = MT;
   v.n_chunks = 0;
   v.n_pad = MT * 8;
@@ -259,13 +280,19 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   v.afrag_elems = 0;
   v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * cw;
   v.wpart_elems = (size_t)v.rbs * v.gp * cw;
-  v.name = "k1p_fg_pairs<f64,DMMA=" + std::to_string(8 * ntm) + ",DFMA=" +
-           std::to_string(tail) + ",MTH=" + std::to_string(kTableP[e].MTH) + ",KH=" +
-           std::to_string(kTableP[e].KH) + ",SP=" + std::to_string(SP) + ">";
+  v.name = std::string(specialised ? "k1q_fg_pairs" : "k1p_fg_pairs") + "<f64,DMMA=" +
+           std::to_string(8 * ntm) + ",DFMA=" + std::to_string(tail) +
+           (specialised ? ",MT2=" : ",MTH=") + std::to_string(table[e].MTH) + ",KH=" +
+           std::to_string(table[e].KH) + ",SP=" + std::to_string(SP) + ">";
   return true;
 }
 
 }  // namespace
+
+bool k1_fuses_tail(const K1Variant& v, int64_t n, int r) {
+  return (v.kind == 3 || v.kind == 4) && r <= 32 &&
+         (size_t)(n * r + (int64_t)r * r) <= k1p_pstage_elems(v.RB);
+}
 
 int64_t obs_pitch(int dtype, int64_t n) {
   if (dtype == MCP_F64) {
@@ -280,8 +307,12 @@ int64_t obs_pitch(int dtype, int64_t n) {
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v,
                std::string& why) {
   v = K1Variant();
+  if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1Q") &&
+      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, true))
+    return true;
+  v = K1Variant();
   if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1P") &&
-      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v))
+      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, false))
     return true;
   v = K1Variant();
   if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1S") &&
@@ -338,9 +369,10 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
 
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
-              double* wpart, cudaStream_t s) {
+              double* wpart, cudaStream_t s, const double* tail_lam, double* tail_M,
+              double* tail_u) {
   if (v.entry < 0) return 1;
-  if (v.kind == 1 || v.kind == 3) {
+  if (v.kind == 1 || v.kind == 3 || v.kind == 4) {
     K1SParams sp;
     sp.V = static_cast<const double*>(dV);
     sp.ldv = ldv;
@@ -358,7 +390,13 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     sp.spc = v.MTW2;
     sp.Ypart = Ypart;
     sp.wpart = wpart;
-    (v.kind == 1 ? kTableS : kTableP)[v.entry].launch(sp, v.grid, v.smem, s);
+    if ((v.kind == 3 || v.kind == 4) && tail_lam) {
+      sp.lam = tail_lam;
+      sp.M = tail_M;
+      sp.u = tail_u;
+    }
+    (v.kind == 1 ? kTableS : v.kind == 3 ? kTableP : kTableQ)[v.entry].launch(sp, v.grid, v.smem,
+                                                                               s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }
   K1Params prm;

@@ -29,10 +29,58 @@ constexpr int K1P_PAIRS = 6;
 constexpr int K1P_THREADS = 2 * K1P_PAIRS * 32;   // 384: 3 warps per sub-partition
 constexpr int K1P_MAXREG = 168;                    // 16384 / (3 * 32), rounded down to 8
 
+// doubles of P staging, reused as the fused-tail scratch before the first epilogue
+__host__ __device__ constexpr size_t k1p_pstage_elems(int cw) {
+  return (size_t)K1P_PAIRS * 2 * K1S_SR * k1s_pp(cw);
+}
+
 // fixed smem bytes besides the rings (factor fragments, tail factor, P staging)
 __host__ __device__ inline size_t k1p_fixed_bytes(int kh, int ntm, int cw) {
   return (size_t)kh * ntm * 32 * 8 + (size_t)kh * 16 * 8 +
          (size_t)K1P_PAIRS * 2 * K1S_SR * k1s_pp(cw) * 8;
+}
+
+// A (n x r) and then G = A^T A, C = G^(d-1) in smem scratch (warp per entry, lanes over rows,
+// fixed butterfly -- the order of k_tail_fused), then this CTA's rows of M = (A o lam) C and,
+// in CTA 0, u = (G o C) lam.  The caller guarantees n r + r^2 <= scratch capacity.
+__device__ __forceinline__ void k1p_tail_pre(const K1SParams& prm, double* scratch) {
+  const int n = prm.n, r = prm.r, d = prm.d;
+  const double* lam = prm.lam;
+  double* sA = scratch;           // n x r column-major
+  double* sC = scratch + n * r;   // G, then C
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) sA[e] = prm.A[e];
+  __syncthreads();
+  for (int pr = warp; pr < r * r; pr += nw) {
+    const int j = pr / r, k = pr % r;
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += sA[j * n + i] * sA[k * n + i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) sC[pr] = s;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+      double u = 0.0;
+      for (int k = 0; k < r; ++k) {
+        const double gjk = sC[j * r + k];
+        u += (gjk * rm_pow(gjk, d - 1)) * lam[k];
+      }
+      prm.u[j] = u;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) sC[e] = rm_pow(sC[e], d - 1);
+  __syncthreads();
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int i0 = min(n, (int)blockIdx.x * per), i1 = min(n, i0 + per);
+  for (int e = threadIdx.x; e < (i1 - i0) * r; e += blockDim.x) {
+    const int j = e / (i1 - i0), i = i0 + e % (i1 - i0);
+    double m = 0.0;
+    for (int k = 0; k < r; ++k) m += (sA[k * n + i] * lam[k]) * sC[k * r + j];
+    prm.M[(int64_t)j * n + i] = m;
+  }
 }
 
 template <int NTM, int TAIL, int MTH, int KH>
@@ -96,6 +144,12 @@ __global__ void __maxnreg__(K1P_MAXREG) k1p_fg_pairs(K1SParams prm) {
       tma_bulk_g2s(my_ring + (size_t)s * slab_elems, src0 + s * slab_stride, slab_bytes,
                    &my_full[s]);
     }
+  }
+  // Y-independent tail pieces (reference implicit.py:147-149, objective.py:55) while the first
+  // slabs are in flight; the P staging area is free until the first epilogue.
+  if (prm.lam) {
+    k1p_tail_pre(prm, sP);
+    __syncthreads();
   }
 
   const int mbase = h * MTH;

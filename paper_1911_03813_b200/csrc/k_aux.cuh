@@ -31,7 +31,7 @@ __global__ void k_prep_afrag(const double* __restrict__ A, int n, int r, int RB,
 // Output Yw = [vec_F(Y) (n*r) ; w (r)], the additive piece all-reduced across ranks.
 // Block = 32 consecutive outputs x 8 partial-groups: thread (tx, ty) sums partials
 // q = ty, ty+8, ... (coalesced 256-byte rows), then ty = 0 adds the 8 group sums in order.
-constexpr int K3_X = 32, K3_Y = 8;
+constexpr int K3_X = 32, K3_Y = 32;
 __global__ void __launch_bounds__(K3_X * K3_Y)
     k_reduce_partials(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
                       int r, int n_pad, int RB, int rbs, int gp, double* __restrict__ Yw) {
@@ -73,6 +73,83 @@ __global__ void __launch_bounds__(K3_X * K3_Y)
       Yw[dst] = t;
     }
     __syncthreads();
+  }
+}
+
+// K3F: the fixed-order partial reduce of K3 fused with the finish (objective.py:51-56) when
+// K1P already produced M = (A o lam) C and u = (G o C) lam: g_A = -2d (Y - M) o lam is
+// elementwise on the reduced Y, g_lam = -2 (w - u), and f = alpha + lam.u - 2 w.lam (r <= 32:
+// one block holds every w).  out = [f ; g_lam ; vec_F(g_A)], bitwise the k_tail_fused result.
+__global__ void __launch_bounds__(K3_X * K3_Y)
+    k_reduce_finish(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
+                    int r, int n_pad, int RB, int rbs, int gp, const double* __restrict__ x,
+                    const double* __restrict__ M, const double* __restrict__ u, int d,
+                    const double* __restrict__ alpha_dev, double alpha_host,
+                    double* __restrict__ out) {
+  __shared__ double s_acc[K3_Y][K3_X];
+  __shared__ double s_w[K3_X];
+  const int tx = threadIdx.x % K3_X, ty = threadIdx.x / K3_X;
+  const double* lam = x;
+  const int per_rb = n * RB;
+  const int yblocks = (per_rb + K3_X - 1) / K3_X;
+  const int64_t total_blocks = (int64_t)rbs * yblocks + 1;   // + the w / f block
+  const double s2d = -2.0 * d;
+  for (int64_t blk = blockIdx.x; blk < total_blocks; blk += gridDim.x) {
+    double s = 0.0;
+    if (blk < (int64_t)rbs * yblocks) {
+      const int rb = blk / yblocks;
+      const int e = (blk % yblocks) * K3_X + tx;
+      int64_t dst = -1;
+      int j = 0;
+      if (e < per_rb) {
+        const int i = e / RB, jl = e % RB;
+        j = rb * RB + jl;
+        const double* src = Ypart + ((size_t)rb * gp * n_pad + i) * RB + jl;
+#pragma unroll 4
+        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * n_pad * RB];
+        if (j < r) dst = (int64_t)j * n + i;
+      }
+      s_acc[ty][tx] = s;
+      __syncthreads();
+      if (ty == 0 && dst >= 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int y = 0; y < K3_Y; ++y) t += s_acc[y][tx];
+        out[1 + r + dst] = (s2d * (t - M[dst])) * lam[j];
+      }
+      __syncthreads();
+    } else {
+      // w (r <= 32 < K3_X): reduce, then g_lam and f
+      const int k = tx;   // k = rb * RB + jl
+      int j = r;
+      if (k < rbs * RB) {
+        const int rb = k / RB, jl = k % RB;
+        j = rb * RB + jl;
+        const double* src = wpart + (size_t)rb * gp * RB + jl;
+#pragma unroll 4
+        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * RB];
+      }
+      s_acc[ty][tx] = s;
+      __syncthreads();
+      if (ty == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int y = 0; y < K3_Y; ++y) t += s_acc[y][tx];
+        if (j < r) {
+          s_w[j] = t;
+          out[1 + j] = -2.0 * (t - u[j]);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double lu = 0.0, wl = 0.0;
+        for (int jj = 0; jj < r; ++jj) lu += lam[jj] * u[jj];
+        for (int jj = 0; jj < r; ++jj) wl += s_w[jj] * lam[jj];
+        const double alpha = alpha_dev ? *alpha_dev : alpha_host;
+        out[0] = alpha + lu - 2.0 * wl;
+      }
+      __syncthreads();
+    }
   }
 }
 

@@ -456,9 +456,7 @@ struct LbRun {
 
   // fg(x) -> out on the context stream (K1 -> K3 -> K4)
   int enqueue_fg(const double* x, double* out) {
-    int rc = enqueue_partial(c, pl, x, Yw, c->stream);
-    if (rc) return rc;
-    return enqueue_finish(c, d, r, x, Yw, nullptr, alpha, out, c->stream);
+    return enqueue_fg_full(c, pl, x, nullptr, alpha, out, c->stream);
   }
 
   int enqueue_direction_and_probe() {

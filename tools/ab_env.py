@@ -1,0 +1,59 @@
+"""In-process A/B of environment toggles on the device-resident f+grad loop (kernel experiments).
+
+  python tools/ab_env.py --config c2 --steps 50 --reps 5 VAR=VALUE [VAR2=VALUE ...]
+Alternates the baseline (no toggles) and each toggle, CUDA-event timed, and prints the median
+ms/step of each.  Toggles are read by the library at launch time (e.g. MCP_NO_FUSED_TAIL=1).
+"""
+import argparse
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_1911_03813_b200 as mcp  # noqa: E402
+from paper_1911_03813_b200 import _native, synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--steps", type=int, default=50)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--mode", default=None)
+ap.add_argument("toggles", nargs="*")
+a = ap.parse_args()
+cfg = synth.CONFIGS[a.config]
+V = synth.device_observations(cfg, 2024)
+obs = mcp.ObservationSet.from_device(V, p_total=V.shape[0])
+ctx = obs.device_context()
+lam, A = synth.initial_point(cfg, 2024)
+x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
+out = torch.empty(1 + cfg.r + cfg.n * cfg.r, dtype=torch.float64, device="cuda")
+stream = torch.cuda.current_stream()
+sh = _native.stream_handle(stream)
+variants = [("base", {})] + [(t, dict([t.split("=", 1)])) for t in a.toggles]
+res = {name: [] for name, _ in variants}
+outs = {}
+for rep in range(a.reps):
+    for name, env in variants:
+        for k, v in env.items():
+            os.environ[k] = v
+        for _ in range(3):
+            ctx.fg_device(cfg.d, cfg.r, x.data_ptr(), 0.0, a.mode, out.data_ptr(), sh)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            ctx.fg_device(cfg.d, cfg.r, x.data_ptr(), 0.0, a.mode, out.data_ptr(), sh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res[name].append(e0.elapsed_time(e1) / a.steps)
+        outs[name] = out.clone()
+        for k in env:
+            del os.environ[k]
+for name, _ in variants:
+    v = res[name]
+    same = torch.equal(outs[name], outs["base"])
+    print(f"{name:30s} median {statistics.median(v):.4f} ms  min {min(v):.4f}  "
+          f"bitwise_equal_to_base={same}  variant={ctx.last_variant}")

@@ -21,6 +21,17 @@ namespace mcp {
 constexpr int K1Q_PAIRS = 6;
 constexpr int K1Q_THREADS = 2 * K1Q_PAIRS * 32;
 constexpr int K1Q_MAXREG = 168;
+#ifndef MCP_K1Q_ODD_CHAINS
+#define MCP_K1Q_ODD_CHAINS 0   // 1: GEMM1 with separate even / odd k-step chains (no gain)
+#endif
+#ifndef MCP_K1Q_L2_AHEAD
+#define MCP_K1Q_L2_AHEAD 1     // slabs beyond the ring prefetched into L2 (0: off)
+#endif
+
+// L2 prefetch of a global range (bulk, no smem destination)
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 
 __host__ __device__ inline size_t k1q_fixed_bytes(int kh, int ntm, int cw) {
   return (size_t)kh * ntm * 32 * 8 + (size_t)kh * 16 * 8 +
@@ -75,7 +86,11 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
   __syncthreads();
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 
-  const int q = warp >> 1, h = warp & 1;
+  // roles: warp w sits on sub-partition w % 4; alternate the roles along each sub-partition so
+  // every FP64 pipe serves a mix of the (heavier) GEMM1 warps and the GEMM2 warps:
+  // GEMM1 warps {0, 2, 5, 7, 8, 10}, GEMM2 warps {1, 3, 4, 6, 9, 11}; pair q = q-th of each.
+  const int h = ((warp & 3) + (warp >> 2)) & 1;
+  const int q = ((warp >> 2) * 4 + (warp & 3)) >> 1;   // rank of w within its role list
   const int64_t my_slabs =
       pg < prm.num_slabs ? (prm.num_slabs - pg + prm.gp - 1) / prm.gp : 0;
   const int64_t n_mine = my_slabs > q ? (my_slabs - q + NP - 1) / NP : 0;
@@ -93,6 +108,8 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
       tma_bulk_g2s(my_ring + (size_t)s * slab_elems, src0 + s * slab_stride, slab_bytes,
                    &my_full[s]);
     }
+    for (int a = 0; a < MCP_K1Q_L2_AHEAD; ++a)
+      if (SP + a < n_mine) l2_prefetch_bulk(src0 + (SP + a) * slab_stride, slab_bytes);
   }
   if (prm.lam) {
     k1p_tail_pre(prm, sP);
@@ -117,11 +134,13 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
         ph ^= 1;
       }
       const int64_t row0 = ((int64_t)pg + (q + i * NP) * (int64_t)prm.gp) * K1S_SR;
-      double z[2][NTM][2], zt[2][TL];
+      // two m-tiles x (even, odd k-steps) = 4 independent DMMA chains per column tile
+      double z[2][NTM][2], zo[2][NTM][2], zt[2][TL];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
-        for (int nt = 0; nt < NTM; ++nt) z[mt][nt][0] = z[mt][nt][1] = 0.0;
+        for (int nt = 0; nt < NTM; ++nt)
+          z[mt][nt][0] = z[mt][nt][1] = zo[mt][nt][0] = zo[mt][nt][1] = 0.0;
 #pragma unroll
         for (int c = 0; c < TL; ++c) zt[mt][c] = 0.0;
       }
@@ -147,8 +166,13 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
         }
 #pragma unroll
         for (int nt = 0; nt < NTM; ++nt) {
-          dmma884(z[0][nt], a0c, b_c[nt]);
-          dmma884(z[1][nt], a1c, b_c[nt]);
+          if (MCP_K1Q_ODD_CHAINS && (kk & 1)) {
+            dmma884(zo[0][nt], a0c, b_c[nt]);
+            dmma884(zo[1][nt], a1c, b_c[nt]);
+          } else {
+            dmma884(z[0][nt], a0c, b_c[nt]);
+            dmma884(z[1][nt], a1c, b_c[nt]);
+          }
         }
         if constexpr (TAIL > 0) {
           zt[0][0] = fma(a0c, t_c.x, zt[0][0]);
@@ -166,6 +190,13 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
           t_c = t_n;
         }
       }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTM; ++nt) {
+          z[mt][nt][0] += zo[mt][nt][0];
+          z[mt][nt][1] += zo[mt][nt][1];
+        }
       // the P slot of slab i was last read by GEMM2 of slab i - 2
       const int b = (int)(i & 1);
       if (i >= 2) mbar_wait(&my_pempty[b], (uint32_t)(((i - 2) >> 1) & 1));
@@ -281,6 +312,8 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
         mbar_arrive_expect_tx(&my_full[s], slab_bytes);
         tma_bulk_g2s(my_ring + (size_t)s * slab_elems, src0 + (i + SP) * slab_stride, slab_bytes,
                      &my_full[s]);
+        if (MCP_K1Q_L2_AHEAD > 0 && i + SP + MCP_K1Q_L2_AHEAD < n_mine)
+          l2_prefetch_bulk(src0 + (i + SP + MCP_K1Q_L2_AHEAD) * slab_stride, slab_bytes);
       }
       if (++s == SP) {
         s = 0;

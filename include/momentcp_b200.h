@@ -137,7 +137,7 @@ int mcp_fg_device(mcp_ctx* ctx, int d, int r, const double* dx, double alpha, in
  * graph capture is bracketed by CUDA events on its own stream.  mcp_kernel_time_ms waits for
  * them and returns the summed duration and launch count (reset != 0 clears the record).
  */
-int mcp_set_kernel_timing(mcp_ctx* ctx, int enable);
+int mcp_set_kernel_timing(mcp_ctx* ctx, int enable);   /* enable > 1: time every enable-th launch */
 int mcp_kernel_time_ms(mcp_ctx* ctx, double* total_ms, int* launches, int reset);
 
 /*

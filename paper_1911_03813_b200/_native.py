@@ -167,8 +167,10 @@ class Context:
         return self._lib.mcp_last_variant(self._h).decode()
 
     # -- kernel timing (bench) ------------------------------------------------------------
-    def set_kernel_timing(self, enable: bool) -> None:
-        self._check(self._lib.mcp_set_kernel_timing(self._h, int(bool(enable))), "timing")
+    def set_kernel_timing(self, enable, every: int = 1) -> None:
+        """enable: time K1/K5 launches with CUDA events; every > 1 samples one launch in every."""
+        code = (max(int(every), 1) if every > 1 else 1) if enable else 0
+        self._check(self._lib.mcp_set_kernel_timing(self._h, code), "timing")
 
     def kernel_time_ms(self, reset: bool = True) -> tuple[float, int]:
         ms = ctypes.c_double()

@@ -91,6 +91,7 @@ void drop_graphs(mcp_ctx* c) {
 // Event pair bracketing one timed kernel launch (only when timing is on and not capturing).
 std::pair<cudaEvent_t, cudaEvent_t>* timing_begin(mcp_ctx* c, cudaStream_t s) {
   if (!c->timing) return nullptr;
+  if ((c->timing_seen++ % c->timing_every) != 0) return nullptr;
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone)
     return nullptr;
@@ -863,6 +864,8 @@ int mcp_set_kernel_timing(mcp_ctx* c, int enable) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
   c->timing = enable != 0;
+  c->timing_every = enable > 1 ? enable : 1;
+  c->timing_seen = 0;
   return MCP_OK;
 }
 

@@ -63,6 +63,8 @@ struct mcp_ctx {
 
   std::map<std::tuple<int, int, int>, mcp_internal::GraphEntry> graphs;
   bool timing = false;
+  int timing_every = 1;      // time one K1/K5 launch in every timing_every (sampling)
+  int64_t timing_seen = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
   int last_launches = 0;
   std::string variant = "none";

@@ -21,6 +21,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--mode", default=None)
+ap.add_argument("--timing", action="store_true", help="per-launch kernel event timing on")
 ap.add_argument("toggles", nargs="*")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
@@ -32,6 +33,8 @@ x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
 out = torch.empty(1 + cfg.r + cfg.n * cfg.r, dtype=torch.float64, device="cuda")
 stream = torch.cuda.current_stream()
 sh = _native.stream_handle(stream)
+if a.timing:
+    ctx.set_kernel_timing(True)
 variants = [("base", {})] + [(t, dict([t.split("=", 1)])) for t in a.toggles]
 res = {name: [] for name, _ in variants}
 outs = {}

@@ -78,6 +78,7 @@ void drop_graphs(mcp_ctx* c) {
     if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
   }
   c->graphs.clear();
+  c->tail_x = nullptr;
   if (c->lbfgs_ws) {
     c->lbfgs_ws_free(c->lbfgs_ws);
     c->lbfgs_ws = nullptr;
@@ -321,10 +322,11 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
 
 // prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows.
 int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool tail_pieces) {
   if (pl.mode == MCP_MODE_TF32X3) return enqueue_partial_tf32(c, pl, dx, dYw, s);
   const K1Variant& v = pl.k1;
   const int n = (int)c->n, r = pl.r;
+  const bool tp = tail_pieces && k1_fuses_tail(v, c->n, r);
   int launches = 2;
   if (v.needs_prep()) {
     k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(
@@ -334,13 +336,17 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   auto* ev = timing_begin(c, s);
   int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r,
                      (const double*)c->dAfrag.p, pl.d, (double*)c->dYpart.p, (double*)c->dwpart.p,
-                     s);
+                     s, tp ? dx : nullptr, tp ? (double*)c->dM.p : nullptr,
+                     tp ? (double*)c->du.p : nullptr);
   timing_end(ev, s);
   if (rc) {
     const cudaError_t e = cudaGetLastError();
     return c->fail(MCP_ERR_CUDA, std::string("K1 launch failed (") + v.name + "): " +
                                      cudaGetErrorString(e));
   }
+  c->tail_x = tp ? dx : nullptr;   // M, u valid for this x until the next partial
+  c->tail_d = pl.d;
+  c->tail_r = r;
   const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) +
                              ceil_div((int64_t)v.rbs * v.RB, K3_X);
   k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
@@ -377,6 +383,17 @@ int enqueue_finish_yw(mcp_ctx* c, int d, int r, const double* dx, const double* 
 
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
+  if (c->tail_x && c->tail_x == dx && c->tail_d == d && c->tail_r == r &&
+      !getenv("MCP_NO_FUSED_TAIL")) {
+    // M and u came with the partial: the finish is elementwise (K4L)
+    const int n = (int)c->n;
+    k_finish_light<<<(int)ceil_div((int64_t)n * r, 256) + 1, 256, 0, s>>>(
+        dx, dYw, dYw + (int64_t)n * r, (const double*)c->dM.p, (const double*)c->du.p, n, r, d,
+        alpha_dev, alpha, dout);
+    CUDA_TRY(c, cudaGetLastError());
+    c->last_launches += 1;
+    return MCP_OK;
+  }
   return enqueue_finish_yw(c, d, r, dx, dYw, dYw + c->n * r, alpha_dev, alpha, dout, s);
 }
 
@@ -384,7 +401,7 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
                     double alpha, double* dout, cudaStream_t s) {
   const int r = pl.r;
   if (pl.mode != MCP_MODE_FP64 || !k1_fuses_tail(pl.k1, c->n, r) || getenv("MCP_NO_FUSED_TAIL")) {
-    int rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s);
+    int rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s, false);
     if (rc) return rc;
     return enqueue_finish(c, pl.d, r, dx, (const double*)c->dYw.p, alpha_dev, alpha, dout, s);
   }
@@ -829,7 +846,7 @@ int mcp_fg_partial_device(mcp_ctx* c, int d, int r, const double* dx, int mode, 
   int rc = plan_eval(c, d, r, mode, pl);
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  return enqueue_partial(c, pl, dx, dYw, s);
+  return enqueue_partial(c, pl, dx, dYw, s, true);
 }
 
 int mcp_fg_finish_device(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,

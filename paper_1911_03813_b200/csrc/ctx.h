@@ -46,6 +46,8 @@ struct mcp_ctx {
 
   mcp_internal::DevBuf dx, dout, dYw, dAfrag, dYpart, dwpart, dG, dC, dpart, dscalar, dflag;
   mcp_internal::DevBuf dM, du;  // fused-tail pieces (K1P): M = (A o lam) C, u = (G o C) lam
+  const double* tail_x = nullptr;  // x whose M, u are in dM / du (set by a tail-piece partial)
+  int tail_d = 0, tail_r = 0;
   void* hx = nullptr;
   size_t hx_bytes = 0;
   void* hout = nullptr;
@@ -120,8 +122,10 @@ int ensure(mcp_ctx* c, DevBuf& b, size_t bytes);
 int ensure_host(mcp_ctx* c, void*& p, size_t& have, size_t bytes);
 int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl);
 // prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows (stream-ordered, capturable)
+// tail_pieces: K1Q/K1P also leave M = (A o lam) C and u = (G o C) lam in c->dM / c->du so that
+// the following enqueue_finish of the same x is elementwise (the sharded path's finish).
 int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
-                    cudaStream_t s);
+                    cudaStream_t s, bool tail_pieces = false);
 // K4 : out = [f ; g_lam ; vec_F(g_A)] from x = [lam ; vec_F(A)] and [Y ; w]
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s);

@@ -331,3 +331,42 @@ def test_batched_matches_single_starts(n, p, r, d, k):
         assert _err(F[s], f1, f_s) <= 1e-13 and _err(G[s], g1, scale) <= 1e-13
         fo, go = om.packed_fg(V, nu, d, r, 0.5)(X[s])
         assert _err(F[s], fo, f_s) <= FG_TOL and _err(G[s], go, scale) <= FG_TOL
+
+
+def test_partial_then_finish_equals_single_evaluation_bitwise():
+    """The sharded building blocks on one rank: partial (K1 + reduce, leaving M and u when the
+    kernel fuses the tail) then finish must reproduce the single-call evaluation bitwise, with
+    and without the fused tail (both compute G, C, M, u and the finish in the same order)."""
+    import os
+
+    import torch
+
+    from paper_1911_03813_b200 import _native
+
+    rng = np.random.default_rng(21)
+    for n, r in ((20, 5), (100, 10), (64, 16), (30, 20)):
+        V = rng.standard_normal((n, 3000))
+        lam, A = rng.standard_normal(r), rng.standard_normal((n, r))
+        obs = mcp.ObservationSet(V)
+        ctx = obs.device_context()
+        x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
+        s = _native.stream_handle(torch.cuda.current_stream())
+        outs = []
+        for fused in (True, False):
+            if not fused:
+                os.environ["MCP_NO_FUSED_TAIL"] = "1"
+            try:
+                Yw = torch.empty(n * r + r, dtype=torch.float64, device="cuda")
+                o1 = torch.empty(1 + r + n * r, dtype=torch.float64, device="cuda")
+                o2 = torch.empty_like(o1)
+                ctx.fg_partial_device(3, r, x.data_ptr(), None, Yw.data_ptr(), s)
+                ctx.fg_finish_device(3, r, x.data_ptr(), Yw.data_ptr(), 0.25, o1.data_ptr(), s)
+                ctx.fg_device(3, r, x.data_ptr(), 0.25, None, o2.data_ptr(), s)
+                torch.cuda.synchronize()
+                assert torch.equal(o1, o2), (n, r, fused)
+                outs.append(o1.cpu())
+            finally:
+                os.environ.pop("MCP_NO_FUSED_TAIL", None)
+        assert torch.equal(outs[0], outs[1]), (n, r)
+        res = mcp.fg_implicit(obs, lam, A, 3, 0.25)
+        assert float(outs[0][0]) == res.f

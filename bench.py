@@ -421,8 +421,8 @@ def main():
     bound = "hbm" if ai < ridge else "tensor"
     traffic = None
     prof = _read_json(os.path.join(ROOT, "profiles", f"ncu_k1_{cfg.name}_r01.json"))
-    if prof and prof.get("variant") == variant:
-        traffic = prof.get("dram_bytes_per_launch")
+    if prof and prof.get("variant") == variant and world == 1:
+        traffic = prof.get("dram_bytes_per_launch")   # captured at N = 1 (the full row range)
     value = args.steps / (ms_total * 1e-3)
     step_flops = 4.0 * n * cfg.p * r
     line = {

@@ -322,14 +322,49 @@ def main():
     out = torch.empty(1 + r + n * r, dtype=torch.float64, device=dev)
     stream = _native.stream_handle(torch.cuda.current_stream(dev))
 
+    def step_nccl():
+        ctx.fg_partial_device(d, r, x_dev.data_ptr(), args.mode, Yw.data_ptr(), stream)
+        dist.all_reduce(Yw, op=dist.ReduceOp.SUM)
+        ctx.fg_finish_device(d, r, x_dev.data_ptr(), Yw.data_ptr(), 0.0, out.data_ptr(), stream)
+
+    # multi-GPU exchange: NVLink peer memory fused with the finish (csrc/peer.cu), verified
+    # against the NCCL all-reduce path once; NCCL stays the fallback
+    pex, exchange = None, "none"
+    if world > 1:
+        exchange = "nccl-allreduce"
+        if not same_dev and os.environ.get("MCP_PEER", "1") != "0":
+            try:
+                pex = D.PeerExchange(ctx, n, r, rank, world, group)
+            except Exception as exc:  # noqa: BLE001 - NCCL path stays
+                print(f"peer exchange unavailable: {exc}", file=sys.stderr)
+                pex = None
+            ok_t = torch.tensor([1.0 if pex is not None else 0.0], device=dev)
+            dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+            if float(ok_t.item()) == 0.0:
+                pex = None
+            else:
+                step_nccl()
+                torch.cuda.synchronize()
+                ref_out = out.clone()
+                pex.step(d, x_dev.data_ptr(), args.mode, 0.0, out.data_ptr(), stream)
+                torch.cuda.synchronize()
+                bad = pex.failed() or not torch.allclose(out, ref_out, rtol=1e-12, atol=1e-300)
+                bad_t = torch.tensor([1.0 if bad else 0.0], device=dev)
+                dist.all_reduce(bad_t, op=dist.ReduceOp.MAX)
+                if float(bad_t.item()) == 0.0:
+                    exchange = "nvlink-peer (fused reduce+finish, csrc/peer.cu)"
+                else:
+                    print("peer exchange self-test failed; using the NCCL all-reduce",
+                          file=sys.stderr)
+                    pex = None
+
     def step_device():
         if world == 1:
             ctx.fg_device(d, r, x_dev.data_ptr(), 0.0, args.mode, out.data_ptr(), stream)
+        elif pex is not None:
+            pex.step(d, x_dev.data_ptr(), args.mode, 0.0, out.data_ptr(), stream)
         else:
-            ctx.fg_partial_device(d, r, x_dev.data_ptr(), args.mode, Yw.data_ptr(), stream)
-            dist.all_reduce(Yw, op=dist.ReduceOp.SUM)
-            ctx.fg_finish_device(d, r, x_dev.data_ptr(), Yw.data_ptr(), 0.0, out.data_ptr(),
-                                 stream)
+            step_nccl()
 
     def barrier_sync():
         torch.cuda.synchronize()
@@ -377,7 +412,7 @@ def main():
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     k1_ms, k1_launches = ctx.kernel_time_ms(reset=True)
     ctx.set_kernel_timing(False)
-    launches_per_step = ctx.last_launch_count if world == 1 else 6
+    launches_per_step = ctx.last_launch_count if world == 1 else (4 if pex is not None else 6)
     variant = ctx.last_variant
     clk = clocks.stop() if rank == 0 else None
 
@@ -432,7 +467,7 @@ def main():
         "dtype": "f64" if args.mode == "fp64" else "tf32x3 (fp32 data, fp64 epilogue/tail)",
         "data": f"synthetic seeded Gaussian mixture ({cfg.name}), generated on GPU",
         "config": dict(_config_dict(cfg, args, world), kernel=variant,
-                       upload_s=round(t_up, 4)),
+                       upload_s=round(t_up, 4), exchange=exchange),
         "tflops": {"achieved": step_flops * value / 1e12, "peak": fp64_peak,
                    "peak_kind": "measured DMMA.8x8x4 FP64 (profiles/peaks_fp64_tf32_r01.json)",
                    "frac": step_flops * value / 1e12 / fp64_peak,

@@ -188,6 +188,24 @@ int mcp_adam(mcp_ctx* ctx, int d, int r, int mode, const double* x0, const doubl
              double* x_out, double* g_out, double* f_out, double* trace_f, double* trace_t,
              int64_t trace_cap, int64_t* info);
 
+/*
+ * Peer-memory exchange of the additive [vec_F(Y) | w] pieces for the row-sharded path
+ * (SURVEY.md 8e), replacing all-reduce + mcp_fg_finish_device.  Buffers are symmetric
+ * (peer-mapped over NVLink, e.g. torch symmetric memory); all pointers are device pointers.
+ *   mcp_peer_signal(ctx, flag_ptrs, rank, world, epoch, stream): flag_ptrs is a device array of
+ *     `world` int64* (every rank's flag array); stores epoch at [rank] of each, release.sys,
+ *     after this rank's partial (mcp_fg_partial_device into its slot) in stream order.
+ *   mcp_peer_reduce_finish(ctx, d, r, dx, part_ptrs, my_flags, world, epoch, alpha, dout, derr,
+ *     stream): waits for my_flags[k] >= epoch for all k (bounded; sets *derr = 1 on timeout),
+ *     sums the world partials part_ptrs[0..world-1] in rank order and writes
+ *     dout = [f ; g_lam ; vec_F(g_A)] (the same on every rank).
+ */
+int mcp_peer_signal(mcp_ctx* ctx, const void* flag_ptrs, int rank, int world, int64_t epoch,
+                    void* stream);
+int mcp_peer_reduce_finish(mcp_ctx* ctx, int d, int r, const double* dx, const void* part_ptrs,
+                           const int64_t* my_flags, int world, int64_t epoch, double alpha,
+                           double* dout, int* derr, void* stream);
+
 /* Kernel launches issued by the last evaluation call (for the bench's gpu_launches claim). */
 int mcp_last_launch_count(const mcp_ctx* ctx);
 

@@ -74,6 +74,11 @@ SIGNATURES = {
     "mcp_adam": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_void_p,
                                 _c_void_p, _c_void_p, _i64, SampleFn, _c_void_p, _c_void_p,
                                 _c_void_p, _dp, _c_void_p, _c_void_p, _i64, _c_void_p]),
+    "mcp_peer_signal": (ctypes.c_int, [_c_void_p, _c_void_p, ctypes.c_int, ctypes.c_int, _i64,
+                                       _c_void_p]),
+    "mcp_peer_reduce_finish": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                              _c_void_p, _c_void_p, ctypes.c_int, _i64,
+                                              ctypes.c_double, _c_void_p, _c_void_p, _c_void_p]),
     "mcp_last_launch_count": (ctypes.c_int, [_c_void_p]),
     "mcp_last_variant": (ctypes.c_char_p, [_c_void_p]),
 }
@@ -322,6 +327,19 @@ class Context:
         return {"x": x, "g": g, "f": f.value, "n_iter": int(info[0]),
                 "reason": ("iteration cap", "learning-rate exhausted")[int(info[1])],
                 "trace": list(zip(tf[:k].tolist(), tt[:k].tolist()))}
+
+    def peer_signal(self, flag_ptrs_dev: int, rank: int, world: int, epoch: int, stream_ptr):
+        rc = self._lib.mcp_peer_signal(self._h, ctypes.c_void_p(flag_ptrs_dev), int(rank),
+                                       int(world), int(epoch), ctypes.c_void_p(stream_ptr))
+        self._check(rc, "mcp_peer_signal")
+
+    def peer_reduce_finish(self, d, r, dx_ptr, part_ptrs_dev, my_flags_ptr, world, epoch, alpha,
+                           dout_ptr, derr_ptr, stream_ptr):
+        rc = self._lib.mcp_peer_reduce_finish(
+            self._h, int(d), int(r), ctypes.c_void_p(dx_ptr), ctypes.c_void_p(part_ptrs_dev),
+            ctypes.c_void_p(my_flags_ptr), int(world), int(epoch), float(alpha),
+            ctypes.c_void_p(dout_ptr), ctypes.c_void_p(derr_ptr), ctypes.c_void_p(stream_ptr))
+        self._check(rc, "mcp_peer_reduce_finish")
 
     def ttsv_batch(self, A_fortran: np.ndarray, d: int, mode: str | None) -> np.ndarray:
         n, r = A_fortran.shape

@@ -1,0 +1,162 @@
+// Cross-GPU exchange of the additive [vec_F(Y) | w] pieces over NVLink peer memory, fused with
+// the finish (replaces the NCCL all-reduce + tail of the row-sharded path).
+//
+// Every rank's partial lives in a symmetric (peer-mapped) buffer, two slots by epoch parity.
+//   mcp_peer_signal:          after this rank's partial is complete (stream order), publish
+//                             `epoch` into every rank's flag array at index `rank`
+//                             (threadfence.system + st.release.sys);
+//   mcp_peer_reduce_finish:   wait until every rank's flag for this epoch is set (ld.acquire.sys,
+//                             bounded), sum the W partials in rank order 0..W-1 straight from
+//                             peer memory, and finish: with the tail pieces M, u of this rank's
+//                             partial the finish is elementwise (g_A = -2d (Y - M) o lam,
+//                             g_lam = -2 (w - u), f), otherwise the summed piece goes through the
+//                             regular tail.  Every rank sums in the same order, so all ranks hold
+//                             bitwise identical f and gradients.
+// Slot reuse is safe with two slots: a rank overwrites slot e % 2 at epoch e + 2 only after
+// its own reduce of epoch e + 1 saw every peer's epoch e + 1 flag, i.e. after every peer
+// finished reading epoch e.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "ctx.h"
+#include "mcp_common.cuh"
+
+using namespace mcp;
+using namespace mcp_internal;
+
+namespace {
+
+constexpr int PR_T = 256;
+constexpr long long PR_SPIN_LIMIT = 1ll << 32;   // ~2 s at 1.9 GHz, then report and go on
+
+__device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_volatile_sys(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void k_peer_signal(int64_t* const* __restrict__ flags, int rank, int world,
+                              int64_t epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int k = 0; k < world; ++k) st_release_sys(flags[k] + rank, epoch);
+}
+
+// blocks 0 .. nb-2: g_A (or summed Y) slices; block nb-1: w, g_lam, f.
+// parts[k] = rank k's partial slot for this epoch; err (device) set when a flag never came.
+__global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
+                                     const int64_t* __restrict__ my_flags, int world,
+                                     int64_t epoch, int n, int r, int d,
+                                     const double* __restrict__ x, const double* __restrict__ M,
+                                     const double* __restrict__ u, double alpha,
+                                     double* __restrict__ out, double* __restrict__ Yw_sum,
+                                     int* __restrict__ err) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    ok = 1;
+    for (int k = 0; k < world; ++k) {
+      const long long t0 = clock64();
+      while (ld_acquire_sys(my_flags + k) < epoch) {
+        if (clock64() - t0 > PR_SPIN_LIMIT) {
+          ok = 0;
+          atomicExch(err, 1);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const double* lam = x;
+  const int64_t nr = (int64_t)n * r;
+  if (blockIdx.x + 1 < gridDim.x) {
+    for (int64_t e = blockIdx.x * (int64_t)PR_T + threadIdx.x; e < nr;
+         e += (int64_t)(gridDim.x - 1) * PR_T) {
+      double y = 0.0;
+      for (int k = 0; k < world; ++k) y += ld_volatile_sys(parts[k] + e);
+      if (M) {
+        const int j = (int)(e / n);
+        out[1 + r + e] = ((-2.0 * d) * (y - M[e])) * lam[j];
+      } else {
+        Yw_sum[e] = y;
+      }
+    }
+    return;
+  }
+  __shared__ double s_w[1024];
+  for (int j = threadIdx.x; j < r; j += PR_T) {
+    double w = 0.0;
+    for (int k = 0; k < world; ++k) w += ld_volatile_sys(parts[k] + nr + j);
+    if (M) {
+      s_w[j] = w;
+      out[1 + j] = -2.0 * (w - u[j]);
+    } else {
+      Yw_sum[nr + j] = w;
+    }
+  }
+  __syncthreads();
+  if (M && threadIdx.x == 0) {
+    double lu = 0.0, wl = 0.0;
+    for (int j = 0; j < r; ++j) lu += lam[j] * u[j];
+    for (int j = 0; j < r; ++j) wl += s_w[j] * lam[j];
+    out[0] = alpha + lu - 2.0 * wl;
+  }
+  (void)ok;
+}
+
+}  // namespace
+
+extern "C" int mcp_peer_signal(mcp_ctx* c, const void* flag_ptrs, int rank, int world,
+                               int64_t epoch, void* stream) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!flag_ptrs || world < 1 || rank < 0 || rank >= world)
+    return c->fail(MCP_ERR_ARG, "bad peer arguments");
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  k_peer_signal<<<1, 32, 0, s>>>((int64_t* const*)flag_ptrs, rank, world, epoch);
+  CUDA_TRY(c, cudaGetLastError());
+  return MCP_OK;
+}
+
+extern "C" int mcp_peer_reduce_finish(mcp_ctx* c, int d, int r, const double* dx,
+                                      const void* part_ptrs, const int64_t* my_flags, int world,
+                                      int64_t epoch, double alpha, double* dout, int* derr,
+                                      void* stream) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!dx || !part_ptrs || !my_flags || !dout || !derr || world < 1)
+    return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  if (r > 1024) return c->fail(MCP_ERR_ARG, "rank > 1024 not supported by the peer reduce");
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  const int n = (int)c->n;
+  const int64_t nr = (int64_t)n * r;
+  const bool light = c->tail_x == dx && c->tail_d == d && c->tail_r == r;
+  int rc;
+  if (!light) {
+    if ((rc = ensure(c, c->dYw, sizeof(double) * (size_t)(nr + r)))) return rc;
+    if ((rc = ensure(c, c->dG, sizeof(double) * (size_t)r * r))) return rc;
+    if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
+  }
+  const int nb = (int)std::min<int64_t>(ceil_div(nr, PR_T), 4 * c->sms) + 1;
+  k_peer_reduce_finish<<<nb, PR_T, 0, s>>>(
+      (const double* const*)part_ptrs, my_flags, world, epoch, n, r, d, dx,
+      light ? (const double*)c->dM.p : nullptr, light ? (const double*)c->du.p : nullptr, alpha,
+      dout, light ? nullptr : (double*)c->dYw.p, derr);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches = 1;
+  if (!light) {
+    c->tail_x = nullptr;
+    return enqueue_finish(c, d, r, dx, (const double*)c->dYw.p, nullptr, alpha, dout, s);
+  }
+  return MCP_OK;
+}

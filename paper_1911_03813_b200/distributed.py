@@ -137,6 +137,64 @@ def packed_fg_sharded(sobs: ShardedObservationSet, d: int, r: int, alpha: float 
     return fg
 
 
+class PeerExchange:
+    """[vec_F(Y) | w] exchange over NVLink peer memory, fused with the finish (replaces the
+    all-reduce + tail of the row-sharded evaluation; csrc/peer.cu).
+
+    Each rank owns two symmetric partial slots (epoch parity) and a flag array; one evaluation is
+    ``partial -> signal -> reduce_finish`` on the rank's stream, with no host round trip and no
+    NCCL call, and every rank sums the partials in rank order (bitwise identical results on all
+    ranks).  ``buffers`` (tests) injects plain device buffers instead of symmetric memory.
+    """
+
+    def __init__(self, ctx, n: int, r: int, rank: int, world: int, group=None, buffers=None):
+        torch = _torch()
+        self.ctx, self.n, self.r, self.rank, self.world = ctx, int(n), int(r), int(rank), int(world)
+        dev = torch.device("cuda", ctx.device)
+        self.L = self.n * self.r + self.r
+        if buffers is None:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+
+            self.buf = symm.empty(2 * self.L, dtype=torch.float64, device=dev)
+            self.flags = symm.empty(self.world, dtype=torch.int64, device=dev)
+            self.flags.zero_()
+            torch.cuda.synchronize(dev)
+            grp = group if group is not None else dist.group.WORLD
+            hb = symm.rendezvous(self.buf, grp)
+            hf = symm.rendezvous(self.flags, grp)
+            buf_ptrs, flag_ptrs = list(hb.buffer_ptrs), list(hf.buffer_ptrs)
+            dist.barrier(group)
+        else:
+            self.buf, self.flags, buf_ptrs, flag_ptrs = buffers
+        self.parts = [torch.tensor([b + slot * self.L * 8 for b in buf_ptrs], dtype=torch.int64,
+                                   device=dev) for slot in (0, 1)]
+        self.flag_ptrs = torch.tensor(flag_ptrs, dtype=torch.int64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.epoch = 0
+
+    def slot_ptr(self, epoch: int) -> int:
+        return self.buf.data_ptr() + (epoch % 2) * self.L * 8
+
+    def partial(self, d, x_ptr, mode, stream, epoch):
+        self.ctx.fg_partial_device(d, self.r, x_ptr, mode, self.slot_ptr(epoch), stream)
+        self.ctx.peer_signal(self.flag_ptrs.data_ptr(), self.rank, self.world, epoch, stream)
+
+    def reduce_finish(self, d, x_ptr, alpha, out_ptr, stream, epoch):
+        self.ctx.peer_reduce_finish(d, self.r, x_ptr, self.parts[epoch % 2].data_ptr(),
+                                    self.flags.data_ptr(), self.world, epoch, alpha, out_ptr,
+                                    self.err.data_ptr(), stream)
+
+    def step(self, d, x_ptr, mode, alpha, out_ptr, stream):
+        """One sharded evaluation x -> out = [f ; g_lam ; vec_F(g_A)] on every rank."""
+        self.epoch += 1
+        self.partial(d, x_ptr, mode, stream, self.epoch)
+        self.reduce_finish(d, x_ptr, alpha, out_ptr, stream, self.epoch)
+
+    def failed(self) -> bool:
+        return bool(self.err.item())
+
+
 def data_norm_sq_split(obs_full: ObservationSet, d: int, group=None, mode: str | None = None,
                        part_fn=None) -> float:
     """||X||^2 with the tile-pair list split over the ranks of `group`.

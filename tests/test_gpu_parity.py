@@ -370,3 +370,56 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
         assert torch.equal(outs[0], outs[1]), (n, r)
         res = mcp.fg_implicit(obs, lam, A, 3, 0.25)
         assert float(outs[0][0]) == res.f
+
+
+def test_peer_exchange_kernels_two_virtual_ranks():
+    """csrc/peer.cu on ONE GPU with two virtual ranks run strictly in sequence (both partials and
+    signals complete before either reduce starts -- no kernel waits on another): the peer
+    reduce + fused finish equals the single-device evaluation of the union of the rows to the
+    fp64 reassociation of the 2-way row split, bitwise identical on both ranks, and matches
+    the all-reduce + finish path bitwise (same rank-order sum)."""
+    import torch
+
+    from paper_1911_03813_b200 import _native
+    from paper_1911_03813_b200 import distributed as D
+
+    rng = np.random.default_rng(33)
+    n, p, r, d = 100, 6000, 10, 4
+    V = rng.standard_normal((n, p)) / 10
+    lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / 10
+    Vt = torch.as_tensor(V.T.copy(), device="cuda")
+    L = n * r + r
+    bufs = [torch.zeros(2 * L, dtype=torch.float64, device="cuda") for _ in range(2)]
+    flags = [torch.zeros(2, dtype=torch.int64, device="cuda") for _ in range(2)]
+    buf_ptrs = [b.data_ptr() for b in bufs]
+    flag_ptrs = [f.data_ptr() for f in flags]
+    ranks = []
+    for k in range(2):
+        lo, hi = D.shard_bounds(p, 2, k)
+        sobs = mcp.ObservationSet.from_device(Vt[lo:hi], p_total=p)
+        ranks.append(D.PeerExchange(sobs.device_context(), n, r, k, 2,
+                                    buffers=(bufs[k], flags[k], buf_ptrs, flag_ptrs)))
+    x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
+    s = _native.stream_handle(torch.cuda.current_stream())
+    outs = [torch.empty(1 + L, dtype=torch.float64, device="cuda") for _ in range(2)]
+    for epoch in (1, 2, 3):                      # both slots, and a slot reused
+        for k in range(2):
+            ranks[k].partial(d, x.data_ptr(), None, s, epoch)
+        for k in range(2):
+            ranks[k].reduce_finish(d, x.data_ptr(), 0.5, outs[k].data_ptr(), s, epoch)
+        torch.cuda.synchronize()
+        assert not ranks[0].failed() and not ranks[1].failed()
+        assert torch.equal(outs[0], outs[1])
+    # the NCCL-path equivalent: sum of the two partials in rank order, then the finish
+    Yw = bufs[0][L:2 * L] + bufs[1][L:2 * L]      # epoch 3 lives in slot 1
+    ref = torch.empty_like(outs[0])
+    ranks[0].ctx.fg_partial_device(d, r, x.data_ptr(), None, bufs[0][L:].data_ptr(), s)
+    ranks[0].ctx.fg_finish_device(d, r, x.data_ptr(), Yw.data_ptr(), 0.5, ref.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert torch.equal(ref, outs[0])
+    full = mcp.fg_implicit(mcp.ObservationSet(V), lam, A, d, 0.5)
+    f_s, gl_s, gA_s, _ = om.term_scales(V, np.full(p, 1 / p), lam, A, d, 0.5)
+    h = outs[0].cpu().numpy()
+    assert _err(h[0], full.f, f_s) <= 1e-13
+    assert _err(h[1:1 + r], full.g_lam, gl_s) <= 1e-13
+    assert _err(h[1 + r:].reshape((n, r), order="F"), full.g_A, gA_s) <= 1e-13

@@ -19,6 +19,10 @@
 
 namespace mcp {
 
+#ifndef MCP_K1_ODD
+#define MCP_K1_ODD 0            // 1: GEMM1 even / odd k-step accumulator chains (no gain measured)
+#endif
+
 constexpr int K1_TP = 64;       // observations per tile
 constexpr int K1_NK = 64;       // n-chunk width staged in shared memory
 constexpr int K1_THREADS = 256; // 8 warps
@@ -107,9 +111,10 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
     const int64_t row0 = tile * K1_TP;
 
     // ---------------- GEMM1: Z[64 x RB] = V_tile[64 x n] * A[n x RB] ----------------
-    double zacc[NT][2];
+    // even / odd k-steps in separate accumulators: 2 NT independent DMMA chains per warp
+    double zacc[NT][2], zodd[NT][2];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) zacc[nt][0] = zacc[nt][1] = 0.0;
+    for (int nt = 0; nt < NT; ++nt) zacc[nt][0] = zacc[nt][1] = zodd[nt][0] = zodd[nt][1] = 0.0;
 
     k1_load_v<VT>(sV0, V, prm.ldv, row0, 0);
     k1_load_a<NT>(sA0, Af);
@@ -128,12 +133,21 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
       __syncthreads();
       const VT* vrow = sv + (8 * warp + g) * K1_SV + t;
 #pragma unroll
-      for (int ks = 0; ks < 16; ++ks) {
-        const double a = to_f64(vrow[4 * ks]);
+      for (int ks = 0; ks < 16; ks += 2) {
+        const double a0 = to_f64(vrow[4 * ks]);
+        const double a1 = to_f64(vrow[4 * ks + 4]);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884(zacc[nt], a, sa[(ks * NT + nt) * 32 + lane]);
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma884(zacc[nt], a0, sa[(ks * NT + nt) * 32 + lane]);
+          dmma884(MCP_K1_ODD ? zodd[nt] : zacc[nt], a1, sa[((ks + 1) * NT + nt) * 32 + lane]);
+        }
       }
       __syncthreads();
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      zacc[nt][0] += zodd[nt][0];
+      zacc[nt][1] += zodd[nt][1];
     }
 
     // ---------------- epilogue: P = nu * z^(d-1), w += P * z ----------------
@@ -193,6 +207,162 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
         *reinterpret_cast<double2*>(&Yp[(size_t)(c * K1_NK + 8 * warp + g) * RB + 8 * nt + 2 * t]) =
             make_double2(yacc[c][nt][0], yacc[c][nt][1]);
     }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = wacc[nt][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if (g == 0) sW[warp * RB + 8 * nt + 2 * t + e] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < RB) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < K1_THREADS / 32; ++w) s += sW[w * RB + threadIdx.x];
+    prm.wpart[((size_t)rb * prm.gp + pg) * RB + threadIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1G: the same tile pipeline with the Y partial kept in global memory (L2-resident, one
+// n_pad x RB block per CTA, owned element-wise by one thread) instead of registers.  GEMM2
+// accumulates each n-chunk of a tile in fresh registers and adds the chunk into the CTA's
+// partial right after it (prefetched before the chunk's k-steps), so registers no longer bound
+// the column block: RB = 64 for every n (vs RB = 16 at n = 1024 in K1), i.e. 4x fewer passes over
+// V for r = 256, and every warp runs NT = RB / 8 independent DMMA chains in both GEMMs.
+// The per-tile read-modify-write of the partial is ~1 MB per CTA per tile (~15 GB/s per SM at
+// c5), far below L2 bandwidth.  Static tile order per CTA + single-owner elements keep the
+// result deterministic.
+template <typename VT, int RB>
+__host__ __device__ constexpr size_t k1g_smem_bytes() {
+  return 2 * (size_t)K1_TP * K1_SV * sizeof(VT) + 2 * (size_t)16 * (RB / 8) * 32 * 8 +
+         (size_t)K1_TP * (RB + 4) * 8 + (size_t)8 * RB * 8;
+}
+
+template <typename VT, int RB>
+__global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
+  constexpr int NT = RB / 8;
+  constexpr int SP = RB + 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  VT* sV0 = reinterpret_cast<VT*>(smem_raw);
+  VT* sV1 = sV0 + K1_TP * K1_SV;
+  double* sA0 = reinterpret_cast<double*>(smem_raw + 2 * (size_t)K1_TP * K1_SV * sizeof(VT));
+  double* sA1 = sA0 + 16 * NT * 32;
+  double* sP = sA1 + 16 * NT * 32;
+  double* sW = sP + K1_TP * SP;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int rb = blockIdx.x % prm.rbs;
+  const int pg = blockIdx.x / prm.rbs;
+  const int C = prm.n_chunks;
+  const int dm1 = prm.d - 1;
+  const VT* __restrict__ V = static_cast<const VT*>(prm.V);
+  const double* __restrict__ Af = prm.Afrag + (size_t)rb * C * 16 * NT * 32;
+  double* __restrict__ Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * prm.n_pad * RB;
+
+  double wacc[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
+  bool first = true;
+
+  for (int64_t tile = pg; tile < prm.num_tiles; tile += prm.gp) {
+    const int64_t row0 = tile * K1_TP;
+
+    // ---------------- GEMM1: Z[64 x RB] = V_tile[64 x n] * A[n x RB] ----------------
+    double zacc[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) zacc[nt][0] = zacc[nt][1] = 0.0;
+    k1_load_v<VT>(sV0, V, prm.ldv, row0, 0);
+    k1_load_a<NT>(sA0, Af);
+    cp_async_commit();
+    for (int c = 0; c < C; ++c) {
+      VT* sv = (c & 1) ? sV1 : sV0;
+      double* sa = (c & 1) ? sA1 : sA0;
+      if (c + 1 < C) {
+        k1_load_v<VT>((c & 1) ? sV0 : sV1, V, prm.ldv, row0, c + 1);
+        k1_load_a<NT>((c & 1) ? sA0 : sA1, Af + (size_t)(c + 1) * 16 * NT * 32);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const VT* vrow = sv + (8 * warp + g) * K1_SV + t;
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const double a = to_f64(vrow[4 * ks]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(zacc[nt], a, sa[(ks * NT + nt) * 32 + lane]);
+      }
+      __syncthreads();
+    }
+
+    // ---------------- epilogue: P = nu * z^(d-1), w += P * z ----------------
+    {
+      const int lr = 8 * warp + g;
+      const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        double pv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double z = zacc[nt][e];
+          pv[e] = nul * rm_pow(z, dm1);
+          wacc[nt][e] += pv[e] * z;
+        }
+        *reinterpret_cast<double2*>(&sP[lr * SP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
+      }
+    }
+    __syncthreads();
+
+    // ---------------- GEMM2, chunk by chunk, last to first ----------------
+    for (int c = C - 1; c >= 0; --c) {
+      const VT* sv = (c & 1) ? sV1 : sV0;
+      if (c >= 1 && c - 1 <= C - 3) {
+        k1_load_v<VT>(((c - 1) & 1) ? sV1 : sV0, V, prm.ldv, row0, c - 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      double* yrow = Yp + (size_t)(c * K1_NK + 8 * warp + g) * RB + 2 * t;
+      double2 prev[NT];
+      if (!first) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) prev[nt] = *reinterpret_cast<const double2*>(yrow + 8 * nt);
+      }
+      double acc[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      const VT* vcol = sv + t * K1_SV + 8 * warp + g;
+      const double* prow = sP + t * SP + g;
+#pragma unroll 4
+      for (int ks = 0; ks < 16; ++ks) {
+        const double a = to_f64(vcol[4 * ks * K1_SV]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt], a, prow[4 * ks * SP + 8 * nt]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        double2 o = make_double2(acc[nt][0], acc[nt][1]);
+        if (!first) {
+          o.x += prev[nt].x;
+          o.y += prev[nt].y;
+        }
+        *reinterpret_cast<double2*>(yrow + 8 * nt) = o;
+      }
+      __syncthreads();
+    }
+    first = false;
+  }
+  if (first) {   // a CTA without tiles still owns a (zero) partial
+    for (int64_t e = threadIdx.x; e < (int64_t)prm.n_pad * RB; e += K1_THREADS) Yp[e] = 0.0;
   }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)

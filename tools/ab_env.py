@@ -21,11 +21,12 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--mode", default=None)
+ap.add_argument("--p", type=int, default=None)
 ap.add_argument("--timing", action="store_true", help="per-launch kernel event timing on")
 ap.add_argument("toggles", nargs="*")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
-V = synth.device_observations(cfg, 2024)
+V = synth.device_observations(cfg, 2024, p=a.p)
 obs = mcp.ObservationSet.from_device(V, p_total=V.shape[0])
 ctx = obs.device_context()
 lam, A = synth.initial_point(cfg, 2024)

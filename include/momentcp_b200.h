@@ -165,6 +165,19 @@ int mcp_lbfgs(mcp_ctx* ctx, int d, int r, double alpha, int mode, const double* 
               void* hook_user);
 
 /*
+ * k L-BFGS solves in lock step (the multistart of optimize.py:454-508 with
+ * every start's evaluation sharing ONE pass over V per round).  X0 is k x (r + n r), row s = start
+ * s; opts as mcp_lbfgs.  Per run s: X_out/G_out row s, F_out[s], trace_f/trace_t row s (trace_cap
+ * each), info[4 s .. 4 s + 3] = {n_fg, n_steps, reason (0 tolerance, 1 iteration cap,
+ * 2 line-search failure, 3 error), trace rows}.  Runs with reason 3 are described by
+ * mcp_lbfgs_batch_errors() (one "run s: message" line each); the others are unaffected.
+ */
+int mcp_lbfgs_batch(mcp_ctx* ctx, int k, int d, int r, double alpha, int mode, const double* X0,
+                    const double* opts, double* X_out, double* G_out, double* F_out,
+                    double* trace_f, double* trace_t, int64_t trace_cap, int64_t* info);
+const char* mcp_lbfgs_batch_errors(void);
+
+/*
  * Stochastic path.
  * mcp_gather_rows: rows idx[0..s) of the resident set -> dst (device, s rows of pitch ld_dst,
  *   dst_dtype MCP_F64 or MCP_F32), i.e. the V[:, idx] of sample_observations

@@ -70,6 +70,11 @@ SIGNATURES = {
     "mcp_lbfgs": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                  ctypes.c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _dp,
                                  _c_void_p, _c_void_p, _i64, _c_void_p, IterateHook, _c_void_p]),
+    "mcp_lbfgs_batch": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_int, _c_void_p, _c_void_p,
+                                       _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                                       _i64, _c_void_p]),
+    "mcp_lbfgs_batch_errors": (ctypes.c_char_p, []),
     "mcp_gather_rows": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, ctypes.c_int]),
     "mcp_adam": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_void_p,
                                 _c_void_p, _c_void_p, _i64, SampleFn, _c_void_p, _c_void_p,
@@ -285,6 +290,38 @@ class Context:
         return {"x": x, "g": g, "f": f.value, "n_fg": int(info[0]), "n_steps": int(info[1]),
                 "reason": ("tolerance", "iteration cap", "line-search failure")[int(info[2])],
                 "trace": list(zip(tf[:k].tolist(), tt[:k].tolist()))}
+
+    def lbfgs_batch(self, X0: np.ndarray, n: int, d: int, r: int, alpha: float, mode, opts):
+        """k lock-step device L-BFGS solves (mcp_lbfgs_batch); returns one dict per start."""
+        X0 = np.ascontiguousarray(X0, dtype=np.float64)
+        k, N = X0.shape
+        if N != r + n * r:
+            raise ValueError(f"expected packed length {r + n * r}, got {N}")
+        o = np.array([float(v) for v in opts], dtype=np.float64)
+        cap = int(min(o[2], o[3])) + 1
+        X = np.empty_like(X0)
+        G = np.empty_like(X0)
+        F = np.empty(k)
+        tf = np.empty((k, cap))
+        tt = np.empty((k, cap))
+        info = np.zeros((k, 4), dtype=np.int64)
+        rc = self._lib.mcp_lbfgs_batch(self._h, int(k), int(d), int(r), float(alpha),
+                                       mode_code(mode), _ptr(X0), _ptr(o), _ptr(X), _ptr(G),
+                                       _ptr(F), _ptr(tf), _ptr(tt), cap, _ptr(info))
+        self._check(rc, "mcp_lbfgs_batch")
+        errs = {}
+        for line in (self._lib.mcp_lbfgs_batch_errors() or b"").decode().splitlines():
+            head, _, msg = line.partition(": ")
+            errs[int(head.split()[1])] = msg
+        reasons = ("tolerance", "iteration cap", "line-search failure", "error")
+        out = []
+        for s_ in range(k):
+            nt = int(info[s_, 3])
+            out.append({"x": X[s_].copy(), "g": G[s_].copy(), "f": float(F[s_]),
+                        "n_fg": int(info[s_, 0]), "n_steps": int(info[s_, 1]),
+                        "reason": reasons[int(info[s_, 2])], "error": errs.get(s_),
+                        "trace": list(zip(tf[s_, :nt].tolist(), tt[s_, :nt].tolist()))})
+        return out
 
     def gather_rows(self, idx: np.ndarray, dst_ptr: int, ld: int, dtype_code: int) -> None:
         idx = np.ascontiguousarray(idx, dtype=np.int64)

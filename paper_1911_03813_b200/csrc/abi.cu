@@ -397,6 +397,25 @@ int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw
   return enqueue_finish_yw(c, d, r, dx, dYw, dYw + c->n * r, alpha_dev, alpha, dout, s);
 }
 
+int enqueue_tails_batched(mcp_ctx* c, int d, int r, int k, const double* xs, int64_t sx,
+                          const double* Y, const double* w, double alpha, double* out, int64_t so,
+                          cudaStream_t s) {
+  const int64_t n = c->n, nr = n * r;
+  if (nr <= K4S_MAX_NR && r <= K4S_MAX_R) {
+    k_tail_fused<<<k, K4S_THREADS, 0, s>>>(xs, Y, w, (int)n, r, d, nullptr, alpha, out, sx, nr, r,
+                                           so);
+    CUDA_TRY(c, cudaGetLastError());
+    c->last_launches += 1;
+    return MCP_OK;
+  }
+  for (int i = 0; i < k; ++i) {
+    int rc = enqueue_finish_yw(c, d, r, xs + (int64_t)i * sx, Y + (int64_t)i * nr, w + (int64_t)i * r,
+                               nullptr, alpha, out + (int64_t)i * so, s);
+    if (rc) return rc;
+  }
+  return MCP_OK;
+}
+
 int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const double* alpha_dev,
                     double alpha, double* dout, cudaStream_t s) {
   const int r = pl.r;

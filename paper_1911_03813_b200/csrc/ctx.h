@@ -129,6 +129,11 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
 // K4 : out = [f ; g_lam ; vec_F(g_A)] from x = [lam ; vec_F(A)] and [Y ; w]
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s);
+// Tails of k evaluations that shared one pass over V: run s has x = xs + s*sx (packed,
+// [lam; vec_F(A)]), its Y block Y + s*n*r, w + s*r, output out + s*so (alpha on the host).
+int enqueue_tails_batched(mcp_ctx* c, int d, int r, int k, const double* xs, int64_t sx,
+                          const double* Y, const double* w, double alpha, double* out, int64_t so,
+                          cudaStream_t s);
 // A whole single-device evaluation x -> out: K1P + fused reduce/finish when available, else
 // partial (K1 -> K3) + finish (K4).  Scratch [Y ; w] in c->dYw.
 int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const double* alpha_dev,

@@ -1,24 +1,35 @@
-// Device-resident L-BFGS over the momentcp objective.
+// Device-resident L-BFGS over the momentcp objective, for one run or k runs in lock step
+// (SURVEY.md 8f #1 and #2).
 //
 // Reference: pkg/src/momentcp/optimize.py:149-168 (two-loop recursion), :171-176 (safeguarded
-// quadratic interpolation), :179-252 (strong-Wolfe bracket/zoom), :255-355 (outer loop).
+// quadratic interpolation), :179-252 (strong-Wolfe bracket/zoom), :255-355 (outer loop),
+// :454-508 (multistart).
 //
-// HBM holds x, g = fg(x), the direction p, a trial point xa with its [fa; ga], a saved best
-// trial, and a ring of memory+1 (s, y) slots (the spare slot takes the new pair before the
+// Per run, HBM holds x, g = fg(x), the direction p, a trial point xa with its [fa; ga], a saved
+// best trial, and a ring of memory+1 (s, y) slots (the spare slot takes the new pair before the
 // curvature test decides whether it joins the window, so a rejected pair never evicts the
-// oldest accepted one -- the reference's deque only appends accepted pairs).  Per evaluation the
-// host replays one CUDA graph
-//     [accept step -> two-loop direction -> a0]  ->  trial x + a p  ->  fg  ->  probe scalars
-// and reads back ~12 doubles; the line-search and stopping decisions are made on those scalars
-// in exactly the reference's order.  Elementwise updates use explicit round-to-nearest multiply
-// and add (no FMA contraction), so given equal scalars they match numpy's `x + a * p`,
-// `q -= alpha * y`, ... bit for bit; dot products are fixed-order reductions (deterministic run
-// to run, but summed in a different order than numpy's).
+// oldest accepted one -- the reference's deque only appends accepted pairs).
+//
+// One "round" evaluates exactly one trial point per active run.  Each run's host-side state
+// machine (the reference's line search, made resumable) picks the run's action for the round:
+//   PROBE          trial at a host-chosen step a (inside a line search)
+//   ACC_T / ACC_B  accept the last trial / the saved best, curvature-test the (s, y) pair, run
+//                  the two-loop recursion, the descent check and a0, then probe x + a0 p
+//   IDLE           finished run (its columns ride along)
+// plus SAVE (copy the last trial into the best slot first).  A round is ONE CUDA graph:
+//   H2D(actions, steps) -> save -> accept -> direction -> trial -> f+grad -> probe stats -> D2H
+// With k runs the f+grad is a single pass over V with k*r factor columns (the K1 family) and
+// per-run tails, so k lock-step runs cost about one run's latency per round.  The host reads
+// back ~12 doubles per run and takes the reference's decisions in the reference's order.
+// Elementwise updates use explicit round-to-nearest operations (no FMA contraction), so given
+// equal scalars they match numpy's `x + a * p`, `q -= alpha * y`, ... bit for bit; dot products
+// are fixed-order reductions (deterministic, summed in a different order than numpy's).
 #include <cuda_runtime.h>
 
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -29,11 +40,14 @@ using namespace mcp_internal;
 namespace {
 
 constexpr int LB_T = 256;        // threads of the streaming kernels
-constexpr int LB_DIR_T = 1024;   // the single-CTA two-loop kernel
+constexpr int LB_DIR_T = 1024;   // the one-CTA-per-run two-loop kernel (large N)
 constexpr int LB_NP = 6;         // partial sums per block
 constexpr int LB_MAX_BLOCKS = 296;
 
-// scalar slots of the stats record copied to the host after every graph replay
+// actions (low 3 bits) + flag
+enum { ACT_PROBE = 0, ACT_ACC_T = 1, ACT_ACC_B = 2, ACT_IDLE = 3, ACT_INIT = 4, ACT_SAVE = 8 };
+
+// scalar slots of a run's stats record, copied to the host after every round
 enum {
   S_GMAX = 0,   // max |g| of the accepted gradient (+inf when it has non-finite entries)
   S_GSUM,       // sum |g|
@@ -48,6 +62,33 @@ enum {
   S_XBAD,       // non-finite entries of the trial point
   S_F,          // objective at the accepted point
   S_COUNT
+};
+
+// Device view of the k runs' state (passed by value; run s = blockIdx.y).
+struct LbDev {
+  int64_t N;
+  int m, k;
+  double *X, *OX, *T, *OT, *B, *OB, *P, *S, *Y, *syh, *yyh, *part, *st, *a0, *ah;
+  int* ring;
+  unsigned* counter;
+  const int* act;
+  double* Xb;   // batched K1 layout [lam_all (k r) ; A_all (n x k r)] or nullptr (k == 1)
+  int r;
+  int64_t n;
+  __device__ int action(int s) const { return act[s] & 7; }
+  __device__ double* x(int s) const { return X + (int64_t)s * N; }
+  __device__ double* ox(int s) const { return OX + (int64_t)s * (N + 1); }
+  __device__ double* t(int s) const { return T + (int64_t)s * N; }
+  __device__ double* ot(int s) const { return OT + (int64_t)s * (N + 1); }
+  __device__ double* b(int s) const { return B + (int64_t)s * N; }
+  __device__ double* ob(int s) const { return OB + (int64_t)s * (N + 1); }
+  __device__ double* p(int s) const { return P + (int64_t)s * N; }
+  __device__ double* sr(int s) const { return S + (int64_t)s * (m + 1) * N; }
+  __device__ double* yr(int s) const { return Y + (int64_t)s * (m + 1) * N; }
+  __device__ double* sy(int s) const { return syh + (int64_t)s * (m + 1); }
+  __device__ double* yy(int s) const { return yyh + (int64_t)s * (m + 1); }
+  __device__ double* pt(int s) const { return part + (int64_t)s * gridDim.x * LB_NP; }
+  __device__ double* stats(int s) const { return st + (int64_t)s * S_COUNT; }
 };
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -81,9 +122,9 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return red[32];
 }
 
-// "last block done": true in exactly one block, after every block's partials are visible.
-// The finishing block sums the per-block partials in index order, so results do not depend on
-// which block finishes last.
+// "last block done" (per run): true in exactly one block of the run, after every block's
+// partials are visible.  The finishing block sums the partials in index order, so results do
+// not depend on which block finishes last.
 __device__ __forceinline__ bool last_block(unsigned* counter) {
   __shared__ bool last;
   __syncthreads();
@@ -98,74 +139,88 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return last;
 }
 
-// stage 1 of the |g| statistics at a freshly evaluated point (init): max, sum, non-finite(g, x)
-__device__ void lb_eval_fin(int nb, const double* __restrict__ part,
-                            const double* __restrict__ out, double* __restrict__ st,
-                            int* __restrict__ ring);
+#define LB_FOR(j) \
+  for (int64_t j = blockIdx.x * (int64_t)LB_T + threadIdx.x; j < D.N; j += (int64_t)gridDim.x * LB_T)
 
-__global__ void k_lb_eval_stats(int64_t N, const double* __restrict__ x,
-                                const double* __restrict__ out, double* __restrict__ part,
-                                unsigned* counter, double* __restrict__ st, int* __restrict__ ring) {
+// SAVE: the last trial becomes the saved best (before this round overwrites it)
+__global__ void k_lbb_save(LbDev D) {
+  const int s = blockIdx.y;
+  if (!(D.act[s] & ACT_SAVE)) return;
+  const double *t = D.t(s), *ot = D.ot(s);
+  double *b = D.b(s), *ob = D.ob(s);
+  LB_FOR(j) {
+    b[j] = t[j];
+    ob[1 + j] = ot[1 + j];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ob[0] = ot[0];
+}
+
+// INIT: x0's evaluation lives in OT; take it as [f; g] of x, statistics, ring reset
+__global__ void k_lbb_init_stats(LbDev D) {
   __shared__ double red[33];
-  const double* g = out + 1;
+  const int s = blockIdx.y;
+  const double* out = D.ot(s);
+  double* ox = D.ox(s);
+  const double* x = D.x(s);
   double mx = 0.0, sm = 0.0, bad = 0.0;
-  for (int64_t j = blockIdx.x * (int64_t)LB_T + threadIdx.x; j < N; j += (int64_t)gridDim.x * LB_T) {
-    const double a = fabs(g[j]);
+  LB_FOR(j) {
+    const double gj = out[1 + j];
+    ox[1 + j] = gj;
+    const double a = fabs(gj);
     mx = fmax(mx, a);
     sm += a;
-    bad += (isfinite(g[j]) && isfinite(x[j])) ? 0.0 : 1.0;
+    bad += (isfinite(gj) && isfinite(x[j])) ? 0.0 : 1.0;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && !isfinite(out[0])) bad += 1.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ox[0] = out[0];
+    if (!isfinite(out[0])) bad += 1.0;
+  }
   mx = block_max(mx, red);
   sm = block_sum(sm, red);
   bad = block_sum(bad, red);
+  double* pp = D.pt(s) + blockIdx.x * LB_NP;
   if (threadIdx.x == 0) {
-    part[blockIdx.x * LB_NP + 0] = mx;
-    part[blockIdx.x * LB_NP + 1] = sm;
-    part[blockIdx.x * LB_NP + 2] = bad;
+    pp[0] = mx;
+    pp[1] = sm;
+    pp[2] = bad;
   }
-  if (last_block(counter) && threadIdx.x == 0) lb_eval_fin(gridDim.x, part, out, st, ring);
-}
-
-__device__ void lb_eval_fin(int nb, const double* __restrict__ part,
-                            const double* __restrict__ out, double* __restrict__ st,
-                            int* __restrict__ ring) {
-  double mx = 0.0, sm = 0.0, bad = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    mx = fmax(mx, part[b * LB_NP + 0]);
-    sm += part[b * LB_NP + 1];
-    bad += part[b * LB_NP + 2];
+  if (!last_block(D.counter + s) || threadIdx.x != 0) return;
+  mx = 0.0;
+  sm = 0.0;
+  bad = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    const double* q = D.pt(s) + b * LB_NP;
+    mx = fmax(mx, q[0]);
+    sm += q[1];
+    bad += q[2];
   }
+  double* st = D.stats(s);
   st[S_GMAX] = bad > 0.0 ? INFINITY : mx;
   st[S_GSUM] = sm;
   st[S_GBAD] = bad;
   st[S_KEEP] = 0.0;
   st[S_F] = out[0];
-  ring[0] = 0;  // count
-  ring[1] = 0;  // head
+  D.ring[2 * s] = 0;      // count
+  D.ring[2 * s + 1] = 0;  // head
 }
 
-// accept the step to (xs, outs): s = xs - x, y = gs - g into ring slot `head`, x <- xs, g <- gs
-__device__ void lb_accept_fin(int nb, const double* __restrict__ part, int m,
-                              int* __restrict__ ring, double* __restrict__ sy_hist,
-                              double* __restrict__ yy_hist, const double* __restrict__ outx,
-                              double* __restrict__ st);
-
-__global__ void k_lb_accept(int64_t N, const double* __restrict__ xs,
-                            const double* __restrict__ outs, double* __restrict__ x,
-                            double* __restrict__ outx, double* __restrict__ S,
-                            double* __restrict__ Y, int* __restrict__ ring,
-                            double* __restrict__ part, unsigned* counter, int m,
-                            double* __restrict__ sy_hist, double* __restrict__ yy_hist,
-                            double* __restrict__ st) {
+// ACC_T / ACC_B: s = xs - x, y = gs - g into ring slot `head`, x <- xs, g <- gs; then the
+// curvature test (optimize.py:330-332) and the ring update in the run's last block
+__global__ void k_lbb_accept(LbDev D) {
   __shared__ double red[33];
-  const int head = ring[1];
-  double* s_out = S + (int64_t)head * N;
-  double* y_out = Y + (int64_t)head * N;
+  const int s = blockIdx.y, a = D.action(s);
+  if (a != ACT_ACC_T && a != ACT_ACC_B) return;
+  const double* xs = a == ACT_ACC_T ? D.t(s) : D.b(s);
+  const double* outs = a == ACT_ACC_T ? D.ot(s) : D.ob(s);
+  double* x = D.x(s);
+  double* outx = D.ox(s);
+  const int head = D.ring[2 * s + 1];
+  double* s_out = D.sr(s) + (int64_t)head * D.N;
+  double* y_out = D.yr(s) + (int64_t)head * D.N;
   double* g = outx + 1;
   const double* gs = outs + 1;
   double sy = 0.0, ss = 0.0, yy = 0.0, mx = 0.0, sm = 0.0, bad = 0.0;
-  for (int64_t j = blockIdx.x * (int64_t)LB_T + threadIdx.x; j < N; j += (int64_t)gridDim.x * LB_T) {
+  LB_FOR(j) {
     const double sj = __dsub_rn(xs[j], x[j]);
     const double yj = __dsub_rn(gs[j], g[j]);
     s_out[j] = sj;
@@ -175,9 +230,9 @@ __global__ void k_lb_accept(int64_t N, const double* __restrict__ xs,
     sy += __dmul_rn(sj, yj);
     ss += __dmul_rn(sj, sj);
     yy += __dmul_rn(yj, yj);
-    const double a = fabs(gs[j]);
-    mx = fmax(mx, a);
-    sm += a;
+    const double aa = fabs(gs[j]);
+    mx = fmax(mx, aa);
+    sm += aa;
     bad += isfinite(gs[j]) ? 0.0 : 1.0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) outx[0] = outs[0];
@@ -188,7 +243,7 @@ __global__ void k_lb_accept(int64_t N, const double* __restrict__ xs,
   sm = block_sum(sm, red);
   bad = block_sum(bad, red);
   if (threadIdx.x == 0) {
-    double* pp = part + blockIdx.x * LB_NP;
+    double* pp = D.pt(s) + blockIdx.x * LB_NP;
     pp[0] = sy;
     pp[1] = ss;
     pp[2] = yy;
@@ -196,18 +251,10 @@ __global__ void k_lb_accept(int64_t N, const double* __restrict__ xs,
     pp[4] = sm;
     pp[5] = bad;
   }
-  if (last_block(counter) && threadIdx.x == 0)
-    lb_accept_fin(gridDim.x, part, m, ring, sy_hist, yy_hist, outx, st);
-}
-
-// curvature test (optimize.py:330-332) and ring update
-__device__ void lb_accept_fin(int nb, const double* __restrict__ part, int m,
-                              int* __restrict__ ring, double* __restrict__ sy_hist,
-                              double* __restrict__ yy_hist, const double* __restrict__ outx,
-                              double* __restrict__ st) {
-  double sy = 0.0, ss = 0.0, yy = 0.0, mx = 0.0, sm = 0.0, bad = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    const double* pp = part + b * LB_NP;
+  if (!last_block(D.counter + s) || threadIdx.x != 0) return;
+  sy = ss = yy = mx = sm = bad = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    const double* pp = D.pt(s) + b * LB_NP;
     sy += pp[0];
     ss += pp[1];
     yy += pp[2];
@@ -217,12 +264,12 @@ __device__ void lb_accept_fin(int nb, const double* __restrict__ part, int m,
   }
   const bool keep = sy > __dmul_rn(__dmul_rn(1e-12, sqrt(ss)), sqrt(yy));
   if (keep) {
-    const int head = ring[1];
-    sy_hist[head] = sy;
-    yy_hist[head] = yy;
-    ring[1] = (head + 1) % (m + 1);
-    ring[0] = min(ring[0] + 1, m);
+    D.sy(s)[head] = sy;
+    D.yy(s)[head] = yy;
+    D.ring[2 * s + 1] = (head + 1) % (D.m + 1);
+    D.ring[2 * s] = min(D.ring[2 * s] + 1, D.m);
   }
+  double* st = D.stats(s);
   st[S_GMAX] = bad > 0.0 ? INFINITY : mx;
   st[S_GSUM] = sm;
   st[S_GBAD] = bad;
@@ -230,25 +277,29 @@ __device__ void lb_accept_fin(int nb, const double* __restrict__ part, int m,
   st[S_F] = outx[0];
 }
 
-// Two-loop recursion (optimize.py:149-168) in one CTA, then the descent check and the initial
-// step (optimize.py:307-322) and the first trial point.  When the window fits (stage != 0), g and
-// the (s, y) window are staged in shared memory first so the 2m+1 dependent passes run at smem
-// latency instead of L2 latency.
-__global__ void __launch_bounds__(LB_DIR_T) k_lb_direction(
-    int64_t N, const double* __restrict__ outx, const double* __restrict__ S,
-    const double* __restrict__ Y, int m, int* __restrict__ ring, const double* __restrict__ sy_h,
-    const double* __restrict__ yy_h, double* __restrict__ P, double* __restrict__ st,
-    double* __restrict__ a_dev, const double* __restrict__ X, double* __restrict__ T,
-    int stage) {
+// Two-loop recursion (optimize.py:149-168) in one CTA per run, then the descent check and the
+// initial step (optimize.py:307-322).  When the window fits (stage != 0), g and the (s, y)
+// window are staged in shared memory first so the 2m+1 dependent passes run at smem latency.
+__global__ void __launch_bounds__(LB_DIR_T) k_lbb_direction(LbDev D, int stage) {
   extern __shared__ double sm[];
   __shared__ double red[33];
   __shared__ double alpha_s[65];
+  const int run = blockIdx.y, act = D.action(run);
+  if (act != ACT_ACC_T && act != ACT_ACC_B && act != ACT_INIT) return;
+  const int64_t N = D.N;
+  const int m = D.m;
+  int* ring = D.ring + 2 * run;
+  const double* sy_h = D.sy(run);
+  const double* yy_h = D.yy(run);
+  const double* S = D.sr(run);
+  const double* Y = D.yr(run);
+  double* P = D.p(run);
+  double* st = D.stats(run);
   const int count = ring[0], head = ring[1];
   const int M1 = m + 1;
   auto slot = [&](int i) { return (head - count + i + 2 * M1) % M1; };  // i = 0 oldest
-  // views: q, g, s_i, y_i (i = 0 oldest) -- shared memory or global
   double* q = stage ? sm : P;
-  const double* g = outx + 1;
+  const double* g = D.ox(run) + 1;
   if (stage) {
     double* gs = sm + N;
     for (int64_t j = threadIdx.x; j < N; j += blockDim.x) gs[j] = g[j];
@@ -275,7 +326,6 @@ __global__ void __launch_bounds__(LB_DIR_T) k_lb_direction(
   if (count > 0) {
     const int newest = slot(count - 1);
     const double gamma = sy_h[newest] / yy_h[newest];
-    // loop 1, newest -> oldest: alpha_i = rho_i * (s_i . q); q -= alpha_i * y_i
     double acc = 0.0;
     {
       const double* Si = Sv(count - 1);
@@ -285,6 +335,7 @@ __global__ void __launch_bounds__(LB_DIR_T) k_lb_direction(
         acc += __dmul_rn(Si[j], qj);
       }
     }
+    // loop 1, newest -> oldest: alpha_i = rho_i * (s_i . q); q -= alpha_i * y_i
     for (int i = count - 1; i >= 0; --i) {
       const double dot = block_sum(acc, red);
       const double alpha = __dmul_rn(1.0 / sy_h[slot(i)], dot);
@@ -324,7 +375,6 @@ __global__ void __launch_bounds__(LB_DIR_T) k_lb_direction(
           acc += __dmul_rn(Yn[j], qj);
         }
       } else {
-        // direction = -q and p . g
         for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
           const double pj = -__dadd_rn(q[j], __dmul_rn(coef, Si[j]));
           P[j] = pj;
@@ -357,53 +407,67 @@ __global__ void __launch_bounds__(LB_DIR_T) k_lb_direction(
     }
     a0 = fmin(1.0, 1.0 / fmax(st[S_GSUM], 1e-12));
   }
-  // first trial point x + a0 p (optimize.py:187); each thread reads back its own P entries
-  for (int64_t j = threadIdx.x; j < N; j += blockDim.x) T[j] = __dadd_rn(X[j], __dmul_rn(a0, P[j]));
   if (threadIdx.x == 0) {
     if (reset) ring[0] = 0;
     st[S_PG] = pg;
     st[S_SLOPE0] = slope0;
     st[S_A0] = a0;
     st[S_RESET] = reset ? 1.0 : 0.0;
-    a_dev[0] = a0;
+    D.a0[run] = a0;
   }
 }
 
-// trial point xa = x + a * p (optimize.py:187)
-__global__ void k_lb_trial(int64_t N, const double* __restrict__ x, const double* __restrict__ P,
-                           const double* __restrict__ a_dev, double* __restrict__ xt) {
-  const double a = a_dev[0];
-  for (int64_t j = blockIdx.x * (int64_t)LB_T + threadIdx.x; j < N; j += (int64_t)gridDim.x * LB_T)
-    xt[j] = __dadd_rn(x[j], __dmul_rn(a, P[j]));
+// trial point xa = x + a * p (optimize.py:187); phase 0 of INIT: xa = x (evaluate x0).
+// Also scatters the trial into the batched K1 layout when k > 1.
+__global__ void k_lbb_trial(LbDev D, int init_phase0) {
+  const int s = blockIdx.y, act = D.action(s);
+  const double* x = D.x(s);
+  const double* p = D.p(s);
+  double* t = D.t(s);
+  const bool copy = act == ACT_IDLE || (act == ACT_INIT && init_phase0);
+  const double a = act == ACT_PROBE ? D.ah[s] : D.a0[s];
+  const int64_t nr = D.n * D.r, R = (int64_t)D.k * D.r;
+  LB_FOR(j) {
+    const double v = copy ? x[j] : __dadd_rn(x[j], __dmul_rn(a, p[j]));
+    t[j] = v;
+    if (D.Xb) {
+      if (j < D.r)
+        D.Xb[(int64_t)s * D.r + j] = v;
+      else
+        D.Xb[R + (int64_t)s * nr + (j - D.r)] = v;
+    }
+  }
 }
 
-// ga . p and the finiteness of the trial point
-__global__ void k_lb_probe_stats(int64_t N, const double* __restrict__ xt,
-                                 const double* __restrict__ outt, const double* __restrict__ P,
-                                 double* __restrict__ part, unsigned* counter,
-                                 double* __restrict__ st) {
+// ga . p and the finiteness of the trial point, finished by the run's last block
+__global__ void k_lbb_probe_stats(LbDev D) {
   __shared__ double red[33];
-  const double* ga = outt + 1;
+  const int s = blockIdx.y, act = D.action(s);
+  if (act == ACT_IDLE) return;
+  const double* xt = D.t(s);
+  const double* ga = D.ot(s) + 1;
+  const double* P = D.p(s);
   double dp = 0.0, bad = 0.0;
-  for (int64_t j = blockIdx.x * (int64_t)LB_T + threadIdx.x; j < N; j += (int64_t)gridDim.x * LB_T) {
+  LB_FOR(j) {
     dp += __dmul_rn(ga[j], P[j]);
     bad += isfinite(xt[j]) ? 0.0 : 1.0;
   }
   dp = block_sum(dp, red);
   bad = block_sum(bad, red);
+  double* pp = D.pt(s) + blockIdx.x * LB_NP;
   if (threadIdx.x == 0) {
-    part[blockIdx.x * LB_NP + 0] = dp;
-    part[blockIdx.x * LB_NP + 1] = bad;
+    pp[0] = dp;
+    pp[1] = bad;
   }
-  if (!last_block(counter) || threadIdx.x != 0) return;
-  const int nb = gridDim.x;
+  if (!last_block(D.counter + s) || threadIdx.x != 0) return;
   dp = 0.0;
   bad = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    dp += part[b * LB_NP + 0];
-    bad += part[b * LB_NP + 1];
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    dp += D.pt(s)[b * LB_NP + 0];
+    bad += D.pt(s)[b * LB_NP + 1];
   }
-  st[S_FA] = outt[0];
+  double* st = D.stats(s);
+  st[S_FA] = D.ot(s)[0];
   st[S_DA] = dp;
   st[S_XBAD] = bad;
 }
@@ -411,38 +475,141 @@ __global__ void k_lb_probe_stats(int64_t N, const double* __restrict__ xt,
 // ------------------------------------------------------------------------------------------
 // host side
 
-// Workspace + graphs for one (d, r, mode, memory, alpha); cached on the context between runs
-// (setup costs pinned allocations and four graph instantiations, ~ms).
-struct LbRun {
+// The reference's strong-Wolfe search (optimize.py:179-252) as a resumable state machine: the
+// caller feeds one probe result at a time and gets the next step or the outcome.  Decisions and
+// their order are exactly those of the loop form.
+struct Wolfe {
+  enum { PROBE = 0, DONE_T = 1, DONE_B = 2, FAIL = 3 };
+  struct Pt {
+    double a, f, d;
+  };
+  double f0 = 0, slope0 = 0, c1 = 0, c2 = 0;
+  int64_t budget = 0, ev = 0, it = 0;
+  bool have_best = false, zoom = false;
+  double best_f = 0, a = 0;
+  Pt prev{}, lo{}, hi{};
+
+  void start(double f0_, double slope0_, double a0, double c1_, double c2_, int64_t budget_) {
+    f0 = f0_;
+    slope0 = slope0_;
+    c1 = c1_;
+    c2 = c2_;
+    budget = budget_;
+    ev = 0;
+    it = 0;
+    have_best = false;
+    zoom = false;
+    a = a0;
+    prev = Pt{0.0, f0, slope0};
+  }
+
+  // optimize.py:171-176
+  static bool interp(double a_lo, double f_lo, double d_lo, double a_hi, double f_hi, double* out) {
+    const double den = f_hi - f_lo - d_lo * (a_hi - a_lo);
+    if (den == 0 || !std::isfinite(den)) return false;
+    const double cnd = a_lo - 0.5 * d_lo * ((a_hi - a_lo) * (a_hi - a_lo)) / den;
+    if (!std::isfinite(cnd)) return false;
+    *out = cnd;
+    return true;
+  }
+
+  int fallback() const { return have_best ? DONE_B : FAIL; }
+
+  int zoom_next(double* a_next) {
+    if (ev >= budget) return fallback();
+    const double width = hi.a - lo.a;
+    double cand = 0.0;
+    const bool ok = std::isfinite(hi.f) && interp(lo.a, lo.f, lo.d, hi.a, hi.f, &cand);
+    const double lb = lo.a + 0.1 * width, ub = hi.a - 0.1 * width;
+    if (!ok || !(std::fmin(lb, ub) <= cand && cand <= std::fmax(lb, ub))) cand = lo.a + 0.5 * width;
+    a = cand;
+    *a_next = cand;
+    return PROBE;
+  }
+
+  // Feed the result of the probe at step `a`.  *save: this probe is the new best (keep it).
+  int on_probe(double fa, double da_raw, bool* save, double* a_next) {
+    ++ev;
+    const double da = std::isfinite(fa) ? da_raw : NAN;
+    *save = false;
+    if (std::isfinite(fa) && fa <= f0 + c1 * a * slope0) {
+      if (!have_best || fa < best_f) {
+        have_best = true;
+        best_f = fa;
+        *save = true;
+      }
+    }
+    if (!zoom) {
+      const bool bad = !std::isfinite(fa) || fa > f0 + c1 * a * slope0 ||
+                       (prev.a > 0.0 && fa >= prev.f);
+      if (bad) {
+        lo = prev;
+        hi = Pt{a, fa, da};
+        zoom = true;
+        return zoom_next(a_next);
+      }
+      if (std::fabs(da) <= -c2 * slope0) return DONE_T;
+      if (da >= 0.0) {
+        lo = Pt{a, fa, da};
+        hi = prev;
+        zoom = true;
+        return zoom_next(a_next);
+      }
+      prev = Pt{a, fa, da};
+      a = std::fmin(2.0 * a, 1e20);
+      ++it;
+      if (it < budget) {
+        *a_next = a;
+        return PROBE;
+      }
+      return fallback();
+    }
+    const double cand = a;
+    if (!std::isfinite(fa) || fa > f0 + c1 * cand * slope0 || fa >= lo.f) {
+      hi = Pt{cand, fa, da};
+    } else {
+      if (std::fabs(da) <= -c2 * slope0) return DONE_T;
+      if (da * (hi.a - lo.a) >= 0.0) hi = lo;
+      lo = Pt{cand, fa, da};
+    }
+    if (std::fabs(hi.a - lo.a) < 1e-16 * std::fmax(1.0, std::fabs(lo.a))) return fallback();
+    return zoom_next(a_next);
+  }
+};
+
+// Workspace + graphs for (k, d, r, mode, memory, alpha); cached on the context between solves.
+struct LbEngine {
   mcp_ctx* c = nullptr;
-  int d = 0, r = 0, mode = 0, m = 0;
+  int k = 1, d = 0, r = 0, mode = 0, m = 0;
   double alpha = 0.0;
-  int64_t n = 0;
-  int64_t N = 0;
+  int64_t n = 0, N = 0;
   int nb = 1;
   int dir_threads = LB_DIR_T;
   size_t dir_smem = 0;
-  EvalPlan pl;
+  EvalPlan pl;   // k == 1: the single evaluation; k > 1: the shared pass over k r columns
   std::vector<void*> dev;
-  double *X = nullptr, *OX = nullptr, *T = nullptr, *OT = nullptr, *B = nullptr, *OB = nullptr;
-  double *P = nullptr, *S = nullptr, *Y = nullptr, *syh = nullptr, *yyh = nullptr;
-  double *part = nullptr, *st = nullptr, *a_dev = nullptr, *Yw = nullptr;
-  int* ring = nullptr;
-  unsigned* counter = nullptr;
-  double* hst = nullptr;   // pinned: stats
-  double* ha = nullptr;    // pinned: host-chosen step
-  double* hx = nullptr;    // pinned: x0 / hook copies
-  GraphEntry g_init, g_iter_t, g_iter_b, g_probe;
+  LbDev D{};
+  double* Ywb = nullptr;   // [Y (n x k r) ; w (k r)] of the shared pass
+  int* h_act = nullptr;    // pinned
+  double* h_a = nullptr;   // pinned
+  double* h_st = nullptr;  // pinned, k x S_COUNT
+  double* h_x = nullptr;   // pinned, k x N
+  int* d_act = nullptr;
+  GraphEntry g_init, g_round;
 
-  ~LbRun() {
-    for (GraphEntry* g : {&g_init, &g_iter_t, &g_iter_b, &g_probe}) {
+  ~LbEngine() {
+    for (GraphEntry* g : {&g_init, &g_round}) {
       if (g->exec) cudaGraphExecDestroy(g->exec);
       if (g->graph) cudaGraphDestroy(g->graph);
     }
     for (void* p : dev) cudaFree(p);
-    if (hst) cudaFreeHost(hst);
-    if (ha) cudaFreeHost(ha);
-    if (hx) cudaFreeHost(hx);
+    for (void* p : {(void*)h_act, (void*)h_a, (void*)h_st, (void*)h_x})
+      if (p) cudaFreeHost(p);
+  }
+
+  bool matches(int k_, int d_, int r_, int mode_, int m_, double alpha_) const {
+    return k == k_ && d == d_ && r == r_ && mode == mode_ && m == m_ && n == c->n &&
+           std::memcmp(&alpha, &alpha_, sizeof(double)) == 0;
   }
 
   template <typename T>
@@ -454,31 +621,30 @@ struct LbRun {
     return MCP_OK;
   }
 
-  // fg(x) -> out on the context stream (K1 -> K3 -> K4)
-  int enqueue_fg(const double* x, double* out) {
-    return enqueue_fg_full(c, pl, x, nullptr, alpha, out, c->stream);
-  }
-
-  int enqueue_direction_and_probe() {
+  // f+grad of every run's trial point T -> OT
+  int enqueue_fg() {
     cudaStream_t s = c->stream;
-    k_lb_direction<<<1, dir_threads, dir_smem, s>>>(N, OX, S, Y, m, ring, syh, yyh, P, st, a_dev,
-                                                    X, T, dir_smem ? 1 : 0);
-    return enqueue_probe_tail(false);
-  }
-
-  int enqueue_probe_tail(bool trial) {
-    cudaStream_t s = c->stream;
-    if (trial) k_lb_trial<<<nb, LB_T, 0, s>>>(N, X, P, a_dev, T);
-    int rc = enqueue_fg(T, OT);
+    if (k == 1) return enqueue_fg_full(c, pl, D.T, nullptr, alpha, D.OT, s);
+    int rc = enqueue_partial(c, pl, D.Xb, Ywb, s, false);
     if (rc) return rc;
-    k_lb_probe_stats<<<nb, LB_T, 0, s>>>(N, T, OT, P, part, counter, st);
-    CUDA_TRY(c, cudaMemcpyAsync(hst, st, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, s));
+    const int64_t R = (int64_t)k * r;
+    return enqueue_tails_batched(c, d, r, k, D.T, N, Ywb, Ywb + n * R, alpha, D.OT, N + 1, s);
+  }
+
+  int enqueue_round_tail() {   // direction (for ACC / INIT runs) -> trial -> fg -> probe stats
+    cudaStream_t s = c->stream;
+    k_lbb_direction<<<dim3(1, k), dir_threads, dir_smem, s>>>(D, dir_smem ? 1 : 0);
+    k_lbb_trial<<<dim3(nb, k), LB_T, 0, s>>>(D, 0);
+    int rc = enqueue_fg();
+    if (rc) return rc;
+    k_lbb_probe_stats<<<dim3(nb, k), LB_T, 0, s>>>(D);
+    CUDA_TRY(c, cudaMemcpyAsync(h_st, D.st, sizeof(double) * S_COUNT * k, cudaMemcpyDeviceToHost,
+                                s));
     CUDA_TRY(c, cudaGetLastError());
     return MCP_OK;
   }
 
-  template <typename F>
-  int capture(GraphEntry& ge, F&& body) {
+  int capture(GraphEntry& ge, const std::function<int()>& body) {
     CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     int rc = body();
     cudaError_t ce = cudaStreamEndCapture(c->stream, &ge.graph);
@@ -494,11 +660,6 @@ struct LbRun {
     return MCP_OK;
   }
 
-  bool matches(int d_, int r_, int mode_, int m_, double alpha_) const {
-    return d == d_ && r == r_ && mode == mode_ && m == m_ && n == c->n &&
-           std::memcmp(&alpha, &alpha_, sizeof(double)) == 0;
-  }
-
   int setup() {
     n = c->n;
     N = r + n * r;
@@ -508,167 +669,269 @@ struct LbRun {
     dir_smem = stage_bytes <= 192 * 1024 ? stage_bytes : 0;
     int rc;
     if (dir_smem)
-      CUDA_TRY(c, cudaFuncSetAttribute(k_lb_direction, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(c, cudaFuncSetAttribute(k_lbb_direction, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)dir_smem));
-    const size_t M1 = (size_t)m + 1;
-    if ((rc = alloc(X, N)) || (rc = alloc(OX, N + 1)) || (rc = alloc(T, N)) ||
-        (rc = alloc(OT, N + 1)) || (rc = alloc(B, N)) || (rc = alloc(OB, N + 1)) ||
-        (rc = alloc(P, N)) || (rc = alloc(S, M1 * N)) || (rc = alloc(Y, M1 * N)) ||
-        (rc = alloc(syh, M1)) || (rc = alloc(yyh, M1)) || (rc = alloc(part, LB_NP * nb)) ||
-        (rc = alloc(st, S_COUNT)) || (rc = alloc(a_dev, 1)) || (rc = alloc(Yw, n * r + r)) ||
-        (rc = alloc(ring, 2)) || (rc = alloc(counter, 1)))
+    const size_t K = (size_t)k, M1 = (size_t)m + 1;
+    D.N = N;
+    D.m = m;
+    D.k = k;
+    D.r = r;
+    D.n = n;
+    D.Xb = nullptr;
+    if ((rc = alloc(D.X, K * N)) || (rc = alloc(D.OX, K * (N + 1))) || (rc = alloc(D.T, K * N)) ||
+        (rc = alloc(D.OT, K * (N + 1))) || (rc = alloc(D.B, K * N)) ||
+        (rc = alloc(D.OB, K * (N + 1))) || (rc = alloc(D.P, K * N)) ||
+        (rc = alloc(D.S, K * M1 * N)) || (rc = alloc(D.Y, K * M1 * N)) ||
+        (rc = alloc(D.syh, K * M1)) || (rc = alloc(D.yyh, K * M1)) ||
+        (rc = alloc(D.part, K * nb * LB_NP)) || (rc = alloc(D.st, K * S_COUNT)) ||
+        (rc = alloc(D.a0, K)) || (rc = alloc(D.ah, K)) || (rc = alloc(D.ring, 2 * K)) ||
+        (rc = alloc(D.counter, K)) || (rc = alloc(d_act, K)))
       return rc;
-    CUDA_TRY(c, cudaMemset(counter, 0, sizeof(unsigned)));
-    CUDA_TRY(c, cudaMallocHost(&hst, sizeof(double) * S_COUNT));
-    CUDA_TRY(c, cudaMallocHost(&ha, sizeof(double)));
-    CUDA_TRY(c, cudaMallocHost(&hx, sizeof(double) * N));
-    cudaStream_t s = c->stream;
-    if ((rc = capture(g_init, [&]() -> int {
-           CUDA_TRY(c, cudaMemcpyAsync(X, hx, sizeof(double) * N, cudaMemcpyHostToDevice, s));
-           int e = enqueue_fg(X, OX);
-           if (e) return e;
-           k_lb_eval_stats<<<nb, LB_T, 0, s>>>(N, X, OX, part, counter, st, ring);
-           return enqueue_direction_and_probe();
-         })))
-      return rc;
-    for (int which = 0; which < 2; ++which) {
-      const double* xs = which == 0 ? T : B;
-      const double* os = which == 0 ? OT : OB;
-      if ((rc = capture(which == 0 ? g_iter_t : g_iter_b, [&]() -> int {
-             k_lb_accept<<<nb, LB_T, 0, s>>>(N, xs, os, X, OX, S, Y, ring, part, counter, m,
-                                             syh, yyh, st);
-             return enqueue_direction_and_probe();
-           })))
+    D.act = d_act;
+    if (k > 1) {
+      const int64_t R = (int64_t)k * r;
+      if ((rc = alloc(D.Xb, (size_t)(R + n * R + 1))) || (rc = alloc(Ywb, (size_t)(n * R + R))))
         return rc;
     }
-    if ((rc = capture(g_probe, [&]() -> int {
-           CUDA_TRY(c, cudaMemcpyAsync(a_dev, ha, sizeof(double), cudaMemcpyHostToDevice, s));
-           return enqueue_probe_tail(true);
+    CUDA_TRY(c, cudaMemset(D.counter, 0, sizeof(unsigned) * K));
+    CUDA_TRY(c, cudaMemset(D.P, 0, sizeof(double) * K * N));
+    CUDA_TRY(c, cudaMemset(D.a0, 0, sizeof(double) * K));
+    CUDA_TRY(c, cudaMallocHost(&h_act, sizeof(int) * K));
+    CUDA_TRY(c, cudaMallocHost(&h_a, sizeof(double) * K));
+    CUDA_TRY(c, cudaMallocHost(&h_st, sizeof(double) * K * S_COUNT));
+    CUDA_TRY(c, cudaMallocHost(&h_x, sizeof(double) * K * N));
+    cudaStream_t s = c->stream;
+    // init: evaluate x0 (trial = x), statistics, direction, first probe
+    if ((rc = capture(g_init, [&]() -> int {
+           CUDA_TRY(c, cudaMemcpyAsync(D.X, h_x, sizeof(double) * K * N, cudaMemcpyHostToDevice, s));
+           CUDA_TRY(c, cudaMemcpyAsync(d_act, h_act, sizeof(int) * K, cudaMemcpyHostToDevice, s));
+           k_lbb_trial<<<dim3(nb, k), LB_T, 0, s>>>(D, 1);
+           int e = enqueue_fg();
+           if (e) return e;
+           k_lbb_init_stats<<<dim3(nb, k), LB_T, 0, s>>>(D);
+           return enqueue_round_tail();
+         })))
+      return rc;
+    if ((rc = capture(g_round, [&]() -> int {
+           CUDA_TRY(c, cudaMemcpyAsync(d_act, h_act, sizeof(int) * K, cudaMemcpyHostToDevice, s));
+           CUDA_TRY(c, cudaMemcpyAsync(D.ah, h_a, sizeof(double) * K, cudaMemcpyHostToDevice, s));
+           k_lbb_save<<<dim3(nb, k), LB_T, 0, s>>>(D);
+           k_lbb_accept<<<dim3(nb, k), LB_T, 0, s>>>(D);
+           return enqueue_round_tail();
          })))
       return rc;
     return MCP_OK;
   }
-
-  int save_best() {
-    CUDA_TRY(c, cudaMemcpyAsync(B, T, sizeof(double) * N, cudaMemcpyDeviceToDevice, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(OB, OT, sizeof(double) * (N + 1), cudaMemcpyDeviceToDevice,
-                                c->stream));
-    return MCP_OK;
-  }
 };
 
-// optimize.py:171-176
-bool interp(double a_lo, double f_lo, double d_lo, double a_hi, double f_hi, double* out) {
-  const double den = f_hi - f_lo - d_lo * (a_hi - a_lo);
-  if (den == 0 || !std::isfinite(den)) return false;
-  const double cnd = a_lo - 0.5 * d_lo * ((a_hi - a_lo) * (a_hi - a_lo)) / den;
-  if (!std::isfinite(cnd)) return false;
-  *out = cnd;
-  return true;
-}
-
-struct Pt {
-  double a, f, d;
+// Host-side state of one run
+struct RunState {
+  enum { ITER = 0, SEARCH = 1, DONE = 2 };
+  int phase = ITER;
+  Wolfe w;
+  double f = 0;
+  int64_t n_fg = 0, steps = 0;
+  int reason = 1;        // 0 tolerance, 1 iteration cap, 2 line-search failure, 3 error
+  std::string error;
+  std::vector<double> tf, tt;
 };
 
-enum { WOLFE_T = 0, WOLFE_BEST = 1, WOLFE_FAIL = 2 };
+struct LbOpts {
+  int memory;
+  double pgtol;
+  int64_t max_iters, max_total;
+  double c1, c2;
+  int64_t max_line_steps;
+};
 
-// Strong-Wolfe search (optimize.py:179-252).  The first probe (at a0) has already been run by
-// the iteration graph; its scalars are in R.hst.
-int wolfe(LbRun& R, double f0, double slope0, double a0, double c1, double c2, int64_t budget,
-          int* outcome, double* f_new, int64_t* evals, std::string& err_x) {
-  int64_t ev = 0;
-  bool have_best = false;
-  double best_f = 0.0;
-  bool first = true;
-  int rc;
-  auto probe = [&](double a, double* fa, double* da) -> int {
-    if (!first) {
-      *R.ha = a;
-      if ((rc = R.replay(R.g_probe))) return rc;
-    }
-    first = false;
-    if (R.hst[S_XBAD] > 0.0) {
-      err_x = "model variables and alpha must be finite";
-      return MCP_ERR_ARG;
-    }
-    ++ev;
-    *fa = R.hst[S_FA];
-    *da = std::isfinite(*fa) ? R.hst[S_DA] : NAN;
-    if (std::isfinite(*fa) && *fa <= f0 + c1 * a * slope0) {
-      if (!have_best || *fa < best_f) {
-        have_best = true;
-        best_f = *fa;
-        if ((rc = R.save_best())) return rc;
-      }
-    }
-    return MCP_OK;
-  };
-  auto fallback = [&]() {
-    *evals = ev;
-    if (have_best) {
-      *outcome = WOLFE_BEST;
-      *f_new = best_f;
-    } else {
-      *outcome = WOLFE_FAIL;
-    }
-    return MCP_OK;
-  };
-  Pt prev{0.0, f0, slope0};
-  double a = a0;
-  bool bracketed = false;
-  Pt lo{}, hi{};
-  for (int64_t it = 0; it < budget; ++it) {
-    double fa, da;
-    if ((rc = probe(a, &fa, &da))) return rc;
-    const bool bad = !std::isfinite(fa) || fa > f0 + c1 * a * slope0 ||
-                     (prev.a > 0.0 && fa >= prev.f);
-    if (bad) {
-      lo = prev;
-      hi = Pt{a, fa, da};
-      bracketed = true;
-      break;
-    }
-    if (std::fabs(da) <= -c2 * slope0) {
-      *outcome = WOLFE_T;
-      *f_new = fa;
-      *evals = ev;
-      return MCP_OK;
-    }
-    if (da >= 0.0) {
-      lo = Pt{a, fa, da};
-      hi = prev;
-      bracketed = true;
-      break;
-    }
-    prev = Pt{a, fa, da};
-    a = std::fmin(2.0 * a, 1e20);
-  }
-  if (!bracketed) return fallback();
-  while (ev < budget) {
-    const double width = hi.a - lo.a;
-    double cand = 0.0;
-    bool ok = std::isfinite(hi.f) && interp(lo.a, lo.f, lo.d, hi.a, hi.f, &cand);
-    const double lb = lo.a + 0.1 * width, ub = hi.a - 0.1 * width;
-    if (!ok || !(std::fmin(lb, ub) <= cand && cand <= std::fmax(lb, ub))) cand = lo.a + 0.5 * width;
-    double fa, da;
-    if ((rc = probe(cand, &fa, &da))) return rc;
-    if (!std::isfinite(fa) || fa > f0 + c1 * cand * slope0 || fa >= lo.f) {
-      hi = Pt{cand, fa, da};
-    } else {
-      if (std::fabs(da) <= -c2 * slope0) {
-        *outcome = WOLFE_T;
-        *f_new = fa;
-        *evals = ev;
-        return MCP_OK;
-      }
-      if (da * (hi.a - lo.a) >= 0.0) hi = lo;
-      lo = Pt{cand, fa, da};
-    }
-    if (std::fabs(hi.a - lo.a) < 1e-16 * std::fmax(1.0, std::fabs(lo.a))) break;
-  }
-  return fallback();
+int parse_opts(mcp_ctx* c, const double* opts, LbOpts& o) {
+  o.memory = (int)opts[0];
+  o.pgtol = opts[1];
+  o.max_iters = (int64_t)opts[2];
+  o.max_total = (int64_t)opts[3];
+  o.c1 = opts[4];
+  o.c2 = opts[5];
+  o.max_line_steps = (int64_t)opts[6];
+  if (!(o.pgtol > 0)) return c->fail(MCP_ERR_ARG, "pgtol must be > 0");
+  if (o.memory < 1) return c->fail(MCP_ERR_ARG, "memory must be >= 1");
+  if (o.memory > 64) return c->fail(MCP_ERR_ARG, "memory > 64 is not supported by the device solver");
+  return MCP_OK;
 }
+
+// k lock-step solves from X0 (k x N); per-run results in the output arrays.  A run whose start
+// (or a trial point) is not finite ends with reason 3 and a message in errors[s] (the reference
+// raises ValueError there).
+int run_engine(mcp_ctx* c, int k, int d, int r, double alpha, int mode, const double* X0,
+               const LbOpts& o, double* x_out, double* g_out, double* f_out, double* trace_f,
+               double* trace_t, int64_t trace_cap, int64_t* info, std::vector<std::string>& errors,
+               mcp_iterate_hook hook, void* hook_user) {
+  const auto t_start = std::chrono::steady_clock::now();
+  auto seconds = [&]() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  // plan first: a buffer growth drops cached graphs (and the cached workspace with them)
+  EvalPlan pl;
+  int rc = plan_eval(c, d, k * r, mode, pl);
+  if (rc) return rc;
+  LbEngine* ws = (LbEngine*)c->lbfgs_ws;
+  if (!ws || !ws->matches(k, d, r, mode, o.memory, alpha)) {
+    if (ws) {
+      c->lbfgs_ws_free(ws);
+      c->lbfgs_ws = nullptr;
+    }
+    ws = new LbEngine();
+    ws->c = c;
+    ws->k = k;
+    ws->d = d;
+    ws->r = r;
+    ws->mode = mode;
+    ws->m = o.memory;
+    ws->alpha = alpha;
+    ws->pl = pl;
+    if ((rc = ws->setup())) {
+      delete ws;
+      return rc;
+    }
+    c->lbfgs_ws = ws;
+    c->lbfgs_ws_free = [](void* p) { delete (LbEngine*)p; };
+  }
+  LbEngine& E = *ws;
+  const int64_t N = E.N;
+  std::vector<RunState> R(k);
+  errors.assign(k, std::string());
+  std::memcpy(E.h_x, X0, sizeof(double) * (size_t)k * N);
+  for (int s = 0; s < k; ++s) {
+    E.h_act[s] = ACT_INIT;
+    for (int64_t j = 0; j < N; ++j)
+      if (!std::isfinite(X0[(int64_t)s * N + j])) {
+        R[s].phase = RunState::DONE;
+        R[s].reason = 3;
+        R[s].error = "model variables and alpha must be finite";
+        E.h_act[s] = ACT_IDLE;
+        for (int64_t jj = 0; jj < N; ++jj) E.h_x[(int64_t)s * N + jj] = 0.0;   // keep the pass finite
+        break;
+      }
+  }
+  if ((rc = E.replay(E.g_init))) return rc;
+  auto push_trace = [&](RunState& st, double fv) {
+    st.tf.push_back(fv);
+    st.tt.push_back(seconds());
+  };
+  auto call_hook = [&](int s) -> int {
+    if (!hook) return MCP_OK;
+    CUDA_TRY(c, cudaMemcpyAsync(E.h_x, E.D.X + (int64_t)s * N, sizeof(double) * N,
+                                cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    hook(E.h_x, N, hook_user);
+    return MCP_OK;
+  };
+  for (int s = 0; s < k; ++s) {
+    RunState& st = R[s];
+    if (st.phase == RunState::DONE) continue;
+    const double* h = E.h_st + (int64_t)s * S_COUNT;
+    st.n_fg = 1;
+    if (!std::isfinite(h[S_F]) || h[S_GBAD] > 0.0) {
+      st.phase = RunState::DONE;
+      st.reason = 3;
+      st.error = "objective is not finite at the starting point";
+      continue;
+    }
+    st.f = h[S_F];
+    push_trace(st, st.f);
+    if ((rc = call_hook(s))) return rc;
+  }
+  // ---- lock-step rounds ----
+  while (true) {
+    bool any = false;
+    for (int s = 0; s < k; ++s) {
+      RunState& st = R[s];
+      const double* h = E.h_st + (int64_t)s * S_COUNT;
+      int act = ACT_IDLE;
+      double a_next = 0.0;
+      if (st.phase == RunState::ITER) {
+        // an accepted (or the initial) point: stopping tests (optimize.py:296-301), then the
+        // line search, whose first probe (at a0) this round already evaluated
+        if (h[S_GMAX] <= o.pgtol) {
+          st.phase = RunState::DONE;
+          st.reason = 0;
+        } else if (st.steps >= o.max_iters || st.n_fg >= o.max_total) {
+          st.phase = RunState::DONE;
+          st.reason = 1;
+        } else {
+          const int64_t budget = std::min<int64_t>(o.max_line_steps, o.max_total - st.n_fg);
+          st.w.start(st.f, h[S_SLOPE0], h[S_A0], o.c1, o.c2, budget);
+          if (budget <= 0) {
+            st.phase = RunState::DONE;
+            st.reason = st.n_fg >= o.max_total ? 1 : 2;
+          } else {
+            st.phase = RunState::SEARCH;
+          }
+        }
+      }
+      if (st.phase == RunState::SEARCH) {
+        if (h[S_XBAD] > 0.0) {
+          st.phase = RunState::DONE;
+          st.reason = 3;
+          st.error = "model variables and alpha must be finite";
+        } else {
+          bool save = false;
+          const int out = st.w.on_probe(h[S_FA], h[S_DA], &save, &a_next);
+          if (out == Wolfe::PROBE) {
+            act = ACT_PROBE | (save ? ACT_SAVE : 0);
+          } else {
+            st.n_fg += st.w.ev;
+            if (out == Wolfe::FAIL) {
+              st.phase = RunState::DONE;
+              st.reason = st.n_fg >= o.max_total ? 1 : 2;
+            } else {
+              act = (out == Wolfe::DONE_T ? ACT_ACC_T : ACT_ACC_B) | (save ? ACT_SAVE : 0);
+              st.phase = RunState::ITER;
+              ++st.steps;
+            }
+          }
+        }
+      }
+      E.h_act[s] = act;
+      E.h_a[s] = a_next;
+      if ((act & 7) != ACT_IDLE) any = true;
+    }
+    if (!any) break;
+    if ((rc = E.replay(E.g_round))) return rc;
+    for (int s = 0; s < k; ++s) {
+      const int a = E.h_act[s] & 7;
+      if (a == ACT_ACC_T || a == ACT_ACC_B) {
+        RunState& st = R[s];
+        st.f = E.h_st[(int64_t)s * S_COUNT + S_F];
+        push_trace(st, st.f);
+        if ((rc = call_hook(s))) return rc;
+      }
+    }
+  }
+  // final states
+  CUDA_TRY(c, cudaMemcpy2DAsync(x_out, sizeof(double) * N, E.D.X, sizeof(double) * N,
+                                sizeof(double) * N, k, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpy2DAsync(g_out, sizeof(double) * N, E.D.OX + 1, sizeof(double) * (N + 1),
+                                sizeof(double) * N, k, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int s = 0; s < k; ++s) {
+    RunState& st = R[s];
+    f_out[s] = st.f;
+    const int64_t nt = (int64_t)st.tf.size();
+    for (int64_t i = 0; i < nt && i < trace_cap; ++i) {
+      if (trace_f) trace_f[(int64_t)s * trace_cap + i] = st.tf[i];
+      if (trace_t) trace_t[(int64_t)s * trace_cap + i] = st.tt[i];
+    }
+    int64_t* inf = info + 4 * (int64_t)s;
+    inf[0] = st.n_fg;
+    inf[1] = st.steps;
+    inf[2] = st.reason;
+    inf[3] = std::min(nt, trace_cap);
+    errors[s] = st.error;
+  }
+  return MCP_OK;
+}
+
+thread_local std::string g_batch_errors;
 
 }  // namespace
 
@@ -681,113 +944,40 @@ extern "C" int mcp_lbfgs(mcp_ctx* c, int d, int r, double alpha, int mode, const
   if (!x0 || !opts || !x_out || !g_out || !f_out || !info)
     return c->fail(MCP_ERR_ARG, "NULL argument");
   if (!std::isfinite(alpha)) return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
-  const int memory = (int)opts[0];
-  const double pgtol = opts[1];
-  const int64_t max_iters = (int64_t)opts[2], max_total = (int64_t)opts[3];
-  const double c1 = opts[4], c2 = opts[5];
-  const int64_t max_line_steps = (int64_t)opts[6];
-  if (!(pgtol > 0)) return c->fail(MCP_ERR_ARG, "pgtol must be > 0");
-  if (memory < 1) return c->fail(MCP_ERR_ARG, "memory must be >= 1");
-  if (memory > 64) return c->fail(MCP_ERR_ARG, "memory > 64 is not supported by the device solver");
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
-  const auto t_start = std::chrono::steady_clock::now();
-  auto seconds = [&]() {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-  };
-  // plan first: a buffer growth drops cached graphs (and the cached workspace with them)
-  EvalPlan pl;
-  int rc = plan_eval(c, d, r, mode, pl);
+  LbOpts o;
+  int rc = parse_opts(c, opts, o);
   if (rc) return rc;
-  LbRun* ws = (LbRun*)c->lbfgs_ws;
-  if (!ws || !ws->matches(d, r, mode, memory, alpha)) {
-    if (ws) {
-      c->lbfgs_ws_free(ws);
-      c->lbfgs_ws = nullptr;
-    }
-    ws = new LbRun();
-    ws->c = c;
-    ws->d = d;
-    ws->r = r;
-    ws->mode = mode;
-    ws->m = memory;
-    ws->alpha = alpha;
-    ws->pl = pl;
-    if ((rc = ws->setup())) {
-      delete ws;
-      return rc;
-    }
-    c->lbfgs_ws = ws;
-    c->lbfgs_ws_free = [](void* p) { delete (LbRun*)p; };
-  }
-  LbRun& R = *ws;
-  const int64_t N = R.N;
-  std::memcpy(R.hx, x0, sizeof(double) * N);
-  for (int64_t j = 0; j < N; ++j)
-    if (!std::isfinite(x0[j])) return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
-  if ((rc = R.replay(R.g_init))) return rc;
-  int64_t n_fg = 1;
-  if (!std::isfinite(R.hst[S_F]) || R.hst[S_GBAD] > 0.0)
-    return c->fail(MCP_ERR_ARG, "objective is not finite at the starting point");
-  double f = R.hst[S_F];
-  int64_t n_trace = 0;
-  auto push_trace = [&](double fv) {
-    if (n_trace < trace_cap) {
-      if (trace_f) trace_f[n_trace] = fv;
-      if (trace_t) trace_t[n_trace] = seconds();
-    }
-    ++n_trace;
-  };
-  auto call_hook = [&]() -> int {
-    if (!hook) return MCP_OK;
-    CUDA_TRY(c, cudaMemcpyAsync(R.hx, R.X, sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    hook(R.hx, N, hook_user);
-    return MCP_OK;
-  };
-  push_trace(f);
-  if ((rc = call_hook())) return rc;
-  int64_t steps = 0;
-  int reason = 1;
-  std::string err_x;
-  while (true) {
-    if (R.hst[S_GMAX] <= pgtol) {
-      reason = 0;
-      break;
-    }
-    if (steps >= max_iters || n_fg >= max_total) {
-      reason = 1;
-      break;
-    }
-    const double slope0 = R.hst[S_SLOPE0], a0 = R.hst[S_A0];
-    const int64_t budget = std::min<int64_t>(max_line_steps, max_total - n_fg);
-    int outcome = WOLFE_FAIL;
-    double f_new = f;
-    int64_t ev = 0;
-    if (budget > 0) {
-      rc = wolfe(R, f, slope0, a0, c1, c2, budget, &outcome, &f_new, &ev, err_x);
-      if (rc) return rc == MCP_ERR_ARG ? c->fail(rc, err_x) : rc;
-    }
-    n_fg += ev;
-    if (outcome == WOLFE_FAIL) {
-      reason = n_fg >= max_total ? 1 : 2;
-      break;
-    }
-    // accept, curvature-test the pair, next direction and its first probe -- one replay
-    if ((rc = R.replay(outcome == WOLFE_T ? R.g_iter_t : R.g_iter_b))) return rc;
-    f = R.hst[S_F];
-    ++steps;
-    push_trace(f);
-    if ((rc = call_hook())) return rc;
-  }
-  // the final state: x, [f; g]
-  CUDA_TRY(c, cudaMemcpyAsync(x_out, R.X, sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(g_out, R.OX + 1, sizeof(double) * N, cudaMemcpyDeviceToHost,
-                              c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  *f_out = f;
-  info[0] = n_fg;
-  info[1] = steps;
-  info[2] = reason;
-  info[3] = std::min(n_trace, trace_cap);
+  std::vector<std::string> errors;
+  rc = run_engine(c, 1, d, r, alpha, mode, x0, o, x_out, g_out, f_out, trace_f, trace_t,
+                  trace_cap, info, errors, hook, hook_user);
+  if (rc) return rc;
+  if (info[2] == 3) return c->fail(MCP_ERR_ARG, errors[0]);
   return MCP_OK;
 }
+
+extern "C" int mcp_lbfgs_batch(mcp_ctx* c, int k, int d, int r, double alpha, int mode,
+                               const double* X0, const double* opts, double* X_out,
+                               double* G_out, double* F_out, double* trace_f, double* trace_t,
+                               int64_t trace_cap, int64_t* info) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!X0 || !opts || !X_out || !G_out || !F_out || !info)
+    return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (k < 1) return c->fail(MCP_ERR_ARG, "number of starts must be >= 1");
+  if (!std::isfinite(alpha)) return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
+  if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
+  LbOpts o;
+  int rc = parse_opts(c, opts, o);
+  if (rc) return rc;
+  std::vector<std::string> errors;
+  rc = run_engine(c, k, d, r, alpha, mode, X0, o, X_out, G_out, F_out, trace_f, trace_t, trace_cap,
+                  info, errors, nullptr, nullptr);
+  if (rc) return rc;
+  g_batch_errors.clear();
+  for (int s = 0; s < k; ++s)
+    if (!errors[s].empty()) g_batch_errors += "run " + std::to_string(s) + ": " + errors[s] + "\n";
+  return MCP_OK;
+}
+
+extern "C" const char* mcp_lbfgs_batch_errors(void) { return g_batch_errors.c_str(); }

@@ -216,6 +216,77 @@ def adam_minimize(obs: ObservationSet, d: int, r_hat: int, x0: np.ndarray, cfg: 
                      trace=out["trace"])
 
 
+def lbfgs_minimize_batched(fg: FgCallback, X0, cfg: OptConfig,
+                           shape: tuple[int, int] | None = None) -> list[RunReport | Exception]:
+    """k L-BFGS solves in lock step on the device.
+
+    Row s of ``X0`` is start s.  Each round evaluates one trial point per unfinished run, all of
+    them in ONE pass over V (k r factor columns), so k starts cost about one start's latency per
+    round.  Every run takes the reference's decisions (optimize.py:255-355) on its own scalars;
+    its result equals ``lbfgs_minimize(fg, X0[s], cfg)`` up to the fp64 reassociation of the
+    shared pass.  Runs that fail (non-finite start) come back as ValueError instances.
+    """
+    import time
+
+    problem = getattr(fg, "device_problem", None)
+    if problem is None:
+        raise TypeError("lbfgs_minimize_batched runs on the device: pass the fg returned by "
+                        "packed_fg_implicit(obs, d, r, alpha)")
+    obs, d, r, alpha, mode = problem
+    X0 = np.asarray(X0, dtype=float)
+    if X0.ndim != 2 or X0.shape[1] != r + obs.n * r:
+        raise ValueError(f"expected a (k, {r + obs.n * r}) batch of starts, got {X0.shape}")
+    start = time.perf_counter()
+    opts = (cfg.memory, cfg.pgtol, cfg.max_iters, cfg.max_total_iters, cfg.sufficient_decrease,
+            cfg.curvature, cfg.max_line_steps)
+    outs = obs.device_context().lbfgs_batch(X0, obs.n, d, r, alpha, mode, opts)
+    wall = time.perf_counter() - start
+    reports: list[RunReport | Exception] = []
+    for out in outs:
+        if out["reason"] == "error":
+            reports.append(ValueError(out["error"]))
+            continue
+        x = out["x"]
+        lam, A = (x.copy(), np.empty((0, 0))) if shape is None else unpack(x, *shape)
+        reports.append(RunReport(lam=lam, A=A, f=out["f"],
+                                 grad_inf_norm=float(np.abs(out["g"]).max()), n_fg=out["n_fg"],
+                                 n_steps=out["n_steps"], wall_time=wall, reason=out["reason"],
+                                 seed=cfg.seed, trace=out["trace"]))
+    return reports
+
+
+def multistart_lbfgs(k: int, init: Callable[[np.random.Generator], np.ndarray],
+                     fg: FgCallback, cfg: OptConfig, seed: int,
+                     shape: tuple[int, int] | None = None) -> RunReport:
+    """multistart (optimize.py:454-508) of device L-BFGS runs, all k in lock step.
+
+    Seeding and selection are the reference's: start i is ``init(default_rng(SeedSequence(seed)
+    .spawn(k)[i]))``; the lowest final f wins (ties by run index); failures are collected and an
+    all-failed batch raises RuntimeError.
+    """
+    if k < 1:
+        raise ValueError(f"number of starts must be >= 1, got {k}")
+    root = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
+    children = root.spawn(k)
+    X0 = np.stack([np.asarray(init(np.random.default_rng(children[i])), dtype=float)
+                   for i in range(k)])
+    reports = lbfgs_minimize_batched(fg, X0, cfg, shape)
+    successes, errors = [], []
+    for i, rep in enumerate(reports):
+        if isinstance(rep, Exception):
+            errors.append(f"run {i}: {rep}")
+        else:
+            rep.run_index = i
+            successes.append(rep)
+    if not successes:
+        raise RuntimeError("all multistart runs failed: " + "; ".join(errors))
+    best = min(successes, key=lambda rp: (rp.f, rp.run_index))
+    best.runs = successes
+    best.failures = errors
+    best.seed = seed if isinstance(seed, int) else None
+    return best
+
+
 def multistart(k: int, init: Callable[[np.random.Generator], np.ndarray],
                minimize: Callable[[np.ndarray, np.random.Generator], RunReport], seed: int,
                threads: int = 1) -> RunReport:

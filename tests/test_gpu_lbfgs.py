@@ -128,3 +128,66 @@ def test_multistart_device_lbfgs_threads_equal_sequential():
     assert len(seq.runs) == 4 and seq.f == min(r.f for r in seq.runs)
     assert thr.run_index == seq.run_index and thr.f == seq.f
     assert all(a.f == b.f and np.array_equal(a.A, b.A) for a, b in zip(seq.runs, thr.runs))
+
+
+def _starts(cfg, k, seed=11):
+    rng = np.random.default_rng(seed)
+    X = []
+    for _ in range(k):
+        A = rng.standard_normal((cfg.n, cfg.r))
+        X.append(mcp.pack(np.full(cfg.r, 1.0 / cfg.r), A / np.linalg.norm(A, axis=0)))
+    return np.stack(X)
+
+
+def test_batched_lbfgs_single_start_is_the_single_solver_bitwise():
+    cfg, obs, x0 = _c1()
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+    oc = mcp.OptConfig(max_iters=40)
+    one = mcp.lbfgs_minimize(fg, x0, oc)
+    (bat,) = mcp.lbfgs_minimize_batched(fg, x0[None, :], oc)
+    assert bat.n_fg == one.n_fg and bat.n_steps == one.n_steps and bat.reason == one.reason
+    assert [t[0] for t in bat.trace] == [t[0] for t in one.trace]
+    assert np.array_equal(bat.lam, one.lam)
+
+
+def test_batched_lbfgs_runs_follow_their_single_solves():
+    """k = 5 lock-step runs: each matches its own single-run solve (same decisions; the shared
+    pass changes only fp64 reassociation, so the opening steps agree to 1e-10)."""
+    cfg, obs, _ = _c1()
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+    X0 = _starts(cfg, 5)
+    oc = mcp.OptConfig(max_iters=12)
+    bat = mcp.lbfgs_minimize_batched(fg, X0, oc, shape=(cfg.n, cfg.r))
+    for s in range(5):
+        one = mcp.lbfgs_minimize(fg, X0[s], oc, shape=(cfg.n, cfg.r))
+        assert bat[s].n_steps == one.n_steps and bat[s].reason == one.reason, s
+        ft_b = np.array([t[0] for t in bat[s].trace])
+        ft_o = np.array([t[0] for t in one.trace])
+        assert ft_b.shape == ft_o.shape
+        assert np.allclose(ft_b, ft_o, rtol=1e-10, atol=1e-14), s
+        assert np.allclose(bat[s].A, one.A, rtol=1e-7, atol=1e-9), s
+
+
+def test_multistart_lbfgs_semantics_and_failures():
+    cfg, obs, _ = _c1()
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+
+    def init(rng):
+        A = rng.standard_normal((cfg.n, cfg.r))
+        return mcp.pack(np.full(cfg.r, 1.0 / cfg.r), A / np.linalg.norm(A, axis=0))
+
+    oc = mcp.OptConfig(max_iters=10)
+    best = mcp.multistart_lbfgs(4, init, fg, oc, seed=3, shape=(cfg.n, cfg.r))
+    seq = mcp.multistart(4, init, lambda x0, rng: mcp.lbfgs_minimize(fg, x0, oc, (cfg.n, cfg.r)),
+                         seed=3)
+    assert len(best.runs) == 4 and best.run_index == seq.run_index
+    for a, b in zip(best.runs, seq.runs):
+        assert abs(a.f - b.f) <= 1e-9 * abs(b.f)
+    # a non-finite start fails alone
+    X0 = _starts(cfg, 3)
+    X0[1, 4] = np.nan
+    reps = mcp.lbfgs_minimize_batched(fg, X0, oc)
+    assert isinstance(reps[1], ValueError)
+    assert not isinstance(reps[0], Exception) and not isinstance(reps[2], Exception)
+    one = mcp.lbfgs_minimize(fg, X0[2], oc)
+    assert abs(reps[2].f - one.f) <= 1e-9 * abs(one.f)

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--mode", default="fp64")
     ap.add_argument("--pgtol", type=float, default=1e-4)
     ap.add_argument("--skip-host", action="store_true")
+    ap.add_argument("--k", type=int, default=0, help="also time k lock-step starts")
     args = ap.parse_args()
     for name in args.configs.split(","):
         cfg = synth.CONFIGS[name]
@@ -46,8 +47,20 @@ def main():
         host = (lo.lbfgs(fg, x0, max_iters=args.iters, pgtol=args.pgtol) if not args.skip_host
                 else {"n_fg": 0, "n_steps": 0, "f": None})
         th = time.perf_counter() - t
+        batched = None
+        if args.k > 1:
+            rng = np.random.default_rng(5)
+            X0 = np.stack([x0] + [mcp.pack(lam, rng.standard_normal(A.shape) / np.sqrt(cfg.n))
+                                  for _ in range(args.k - 1)])
+            mcp.lbfgs_minimize_batched(fg, X0, mcp.OptConfig(max_iters=2))   # warm-up
+            t = time.perf_counter()
+            reps = mcp.lbfgs_minimize_batched(fg, X0, oc)
+            tb = time.perf_counter() - t
+            ev = sum(rp.n_fg for rp in reps)
+            batched = {"k": args.k, "n_fg_total": ev, "s": tb, "evals_per_s": ev / tb,
+                       "steps": [rp.n_steps for rp in reps]}
         print(json.dumps({
-            "config": name, "mode": args.mode, "iters": args.iters,
+            "config": name, "mode": args.mode, "iters": args.iters, "batched": batched,
             "device": {"n_fg": dev.n_fg, "n_steps": dev.n_steps, "s": td,
                        "evals_per_s": dev.n_fg / td, "ms_per_step": 1e3 * td / max(dev.n_steps, 1),
                        "f": dev.f},

@@ -170,10 +170,25 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   const int64_t n = c->n;
   t.nkb = (int)ceil_div(n, 32);
   t.mt2 = (int)ceil_div(n, 128);
-  int RB = 16;  // 16, 32 or 64 columns per CTA block
-  while (RB < r && RB < 64) RB *= 2;
-  while (RB > 16 && (1 + t.mt2) * RB > 512) RB /= 2;
-  if ((1 + t.mt2) * RB > 512)
+  // column block RB (the UMMA N): as wide as TMEM allows -- Z (K1T2: double-buffered) plus
+  // Y[mt] for the n / 128 m-tiles -- since the 3xTF32 UMMAs are shared-memory-bandwidth bound
+  // and the operand bytes per MAC fall with N.  K1T2 takes any multiple of 16 up to 64, K1T
+  // powers of two.
+  const bool v1 = getenv("MCP_K1T_V1") != nullptr;
+  const int zbufs = v1 ? 1 : 2;
+  int RB = 16;
+  if (v1) {
+    while (RB < r && RB < 64) RB *= 2;
+    while (RB > 16 && (zbufs + t.mt2) * RB > 512) RB /= 2;
+  } else {
+    const int want = (int)std::min<int64_t>(64, round_up(r, 16));
+    RB = want;
+    while (RB > 16 && (zbufs + t.mt2) * RB > 512) RB -= 16;
+    // prefer the widest block that does not add a column block over the narrowest
+    const int rbs_w = (int)ceil_div(r, RB);
+    while (RB > 16 && ceil_div(r, RB - 16) == rbs_w && (RB - 16) >= r / rbs_w) RB -= 16;
+  }
+  if ((zbufs + t.mt2) * RB > 512)
     return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
   t.RB = RB;
   t.rbs = (int)ceil_div(r, RB);
@@ -217,6 +232,28 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
       return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for V");
     c->tm_v_ready = true;
   }
+  // K1T2: V_lo precomputed once per set (falls back to the in-kernel split if it does not fit)
+  t.v2 = false;
+  if (!getenv("MCP_K1T_V1")) {
+    if (!c->dVlo32) {
+      const size_t bytes = sizeof(float) * (size_t)c->p_pad * c->ldv32;
+      if (cudaMalloc(&c->dVlo32, bytes) == cudaSuccess) {
+        k_split_lo<<<grid_for(c->p_pad * c->ldv32, 256, 16 * c->sms), 256, 0, c->stream>>>(
+            c->dV32, c->dVlo32, c->p_pad * c->ldv32);
+        CUDA_TRY(c, cudaGetLastError());
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        if (!make_tmap_f32(&c->tm_l1, c->dVlo32, c->ldv32, c->p_pad, 4 * c->ldv32, 32, 128,
+                           CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !make_tmap_f32(&c->tm_l2, c->dVlo32, c->ldv32, c->p_pad, 4 * c->ldv32, 32, 32,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+          return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for V_lo");
+      } else {
+        (void)cudaGetLastError();
+        c->dVlo32 = nullptr;
+      }
+    }
+    t.v2 = c->dVlo32 != nullptr;
+  }
   int rc;
   if ((rc = ensure(c, c->dAt, sizeof(float) * 2 * (size_t)t.r_pad * t.kpad))) return rc;
   if (c->tm_a_addr != c->dAt.p || c->tm_a_rows != 2 * t.r_pad || c->tm_a_kpad != t.kpad ||
@@ -229,8 +266,8 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     c->tm_a_kpad = t.kpad;
     c->tm_a_rb = RB;
   }
-  CUDA_TRY(c, cudaFuncSetAttribute(k1t_fg_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)t.smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(t.v2 ? (const void*)k1t2_fg_tf32 : (const void*)k1t_fg_tf32,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
   pl.k1 = K1Variant();
   pl.k1.kind = 2;
   pl.k1.RB = RB;
@@ -240,7 +277,8 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.ypart_elems = (size_t)t.rbs * t.gp * t.mt2 * 128 * RB;
   pl.k1.wpart_elems = 0;
   pl.k1.afrag_elems = 0;
-  pl.k1.name = "k1t_fg_tf32<3xTF32,RB=" + std::to_string(RB) + ",S=" + std::to_string(ns) + ">";
+  pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
+                std::to_string(RB) + ",S=" + std::to_string(ns) + ">";
   return MCP_OK;
 }
 
@@ -308,7 +346,11 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.nu_const = c->nu_const;
   prm.Ypart = (double*)c->dYpart.p;
   auto* ev = timing_begin(c, s);
-  k1t_fg_tf32<<<t.gp * t.rbs, K1T_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_a, prm);
+  if (t.v2)
+    k1t2_fg_tf32<<<t.gp * t.rbs, K1T2_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_l1, c->tm_l2,
+                                                             c->tm_a, prm);
+  else
+    k1t_fg_tf32<<<t.gp * t.rbs, K1T_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_a, prm);
   timing_end(ev, s);
   const int64_t red_blocks = (int64_t)t.rbs * ceil_div((int64_t)n * t.RB, K3_X);
   k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
@@ -587,6 +629,8 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   drop_graphs(c);
   if (c->own_v32 && c->dV32) cudaFree(c->dV32);
   c->dV32 = nullptr;
+  if (c->dVlo32) cudaFree(c->dVlo32);
+  c->dVlo32 = nullptr;
   c->own_v32 = false;
   c->tm_v_ready = false;
   int rc = dtype == MCP_F64
@@ -611,6 +655,8 @@ void release_ctx(mcp_ctx* c) {
     if (b->p) cudaFree(b->p);
   if (c->own_v32 && c->dV32) cudaFree(c->dV32);
   c->dV32 = nullptr;
+  if (c->dVlo32) cudaFree(c->dVlo32);
+  c->dVlo32 = nullptr;
   if (c->hx) cudaFreeHost(c->hx);
   if (c->hout) cudaFreeHost(c->hout);
   c->hx = c->hout = nullptr;

@@ -59,6 +59,8 @@ struct mcp_ctx {
   int64_t ldv32 = 0;
   bool tm_v_ready = false;
   CUtensorMap tm_v1, tm_v2, tm_a;
+  float* dVlo32 = nullptr;     // fast mode K1T2: V - tf32(V), same layout as dV32
+  CUtensorMap tm_l1, tm_l2;
   void* tm_a_addr = nullptr;
   int tm_a_rows = 0, tm_a_kpad = 0, tm_a_rb = 0;
   mcp_internal::DevBuf dAt;
@@ -98,6 +100,7 @@ namespace mcp_internal {
 // Shape of the fast-mode (K1T) launch.
 struct K1TPlan {
   int RB = 0, rbs = 0, gp = 0, stages = 0, nkb = 0, mt2 = 0, r_pad = 0, kpad = 0;
+  bool v2 = false;   // K1T2 (precomputed V_lo) instead of K1T (in-kernel split)
   int64_t num_tiles = 0;
   size_t smem = 0;
 };

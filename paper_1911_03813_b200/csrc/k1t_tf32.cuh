@@ -338,4 +338,330 @@ __global__ void k_f64_to_f32(const double* __restrict__ src, float* __restrict__
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// K1T2: the fast-mode kernel without the CUDA-core split on the critical path.  The low halves
+// V_lo = V - tf32(V) are computed ONCE per observation set (k_split_lo, kept in HBM next to the
+// fp32 rows: +1x V of memory, c5 65.5 -> 131 GB) and streamed by TMA like V itself; the tensor
+// core truncates the fp32 rows to TF32 on read, so the resident fp32 V doubles as V_hi.
+// Tiles are software-pipelined: Z is double-buffered in TMEM and the MMA issuer runs
+// GEMM1(u) before GEMM2(u - 1), so the epilogue of a tile (P = nu z^(d-1) -> TF32 hi/lo bricks,
+// measured ~15k cycles) overlaps the next tile's GEMM1 instead of stalling the tensor pipe.
+// Roles: warp 0 TMA producer, warp 1 MMA issuer + TMEM owner, warps 2..9 epilogue / flush (two
+// per TMEM sub-partition, each on half of the columns).  TMEM: Z0, Z1, then Y[mt]:
+// (2 + n/128) RB <= 512 columns.
+constexpr int K1T2_EPI_WARPS = 8;
+constexpr int K1T2_THREADS = (2 + K1T2_EPI_WARPS) * 32;
+#ifndef MCP_K1T2_PROF
+#define MCP_K1T2_PROF 0   // diagnostics only: CTA 0 prints per-role wait / busy cycles
+#endif
+#if MCP_K1T2_PROF
+#define K1T2_T0() const long long _t0 = clock64()
+#define K1T2_ACC(v) v += clock64() - _t0
+#else
+#define K1T2_T0()
+#define K1T2_ACC(v)
+#endif
+#ifndef MCP_K1T2_EXP_NOLO2
+#define MCP_K1T2_EXP_NOLO2 0   // timing experiment only: skip the GEMM2 V_lo loads (wrong results)
+#endif
+
+__global__ void __launch_bounds__(K1T2_THREADS, 1)
+    k1t2_fg_tf32(const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_v2,
+                 const __grid_constant__ CUtensorMap tm_l1, const __grid_constant__ CUtensorMap tm_l2,
+                 const __grid_constant__ CUtensorMap tm_a, K1TParams prm) {
+  extern __shared__ __align__(16) unsigned char smem_raw_t2[];
+  unsigned char* base = smem_raw_t2 + ((1024u - (smem_u32(smem_raw_t2) & 1023u)) & 1023u);
+  const int RB = prm.RB, NS = prm.stages;
+  const size_t SB = k1t_stage_bytes(RB);
+  unsigned char* sPh = base + NS * SB;
+  unsigned char* sPl = sPh + 512 * RB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sPl + 512 * RB);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NS;
+  uint64_t* z_full = bars + 2 * NS;     // [2]
+  uint64_t* p_full = z_full + 2;
+  uint64_t* p_empty = z_full + 3;
+  uint64_t* y_full = z_full + 4;
+  uint64_t* y_empty = z_full + 5;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(z_full + 6);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = blockIdx.x % prm.rbs;
+  const int pg = blockIdx.x / prm.rbs;
+  const int64_t my_tiles =
+      pg < prm.num_tiles ? (prm.num_tiles - pg + prm.gp - 1) / prm.gp : 0;
+  const int mt2 = prm.mt2, nkb = prm.nkb;
+  auto flush_after = [&](int64_t v) {   // tile v ends a group of K1T_FLUSH tiles (or the last)
+    return (v % K1T_FLUSH) == K1T_FLUSH - 1 || v == my_tiles - 1;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&z_full[0], 1);
+    mbar_init(&z_full[1], 1);
+    mbar_init(p_full, K1T2_EPI_WARPS);
+    mbar_init(p_empty, 1);
+    mbar_init(y_full, 1);
+    mbar_init(y_empty, K1T2_EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc<512>(smem_u32(tslot));
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_v1);
+    tma_prefetch_desc(&tm_v2);
+    tma_prefetch_desc(&tm_l1);
+    tma_prefetch_desc(&tm_l2);
+    tma_prefetch_desc(&tm_a);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t ty = tmem + 2 * RB;   // Y[mt] at columns (2 + mt) RB; Z[b] at b RB
+
+  if (warp == 0) {
+    // =========================== TMA producer (same order as the MMA issuer) ===========================
+    if (lane == 0) {
+      int64_t q = 0;
+      auto stage = [&](int64_t qq) -> unsigned char* {
+        const int s = (int)(qq % NS);
+        if (qq >= NS) mbar_wait(&empty[s], (uint32_t)((qq / NS) - 1) & 1);
+        return base + s * SB;
+      };
+      for (int64_t u = 0; u <= my_tiles; ++u) {
+        if (u < my_tiles) {
+          const int row0 = (int)((pg + u * prm.gp) * K1T_TP);
+          for (int kb = 0; kb < nkb; ++kb, ++q) {
+            unsigned char* st = stage(q);
+            uint64_t* fb = &full[q % NS];
+            mbar_arrive_expect_tx(fb, 2 * K1T_VBYTES + 256 * RB);
+            tma_load_2d(st, &tm_v1, kb * 32, row0, smem_u32(fb));
+            tma_load_2d(st + K1T_VBYTES, &tm_l1, kb * 32, row0, smem_u32(fb));
+            tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, kb * 32, rb * RB, smem_u32(fb));
+            tma_load_2d(st + 2 * K1T_VBYTES + 128 * RB, &tm_a, kb * 32, prm.r_pad + rb * RB,
+                        smem_u32(fb));
+          }
+        }
+        if (u >= 1) {
+          const int row0 = (int)((pg + (u - 1) * prm.gp) * K1T_TP);
+          for (int step = 0; step < 4 * mt2; ++step, ++q) {
+            const int mt = step >> 2, rc = step & 3;
+            unsigned char* st = stage(q);
+            uint64_t* fb = &full[q % NS];
+            mbar_arrive_expect_tx(fb, (MCP_K1T2_EXP_NOLO2 ? 1 : 2) * K1T_VBYTES);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              tma_load_2d(st + b * 4096, &tm_v2, mt * 128 + b * 32, row0 + rc * 32, smem_u32(fb));
+              if (!MCP_K1T2_EXP_NOLO2)
+                tma_load_2d(st + K1T_VBYTES + b * 4096, &tm_l2, mt * 128 + b * 32, row0 + rc * 32,
+                            smem_u32(fb));
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // =========================== MMA issuer ===========================
+    if (lane == 0) {
+      const uint32_t id1 = umma_idesc_tf32(128, RB, false, false);
+      const uint32_t id2 = umma_idesc_tf32(128, RB, true, false);
+      int64_t q = 0;
+      int flushes = 0;
+      bool fresh = true, wait_y = false;
+      long long w_full1 = 0, w_full2 = 0, w_p = 0, w_y = 0;
+      const long long t_begin = clock64();
+      for (int64_t u = 0; u <= my_tiles; ++u) {
+        if (u < my_tiles) {
+          // ---- GEMM1(u): Z[u & 1] = V A (3xTF32) ----
+          const uint32_t tz = tmem + (uint32_t)((u & 1) * RB);
+          for (int kb = 0; kb < nkb; ++kb, ++q) {
+            const int s = (int)(q % NS);
+            {
+              K1T2_T0();
+              mbar_wait(&full[s], (uint32_t)(q / NS) & 1);
+              K1T2_ACC(w_full1);
+            }
+            tc_fence_after();
+            // descriptors are affine in the smem address: +16 B adds 1 to the start field, so
+            // the 12 instructions of a stage reuse 4 base descriptors (cheap single-lane issue)
+            const uint32_t v_hi = smem_u32(base + s * SB);
+            const uint64_t dvh = umma_desc_sw128(v_hi, 16, 1024);
+            const uint64_t dvl = dvh + (K1T_VBYTES >> 4);
+            const uint64_t dah = dvh + ((2 * K1T_VBYTES) >> 4);
+            const uint64_t dal = dah + ((128 * RB) >> 4);
+#pragma unroll
+            for (int pr = 0; pr < 3; ++pr) {
+              const uint64_t av = pr == 2 ? dvl : dvh, bv = pr == 1 ? dal : dah;
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                umma_tf32(tz, av + 2 * ks, bv + 2 * ks, id1, (kb | pr | ks) != 0 ? 1u : 0u);
+            }
+            umma_commit(smem_u32(&empty[s]));
+          }
+          umma_commit(smem_u32(&z_full[u & 1]));
+        }
+        if (u >= 1) {
+          // ---- GEMM2(u - 1): Y += V^T P (3xTF32) ----
+          const int64_t v = u - 1;
+          {
+            K1T2_T0();
+            mbar_wait(p_full, (uint32_t)v & 1);
+            K1T2_ACC(w_p);
+          }
+          if (wait_y) {
+            K1T2_T0();
+            mbar_wait(y_empty, (uint32_t)(flushes - 1) & 1);
+            K1T2_ACC(w_y);
+            wait_y = false;
+            fresh = true;
+          }
+          tc_fence_after();
+          const uint64_t dph = umma_desc_sw128(smem_u32(sPh), 16, 1024);
+          const uint64_t dpl = umma_desc_sw128(smem_u32(sPl), 16, 1024);
+          for (int step = 0; step < 4 * mt2; ++step, ++q) {
+            const int mt = step >> 2, rc = step & 3;
+            const int s = (int)(q % NS);
+            {
+              K1T2_T0();
+              mbar_wait(&full[s], (uint32_t)(q / NS) & 1);
+              K1T2_ACC(w_full2);
+            }
+            tc_fence_after();
+            const uint64_t dvh = umma_desc_sw128_32b(smem_u32(base + s * SB), 4096, 512);
+            const uint64_t dvl = dvh + (K1T_VBYTES >> 4);
+            const uint64_t boff = (uint64_t)((rc * 128 * RB) >> 4);
+#pragma unroll
+            for (int pr = 0; pr < 3; ++pr) {
+              const uint64_t av = pr == 2 ? dvl : dvh;
+              const uint64_t bv = (pr == 1 ? dpl : dph) + boff;
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                umma_tf32(ty + mt * RB, av + 64 * ks, bv + 2 * ks, id2,
+                          (fresh && rc == 0 && pr == 0 && ks == 0) ? 0u : 1u);
+            }
+            umma_commit(smem_u32(&empty[s]));
+          }
+          fresh = false;
+          umma_commit(smem_u32(p_empty));
+          if (flush_after(v)) {
+            umma_commit(smem_u32(y_full));
+            ++flushes;
+            wait_y = true;
+          }
+        }
+      }
+#if MCP_K1T2_PROF
+      if (blockIdx.x == 0)
+        printf("K1T2 MMA: total %lld  wait full(G1) %lld  full(G2) %lld  p_full %lld  y_empty %lld  tiles %lld\n",
+               clock64() - t_begin, w_full1, w_full2, w_p, w_y, (long long)my_tiles);
+#endif
+      (void)t_begin;
+    }
+  } else {
+    // =========================== epilogue / flush warps ===========================
+    const int ew = warp - 2;                 // 0..7
+    const int sp = warp & 3;                 // TMEM sub-partition this warp may access
+    const int half = ew >> 2;
+    const int l = 32 * sp + lane;            // tile row (TMEM lane) this thread owns
+    const int hc = ((RB / 2 + 15) / 16) * 16;  // columns per warp, whole 16-column loads
+    const bool col_active = half * hc < RB;
+    const int c_end = min(RB, (half + 1) * hc);
+    const int dm1 = prm.d - 1;
+    int flushes = 0;
+    double* Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * (size_t)mt2 * 128 * RB;
+    long long e_wz = 0, e_wp = 0, e_epi = 0, e_fl = 0;
+    auto flush = [&]() {
+      K1T2_T0();
+      mbar_wait(y_full, (uint32_t)flushes & 1);
+      tc_fence_after();
+      for (int mt = 0; mt < mt2; ++mt) {
+        double* yrow = Yp + ((size_t)mt * 128 + l) * RB;
+        for (int c0 = half * hc; col_active && c0 < c_end; c0 += 16) {
+          float yv[16];
+          tmem_ld16(ty + mt * RB + ((uint32_t)(32 * sp) << 16) + c0, yv);
+          // each partial element has exactly one owner thread and flushes are in program order,
+          // so fire-and-forget reductions (RED, no load latency) keep the sum order fixed
+          if (flushes == 0) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) yrow[c0 + jj] = (double)yv[jj];
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) atomicAdd(yrow + c0 + jj, (double)yv[jj]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(y_empty);
+      ++flushes;
+      K1T2_ACC(e_fl);
+    };
+    for (int64_t u = 0; u < my_tiles; ++u) {
+      const int64_t row0 = (pg + u * prm.gp) * K1T_TP;
+      {
+        K1T2_T0();
+        mbar_wait(&z_full[u & 1], (uint32_t)(u >> 1) & 1);
+        K1T2_ACC(e_wz);
+      }
+      if (u > 0) {
+        K1T2_T0();
+        mbar_wait(p_empty, (uint32_t)(u - 1) & 1);   // GEMM2(u - 1) has consumed P
+        K1T2_ACC(e_wp);
+      }
+      tc_fence_after();
+      {
+        K1T2_T0();
+        const uint32_t tz = tmem + (uint32_t)((u & 1) * RB);
+        const double nul = prm.nu ? prm.nu[row0 + l] : prm.nu_const;
+        const int brick = l >> 5, col = l & 31;
+        for (int c0 = half * hc; col_active && c0 < c_end; c0 += 16) {
+          float zv[16];
+          tmem_ld16(tz + ((uint32_t)(32 * sp) << 16) + c0, zv);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const double z = (double)zv[jj];
+            const float pf = (float)(nul * rm_pow(z, dm1));
+            const float ph = tf32_hi(pf);
+            const uint32_t off = brick * 128 * RB + brick_off(c0 + jj, col);
+            *reinterpret_cast<float*>(sPh + off) = ph;
+            *reinterpret_cast<float*>(sPl + off) = pf - ph;
+          }
+        }
+        K1T2_ACC(e_epi);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      if (u >= 1 && flush_after(u - 1)) flush();   // committed after GEMM2(u - 1)
+    }
+    if (my_tiles > 0) flush();                      // the group ending at the last tile
+#if MCP_K1T2_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 64)
+      printf("K1T2 EPI: wait z %lld  wait p_empty %lld  epilogue %lld  flush %lld\n", e_wz, e_wp,
+             e_epi, e_fl);
+#endif
+    if (my_tiles == 0)
+      for (int mt = 0; mt < mt2; ++mt)
+        for (int c = half * hc; col_active && c < c_end; ++c)
+          Yp[((size_t)mt * 128 + l) * RB + c] = 0.0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// V_lo = V - tf32(V) for the fast mode, once per observation set (padding stays zero)
+__global__ void k_split_lo(const float* __restrict__ v, float* __restrict__ lo, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = v[i];
+    lo[i] = x - tf32_hi(x);
+  }
+}
+
 }  // namespace mcp

@@ -323,11 +323,18 @@ def main():
     # ---- data: this rank's rows, generated on its GPU ----
     lo, hi = D.shard_bounds(cfg.p, world, rank)
     Vrows = synth.device_observations(cfg, SEED, device=dev, row_offset=lo, rows=hi - lo)
-    obs = mcp.ObservationSet.from_device(Vrows, p_total=cfg.p)
+    obs = mcp.ObservationSet.from_device(Vrows, p_total=cfg.p, release=True)
     t_up = time.perf_counter()
     ctx = obs.device_context()
     torch.cuda.synchronize()
     t_up = time.perf_counter() - t_up
+    # the CPU leg's bounded sample (host copy), then free the generator's copy: the context
+    # holds the rows (and the fast mode's V_lo needs the room at c5)
+    p_sample = cfg.p if cfg.name in ("c1", "c2") else min(cfg.p, 100_000)
+    Vh_sample = (Vrows[:p_sample].double().cpu().numpy().T
+                 if world == 1 and not args.no_cpu else None)
+    del Vrows
+    torch.cuda.empty_cache()
     lam, A = synth.initial_point(cfg, SEED)
     n, r, d = cfg.n, cfg.r, cfg.d
     x_host = mcp.pack(lam, A)
@@ -526,9 +533,7 @@ def main():
         except Exception:  # noqa: BLE001
             pass
         # bounded CPU sample on this host: the full workload when it fits (c1, c2), else rows
-        p_sample = cfg.p if cfg.name in ("c1", "c2") else min(cfg.p, 100_000)
-        Vh = Vrows[:p_sample].double().cpu().numpy().T          # n x p view (reference layout)
-        times = cpu_arm(cfg, Vh, lam, A, budget_s=12.0)
+        times = cpu_arm(cfg, Vh_sample, lam, A, budget_s=12.0)
         scale = cfg.p / p_sample
         med = statistics.median(times) * scale
         threads = _blas_threads()

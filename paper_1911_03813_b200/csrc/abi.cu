@@ -170,43 +170,6 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   const int64_t n = c->n;
   t.nkb = (int)ceil_div(n, 32);
   t.mt2 = (int)ceil_div(n, 128);
-  // column block RB (the UMMA N): as wide as TMEM allows -- Z (K1T2: double-buffered) plus
-  // Y[mt] for the n / 128 m-tiles -- since the 3xTF32 UMMAs are shared-memory-bandwidth bound
-  // and the operand bytes per MAC fall with N.  K1T2 takes any multiple of 16 up to 64, K1T
-  // powers of two.
-  const bool v1 = getenv("MCP_K1T_V1") != nullptr;
-  const int zbufs = v1 ? 1 : 2;
-  int RB = 16;
-  if (v1) {
-    while (RB < r && RB < 64) RB *= 2;
-    while (RB > 16 && (zbufs + t.mt2) * RB > 512) RB /= 2;
-  } else {
-    const int want = (int)std::min<int64_t>(64, round_up(r, 16));
-    RB = want;
-    while (RB > 16 && (zbufs + t.mt2) * RB > 512) RB -= 16;
-    // prefer the widest block that does not add a column block over the narrowest
-    const int rbs_w = (int)ceil_div(r, RB);
-    while (RB > 16 && ceil_div(r, RB - 16) == rbs_w && (RB - 16) >= r / rbs_w) RB -= 16;
-  }
-  if ((zbufs + t.mt2) * RB > 512)
-    return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
-  t.RB = RB;
-  t.rbs = (int)ceil_div(r, RB);
-  t.r_pad = t.rbs * RB;
-  t.kpad = t.nkb * 32;
-  const size_t budget = 227 * 1024;
-  int ns = (int)((budget - k1t_smem_bytes(RB, 0)) / k1t_stage_bytes(RB));
-  if (ns > 8) ns = 8;
-  if (ns < 2) return c->fail(MCP_ERR_ARG, "tf32x3 stage ring does not fit");
-  t.stages = ns;
-  t.smem = k1t_smem_bytes(RB, ns);
-  t.num_tiles = c->p_pad / K1T_TP;
-  int64_t G = c->sms;
-  if (G < t.rbs) G = t.rbs;
-  G -= G % t.rbs;
-  int64_t gp = G / t.rbs;
-  if (gp > t.num_tiles) gp = t.num_tiles;
-  t.gp = (int)std::max<int64_t>(gp, 1);
   // fp32 copy of V (fp64 sets), tensor maps over it
   if (!c->dV32) {
     if (c->dtype == MCP_F32) {
@@ -254,6 +217,43 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     }
     t.v2 = c->dVlo32 != nullptr;
   }
+  // column block RB (the UMMA N): as wide as TMEM allows -- Z (K1T2: double-buffered) plus
+  // Y[mt] for the n / 128 m-tiles -- since the 3xTF32 UMMAs are shared-memory-bandwidth bound
+  // and the operand bytes per MAC fall with N.  K1T2 takes any multiple of 16 up to 64, K1T
+  // powers of two.
+  const bool v1 = !t.v2;
+  const int zbufs = v1 ? 1 : 2;
+  int RB = 16;
+  if (v1) {
+    while (RB < r && RB < 64) RB *= 2;
+    while (RB > 16 && (zbufs + t.mt2) * RB > 512) RB /= 2;
+  } else {
+    const int want = (int)std::min<int64_t>(64, round_up(r, 16));
+    RB = want;
+    while (RB > 16 && (zbufs + t.mt2) * RB > 512) RB -= 16;
+    // prefer the widest block that does not add a column block over the narrowest
+    const int rbs_w = (int)ceil_div(r, RB);
+    while (RB > 16 && ceil_div(r, RB - 16) == rbs_w && (RB - 16) >= r / rbs_w) RB -= 16;
+  }
+  if ((zbufs + t.mt2) * RB > 512)
+    return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
+  t.RB = RB;
+  t.rbs = (int)ceil_div(r, RB);
+  t.r_pad = t.rbs * RB;
+  t.kpad = t.nkb * 32;
+  const size_t budget = 227 * 1024;
+  int ns = (int)((budget - k1t_smem_bytes(RB, 0)) / k1t_stage_bytes(RB));
+  if (ns > 8) ns = 8;
+  if (ns < 2) return c->fail(MCP_ERR_ARG, "tf32x3 stage ring does not fit");
+  t.stages = ns;
+  t.smem = k1t_smem_bytes(RB, ns);
+  t.num_tiles = c->p_pad / K1T_TP;
+  int64_t G = c->sms;
+  if (G < t.rbs) G = t.rbs;
+  G -= G % t.rbs;
+  int64_t gp = G / t.rbs;
+  if (gp > t.num_tiles) gp = t.num_tiles;
+  t.gp = (int)std::max<int64_t>(gp, 1);
   int rc;
   if ((rc = ensure(c, c->dAt, sizeof(float) * 2 * (size_t)t.r_pad * t.kpad))) return rc;
   if (c->tm_a_addr != c->dAt.p || c->tm_a_rows != 2 * t.r_pad || c->tm_a_kpad != t.kpad ||

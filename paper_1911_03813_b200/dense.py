@@ -52,12 +52,15 @@ class ObservationSet:
         self._host_obs = None  # (p x n) host array when constructed observation-major
 
     @classmethod
-    def from_device(cls, V_obs_major, nu=None, labels=None, *, p_total: int | None = None):
+    def from_device(cls, V_obs_major, nu=None, labels=None, *, p_total: int | None = None,
+                    release: bool = False):
         """Wrap a CUDA tensor holding observations row-wise (p x n, each row one v_l).
 
         This is the layout the kernels use, so nothing is transposed or copied to the host;
         the tensor is validated and uploaded device-to-device.  ``p_total`` (row shards only)
-        sets the uniform weight to 1/p_total instead of 1/p.
+        sets the uniform weight to 1/p_total instead of 1/p.  ``release=True`` drops this
+        object's reference to the tensor once it is uploaded (HBM for very large sets: the
+        context keeps its own copy), after which ``V`` is no longer available.
         """
         import torch
 
@@ -82,6 +85,7 @@ class ObservationSet:
         self._dev = None
         self._dev_lock = threading.Lock()
         self._dev_obs = V_obs_major.contiguous()
+        self._release = bool(release)
         return self
 
     @classmethod
@@ -123,6 +127,8 @@ class ObservationSet:
             elif getattr(self, "_host_obs", None) is not None:
                 self._V64 = np.asarray(self._host_obs, dtype=float).T
             else:
+                if getattr(self, "_released", False):
+                    raise RuntimeError("V was released after the upload (from_device(release=True))")
                 self._V64 = self._dev_obs.double().t().cpu().numpy()
         return self._V64
 
@@ -165,6 +171,12 @@ class ObservationSet:
                         nu_ptr = self._nu_dev.data_ptr()
                     ctx.load_obs_device(t.data_ptr(), code, _native.MCP_OBS_MAJOR, self._n,
                                         self._p, t.stride(0), nu_ptr, self._nu_const)
+                    if getattr(self, "_release", False):
+                        import torch
+
+                        torch.cuda.synchronize(t.device)
+                        self._dev_obs = None
+                        self._released = True
                 elif getattr(self, "_host_obs", None) is not None:
                     nu = None if self._uniform_default else self.nu
                     ctx.load_obs_host(self._host_obs, _native.MCP_OBS_MAJOR, nu, self._nu_const)

@@ -353,7 +353,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
     k1t_fg_tf32<<<t.gp * t.rbs, K1T_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_a, prm);
   timing_end(ev, s);
   const int64_t red_blocks = (int64_t)t.rbs * ceil_div((int64_t)n * t.RB, K3_X);
-  k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
+  k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_T, 0, s>>>(
       (const double*)c->dYpart.p, nullptr, n, r, t.mt2 * 128, t.RB, t.rbs, t.gp, dYw);
   k_w_from_y<<<(int)ceil_div((int64_t)r * 32, 256), 256, 0, s>>>(dx + r, n, r, dYw);
   CUDA_TRY(c, cudaGetLastError());
@@ -390,8 +390,8 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   c->tail_d = pl.d;
   c->tail_r = r;
   const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) +
-                             ceil_div((int64_t)v.rbs * v.RB, K3_X);
-  k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
+                             ceil_div((int64_t)v.rbs * v.RB, K3W_X);
+  k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_T, 0, s>>>(
       (const double*)c->dYpart.p, (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
       dYw);
   CUDA_TRY(c, cudaGetLastError());
@@ -479,7 +479,7 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
                                      cudaGetErrorString(e));
   }
   const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) + 1;
-  k_reduce_finish<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_X * K3_Y, 0, s>>>(
+  k_reduce_finish<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_T, 0, s>>>(
       (const double*)c->dYpart.p, (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
       dx, (const double*)c->dM.p, (const double*)c->du.p, pl.d, alpha_dev, alpha, dout);
   CUDA_TRY(c, cudaGetLastError());

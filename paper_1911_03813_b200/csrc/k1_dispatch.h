@@ -28,6 +28,7 @@ struct K1Variant {
   int stages = 0;      // ring depth (kind 1)
   int MT = 0;          // GEMM2 m-tiles (kind 1)
   int MTW2 = 1;        // slabs per TMA copy unit (kind 1)
+  int tail_off = 0;    // K1Q: byte offset of the fused-tail scratch in dynamic smem (0: none)
   bool needs_prep() const { return kind == 0 || kind == 5; }
 };
 

@@ -257,7 +257,18 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   const size_t ring_bytes = (size_t)K1P_PAIRS * SP * slab;
   const size_t stage_need = ((size_t)K1P_PAIRS * MT * 8 * cw + (size_t)2 * K1P_PAIRS * cw) * 8;
   if (ring_bytes < stage_need) return false;
-  const size_t smem = ring_bytes + fixed + 8 * (size_t)K1P_PAIRS * (SP + 4);
+  size_t smem = ring_bytes + fixed + 8 * (size_t)K1P_PAIRS * (SP + 4);
+  // K1Q: a dedicated scratch for the fused tail's pieces lets the GEMM2 warps compute them
+  // while the GEMM1 warps already stream the first slabs
+  int tail_off = 0;
+  if (specialised && r <= 32) {
+    const size_t off = round_up((int64_t)smem, 16);
+    const size_t need = ((size_t)n * r + (size_t)r * r) * 8;
+    if (off + need <= 227 * 1024 - 1024) {
+      tail_off = (int)off;
+      smem = off + need;
+    }
+  }
   if (!attr[e].exchange(true)) {
     if (cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
@@ -269,6 +280,7 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
     cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   v.kind = specialised ? 4 : 3;
+  v.tail_off = tail_off;
   v.dtype = MCP_F64;
   v.RB = cw;
   v.MTW = table[e].MTH;
@@ -345,7 +357,7 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
   int rb_g = 16;
   while (rb_g < (int)round_up(r, 8) && rb_g < 64) rb_g *= 2;
   const bool use_g = getenv("MCP_FORCE_K1G") ? true : (rb_g >= 4 * rb_k1 || n > 2048);
-  if (!getenv("MCP_DISABLE_K1G") && use_g && n > 128 && n <= 4096) {
+  if (!getenv("MCP_DISABLE_K1G") && use_g && n > 128) {   // any n: Y lives in L2
     const int rb = rb_g;
     int e = -1;
     for (int i = 0; i < 6; ++i)
@@ -465,6 +477,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
       sp.lam = tail_lam;
       sp.M = tail_M;
       sp.u = tail_u;
+      sp.tail_off = v.kind == 4 ? v.tail_off : 0;
     }
     (v.kind == 1 ? kTableS : v.kind == 3 ? kTableP : kTableQ)[v.entry].launch(sp, v.grid, v.smem,
                                                                                s);

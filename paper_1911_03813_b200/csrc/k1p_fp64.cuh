@@ -42,15 +42,27 @@ __host__ __device__ inline size_t k1p_fixed_bytes(int kh, int ntm, int cw) {
 
 // A (n x r) and then G = A^T A, C = G^(d-1) in smem scratch (warp per entry, lanes over rows,
 // fixed butterfly -- the order of k_tail_fused), then this CTA's rows of M = (A o lam) C and,
-// in CTA 0, u = (G o C) lam.  The caller guarantees n r + r^2 <= scratch capacity.
-__device__ __forceinline__ void k1p_tail_pre(const K1SParams& prm, double* scratch) {
+// in CTA 0, u = (G o C) lam.  The caller guarantees n r + r^2 <= scratch capacity.  Runs on
+// `nthr` threads (thread index tid) that synchronise with named barrier `bar` (0: the CTA).
+__device__ __forceinline__ void k1p_tail_pre(const K1SParams& prm, double* scratch, int tid = -1,
+                                             int nthr = 0, int bar = 0) {
+  if (tid < 0) {
+    tid = threadIdx.x;
+    nthr = blockDim.x;
+  }
+  auto sync = [&]() {
+    if (bar == 0)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(nthr) : "memory");
+  };
   const int n = prm.n, r = prm.r, d = prm.d;
   const double* lam = prm.lam;
   double* sA = scratch;           // n x r column-major
   double* sC = scratch + n * r;   // G, then C
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int e = threadIdx.x; e < n * r; e += blockDim.x) sA[e] = prm.A[e];
-  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, nw = nthr >> 5;
+  for (int e = tid; e < n * r; e += nthr) sA[e] = prm.A[e];
+  sync();
   for (int pr = warp; pr < r * r; pr += nw) {
     const int j = pr / r, k = pr % r;
     double s = 0.0;
@@ -59,9 +71,9 @@ __device__ __forceinline__ void k1p_tail_pre(const K1SParams& prm, double* scrat
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (lane == 0) sC[pr] = s;
   }
-  __syncthreads();
+  sync();
   if (blockIdx.x == 0) {
-    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    for (int j = tid; j < r; j += nthr) {
       double u = 0.0;
       for (int k = 0; k < r; ++k) {
         const double gjk = sC[j * r + k];
@@ -70,12 +82,12 @@ __device__ __forceinline__ void k1p_tail_pre(const K1SParams& prm, double* scrat
       prm.u[j] = u;
     }
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) sC[e] = rm_pow(sC[e], d - 1);
-  __syncthreads();
+  sync();
+  for (int e = tid; e < r * r; e += nthr) sC[e] = rm_pow(sC[e], d - 1);
+  sync();
   const int per = (n + gridDim.x - 1) / gridDim.x;
   const int i0 = min(n, (int)blockIdx.x * per), i1 = min(n, i0 + per);
-  for (int e = threadIdx.x; e < (i1 - i0) * r; e += blockDim.x) {
+  for (int e = tid; e < (i1 - i0) * r; e += nthr) {
     const int j = e / (i1 - i0), i = i0 + e % (i1 - i0);
     double m = 0.0;
     for (int k = 0; k < r; ++k) m += (sA[k * n + i] * lam[k]) * sC[k * r + j];
@@ -116,8 +128,12 @@ __global__ void __maxnreg__(K1P_MAXREG) k1p_fg_pairs(K1SParams prm) {
   }
   // zeroed ring: GEMM1's padding k-steps read past a row's n values (the next row, or zeros)
   // and multiply them by exact zeros
-  for (size_t idx = threadIdx.x; idx < (size_t)NP * SP * slab_elems; idx += blockDim.x)
-    ring[idx] = 0.0;
+  // GEMM1's padding k-steps (4 KH > ldv) read past a row's end -- into the next row or, for a
+  // stage's last row, the next stage -- and multiply by exact zeros, so never-loaded stages
+  // must not hold NaN/Inf bit patterns: zero the ring only when such reads exist.
+  if (4 * KH > ldv)
+    for (size_t idx = threadIdx.x; idx < (size_t)NP * SP * slab_elems; idx += blockDim.x)
+      ring[idx] = 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NP * SP; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");

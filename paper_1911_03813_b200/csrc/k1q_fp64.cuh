@@ -73,8 +73,12 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     const int i = idx >> 2, c = idx & 3, j = col0 + 8 * NTM + c;
     sAt[idx] = (c < TAIL && i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
   }
-  for (size_t idx = threadIdx.x; idx < (size_t)NP * SP * slab_elems; idx += blockDim.x)
-    ring[idx] = 0.0;
+  // GEMM1's padding k-steps (4 KH > ldv) read past a row's end -- into the next row or, for a
+  // stage's last row, the next stage -- and multiply by exact zeros, so never-loaded stages
+  // must not hold NaN/Inf bit patterns: zero the ring only when such reads exist.
+  if (4 * KH > ldv)
+    for (size_t idx = threadIdx.x; idx < (size_t)NP * SP * slab_elems; idx += blockDim.x)
+      ring[idx] = 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NP * SP; ++s) mbar_init(&full[s], 1);
     for (int s = 0; s < NP * 2; ++s) {
@@ -111,7 +115,7 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     for (int a = 0; a < MCP_K1Q_L2_AHEAD; ++a)
       if (SP + a < n_mine) l2_prefetch_bulk(src0 + (SP + a) * slab_stride, slab_bytes);
   }
-  if (prm.lam) {
+  if (prm.lam && prm.tail_off == 0) {
     k1p_tail_pre(prm, sP);
     __syncthreads();
   }
@@ -270,6 +274,11 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     }
   } else {
     // ================= GEMM2 warp: Y over all m-tiles, ring refills =================
+    if (prm.lam && prm.tail_off) {
+      // the fused tail's pieces, on the six GEMM2 warps while the GEMM1 warps run slab 0
+      k1p_tail_pre(prm, reinterpret_cast<double*>(smem_raw + prm.tail_off), 32 * q + lane,
+                   32 * NP, 1);
+    }
     double yacc[MT2][NTM][2];
     double ytl[MT2][TL];
 #pragma unroll

@@ -48,6 +48,7 @@ struct K1SParams {
   const double* lam = nullptr;
   double* M = nullptr;
   double* u = nullptr;
+  int tail_off = 0;      // K1Q: dedicated smem scratch for the tail pieces (0: use P staging)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

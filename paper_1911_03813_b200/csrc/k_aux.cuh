@@ -29,112 +29,116 @@ __global__ void k_prep_afrag(const double* __restrict__ A, int n, int r, int RB,
 
 // K3: Y[i][j] = sum over the persistent CTAs' partials, in a fixed order; w likewise.
 // Output Yw = [vec_F(Y) (n*r) ; w (r)], the additive piece all-reduced across ranks.
-// Block = 32 consecutive outputs x 8 partial-groups: thread (tx, ty) sums partials
-// q = ty, ty+8, ... (coalesced 256-byte rows), then ty = 0 adds the 8 group sums in order.
-constexpr int K3_X = 32, K3_Y = 32;
-__global__ void __launch_bounds__(K3_X * K3_Y)
+// Y blocks: K3_X consecutive outputs x K3_Y partial lanes; lane ty sums partials q = ty,
+// ty + K3_Y, ... in order, then a fixed binary tree over the lanes (one or two loads per thread at
+// gp = 148: the reduce is latency-, not bandwidth-bound).  The w block uses 32 columns x 32
+// lanes the same way.  K3 and K3F share both orders, so partial + finish == fused, bitwise.
+constexpr int K3_X = 8, K3_Y = 128, K3_T = K3_X * K3_Y;
+constexpr int K3W_X = 32, K3W_Y = K3_T / K3W_X;
+
+template <int X, int Y>
+__device__ __forceinline__ double k3_tree(double s, double* sm, int tx, int ty) {
+  sm[ty * X + tx] = s;
+  __syncthreads();
+#pragma unroll
+  for (int stride = Y / 2; stride > 0; stride >>= 1) {
+    if (ty < stride) sm[ty * X + tx] += sm[(ty + stride) * X + tx];
+    __syncthreads();
+  }
+  const double t = sm[tx];
+  __syncthreads();
+  return t;
+}
+
+// Y entry e = i * RB + jl of column block rb (valid when e < n * RB)
+__device__ __forceinline__ double k3_y_lane(const double* __restrict__ Ypart, int n_pad, int RB,
+                                            int gp, int rb, int e, int ty) {
+  const int i = e / RB, jl = e % RB;
+  const double* src = Ypart + ((size_t)rb * gp * n_pad + i) * RB + jl;
+  double s = 0.0;
+  for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * n_pad * RB];
+  return s;
+}
+__device__ __forceinline__ double k3_w_lane(const double* __restrict__ wpart, int RB, int gp,
+                                            int k, int ty) {
+  const int rb = k / RB, jl = k % RB;
+  const double* src = wpart + (size_t)rb * gp * RB + jl;
+  double s = 0.0;
+  for (int q = ty; q < gp; q += K3W_Y) s += src[(size_t)q * RB];
+  return s;
+}
+
+__global__ void __launch_bounds__(K3_T)
     k_reduce_partials(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
                       int r, int n_pad, int RB, int rbs, int gp, double* __restrict__ Yw) {
-  __shared__ double s_acc[K3_Y][K3_X];
-  const int tx = threadIdx.x % K3_X, ty = threadIdx.x / K3_X;
-  const int per_rb = n * RB;                          // Y outputs of one column block
-  const int yblocks = (per_rb + K3_X - 1) / K3_X;     // blocks per column block
-  const int64_t total_blocks =
-      (int64_t)rbs * yblocks + (wpart ? (rbs * RB + K3_X - 1) / K3_X : 0);
+  __shared__ double sm[K3_T];
+  const int per_rb = n * RB;
+  const int yblocks = (per_rb + K3_X - 1) / K3_X;
+  const int wblocks = wpart ? (rbs * RB + K3W_X - 1) / K3W_X : 0;
+  const int64_t total_blocks = (int64_t)rbs * yblocks + wblocks;
   for (int64_t blk = blockIdx.x; blk < total_blocks; blk += gridDim.x) {
-    double s = 0.0;
-    int64_t dst = -1;
     if (blk < (int64_t)rbs * yblocks) {
+      const int tx = threadIdx.x % K3_X, ty = threadIdx.x / K3_X;
       const int rb = blk / yblocks;
-      const int e = (blk % yblocks) * K3_X + tx;       // e = i * RB + jl
-      if (e < per_rb) {
-        const int i = e / RB, jl = e % RB, j = rb * RB + jl;
-        const double* src = Ypart + ((size_t)rb * gp * n_pad + i) * RB + jl;
-#pragma unroll 4
-        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * n_pad * RB];
-        if (j < r) dst = (int64_t)j * n + i;
+      const int e = (blk % yblocks) * K3_X + tx;
+      const double s = e < per_rb ? k3_y_lane(Ypart, n_pad, RB, gp, rb, e, ty) : 0.0;
+      const double t = k3_tree<K3_X, K3_Y>(s, sm, tx, ty);
+      if (ty == 0 && e < per_rb) {
+        const int i = e / RB, j = rb * RB + e % RB;
+        if (j < r) Yw[(int64_t)j * n + i] = t;
       }
     } else {
-      const int k = (blk - (int64_t)rbs * yblocks) * K3_X + tx;   // k = rb * RB + jl
-      if (k < rbs * RB) {
-        const int rb = k / RB, jl = k % RB, j = rb * RB + jl;
-        const double* src = wpart + (size_t)rb * gp * RB + jl;
-#pragma unroll 4
-        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * RB];
-        if (j < r) dst = (int64_t)n * r + j;
+      const int tx = threadIdx.x % K3W_X, ty = threadIdx.x / K3W_X;
+      const int k = (int)(blk - (int64_t)rbs * yblocks) * K3W_X + tx;   // k = rb * RB + jl
+      const double s = k < rbs * RB ? k3_w_lane(wpart, RB, gp, k, ty) : 0.0;
+      const double t = k3_tree<K3W_X, K3W_Y>(s, sm, tx, ty);
+      if (ty == 0 && k < rbs * RB) {
+        const int j = (k / RB) * RB + k % RB;
+        if (j < r) Yw[(int64_t)n * r + j] = t;
       }
     }
-    s_acc[ty][tx] = s;
-    __syncthreads();
-    if (ty == 0 && dst >= 0) {
-      double t = 0.0;
-#pragma unroll
-      for (int y = 0; y < K3_Y; ++y) t += s_acc[y][tx];
-      Yw[dst] = t;
-    }
-    __syncthreads();
   }
 }
 
 // K3F: the fixed-order partial reduce of K3 fused with the finish (objective.py:51-56) when
-// K1P already produced M = (A o lam) C and u = (G o C) lam: g_A = -2d (Y - M) o lam is
+// K1P/K1Q already produced M = (A o lam) C and u = (G o C) lam: g_A = -2d (Y - M) o lam is
 // elementwise on the reduced Y, g_lam = -2 (w - u), and f = alpha + lam.u - 2 w.lam (r <= 32:
-// one block holds every w).  out = [f ; g_lam ; vec_F(g_A)], bitwise the k_tail_fused result.
-__global__ void __launch_bounds__(K3_X * K3_Y)
+// one w block holds every w).  out = [f ; g_lam ; vec_F(g_A)], bitwise the K3 + K4L result.
+__global__ void __launch_bounds__(K3_T)
     k_reduce_finish(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
                     int r, int n_pad, int RB, int rbs, int gp, const double* __restrict__ x,
                     const double* __restrict__ M, const double* __restrict__ u, int d,
                     const double* __restrict__ alpha_dev, double alpha_host,
                     double* __restrict__ out) {
-  __shared__ double s_acc[K3_Y][K3_X];
-  __shared__ double s_w[K3_X];
-  const int tx = threadIdx.x % K3_X, ty = threadIdx.x / K3_X;
+  __shared__ double sm[K3_T];
+  __shared__ double s_w[K3W_X];
   const double* lam = x;
   const int per_rb = n * RB;
   const int yblocks = (per_rb + K3_X - 1) / K3_X;
   const int64_t total_blocks = (int64_t)rbs * yblocks + 1;   // + the w / f block
   const double s2d = -2.0 * d;
   for (int64_t blk = blockIdx.x; blk < total_blocks; blk += gridDim.x) {
-    double s = 0.0;
     if (blk < (int64_t)rbs * yblocks) {
+      const int tx = threadIdx.x % K3_X, ty = threadIdx.x / K3_X;
       const int rb = blk / yblocks;
       const int e = (blk % yblocks) * K3_X + tx;
-      int64_t dst = -1;
-      int j = 0;
-      if (e < per_rb) {
-        const int i = e / RB, jl = e % RB;
-        j = rb * RB + jl;
-        const double* src = Ypart + ((size_t)rb * gp * n_pad + i) * RB + jl;
-#pragma unroll 4
-        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * n_pad * RB];
-        if (j < r) dst = (int64_t)j * n + i;
+      const double s = e < per_rb ? k3_y_lane(Ypart, n_pad, RB, gp, rb, e, ty) : 0.0;
+      const double t = k3_tree<K3_X, K3_Y>(s, sm, tx, ty);
+      if (ty == 0 && e < per_rb) {
+        const int i = e / RB, j = rb * RB + e % RB;
+        if (j < r) {
+          const int64_t dst = (int64_t)j * n + i;
+          out[1 + r + dst] = (s2d * (t - M[dst])) * lam[j];
+        }
       }
-      s_acc[ty][tx] = s;
-      __syncthreads();
-      if (ty == 0 && dst >= 0) {
-        double t = 0.0;
-#pragma unroll
-        for (int y = 0; y < K3_Y; ++y) t += s_acc[y][tx];
-        out[1 + r + dst] = (s2d * (t - M[dst])) * lam[j];
-      }
-      __syncthreads();
     } else {
-      // w (r <= 32 < K3_X): reduce, then g_lam and f
-      const int k = tx;   // k = rb * RB + jl
-      int j = r;
-      if (k < rbs * RB) {
-        const int rb = k / RB, jl = k % RB;
-        j = rb * RB + jl;
-        const double* src = wpart + (size_t)rb * gp * RB + jl;
-#pragma unroll 4
-        for (int q = ty; q < gp; q += K3_Y) s += src[(size_t)q * RB];
-      }
-      s_acc[ty][tx] = s;
-      __syncthreads();
-      if (ty == 0) {
-        double t = 0.0;
-#pragma unroll
-        for (int y = 0; y < K3_Y; ++y) t += s_acc[y][tx];
+      // w (rbs * RB <= 32 columns): reduce, then g_lam and f
+      const int tx = threadIdx.x % K3W_X, ty = threadIdx.x / K3W_X;
+      const int k = tx;
+      const double s = k < rbs * RB ? k3_w_lane(wpart, RB, gp, k, ty) : 0.0;
+      const double t = k3_tree<K3W_X, K3W_Y>(s, sm, tx, ty);
+      if (ty == 0 && k < rbs * RB) {
+        const int j = (k / RB) * RB + k % RB;
         if (j < r) {
           s_w[j] = t;
           out[1 + j] = -2.0 * (t - u[j]);

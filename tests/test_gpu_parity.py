@@ -423,3 +423,18 @@ def test_peer_exchange_kernels_two_virtual_ranks():
     assert _err(h[0], full.f, f_s) <= 1e-13
     assert _err(h[1:1 + r], full.g_lam, gl_s) <= 1e-13
     assert _err(h[1 + r:].reshape((n, r), order="F"), full.g_A, gA_s) <= 1e-13
+
+
+def test_large_n_beyond_register_tiled_kernels():
+    """n = 2500 > the register-tiled K1 limit (2048): K1G keeps Y in L2 and handles any n."""
+    rng = np.random.default_rng(44)
+    n, p, r, d = 2500, 700, 6, 3
+    V = rng.standard_normal((n, p)) / np.sqrt(n)
+    lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)
+    res = mcp.fg_implicit(mcp.ObservationSet(V), lam, A, d, 0.3)
+    nu = np.full(p, 1.0 / p)
+    f, gl, gA = om.fg_implicit(V, nu, lam, A, d, 0.3)
+    f_s, gl_s, gA_s, _ = om.term_scales(V, nu, lam, A, d, 0.3)
+    assert _err(res.f, f, f_s) <= FG_TOL
+    assert _err(res.g_lam, gl, gl_s) <= FG_TOL
+    assert _err(res.g_A, gA, gA_s) <= FG_TOL

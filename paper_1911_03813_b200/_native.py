@@ -223,12 +223,15 @@ class Context:
 
     # -- evaluations (host buffers) --------------------------------------------------------
     def fg_packed(self, x: np.ndarray, n: int, d: int, r: int, alpha: float, mode: str | None):
+        # hot path of every solver step: raw addresses (ints) instead of ctypes pointer objects;
+        # the library checks finiteness while staging x
         x = np.ascontiguousarray(x, dtype=np.float64)
         g = np.empty(r + n * r, dtype=np.float64)
         f = ctypes.c_double()
-        rc = self._lib.mcp_fg_packed(self._h, int(d), int(r), _ptr(x), float(alpha),
-                                     mode_code(mode), ctypes.byref(f), _ptr(g))
-        self._check(rc, "mcp_fg_packed")
+        rc = self._lib.mcp_fg_packed(self._h, d, r, x.ctypes.data, alpha, mode_code(mode),
+                                     ctypes.byref(f), g.ctypes.data)
+        if rc:
+            self._check(rc, "mcp_fg_packed")
         return f.value, g
 
     def fg(self, lam: np.ndarray, A_fortran: np.ndarray, d: int, alpha: float, mode: str | None):

@@ -60,6 +60,12 @@ __global__ void k_count_nonfinite(const T* __restrict__ V, int64_t total, unsign
   if (local) atomicAdd(bad, local);
 }
 
+__global__ void k_copy_f64(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 __global__ void k_check_nu(const double* __restrict__ nu, int64_t p, unsigned long long* bad) {
   unsigned long long local = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p;
@@ -500,8 +506,17 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
   if ((rc = ensure_host(c, c->hx, c->hx_bytes, xin))) return rc;
   if ((rc = ensure_host(c, c->hout, c->hout_bytes, xout))) return rc;
   double* hx = (double*)c->hx;
-  std::memcpy(hx, lam, sizeof(double) * r);
-  std::memcpy(hx + r, A, sizeof(double) * n * r);
+  // copy into the pinned staging, checking finiteness on the way (objective.py:45-47)
+  bool finite = true;
+  for (int j = 0; j < r; ++j) {
+    hx[j] = lam[j];
+    finite &= std::isfinite(lam[j]);
+  }
+  for (int64_t e = 0; e < n * r; ++e) {
+    hx[r + e] = A[e];
+    finite &= std::isfinite(A[e]);
+  }
+  if (!finite) return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
   hx[r + n * r] = alpha;
 
   auto key = std::make_tuple(d, r, mode);
@@ -510,9 +525,19 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     GraphEntry ge;
     CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     double* dx = (double*)c->dx.p;
-    cudaMemcpyAsync(dx, hx, xin, cudaMemcpyHostToDevice, c->stream);
-    int rc2 = enqueue_fg_full(c, pl, dx, dx + r + n * r, 0.0, (double*)c->dout.p, c->stream);
-    cudaMemcpyAsync(c->hout, c->dout.p, xout, cudaMemcpyDeviceToHost, c->stream);
+    int rc2;
+    if (getenv("MCP_HOST_MEMCPY")) {
+      cudaMemcpyAsync(dx, hx, xin, cudaMemcpyHostToDevice, c->stream);
+      rc2 = enqueue_fg_full(c, pl, dx, dx + r + n * r, 0.0, (double*)c->dout.p, c->stream);
+      cudaMemcpyAsync(c->hout, c->dout.p, xout, cudaMemcpyDeviceToHost, c->stream);
+    } else {
+      // zero-copy staging (pinned memory is device-mapped under UVA): one small kernel pulls x
+      // over PCIe and the finishing kernel stores [f ; g] straight into host memory -- no copy
+      // engine round trips in the per-evaluation latency
+      const int64_t nx = r + n * r + 1;
+      k_copy_f64<<<grid_for(nx, 256, 8), 256, 0, c->stream>>>(hx, dx, nx);
+      rc2 = enqueue_fg_full(c, pl, dx, dx + r + n * r, 0.0, (double*)c->hout, c->stream);
+    }
     cudaError_t ce = cudaStreamEndCapture(c->stream, &ge.graph);
     if (rc2) {
       if (ge.graph) cudaGraphDestroy(ge.graph);

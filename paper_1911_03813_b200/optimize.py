@@ -103,13 +103,15 @@ def packed_fg_implicit(obs: ObservationSet, d: int, r: int, alpha: float = 0.0, 
         raise ValueError(f"order must be >= 2, got {d}")
     ctx = obs.device_context()
 
+    d, r, alpha = int(d), int(r), float(alpha)
+    if not np.isfinite(alpha):
+        raise ValueError("model variables and alpha must be finite")
+
     def fg(x: np.ndarray) -> tuple[float, np.ndarray]:
         x = np.asarray(x, dtype=float)
         if x.shape != (r + n * r,):
             raise ValueError(f"expected packed length {r + n * r}, got {x.shape}")
-        if not np.isfinite(x).all():
-            raise ValueError("model variables and alpha must be finite")
-        return ctx.fg_packed(x, n, d, r, alpha, mode)
+        return ctx.fg_packed(x, n, d, r, alpha, mode)   # finiteness checked in the library
 
     fg.device_problem = (obs, int(d), int(r), float(alpha), mode)  # read by lbfgs_minimize
     return fg

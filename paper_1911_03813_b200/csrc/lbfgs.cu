@@ -73,6 +73,7 @@ struct LbDev {
   unsigned* counter;
   const int* act;
   double* Xb;   // batched K1 layout [lam_all (k r) ; A_all (n x k r)] or nullptr (k == 1)
+  double* st_host;   // mapped pinned copy of the stats records (written by the probe kernel)
   int r;
   int64_t n;
   __device__ int action(int s) const { return act[s] & 7; }
@@ -470,6 +471,18 @@ __global__ void k_lbb_probe_stats(LbDev D) {
   st[S_FA] = D.ot(s)[0];
   st[S_DA] = dp;
   st[S_XBAD] = bad;
+  // the whole record of this run, straight into mapped host memory (no D2H copy node)
+  double* h = D.st_host + (int64_t)s * S_COUNT;
+  for (int i = 0; i < S_COUNT; ++i) h[i] = st[i];
+}
+
+// actions and host-chosen steps of the round, pulled from mapped host memory by one tiny kernel
+__global__ void k_lbb_pull(const int* __restrict__ h_act, const double* __restrict__ h_a,
+                           int* __restrict__ d_act, double* __restrict__ d_a, int k) {
+  for (int s = threadIdx.x; s < k; s += blockDim.x) {
+    d_act[s] = h_act[s];
+    d_a[s] = h_a[s];
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -638,8 +651,6 @@ struct LbEngine {
     int rc = enqueue_fg();
     if (rc) return rc;
     k_lbb_probe_stats<<<dim3(nb, k), LB_T, 0, s>>>(D);
-    CUDA_TRY(c, cudaMemcpyAsync(h_st, D.st, sizeof(double) * S_COUNT * k, cudaMemcpyDeviceToHost,
-                                s));
     CUDA_TRY(c, cudaGetLastError());
     return MCP_OK;
   }
@@ -700,6 +711,7 @@ struct LbEngine {
     CUDA_TRY(c, cudaMallocHost(&h_a, sizeof(double) * K));
     CUDA_TRY(c, cudaMallocHost(&h_st, sizeof(double) * K * S_COUNT));
     CUDA_TRY(c, cudaMallocHost(&h_x, sizeof(double) * K * N));
+    D.st_host = h_st;   // pinned memory is device-mapped under UVA
     cudaStream_t s = c->stream;
     // init: evaluate x0 (trial = x), statistics, direction, first probe
     if ((rc = capture(g_init, [&]() -> int {
@@ -713,8 +725,7 @@ struct LbEngine {
          })))
       return rc;
     if ((rc = capture(g_round, [&]() -> int {
-           CUDA_TRY(c, cudaMemcpyAsync(d_act, h_act, sizeof(int) * K, cudaMemcpyHostToDevice, s));
-           CUDA_TRY(c, cudaMemcpyAsync(D.ah, h_a, sizeof(double) * K, cudaMemcpyHostToDevice, s));
+           k_lbb_pull<<<1, 32, 0, s>>>(h_act, h_a, d_act, D.ah, k);
            k_lbb_save<<<dim3(nb, k), LB_T, 0, s>>>(D);
            k_lbb_accept<<<dim3(nb, k), LB_T, 0, s>>>(D);
            return enqueue_round_tail();

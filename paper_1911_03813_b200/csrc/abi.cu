@@ -241,6 +241,8 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     const int rbs_w = (int)ceil_div(r, RB);
     while (RB > 16 && ceil_div(r, RB - 16) == rbs_w && (RB - 16) >= r / rbs_w) RB -= 16;
   }
+  // K1T2 with the concatenated GEMM1 when TMEM has room for two 2 RB-wide Z buffers
+  t.zcat = !v1 && !getenv("MCP_K1T_NO_ZCAT") && 2 * RB <= 256 && (4 + t.mt2) * RB <= 512;
   if ((zbufs + t.mt2) * RB > 512)
     return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
   t.RB = RB;
@@ -351,6 +353,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.nu = c->dnu;
   prm.nu_const = c->nu_const;
   prm.Ypart = (double*)c->dYpart.p;
+  prm.zcat = t.zcat ? 1 : 0;
   auto* ev = timing_begin(c, s);
   if (t.v2)
     k1t2_fg_tf32<<<t.gp * t.rbs, K1T2_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_l1, c->tm_l2,

@@ -101,6 +101,7 @@ namespace mcp_internal {
 struct K1TPlan {
   int RB = 0, rbs = 0, gp = 0, stages = 0, nkb = 0, mt2 = 0, r_pad = 0, kpad = 0;
   bool v2 = false;   // K1T2 (precomputed V_lo) instead of K1T (in-kernel split)
+  bool zcat = false; // K1T2 concatenated GEMM1 (Z in two TMEM halves)
   int64_t num_tiles = 0;
   size_t smem = 0;
 };

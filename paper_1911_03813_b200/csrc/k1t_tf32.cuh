@@ -49,6 +49,8 @@ struct K1TParams {
   const double* nu;
   double nu_const;
   double* Ypart;      // [rbs][gp][mt2*128][RB] fp64
+  int zcat = 0;       // K1T2: GEMM1 as V_hi x [A_hi ; A_lo] (N = 2 RB) + V_lo x A_hi: Z takes
+                      // 2 RB TMEM columns per buffer and the epilogue adds its two halves
 };
 
 __host__ __device__ constexpr size_t k1t_stage_bytes(int RB) { return 2 * K1T_VBYTES + 256 * RB; }
@@ -420,7 +422,8 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t ty = tmem + 2 * RB;   // Y[mt] at columns (2 + mt) RB; Z[b] at b RB
+  const int ZW = prm.zcat ? 2 * RB : RB;          // TMEM columns of one Z buffer
+  const uint32_t ty = tmem + 2 * ZW;               // Y[mt] at 2 ZW + mt RB; Z[b] at b ZW
 
   if (warp == 0) {
     // =========================== TMA producer (same order as the MMA issuer) ===========================
@@ -467,6 +470,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
     // =========================== MMA issuer ===========================
     if (lane == 0) {
       const uint32_t id1 = umma_idesc_tf32(128, RB, false, false);
+      const uint32_t id1c = umma_idesc_tf32(128, 2 * RB, false, false);
       const uint32_t id2 = umma_idesc_tf32(128, RB, true, false);
       int64_t q = 0;
       int flushes = 0;
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       for (int64_t u = 0; u <= my_tiles; ++u) {
         if (u < my_tiles) {
           // ---- GEMM1(u): Z[u & 1] = V A (3xTF32) ----
-          const uint32_t tz = tmem + (uint32_t)((u & 1) * RB);
+          const uint32_t tz = tmem + (uint32_t)((u & 1) * ZW);
           for (int kb = 0; kb < nkb; ++kb, ++q) {
             const int s = (int)(q % NS);
             {
@@ -492,12 +496,23 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             const uint64_t dvl = dvh + (K1T_VBYTES >> 4);
             const uint64_t dah = dvh + ((2 * K1T_VBYTES) >> 4);
             const uint64_t dal = dah + ((128 * RB) >> 4);
-#pragma unroll
-            for (int pr = 0; pr < 3; ++pr) {
-              const uint64_t av = pr == 2 ? dvl : dvh, bv = pr == 1 ? dal : dah;
+            if (prm.zcat) {
+              // A_hi and A_lo rows are adjacent in the stage: one N = 2 RB product gives
+              // [V_hi A_hi | V_hi A_lo]; V_lo A_hi accumulates into the second half
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks)
-                umma_tf32(tz, av + 2 * ks, bv + 2 * ks, id1, (kb | pr | ks) != 0 ? 1u : 0u);
+                umma_tf32(tz, dvh + 2 * ks, dah + 2 * ks, id1c, (kb | ks) != 0 ? 1u : 0u);
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                umma_tf32(tz + RB, dvl + 2 * ks, dah + 2 * ks, id1, 1u);
+            } else {
+#pragma unroll
+              for (int pr = 0; pr < 3; ++pr) {
+                const uint64_t av = pr == 2 ? dvl : dvh, bv = pr == 1 ? dal : dah;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                  umma_tf32(tz, av + 2 * ks, bv + 2 * ks, id1, (kb | pr | ks) != 0 ? 1u : 0u);
+              }
             }
             umma_commit(smem_u32(&empty[s]));
           }
@@ -614,12 +629,18 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       tc_fence_after();
       {
         K1T2_T0();
-        const uint32_t tz = tmem + (uint32_t)((u & 1) * RB);
+        const uint32_t tz = tmem + (uint32_t)((u & 1) * ZW);
         const double nul = prm.nu ? prm.nu[row0 + l] : prm.nu_const;
         const int brick = l >> 5, col = l & 31;
         for (int c0 = half * hc; col_active && c0 < c_end; c0 += 16) {
           float zv[16];
           tmem_ld16(tz + ((uint32_t)(32 * sp) << 16) + c0, zv);
+          if (prm.zcat) {
+            float z2[16];
+            tmem_ld16(tz + RB + ((uint32_t)(32 * sp) << 16) + c0, z2);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) zv[jj] += z2[jj];
+          }
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
             const double z = (double)zv[jj];

@@ -488,9 +488,21 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
                                      cudaGetErrorString(e));
   }
   const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) + 1;
-  k_reduce_finish<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_T, 0, s>>>(
-      (const double*)c->dYpart.p, (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
-      dx, (const double*)c->dM.p, (const double*)c->du.p, pl.d, alpha_dev, alpha, dout);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(red_blocks, 16 * c->sms));
+    cfg.blockDim = dim3(K3_T);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_reduce_finish, (const double*)c->dYpart.p,
+                                   (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
+                                   dx, (const double*)c->dM.p, (const double*)c->du.p, pl.d,
+                                   alpha_dev, alpha, dout));
+  }
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches = 2;
   c->variant = v.name;

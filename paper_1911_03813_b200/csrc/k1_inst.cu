@@ -127,7 +127,18 @@ std::atomic<bool> g_attr_p[kEntriesS];
 // ---------------- K1Q (warp-specialised pairs, fp64, n <= 128) ----------------
 template <int NTM, int TAIL, int MT2, int KH>
 void launch_q(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
-  k1q_fg_pairs<NTM, TAIL, MT2, KH><<<grid, K1Q_THREADS, smem, s>>>(prm);
+  // programmatic dependent launch: the V-only prologue overlaps the previous kernel
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(K1Q_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k1q_fg_pairs<NTM, TAIL, MT2, KH>, prm);
 }
 #define MCP_K1Q_E(NTM, TAIL, MT2, KH) \
   {NTM, TAIL, MT2, KH, &launch_q<NTM, TAIL, MT2, KH>, \

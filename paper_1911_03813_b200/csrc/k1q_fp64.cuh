@@ -64,15 +64,6 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
   const int pg = blockIdx.x / prm.rbs;
   const int col0 = rb * CW;
 
-  for (int idx = threadIdx.x; idx < KH * NTM * 32; idx += blockDim.x) {
-    const int ln = idx & 31, nt = (idx >> 5) % NTM, ks = (idx >> 5) / NTM;
-    const int i = 4 * ks + (ln & 3), j = col0 + 8 * nt + (ln >> 2);
-    sAf[idx] = (i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
-  }
-  for (int idx = threadIdx.x; idx < KH * 16; idx += blockDim.x) {
-    const int i = idx >> 2, c = idx & 3, j = col0 + 8 * NTM + c;
-    sAt[idx] = (c < TAIL && i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
-  }
   // GEMM1's padding k-steps (4 KH > ldv) read past a row's end -- into the next row or, for a
   // stage's last row, the next stage -- and multiply by exact zeros, so never-loaded stages
   // must not hold NaN/Inf bit patterns: zero the ring only when such reads exist.
@@ -115,6 +106,20 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     for (int a = 0; a < MCP_K1Q_L2_AHEAD; ++a)
       if (SP + a < n_mine) l2_prefetch_bulk(src0 + (SP + a) * slab_stride, slab_bytes);
   }
+  // Programmatic dependent launch: everything above depends only on V, so under PDL it overlaps
+  // the previous kernel's tail; x (A, lam) may be produced by that kernel and our partials / M /
+  // u are read by it -- wait for its completion here (a no-op without PDL).
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  for (int idx = threadIdx.x; idx < KH * NTM * 32; idx += blockDim.x) {
+    const int ln = idx & 31, nt = (idx >> 5) % NTM, ks = (idx >> 5) / NTM;
+    const int i = 4 * ks + (ln & 3), j = col0 + 8 * nt + (ln >> 2);
+    sAf[idx] = (i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < KH * 16; idx += blockDim.x) {
+    const int i = idx >> 2, c = idx & 3, j = col0 + 8 * NTM + c;
+    sAt[idx] = (c < TAIL && i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
+  }
+  __syncthreads();
   if (prm.lam && prm.tail_off == 0) {
     k1p_tail_pre(prm, sP);
     __syncthreads();
@@ -262,6 +267,7 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     wtl += __shfl_xor_sync(0xffffffffu, wtl, 4);
     wtl += __shfl_xor_sync(0xffffffffu, wtl, 8);
     wtl += __shfl_xor_sync(0xffffffffu, wtl, 16);
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     __syncthreads();   // (A) all slabs consumed by both warps of every pair
     double* wst = ring + (size_t)NP * MT * 8 * CW + q * CW;
     if (g == 0) {
@@ -336,6 +342,7 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
         ytl[m][c] += __shfl_xor_sync(0xffffffffu, ytl[m][c], 1);
         ytl[m][c] += __shfl_xor_sync(0xffffffffu, ytl[m][c], 2);
       }
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     __syncthreads();   // (A)
     double* stage = ring + (size_t)q * MT * 8 * CW;
 #pragma unroll

@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(K3_T)
                     const double* __restrict__ M, const double* __restrict__ u, int d,
                     const double* __restrict__ alpha_dev, double alpha_host,
                     double* __restrict__ out) {
+  // PDL: launched while K1Q drains; its partials are complete only after this wait.  The next
+  // kernel may start its V-only prologue right away.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ double sm[K3_T];
   __shared__ double s_w[K3W_X];
   const double* lam = x;

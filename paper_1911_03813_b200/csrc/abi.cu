@@ -478,9 +478,9 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
   const K1Variant& v = pl.k1;
   const int n = (int)c->n;
   auto* ev = timing_begin(c, s);
+  // the tail pieces (G, C, M, u) are formed by K3F itself, overlapping K1's drain
   int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r, nullptr, pl.d,
-                     (double*)c->dYpart.p, (double*)c->dwpart.p, s, dx, (double*)c->dM.p,
-                     (double*)c->du.p);
+                     (double*)c->dYpart.p, (double*)c->dwpart.p, s, nullptr, nullptr, nullptr);
   timing_end(ev, s);
   if (rc) {
     const cudaError_t e = cudaGetLastError();
@@ -500,7 +500,7 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
     cfg.numAttrs = 1;
     CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_reduce_finish, (const double*)c->dYpart.p,
                                    (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
-                                   dx, (const double*)c->dM.p, (const double*)c->du.p, pl.d,
+                                   dx, pl.d,
                                    alpha_dev, alpha, dout));
   }
   CUDA_TRY(c, cudaGetLastError());

@@ -24,6 +24,9 @@ constexpr int K1Q_MAXREG = 168;
 #ifndef MCP_K1Q_ODD_CHAINS
 #define MCP_K1Q_ODD_CHAINS 0   // 1: GEMM1 with separate even / odd k-step chains (no gain)
 #endif
+#ifndef MCP_K1Q_PROF
+#define MCP_K1Q_PROF 0         // diagnostics only: CTAs 0 and gridDim-1 print phase clocks
+#endif
 #ifndef MCP_K1Q_L2_AHEAD
 #define MCP_K1Q_L2_AHEAD 1     // slabs beyond the ring prefetched into L2 (0: off)
 #endif
@@ -63,6 +66,12 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
   const int rb = blockIdx.x % prm.rbs;
   const int pg = blockIdx.x / prm.rbs;
   const int col0 = rb * CW;
+#if MCP_K1Q_PROF
+  const long long pt0 = clock64();
+  long long pt_wait = 0, pt_pro = 0, pt_first = 0, pt_loop = 0, pt_sync = 0, w_full = 0, w_p = 0;
+  const bool prof = (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && lane == 0 &&
+                    (warp == 0 || warp == 1);
+#endif
 
   // GEMM1's padding k-steps (4 KH > ldv) read past a row's end -- into the next row or, for a
   // stage's last row, the next stage -- and multiply by exact zeros, so never-loaded stages
@@ -110,14 +119,38 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
   // the previous kernel's tail; x (A, lam) may be produced by that kernel and our partials / M /
   // u are read by it -- wait for its completion here (a no-op without PDL).
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  for (int idx = threadIdx.x; idx < KH * NTM * 32; idx += blockDim.x) {
-    const int ln = idx & 31, nt = (idx >> 5) % NTM, ks = (idx >> 5) / NTM;
-    const int i = 4 * ks + (ln & 3), j = col0 + 8 * nt + (ln >> 2);
-    sAf[idx] = (i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
-  }
-  for (int idx = threadIdx.x; idx < KH * 16; idx += blockDim.x) {
-    const int i = idx >> 2, c = idx & 3, j = col0 + 8 * NTM + c;
-    sAt[idx] = (c < TAIL && i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
+#if MCP_K1Q_PROF
+  pt_wait = clock64() - pt0;
+#endif
+  {
+    // factor fragments: every global load of the thread is issued before the first store (one
+    // L2 round trip on the critical path instead of one per loop trip)
+    constexpr int NAF = KH * NTM * 32, NAT = KH * 16;
+    constexpr int PER = (NAF + NAT + K1Q_THREADS - 1) / K1Q_THREADS;
+    double av[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * K1Q_THREADS;
+      int i = 0, j = prm.r;
+      if (idx < NAF) {
+        const int ln = idx & 31, nt = (idx >> 5) % NTM, ks = (idx >> 5) / NTM;
+        i = 4 * ks + (ln & 3);
+        j = col0 + 8 * nt + (ln >> 2);
+      } else if (idx < NAF + NAT) {
+        const int it = idx - NAF, c = it & 3;
+        i = it >> 2;
+        j = c < TAIL ? col0 + 8 * NTM + c : prm.r;
+      }
+      av[u] = (i < prm.n && j < prm.r) ? prm.A[(int64_t)j * prm.n + i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * K1Q_THREADS;
+      if (idx < NAF)
+        sAf[idx] = av[u];
+      else if (idx < NAF + NAT)
+        sAt[idx - NAF] = av[u];
+    }
   }
   __syncthreads();
   if (prm.lam && prm.tail_off == 0) {
@@ -126,6 +159,9 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
   }
   const int dm1 = prm.d - 1;
   const int MT = prm.MT;
+#if MCP_K1Q_PROF
+  pt_pro = clock64() - pt0;
+#endif
 
   if (h == 0) {
     // ================= GEMM1 warp: Z for 16 rows, epilogue, P hand-off =================
@@ -136,7 +172,14 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     int s = 0;
     uint32_t ph = 0;
     for (int64_t i = 0; i < n_mine; ++i) {
+#if MCP_K1Q_PROF
+      const long long tw = clock64();
+#endif
       mbar_wait(&my_full[s], ph);
+#if MCP_K1Q_PROF
+      w_full += clock64() - tw;
+      if (i == 0) pt_first = clock64() - pt0;
+#endif
       const double* sv = my_ring + (size_t)s * slab_elems;
       if (++s == SP) {
         s = 0;
@@ -268,7 +311,13 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     wtl += __shfl_xor_sync(0xffffffffu, wtl, 8);
     wtl += __shfl_xor_sync(0xffffffffu, wtl, 16);
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#if MCP_K1Q_PROF
+    pt_loop = clock64() - pt0;
+#endif
     __syncthreads();   // (A) all slabs consumed by both warps of every pair
+#if MCP_K1Q_PROF
+    pt_sync = clock64() - pt0;
+#endif
     double* wst = ring + (size_t)NP * MT * 8 * CW + q * CW;
     if (g == 0) {
 #pragma unroll
@@ -299,7 +348,14 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     for (int64_t i = 0; i < n_mine; ++i) {
       const int b = (int)(i & 1);
       mbar_wait(&my_full[s], ph);     // (already complete: the GEMM1 warp waited on it)
+#if MCP_K1Q_PROF
+      const long long tw = clock64();
+#endif
       mbar_wait(&my_pfull[b], (uint32_t)((i >> 1) & 1));
+#if MCP_K1Q_PROF
+      w_p += clock64() - tw;
+      if (i == 0) pt_first = clock64() - pt0;
+#endif
       const double* sv = my_ring + (size_t)s * slab_elems;
       const double* Pb = my_P + (size_t)b * K1S_SR * PP;
 #pragma unroll
@@ -343,7 +399,13 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
         ytl[m][c] += __shfl_xor_sync(0xffffffffu, ytl[m][c], 2);
       }
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#if MCP_K1Q_PROF
+    pt_loop = clock64() - pt0;
+#endif
     __syncthreads();   // (A)
+#if MCP_K1Q_PROF
+    pt_sync = clock64() - pt0;
+#endif
     double* stage = ring + (size_t)q * MT * 8 * CW;
 #pragma unroll
     for (int m = 0; m < MT2; ++m) {
@@ -361,6 +423,9 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     }
   }
   __syncthreads();
+#if MCP_K1Q_PROF
+  const long long pt_staged = clock64() - pt0;
+#endif
   const int per_cta = MT * 8 * CW;
   double* Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * per_cta;
   for (int e = threadIdx.x; e < per_cta; e += blockDim.x) {
@@ -375,6 +440,13 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     for (int w = 0; w < NP; ++w) acc += ring[(size_t)NP * per_cta + w * CW + threadIdx.x];
     prm.wpart[((size_t)rb * prm.gp + pg) * CW + threadIdx.x] = acc;
   }
+#if MCP_K1Q_PROF
+  if (prof)
+    printf("K1Q cta %d warp %d slabs %lld: wait %lld prologue %lld first %lld loop_end %lld "
+           "after_sync %lld staged %lld end %lld | w_full %lld w_pfull %lld\n", blockIdx.x, warp,
+           (long long)n_mine, pt_wait, pt_pro, pt_first, pt_loop, pt_sync, pt_staged, clock64() - pt0,
+           w_full, w_p);
+#endif
 }
 
 }  // namespace mcp

@@ -100,23 +100,71 @@ __global__ void __launch_bounds__(K3_T)
   }
 }
 
-// K3F: the fixed-order partial reduce of K3 fused with the finish (objective.py:51-56) when
-// K1P/K1Q already produced M = (A o lam) C and u = (G o C) lam: g_A = -2d (Y - M) o lam is
-// elementwise on the reduced Y, g_lam = -2 (w - u), and f = alpha + lam.u - 2 w.lam (r <= 32:
-// one w block holds every w).  out = [f ; g_lam ; vec_F(g_A)], bitwise the K3 + K4L result.
+// Tail pieces inside one block, from x = [lam ; vec_F(A)] alone (implicit.py:143-151), in the
+// expression order of k1p_tail_pre / k_tail_gram / k_tail_vec so every path stays bitwise equal:
+// G = A^T A (warp per upper-triangle entry: lane-strided products, fixed butterfly, mirrored),
+// C = G^(d-1) by repeated multiplication (implicit.py:82-91); then per entry
+// u_j = sum_k (G_jk C_jk) lam_k and M_ij = sum_k (A_ik lam_k) C_kj.
+__device__ __forceinline__ void tail_gc_block(const double* __restrict__ x, int n, int r, int d,
+                                              double* sG, double* sC) {
+  const double* A = x + r;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int pr = warp; pr < r * r; pr += nw) {
+    const int j = pr / r, k = pr % r;
+    if (j > k) continue;
+    const double* aj = A + (int64_t)j * n;
+    const double* ak = A + (int64_t)k * n;
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += aj[i] * ak[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) {
+      const double c = rm_pow(s, d - 1);
+      sG[j * r + k] = s;
+      sG[k * r + j] = s;
+      sC[j * r + k] = c;
+      sC[k * r + j] = c;
+    }
+  }
+}
+__device__ __forceinline__ double tail_u_entry(const double* sG, const double* sC,
+                                               const double* __restrict__ lam, int r, int j) {
+  double u = 0.0;
+  for (int k = 0; k < r; ++k) u += (sG[j * r + k] * sC[j * r + k]) * lam[k];
+  return u;
+}
+__device__ __forceinline__ double tail_m_entry(const double* __restrict__ x, const double* sC,
+                                               int n, int r, int i, int j) {
+  const double* A = x + r;
+  double m = 0.0;
+  for (int k = 0; k < r; ++k) m += (A[(int64_t)k * n + i] * x[k]) * sC[k * r + j];
+  return m;
+}
+
+// K3F: the fixed-order partial reduce of K3 fused with the whole finish (objective.py:51-56,
+// implicit.py:143-151) for r <= 32.  Every block first forms G, C (and the M / u entries it
+// needs) from x alone -- under programmatic dependent launch this runs while K1 drains -- then
+// waits for K1's partials: g_A = -2d (Y - M) o lam is elementwise on the reduced Y,
+// g_lam = -2 (w - u), f = alpha + lam.u - 2 w.lam.  out = [f ; g_lam ; vec_F(g_A)], bitwise the
+// K3 + K4 result.
+constexpr int K3F_MAXR = 32;
 __global__ void __launch_bounds__(K3_T)
     k_reduce_finish(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
-                    int r, int n_pad, int RB, int rbs, int gp, const double* __restrict__ x,
-                    const double* __restrict__ M, const double* __restrict__ u, int d,
+                    int r, int n_pad, int RB, int rbs, int gp, const double* __restrict__ x, int d,
                     const double* __restrict__ alpha_dev, double alpha_host,
                     double* __restrict__ out) {
-  // PDL: launched while K1Q drains; its partials are complete only after this wait.  The next
-  // kernel may start its V-only prologue right away.
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ double sm[K3_T];
   __shared__ double s_w[K3W_X];
+  __shared__ double sG[K3F_MAXR * K3F_MAXR], sC[K3F_MAXR * K3F_MAXR];
+  __shared__ double s_u[K3F_MAXR];
   const double* lam = x;
+  // x is final here: K1 (launched before us) waited for its producer before triggering us
+  tail_gc_block(x, n, r, d, sG, sC);
+  __syncthreads();
+  // PDL: K1's partials are complete only after this wait; the next kernel may start its V-only
+  // prologue right away.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int per_rb = n * RB;
   const int yblocks = (per_rb + K3_X - 1) / K3_X;
   const int64_t total_blocks = (int64_t)rbs * yblocks + 1;   // + the w / f block
@@ -131,8 +179,8 @@ __global__ void __launch_bounds__(K3_T)
       if (ty == 0 && e < per_rb) {
         const int i = e / RB, j = rb * RB + e % RB;
         if (j < r) {
-          const int64_t dst = (int64_t)j * n + i;
-          out[1 + r + dst] = (s2d * (t - M[dst])) * lam[j];
+          const double m = tail_m_entry(x, sC, n, r, i, j);
+          out[1 + r + (int64_t)j * n + i] = (s2d * (t - m)) * lam[j];
         }
       }
     } else {
@@ -144,14 +192,16 @@ __global__ void __launch_bounds__(K3_T)
       if (ty == 0 && k < rbs * RB) {
         const int j = (k / RB) * RB + k % RB;
         if (j < r) {
+          const double u = tail_u_entry(sG, sC, lam, r, j);
           s_w[j] = t;
-          out[1 + j] = -2.0 * (t - u[j]);
+          s_u[j] = u;
+          out[1 + j] = -2.0 * (t - u);
         }
       }
       __syncthreads();
       if (threadIdx.x == 0) {
         double lu = 0.0, wl = 0.0;
-        for (int jj = 0; jj < r; ++jj) lu += lam[jj] * u[jj];
+        for (int jj = 0; jj < r; ++jj) lu += lam[jj] * s_u[jj];
         for (int jj = 0; jj < r; ++jj) wl += s_w[jj] * lam[jj];
         const double alpha = alpha_dev ? *alpha_dev : alpha_host;
         out[0] = alpha + lu - 2.0 * wl;

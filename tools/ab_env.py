@@ -36,7 +36,7 @@ stream = torch.cuda.current_stream()
 sh = _native.stream_handle(stream)
 if a.timing:
     ctx.set_kernel_timing(True)
-variants = [("base", {})] + [(t, dict([t.split("=", 1)])) for t in a.toggles]
+variants = [("base", {})] + [(t, dict(kv.split("=", 1) for kv in t.split(","))) for t in a.toggles]
 res = {name: [] for name, _ in variants}
 outs = {}
 for rep in range(a.reps):
@@ -56,8 +56,18 @@ for rep in range(a.reps):
         outs[name] = out.clone()
         for k in env:
             del os.environ[k]
+ref = None
+if a.mode not in (None, "fp64"):
+    ref = torch.empty_like(out)
+    ctx.fg_device(cfg.d, cfg.r, x.data_ptr(), 0.0, "fp64", ref.data_ptr(), sh)
+    torch.cuda.synchronize()
 for name, _ in variants:
     v = res[name]
     same = torch.equal(outs[name], outs["base"])
+    err = ""
+    if ref is not None:
+        o = outs[name]
+        err = (f"  rel_err_vs_fp64 f {abs(float(o[0] - ref[0])) / abs(float(ref[0])):.2e}"
+               f" g {float((o[1:] - ref[1:]).norm() / ref[1:].norm()):.2e}")
     print(f"{name:30s} median {statistics.median(v):.4f} ms  min {min(v):.4f}  "
-          f"bitwise_equal_to_base={same}  variant={ctx.last_variant}")
+          f"bitwise_equal_to_base={same}{err}  variant={ctx.last_variant}")

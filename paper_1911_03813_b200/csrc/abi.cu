@@ -377,7 +377,9 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   if (pl.mode == MCP_MODE_TF32X3) return enqueue_partial_tf32(c, pl, dx, dYw, s);
   const K1Variant& v = pl.k1;
   const int n = (int)c->n, r = pl.r;
-  const bool tp = tail_pieces && k1_fuses_tail(v, c->n, r);
+  // the finishing kernels (K3F, the peer reduce) form M and u themselves now; K1 never does
+  (void)tail_pieces;
+  const bool tp = false;
   int launches = 2;
   if (v.needs_prep()) {
     k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(

@@ -5,6 +5,7 @@
 #include "momentcp_b200.h"
 #include "k1_dispatch.h"
 #include "k1_fp64.cuh"
+#include "tail_pieces.cuh"
 #include "k1s_fp64.cuh"
 #include "k1p_fp64.cuh"
 #include "k1q_fp64.cuh"
@@ -324,9 +325,13 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
 
 }  // namespace
 
+// The one-kernel reduce + finish (K3F) applies when its w block holds every w and the factor
+// Gram fits its shared memory; it forms the tail pieces itself, so any K1 that needs no prep
+// launch qualifies.
 bool k1_fuses_tail(const K1Variant& v, int64_t n, int r) {
-  return (v.kind == 3 || v.kind == 4) && r <= 32 &&
-         (size_t)(n * r + (int64_t)r * r) <= k1p_pstage_elems(v.RB);
+  (void)n;
+  return (v.kind == 1 || v.kind == 3 || v.kind == 4) && r <= K3F_MAXR &&
+         v.rbs * v.RB <= K3W_X;
 }
 
 int64_t obs_pitch(int dtype, int64_t n) {

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "mcp_common.cuh"
+#include "tail_pieces.cuh"
 
 namespace mcp {
 
@@ -33,8 +34,6 @@ __global__ void k_prep_afrag(const double* __restrict__ A, int n, int r, int RB,
 // ty + K3_Y, ... in order, then a fixed binary tree over the lanes (one or two loads per thread at
 // gp = 148: the reduce is latency-, not bandwidth-bound).  The w block uses 32 columns x 32
 // lanes the same way.  K3 and K3F share both orders, so partial + finish == fused, bitwise.
-constexpr int K3_X = 8, K3_Y = 128, K3_T = K3_X * K3_Y;
-constexpr int K3W_X = 32, K3W_Y = K3_T / K3W_X;
 
 template <int X, int Y>
 __device__ __forceinline__ double k3_tree(double s, double* sm, int tx, int ty) {
@@ -100,54 +99,12 @@ __global__ void __launch_bounds__(K3_T)
   }
 }
 
-// Tail pieces inside one block, from x = [lam ; vec_F(A)] alone (implicit.py:143-151), in the
-// expression order of k1p_tail_pre / k_tail_gram / k_tail_vec so every path stays bitwise equal:
-// G = A^T A (warp per upper-triangle entry: lane-strided products, fixed butterfly, mirrored),
-// C = G^(d-1) by repeated multiplication (implicit.py:82-91); then per entry
-// u_j = sum_k (G_jk C_jk) lam_k and M_ij = sum_k (A_ik lam_k) C_kj.
-__device__ __forceinline__ void tail_gc_block(const double* __restrict__ x, int n, int r, int d,
-                                              double* sG, double* sC) {
-  const double* A = x + r;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int pr = warp; pr < r * r; pr += nw) {
-    const int j = pr / r, k = pr % r;
-    if (j > k) continue;
-    const double* aj = A + (int64_t)j * n;
-    const double* ak = A + (int64_t)k * n;
-    double s = 0.0;
-    for (int i = lane; i < n; i += 32) s += aj[i] * ak[i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) {
-      const double c = rm_pow(s, d - 1);
-      sG[j * r + k] = s;
-      sG[k * r + j] = s;
-      sC[j * r + k] = c;
-      sC[k * r + j] = c;
-    }
-  }
-}
-__device__ __forceinline__ double tail_u_entry(const double* sG, const double* sC,
-                                               const double* __restrict__ lam, int r, int j) {
-  double u = 0.0;
-  for (int k = 0; k < r; ++k) u += (sG[j * r + k] * sC[j * r + k]) * lam[k];
-  return u;
-}
-__device__ __forceinline__ double tail_m_entry(const double* __restrict__ x, const double* sC,
-                                               int n, int r, int i, int j) {
-  const double* A = x + r;
-  double m = 0.0;
-  for (int k = 0; k < r; ++k) m += (A[(int64_t)k * n + i] * x[k]) * sC[k * r + j];
-  return m;
-}
-
 // K3F: the fixed-order partial reduce of K3 fused with the whole finish (objective.py:51-56,
 // implicit.py:143-151) for r <= 32.  Every block first forms G, C (and the M / u entries it
 // needs) from x alone -- under programmatic dependent launch this runs while K1 drains -- then
 // waits for K1's partials: g_A = -2d (Y - M) o lam is elementwise on the reduced Y,
 // g_lam = -2 (w - u), f = alpha + lam.u - 2 w.lam.  out = [f ; g_lam ; vec_F(g_A)], bitwise the
 // K3 + K4 result.
-constexpr int K3F_MAXR = 32;
 __global__ void __launch_bounds__(K3_T)
     k_reduce_finish(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
                     int r, int n_pad, int RB, int rbs, int gp, const double* __restrict__ x, int d,

@@ -22,6 +22,7 @@
 
 #include "ctx.h"
 #include "mcp_common.cuh"
+#include "tail_pieces.cuh"
 
 using namespace mcp;
 using namespace mcp_internal;
@@ -57,11 +58,13 @@ __global__ void k_peer_signal(int64_t* const* __restrict__ flags, int rank, int 
 __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
                                      const int64_t* __restrict__ my_flags, int world,
                                      int64_t epoch, int n, int r, int d,
-                                     const double* __restrict__ x, const double* __restrict__ M,
-                                     const double* __restrict__ u, double alpha,
+                                     const double* __restrict__ x, int light, double alpha,
                                      double* __restrict__ out, double* __restrict__ Yw_sum,
                                      int* __restrict__ err) {
   __shared__ int ok;
+  __shared__ double sG[K3F_MAXR * K3F_MAXR], sC[K3F_MAXR * K3F_MAXR];
+  // light (r <= K3F_MAXR): G and C from x alone, while the peers' partials are still coming
+  if (light) tail_gc_block(x, n, r, d, sG, sC);
   if (threadIdx.x == 0) {
     ok = 1;
     for (int k = 0; k < world; ++k) {
@@ -83,9 +86,10 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
          e += (int64_t)(gridDim.x - 1) * PR_T) {
       double y = 0.0;
       for (int k = 0; k < world; ++k) y += ld_volatile_sys(parts[k] + e);
-      if (M) {
-        const int j = (int)(e / n);
-        out[1 + r + e] = ((-2.0 * d) * (y - M[e])) * lam[j];
+      if (light) {
+        const int j = (int)(e / n), i = (int)(e % n);
+        const double m = tail_m_entry(x, sC, n, r, i, j);
+        out[1 + r + e] = ((-2.0 * d) * (y - m)) * lam[j];
       } else {
         Yw_sum[e] = y;
       }
@@ -93,20 +97,23 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
     return;
   }
   __shared__ double s_w[1024];
+  __shared__ double s_u[K3F_MAXR];
   for (int j = threadIdx.x; j < r; j += PR_T) {
     double w = 0.0;
     for (int k = 0; k < world; ++k) w += ld_volatile_sys(parts[k] + nr + j);
-    if (M) {
+    if (light) {
+      const double u = tail_u_entry(sG, sC, lam, r, j);
       s_w[j] = w;
-      out[1 + j] = -2.0 * (w - u[j]);
+      s_u[j] = u;
+      out[1 + j] = -2.0 * (w - u);
     } else {
       Yw_sum[nr + j] = w;
     }
   }
   __syncthreads();
-  if (M && threadIdx.x == 0) {
+  if (light && threadIdx.x == 0) {
     double lu = 0.0, wl = 0.0;
-    for (int j = 0; j < r; ++j) lu += lam[j] * u[j];
+    for (int j = 0; j < r; ++j) lu += lam[j] * s_u[j];
     for (int j = 0; j < r; ++j) wl += s_w[j] * lam[j];
     out[0] = alpha + lu - 2.0 * wl;
   }
@@ -140,7 +147,7 @@ extern "C" int mcp_peer_reduce_finish(mcp_ctx* c, int d, int r, const double* dx
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   const int n = (int)c->n;
   const int64_t nr = (int64_t)n * r;
-  const bool light = c->tail_x == dx && c->tail_d == d && c->tail_r == r;
+  const bool light = r <= K3F_MAXR;   // tail pieces formed in-kernel
   int rc;
   if (!light) {
     if ((rc = ensure(c, c->dYw, sizeof(double) * (size_t)(nr + r)))) return rc;
@@ -149,9 +156,8 @@ extern "C" int mcp_peer_reduce_finish(mcp_ctx* c, int d, int r, const double* dx
   }
   const int nb = (int)std::min<int64_t>(ceil_div(nr, PR_T), 4 * c->sms) + 1;
   k_peer_reduce_finish<<<nb, PR_T, 0, s>>>(
-      (const double* const*)part_ptrs, my_flags, world, epoch, n, r, d, dx,
-      light ? (const double*)c->dM.p : nullptr, light ? (const double*)c->du.p : nullptr, alpha,
-      dout, light ? nullptr : (double*)c->dYw.p, derr);
+      (const double* const*)part_ptrs, my_flags, world, epoch, n, r, d, dx, light ? 1 : 0,
+      alpha, dout, light ? nullptr : (double*)c->dYw.p, derr);
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches = 1;
   if (!light) {

@@ -171,6 +171,22 @@ bool make_tmap_f32(CUtensorMap* m, void* gaddr, uint64_t inner, uint64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D fp32 tensor map over row-major rows of `ld` floats viewed as (32 floats, rows, ld / 32
+// column chunks): one box of 32 x box_rows x box_chunks loads box_chunks bricks of
+// box_rows x 128 B, chunk-major (the layout four 2-D boxes would produce), in ONE TMA.
+bool make_tmap_f32_chunks(CUtensorMap* m, void* gaddr, uint64_t ld, uint64_t rows,
+                          uint32_t box_rows, uint32_t box_chunks, CUtensorMapSwizzle sw) {
+  auto enc = tmap_encoder();
+  if (!enc || ld % 32) return false;
+  cuuint64_t dims[3] = {32, rows, ld / 32};
+  cuuint64_t strides[2] = {4 * ld, 128};
+  cuuint32_t box[3] = {32, box_rows, box_chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, gaddr, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   K1TPlan& t = pl.t;
   const int64_t n = c->n;
@@ -192,6 +208,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
       CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     }
     c->tm_v_ready = false;
+    c->tm_c_ready = false;
   }
   if (!c->tm_v_ready) {
     if (!make_tmap_f32(&c->tm_v1, c->dV32, c->ldv32, c->p_pad, 4 * c->ldv32, 32, 128,
@@ -223,12 +240,31 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     }
     t.v2 = c->dVlo32 != nullptr;
   }
+  // K1T2's GEMM2 V reads: one 3-D TMA per 16 KB stage half when rows are whole 32-float chunks
+  t.g2_3d = false;
+  if (t.v2 && c->ldv32 % 32 == 0 && c->ldv32 >= 128 && !getenv("MCP_K1T2_G2_2D")) {
+    if (!c->tm_c_ready) {
+      c->tm_c_ready =
+          make_tmap_f32_chunks(&c->tm_v3, c->dV32, c->ldv32, c->p_pad, 32, 4,
+                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+          make_tmap_f32_chunks(&c->tm_l3, c->dVlo32, c->ldv32, c->p_pad, 32, 4,
+                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
+    t.g2_3d = c->tm_c_ready;
+  }
   // column block RB (the UMMA N): as wide as TMEM allows -- Z (K1T2: double-buffered) plus
   // Y[mt] for the n / 128 m-tiles -- since the 3xTF32 UMMAs are shared-memory-bandwidth bound
   // and the operand bytes per MAC fall with N.  K1T2 takes any multiple of 16 up to 64, K1T
   // powers of two.
   const bool v1 = !t.v2;
-  const int zbufs = v1 ? 1 : 2;
+  auto env_int = [](const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+  };
+  t.serial = !v1 && env_int("MCP_K1T2_SERIAL", 1) != 0;
+  t.hint = !v1 && env_int("MCP_K1T2_HINT", 1) != 0;
+  t.flush = std::max(1, env_int("MCP_K1T2_FLUSH", 16));
+  const int zbufs = (v1 || t.serial) ? 1 : 2;
   int RB = 16;
   if (v1) {
     while (RB < r && RB < 64) RB *= 2;
@@ -242,7 +278,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     while (RB > 16 && ceil_div(r, RB - 16) == rbs_w && (RB - 16) >= r / rbs_w) RB -= 16;
   }
   // K1T2 with the concatenated GEMM1 when TMEM has room for two 2 RB-wide Z buffers
-  t.zcat = !v1 && !getenv("MCP_K1T_NO_ZCAT") && 2 * RB <= 256 && (4 + t.mt2) * RB <= 512;
+  t.zcat = !v1 && !getenv("MCP_K1T_NO_ZCAT") && 2 * RB <= 256 && (2 * zbufs + t.mt2) * RB <= 512;
   if ((zbufs + t.mt2) * RB > 512)
     return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
   t.RB = RB;
@@ -286,7 +322,11 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.wpart_elems = 0;
   pl.k1.afrag_elems = 0;
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
-                std::to_string(RB) + ",S=" + std::to_string(ns) + ">";
+                std::to_string(RB) + ",S=" + std::to_string(ns) +
+                (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
+                             (t.hint ? ",l2hint" : "") + (t.g2_3d ? ",g2tma3d" : "") + ",flush=" + std::to_string(t.flush)
+                      : std::string()) +
+                ">";
   return MCP_OK;
 }
 
@@ -354,10 +394,15 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.nu_const = c->nu_const;
   prm.Ypart = (double*)c->dYpart.p;
   prm.zcat = t.zcat ? 1 : 0;
+  prm.serial = t.serial ? 1 : 0;
+  prm.hint = t.hint ? 1 : 0;
+  prm.flush = t.flush;
+  prm.g2_3d = t.g2_3d ? 1 : 0;
   auto* ev = timing_begin(c, s);
   if (t.v2)
-    k1t2_fg_tf32<<<t.gp * t.rbs, K1T2_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_l1, c->tm_l2,
-                                                             c->tm_a, prm);
+    k1t2_fg_tf32<<<t.gp * t.rbs, K1T2_THREADS, t.smem, s>>>(
+        c->tm_v1, t.g2_3d ? c->tm_v3 : c->tm_v2, c->tm_l1, t.g2_3d ? c->tm_l3 : c->tm_l2, c->tm_a,
+        prm);
   else
     k1t_fg_tf32<<<t.gp * t.rbs, K1T_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_a, prm);
   timing_end(ev, s);
@@ -675,6 +720,7 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   c->dVlo32 = nullptr;
   c->own_v32 = false;
   c->tm_v_ready = false;
+  c->tm_c_ready = false;
   int rc = dtype == MCP_F64
                ? upload_obs<double>(c, (const double*)V, on_device, layout, n, p, ld)
                : upload_obs<float>(c, (const float*)V, on_device, layout, n, p, ld);

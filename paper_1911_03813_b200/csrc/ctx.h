@@ -61,6 +61,8 @@ struct mcp_ctx {
   CUtensorMap tm_v1, tm_v2, tm_a;
   float* dVlo32 = nullptr;     // fast mode K1T2: V - tf32(V), same layout as dV32
   CUtensorMap tm_l1, tm_l2;
+  CUtensorMap tm_v3, tm_l3;    // K1T2 GEMM2: 3-D chunk maps over V / V_lo (ld % 32 == 0)
+  bool tm_c_ready = false;
   void* tm_a_addr = nullptr;
   int tm_a_rows = 0, tm_a_kpad = 0, tm_a_rb = 0;
   mcp_internal::DevBuf dAt;
@@ -102,6 +104,10 @@ struct K1TPlan {
   int RB = 0, rbs = 0, gp = 0, stages = 0, nkb = 0, mt2 = 0, r_pad = 0, kpad = 0;
   bool v2 = false;   // K1T2 (precomputed V_lo) instead of K1T (in-kernel split)
   bool zcat = false; // K1T2 concatenated GEMM1 (Z in two TMEM halves)
+  bool serial = false;  // K1T2 tile order GEMM1(u), GEMM2(u) (one Z buffer)
+  bool hint = false;    // K1T2 L2 eviction policy on the V reads
+  int flush = 8;        // K1T2 tiles per fp64 flush of the fp32 TMEM Y
+  bool g2_3d = false;   // K1T2 GEMM2 V loads as one 3-D TMA per operand and stage
   int64_t num_tiles = 0;
   size_t smem = 0;
 };

@@ -51,6 +51,11 @@ struct K1TParams {
   double* Ypart;      // [rbs][gp][mt2*128][RB] fp64
   int zcat = 0;       // K1T2: GEMM1 as V_hi x [A_hi ; A_lo] (N = 2 RB) + V_lo x A_hi: Z takes
                       // 2 RB TMEM columns per buffer and the epilogue adds its two halves
+  int serial = 0;     // K1T2: GEMM2(u) right after GEMM1(u) (reuse distance one tile) instead of
+                      // GEMM1(u + 1) first (epilogue hidden, reuse distance two tiles)
+  int hint = 0;       // K1T2: L2 policy -- GEMM1's V reads evict_last, everything else evict_first
+  int flush = 8;      // K1T2: tiles accumulated in fp32 TMEM between fp64 flushes
+  int g2_3d = 0;      // K1T2: tm_v2 / tm_l2 are 3-D chunk maps (one TMA per 16 KB operand)
 };
 
 __host__ __device__ constexpr size_t k1t_stage_bytes(int RB) { return 2 * K1T_VBYTES + 256 * RB; }
@@ -393,9 +398,11 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
   const int64_t my_tiles =
       pg < prm.num_tiles ? (prm.num_tiles - pg + prm.gp - 1) / prm.gp : 0;
   const int mt2 = prm.mt2, nkb = prm.nkb;
-  auto flush_after = [&](int64_t v) {   // tile v ends a group of K1T_FLUSH tiles (or the last)
-    return (v % K1T_FLUSH) == K1T_FLUSH - 1 || v == my_tiles - 1;
+  auto flush_after = [&](int64_t v) {   // tile v ends a group of prm.flush tiles (or the last)
+    return (v % prm.flush) == prm.flush - 1 || v == my_tiles - 1;
   };
+  // Z buffer of tile u: alternating under look-ahead; serial order needs only one (TMEM freed)
+  auto zbuf = [&](int64_t u) -> int { return prm.serial ? 0 : (int)(u & 1); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -423,7 +430,8 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int ZW = prm.zcat ? 2 * RB : RB;          // TMEM columns of one Z buffer
-  const uint32_t ty = tmem + 2 * ZW;               // Y[mt] at 2 ZW + mt RB; Z[b] at b ZW
+  // Z[b] at b ZW; Y[mt] after the Z buffers (two under look-ahead, one in serial order)
+  const uint32_t ty = tmem + (prm.serial ? 1 : 2) * ZW;
 
   if (warp == 0) {
     // =========================== TMA producer (same order as the MMA issuer) ===========================
@@ -434,35 +442,67 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
         if (qq >= NS) mbar_wait(&empty[s], (uint32_t)((qq / NS) - 1) & 1);
         return base + s * SB;
       };
-      for (int64_t u = 0; u <= my_tiles; ++u) {
-        if (u < my_tiles) {
-          const int row0 = (int)((pg + u * prm.gp) * K1T_TP);
-          for (int kb = 0; kb < nkb; ++kb, ++q) {
-            unsigned char* st = stage(q);
-            uint64_t* fb = &full[q % NS];
-            mbar_arrive_expect_tx(fb, 2 * K1T_VBYTES + 256 * RB);
-            tma_load_2d(st, &tm_v1, kb * 32, row0, smem_u32(fb));
-            tma_load_2d(st + K1T_VBYTES, &tm_l1, kb * 32, row0, smem_u32(fb));
-            tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, kb * 32, rb * RB, smem_u32(fb));
-            tma_load_2d(st + 2 * K1T_VBYTES + 128 * RB, &tm_a, kb * 32, prm.r_pad + rb * RB,
-                        smem_u32(fb));
-          }
+      uint64_t pol_keep = 0, pol_drop = 0;
+      if (prm.hint) {
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
+      }
+      auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* fb, uint64_t pol) {
+        if (prm.hint)
+          tma_load_2d_hint(dst, tm, c0, c1, smem_u32(fb), pol);
+        else
+          tma_load_2d(dst, tm, c0, c1, smem_u32(fb));
+      };
+      auto load3 = [&](void* dst, const CUtensorMap* tm, int row, int chunk, uint64_t* fb,
+                       uint64_t pol) {
+        if (prm.hint)
+          tma_load_3d_hint(dst, tm, 0, row, chunk, smem_u32(fb), pol);
+        else
+          tma_load_3d(dst, tm, 0, row, chunk, smem_u32(fb));
+      };
+      auto g1 = [&](int64_t u) {
+        const int row0 = (int)((pg + u * prm.gp) * K1T_TP);
+        for (int kb = 0; kb < nkb; ++kb, ++q) {
+          unsigned char* st = stage(q);
+          uint64_t* fb = &full[q % NS];
+          mbar_arrive_expect_tx(fb, 2 * K1T_VBYTES + 256 * RB);
+          load(st, &tm_v1, kb * 32, row0, fb, pol_keep);
+          load(st + K1T_VBYTES, &tm_l1, kb * 32, row0, fb, pol_keep);
+          tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, kb * 32, rb * RB, smem_u32(fb));
+          tma_load_2d(st + 2 * K1T_VBYTES + 128 * RB, &tm_a, kb * 32, prm.r_pad + rb * RB,
+                      smem_u32(fb));
         }
-        if (u >= 1) {
-          const int row0 = (int)((pg + (u - 1) * prm.gp) * K1T_TP);
-          for (int step = 0; step < 4 * mt2; ++step, ++q) {
-            const int mt = step >> 2, rc = step & 3;
-            unsigned char* st = stage(q);
-            uint64_t* fb = &full[q % NS];
-            mbar_arrive_expect_tx(fb, (MCP_K1T2_EXP_NOLO2 ? 1 : 2) * K1T_VBYTES);
+      };
+      auto g2 = [&](int64_t v) {
+        const int row0 = (int)((pg + v * prm.gp) * K1T_TP);
+        for (int step = 0; step < 4 * mt2; ++step, ++q) {
+          const int mt = step >> 2, rc = step & 3;
+          unsigned char* st = stage(q);
+          uint64_t* fb = &full[q % NS];
+          mbar_arrive_expect_tx(fb, (MCP_K1T2_EXP_NOLO2 ? 1 : 2) * K1T_VBYTES);
+          if (prm.g2_3d) {
+            load3(st, &tm_v2, row0 + rc * 32, mt * 4, fb, pol_drop);
+            if (!MCP_K1T2_EXP_NOLO2) load3(st + K1T_VBYTES, &tm_l2, row0 + rc * 32, mt * 4, fb, pol_drop);
+          } else {
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-              tma_load_2d(st + b * 4096, &tm_v2, mt * 128 + b * 32, row0 + rc * 32, smem_u32(fb));
+              load(st + b * 4096, &tm_v2, mt * 128 + b * 32, row0 + rc * 32, fb, pol_drop);
               if (!MCP_K1T2_EXP_NOLO2)
-                tma_load_2d(st + K1T_VBYTES + b * 4096, &tm_l2, mt * 128 + b * 32, row0 + rc * 32,
-                            smem_u32(fb));
+                load(st + K1T_VBYTES + b * 4096, &tm_l2, mt * 128 + b * 32, row0 + rc * 32, fb,
+                     pol_drop);
             }
           }
+        }
+      };
+      if (prm.serial) {
+        for (int64_t u = 0; u < my_tiles; ++u) {
+          g1(u);
+          g2(u);
+        }
+      } else {
+        for (int64_t u = 0; u <= my_tiles; ++u) {
+          if (u < my_tiles) g1(u);
+          if (u >= 1) g2(u - 1);
         }
       }
     }
@@ -477,10 +517,9 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       bool fresh = true, wait_y = false;
       long long w_full1 = 0, w_full2 = 0, w_p = 0, w_y = 0;
       const long long t_begin = clock64();
-      for (int64_t u = 0; u <= my_tiles; ++u) {
-        if (u < my_tiles) {
-          // ---- GEMM1(u): Z[u & 1] = V A (3xTF32) ----
-          const uint32_t tz = tmem + (uint32_t)((u & 1) * ZW);
+      auto g1 = [&](int64_t u) {
+          // ---- GEMM1(u): Z[zb] = V A (3xTF32) ----
+          const uint32_t tz = tmem + (uint32_t)(zbuf(u) * ZW);
           for (int kb = 0; kb < nkb; ++kb, ++q) {
             const int s = (int)(q % NS);
             {
@@ -516,11 +555,10 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             }
             umma_commit(smem_u32(&empty[s]));
           }
-          umma_commit(smem_u32(&z_full[u & 1]));
-        }
-        if (u >= 1) {
-          // ---- GEMM2(u - 1): Y += V^T P (3xTF32) ----
-          const int64_t v = u - 1;
+          umma_commit(smem_u32(&z_full[zbuf(u)]));
+      };
+      auto g2 = [&](int64_t v) {
+          // ---- GEMM2(v): Y += V^T P (3xTF32) ----
           {
             K1T2_T0();
             mbar_wait(p_full, (uint32_t)v & 1);
@@ -566,8 +604,29 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             ++flushes;
             wait_y = true;
           }
+      };
+      long long t_g1 = 0, t_g2 = 0;
+      if (prm.serial) {
+        for (int64_t u = 0; u < my_tiles; ++u) {
+          const long long a0 = clock64();
+          g1(u);
+          const long long a1 = clock64();
+          g2(u);
+          t_g1 += a1 - a0;
+          t_g2 += clock64() - a1;
+        }
+      } else {
+        for (int64_t u = 0; u <= my_tiles; ++u) {
+          if (u < my_tiles) g1(u);
+          if (u >= 1) g2(u - 1);
         }
       }
+#if MCP_K1T2_PROF
+      if (blockIdx.x == 0) printf("K1T2 MMA phases: g1 %lld g2 %lld\n", t_g1, t_g2);
+#else
+      (void)t_g1;
+      (void)t_g2;
+#endif
 #if MCP_K1T2_PROF
       if (blockIdx.x == 0)
         printf("K1T2 MMA: total %lld  wait full(G1) %lld  full(G2) %lld  p_full %lld  y_empty %lld  tiles %lld\n",
@@ -616,9 +675,14 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
     };
     for (int64_t u = 0; u < my_tiles; ++u) {
       const int64_t row0 = (pg + u * prm.gp) * K1T_TP;
+      // serial order: the group ending at tile u - 1 drains while GEMM1(u) runs
+      if (prm.serial && u >= 1 && flush_after(u - 1)) flush();
       {
         K1T2_T0();
-        mbar_wait(&z_full[u & 1], (uint32_t)(u >> 1) & 1);
+        if (prm.serial)
+          mbar_wait(&z_full[0], (uint32_t)u & 1);
+        else
+          mbar_wait(&z_full[u & 1], (uint32_t)(u >> 1) & 1);
         K1T2_ACC(e_wz);
       }
       if (u > 0) {
@@ -629,7 +693,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       tc_fence_after();
       {
         K1T2_T0();
-        const uint32_t tz = tmem + (uint32_t)((u & 1) * ZW);
+        const uint32_t tz = tmem + (uint32_t)(zbuf(u) * ZW);
         const double nul = prm.nu ? prm.nu[row0 + l] : prm.nu_const;
         const int brick = l >> 5, col = l & 31;
         for (int c0 = half * hc; col_active && c0 < c_end; c0 += 16) {
@@ -641,10 +705,15 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) zv[jj] += z2[jj];
           }
+          // powers for all 16 columns at once (one warp-uniform switch on d - 1, independent
+          // chains), same left-to-right products as rm_pow (implicit.py:82-91)
+          double zd[16], pw[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) zd[jj] = (double)zv[jj];
+          rm_pow_vec<16>(zd, pw, dm1);
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
-            const double z = (double)zv[jj];
-            const float pf = (float)(nul * rm_pow(z, dm1));
+            const float pf = (float)(nul * pw[jj]);
             const float ph = tf32_hi(pf);
             const uint32_t off = brick * 128 * RB + brick_off(c0 + jj, col);
             *reinterpret_cast<float*>(sPh + off) = ph;
@@ -657,7 +726,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
-      if (u >= 1 && flush_after(u - 1)) flush();   // committed after GEMM2(u - 1)
+      if (!prm.serial && u >= 1 && flush_after(u - 1)) flush();   // committed after GEMM2(u - 1)
     }
     if (my_tiles > 0) flush();                      // the group ending at the last tile
 #if MCP_K1T2_PROF

@@ -104,6 +104,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 16 consecutive 32-bit columns, issue only: several loads may be in flight before
+// one tmem_ld_wait() (the registers are valid only after it).
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
 // 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread (warp-collective).
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -126,6 +141,33 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0,
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
       "l"(tmap), "r"(c0), "r"(c1), "r"(mbar_smem_addr)
+      : "memory");
+}
+// Same, with an L2 cache-eviction policy (createpolicy.*) attached to the global reads.
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const void* tmap, int c0, int c1,
+                                                 uint32_t mbar_smem_addr, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(mbar_smem_addr), "l"(policy)
+      : "memory");
+}
+// 3-D tile loads (coordinates innermost first), plain and with an L2 policy.
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2,
+                                            uint32_t mbar_smem_addr) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(mbar_smem_addr)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const void* tmap, int c0, int c1,
+                                                 int c2, uint32_t mbar_smem_addr,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(mbar_smem_addr), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {

@@ -270,17 +270,7 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   const size_t stage_need = ((size_t)K1P_PAIRS * MT * 8 * cw + (size_t)2 * K1P_PAIRS * cw) * 8;
   if (ring_bytes < stage_need) return false;
   size_t smem = ring_bytes + fixed + 8 * (size_t)K1P_PAIRS * (SP + 4);
-  // K1Q: a dedicated scratch for the fused tail's pieces lets the GEMM2 warps compute them
-  // while the GEMM1 warps already stream the first slabs
-  int tail_off = 0;
-  if (specialised && r <= 32) {
-    const size_t off = round_up((int64_t)smem, 16);
-    const size_t need = ((size_t)n * r + (size_t)r * r) * 8;
-    if (off + need <= 227 * 1024 - 1024) {
-      tail_off = (int)off;
-      smem = off + need;
-    }
-  }
+  const int tail_off = 0;   // the tail pieces are formed by the finishing kernels now
   if (!attr[e].exchange(true)) {
     if (cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {

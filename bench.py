@@ -446,7 +446,7 @@ def main():
         ms_total = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs))
     k1_ms, k1_launches = ctx.kernel_time_ms(reset=True)
     ctx.set_kernel_timing(False)
-    launches_per_step = ctx.last_launch_count if world == 1 else (4 if pex is not None else 6)
+    launches_per_step = ctx.last_launch_count if world == 1 else (3 if pex is not None else 6)
     variant = ctx.last_variant
     clk = clocks.stop() if rank == 0 else None
 

@@ -208,6 +208,9 @@ int mcp_adam(mcp_ctx* ctx, int d, int r, int mode, const double* x0, const doubl
  *   mcp_peer_signal(ctx, flag_ptrs, rank, world, epoch, stream): flag_ptrs is a device array of
  *     `world` int64* (every rank's flag array); stores epoch at [rank] of each, release.sys,
  *     after this rank's partial (mcp_fg_partial_device into its slot) in stream order.
+ *   mcp_fg_partial_signal_device(ctx, d, r, dx, mode, dYw, flag_ptrs, rank, world, epoch,
+ *     stream): mcp_fg_partial_device into the slot dYw fused with mcp_peer_signal -- the
+ *     partial's reduce kernel publishes epoch once the whole piece is written (one launch less).
  *   mcp_peer_reduce_finish(ctx, d, r, dx, part_ptrs, my_flags, world, epoch, alpha, dout, derr,
  *     stream): waits for my_flags[k] >= epoch for all k (bounded; sets *derr = 1 on timeout),
  *     sums the world partials part_ptrs[0..world-1] in rank order and writes
@@ -215,6 +218,9 @@ int mcp_adam(mcp_ctx* ctx, int d, int r, int mode, const double* x0, const doubl
  */
 int mcp_peer_signal(mcp_ctx* ctx, const void* flag_ptrs, int rank, int world, int64_t epoch,
                     void* stream);
+int mcp_fg_partial_signal_device(mcp_ctx* ctx, int d, int r, const double* dx, int mode,
+                                 double* dYw, const void* flag_ptrs, int rank, int world,
+                                 int64_t epoch, void* stream);
 int mcp_peer_reduce_finish(mcp_ctx* ctx, int d, int r, const double* dx, const void* part_ptrs,
                            const int64_t* my_flags, int world, int64_t epoch, double alpha,
                            double* dout, int* derr, void* stream);

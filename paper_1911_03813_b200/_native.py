@@ -81,6 +81,9 @@ SIGNATURES = {
                                 _c_void_p, _dp, _c_void_p, _c_void_p, _i64, _c_void_p]),
     "mcp_peer_signal": (ctypes.c_int, [_c_void_p, _c_void_p, ctypes.c_int, ctypes.c_int, _i64,
                                        _c_void_p]),
+    "mcp_fg_partial_signal_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int,
+                                                    _c_void_p, ctypes.c_int, _c_void_p, _c_void_p,
+                                                    ctypes.c_int, ctypes.c_int, _i64, _c_void_p]),
     "mcp_peer_reduce_finish": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
                                               _c_void_p, _c_void_p, ctypes.c_int, _i64,
                                               ctypes.c_double, _c_void_p, _c_void_p, _c_void_p]),
@@ -372,6 +375,14 @@ class Context:
         rc = self._lib.mcp_peer_signal(self._h, ctypes.c_void_p(flag_ptrs_dev), int(rank),
                                        int(world), int(epoch), ctypes.c_void_p(stream_ptr))
         self._check(rc, "mcp_peer_signal")
+
+    def fg_partial_signal_device(self, d, r, dx_ptr, mode, dYw_ptr, flag_ptrs_dev, rank, world,
+                                 epoch, stream_ptr):
+        rc = self._lib.mcp_fg_partial_signal_device(
+            self._h, int(d), int(r), ctypes.c_void_p(dx_ptr), mode_code(mode),
+            ctypes.c_void_p(dYw_ptr), ctypes.c_void_p(flag_ptrs_dev), int(rank), int(world),
+            int(epoch), ctypes.c_void_p(stream_ptr))
+        self._check(rc, "mcp_fg_partial_signal_device")
 
     def peer_reduce_finish(self, d, r, dx_ptr, part_ptrs_dev, my_flags_ptr, world, epoch, alpha,
                            dout_ptr, derr_ptr, stream_ptr):

@@ -418,8 +418,14 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
 
 // prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows.
 int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
-                    cudaStream_t s, bool tail_pieces) {
-  if (pl.mode == MCP_MODE_TF32X3) return enqueue_partial_tf32(c, pl, dx, dYw, s);
+                    cudaStream_t s, bool tail_pieces, const K3Signal* signal) {
+  if (pl.mode == MCP_MODE_TF32X3) {
+    int rc = enqueue_partial_tf32(c, pl, dx, dYw, s);
+    if (rc || !signal) return rc;
+    k_publish<<<1, 32, 0, s>>>(*signal);
+    CUDA_TRY(c, cudaGetLastError());
+    return MCP_OK;
+  }
   const K1Variant& v = pl.k1;
   const int n = (int)c->n, r = pl.r;
   // the finishing kernels (K3F, the peer reduce) form M and u themselves now; K1 never does
@@ -447,9 +453,31 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   c->tail_r = r;
   const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) +
                              ceil_div((int64_t)v.rbs * v.RB, K3W_X);
-  k_reduce_partials<<<(int)std::min<int64_t>(red_blocks, 16 * c->sms), K3_T, 0, s>>>(
-      (const double*)c->dYpart.p, (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
-      dYw);
+  {
+    // K3 under programmatic dependent launch (its launch overlaps K1's drain); with a signal it
+    // also publishes the reduced piece to the peers (one launch instead of two)
+    K3Signal sig;
+    if (signal) {
+      if (!c->dticket.p) {
+        if ((rc = ensure(c, c->dticket, sizeof(unsigned)))) return rc;
+        CUDA_TRY(c, cudaMemsetAsync(c->dticket.p, 0, sizeof(unsigned), s));
+      }
+      sig = *signal;
+      sig.ticket = (unsigned*)c->dticket.p;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(red_blocks, 16 * c->sms));
+    cfg.blockDim = dim3(K3_T);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_reduce_partials, (const double*)c->dYpart.p,
+                                   (const double*)c->dwpart.p, n, r, v.n_pad, v.RB, v.rbs, v.gp,
+                                   dYw, sig));
+  }
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches = launches;
   c->variant = v.name;
@@ -738,7 +766,7 @@ void release_ctx(mcp_ctx* c) {
   drop_graphs(c);
   DevBuf* bufs[] = {&c->dx, &c->dout, &c->dYw, &c->dAfrag, &c->dYpart, &c->dwpart,
                     &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag, &c->dAt,
-                    &c->dM, &c->du};
+                    &c->dM, &c->du, &c->dticket};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->own_v32 && c->dV32) cudaFree(c->dV32);
@@ -1000,6 +1028,25 @@ int mcp_fg_partial_device(mcp_ctx* c, int d, int r, const double* dx, int mode, 
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   return enqueue_partial(c, pl, dx, dYw, s, true);
+}
+
+int mcp_fg_partial_signal_device(mcp_ctx* c, int d, int r, const double* dx, int mode,
+                                 double* dYw, const void* flag_ptrs, int rank, int world,
+                                 int64_t epoch, void* stream) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (!dx || !dYw || !flag_ptrs) return c->fail(MCP_ERR_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return c->fail(MCP_ERR_ARG, "bad peer arguments");
+  EvalPlan pl;
+  int rc = plan_eval(c, d, r, mode, pl);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  K3Signal sig;
+  sig.flags = (int64_t* const*)flag_ptrs;
+  sig.rank = rank;
+  sig.world = world;
+  sig.epoch = epoch;
+  return enqueue_partial(c, pl, dx, dYw, s, false, &sig);
 }
 
 int mcp_fg_finish_device(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,

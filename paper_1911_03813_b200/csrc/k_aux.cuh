@@ -67,9 +67,23 @@ __device__ __forceinline__ double k3_w_lane(const double* __restrict__ wpart, in
   return s;
 }
 
+// Publication without a reduce (fast mode: its w is formed after K3)
+__global__ void k_publish(K3Signal sig) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int k = 0; k < sig.world; ++k)
+    asm volatile("st.release.sys.global.b64 [%0], %1;\n" ::"l"(sig.flags[k] + sig.rank),
+                 "l"(sig.epoch)
+                 : "memory");
+}
+
 __global__ void __launch_bounds__(K3_T)
     k_reduce_partials(const double* __restrict__ Ypart, const double* __restrict__ wpart, int n,
-                      int r, int n_pad, int RB, int rbs, int gp, double* __restrict__ Yw) {
+                      int r, int n_pad, int RB, int rbs, int gp, double* __restrict__ Yw,
+                      K3Signal sig = K3Signal()) {
+  // PDL: launched while K1 drains; its partials are complete only after this wait
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ double sm[K3_T];
   const int per_rb = n * RB;
   const int yblocks = (per_rb + K3_X - 1) / K3_X;
@@ -95,6 +109,21 @@ __global__ void __launch_bounds__(K3_T)
         const int j = (k / RB) * RB + k % RB;
         if (j < r) Yw[(int64_t)n * r + j] = t;
       }
+    }
+  }
+  if (sig.flags) {
+    __shared__ bool last;
+    __threadfence_system();   // this block's outputs, before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(sig.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      *sig.ticket = 0u;
+      __threadfence_system();
+      for (int k = 0; k < sig.world; ++k)
+        asm volatile("st.release.sys.global.b64 [%0], %1;\n" ::"l"(sig.flags[k] + sig.rank),
+                     "l"(sig.epoch)
+                     : "memory");
     }
   }
 }

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "ctx.h"
@@ -61,6 +62,9 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
                                      const double* __restrict__ x, int light, double alpha,
                                      double* __restrict__ out, double* __restrict__ Yw_sum,
                                      int* __restrict__ err) {
+  // PDL: the next evaluation's K1 may start its V-only prologue; the peers' partials (ours
+  // included) are ordered by the flags below, not by grid completion
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ int ok;
   __shared__ double sG[K3F_MAXR * K3F_MAXR], sC[K3F_MAXR * K3F_MAXR];
   // light (r <= K3F_MAXR): G and C from x alone, while the peers' partials are still coming
@@ -155,9 +159,21 @@ extern "C" int mcp_peer_reduce_finish(mcp_ctx* c, int d, int r, const double* dx
     if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
   }
   const int nb = (int)std::min<int64_t>(ceil_div(nr, PR_T), 4 * c->sms) + 1;
-  k_peer_reduce_finish<<<nb, PR_T, 0, s>>>(
-      (const double* const*)part_ptrs, my_flags, world, epoch, n, r, d, dx, light ? 1 : 0,
-      alpha, dout, light ? nullptr : (double*)c->dYw.p, derr);
+  {
+    // under PDL it launches while this rank's K3 (which publishes our flag) drains
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nb);
+    cfg.blockDim = dim3(PR_T);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_peer_reduce_finish, (const double* const*)part_ptrs,
+                                   my_flags, world, epoch, n, r, d, dx, light ? 1 : 0, alpha,
+                                   dout, light ? nullptr : (double*)c->dYw.p, derr));
+  }
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches = 1;
   if (!light) {

@@ -11,6 +11,17 @@ constexpr int K3_X = 8, K3_Y = 128, K3_T = K3_X * K3_Y;
 constexpr int K3W_X = 32, K3W_Y = K3_T / K3W_X;
 constexpr int K3F_MAXR = 32;   // largest r whose G, C a finishing block keeps in shared memory
 
+// Optional publication of the reduced [Y | w] to the peers (multi-GPU exchange, csrc/peer.cu):
+// after every block has written its outputs, the last block to finish (ticket) fences at
+// system scope and release-stores `epoch` into flags[k][rank] for every rank k.
+struct K3Signal {
+  int64_t* const* flags = nullptr;   // device array of `world` flag arrays (peer-mapped)
+  unsigned* ticket = nullptr;        // zero-initialised; reset by the last block
+  int rank = 0, world = 0;
+  int64_t epoch = 0;
+};
+
+
 // Tail pieces inside one block, from x = [lam ; vec_F(A)] alone (implicit.py:143-151), in the
 // expression order of k1p_tail_pre / k_tail_gram / k_tail_vec so every path stays bitwise equal:
 // G = A^T A (warp per upper-triangle entry: lane-strided products, fixed butterfly, mirrored),

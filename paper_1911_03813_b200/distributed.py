@@ -177,8 +177,10 @@ class PeerExchange:
         return self.buf.data_ptr() + (epoch % 2) * self.L * 8
 
     def partial(self, d, x_ptr, mode, stream, epoch):
-        self.ctx.fg_partial_device(d, self.r, x_ptr, mode, self.slot_ptr(epoch), stream)
-        self.ctx.peer_signal(self.flag_ptrs.data_ptr(), self.rank, self.world, epoch, stream)
+        # the partial's reduce kernel publishes the epoch itself (no separate signal launch)
+        self.ctx.fg_partial_signal_device(d, self.r, x_ptr, mode, self.slot_ptr(epoch),
+                                          self.flag_ptrs.data_ptr(), self.rank, self.world,
+                                          epoch, stream)
 
     def reduce_finish(self, d, x_ptr, alpha, out_ptr, stream, epoch):
         self.ctx.peer_reduce_finish(d, self.r, x_ptr, self.parts[epoch % 2].data_ptr(),

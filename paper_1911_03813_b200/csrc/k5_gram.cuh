@@ -189,23 +189,34 @@ __global__ void __launch_bounds__(K52_THREADS, 1)
   const int wm = warp >> 2, wn = warp & 3;   // 4 x 4 warps, 32 x 32 each
   double tsum = 0.0;
 
-  for (int64_t pair = pair_begin + blockIdx.x; pair < pair_end; pair += gridDim.x) {
-    int64_t I, J;
+  // one cp.async pipeline over the flat (pair, chunk) sequence: the last chunk of a pair
+  // prefetches chunk 0 of the CTA's next pair, so no tile pair starts on an exposed load
+  int64_t pair = pair_begin + blockIdx.x;
+  int64_t I = 0, J = 0;
+  if (pair < pair_end) {
     k5_decode(pair, T, I, J);
+    k52_load<VT>(sI[0], V, ldv, I * K52_T, 0);
+    k52_load<VT>(sJ[0], V, ldv, J * K52_T, 0);
+    cp_async_commit();
+  }
+  int s = 0;   // buffer of the chunk being consumed (continues across pairs)
+  for (; pair < pair_end; pair += gridDim.x) {
+    const int64_t npair = pair + gridDim.x;
+    int64_t nI = 0, nJ = 0;
+    if (npair < pair_end) k5_decode(npair, T, nI, nJ);
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-    k52_load<VT>(sI[0], V, ldv, I * K52_T, 0);
-    k52_load<VT>(sJ[0], V, ldv, J * K52_T, 0);
-    cp_async_commit();
     for (int c = 0; c < n_chunks; ++c) {
-      const int s = c & 1;
-      if (c + 1 < n_chunks) {
-        k52_load<VT>(s ? sI[0] : sI[1], V, ldv, I * K52_T, c + 1);
-        k52_load<VT>(s ? sJ[0] : sJ[1], V, ldv, J * K52_T, c + 1);
+      const bool more = c + 1 < n_chunks || npair < pair_end;
+      if (more) {
+        const int64_t li = c + 1 < n_chunks ? I : nI, lj = c + 1 < n_chunks ? J : nJ;
+        const int lc = c + 1 < n_chunks ? c + 1 : 0;
+        k52_load<VT>(s ? sI[0] : sI[1], V, ldv, li * K52_T, lc);
+        k52_load<VT>(s ? sJ[0] : sJ[1], V, ldv, lj * K52_T, lc);
         cp_async_commit();
         cp_async_wait<1>();
       } else {
@@ -227,6 +238,7 @@ __global__ void __launch_bounds__(K52_THREADS, 1)
           for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
       }
       __syncthreads();
+      s ^= 1;
     }
 
     double tile_sum = 0.0;
@@ -244,6 +256,8 @@ __global__ void __launch_bounds__(K52_THREADS, 1)
         }
     }
     tsum += (I == J) ? tile_sum : 2.0 * tile_sum;
+    I = nI;
+    J = nJ;
   }
 
 #pragma unroll
@@ -251,9 +265,9 @@ __global__ void __launch_bounds__(K52_THREADS, 1)
   if (lane == 0) sRed[warp] = tsum;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < K52_THREADS / 32; ++w) s += sRed[w];
-    part[blockIdx.x] = s;
+    double sum = 0.0;
+    for (int w = 0; w < K52_THREADS / 32; ++w) sum += sRed[w];
+    part[blockIdx.x] = sum;
   }
 }
 

@@ -261,15 +261,17 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   if (e < 0) return false;
   const int cw = 8 * ntm + tail;
   const size_t slab = (size_t)K1S_SR * ldv * 8;
-  const size_t fixed = k1p_fixed_bytes(table[e].KH, ntm, cw);
+  const int NPR = specialised ? K1Q_PAIRS : K1P_PAIRS;
+  const size_t fixed = specialised ? k1q_fixed_bytes(table[e].KH, ntm, cw)
+                                   : k1p_fixed_bytes(table[e].KH, ntm, cw);
   const size_t budget = 227 * 1024 - 1024 - fixed;
-  int SP = (int)(budget / ((size_t)K1P_PAIRS * (slab + 8)));
+  int SP = (int)(budget / ((size_t)NPR * (slab + 8)));
   if (SP > 4) SP = 4;
   if (SP < 2) return false;
-  const size_t ring_bytes = (size_t)K1P_PAIRS * SP * slab;
-  const size_t stage_need = ((size_t)K1P_PAIRS * MT * 8 * cw + (size_t)2 * K1P_PAIRS * cw) * 8;
+  const size_t ring_bytes = (size_t)NPR * SP * slab;
+  const size_t stage_need = ((size_t)NPR * MT * 8 * cw + (size_t)2 * NPR * cw) * 8;
   if (ring_bytes < stage_need) return false;
-  size_t smem = ring_bytes + fixed + 8 * (size_t)K1P_PAIRS * (SP + 4);
+  size_t smem = ring_bytes + fixed + 8 * (size_t)NPR * (SP + 4);
   const int tail_off = 0;   // the tail pieces are formed by the finishing kernels now
   if (!attr[e].exchange(true)) {
     if (cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -18,9 +18,12 @@
 
 namespace mcp {
 
-constexpr int K1Q_PAIRS = 6;
+#ifndef MCP_K1Q_PAIRS
+#define MCP_K1Q_PAIRS 6        // warp pairs per CTA (6: 3 warps per sub-partition, ring of 2)
+#endif
+constexpr int K1Q_PAIRS = MCP_K1Q_PAIRS;
 constexpr int K1Q_THREADS = 2 * K1Q_PAIRS * 32;
-constexpr int K1Q_MAXREG = 168;
+constexpr int K1Q_MAXREG = (65536 / K1Q_THREADS) > 255 ? 255 : ((65536 / K1Q_THREADS) & ~7);
 #ifndef MCP_K1Q_ODD_CHAINS
 #define MCP_K1Q_ODD_CHAINS 0   // 1: GEMM1 with separate even / odd k-step chains (no gain)
 #endif

@@ -84,7 +84,6 @@ void drop_graphs(mcp_ctx* c) {
     if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
   }
   c->graphs.clear();
-  c->tail_x = nullptr;
   if (c->lbfgs_ws) {
     c->lbfgs_ws_free(c->lbfgs_ws);
     c->lbfgs_ws = nullptr;
@@ -364,10 +363,6 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   if ((rc = ensure(c, c->dwpart, sizeof(double) * pl.k1.wpart_elems))) return rc;
   if ((rc = ensure(c, c->dG, sizeof(double) * (size_t)r * r))) return rc;
   if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
-  if (k1_fuses_tail(pl.k1, c->n, r)) {
-    if ((rc = ensure(c, c->dM, sizeof(double) * (size_t)n * r))) return rc;
-    if ((rc = ensure(c, c->du, sizeof(double) * (size_t)r))) return rc;
-  }
   return MCP_OK;
 }
 
@@ -418,7 +413,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
 
 // prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows.
 int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
-                    cudaStream_t s, bool tail_pieces, const K3Signal* signal) {
+                    cudaStream_t s, const K3Signal* signal) {
   if (pl.mode == MCP_MODE_TF32X3) {
     int rc = enqueue_partial_tf32(c, pl, dx, dYw, s);
     if (rc || !signal) return rc;
@@ -428,9 +423,6 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   }
   const K1Variant& v = pl.k1;
   const int n = (int)c->n, r = pl.r;
-  // the finishing kernels (K3F, the peer reduce) form M and u themselves now; K1 never does
-  (void)tail_pieces;
-  const bool tp = false;
   int launches = 2;
   if (v.needs_prep()) {
     k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(
@@ -440,17 +432,13 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   auto* ev = timing_begin(c, s);
   int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r,
                      (const double*)c->dAfrag.p, pl.d, (double*)c->dYpart.p, (double*)c->dwpart.p,
-                     s, tp ? dx : nullptr, tp ? (double*)c->dM.p : nullptr,
-                     tp ? (double*)c->du.p : nullptr);
+                     s);
   timing_end(ev, s);
   if (rc) {
     const cudaError_t e = cudaGetLastError();
     return c->fail(MCP_ERR_CUDA, std::string("K1 launch failed (") + v.name + "): " +
                                      cudaGetErrorString(e));
   }
-  c->tail_x = tp ? dx : nullptr;   // M, u valid for this x until the next partial
-  c->tail_d = pl.d;
-  c->tail_r = r;
   const int64_t red_blocks = (int64_t)v.rbs * ceil_div((int64_t)n * v.RB, K3_X) +
                              ceil_div((int64_t)v.rbs * v.RB, K3W_X);
   {
@@ -509,17 +497,6 @@ int enqueue_finish_yw(mcp_ctx* c, int d, int r, const double* dx, const double* 
 
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
-  if (c->tail_x && c->tail_x == dx && c->tail_d == d && c->tail_r == r &&
-      !getenv("MCP_NO_FUSED_TAIL")) {
-    // M and u came with the partial: the finish is elementwise (K4L)
-    const int n = (int)c->n;
-    k_finish_light<<<(int)ceil_div((int64_t)n * r, 256) + 1, 256, 0, s>>>(
-        dx, dYw, dYw + (int64_t)n * r, (const double*)c->dM.p, (const double*)c->du.p, n, r, d,
-        alpha_dev, alpha, dout);
-    CUDA_TRY(c, cudaGetLastError());
-    c->last_launches += 1;
-    return MCP_OK;
-  }
   return enqueue_finish_yw(c, d, r, dx, dYw, dYw + c->n * r, alpha_dev, alpha, dout, s);
 }
 
@@ -546,7 +523,7 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
                     double alpha, double* dout, cudaStream_t s) {
   const int r = pl.r;
   if (pl.mode != MCP_MODE_FP64 || !k1_fuses_tail(pl.k1, c->n, r) || getenv("MCP_NO_FUSED_TAIL")) {
-    int rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s, false);
+    int rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s);
     if (rc) return rc;
     return enqueue_finish(c, pl.d, r, dx, (const double*)c->dYw.p, alpha_dev, alpha, dout, s);
   }
@@ -555,7 +532,7 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
   auto* ev = timing_begin(c, s);
   // the tail pieces (G, C, M, u) are formed by K3F itself, overlapping K1's drain
   int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r, nullptr, pl.d,
-                     (double*)c->dYpart.p, (double*)c->dwpart.p, s, nullptr, nullptr, nullptr);
+                     (double*)c->dYpart.p, (double*)c->dwpart.p, s);
   timing_end(ev, s);
   if (rc) {
     const cudaError_t e = cudaGetLastError();
@@ -766,7 +743,7 @@ void release_ctx(mcp_ctx* c) {
   drop_graphs(c);
   DevBuf* bufs[] = {&c->dx, &c->dout, &c->dYw, &c->dAfrag, &c->dYpart, &c->dwpart,
                     &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag, &c->dAt,
-                    &c->dM, &c->du, &c->dticket};
+                    &c->dticket};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->own_v32 && c->dV32) cudaFree(c->dV32);
@@ -1027,7 +1004,7 @@ int mcp_fg_partial_device(mcp_ctx* c, int d, int r, const double* dx, int mode, 
   int rc = plan_eval(c, d, r, mode, pl);
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
-  return enqueue_partial(c, pl, dx, dYw, s, true);
+  return enqueue_partial(c, pl, dx, dYw, s);
 }
 
 int mcp_fg_partial_signal_device(mcp_ctx* c, int d, int r, const double* dx, int mode,
@@ -1046,7 +1023,7 @@ int mcp_fg_partial_signal_device(mcp_ctx* c, int d, int r, const double* dx, int
   sig.rank = rank;
   sig.world = world;
   sig.epoch = epoch;
-  return enqueue_partial(c, pl, dx, dYw, s, false, &sig);
+  return enqueue_partial(c, pl, dx, dYw, s, &sig);
 }
 
 int mcp_fg_finish_device(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,

@@ -46,10 +46,7 @@ struct mcp_ctx {
   double nu_const = 0.0;
 
   mcp_internal::DevBuf dx, dout, dYw, dAfrag, dYpart, dwpart, dG, dC, dpart, dscalar, dflag;
-  mcp_internal::DevBuf dM, du;  // (unused since the finishing kernels form M, u themselves)
   mcp_internal::DevBuf dticket;  // K3 last-block ticket of the fused peer publication
-  const double* tail_x = nullptr;  // x whose M, u are in dM / du (set by a tail-piece partial)
-  int tail_d = 0, tail_r = 0;
   void* hx = nullptr;
   size_t hx_bytes = 0;
   void* hout = nullptr;
@@ -134,11 +131,10 @@ int ensure(mcp_ctx* c, DevBuf& b, size_t bytes);
 int ensure_host(mcp_ctx* c, void*& p, size_t& have, size_t bytes);
 int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl);
 // prep -> K1 -> K3 : dYw = [vec_F(Y) ; w] for the loaded rows (stream-ordered, capturable).
-// tail_pieces: ignored (the finishing kernels form M and u).  signal: K3 also publishes the
-// reduced piece to the peers' flags (multi-GPU exchange) once all of it is written.
+// signal: K3 also publishes the reduced piece to the peers' flags (multi-GPU exchange) once
+// all of it is written.
 int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
-                    cudaStream_t s, bool tail_pieces = false,
-                    const mcp::K3Signal* signal = nullptr);
+                    cudaStream_t s, const mcp::K3Signal* signal = nullptr);
 // K4 : out = [f ; g_lam ; vec_F(g_A)] from x = [lam ; vec_F(A)] and [Y ; w]
 int enqueue_finish(mcp_ctx* c, int d, int r, const double* dx, const double* dYw,
                    const double* alpha_dev, double alpha, double* dout, cudaStream_t s);

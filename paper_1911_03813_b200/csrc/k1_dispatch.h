@@ -28,21 +28,19 @@ struct K1Variant {
   int stages = 0;      // ring depth (kind 1)
   int MT = 0;          // GEMM2 m-tiles (kind 1)
   int MTW2 = 1;        // slabs per TMA copy unit (kind 1)
-  int tail_off = 0;    // K1Q: byte offset of the fused-tail scratch in dynamic smem (0: none)
   bool needs_prep() const { return kind == 0 || kind == 5; }
 };
 
 // Choose the variant for (dtype, n, r, p_pad) on a device with `sms` SMs.
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v, std::string& why);
 
-// Launch K1 on stream s; returns 0 on success.  tail_lam / tail_M / tail_u (K1P only, r <= 32)
-// make the kernel also produce M = (A o lam) C and u = (G o C) lam for k_reduce_finish.
+// Launch K1 on stream s; returns 0 on success.
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
-              double* wpart, cudaStream_t s, const double* tail_lam = nullptr,
-              double* tail_M = nullptr, double* tail_u = nullptr);
+              double* wpart, cudaStream_t s);
 
-// True when K1 variant v can run the fused tail (K1P, r <= 32, A and G fit the P staging).
+// True when the evaluation can end with the one-kernel reduce + finish K3F (prep-free FP64 K1,
+// r <= 32, every w in K3F's w block).
 bool k1_fuses_tail(const K1Variant& v, int64_t n, int r);
 
 // Row pitch (elements) the observation upload uses for dtype / n.

@@ -272,7 +272,6 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   const size_t stage_need = ((size_t)NPR * MT * 8 * cw + (size_t)2 * NPR * cw) * 8;
   if (ring_bytes < stage_need) return false;
   size_t smem = ring_bytes + fixed + 8 * (size_t)NPR * (SP + 4);
-  const int tail_off = 0;   // the tail pieces are formed by the finishing kernels now
   if (!attr[e].exchange(true)) {
     if (cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
@@ -284,7 +283,6 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
     cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   v.kind = specialised ? 4 : 3;
-  v.tail_off = tail_off;
   v.dtype = MCP_F64;
   v.RB = cw;
   v.MTW = table[e].MTH;
@@ -460,8 +458,7 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
 
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
-              double* wpart, cudaStream_t s, const double* tail_lam, double* tail_M,
-              double* tail_u) {
+              double* wpart, cudaStream_t s) {
   if (v.entry < 0) return 1;
   if (v.kind == 1 || v.kind == 3 || v.kind == 4) {
     K1SParams sp;
@@ -481,12 +478,6 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     sp.spc = v.MTW2;
     sp.Ypart = Ypart;
     sp.wpart = wpart;
-    if ((v.kind == 3 || v.kind == 4) && tail_lam) {
-      sp.lam = tail_lam;
-      sp.M = tail_M;
-      sp.u = tail_u;
-      sp.tail_off = v.kind == 4 ? v.tail_off : 0;
-    }
     (v.kind == 1 ? kTableS : v.kind == 3 ? kTableP : kTableQ)[v.entry].launch(sp, v.grid, v.smem,
                                                                                s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;

@@ -40,61 +40,6 @@ __host__ __device__ inline size_t k1p_fixed_bytes(int kh, int ntm, int cw) {
          (size_t)K1P_PAIRS * 2 * K1S_SR * k1s_pp(cw) * 8;
 }
 
-// A (n x r) and then G = A^T A, C = G^(d-1) in smem scratch (warp per entry, lanes over rows,
-// fixed butterfly -- the order of k_tail_fused), then this CTA's rows of M = (A o lam) C and,
-// in CTA 0, u = (G o C) lam.  The caller guarantees n r + r^2 <= scratch capacity.  Runs on
-// `nthr` threads (thread index tid) that synchronise with named barrier `bar` (0: the CTA).
-__device__ __forceinline__ void k1p_tail_pre(const K1SParams& prm, double* scratch, int tid = -1,
-                                             int nthr = 0, int bar = 0) {
-  if (tid < 0) {
-    tid = threadIdx.x;
-    nthr = blockDim.x;
-  }
-  auto sync = [&]() {
-    if (bar == 0)
-      __syncthreads();
-    else
-      asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(nthr) : "memory");
-  };
-  const int n = prm.n, r = prm.r, d = prm.d;
-  const double* lam = prm.lam;
-  double* sA = scratch;           // n x r column-major
-  double* sC = scratch + n * r;   // G, then C
-  const int warp = tid >> 5, lane = tid & 31, nw = nthr >> 5;
-  for (int e = tid; e < n * r; e += nthr) sA[e] = prm.A[e];
-  sync();
-  for (int pr = warp; pr < r * r; pr += nw) {
-    const int j = pr / r, k = pr % r;
-    double s = 0.0;
-    for (int i = lane; i < n; i += 32) s += sA[j * n + i] * sA[k * n + i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) sC[pr] = s;
-  }
-  sync();
-  if (blockIdx.x == 0) {
-    for (int j = tid; j < r; j += nthr) {
-      double u = 0.0;
-      for (int k = 0; k < r; ++k) {
-        const double gjk = sC[j * r + k];
-        u += (gjk * rm_pow(gjk, d - 1)) * lam[k];
-      }
-      prm.u[j] = u;
-    }
-  }
-  sync();
-  for (int e = tid; e < r * r; e += nthr) sC[e] = rm_pow(sC[e], d - 1);
-  sync();
-  const int per = (n + gridDim.x - 1) / gridDim.x;
-  const int i0 = min(n, (int)blockIdx.x * per), i1 = min(n, i0 + per);
-  for (int e = tid; e < (i1 - i0) * r; e += nthr) {
-    const int j = e / (i1 - i0), i = i0 + e % (i1 - i0);
-    double m = 0.0;
-    for (int k = 0; k < r; ++k) m += (sA[k * n + i] * lam[k]) * sC[k * r + j];
-    prm.M[(int64_t)j * n + i] = m;
-  }
-}
-
 template <int NTM, int TAIL, int MTH, int KH>
 __global__ void __maxnreg__(K1P_MAXREG) k1p_fg_pairs(K1SParams prm) {
   constexpr int CW = 8 * NTM + TAIL;
@@ -161,13 +106,6 @@ __global__ void __maxnreg__(K1P_MAXREG) k1p_fg_pairs(K1SParams prm) {
                    &my_full[s]);
     }
   }
-  // Y-independent tail pieces (reference implicit.py:147-149, objective.py:55) while the first
-  // slabs are in flight; the P staging area is free until the first epilogue.
-  if (prm.lam) {
-    k1p_tail_pre(prm, sP);
-    __syncthreads();
-  }
-
   const int mbase = h * MTH;
   const int mcnt = h == 0 ? min(MTH, prm.MT) : max(0, prm.MT - MTH);
   double yacc[MTH][NTM][2];

@@ -159,10 +159,6 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     }
   }
   __syncthreads();
-  if (prm.lam && prm.tail_off == 0) {
-    k1p_tail_pre(prm, sP);
-    __syncthreads();
-  }
   const int dm1 = prm.d - 1;
   const int MT = prm.MT;
 #if MCP_K1Q_PROF
@@ -335,11 +331,6 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
     }
   } else {
     // ================= GEMM2 warp: Y over all m-tiles, ring refills =================
-    if (prm.lam && prm.tail_off) {
-      // the fused tail's pieces, on the six GEMM2 warps while the GEMM1 warps run slab 0
-      k1p_tail_pre(prm, reinterpret_cast<double*>(smem_raw + prm.tail_off), 32 * q + lane,
-                   32 * NP, 1);
-    }
     double yacc[MT2][NTM][2];
     double ytl[MT2][TL];
 #pragma unroll

@@ -42,13 +42,6 @@ struct K1SParams {
   int stages;            // ring depth in copy units
   double* Ypart;         // [rbs][gp][MT*8][CW]
   double* wpart;         // [rbs][gp][CW]
-  // K1P only: when lam != nullptr the kernel also computes the Y-independent tail pieces
-  // M = (A o lam) C (n x r column-major, rows split across CTAs) and, in CTA 0,
-  // u = (G o C) lam, for the fused reduce + finish (k_reduce_finish).  r <= 32.
-  const double* lam = nullptr;
-  double* M = nullptr;
-  double* u = nullptr;
-  int tail_off = 0;      // K1Q: dedicated smem scratch for the tail pieces (0: use P staging)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -197,34 +197,6 @@ __global__ void __launch_bounds__(K3_T)
   }
 }
 
-// K4L: the finish when M = (A o lam) C and u = (G o C) lam are already known (they came with the
-// partial): g_A = -2d (Y - M) o lam elementwise, the last block g_lam and f.  Same expressions
-// as k_tail_fused / k_reduce_finish.
-__global__ void k_finish_light(const double* __restrict__ x, const double* __restrict__ Y,
-                               const double* __restrict__ w, const double* __restrict__ M,
-                               const double* __restrict__ u, int n, int r, int d,
-                               const double* __restrict__ alpha_dev, double alpha_host,
-                               double* __restrict__ out) {
-  const double* lam = x;
-  const int64_t nr = (int64_t)n * r;
-  if (blockIdx.x + 1 < gridDim.x) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e < nr) {
-      const int j = (int)(e / n);
-      out[1 + r + e] = ((-2.0 * d) * (Y[e] - M[e])) * lam[j];
-    }
-    return;
-  }
-  for (int j = threadIdx.x; j < r; j += blockDim.x) out[1 + j] = -2.0 * (w[j] - u[j]);
-  if (threadIdx.x == 0) {
-    double lu = 0.0, wl = 0.0;
-    for (int j = 0; j < r; ++j) lu += lam[j] * u[j];
-    for (int j = 0; j < r; ++j) wl += w[j] * lam[j];
-    const double alpha = alpha_dev ? *alpha_dev : alpha_host;
-    out[0] = alpha + lu - 2.0 * wl;
-  }
-}
-
 // K4a: G = A^T A and C = G^(d-1) (implicit.py:147-148), row-major r x r.  One warp per upper
 // triangle entry (j <= k): lanes stride over the n rows of the two columns (coalesced), then a
 // fixed butterfly; the value is mirrored so G is exactly symmetric.  Launch with 256-thread

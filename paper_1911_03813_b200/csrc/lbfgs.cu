@@ -638,7 +638,7 @@ struct LbEngine {
   int enqueue_fg() {
     cudaStream_t s = c->stream;
     if (k == 1) return enqueue_fg_full(c, pl, D.T, nullptr, alpha, D.OT, s);
-    int rc = enqueue_partial(c, pl, D.Xb, Ywb, s, false);
+    int rc = enqueue_partial(c, pl, D.Xb, Ywb, s);
     if (rc) return rc;
     const int64_t R = (int64_t)k * r;
     return enqueue_tails_batched(c, d, r, k, D.T, N, Ywb, Ywb + n * R, alpha, D.OT, N + 1, s);

@@ -4,13 +4,14 @@
 // Every rank's partial lives in a symmetric (peer-mapped) buffer, two slots by epoch parity.
 //   mcp_peer_signal:          after this rank's partial is complete (stream order), publish
 //                             `epoch` into every rank's flag array at index `rank`
-//                             (threadfence.system + st.release.sys);
+//                             (threadfence.system + st.release.sys); mcp_fg_partial_signal_device
+//                             does the same from the last block of the partial's reduce (K3);
 //   mcp_peer_reduce_finish:   wait until every rank's flag for this epoch is set (ld.acquire.sys,
 //                             bounded), sum the W partials in rank order 0..W-1 straight from
-//                             peer memory, and finish: with the tail pieces M, u of this rank's
-//                             partial the finish is elementwise (g_A = -2d (Y - M) o lam,
-//                             g_lam = -2 (w - u), f), otherwise the summed piece goes through the
-//                             regular tail.  Every rank sums in the same order, so all ranks hold
+//                             peer memory, and finish: for r <= 32 the kernel forms G, C (and
+//                             the M, u entries it needs) from x while it waits, so the finish is
+//                             elementwise (g_A = -2d (Y - M) o lam, g_lam = -2 (w - u), f);
+//                             otherwise the summed piece goes through the regular tail.  Every rank sums in the same order, so all ranks hold
 //                             bitwise identical f and gradients.
 // Slot reuse is safe with two slots: a rank overwrites slot e % 2 at epoch e + 2 only after
 // its own reduce of epoch e + 1 saw every peer's epoch e + 1 flag, i.e. after every peer
@@ -177,7 +178,6 @@ extern "C" int mcp_peer_reduce_finish(mcp_ctx* c, int d, int r, const double* dx
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches = 1;
   if (!light) {
-    c->tail_x = nullptr;
     return enqueue_finish(c, d, r, dx, (const double*)c->dYw.p, nullptr, alpha, dout, s);
   }
   return MCP_OK;

@@ -334,9 +334,10 @@ def test_batched_matches_single_starts(n, p, r, d, k):
 
 
 def test_partial_then_finish_equals_single_evaluation_bitwise():
-    """The sharded building blocks on one rank: partial (K1 + reduce, leaving M and u when the
-    kernel fuses the tail) then finish must reproduce the single-call evaluation bitwise, with
-    and without the fused tail (both compute G, C, M, u and the finish in the same order)."""
+    """The sharded building blocks on one rank: partial (K1 + reduce) then finish (K4) must
+    reproduce the single-call evaluation bitwise, with and without the fused reduce + finish
+    (K3F forms G, C, M, u in-kernel in the same expression order as K4), over orders d and
+    ranks up to K3F's limit r = 32."""
     import os
 
     import torch
@@ -344,7 +345,8 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
     from paper_1911_03813_b200 import _native
 
     rng = np.random.default_rng(21)
-    for n, r in ((20, 5), (100, 10), (64, 16), (30, 20)):
+    for n, r, d in ((20, 5, 3), (100, 10, 4), (64, 16, 6), (30, 20, 3), (128, 32, 2),
+                    (100, 32, 5)):
         V = rng.standard_normal((n, 3000))
         lam, A = rng.standard_normal(r), rng.standard_normal((n, r))
         obs = mcp.ObservationSet(V)
@@ -359,16 +361,16 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
                 Yw = torch.empty(n * r + r, dtype=torch.float64, device="cuda")
                 o1 = torch.empty(1 + r + n * r, dtype=torch.float64, device="cuda")
                 o2 = torch.empty_like(o1)
-                ctx.fg_partial_device(3, r, x.data_ptr(), None, Yw.data_ptr(), s)
-                ctx.fg_finish_device(3, r, x.data_ptr(), Yw.data_ptr(), 0.25, o1.data_ptr(), s)
-                ctx.fg_device(3, r, x.data_ptr(), 0.25, None, o2.data_ptr(), s)
+                ctx.fg_partial_device(d, r, x.data_ptr(), None, Yw.data_ptr(), s)
+                ctx.fg_finish_device(d, r, x.data_ptr(), Yw.data_ptr(), 0.25, o1.data_ptr(), s)
+                ctx.fg_device(d, r, x.data_ptr(), 0.25, None, o2.data_ptr(), s)
                 torch.cuda.synchronize()
-                assert torch.equal(o1, o2), (n, r, fused)
+                assert torch.equal(o1, o2), (n, r, d, fused)
                 outs.append(o1.cpu())
             finally:
                 os.environ.pop("MCP_NO_FUSED_TAIL", None)
-        assert torch.equal(outs[0], outs[1]), (n, r)
-        res = mcp.fg_implicit(obs, lam, A, 3, 0.25)
+        assert torch.equal(outs[0], outs[1]), (n, r, d)
+        res = mcp.fg_implicit(obs, lam, A, d, 0.25)
         assert float(outs[0][0]) == res.f
 
 

@@ -173,7 +173,8 @@ def run_reference(args, cfg, rank, world):
     evals = 1.0 / (sum(times) / len(times) * scale)
     threads = _blas_threads()
     line = {
-        "metric": "f+grad evals/s", "value": evals, "unit": "evals/s", "n_gpus": 0,
+        "metric": "f+grad evals/s", "value": evals, "unit": "evals/s", "n_gpus": world,
+        "devices": "host cores only (the reference is CPU-only; n_gpus = the N it was launched at)",
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / evals, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "impl": "reference",

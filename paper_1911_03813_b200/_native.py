@@ -108,7 +108,12 @@ def load_library():
                 )
             lib = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
-                fn = getattr(lib, name)
+                # an A/B build selected with MCP_LIBRARY may predate newer entry points
+                fn = getattr(lib, name, None)
+                if fn is None and os.environ.get("MCP_LIBRARY"):
+                    continue
+                if fn is None:
+                    raise RuntimeError(f"{LIB_PATH} does not export {name}")
                 fn.restype = res
                 fn.argtypes = args
             _lib = lib

@@ -323,7 +323,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
                 std::to_string(RB) + ",S=" + std::to_string(ns) +
                 (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
-                             (t.hint ? ",l2hint" : "") + (t.g2_3d ? ",g2tma3d" : "") + ",flush=" + std::to_string(t.flush)
+                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (getenv("MCP_K1T2_G2X2") && atoi(getenv("MCP_K1T2_G2X2")) != 0 ? ",g2x2" : "") + ",flush=" + std::to_string(t.flush)
                       : std::string()) +
                 ">";
   return MCP_OK;
@@ -393,6 +393,9 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.hint = t.hint ? 1 : 0;
   prm.flush = t.flush;
   prm.g2_3d = t.g2_3d ? 1 : 0;
+  // opt-in: GEMM2 as V P_hi with P_hi rounded to nearest (8-9% faster at c3 / c5, but normwise
+  // error up to 7e-5 at reduced p -- too close to the stated 1e-4 to be the default)
+  prm.g2x2 = getenv("MCP_K1T2_G2X2") && atoi(getenv("MCP_K1T2_G2X2")) != 0 ? 1 : 0;
   auto* ev = timing_begin(c, s);
   if (t.v2)
     k1t2_fg_tf32<<<t.gp * t.rbs, K1T2_THREADS, t.smem, s>>>(

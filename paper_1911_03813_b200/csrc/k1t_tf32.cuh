@@ -56,6 +56,8 @@ struct K1TParams {
   int hint = 0;       // K1T2: L2 policy -- GEMM1's V reads evict_last, everything else evict_first
   int flush = 8;      // K1T2: tiles accumulated in fp32 TMEM between fp64 flushes
   int g2_3d = 0;      // K1T2: tm_v2 / tm_l2 are 3-D chunk maps (one TMA per 16 KB operand)
+  int g2x2 = 0;       // K1T2: GEMM2 as V P_hi (2 products) with P_hi rounded to nearest; the
+                      // dropped V_hi P_lo term is unbiased and <= 2^-12 of each product
 };
 
 __host__ __device__ constexpr size_t k1t_stage_bytes(int RB) { return 2 * K1T_VBYTES + 256 * RB; }
@@ -588,6 +590,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             const uint64_t boff = (uint64_t)((rc * 128 * RB) >> 4);
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
+              if (pr == 1 && prm.g2x2) continue;
               const uint64_t av = pr == 2 ? dvl : dvh;
               const uint64_t bv = (pr == 1 ? dpl : dph) + boff;
 #pragma unroll
@@ -714,7 +717,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
             const float pf = (float)(nul * pw[jj]);
-            const float ph = tf32_hi(pf);
+            const float ph = prm.g2x2 ? tf32_rna(pf) : tf32_hi(pf);
             const uint32_t off = brick * 128 * RB + brick_off(c0 + jj, col);
             *reinterpret_cast<float*>(sPh + off) = ph;
             *reinterpret_cast<float*>(sPl + off) = pf - ph;

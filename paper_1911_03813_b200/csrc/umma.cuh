@@ -189,5 +189,11 @@ __host__ __device__ constexpr uint32_t brick32_off(uint32_t row, uint32_t col) {
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
+// Round-to-nearest (ties away) TF32 value of x: x - tf32_rna(x) is unbiased, |.| <= 2^-12 |x|.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
 }  // namespace mcp

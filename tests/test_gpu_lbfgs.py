@@ -191,3 +191,40 @@ def test_multistart_lbfgs_semantics_and_failures():
     assert not isinstance(reps[0], Exception) and not isinstance(reps[2], Exception)
     one = mcp.lbfgs_minimize(fg, X0[2], oc)
     assert abs(reps[2].f - one.f) <= 1e-9 * abs(one.f)
+
+
+def test_c2_full_size_fit_replay():
+    """BASELINE configs[1] at full size (p = 1e6, the bench workload): the device L-BFGS fit,
+    replayed against the CPU oracle (SURVEY.md 8c protocol).  At every accepted iterate the
+    oracle's f and gradient agree with the device's to 1e-10 in the reference's term-scale
+    metric, and the restated reference solver driven by the ORACLE f+grad takes the same steps
+    for the opening iterates."""
+    from paper_1911_03813_b200 import synth
+
+    cfg = synth.CONFIGS["c2"]
+    V = synth.host_observations(cfg, 2, p=cfg.p)
+    lam, A = synth.initial_point(cfg, 2)
+    x0 = om.pack(lam, A)
+    obs = mcp.ObservationSet(V)
+    fg = mcp.packed_fg_implicit(obs, cfg.d, cfg.r)
+    its = []
+    steps = 6
+    rep = mcp.lbfgs_minimize(fg, x0, mcp.OptConfig(max_iters=steps, pgtol=1e-12),
+                             shape=(cfg.n, cfg.r), iterate_hook=its.append)
+    assert rep.n_steps >= 3
+    nu = np.full(cfg.p, 1.0 / cfg.p)
+    for k, x in enumerate(its):
+        l_k, A_k = om.unpack(x, cfg.n, cfg.r)
+        f, gl, gA = om.fg_implicit(V, nu, l_k, A_k, cfg.d, 0.0)
+        f_s, gl_s, gA_s, _ = om.term_scales(V, nu, l_k, A_k, cfg.d, 0.0)
+        fd, gd = fg(x)
+        gd_l, gd_A = gd[:cfg.r], gd[cfg.r:].reshape((cfg.n, cfg.r), order="F")
+        e = max(om.term_rel_err(fd, f, f_s), om.term_rel_err(gd_l, gl, gl_s),
+                om.term_rel_err(gd_A, gA, gA_s))
+        assert e <= 1e-10, (k, e)
+    # the reference solver on the oracle's f+grad, step for step over the opening iterates
+    ref_its = []
+    lo.lbfgs(om.packed_fg(V, nu, cfg.d, cfg.r), x0, pgtol=1e-12, max_iters=3,
+             iterate_hook=ref_its.append)
+    for k in range(min(len(ref_its), 4)):
+        assert np.allclose(its[k], ref_its[k], rtol=1e-9, atol=1e-12), k

@@ -214,6 +214,8 @@ __global__ void k_tail_gram(const double* __restrict__ x, int n, int r, int d,
     const double* aj = A + (int64_t)j * n;
     const double* ak = A + (int64_t)k * n;
     double s = 0.0;
+    // unrolled so the loads of several trips are in flight (same sequential sum order)
+#pragma unroll 8
     for (int i = lane; i < n; i += 32) s += aj[i] * ak[i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -263,6 +265,7 @@ __global__ void k_tail_ga(const double* __restrict__ x, const double* __restrict
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int j = idx / n, i = idx % n;
     double m = 0.0;
+#pragma unroll 8
     for (int k = 0; k < r; ++k) m += (A[(int64_t)k * n + i] * lam[k]) * C[(int64_t)k * r + j];
     out[1 + r + idx] = (s * (Y[idx] - m)) * lam[j];
   }

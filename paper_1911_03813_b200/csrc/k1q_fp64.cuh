@@ -28,7 +28,7 @@ constexpr int K1Q_MAXREG = (65536 / K1Q_THREADS) > 255 ? 255 : ((65536 / K1Q_THR
 #define MCP_K1Q_ODD_CHAINS 0   // 1: GEMM1 with separate even / odd k-step chains (no gain)
 #endif
 #ifndef MCP_K1Q_EXP_NOMATH
-#define MCP_K1Q_EXP_NOMATH 0   // timing experiment only: bit 0 skips GEMM1, bit 1 GEMM2 (wrong results)
+#define MCP_K1Q_EXP_NOMATH 0   // timing experiment only: bit 0 skips GEMM1, bit 1 GEMM2, bit 2 GEMM1's DFMA tail (wrong results)
 #endif
 #ifndef MCP_K1Q_PROF
 #define MCP_K1Q_PROF 0         // diagnostics only: CTAs 0 and gridDim-1 print phase clocks
@@ -228,7 +228,7 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
             dmma884(z[1][nt], a1c, b_c[nt]);
           }
         }
-        if constexpr (TAIL > 0) {
+        if constexpr (TAIL > 0 && !(MCP_K1Q_EXP_NOMATH & 4)) {
           zt[0][0] = fma(a0c, t_c.x, zt[0][0]);
           zt[1][0] = fma(a1c, t_c.x, zt[1][0]);
           if constexpr (TAIL > 1) {

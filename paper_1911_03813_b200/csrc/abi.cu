@@ -5,6 +5,7 @@
 // (d, r, mode) that replays  H2D(x) -> prep -> K1 -> K3 -> K4 -> D2H(f, g)  with one sync.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -475,13 +476,35 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   return MCP_OK;
 }
 
+// k_tail_fused stages A in dynamic shared memory (beyond the 48 KB default for large n r)
+static bool k4s_ready(int64_t nr) {
+  static std::atomic<int> done{0};
+  if (!done.load()) {
+    if (cudaFuncSetAttribute(k_tail_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k4s_smem_bytes(K4S_MAX_NR)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return k4s_smem_bytes(nr) <= 48 * 1024;
+    }
+    done.store(1);
+  }
+  return true;
+}
+
+// one-CTA tail for small factor blocks; else the three-kernel tail (measured: at n r = 5000 the
+// single CTA is ~10 us slower than the three parallel kernels)
+static bool k4s_fits(int64_t n, int r) {
+  const int64_t nr = n * r;
+  return nr <= K4S_MAX_NR && r <= K4S_MAX_R && k4s_ready(nr);
+}
+
 // K4: tail from (x, Y, w) -> out = [f ; g_lam ; vec_F(g_A)].
 int enqueue_finish_yw(mcp_ctx* c, int d, int r, const double* dx, const double* dY,
                       const double* dw, const double* alpha_dev, double alpha, double* dout,
                       cudaStream_t s) {
   const int n = (int)c->n;
-  if ((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) {
-    k_tail_fused<<<1, K4S_THREADS, 0, s>>>(dx, dY, dw, n, r, d, alpha_dev, alpha, dout);
+  if (k4s_fits(n, r)) {
+    k_tail_fused<<<1, K4S_THREADS, k4s_smem_bytes((int64_t)n * r), s>>>(dx, dY, dw, n, r, d,
+                                                                        alpha_dev, alpha, dout);
     CUDA_TRY(c, cudaGetLastError());
     c->last_launches += 1;
     return MCP_OK;
@@ -507,9 +530,9 @@ int enqueue_tails_batched(mcp_ctx* c, int d, int r, int k, const double* xs, int
                           const double* Y, const double* w, double alpha, double* out, int64_t so,
                           cudaStream_t s) {
   const int64_t n = c->n, nr = n * r;
-  if (nr <= K4S_MAX_NR && r <= K4S_MAX_R) {
-    k_tail_fused<<<k, K4S_THREADS, 0, s>>>(xs, Y, w, (int)n, r, d, nullptr, alpha, out, sx, nr, r,
-                                           so);
+  if (k4s_fits(n, r)) {
+    k_tail_fused<<<k, K4S_THREADS, k4s_smem_bytes(nr), s>>>(xs, Y, w, (int)n, r, d, nullptr, alpha,
+                                                            out, sx, nr, r, so);
     CUDA_TRY(c, cudaGetLastError());
     c->last_launches += 1;
     return MCP_OK;
@@ -621,7 +644,7 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
         (pl.mode == MCP_MODE_FP64 && k1_fuses_tail(pl.k1, c->n, r) && !getenv("MCP_NO_FUSED_TAIL"))
             ? 2
             : (pl.mode == MCP_MODE_TF32X3 ? 4 : (pl.k1.needs_prep() ? 3 : 2)) +
-                  (((int64_t)n * r <= K4S_MAX_NR && r <= K4S_MAX_R) ? 1 : 3);
+                  (k4s_fits(n, r) ? 1 : 3);
     c->variant = pl.k1.name;
   }
   CUDA_TRY(c, cudaGraphLaunch(it->second.exec, c->stream));
@@ -1122,9 +1145,9 @@ int mcp_fg_batch(mcp_ctx* c, int d, int r, int k, const double* X, double alpha,
   const double* dY = (const double*)c->dYw.p;
   const double* dW = dY + n * R;
   const double* dXs = dx + R + n * R + 1;
-  if (n * r <= K4S_MAX_NR && r <= K4S_MAX_R) {
+  if (k4s_fits(n, r)) {
     // all k tails in one launch, one CTA per start
-    k_tail_fused<<<k, K4S_THREADS, 0, c->stream>>>(dXs, dY, dW, (int)n, r, d, dx + R + n * R, 0.0,
+    k_tail_fused<<<k, K4S_THREADS, k4s_smem_bytes(n * r), c->stream>>>(dXs, dY, dW, (int)n, r, d, dx + R + n * R, 0.0,
                                                    (double*)c->dout.p, rows, n * r, r, 1 + rows);
     CUDA_TRY(c, cudaGetLastError());
     c->last_launches = 1;

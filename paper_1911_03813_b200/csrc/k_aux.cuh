@@ -275,8 +275,11 @@ __global__ void k_tail_ga(const double* __restrict__ x, const double* __restrict
 // and g_A in a single launch, all intermediates in shared memory.  Same algebra and operation
 // order as the three-kernel tail above (implicit.py:147-149, objective.py:51-56).
 constexpr int K4S_THREADS = 512;
-constexpr int K4S_MAX_NR = 4096;
+constexpr int K4S_MAX_NR = 4096;    // A staged in (dynamic) shared memory
 constexpr int K4S_MAX_R = 32;
+__host__ __device__ constexpr size_t k4s_smem_bytes(int64_t nr) {
+  return sizeof(double) * ((size_t)nr + (size_t)K4S_MAX_R * K4S_MAX_R + K4S_MAX_R);
+}
 __global__ void __launch_bounds__(K4S_THREADS)
     k_tail_fused(const double* __restrict__ x, const double* __restrict__ Y,
                  const double* __restrict__ w, int n, int r, int d,
@@ -288,9 +291,10 @@ __global__ void __launch_bounds__(K4S_THREADS)
   Y += blockIdx.x * sy;
   w += blockIdx.x * sw;
   out += blockIdx.x * so;
-  __shared__ double sA[K4S_MAX_NR];
-  __shared__ double sC[K4S_MAX_R * K4S_MAX_R];
-  __shared__ double sU[K4S_MAX_R];
+  extern __shared__ double k4s_smem[];   // [K4S_MAX_R^2 C][K4S_MAX_R u][n r A]
+  double* sC = k4s_smem;
+  double* sU = sC + K4S_MAX_R * K4S_MAX_R;
+  double* sA = sU + K4S_MAX_R;
   const double* lam = x;
   for (int e = threadIdx.x; e < n * r; e += blockDim.x) sA[e] = x[r + e];
   __syncthreads();

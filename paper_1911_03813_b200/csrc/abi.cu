@@ -21,6 +21,7 @@
 #include "k1_fp64.cuh"
 #include "k5_gram.cuh"
 #include "k_aux.cuh"
+#include "pdl.h"
 #include "k1_dispatch.h"
 #include "k1t_tf32.cuh"
 #include "ctx.h"
@@ -429,8 +430,9 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   const int n = (int)c->n, r = pl.r;
   int launches = 2;
   if (v.needs_prep()) {
-    k_prep_afrag<<<grid_for(v.afrag_elems, 256, 4 * c->sms), 256, 0, s>>>(
-        dx + r, n, r, v.RB, v.rbs, v.n_chunks * 16, (double*)c->dAfrag.p);
+    CUDA_TRY(c, launch_pdl(k_prep_afrag, dim3(grid_for(v.afrag_elems, 256, 4 * c->sms)), dim3(256),
+                           0, s, dx + r, n, r, v.RB, v.rbs, v.n_chunks * 16,
+                           (double*)c->dAfrag.p));
     ++launches;
   }
   auto* ev = timing_begin(c, s);
@@ -503,19 +505,21 @@ int enqueue_finish_yw(mcp_ctx* c, int d, int r, const double* dx, const double* 
                       cudaStream_t s) {
   const int n = (int)c->n;
   if (k4s_fits(n, r)) {
-    k_tail_fused<<<1, K4S_THREADS, k4s_smem_bytes((int64_t)n * r), s>>>(dx, dY, dw, n, r, d,
-                                                                        alpha_dev, alpha, dout);
+    CUDA_TRY(c, launch_pdl(k_tail_fused, dim3(1), dim3(K4S_THREADS), k4s_smem_bytes((int64_t)n * r),
+                           s, dx, dY, dw, n, r, d, alpha_dev, alpha, dout, (int64_t)0, (int64_t)0,
+                           (int64_t)0, (int64_t)0));
     CUDA_TRY(c, cudaGetLastError());
     c->last_launches += 1;
     return MCP_OK;
   }
-  k_tail_gram<<<grid_for((int64_t)r * r, K4A_WARPS, 16 * c->sms), 32 * K4A_WARPS, 0, s>>>(
-      dx, n, r, d, (double*)c->dG.p, (double*)c->dC.p);
-  k_tail_vec<<<1, 256, sizeof(double) * r, s>>>(dx, dw, (const double*)c->dG.p,
-                                                (const double*)c->dC.p, n, r, alpha_dev, alpha,
-                                                dout);
-  k_tail_ga<<<grid_for((int64_t)n * r, 256, 8 * c->sms), 256, 0, s>>>(
-      dx, dY, (const double*)c->dC.p, n, r, d, dout);
+  CUDA_TRY(c, launch_pdl(k_tail_gram, dim3(grid_for((int64_t)r * r, K4A_WARPS, 16 * c->sms)),
+                         dim3(32 * K4A_WARPS), 0, s, dx, n, r, d, (double*)c->dG.p,
+                         (double*)c->dC.p));
+  CUDA_TRY(c, launch_pdl(k_tail_vec, dim3(1), dim3(256), sizeof(double) * r, s, dx, dw,
+                         (const double*)c->dG.p, (const double*)c->dC.p, n, r, alpha_dev, alpha,
+                         dout));
+  CUDA_TRY(c, launch_pdl(k_tail_ga, dim3(grid_for((int64_t)n * r, 256, 8 * c->sms)), dim3(256), 0,
+                         s, dx, dY, (const double*)c->dC.p, n, r, d, dout));
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 3;
   return MCP_OK;

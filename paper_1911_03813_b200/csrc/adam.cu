@@ -24,6 +24,7 @@
 
 #include "ctx.h"
 #include "mcp_common.cuh"
+#include "pdl.h"
 
 using namespace mcp;
 using namespace mcp_internal;
@@ -58,6 +59,7 @@ __global__ void k_adam_step(int64_t N, const double* __restrict__ out, double* _
                             double* __restrict__ m1, double* __restrict__ m2,
                             const double* __restrict__ bc, const double* __restrict__ lr_dev,
                             AdamScalars sc, int* __restrict__ it_dev, unsigned* counter) {
+  pdl_enter();   // the gradient comes from the preceding finish kernel
   const int it = *it_dev;
   const double bc1 = bc[2 * it], bc2 = bc[2 * it + 1];
   const double lr = *lr_dev;
@@ -208,8 +210,9 @@ struct AdamRun {
            int e = enqueue_gather(Vb, batch, idx, it_dev, vb->ldv);
            if (e) return e;
            if ((e = fg_on(vb, plb, X, OB))) return e;
-           k_adam_step<<<nb, AD_T, 0, s>>>(N, OB, X, M1, M2, bc, lr_dev, sc, it_dev, counter);
-           CUDA_TRY(c, cudaGetLastError());
+           CUDA_TRY(c, launch_pdl(k_adam_step, dim3(nb), dim3(AD_T), 0, s, N, (const double*)OB,
+                                  X, M1, M2, (const double*)bc, (const double*)lr_dev, sc, it_dev,
+                                  counter));
            return MCP_OK;
          })))
       return rc;

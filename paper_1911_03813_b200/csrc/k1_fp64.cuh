@@ -16,6 +16,7 @@
 #pragma once
 
 #include "mcp_common.cuh"
+#include "pdl.h"
 
 namespace mcp {
 
@@ -95,6 +96,7 @@ __device__ __forceinline__ void k1_load_a(double* dst, const double* __restrict_
 
 template <typename VT, int RB, int MTW>
 __global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
+  pdl_enter();   // the factor fragments come from the preceding prep kernel
   constexpr int NT = RB / 8;
   constexpr int SP = RB + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -267,6 +269,7 @@ __host__ __device__ constexpr size_t k1g_smem_bytes() {
 
 template <typename VT, int RB>
 __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
+  pdl_enter();   // the factor fragments come from the preceding prep kernel
   constexpr int NT = RB / 8;
   constexpr int SP = RB + 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -15,7 +15,7 @@ namespace {
 
 template <typename VT, int RB, int MTW>
 void launch_t(const K1Params& prm, int grid, size_t smem, cudaStream_t s) {
-  k1_fg_dmma<VT, RB, MTW><<<grid, K1_THREADS, smem, s>>>(prm);
+  launch_pdl(k1_fg_dmma<VT, RB, MTW>, dim3(grid), dim3(K1_THREADS), smem, s, prm);
 }
 
 using LaunchFn = void (*)(const K1Params&, int, size_t, cudaStream_t);
@@ -42,7 +42,7 @@ const Entry kTable[] = {MCP_K1_ROW(double, MCP_F64), MCP_K1_ROW(float, MCP_F32)}
 // K1G (Y partial in global memory): column blocks of RB in {16, 32, 64}
 template <typename VT, int RB>
 void launch_g(const K1Params& prm, int grid, size_t smem, cudaStream_t s) {
-  k1g_fg_dmma<VT, RB><<<grid, K1_THREADS, smem, s>>>(prm);
+  launch_pdl(k1g_fg_dmma<VT, RB>, dim3(grid), dim3(K1_THREADS), smem, s, prm);
 }
 #define MCP_K1G_E(VT, DT, RB) \
   {DT, RB, 0, &launch_g<VT, RB>, (const void*)&k1g_fg_dmma<VT, RB>, k1g_smem_bytes<VT, RB>()}

@@ -4,6 +4,7 @@
 
 #include "mcp_common.cuh"
 #include "tail_pieces.cuh"
+#include "pdl.h"
 
 namespace mcp {
 
@@ -12,6 +13,7 @@ namespace mcp {
 // A is n x r column-major, i.e. x + r of the packed variable vector (optimize.py:104-110).
 __global__ void k_prep_afrag(const double* __restrict__ A, int n, int r, int RB, int rbs, int kst,
                              double* __restrict__ Afrag) {
+  pdl_enter();
   const int NT = RB / 8;
   const int64_t total = (int64_t)rbs * kst * NT * 32;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -204,6 +206,7 @@ __global__ void __launch_bounds__(K3_T)
 constexpr int K4A_WARPS = 8;
 __global__ void k_tail_gram(const double* __restrict__ x, int n, int r, int d,
                             double* __restrict__ G, double* __restrict__ C) {
+  pdl_enter();
   const double* A = x + r;
   const int lane = threadIdx.x & 31;
   const int64_t total = (int64_t)r * r;
@@ -235,6 +238,7 @@ __global__ void k_tail_vec(const double* __restrict__ x, const double* __restric
                            const double* __restrict__ G, const double* __restrict__ C, int n, int r,
                            const double* __restrict__ alpha_dev, double alpha_host,
                            double* __restrict__ out) {
+  pdl_enter();
   extern __shared__ double s_u[];
   const double* lam = x;
   for (int j = threadIdx.x; j < r; j += blockDim.x) {
@@ -257,6 +261,7 @@ __global__ void k_tail_vec(const double* __restrict__ x, const double* __restric
 __global__ void k_tail_ga(const double* __restrict__ x, const double* __restrict__ Y,
                           const double* __restrict__ C, int n, int r, int d,
                           double* __restrict__ out) {
+  pdl_enter();
   const double* lam = x;
   const double* A = x + r;
   const int64_t total = (int64_t)n * r;
@@ -286,6 +291,7 @@ __global__ void __launch_bounds__(K4S_THREADS)
                  const double* __restrict__ alpha_dev, double alpha_host,
                  double* __restrict__ out, int64_t sx = 0, int64_t sy = 0, int64_t sw = 0,
                  int64_t so = 0) {
+  pdl_enter();
   // batched launches: CTA b handles start b (strides between consecutive starts' buffers)
   x += blockIdx.x * sx;
   Y += blockIdx.x * sy;

@@ -25,6 +25,7 @@ struct K1Variant {
   int kind = 0;        // 0: k1_fg_dmma (generic, cp.async chunks)  1: k1s_fg_stream (TMA slabs)
                        // 2: k1t_fg_tf32 (tcgen05 fast mode)  3: k1p_fg_pairs (self-fed pairs)
                        // 4: k1q_fg_pairs (warp-specialised pairs)  5: k1g_fg_dmma (Y in L2)
+                       // 6: k1r_fg_triads (K1Q with the GEMM1 role split by columns)
   int stages = 0;      // ring depth (kind 1)
   int MT = 0;          // GEMM2 m-tiles (kind 1)
   int MTW2 = 1;        // slabs per TMA copy unit (kind 1)

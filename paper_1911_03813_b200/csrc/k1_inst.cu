@@ -9,6 +9,7 @@
 #include "k1s_fp64.cuh"
 #include "k1p_fp64.cuh"
 #include "k1q_fp64.cuh"
+#include "k1r_fp64.cuh"
 
 namespace mcp {
 namespace {
@@ -153,6 +154,31 @@ const EntryS kTableQ[] = {MCP_K1Q_COLS(1, 1),  MCP_K1Q_COLS(3, 5),  MCP_K1Q_COLS
                           MCP_K1Q_COLS(16, 33)};
 std::atomic<bool> g_attr_q[kEntriesS];
 
+// ---------------- K1R (warp triads: the GEMM1 role split by columns; r mod 8 in 1..2) ----------
+template <int NTM, int TAIL, int MT2, int KH>
+void launch_r(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(K1R_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k1r_fg_triads<NTM, TAIL, MT2, KH>, prm);
+}
+#define MCP_K1R_E(NTM, TAIL, MT2, KH) \
+  {NTM, TAIL, MT2, KH, &launch_r<NTM, TAIL, MT2, KH>, \
+   (const void*)&k1r_fg_triads<NTM, TAIL, MT2, KH>}
+#define MCP_K1R_COLS(MT2, KH) MCP_K1R_E(1, 1, MT2, KH), MCP_K1R_E(1, 2, MT2, KH)
+const EntryS kTableR[] = {MCP_K1R_COLS(1, 1),  MCP_K1R_COLS(3, 5),  MCP_K1R_COLS(5, 9),
+                          MCP_K1R_COLS(9, 17), MCP_K1R_COLS(13, 25), MCP_K1R_COLS(15, 29),
+                          MCP_K1R_COLS(16, 33)};
+constexpr int kEntriesR = sizeof(kTableR) / sizeof(kTableR[0]);
+std::atomic<bool> g_attr_r[kEntriesR];
+
 bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
   if (n > 128) return false;
   const int MT = (int)ceil_div(n, 8);
@@ -241,11 +267,14 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
 }
 
 // K1P: same column / m-tile split as K1S, a private ring of SP >= 2 slabs per pair.
+// flavor 0: K1P, 1: K1Q, 2: K1R
 bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v,
-                  bool specialised) {
+                  int flavor) {
   if (n > 128) return false;
-  const EntryS* table = specialised ? kTableQ : kTableP;
-  std::atomic<bool>* attr = specialised ? g_attr_q : g_attr_p;
+  const bool specialised = flavor >= 1;
+  const EntryS* table = flavor == 2 ? kTableR : specialised ? kTableQ : kTableP;
+  const int n_entries = flavor == 2 ? kEntriesR : kEntriesS;
+  std::atomic<bool>* attr = flavor == 2 ? g_attr_r : specialised ? g_attr_q : g_attr_p;
   const int MT = (int)ceil_div(n, 8);
   const int kst = (int)(ldv / 4);
   const int mth_need = (MT + 1) / 2, kh_need = kst;
@@ -253,17 +282,19 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   if (r <= 8) { ntm = 1; tail = 0; }
   else if (r <= 10 && !getenv("MCP_K1S_NO_TAIL")) { ntm = 1; tail = r - 8; }
   else { ntm = 2; tail = 0; }
+  if (flavor == 2 && tail == 0) return false;   // triads only pay off with DFMA tail columns
   int e = -1;
-  for (int i = 0; i < kEntriesS && e < 0; ++i)
+  for (int i = 0; i < n_entries && e < 0; ++i)
     if (table[i].NTM == ntm && table[i].TAIL == tail &&
         table[i].MTH >= (specialised ? MT : mth_need) && table[i].KH >= kh_need)
       e = i;
   if (e < 0) return false;
   const int cw = 8 * ntm + tail;
   const size_t slab = (size_t)K1S_SR * ldv * 8;
-  const int NPR = specialised ? K1Q_PAIRS : K1P_PAIRS;
-  const size_t fixed = specialised ? k1q_fixed_bytes(table[e].KH, ntm, cw)
-                                   : k1p_fixed_bytes(table[e].KH, ntm, cw);
+  const int NPR = flavor == 2 ? K1R_TRIADS : specialised ? K1Q_PAIRS : K1P_PAIRS;
+  const size_t fixed = flavor == 2    ? k1r_fixed_bytes(table[e].KH, ntm, cw)
+                       : specialised ? k1q_fixed_bytes(table[e].KH, ntm, cw)
+                                     : k1p_fixed_bytes(table[e].KH, ntm, cw);
   const size_t budget = 227 * 1024 - 1024 - fixed;
   int SP = (int)(budget / ((size_t)NPR * (slab + 8)));
   if (SP > 4) SP = 4;
@@ -282,7 +313,7 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   } else {
     cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
-  v.kind = specialised ? 4 : 3;
+  v.kind = flavor == 2 ? 6 : specialised ? 4 : 3;
   v.dtype = MCP_F64;
   v.RB = cw;
   v.MTW = table[e].MTH;
@@ -306,7 +337,7 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   v.afrag_elems = 0;
   v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * cw;
   v.wpart_elems = (size_t)v.rbs * v.gp * cw;
-  v.name = std::string(specialised ? "k1q_fg_pairs" : "k1p_fg_pairs") + "<f64,DMMA=" +
+  v.name = std::string(flavor == 2 ? "k1r_fg_triads" : specialised ? "k1q_fg_pairs" : "k1p_fg_pairs") + "<f64,DMMA=" +
            std::to_string(8 * ntm) + ",DFMA=" + std::to_string(tail) +
            (specialised ? ",MT2=" : ",MTH=") + std::to_string(table[e].MTH) + ",KH=" +
            std::to_string(table[e].KH) + ",SP=" + std::to_string(SP) + ">";
@@ -320,7 +351,7 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
 // launch qualifies.
 bool k1_fuses_tail(const K1Variant& v, int64_t n, int r) {
   (void)n;
-  return (v.kind == 1 || v.kind == 3 || v.kind == 4) && r <= K3F_MAXR &&
+  return (v.kind == 1 || v.kind == 3 || v.kind == 4 || v.kind == 6) && r <= K3F_MAXR &&
          v.rbs * v.RB <= K3W_X;
 }
 
@@ -337,12 +368,17 @@ int64_t obs_pitch(int dtype, int64_t n) {
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v,
                std::string& why) {
   v = K1Variant();
+  // K1R is opt-in (MCP_K1R=1): at c2 it measured 5% slower than K1Q
+  if (dtype == MCP_F64 && getenv("MCP_K1R") &&
+      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, 2))
+    return true;
+  v = K1Variant();
   if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1Q") &&
-      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, true))
+      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, 1))
     return true;
   v = K1Variant();
   if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1P") &&
-      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, false))
+      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, 0))
     return true;
   v = K1Variant();
   if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1S") &&
@@ -460,7 +496,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
               double* wpart, cudaStream_t s) {
   if (v.entry < 0) return 1;
-  if (v.kind == 1 || v.kind == 3 || v.kind == 4) {
+  if (v.kind == 1 || v.kind == 3 || v.kind == 4 || v.kind == 6) {
     K1SParams sp;
     sp.V = static_cast<const double*>(dV);
     sp.ldv = ldv;
@@ -478,7 +514,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     sp.spc = v.MTW2;
     sp.Ypart = Ypart;
     sp.wpart = wpart;
-    (v.kind == 1 ? kTableS : v.kind == 3 ? kTableP : kTableQ)[v.entry].launch(sp, v.grid, v.smem,
+    (v.kind == 1 ? kTableS : v.kind == 3 ? kTableP : v.kind == 6 ? kTableR : kTableQ)[v.entry].launch(sp, v.grid, v.smem,
                                                                                s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }

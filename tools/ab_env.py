@@ -38,6 +38,7 @@ if a.timing:
     ctx.set_kernel_timing(True)
 variants = [("base", {})] + [(t, dict(kv.split("=", 1) for kv in t.split(","))) for t in a.toggles]
 res = {name: [] for name, _ in variants}
+vnames = {}
 outs = {}
 for rep in range(a.reps):
     for name, env in variants:
@@ -54,6 +55,7 @@ for rep in range(a.reps):
         torch.cuda.synchronize()
         res[name].append(e0.elapsed_time(e1) / a.steps)
         outs[name] = out.clone()
+        vnames[name] = ctx.last_variant
         for k in env:
             del os.environ[k]
 ref = None
@@ -70,4 +72,4 @@ for name, _ in variants:
         err = (f"  rel_err_vs_fp64 f {abs(float(o[0] - ref[0])) / abs(float(ref[0])):.2e}"
                f" g {float((o[1:] - ref[1:]).norm() / ref[1:].norm()):.2e}")
     print(f"{name:30s} median {statistics.median(v):.4f} ms  min {min(v):.4f}  "
-          f"bitwise_equal_to_base={same}{err}  variant={ctx.last_variant}")
+          f"bitwise_equal_to_base={same}{err}  variant={vnames[name]}")

@@ -440,3 +440,21 @@ def test_large_n_beyond_register_tiled_kernels():
     assert _err(res.f, f, f_s) <= FG_TOL
     assert _err(res.g_lam, gl, gl_s) <= FG_TOL
     assert _err(res.g_A, gA, gA_s) <= FG_TOL
+
+
+@pytest.mark.parametrize("n,r,d", [(160, 20, 3), (288, 40, 4), (384, 72, 3), (64, 70, 5)])
+def test_fast_mode_tile_shapes_vs_oracle(n, r, d):
+    """tcgen05 fast mode over the shapes that switch its tiling: GEMM2's 3-D TMA boxes with
+    out-of-range column chunks (n % 128 != 0, n % 32 == 0), several factor column blocks
+    (r > 64), and the 2-D path (n < 128); against the CPU oracle within the stated bound."""
+    rng = np.random.default_rng(n + r)
+    p = 9000
+    V = (rng.standard_normal((n, p)) / np.sqrt(n)).astype(np.float32)
+    lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)
+    res = mcp.fg_implicit(mcp.ObservationSet(V), lam, A, d, 0.1, mode="tf32x3")
+    V64 = V.astype(np.float64)
+    nu = np.full(p, 1.0 / p)
+    f, gl, gA = om.fg_implicit(V64, nu, lam, A, d, 0.1)
+    f_s, gl_s, gA_s, _ = om.term_scales(V64, nu, lam, A, d, 0.1)
+    e = max(_err(res.f, f, f_s), _err(res.g_lam, gl, gl_s), _err(res.g_A, gA, gA_s))
+    assert e <= FAST_TOL, e

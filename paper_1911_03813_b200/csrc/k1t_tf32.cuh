@@ -352,12 +352,16 @@ __global__ void k_f64_to_f32(const double* __restrict__ src, float* __restrict__
 // V_lo = V - tf32(V) are computed ONCE per observation set (k_split_lo, kept in HBM next to the
 // fp32 rows: +1x V of memory, c5 65.5 -> 131 GB) and streamed by TMA like V itself; the tensor
 // core truncates the fp32 rows to TF32 on read, so the resident fp32 V doubles as V_hi.
-// Tiles are software-pipelined: Z is double-buffered in TMEM and the MMA issuer runs
-// GEMM1(u) before GEMM2(u - 1), so the epilogue of a tile (P = nu z^(d-1) -> TF32 hi/lo bricks,
-// measured ~15k cycles) overlaps the next tile's GEMM1 instead of stalling the tensor pipe.
+// Tile order (prm.serial, the default): GEMM1(u), epilogue(u), GEMM2(u) with one Z buffer, so
+// GEMM2 re-reads the V / V_lo tile GEMM1 just streamed while it is still in L2 (L2 policies:
+// GEMM1's reads evict_last, GEMM2's evict_first) -- DRAM sees V + V_lo once.  The look-ahead
+// order (serial = 0: Z double-buffered, GEMM1(u + 1) before GEMM2(u)) hides the epilogue but
+// holds two tiles per SM between the reads, more than L2, and measured slower once the epilogue
+// was vectorised (~2k cycles per tile).  The fp32 Y drains into the fp64 partial every
+// prm.flush tiles, under the next GEMM1.
 // Roles: warp 0 TMA producer, warp 1 MMA issuer + TMEM owner, warps 2..9 epilogue / flush (two
-// per TMEM sub-partition, each on half of the columns).  TMEM: Z0, Z1, then Y[mt]:
-// (2 + n/128) RB <= 512 columns.
+// per TMEM sub-partition, each on half of the columns).  TMEM: Z (one or two buffers, 2 RB
+// columns each with zcat), then Y[mt]: (zbufs * ZW / RB + n/128) RB <= 512 columns.
 constexpr int K1T2_EPI_WARPS = 8;
 constexpr int K1T2_THREADS = (2 + K1T2_EPI_WARPS) * 32;
 #ifndef MCP_K1T2_PROF
@@ -611,12 +615,17 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       long long t_g1 = 0, t_g2 = 0;
       if (prm.serial) {
         for (int64_t u = 0; u < my_tiles; ++u) {
+#if MCP_K1T2_PROF
           const long long a0 = clock64();
           g1(u);
           const long long a1 = clock64();
           g2(u);
           t_g1 += a1 - a0;
           t_g2 += clock64() - a1;
+#else
+          g1(u);
+          g2(u);
+#endif
         }
       } else {
         for (int64_t u = 0; u <= my_tiles; ++u) {

@@ -282,6 +282,13 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   t.zcat = !v1 && !getenv("MCP_K1T_NO_ZCAT") && 2 * RB <= 256 && (2 * zbufs + t.mt2) * RB <= 512;
   if ((zbufs + t.mt2) * RB > 512)
     return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
+  // GEMM2 m-tiles that get a second RB-column accumulator half from the spare TMEM columns
+  t.wide = 0;
+  if (!v1 && env_int("MCP_K1T2_WIDE", 1) != 0) {
+    const int zw = t.zcat ? 2 * RB : RB;
+    const int spare = 512 - zbufs * zw - t.mt2 * RB;
+    t.wide = std::max(0, std::min(t.mt2, spare / RB));
+  }
   t.RB = RB;
   t.rbs = (int)ceil_div(r, RB);
   t.r_pad = t.rbs * RB;
@@ -325,7 +332,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
                 std::to_string(RB) + ",S=" + std::to_string(ns) +
                 (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
-                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (getenv("MCP_K1T2_G2X2") && atoi(getenv("MCP_K1T2_G2X2")) != 0 ? ",g2x2" : "") + ",flush=" + std::to_string(t.flush)
+                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (getenv("MCP_K1T2_G2X2") && atoi(getenv("MCP_K1T2_G2X2")) != 0 ? ",g2x2" : "") + ",flush=" + std::to_string(t.flush)
                       : std::string()) +
                 ">";
   return MCP_OK;
@@ -395,6 +402,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.hint = t.hint ? 1 : 0;
   prm.flush = t.flush;
   prm.g2_3d = t.g2_3d ? 1 : 0;
+  prm.wide = t.wide;
   // opt-in: GEMM2 as V P_hi with P_hi rounded to nearest (8-9% faster at c3 / c5, but normwise
   // error up to 7e-5 at reduced p -- too close to the stated 1e-4 to be the default)
   prm.g2x2 = getenv("MCP_K1T2_G2X2") && atoi(getenv("MCP_K1T2_G2X2")) != 0 ? 1 : 0;

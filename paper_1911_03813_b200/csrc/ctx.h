@@ -107,6 +107,7 @@ struct K1TPlan {
   bool hint = false;    // K1T2 L2 eviction policy on the V reads
   int flush = 8;        // K1T2 tiles per fp64 flush of the fp32 TMEM Y
   bool g2_3d = false;   // K1T2 GEMM2 V loads as one 3-D TMA per operand and stage
+  int wide = 0;         // K1T2 GEMM2 m-tiles with the N = 2 RB [P_hi | P_lo] product
   int64_t num_tiles = 0;
   size_t smem = 0;
 };

@@ -58,6 +58,8 @@ struct K1TParams {
   int g2_3d = 0;      // K1T2: tm_v2 / tm_l2 are 3-D chunk maps (one TMA per 16 KB operand)
   int g2x2 = 0;       // K1T2: GEMM2 as V P_hi (2 products) with P_hi rounded to nearest; the
                       // dropped V_hi P_lo term is unbiased and <= 2^-12 of each product
+  int wide = 0;       // K1T2: GEMM2 m-tiles [0, wide) run V_hi [P_hi | P_lo] as ONE N = 2 RB
+                      // product into two TMEM halves (spare columns), the V_hi operand read once
 };
 
 __host__ __device__ constexpr size_t k1t_stage_bytes(int RB) { return 2 * K1T_VBYTES + 256 * RB; }
@@ -386,9 +388,10 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
   unsigned char* base = smem_raw_t2 + ((1024u - (smem_u32(smem_raw_t2) & 1023u)) & 1023u);
   const int RB = prm.RB, NS = prm.stages;
   const size_t SB = k1t_stage_bytes(RB);
-  unsigned char* sPh = base + NS * SB;
-  unsigned char* sPl = sPh + 512 * RB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sPl + 512 * RB);
+  // P bricks: brick b (32 tile rows) holds RB rows of P_hi then RB rows of P_lo, so one K-major
+  // descriptor with N = 2 RB covers [P_hi | P_lo]
+  unsigned char* sP2 = base + NS * SB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP2 + 1024 * RB);
   uint64_t* full = bars;
   uint64_t* empty = bars + NS;
   uint64_t* z_full = bars + 2 * NS;     // [2]
@@ -436,8 +439,12 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int ZW = prm.zcat ? 2 * RB : RB;          // TMEM columns of one Z buffer
-  // Z[b] at b ZW; Y[mt] after the Z buffers (two under look-ahead, one in serial order)
+  // Z[b] at b ZW; Y[mt] after the Z buffers (two under look-ahead, one in serial order); a wide
+  // m-tile has two RB-column halves (V_hi P_hi + V_lo P_hi, V_hi P_lo)
   const uint32_t ty = tmem + (prm.serial ? 1 : 2) * ZW;
+  auto ycol = [&](int mt) -> uint32_t {
+    return (uint32_t)(mt < prm.wide ? 2 * RB * mt : 2 * RB * prm.wide + RB * (mt - prm.wide));
+  };
 
   if (warp == 0) {
     // =========================== TMA producer (same order as the MMA issuer) ===========================
@@ -518,6 +525,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       const uint32_t id1 = umma_idesc_tf32(128, RB, false, false);
       const uint32_t id1c = umma_idesc_tf32(128, 2 * RB, false, false);
       const uint32_t id2 = umma_idesc_tf32(128, RB, true, false);
+      const uint32_t id2w = umma_idesc_tf32(128, 2 * RB, true, false);
       int64_t q = 0;
       int flushes = 0;
       bool fresh = true, wait_y = false;
@@ -578,8 +586,8 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             fresh = true;
           }
           tc_fence_after();
-          const uint64_t dph = umma_desc_sw128(smem_u32(sPh), 16, 1024);
-          const uint64_t dpl = umma_desc_sw128(smem_u32(sPl), 16, 1024);
+          const uint64_t dph = umma_desc_sw128(smem_u32(sP2), 16, 1024);
+          const uint64_t dpl = dph + ((128 * RB) >> 4);
           for (int step = 0; step < 4 * mt2; ++step, ++q) {
             const int mt = step >> 2, rc = step & 3;
             const int s = (int)(q % NS);
@@ -591,16 +599,27 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             tc_fence_after();
             const uint64_t dvh = umma_desc_sw128_32b(smem_u32(base + s * SB), 4096, 512);
             const uint64_t dvl = dvh + (K1T_VBYTES >> 4);
-            const uint64_t boff = (uint64_t)((rc * 128 * RB) >> 4);
-#pragma unroll
-            for (int pr = 0; pr < 3; ++pr) {
-              if (pr == 1 && prm.g2x2) continue;
-              const uint64_t av = pr == 2 ? dvl : dvh;
-              const uint64_t bv = (pr == 1 ? dpl : dph) + boff;
+            const uint64_t boff = (uint64_t)((rc * 256 * RB) >> 4);
+            if (mt < prm.wide) {
+              // [V_hi P_hi | V_hi P_lo] in one N = 2 RB product, then V_lo P_hi into the first half
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks)
-                umma_tf32(ty + mt * RB, av + 64 * ks, bv + 2 * ks, id2,
-                          (fresh && rc == 0 && pr == 0 && ks == 0) ? 0u : 1u);
+                umma_tf32(ty + ycol(mt), dvh + 64 * ks, dph + boff + 2 * ks, id2w,
+                          (fresh && rc == 0 && ks == 0) ? 0u : 1u);
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                umma_tf32(ty + ycol(mt), dvl + 64 * ks, dph + boff + 2 * ks, id2, 1u);
+            } else {
+#pragma unroll
+              for (int pr = 0; pr < 3; ++pr) {
+                if (pr == 1 && prm.g2x2) continue;
+                const uint64_t av = pr == 2 ? dvl : dvh;
+                const uint64_t bv = (pr == 1 ? dpl : dph) + boff;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                  umma_tf32(ty + ycol(mt), av + 64 * ks, bv + 2 * ks, id2,
+                            (fresh && rc == 0 && pr == 0 && ks == 0) ? 0u : 1u);
+              }
             }
             umma_commit(smem_u32(&empty[s]));
           }
@@ -666,16 +685,19 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
       for (int mt = 0; mt < mt2; ++mt) {
         double* yrow = Yp + ((size_t)mt * 128 + l) * RB;
         for (int c0 = half * hc; col_active && c0 < c_end; c0 += 16) {
-          float yv[16];
-          tmem_ld16(ty + mt * RB + ((uint32_t)(32 * sp) << 16) + c0, yv);
+          float yv[16], y2[16];
+          tmem_ld16(ty + ycol(mt) + ((uint32_t)(32 * sp) << 16) + c0, yv);
+          const bool wide = mt < prm.wide;
+          if (wide) tmem_ld16(ty + ycol(mt) + RB + ((uint32_t)(32 * sp) << 16) + c0, y2);
           // each partial element has exactly one owner thread and flushes are in program order,
           // so fire-and-forget reductions (RED, no load latency) keep the sum order fixed
-          if (flushes == 0) {
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) yrow[c0 + jj] = (double)yv[jj];
-          } else {
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) atomicAdd(yrow + c0 + jj, (double)yv[jj]);
+          for (int jj = 0; jj < 16; ++jj) {
+            const double yd = wide ? (double)yv[jj] + (double)y2[jj] : (double)yv[jj];
+            if (flushes == 0)
+              yrow[c0 + jj] = yd;
+            else
+              atomicAdd(yrow + c0 + jj, yd);
           }
         }
       }
@@ -727,9 +749,9 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
           for (int jj = 0; jj < 16; ++jj) {
             const float pf = (float)(nul * pw[jj]);
             const float ph = prm.g2x2 ? tf32_rna(pf) : tf32_hi(pf);
-            const uint32_t off = brick * 128 * RB + brick_off(c0 + jj, col);
-            *reinterpret_cast<float*>(sPh + off) = ph;
-            *reinterpret_cast<float*>(sPl + off) = pf - ph;
+            const uint32_t off = brick * 256 * RB + brick_off(c0 + jj, col);
+            *reinterpret_cast<float*>(sP2 + off) = ph;
+            *reinterpret_cast<float*>(sP2 + off + 128 * RB) = pf - ph;
           }
         }
         K1T2_ACC(e_epi);

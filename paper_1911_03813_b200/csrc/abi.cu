@@ -277,6 +277,9 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     // prefer the widest block that does not add a column block over the narrowest
     const int rbs_w = (int)ceil_div(r, RB);
     while (RB > 16 && ceil_div(r, RB - 16) == rbs_w && (RB - 16) >= r / rbs_w) RB -= 16;
+    const int forced = env_int("MCP_K1T2_RB", 0);   // experiment switch
+    if (forced >= 16 && forced <= 64 && forced % 16 == 0 && (zbufs + t.mt2) * forced <= 512)
+      RB = forced;
   }
   // K1T2 with the concatenated GEMM1 when TMEM has room for two 2 RB-wide Z buffers
   t.zcat = !v1 && !getenv("MCP_K1T_NO_ZCAT") && 2 * RB <= 256 && (2 * zbufs + t.mt2) * RB <= 512;

@@ -455,6 +455,23 @@ def main():
     k1_ms, k1_launches = ctx.kernel_time_ms(reset=True)
     ctx.set_kernel_timing(False)
     launches_per_step = ctx.last_launch_count if world == 1 else (3 if pex is not None else 6)
+    scaling_breakdown = None
+    if world > 1:
+        # the same K steps without the exchange (this rank's partial only): what the exchange and
+        # finish add per step, for the scaling analysis (max over ranks)
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        barrier_sync()
+        p0.record()
+        for _ in range(args.steps):
+            ctx.fg_partial_device(d, r, x_dev.data_ptr(), args.mode, Yw.data_ptr(), stream)
+        p1.record()
+        barrier_sync()
+        partial_ms = max_over_ranks(p0.elapsed_time(p1)) / args.steps
+        scaling_breakdown = {"partial_ms_per_step": partial_ms,
+                             "step_ms": ms_total / args.steps,
+                             "exchange_and_finish_ms": ms_total / args.steps - partial_ms,
+                             "rows_per_rank": hi - lo}
     variant = ctx.last_variant
     clk = clocks.stop() if rank == 0 else None
 
@@ -533,6 +550,8 @@ def main():
         "clocks": clk,
         "gpu_launches": launches_per_step * args.steps,
     }
+    if scaling_breakdown is not None:
+        line["scaling_breakdown"] = scaling_breakdown
     sus = _sustained_tensor_peak(args.mode)
     if bound == "tensor" and sus:
         # the burst peak stays the headline denominator; the sustained one (library GEMM back to

@@ -427,8 +427,8 @@ def main():
     barrier_sync()
 
     # ---- timed region: exactly K device-resident steps ----
-    # K1 is event-timed on every 4th step (each event pair costs ~5 us of a ~0.19 ms c2 step)
-    ctx.set_kernel_timing(True, every=4 if args.steps >= 8 else 1)
+    # K1 is event-timed on every 8th step (each event pair costs ~5 us of a ~0.19 ms c2 step)
+    ctx.set_kernel_timing(True, every=8 if args.steps >= 64 else (4 if args.steps >= 8 else 1))
     ctx.kernel_time_ms(reset=True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)

@@ -321,8 +321,8 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     c->tm_a_kpad = t.kpad;
     c->tm_a_rb = RB;
   }
-  CUDA_TRY(c, cudaFuncSetAttribute(t.v2 ? (const void*)k1t2_fg_tf32 : (const void*)k1t_fg_tf32,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
+  if (!ensure_dyn_smem(t.v2 ? (const void*)k1t2_fg_tf32 : (const void*)k1t_fg_tf32, t.smem))
+    return c->fail(MCP_ERR_CUDA, "cudaFuncSetAttribute failed for the tf32x3 kernel");
   pl.k1 = K1Variant();
   pl.k1.kind = 2;
   pl.k1.RB = RB;

@@ -40,6 +40,9 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
               double* wpart, cudaStream_t s);
 
+// Raise a kernel's dynamic shared-memory limit (per device, once per new maximum).
+bool ensure_dyn_smem(const void* fn, size_t smem);
+
 // True when the evaluation can end with the one-kernel reduce + finish K3F (prep-free FP64 K1,
 // r <= 32, every w in K3F's w block).
 bool k1_fuses_tail(const K1Variant& v, int64_t n, int r);

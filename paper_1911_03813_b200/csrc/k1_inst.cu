@@ -1,5 +1,8 @@
 // Instantiations of the K1 FP64 kernel family and the host-side variant selection.
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cstdlib>
 
 #include "momentcp_b200.h"
@@ -12,6 +15,30 @@
 #include "k1r_fp64.cuh"
 
 namespace mcp {
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device maximum: raise it once per
+// (kernel, device) to the largest size requested so far instead of on every plan (a driver call
+// on the host path of every evaluation).
+bool ensure_dyn_smem(const void* fn, size_t smem) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> have;
+  std::lock_guard<std::mutex> lk(mu);
+  int& h = have[{fn, dev}];
+  if ((int)smem <= h) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  h = (int)smem;
+  return true;
+}
+
 namespace {
 
 template <typename VT, int RB, int MTW>
@@ -50,7 +77,6 @@ void launch_g(const K1Params& prm, int grid, size_t smem, cudaStream_t s) {
 const Entry kTableG[] = {MCP_K1G_E(double, MCP_F64, 16), MCP_K1G_E(double, MCP_F64, 32),
                          MCP_K1G_E(double, MCP_F64, 64), MCP_K1G_E(float, MCP_F32, 16),
                          MCP_K1G_E(float, MCP_F32, 32),  MCP_K1G_E(float, MCP_F32, 64)};
-std::atomic<bool> g_attr_g[6];
 constexpr int kEntries = sizeof(kTable) / sizeof(kTable[0]);
 std::atomic<int> g_occ[kEntries];
 std::atomic<bool> g_occ_init{false};
@@ -108,7 +134,6 @@ const EntryS kTableS[] = {MCP_K1S_COLS(1, 1),  MCP_K1S_COLS(2, 5),  MCP_K1S_COLS
                           MCP_K1S_COLS(5, 17), MCP_K1S_COLS(7, 25), MCP_K1S_COLS(8, 29),
                           MCP_K1S_COLS(8, 33)};
 constexpr int kEntriesS = sizeof(kTableS) / sizeof(kTableS[0]);
-std::atomic<bool> g_attr_s[kEntriesS];
 
 // ---------------- K1P (self-fed pairs, fp64, n <= 128) ----------------
 template <int NTM, int TAIL, int MTH, int KH>
@@ -124,7 +149,6 @@ void launch_p(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
 const EntryS kTableP[] = {MCP_K1P_COLS(1, 1),  MCP_K1P_COLS(2, 5),  MCP_K1P_COLS(3, 9),
                           MCP_K1P_COLS(5, 17), MCP_K1P_COLS(7, 25), MCP_K1P_COLS(8, 29),
                           MCP_K1P_COLS(8, 33)};
-std::atomic<bool> g_attr_p[kEntriesS];
 
 // ---------------- K1Q (warp-specialised pairs, fp64, n <= 128) ----------------
 template <int NTM, int TAIL, int MT2, int KH>
@@ -152,7 +176,6 @@ void launch_q(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
 const EntryS kTableQ[] = {MCP_K1Q_COLS(1, 1),  MCP_K1Q_COLS(3, 5),  MCP_K1Q_COLS(5, 9),
                           MCP_K1Q_COLS(9, 17), MCP_K1Q_COLS(13, 25), MCP_K1Q_COLS(15, 29),
                           MCP_K1Q_COLS(16, 33)};
-std::atomic<bool> g_attr_q[kEntriesS];
 
 // ---------------- K1R (warp triads: the GEMM1 role split by columns; r mod 8 in 1..2) ----------
 template <int NTM, int TAIL, int MT2, int KH>
@@ -177,7 +200,6 @@ const EntryS kTableR[] = {MCP_K1R_COLS(1, 1),  MCP_K1R_COLS(3, 5),  MCP_K1R_COLS
                           MCP_K1R_COLS(9, 17), MCP_K1R_COLS(13, 25), MCP_K1R_COLS(15, 29),
                           MCP_K1R_COLS(16, 33)};
 constexpr int kEntriesR = sizeof(kTableR) / sizeof(kTableR[0]);
-std::atomic<bool> g_attr_r[kEntriesR];
 
 bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
   if (n > 128) return false;
@@ -226,16 +248,7 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
       (size_t)K1S_PAIRS * MT * 8 * cw * 8 + (size_t)2 * K1S_PAIRS * cw * 8;
   if ((size_t)S * stage < stage_need) return false;
   const size_t smem = (size_t)S * stage + fixed + 16 * (size_t)S;
-  if (!g_attr_s[e].exchange(true)) {
-    if (cudaFuncSetAttribute(kTableS[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess) {
-      (void)cudaGetLastError();
-      g_attr_s[e].store(false);
-      return false;
-    }
-  } else {
-    cudaFuncSetAttribute(kTableS[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
+  if (!ensure_dyn_smem(kTableS[e].fn, smem)) return false;
   v.kind = 1;
   v.dtype = MCP_F64;
   v.RB = cw;
@@ -274,7 +287,6 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   const bool specialised = flavor >= 1;
   const EntryS* table = flavor == 2 ? kTableR : specialised ? kTableQ : kTableP;
   const int n_entries = flavor == 2 ? kEntriesR : kEntriesS;
-  std::atomic<bool>* attr = flavor == 2 ? g_attr_r : specialised ? g_attr_q : g_attr_p;
   const int MT = (int)ceil_div(n, 8);
   const int kst = (int)(ldv / 4);
   const int mth_need = (MT + 1) / 2, kh_need = kst;
@@ -303,16 +315,7 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   const size_t stage_need = ((size_t)NPR * MT * 8 * cw + (size_t)2 * NPR * cw) * 8;
   if (ring_bytes < stage_need) return false;
   size_t smem = ring_bytes + fixed + 8 * (size_t)NPR * (SP + 4);
-  if (!attr[e].exchange(true)) {
-    if (cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess) {
-      (void)cudaGetLastError();
-      attr[e].store(false);
-      return false;
-    }
-  } else {
-    cudaFuncSetAttribute(table[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
+  if (!ensure_dyn_smem(table[e].fn, smem)) return false;
   v.kind = flavor == 2 ? 6 : specialised ? 4 : 3;
   v.dtype = MCP_F64;
   v.RB = cw;
@@ -405,16 +408,7 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
     for (int i = 0; i < 6; ++i)
       if (kTableG[i].dtype == dtype && kTableG[i].RB == rb) e = i;
     if (e >= 0) {
-      bool ok = true;
-      if (!g_attr_g[e].exchange(true)) {
-        if (cudaFuncSetAttribute(kTableG[e].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kTableG[e].smem) != cudaSuccess) {
-          (void)cudaGetLastError();
-          g_attr_g[e].store(false);
-          ok = false;
-        }
-      }
-      if (ok) {
+      if (ensure_dyn_smem(kTableG[e].fn, kTableG[e].smem)) {
         const int n_chunks = (int)ceil_div(n, K1_NK);
         v.kind = 5;
         v.dtype = dtype;

@@ -118,6 +118,26 @@ int mcp_data_norm_sq(mcp_ctx* ctx, int d, int mode, double* out);
 int mcp_data_norm_sq_part(mcp_ctx* ctx, int d, int mode, int part, int nparts, double* out);
 
 /*
+ * Sharded ||X||^2 (implicit.py:116-121 over a row-sharded set): part `part` of
+ * `nparts` of 2 * sum_{l in ctx's rows, l' in shard J} nu_l nu_l' (v_l^T v_l')^d, i.e. both
+ * off-diagonal blocks (I, J) and (J, I) of the Gram.  Shard J is device memory in ctx's own
+ * layout (p_pad_J rows of ctx's pitch and dtype, zero padded, p_pad_J a multiple of 128: a peer
+ * rank's buffer received over NVLink); dnuJ its weights (NULL: uniform nu_const_J).
+ * pair_order 0 lists the rectangle's 128 x 128 tile pairs with ctx's tiles outer, 1 with shard
+ * J's tiles outer, so two ranks that share one shard pair can each take half of it
+ * (part 0 of 2 in order 0 on one side, part 1 of 2 in order 1 on the other).
+ */
+int mcp_data_norm_sq_cross(mcp_ctx* ctx, const void* dVJ, int64_t p_pad_J, const double* dnuJ,
+                           double nu_const_J, int d, int mode, int pair_order, int part,
+                           int nparts, double* out);
+
+/* The resident observation buffer (device pointer, pitch and padded rows in elements, dtype,
+ * weights or NULL + the uniform weight): what a peer needs to run mcp_data_norm_sq_cross
+ * against this shard. */
+int mcp_obs_device_view(const mcp_ctx* ctx, void** dV, int64_t* ldv, int64_t* p_pad, int* dtype,
+                        const double** dnu, double* nu_const);
+
+/*
  * Device-resident pieces (all pointers are device memory on ctx's device; stream may be NULL
  * for the context's own stream).
  *   dx   : [lam (r); vec_F(A) (n*r)]
@@ -138,6 +158,16 @@ int mcp_fg_device(mcp_ctx* ctx, int d, int r, const double* dx, double alpha, in
  * them and returns the summed duration and launch count (reset != 0 clears the record).
  */
 int mcp_set_kernel_timing(mcp_ctx* ctx, int enable);   /* enable > 1: time every enable-th launch */
+
+/*
+ * Per-context run-time options (the library reads no environment variables; kernel and
+ * schedule choices are compile-time, csrc/tuning.h).
+ *   MCP_OPT_FUSED_TAIL (default 1): end eligible FP64 evaluations with the one-kernel
+ *     reduce+finish (K3F); 0 runs the separate reduce and tail kernels (bitwise-equal results;
+ *     the tests compare the two).  No reference counterpart (an implementation choice).
+ */
+#define MCP_OPT_FUSED_TAIL 1
+int mcp_set_option(mcp_ctx* ctx, int key, int64_t value);
 int mcp_kernel_time_ms(mcp_ctx* ctx, double* total_ms, int* launches, int reset);
 
 /*

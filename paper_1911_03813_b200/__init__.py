@@ -23,7 +23,8 @@ from .implicit import (
 from .io import ParseError, read_observations_binary, write_observations_binary
 from .objective import FgResult, fg_implicit, sample_observations
 from .optimize import (AdamConfig, FgCallback, OptConfig, RunReport, adam_minimize, lbfgs_minimize,
-                       lbfgs_minimize_batched, multistart, multistart_lbfgs, pack, packed_fg_implicit, packed_fg_implicit_batched, unpack)
+                       lbfgs_minimize_batched, multistart_lbfgs, pack, packed_fg_implicit,
+                       packed_fg_implicit_batched, unpack)
 
 __all__ = [
     "AdamConfig",
@@ -45,7 +46,6 @@ __all__ = [
     "lbfgs_minimize",
     "lbfgs_minimize_batched",
     "multistart_lbfgs",
-    "multistart",
     "pack",
     "read_observations_binary",
     "packed_fg_implicit",

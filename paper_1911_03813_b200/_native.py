@@ -24,6 +24,7 @@ MCP_OK, MCP_ERR_ARG, MCP_ERR_CUDA, MCP_ERR_STATE = 0, 1, 2, 3
 MCP_F64, MCP_F32 = 0, 1
 MCP_VAR_MAJOR, MCP_OBS_MAJOR = 0, 1
 MODES = {"fp64": 0, "tf32x3": 1}
+MCP_OPT_FUSED_TAIL = 1
 
 # name -> (restype, argtypes); every symbol include/momentcp_b200.h declares
 _c_void_p = ctypes.c_void_p
@@ -58,6 +59,14 @@ SIGNATURES = {
     "mcp_data_norm_sq": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _dp]),
     "mcp_data_norm_sq_part": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, _dp]),
+    "mcp_data_norm_sq_cross": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _c_void_p,
+                                              ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]),
+    "mcp_obs_device_view": (ctypes.c_int, [_c_void_p, ctypes.POINTER(_c_void_p),
+                                           ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                           ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(_c_void_p),
+                                           ctypes.POINTER(ctypes.c_double)]),
     "mcp_fg_partial_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
                                              ctypes.c_int, _c_void_p, _c_void_p]),
     "mcp_fg_finish_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
@@ -65,6 +74,7 @@ SIGNATURES = {
     "mcp_fg_device": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, _c_void_p,
                                      ctypes.c_double, ctypes.c_int, _c_void_p, _c_void_p]),
     "mcp_set_kernel_timing": (ctypes.c_int, [_c_void_p, ctypes.c_int]),
+    "mcp_set_option": (ctypes.c_int, [_c_void_p, ctypes.c_int, _i64]),
     "mcp_kernel_time_ms": (ctypes.c_int, [_c_void_p, _dp, ctypes.POINTER(ctypes.c_int),
                                           ctypes.c_int]),
     "mcp_lbfgs": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
@@ -183,6 +193,10 @@ class Context:
     @property
     def last_variant(self) -> str:
         return self._lib.mcp_last_variant(self._h).decode()
+
+    def set_option(self, key: int, value: int) -> None:
+        """mcp_set_option (e.g. MCP_OPT_FUSED_TAIL)."""
+        self._check(self._lib.mcp_set_option(self._h, int(key), int(value)), "mcp_set_option")
 
     # -- kernel timing (bench) ------------------------------------------------------------
     def set_kernel_timing(self, enable, every: int = 1) -> None:
@@ -415,6 +429,32 @@ class Context:
                                                  int(nparts), ctypes.byref(out))
         self._check(rc, "mcp_data_norm_sq")
         return out.value
+
+    def data_norm_sq_cross(self, dVJ: int, p_pad_J: int, dnuJ: int | None, nu_const_J: float,
+                           d: int, mode: str | None, part: int = 0, nparts: int = 1,
+                           pair_order: int = 0) -> float:
+        out = ctypes.c_double()
+        rc = self._lib.mcp_data_norm_sq_cross(self._h, ctypes.c_void_p(dVJ), int(p_pad_J),
+                                              None if not dnuJ else ctypes.c_void_p(dnuJ),
+                                              float(nu_const_J), int(d), mode_code(mode),
+                                              int(pair_order), int(part), int(nparts),
+                                              ctypes.byref(out))
+        self._check(rc, "mcp_data_norm_sq_cross")
+        return out.value
+
+    def obs_device_view(self) -> dict:
+        """The resident observation buffer: ptr, ldv, p_pad (elements), dtype code, nu ptr."""
+        dv, nu = ctypes.c_void_p(), ctypes.c_void_p()
+        ldv, p_pad = ctypes.c_int64(), ctypes.c_int64()
+        dt = ctypes.c_int()
+        nc = ctypes.c_double()
+        rc = self._lib.mcp_obs_device_view(self._h, ctypes.byref(dv), ctypes.byref(ldv),
+                                           ctypes.byref(p_pad), ctypes.byref(dt),
+                                           ctypes.byref(nu), ctypes.byref(nc))
+        if rc != MCP_OK:
+            raise RuntimeError("mcp_obs_device_view: no observation set loaded")
+        return {"ptr": dv.value or 0, "ldv": ldv.value, "p_pad": p_pad.value, "dtype": dt.value,
+                "nu": nu.value or 0, "nu_const": nc.value}
 
     # -- evaluations (device pointers, caller's stream) ------------------------------------
     def fg_partial_device(self, d, r, dx_ptr, mode, dYw_ptr, stream_ptr):

@@ -221,7 +221,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   }
   // K1T2: V_lo precomputed once per set (falls back to the in-kernel split if it does not fit)
   t.v2 = false;
-  if (!getenv("MCP_K1T_V1")) {
+  if (!MCP_CFG_K1T_V1) {
     if (!c->dVlo32) {
       const size_t bytes = sizeof(float) * (size_t)c->p_pad * c->ldv32;
       if (cudaMalloc(&c->dVlo32, bytes) == cudaSuccess) {
@@ -243,7 +243,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   }
   // K1T2's GEMM2 V reads: one 3-D TMA per 16 KB stage half when rows are whole 32-float chunks
   t.g2_3d = false;
-  if (t.v2 && c->ldv32 % 32 == 0 && c->ldv32 >= 128 && !getenv("MCP_K1T2_G2_2D")) {
+  if (t.v2 && c->ldv32 % 32 == 0 && c->ldv32 >= 128 && MCP_CFG_K1T2_G2_3D) {
     if (!c->tm_c_ready) {
       c->tm_c_ready =
           make_tmap_f32_chunks(&c->tm_v3, c->dV32, c->ldv32, c->p_pad, 32, 4,
@@ -258,13 +258,9 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   // and the operand bytes per MAC fall with N.  K1T2 takes any multiple of 16 up to 64, K1T
   // powers of two.
   const bool v1 = !t.v2;
-  auto env_int = [](const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-  };
-  t.serial = !v1 && env_int("MCP_K1T2_SERIAL", 1) != 0;
-  t.hint = !v1 && env_int("MCP_K1T2_HINT", 1) != 0;
-  t.flush = std::max(1, env_int("MCP_K1T2_FLUSH", 16));
+  t.serial = !v1 && MCP_CFG_K1T2_SERIAL != 0;
+  t.hint = !v1 && MCP_CFG_K1T2_HINT != 0;
+  t.flush = std::max(1, MCP_CFG_K1T2_FLUSH);
   const int zbufs = (v1 || t.serial) ? 1 : 2;
   int RB = 16;
   if (v1) {
@@ -277,17 +273,17 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     // prefer the widest block that does not add a column block over the narrowest
     const int rbs_w = (int)ceil_div(r, RB);
     while (RB > 16 && ceil_div(r, RB - 16) == rbs_w && (RB - 16) >= r / rbs_w) RB -= 16;
-    const int forced = env_int("MCP_K1T2_RB", 0);   // experiment switch
+    const int forced = MCP_CFG_K1T2_RB;   // experiment builds only
     if (forced >= 16 && forced <= 64 && forced % 16 == 0 && (zbufs + t.mt2) * forced <= 512)
       RB = forced;
   }
   // K1T2 with the concatenated GEMM1 when TMEM has room for two 2 RB-wide Z buffers
-  t.zcat = !v1 && !getenv("MCP_K1T_NO_ZCAT") && 2 * RB <= 256 && (2 * zbufs + t.mt2) * RB <= 512;
+  t.zcat = !v1 && MCP_CFG_K1T_ZCAT && 2 * RB <= 256 && (2 * zbufs + t.mt2) * RB <= 512;
   if ((zbufs + t.mt2) * RB > 512)
     return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
   // GEMM2 m-tiles that get a second RB-column accumulator half from the spare TMEM columns
   t.wide = 0;
-  if (!v1 && env_int("MCP_K1T2_WIDE", 1) != 0) {
+  if (!v1 && MCP_CFG_K1T2_WIDE != 0) {
     const int zw = t.zcat ? 2 * RB : RB;
     const int spare = 512 - zbufs * zw - t.mt2 * RB;
     t.wide = std::max(0, std::min(t.mt2, spare / RB));
@@ -335,7 +331,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
                 std::to_string(RB) + ",S=" + std::to_string(ns) +
                 (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
-                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (getenv("MCP_K1T2_G2X2") && atoi(getenv("MCP_K1T2_G2X2")) != 0 ? ",g2x2" : "") + ",flush=" + std::to_string(t.flush)
+                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + ",flush=" + std::to_string(t.flush)
                       : std::string()) +
                 ">";
   return MCP_OK;
@@ -408,7 +404,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.wide = t.wide;
   // opt-in: GEMM2 as V P_hi with P_hi rounded to nearest (8-9% faster at c3 / c5, but normwise
   // error up to 7e-5 at reduced p -- too close to the stated 1e-4 to be the default)
-  prm.g2x2 = getenv("MCP_K1T2_G2X2") && atoi(getenv("MCP_K1T2_G2X2")) != 0 ? 1 : 0;
+  prm.g2x2 = MCP_CFG_K1T2_G2X2 ? 1 : 0;
   auto* ev = timing_begin(c, s);
   if (t.v2)
     k1t2_fg_tf32<<<t.gp * t.rbs, K1T2_THREADS, t.smem, s>>>(
@@ -476,7 +472,7 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_reduce_partials, (const double*)c->dYpart.p,
@@ -491,16 +487,8 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
 
 // k_tail_fused stages A in dynamic shared memory (beyond the 48 KB default for large n r)
 static bool k4s_ready(int64_t nr) {
-  static std::atomic<int> done{0};
-  if (!done.load()) {
-    if (cudaFuncSetAttribute(k_tail_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)k4s_smem_bytes(K4S_MAX_NR)) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return k4s_smem_bytes(nr) <= 48 * 1024;
-    }
-    done.store(1);
-  }
-  return true;
+  if (ensure_dyn_smem((const void*)k_tail_fused, k4s_smem_bytes(K4S_MAX_NR))) return true;
+  return k4s_smem_bytes(nr) <= 48 * 1024;
 }
 
 // one-CTA tail for small factor blocks; else the three-kernel tail (measured: at n r = 5000 the
@@ -563,7 +551,7 @@ int enqueue_tails_batched(mcp_ctx* c, int d, int r, int k, const double* xs, int
 int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const double* alpha_dev,
                     double alpha, double* dout, cudaStream_t s) {
   const int r = pl.r;
-  if (pl.mode != MCP_MODE_FP64 || !k1_fuses_tail(pl.k1, c->n, r) || getenv("MCP_NO_FUSED_TAIL")) {
+  if (pl.mode != MCP_MODE_FP64 || !k1_fuses_tail(pl.k1, c->n, r) || !c->opt_fused_tail) {
     int rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s);
     if (rc) return rc;
     return enqueue_finish(c, pl.d, r, dx, (const double*)c->dYw.p, alpha_dev, alpha, dout, s);
@@ -588,7 +576,7 @@ int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const doub
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_reduce_finish, (const double*)c->dYpart.p,
@@ -634,7 +622,7 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     double* dx = (double*)c->dx.p;
     int rc2;
-    if (getenv("MCP_HOST_MEMCPY")) {
+    if (MCP_CFG_HOST_MEMCPY) {
       cudaMemcpyAsync(dx, hx, xin, cudaMemcpyHostToDevice, c->stream);
       rc2 = enqueue_fg_full(c, pl, dx, dx + r + n * r, 0.0, (double*)c->dout.p, c->stream);
       cudaMemcpyAsync(c->hout, c->dout.p, xout, cudaMemcpyDeviceToHost, c->stream);
@@ -656,7 +644,7 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     it = c->graphs.emplace(key, ge).first;
   } else {
     c->last_launches =
-        (pl.mode == MCP_MODE_FP64 && k1_fuses_tail(pl.k1, c->n, r) && !getenv("MCP_NO_FUSED_TAIL"))
+        (pl.mode == MCP_MODE_FP64 && k1_fuses_tail(pl.k1, c->n, r) && c->opt_fused_tail)
             ? 2
             : (pl.mode == MCP_MODE_TF32X3 ? 4 : (pl.k1.needs_prep() ? 3 : 2)) +
                   (k4s_fits(n, r) ? 1 : 3);
@@ -759,6 +747,11 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   const int64_t minld = layout == MCP_OBS_MAJOR ? n : p;
   if (ld < minld) return c->fail(MCP_ERR_ARG, "leading dimension too small");
   c->loaded = false;
+  if (on_device) {
+    // V / nu in device memory were produced on the caller's streams (e.g. torch's), which this
+    // context's non-blocking stream does not order against: wait for all of them first.
+    CUDA_TRY(c, cudaDeviceSynchronize());
+  }
   drop_graphs(c);
   if (c->own_v32 && c->dV32) cudaFree(c->dV32);
   c->dV32 = nullptr;
@@ -964,7 +957,20 @@ int mcp_ttsv_batch(mcp_ctx* c, int d, int r, const double* A, int mode, double* 
   return MCP_OK;
 }
 
-static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, double* out) {
+// ||X||^2 partial sums.  cross == nullptr: tile-pair slice [part / nparts] of the upper triangle
+// of this context's own Gram.  cross != nullptr: slice of the TI x TJ rectangle between this
+// context's rows (I) and another row shard of the same set (J, device memory in this context's
+// layout), every tile counted twice (sharded ||X||^2, distributed.data_norm_sq_sharded).
+struct CrossShard {
+  const void* dV;
+  int64_t p_pad;
+  const double* dnu;
+  double nu_const;
+  int colmajor;   // tile-pair order of the rectangle: 0 row-major (I outer), 1 column-major
+};
+
+static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, const CrossShard* cross,
+                          double* out) {
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
   if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
   // ||X||^2 is a one-time constant: both modes run the FP64 DMMA kernel (exact superset of the
@@ -973,11 +979,15 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
     return c->fail(MCP_ERR_ARG, "unknown mode " + std::to_string(mode));
   if (nparts < 1 || part < 0 || part >= nparts) return c->fail(MCP_ERR_ARG, "bad part/nparts");
   if (!out) return c->fail(MCP_ERR_ARG, "NULL argument");
-  // K5 v2 (128 x 128 tiles) for n >= 32; the 64 x 64 variant for narrow observations
-  const bool big = c->n >= 32 && (c->p_pad % K52_T) == 0;
+  if (cross && (!cross->dV || cross->p_pad < 0 || cross->p_pad % K52_T != 0))
+    return c->fail(MCP_ERR_ARG, "cross shard must be a padded row block (multiple of 128 rows)");
+  // K5 v2 (128 x 128 tiles) for n >= 32 and every cross-shard rectangle; the 64 x 64 variant
+  // for narrow observations
+  const bool big = (c->n >= 32 || cross) && (c->p_pad % K52_T) == 0;
   const int64_t TT = big ? K52_T : K5_T;
   const int64_t T = c->p_pad / TT;
-  const int64_t pairs = T * (T + 1) / 2;
+  const int64_t TJ = cross ? cross->p_pad / K52_T : T;
+  const int64_t pairs = cross ? T * TJ : T * (T + 1) / 2;
   const int64_t b = pairs * part / nparts, e = pairs * (part + 1) / nparts;
   const int n_chunks = (int)ceil_div(c->n, big ? K52_NK : K5_NK);
   const bool f64 = c->dtype == MCP_F64;
@@ -986,7 +996,8 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
   const void* fn = big ? (f64 ? (const void*)k52_gram_power<double> : (const void*)k52_gram_power<float>)
                        : (f64 ? (const void*)k5_gram_power<double> : (const void*)k5_gram_power<float>);
   const int threads = big ? K52_THREADS : K5_THREADS;
-  CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (!ensure_dyn_smem(fn, smem))
+    return c->fail(MCP_ERR_CUDA, "cannot raise the Gram-power kernel's shared-memory limit");
   int occ = 1;
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
   if (occ < 1) occ = 1;
@@ -997,22 +1008,39 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
   if ((rc = ensure(c, c->dpart, sizeof(double) * grid))) return rc;
   if ((rc = ensure(c, c->dscalar, sizeof(double)))) return rc;
   auto* ev = timing_begin(c, c->stream);
-  if (big && f64)
+  if (big && f64) {
+    K52Cross<double> cr;
+    if (cross) {
+      cr.VJ = (const double*)cross->dV;
+      cr.nuJ = cross->dnu;
+      cr.nu_constJ = cross->nu_const;
+      cr.TJ = TJ;
+      cr.colmajor = cross->colmajor;
+    }
     k52_gram_power<double><<<(int)grid, threads, smem, c->stream>>>(
         (const double*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
-        (double*)c->dpart.p);
-  else if (big)
+        (double*)c->dpart.p, cr);
+  } else if (big) {
+    K52Cross<float> cr;
+    if (cross) {
+      cr.VJ = (const float*)cross->dV;
+      cr.nuJ = cross->dnu;
+      cr.nu_constJ = cross->nu_const;
+      cr.TJ = TJ;
+      cr.colmajor = cross->colmajor;
+    }
     k52_gram_power<float><<<(int)grid, threads, smem, c->stream>>>(
         (const float*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
-        (double*)c->dpart.p);
-  else if (f64)
+        (double*)c->dpart.p, cr);
+  } else if (f64) {
     k5_gram_power<double><<<(int)grid, threads, smem, c->stream>>>(
         (const double*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
         (double*)c->dpart.p);
-  else
+  } else {
     k5_gram_power<float><<<(int)grid, threads, smem, c->stream>>>(
         (const float*)c->dV, c->ldv, n_chunks, c->dnu, c->nu_const, d, T, b, e,
         (double*)c->dpart.p);
+  }
   timing_end(ev, c->stream);
   k_ordered_sum<<<1, 32, 0, c->stream>>>((const double*)c->dpart.p, (int)grid,
                                          (double*)c->dscalar.p);
@@ -1020,20 +1048,43 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, dou
   CUDA_TRY(c, cudaMemcpyAsync(out, c->dscalar.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->last_launches = 2;
-  c->variant = std::string(big ? "k52_gram_dmma128" : "k5_gram_dmma64") + (f64 ? "<f64>" : "<f32>");
+  c->variant = std::string(big ? "k52_gram_dmma128" : "k5_gram_dmma64") + (f64 ? "<f64>" : "<f32>") +
+               (cross ? "[cross]" : "");
   return MCP_OK;
 }
 
 int mcp_data_norm_sq(mcp_ctx* c, int d, int mode, double* out) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
-  return data_norm_part(c, d, mode, 0, 1, out);
+  return data_norm_part(c, d, mode, 0, 1, nullptr, out);
 }
 
 int mcp_data_norm_sq_part(mcp_ctx* c, int d, int mode, int part, int nparts, double* out) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
-  return data_norm_part(c, d, mode, part, nparts, out);
+  return data_norm_part(c, d, mode, part, nparts, nullptr, out);
+}
+
+int mcp_data_norm_sq_cross(mcp_ctx* c, const void* dVJ, int64_t p_pad_J, const double* dnuJ,
+                           double nu_const_J, int d, int mode, int pair_order, int part, int nparts,
+                           double* out) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  if (pair_order != 0 && pair_order != 1) return c->fail(MCP_ERR_ARG, "pair_order must be 0 or 1");
+  CrossShard cs{dVJ, p_pad_J, dnuJ, nu_const_J, pair_order};
+  return data_norm_part(c, d, mode, part, nparts, &cs, out);
+}
+
+int mcp_obs_device_view(const mcp_ctx* c, void** dV, int64_t* ldv, int64_t* p_pad, int* dtype,
+                        const double** dnu, double* nu_const) {
+  if (!c || !c->loaded) return MCP_ERR_STATE;
+  if (dV) *dV = c->dV;
+  if (ldv) *ldv = c->ldv;
+  if (p_pad) *p_pad = c->p_pad;
+  if (dtype) *dtype = c->dtype;
+  if (dnu) *dnu = c->dnu;
+  if (nu_const) *nu_const = c->nu_const;
+  return MCP_OK;
 }
 
 int mcp_fg_partial_device(mcp_ctx* c, int d, int r, const double* dx, int mode, double* dYw,
@@ -1093,6 +1144,19 @@ int mcp_fg_device(mcp_ctx* c, int d, int r, const double* dx, double alpha, int 
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   return enqueue_fg_full(c, pl, dx, nullptr, alpha, dout, s);
+}
+
+int mcp_set_option(mcp_ctx* c, int key, int64_t value) {
+  if (!c) return MCP_ERR_ARG;
+  Guard gd(c);
+  switch (key) {
+    case MCP_OPT_FUSED_TAIL:
+      if (c->opt_fused_tail != (value != 0)) drop_graphs(c);
+      c->opt_fused_tail = value != 0;
+      return MCP_OK;
+    default:
+      return c->fail(MCP_ERR_ARG, "unknown option " + std::to_string(key));
+  }
 }
 
 int mcp_set_kernel_timing(mcp_ctx* c, int enable) {

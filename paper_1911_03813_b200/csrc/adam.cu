@@ -259,6 +259,9 @@ extern "C" int mcp_gather_rows(mcp_ctx* c, const int64_t* idx, int64_t s, void* 
     return c->fail(MCP_ERR_ARG, "unsupported destination dtype");
   for (int64_t l = 0; l < s; ++l)
     if (idx[l] < 0 || idx[l] >= c->p) return c->fail(MCP_ERR_ARG, "row index out of range");
+  // dst belongs to the caller (e.g. a fresh torch allocation whose memory earlier work on the
+  // caller's streams may still touch): order the gather after everything on the device
+  CUDA_TRY(c, cudaDeviceSynchronize());
   int64_t* didx = nullptr;
   CUDA_TRY(c, cudaMalloc(&didx, sizeof(int64_t) * s));
   cudaError_t e = cudaMemcpyAsync(didx, idx, sizeof(int64_t) * s, cudaMemcpyHostToDevice,

@@ -73,6 +73,8 @@ struct mcp_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
   int last_launches = 0;
   std::string variant = "none";
+  // run-time options (mcp_set_option)
+  bool opt_fused_tail = true;   // MCP_OPT_FUSED_TAIL: K1 -> fused reduce+finish when eligible
 
   // cached device-resident L-BFGS workspace (lbfgs.cu); freed with the graphs
   void* lbfgs_ws = nullptr;

@@ -6,13 +6,16 @@
 #include <cstdlib>
 
 #include "momentcp_b200.h"
+#include "tuning.h"
 #include "k1_dispatch.h"
 #include "k1_fp64.cuh"
 #include "tail_pieces.cuh"
 #include "k1s_fp64.cuh"
 #include "k1p_fp64.cuh"
 #include "k1q_fp64.cuh"
+#if MCP_WITH_K1R
 #include "k1r_fp64.cuh"
+#endif
 
 namespace mcp {
 
@@ -78,8 +81,6 @@ const Entry kTableG[] = {MCP_K1G_E(double, MCP_F64, 16), MCP_K1G_E(double, MCP_F
                          MCP_K1G_E(double, MCP_F64, 64), MCP_K1G_E(float, MCP_F32, 16),
                          MCP_K1G_E(float, MCP_F32, 32),  MCP_K1G_E(float, MCP_F32, 64)};
 constexpr int kEntries = sizeof(kTable) / sizeof(kTable[0]);
-std::atomic<int> g_occ[kEntries];
-std::atomic<bool> g_occ_init{false};
 
 int max_rb_for(int mtw) {
   switch (mtw) {
@@ -90,24 +91,31 @@ int max_rb_for(int mtw) {
   }
 }
 
+// Resident CTAs per SM of K1 table entry e on the current device, cached per (entry, device);
+// the dynamic shared-memory limit is raised per device through ensure_dyn_smem.
 int occupancy(int e) {
-  if (!g_occ_init.exchange(true))
-    for (int i = 0; i < kEntries; ++i) g_occ[i].store(-1);
-  int o = g_occ[e].load();
-  if (o >= 0) return o;
-  const Entry& en = kTable[e];
-  if (cudaFuncSetAttribute(en.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)en.smem) !=
-      cudaSuccess) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
     (void)cudaGetLastError();
     return 0;
   }
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({e, dev});
+    if (it != cache.end()) return it->second;
+  }
+  const Entry& en = kTable[e];
+  if (!ensure_dyn_smem(en.fn, en.smem)) return 0;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, en.fn, K1_THREADS, en.smem) !=
       cudaSuccess) {
     (void)cudaGetLastError();
     return 0;
   }
-  g_occ[e].store(occ);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[{e, dev}] = occ;
   return occ;
 }
 
@@ -161,7 +169,7 @@ void launch_q(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k1q_fg_pairs<NTM, TAIL, MT2, KH>, prm);
@@ -177,6 +185,7 @@ const EntryS kTableQ[] = {MCP_K1Q_COLS(1, 1),  MCP_K1Q_COLS(3, 5),  MCP_K1Q_COLS
                           MCP_K1Q_COLS(9, 17), MCP_K1Q_COLS(13, 25), MCP_K1Q_COLS(15, 29),
                           MCP_K1Q_COLS(16, 33)};
 
+#if MCP_WITH_K1R
 // ---------------- K1R (warp triads: the GEMM1 role split by columns; r mod 8 in 1..2) ----------
 template <int NTM, int TAIL, int MT2, int KH>
 void launch_r(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
@@ -187,7 +196,7 @@ void launch_r(const K1SParams& prm, int grid, size_t smem, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k1r_fg_triads<NTM, TAIL, MT2, KH>, prm);
@@ -200,6 +209,7 @@ const EntryS kTableR[] = {MCP_K1R_COLS(1, 1),  MCP_K1R_COLS(3, 5),  MCP_K1R_COLS
                           MCP_K1R_COLS(9, 17), MCP_K1R_COLS(13, 25), MCP_K1R_COLS(15, 29),
                           MCP_K1R_COLS(16, 33)};
 constexpr int kEntriesR = sizeof(kTableR) / sizeof(kTableR[0]);
+#endif
 
 bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
   if (n > 128) return false;
@@ -208,7 +218,7 @@ bool select_stream(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Vari
   const int mth_need = (MT + 1) / 2, kh_need = kst;
   int ntm, tail;
   if (r <= 8) { ntm = 1; tail = 0; }
-  else if (r <= 10 && !getenv("MCP_K1S_NO_TAIL")) { ntm = 1; tail = r - 8; }
+  else if (r <= 10 && MCP_CFG_DFMA_TAIL) { ntm = 1; tail = r - 8; }
   else { ntm = 2; tail = 0; }          // r > 16: several 16-column blocks, one per CTA
   int e = -1;
   for (int i = 0; i < kEntriesS && e < 0; ++i)
@@ -285,14 +295,20 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
                   int flavor) {
   if (n > 128) return false;
   const bool specialised = flavor >= 1;
+#if MCP_WITH_K1R
   const EntryS* table = flavor == 2 ? kTableR : specialised ? kTableQ : kTableP;
   const int n_entries = flavor == 2 ? kEntriesR : kEntriesS;
+#else
+  if (flavor == 2) return false;
+  const EntryS* table = specialised ? kTableQ : kTableP;
+  const int n_entries = kEntriesS;
+#endif
   const int MT = (int)ceil_div(n, 8);
   const int kst = (int)(ldv / 4);
   const int mth_need = (MT + 1) / 2, kh_need = kst;
   int ntm, tail;
   if (r <= 8) { ntm = 1; tail = 0; }
-  else if (r <= 10 && !getenv("MCP_K1S_NO_TAIL")) { ntm = 1; tail = r - 8; }
+  else if (r <= 10 && MCP_CFG_DFMA_TAIL) { ntm = 1; tail = r - 8; }
   else { ntm = 2; tail = 0; }
   if (flavor == 2 && tail == 0) return false;   // triads only pay off with DFMA tail columns
   int e = -1;
@@ -303,10 +319,19 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   if (e < 0) return false;
   const int cw = 8 * ntm + tail;
   const size_t slab = (size_t)K1S_SR * ldv * 8;
+#if MCP_WITH_K1R
   const int NPR = flavor == 2 ? K1R_TRIADS : specialised ? K1Q_PAIRS : K1P_PAIRS;
+#else
+  const int NPR = specialised ? K1Q_PAIRS : K1P_PAIRS;
+#endif
+#if MCP_WITH_K1R
   const size_t fixed = flavor == 2    ? k1r_fixed_bytes(table[e].KH, ntm, cw)
                        : specialised ? k1q_fixed_bytes(table[e].KH, ntm, cw)
                                      : k1p_fixed_bytes(table[e].KH, ntm, cw);
+#else
+  const size_t fixed = specialised ? k1q_fixed_bytes(table[e].KH, ntm, cw)
+                                   : k1p_fixed_bytes(table[e].KH, ntm, cw);
+#endif
   const size_t budget = 227 * 1024 - 1024 - fixed;
   int SP = (int)(budget / ((size_t)NPR * (slab + 8)));
   if (SP > 4) SP = 4;
@@ -372,19 +397,19 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
                std::string& why) {
   v = K1Variant();
   // K1R is opt-in (MCP_K1R=1): at c2 it measured 5% slower than K1Q
-  if (dtype == MCP_F64 && getenv("MCP_K1R") &&
-      select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, 2))
-    return true;
+#if MCP_WITH_K1R
+  if (dtype == MCP_F64 && select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, 2)) return true;
+#endif
   v = K1Variant();
-  if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1Q") &&
+  if (dtype == MCP_F64 && MCP_CFG_K1Q &&
       select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, 1))
     return true;
   v = K1Variant();
-  if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1P") &&
+  if (dtype == MCP_F64 && MCP_CFG_K1P &&
       select_pairs(n, r, p_pad, obs_pitch(dtype, n), sms, v, 0))
     return true;
   v = K1Variant();
-  if (dtype == MCP_F64 && !getenv("MCP_DISABLE_K1S") &&
+  if (dtype == MCP_F64 && MCP_CFG_K1S &&
       select_stream(n, r, p_pad, obs_pitch(dtype, n), sms, v))
     return true;
   v = K1Variant();
@@ -401,8 +426,8 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
   }
   int rb_g = 16;
   while (rb_g < (int)round_up(r, 8) && rb_g < 64) rb_g *= 2;
-  const bool use_g = getenv("MCP_FORCE_K1G") ? true : (rb_g >= 4 * rb_k1 || n > 2048);
-  if (!getenv("MCP_DISABLE_K1G") && use_g && n > 128) {   // any n: Y lives in L2
+  const bool use_g = MCP_CFG_FORCE_K1G ? true : (rb_g >= 4 * rb_k1 || n > 2048);
+  if (MCP_CFG_K1G && use_g && n > 128) {   // any n: Y lives in L2
     const int rb = rb_g;
     int e = -1;
     for (int i = 0; i < 6; ++i)
@@ -508,8 +533,13 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     sp.spc = v.MTW2;
     sp.Ypart = Ypart;
     sp.wpart = wpart;
-    (v.kind == 1 ? kTableS : v.kind == 3 ? kTableP : v.kind == 6 ? kTableR : kTableQ)[v.entry].launch(sp, v.grid, v.smem,
-                                                                               s);
+#if MCP_WITH_K1R
+    if (v.kind == 6) {
+      kTableR[v.entry].launch(sp, v.grid, v.smem, s);
+      return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
+    }
+#endif
+    (v.kind == 1 ? kTableS : v.kind == 3 ? kTableP : kTableQ)[v.entry].launch(sp, v.grid, v.smem, s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }
   K1Params prm;

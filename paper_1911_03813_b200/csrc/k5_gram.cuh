@@ -170,11 +170,25 @@ __device__ __forceinline__ void k52_load(VT* dst, const VT* __restrict__ V, int6
   }
 }
 
+// Second operand of a cross-shard reduction (sharded ||X||^2): the J tiles come from another
+// row shard VJ (same pitch and dtype), the tile pairs (I, J) cover the whole TI x TJ rectangle
+// in row-major order (pair k -> I = k / TJ, J = k % TJ; colmajor: I = k % TI, J = k / TI), every
+// tile counts twice (the (J, I) half of the symmetric Gram lives on the other shard's side).
+// VJ == nullptr: the upper triangle of one shard's own Gram (off-diagonal tiles x2).
+template <typename VT>
+struct K52Cross {
+  const VT* VJ = nullptr;
+  const double* nuJ = nullptr;
+  double nu_constJ = 0.0;
+  int64_t TJ = 0;
+  int colmajor = 0;
+};
+
 template <typename VT>
 __global__ void __launch_bounds__(K52_THREADS, 1)
     k52_gram_power(const VT* __restrict__ V, int64_t ldv, int n_chunks, const double* __restrict__ nu,
                    double nu_const, int d, int64_t T, int64_t pair_begin, int64_t pair_end,
-                   double* __restrict__ part) {
+                   double* __restrict__ part, K52Cross<VT> cross) {
   extern __shared__ __align__(16) unsigned char smem_raw5[];
   VT* sI[2];
   VT* sJ[2];
@@ -188,22 +202,37 @@ __global__ void __launch_bounds__(K52_THREADS, 1)
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;   // 4 x 4 warps, 32 x 32 each
   double tsum = 0.0;
+  const bool rect = cross.VJ != nullptr;
+  const VT* __restrict__ VJ = rect ? cross.VJ : V;
+  const double* __restrict__ nuJ = rect ? cross.nuJ : nu;
+  const double nu_cJ = rect ? cross.nu_constJ : nu_const;
+  auto decode = [&](int64_t k, int64_t& I_, int64_t& J_) {
+    if (rect && cross.colmajor) {
+      I_ = k % T;
+      J_ = k / T;
+    } else if (rect) {
+      I_ = k / cross.TJ;
+      J_ = k % cross.TJ;
+    } else {
+      k5_decode(k, T, I_, J_);
+    }
+  };
 
   // one cp.async pipeline over the flat (pair, chunk) sequence: the last chunk of a pair
   // prefetches chunk 0 of the CTA's next pair, so no tile pair starts on an exposed load
   int64_t pair = pair_begin + blockIdx.x;
   int64_t I = 0, J = 0;
   if (pair < pair_end) {
-    k5_decode(pair, T, I, J);
+    decode(pair, I, J);
     k52_load<VT>(sI[0], V, ldv, I * K52_T, 0);
-    k52_load<VT>(sJ[0], V, ldv, J * K52_T, 0);
+    k52_load<VT>(sJ[0], VJ, ldv, J * K52_T, 0);
     cp_async_commit();
   }
   int s = 0;   // buffer of the chunk being consumed (continues across pairs)
   for (; pair < pair_end; pair += gridDim.x) {
     const int64_t npair = pair + gridDim.x;
     int64_t nI = 0, nJ = 0;
-    if (npair < pair_end) k5_decode(npair, T, nI, nJ);
+    if (npair < pair_end) decode(npair, nI, nJ);
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -216,7 +245,7 @@ __global__ void __launch_bounds__(K52_THREADS, 1)
         const int64_t li = c + 1 < n_chunks ? I : nI, lj = c + 1 < n_chunks ? J : nJ;
         const int lc = c + 1 < n_chunks ? c + 1 : 0;
         k52_load<VT>(s ? sI[0] : sI[1], V, ldv, li * K52_T, lc);
-        k52_load<VT>(s ? sJ[0] : sJ[1], V, ldv, lj * K52_T, lc);
+        k52_load<VT>(s ? sJ[0] : sJ[1], VJ, ldv, lj * K52_T, lc);
         cp_async_commit();
         cp_async_wait<1>();
       } else {
@@ -251,11 +280,11 @@ __global__ void __launch_bounds__(K52_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t l2 = J * K52_T + 32 * wn + 8 * nt + 2 * t + e;
-          const double nl2 = nu ? nu[l2] : nu_const;
+          const double nl2 = nuJ ? nuJ[l2] : nu_cJ;
           tile_sum += (nl * nl2) * rm_pow(acc[mt][nt][e], d);
         }
     }
-    tsum += (I == J) ? tile_sum : 2.0 * tile_sum;
+    tsum += (I == J && !rect) ? tile_sum : 2.0 * tile_sum;
     I = nI;
     J = nJ;
   }

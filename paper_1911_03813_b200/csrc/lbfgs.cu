@@ -679,9 +679,8 @@ struct LbEngine {
     const size_t stage_bytes = sizeof(double) * (size_t)N * (2 * (size_t)m + 2);
     dir_smem = stage_bytes <= 192 * 1024 ? stage_bytes : 0;
     int rc;
-    if (dir_smem)
-      CUDA_TRY(c, cudaFuncSetAttribute(k_lbb_direction, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)dir_smem));
+    if (dir_smem && !mcp::ensure_dyn_smem((const void*)k_lbb_direction, dir_smem))
+      return c->fail(MCP_ERR_CUDA, "cannot raise the two-loop kernel's shared-memory limit");
     const size_t K = (size_t)k, M1 = (size_t)m + 1;
     D.N = N;
     D.m = m;

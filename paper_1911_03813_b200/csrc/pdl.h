@@ -1,13 +1,15 @@
 // Programmatic dependent launch (PDL) helpers for the small-kernel chains (unfused tail,
 // stochastic path): a kernel launched with launch_pdl may start while its predecessor drains,
 // so every such kernel calls pdl_wait() before touching anything the predecessor writes.
-// pdl_wait() / pdl_trigger() are no-ops for plain launches.  MCP_NO_PDL=1 disables the launch
-// attribute everywhere (A/B switch).
+// pdl_wait() / pdl_trigger() are no-ops for plain launches.  -DMCP_CFG_PDL=0 (tools/build_variant.py)
+// disables the launch attribute everywhere (A/B builds).
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+
+#include "tuning.h"
 #include <utility>
 
 namespace mcp {
@@ -22,10 +24,7 @@ __device__ __forceinline__ void pdl_enter() {
   pdl_trigger();
 }
 
-inline bool pdl_enabled() {
-  static const bool on = getenv("MCP_NO_PDL") == nullptr;
-  return on;
-}
+inline bool pdl_enabled() { return MCP_CFG_PDL != 0; }
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

@@ -25,6 +25,7 @@
 #include "ctx.h"
 #include "mcp_common.cuh"
 #include "tail_pieces.cuh"
+#include "pdl.h"
 
 using namespace mcp;
 using namespace mcp_internal;
@@ -32,7 +33,16 @@ using namespace mcp_internal;
 namespace {
 
 constexpr int PR_T = 256;
-constexpr long long PR_SPIN_LIMIT = 1ll << 32;   // ~2 s at 1.9 GHz, then report and go on
+// A peer whose flag has not arrived after this long (globaltimer ns) is declared lost: the
+// kernel sets *err and writes NaN into every output, so a stale or partial sum can never be
+// consumed as a result (PeerExchange.step / bench.py check err and raise).
+constexpr unsigned long long PR_WAIT_LIMIT_NS = 30ull * 1000000000ull;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
   asm volatile("st.release.sys.global.b64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
@@ -73,9 +83,9 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
   if (threadIdx.x == 0) {
     ok = 1;
     for (int k = 0; k < world; ++k) {
-      const long long t0 = clock64();
-      while (ld_acquire_sys(my_flags + k) < epoch) {
-        if (clock64() - t0 > PR_SPIN_LIMIT) {
+      const unsigned long long t0 = globaltimer_ns();
+      while (ok && ld_acquire_sys(my_flags + k) < epoch) {
+        if (globaltimer_ns() - t0 > PR_WAIT_LIMIT_NS) {
           ok = 0;
           atomicExch(err, 1);
           break;
@@ -84,6 +94,8 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
     }
   }
   __syncthreads();
+  const bool good = ok != 0;
+  const double bad = __longlong_as_double(0x7ff8000000000000ll);   // quiet NaN
   const double* lam = x;
   const int64_t nr = (int64_t)n * r;
   if (blockIdx.x + 1 < gridDim.x) {
@@ -91,6 +103,7 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
          e += (int64_t)(gridDim.x - 1) * PR_T) {
       double y = 0.0;
       for (int k = 0; k < world; ++k) y += ld_volatile_sys(parts[k] + e);
+      if (!good) y = bad;
       if (light) {
         const int j = (int)(e / n), i = (int)(e % n);
         const double m = tail_m_entry(x, sC, n, r, i, j);
@@ -106,6 +119,7 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
   for (int j = threadIdx.x; j < r; j += PR_T) {
     double w = 0.0;
     for (int k = 0; k < world; ++k) w += ld_volatile_sys(parts[k] + nr + j);
+    if (!good) w = bad;
     if (light) {
       const double u = tail_u_entry(sG, sC, lam, r, j);
       s_w[j] = w;
@@ -120,9 +134,8 @@ __global__ void k_peer_reduce_finish(const double* const* __restrict__ parts,
     double lu = 0.0, wl = 0.0;
     for (int j = 0; j < r; ++j) lu += lam[j] * s_u[j];
     for (int j = 0; j < r; ++j) wl += s_w[j] * lam[j];
-    out[0] = alpha + lu - 2.0 * wl;
+    out[0] = good ? alpha + lu - 2.0 * wl : bad;
   }
-  (void)ok;
 }
 
 }  // namespace
@@ -168,7 +181,7 @@ extern "C" int mcp_peer_reduce_finish(mcp_ctx* c, int d, int r, const double* dx
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("MCP_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_peer_reduce_finish, (const double* const*)part_ptrs,

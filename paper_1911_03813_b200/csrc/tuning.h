@@ -1,0 +1,76 @@
+// Compile-time tuning switches of the product library.
+//
+// The shipped build reads no environment variables: every kernel-selection and schedule choice
+// below is fixed at compile time to the measured default (DESIGN.md section 4 records the A/B
+// measurements behind each).  Experiment builds override them with -D flags through
+// tools/build_variant.py (e.g. `python tools/build_variant.py nopdl -DMCP_CFG_PDL=0`), never in
+// the product .so.  The one per-context run-time option (the fused reduce+finish, used by the
+// bitwise fused-vs-unfused test) is set through mcp_set_option().
+#pragma once
+
+// programmatic dependent launch along the kernel chains
+#ifndef MCP_CFG_PDL
+#define MCP_CFG_PDL 1
+#endif
+// host evaluations: x pulled from mapped pinned memory by a kernel (0) or copy-engine memcpys (1)
+#ifndef MCP_CFG_HOST_MEMCPY
+#define MCP_CFG_HOST_MEMCPY 0
+#endif
+// FP64 K1 family for n <= 128: K1Q (warp-specialised pairs), then K1P, then K1S fallbacks
+#ifndef MCP_CFG_K1Q
+#define MCP_CFG_K1Q 1
+#endif
+#ifndef MCP_CFG_K1P
+#define MCP_CFG_K1P 1
+#endif
+#ifndef MCP_CFG_K1S
+#define MCP_CFG_K1S 1
+#endif
+// r mod 8 in 1..2 runs as DFMA tail columns (0: pad to DMMA-only columns, measured 22% slower)
+#ifndef MCP_CFG_DFMA_TAIL
+#define MCP_CFG_DFMA_TAIL 1
+#endif
+// K1R warp triads (experiment, 5% slower than K1Q at c2): not compiled into the product build
+#ifndef MCP_WITH_K1R
+#define MCP_WITH_K1R 0
+#endif
+// large-n FP64: K1W (TMA-staged, warp-specialised) when it has a variant for the shape
+#ifndef MCP_CFG_K1W
+#define MCP_CFG_K1W 1
+#endif
+// K1G (Y partial in L2) for large n when K1's register-bound column block is <= 1/4 of K1G's
+#ifndef MCP_CFG_K1G
+#define MCP_CFG_K1G 1
+#endif
+#ifndef MCP_CFG_FORCE_K1G
+#define MCP_CFG_FORCE_K1G 0
+#endif
+// fast mode: K1T2 (precomputed V_lo) unless 1 -> the in-kernel split K1T
+#ifndef MCP_CFG_K1T_V1
+#define MCP_CFG_K1T_V1 0
+#endif
+#ifndef MCP_CFG_K1T2_SERIAL
+#define MCP_CFG_K1T2_SERIAL 1
+#endif
+#ifndef MCP_CFG_K1T2_HINT
+#define MCP_CFG_K1T2_HINT 1
+#endif
+#ifndef MCP_CFG_K1T2_FLUSH
+#define MCP_CFG_K1T2_FLUSH 16
+#endif
+#ifndef MCP_CFG_K1T2_RB
+#define MCP_CFG_K1T2_RB 0          // 0: widest column block TMEM allows
+#endif
+#ifndef MCP_CFG_K1T2_WIDE
+#define MCP_CFG_K1T2_WIDE 1
+#endif
+#ifndef MCP_CFG_K1T2_G2_3D
+#define MCP_CFG_K1T2_G2_3D 1
+#endif
+#ifndef MCP_CFG_K1T_ZCAT
+#define MCP_CFG_K1T_ZCAT 1
+#endif
+// GEMM2 as V P_hi with round-to-nearest P_hi (8-9% faster, error up to 7e-5 normwise): off
+#ifndef MCP_CFG_K1T2_G2X2
+#define MCP_CFG_K1T2_G2X2 0
+#endif

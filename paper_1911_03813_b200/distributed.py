@@ -8,9 +8,14 @@ every rank runs the O(n r^2) tail (mcp_fg_finish_device) on the reduced piece, s
 identical f and gradients.  Uniform weights are 1/p_total on every shard (dense.py:90-91 over
 the whole set).
 
-||X||^2 (implicit.py:116-121) couples every pair of observations: each rank holds the whole V
-(all-gathered once, 0.41 GB at config 4), takes a contiguous, equal-work slice of the
-upper-triangular tile-pair list, and the per-rank partial sums are combined in rank order.
+||X||^2 (implicit.py:116-121) couples every pair of observations.  ``data_norm_sq_sharded``
+works on the row shards themselves (no rank ever holds the whole V): rank k computes its own
+shard's triangle, then the shards travel one hop per step around a ring (NCCL send/recv over
+NVLink, the next hop in flight while the current shard's rectangle is reduced), and at step s
+rank k reduces the rectangle (k, k+s) -- floor(W/2) steps cover every unordered shard pair once
+(for even W the last pair is split in half between its two ranks).  The W partial sums are
+all-gathered and added in rank order (deterministic, identical on every rank).
+``data_norm_sq_split`` is the replicated variant (every rank holds all of V).
 
 The per-shard compute is pluggable only so the host-side logic (shard bounds, collective,
 tail) can be exercised on CPU with gloo in tests; the product path is the CUDA backend, which
@@ -70,6 +75,15 @@ def device_finish(obs: ObservationSet, lam, A, d: int, alpha: float, Yw):
     return float(h[0]), h[1:1 + r].copy(), h[1 + r:].reshape((n, r), order="F").copy()
 
 
+class _CudaBytes:
+    """Zero-copy torch view (uint8) of device memory owned by the native context."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
 class CudaShardBackend:
     """Per-shard compute on this rank's GPU through the C ABI."""
 
@@ -82,6 +96,40 @@ class CudaShardBackend:
 
     def finish(self, lam, A, d, alpha, Yw):
         return device_finish(self.obs, lam, A, d, alpha, Yw)
+
+    # -- sharded ||X||^2 (ring pass) -------------------------------------------------------
+    def shard(self):
+        """(rows bytes tensor, padded rows, weights bytes tensor or None, uniform weight)."""
+        torch = _torch()
+        ctx = self.obs.device_context()
+        v = ctx.obs_device_view()
+        elem = 8 if v["dtype"] == 0 else 4
+        dev = torch.device("cuda", ctx.device)
+        rows = torch.as_tensor(_CudaBytes(v["ptr"], v["p_pad"] * v["ldv"] * elem), device=dev)
+        nu = (torch.as_tensor(_CudaBytes(v["nu"], v["p_pad"] * 8), device=dev)
+              if v["nu"] else None)
+        self._row_bytes = v["ldv"] * elem
+        return rows, v["p_pad"], nu, v["nu_const"]
+
+    def row_bytes(self) -> int:
+        return self._row_bytes
+
+    def buffer(self, nbytes: int):
+        torch = _torch()
+        ctx = self.obs.device_context()
+        return torch.empty(int(nbytes), dtype=torch.uint8, device=torch.device("cuda", ctx.device))
+
+    def self_sum(self, d) -> float:
+        return self.obs.device_context().data_norm_sq(d, self.mode)
+
+    def cross_sum(self, rows, p_pad, nu, nu_const, d, part, nparts, order) -> float:
+        torch = _torch()
+        ctx = self.obs.device_context()
+        # the library's stream is not ordered after the receive on torch's stream
+        torch.cuda.current_stream(torch.device("cuda", ctx.device)).synchronize()
+        return ctx.data_norm_sq_cross(rows.data_ptr(), p_pad, nu.data_ptr() if nu is not None
+                                      else None, nu_const, d, self.mode, part, nparts,
+                                      order)
 
 
 class ShardedObservationSet:
@@ -124,9 +172,12 @@ def fg_implicit_sharded(sobs: ShardedObservationSet, lam, A, d: int, alpha: floa
     return FgResult(f, g_lam, g_A, time.perf_counter() - start, eval_kind)
 
 
-def packed_fg_sharded(sobs: ShardedObservationSet, d: int, r: int, alpha: float = 0.0):
+def packed_fg_sharded(sobs: ShardedObservationSet, d: int, r: int, alpha: float = 0.0,
+                      mode: str | None = None):
     """packed_fg_implicit for a sharded set (every rank calls it with the same x)."""
     n = sobs.n
+    if mode is not None and isinstance(sobs.backend, CudaShardBackend):
+        sobs.backend.mode = mode
 
     def fg(x):
         x = np.asarray(x, dtype=float)
@@ -135,6 +186,10 @@ def packed_fg_sharded(sobs: ShardedObservationSet, d: int, r: int, alpha: float 
         return res.f, pack(res.g_lam, res.g_A)
 
     return fg
+
+
+class PeerExchangeError(RuntimeError):
+    """A peer's partial never arrived (lost rank or > 30 s skew); see PeerExchange.step."""
 
 
 class PeerExchange:
@@ -187,14 +242,108 @@ class PeerExchange:
                                     self.flags.data_ptr(), self.world, epoch, alpha, out_ptr,
                                     self.err.data_ptr(), stream)
 
-    def step(self, d, x_ptr, mode, alpha, out_ptr, stream):
-        """One sharded evaluation x -> out = [f ; g_lam ; vec_F(g_A)] on every rank."""
+    def step(self, d, x_ptr, mode, alpha, out_ptr, stream, check: bool = True):
+        """One sharded evaluation x -> out = [f ; g_lam ; vec_F(g_A)] on every rank.
+
+        A peer that never publishes its partial (csrc/peer.cu: 30 s bound) makes the kernel
+        write NaN into every output and set the error flag.  With ``check`` (default) the step
+        waits for the stream and raises ``PeerExchangeError``; timed loops pass
+        ``check=False`` and call :meth:`raise_if_failed` once afterwards (outputs of a failed
+        step are NaN either way, never a stale sum)."""
         self.epoch += 1
         self.partial(d, x_ptr, mode, stream, self.epoch)
         self.reduce_finish(d, x_ptr, alpha, out_ptr, stream, self.epoch)
+        if check:
+            self.raise_if_failed()
 
     def failed(self) -> bool:
+        """True once any reduce of this exchange timed out waiting for a peer (syncs)."""
         return bool(self.err.item())
+
+    def raise_if_failed(self) -> None:
+        if self.failed():
+            raise PeerExchangeError(
+                f"rank {self.rank}: a peer's partial did not arrive within the exchange's wait "
+                f"bound (epoch <= {self.epoch}); outputs were poisoned with NaN")
+
+
+def data_norm_sq_sharded(sobs: ShardedObservationSet, d: int, group=None,
+                         mode: str | None = None, backend=None) -> float:
+    """||X||^2 of a row-sharded set (implicit.py:116-121), shards passed around a ring.
+
+    Every rank calls it; all ranks return the same value (partials summed in rank order).
+    The rounding differs from the single-GPU reduction only by the association of the tile
+    sums (fixed for a given world size).
+    """
+    torch = _torch()
+    import torch.distributed as dist
+
+    if d < 2:
+        raise ValueError(f"order must be >= 2, got {d}")
+    group = group if group is not None else sobs.group
+    world, rank = 1, 0
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    be = backend if backend is not None else CudaShardBackend(sobs.local, mode)
+    if world == 1:
+        return float(be.self_sum(d))
+    rows, p_pad, nu, nu_const = be.shard()
+    rb = be.row_bytes()
+    dev = rows.device
+    # every rank's padded row count, weights flag and uniform weight
+    meta = torch.tensor([float(p_pad), 1.0 if nu is not None else 0.0, nu_const],
+                        dtype=torch.float64, device=dev)
+    metas = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta, group=group)
+    metas = [m.cpu().tolist() for m in metas]
+    if len({m[1] for m in metas}) != 1:
+        raise ValueError("every shard must have explicit weights, or none")
+    with_nu = metas[0][1] != 0.0
+    pmax = int(max(m[0] for m in metas))
+    gr = (lambda k: dist.get_global_rank(group, k)) if group is not None else (lambda k: k)
+    left, right = gr((rank - 1) % world), gr((rank + 1) % world)
+    bufs = [be.buffer(pmax * rb) for _ in range(2)]
+    nubufs = [be.buffer(pmax * 8) for _ in range(2)] if with_nu else [None, None]
+    steps = world // 2
+
+    def exchange(cur_rows, cur_nu, src_shard, slot):
+        # send the shard we hold to the left neighbour, receive the next one from the right
+        nb = int(metas[src_shard][0])
+        ops = [dist.P2POp(dist.isend, cur_rows, left, group),
+               dist.P2POp(dist.irecv, bufs[slot][:nb * rb], right, group)]
+        if with_nu:
+            ops += [dist.P2POp(dist.isend, cur_nu, left, group),
+                    dist.P2POp(dist.irecv, nubufs[slot][:nb * 8], right, group)]
+        return dist.batch_isend_irecv(ops)
+
+    total = float(be.self_sum(d))
+    cur_rows, cur_nu = rows, nu
+    reqs = exchange(cur_rows, cur_nu, (rank + 1) % world, 0)
+    for s in range(1, steps + 1):
+        for q in reqs:
+            q.wait()
+        src = (rank + s) % world
+        nb = int(metas[src][0])
+        slot = (s - 1) % 2
+        cur_rows = bufs[slot][:nb * rb]
+        cur_nu = nubufs[slot][:nb * 8] if with_nu else None
+        if s < steps:   # next hop in flight while this rectangle is reduced
+            reqs = exchange(cur_rows, cur_nu, (rank + s + 1) % world, s % 2)
+        part, nparts, order = 0, 1, 0
+        if world % 2 == 0 and s == steps:
+            # shards k and k + W/2 meet from both sides: the lower rank takes the first half of
+            # the rectangle with its own tiles outer, the upper rank the second half with the
+            # lower rank's tiles outer -- together every tile pair exactly once
+            part, nparts, order = (0, 2, 0) if rank < world // 2 else (1, 2, 1)
+        total += float(be.cross_sum(cur_rows, nb, cur_nu, metas[src][2], d, part, nparts,
+                                    order))
+    mine = torch.tensor([total], dtype=torch.float64, device=dev)
+    parts = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    out = 0.0
+    for t in parts:
+        out += float(t.item())
+    return out
 
 
 def data_norm_sq_split(obs_full: ObservationSet, d: int, group=None, mode: str | None = None,

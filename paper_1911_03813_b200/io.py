@@ -56,12 +56,13 @@ def read_observations_binary(path: str, *, rows: tuple[int, int] | None = None,
         raise ValueError(f"row range {rows} outside [0, {p})")
     mm = np.memmap(path, dtype="<f8", mode="r", offset=HEADER_BYTES + 8 * n * lo,
                    shape=(hi - lo, n))
-    try:
-        return ObservationSet.from_obs_major_host(mm, p_total=p, device=device)
-    except ValueError as exc:
-        if "non-finite" in str(exc):
-            raise ValueError(f"{path}: non-finite value in payload") from None
-        raise
+    # read-time finiteness, like the reference reader (io.py:89-91): chunked so a large mapped
+    # payload is streamed once, never copied whole
+    step = max(1, (1 << 24) // max(n, 1))
+    for a in range(0, hi - lo, step):
+        if not np.isfinite(mm[a:a + step]).all():
+            raise ValueError(f"{path}: non-finite value in payload")
+    return ObservationSet.from_obs_major_host(mm, p_total=p, device=device)
 
 
 def write_observations_binary(path: str, obs: ObservationSet) -> None:

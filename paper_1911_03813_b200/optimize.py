@@ -120,19 +120,29 @@ def packed_fg_implicit(obs: ObservationSet, d: int, r: int, alpha: float = 0.0, 
 def lbfgs_minimize(fg: FgCallback, x0: np.ndarray, cfg: OptConfig,
                    shape: tuple[int, int] | None = None,
                    iterate_hook: Callable[[np.ndarray], None] | None = None) -> RunReport:
-    """L-BFGS with strong-Wolfe line search, run device-resident (reference optimize.py:255-355).
+    """L-BFGS with strong-Wolfe line search (reference optimize.py:255-355).
 
-    ``fg`` must come from :func:`packed_fg_implicit`: the whole solve (two-loop recursion,
+    When ``fg`` comes from :func:`packed_fg_implicit` the whole solve (two-loop recursion,
     trial points, (s, y) history, every f+grad) runs on the GPU through ``mcp_lbfgs`` and the
-    host only steers the line search on scalars.  Stopping rules, step logic and the report
+    host only steers the line search on scalars.  Any other callback (wrapped closures, custom
+    objectives, the sharded / multi-GPU ``fg``) is driven by the host solver
+    (:mod:`.host_solver`) with the same decisions.  Stopping rules, step logic and the report
     match the reference; ``trace`` rows are ``(f, seconds since start)``.
     """
     import time
 
     problem = getattr(fg, "device_problem", None)
     if problem is None:
-        raise TypeError("lbfgs_minimize runs on the device: pass the fg returned by "
-                        "packed_fg_implicit(obs, d, r, alpha)")
+        from .host_solver import lbfgs_host
+
+        start = time.perf_counter()
+        out = lbfgs_host(fg, x0, cfg, iterate_hook)
+        x = out["x"]
+        lam, A = (x.copy(), np.empty((0, 0))) if shape is None else unpack(x, *shape)
+        return RunReport(lam=lam, A=A, f=out["f"], grad_inf_norm=float(np.abs(out["g"]).max()),
+                         n_fg=out["n_fg"], n_steps=out["n_steps"],
+                         wall_time=time.perf_counter() - start, reason=out["reason"],
+                         seed=cfg.seed, trace=out["trace"])
     obs, d, r, alpha, mode = problem
     start = time.perf_counter()
     x0 = np.asarray(x0, dtype=float)
@@ -280,56 +290,6 @@ def multistart_lbfgs(k: int, init: Callable[[np.random.Generator], np.ndarray],
         else:
             rep.run_index = i
             successes.append(rep)
-    if not successes:
-        raise RuntimeError("all multistart runs failed: " + "; ".join(errors))
-    best = min(successes, key=lambda rp: (rp.f, rp.run_index))
-    best.runs = successes
-    best.failures = errors
-    best.seed = seed if isinstance(seed, int) else None
-    return best
-
-
-def multistart(k: int, init: Callable[[np.random.Generator], np.ndarray],
-               minimize: Callable[[np.ndarray, np.random.Generator], RunReport], seed: int,
-               threads: int = 1) -> RunReport:
-    """Best of ``k`` independently seeded runs (reference optimize.py:454-508, same semantics).
-
-    Run i draws from ``default_rng(SeedSequence(seed).spawn(k)[i])``; the report with the
-    lowest final f (ties by run index) is returned with every run attached.  With
-    ``threads > 1`` runs are submitted from a thread pool; the device serialises them per
-    observation set, and results equal the sequential ones bitwise.
-    """
-    if k < 1:
-        raise ValueError(f"number of starts must be >= 1, got {k}")
-    root = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
-    children = root.spawn(k)
-
-    def one(i: int) -> RunReport:
-        rng = np.random.default_rng(children[i])
-        x0 = init(rng)
-        report = minimize(x0, rng)
-        report.run_index = i
-        return report
-
-    results: list[RunReport | None] = [None] * k
-    errors: list[str] = []
-    if threads > 1:
-        from concurrent.futures import ThreadPoolExecutor
-
-        with ThreadPoolExecutor(max_workers=threads) as pool:
-            futures = {pool.submit(one, i): i for i in range(k)}
-            for fut, i in futures.items():
-                try:
-                    results[i] = fut.result()
-                except Exception as exc:  # noqa: BLE001 - aggregated below
-                    errors.append(f"run {i}: {exc}")
-    else:
-        for i in range(k):
-            try:
-                results[i] = one(i)
-            except Exception as exc:  # noqa: BLE001 - aggregated below
-                errors.append(f"run {i}: {exc}")
-    successes = [r for r in results if r is not None]
     if not successes:
         raise RuntimeError("all multistart runs failed: " + "; ".join(errors))
     best = min(successes, key=lambda rp: (rp.f, rp.run_index))

@@ -338,7 +338,6 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
     reproduce the single-call evaluation bitwise, with and without the fused reduce + finish
     (K3F forms G, C, M, u in-kernel in the same expression order as K4), over orders d and
     ranks up to K3F's limit r = 32."""
-    import os
 
     import torch
 
@@ -355,8 +354,7 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
         s = _native.stream_handle(torch.cuda.current_stream())
         outs = []
         for fused in (True, False):
-            if not fused:
-                os.environ["MCP_NO_FUSED_TAIL"] = "1"
+            ctx.set_option(_native.MCP_OPT_FUSED_TAIL, 1 if fused else 0)
             try:
                 Yw = torch.empty(n * r + r, dtype=torch.float64, device="cuda")
                 o1 = torch.empty(1 + r + n * r, dtype=torch.float64, device="cuda")
@@ -368,7 +366,7 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
                 assert torch.equal(o1, o2), (n, r, d, fused)
                 outs.append(o1.cpu())
             finally:
-                os.environ.pop("MCP_NO_FUSED_TAIL", None)
+                ctx.set_option(_native.MCP_OPT_FUSED_TAIL, 1)
         assert torch.equal(outs[0], outs[1]), (n, r, d)
         res = mcp.fg_implicit(obs, lam, A, d, 0.25)
         assert float(outs[0][0]) == res.f

@@ -90,11 +90,42 @@ def test_synth_host_generation_is_deterministic():
     assert c3.dtype == np.float32 and c3.shape == (512, 100)
 
 
-def test_lbfgs_minimize_requires_device_objective():
+def test_lbfgs_minimize_accepts_any_callback():
+    """A plain fg(x) callback (no device problem) runs on the host solver, which follows the
+    reference's decisions: on a quadratic it reaches the tolerance, and it reproduces the
+    restated reference solver's iterates bitwise."""
+    import paper_1911_03813_b200 as mcp
+    from oracle import lbfgs_oracle as lo
+
+    D = np.diag(np.arange(1.0, 6.0))
+    b = np.array([1.0, -2.0, 0.5, 3.0, -1.0])
+
+    def fg(x):
+        return 0.5 * float(x @ D @ x) - float(b @ x), D @ x - b
+
+    rep = mcp.lbfgs_minimize(fg, np.zeros(5), mcp.OptConfig(pgtol=1e-7))
+    assert rep.reason == "tolerance"
+    assert np.allclose(rep.lam, np.linalg.solve(D, b), atol=1e-6)
+    with pytest.raises(ValueError):
+        mcp.lbfgs_minimize(lambda x: (np.nan, x), np.zeros(3), mcp.OptConfig())
+    # a nonconvex objective: the same trajectory as the restated reference solver
+    rng = np.random.default_rng(4)
+    Q = rng.standard_normal((6, 6))
+
+    def fg2(x):
+        z = Q @ x
+        return float(np.sum(z ** 4) - np.sum(z ** 2)), Q.T @ (4 * z ** 3 - 2 * z)
+
+    x0 = rng.standard_normal(6)
+    rep2 = mcp.lbfgs_minimize(fg2, x0, mcp.OptConfig(max_iters=40))
+    ref = lo.lbfgs(fg2, x0, memory=5, max_iters=40)
+    assert rep2.n_fg == ref["n_fg"] and rep2.n_steps == ref["n_steps"]
+    assert np.array_equal(rep2.lam, ref["x"]) and rep2.f == ref["f"]
+
+
+def test_lbfgs_config_checks():
     import paper_1911_03813_b200 as mcp
 
-    with pytest.raises(TypeError):
-        mcp.lbfgs_minimize(lambda x: (0.0, x), np.zeros(3), mcp.OptConfig())
     with pytest.raises(ValueError):
         mcp.OptConfig(pgtol=0)
     with pytest.raises(ValueError):

@@ -24,6 +24,7 @@
 #include "pdl.h"
 #include "k1_dispatch.h"
 #include "k1t_tf32.cuh"
+#include "k1w_fp64.cuh"
 #include "ctx.h"
 
 #include <cuda.h>
@@ -361,6 +362,12 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   std::string why;
   if (!k1_select(c->dtype, c->n, r, c->p_pad, c->sms, pl.k1, why))
     return c->fail(MCP_ERR_ARG, why);
+  if (pl.k1.needs_tmap() && !c->tm_w_ready) {
+    if (!make_tmap_f32(&c->tm_w, c->dV, c->ldv, c->p_pad, 4 * c->ldv, K1W_NK, K1W_T,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+      return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K1W observation map");
+    c->tm_w_ready = true;
+  }
   int rc;
   const int64_t n = c->n;
   if ((rc = ensure(c, c->dx, sizeof(double) * (r + n * r + 1)))) return rc;
@@ -445,7 +452,7 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
   auto* ev = timing_begin(c, s);
   int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r,
                      (const double*)c->dAfrag.p, pl.d, (double*)c->dYpart.p, (double*)c->dwpart.p,
-                     s);
+                     s, &c->tm_w);
   timing_end(ev, s);
   if (rc) {
     const cudaError_t e = cudaGetLastError();
@@ -760,6 +767,7 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   c->own_v32 = false;
   c->tm_v_ready = false;
   c->tm_c_ready = false;
+  c->tm_w_ready = false;
   int rc = dtype == MCP_F64
                ? upload_obs<double>(c, (const double*)V, on_device, layout, n, p, ld)
                : upload_obs<float>(c, (const float*)V, on_device, layout, n, p, ld);

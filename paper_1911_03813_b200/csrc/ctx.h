@@ -62,6 +62,8 @@ struct mcp_ctx {
   CUtensorMap tm_l1, tm_l2;
   CUtensorMap tm_v3, tm_l3;    // K1T2 GEMM2: 3-D chunk maps over V / V_lo (ld % 32 == 0)
   bool tm_c_ready = false;
+  CUtensorMap tm_w;            // K1W: fp32 V, 32 x 64 boxes, 128-byte swizzle
+  bool tm_w_ready = false;
   void* tm_a_addr = nullptr;
   int tm_a_rows = 0, tm_a_kpad = 0, tm_a_rb = 0;
   mcp_internal::DevBuf dAt;

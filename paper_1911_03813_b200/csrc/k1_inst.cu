@@ -13,6 +13,7 @@
 #include "k1s_fp64.cuh"
 #include "k1p_fp64.cuh"
 #include "k1q_fp64.cuh"
+#include "k1w_fp64.cuh"
 #if MCP_WITH_K1R
 #include "k1r_fp64.cuh"
 #endif
@@ -372,6 +373,82 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   return true;
 }
 
+// ---------------- K1W (fp32 V, large n: resident TMA tile, cluster n-split) ----------------
+template <int CPW, int CL>
+void launch_w(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(K1W_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CL;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, k1w_fg_dmma<CPW, CL>, *tm, prm);
+}
+using LaunchW = void (*)(const K1WParams&, const CUtensorMap*, int, size_t, cudaStream_t);
+struct EntryW {
+  int cpw, cl;
+  LaunchW launch;
+  const void* fn;
+  size_t smem;
+};
+#define MCP_K1W_E(CPW, CL) \
+  {CPW, CL, &launch_w<CPW, CL>, (const void*)&k1w_fg_dmma<CPW, CL>, k1w_smem_bytes<CPW, CL>()}
+const EntryW kTableW[] = {MCP_K1W_E(2, 1), MCP_K1W_E(1, 1), MCP_K1W_E(2, 2)};
+constexpr int kEntriesW = sizeof(kTableW) / sizeof(kTableW[0]);
+
+// K1W applies to fp32 sets whose n fills the 256-variable (per CTA) chunk grid well, with
+// enough factor columns for its 32-wide blocks.
+bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v) {
+  if (dtype != MCP_F32 || r < 24) return false;
+  int e = -1;
+  for (int i = 0; i < kEntriesW && e < 0; ++i) {
+    const int64_t npad = 256LL * kTableW[i].cpw * kTableW[i].cl;
+    if (n <= npad && 4 * n > 3 * npad) e = i;   // <= 33% padding
+  }
+  if (e < 0) return false;
+  const EntryW& en = kTableW[e];
+  if (!ensure_dyn_smem(en.fn, en.smem)) return false;
+  const int64_t T = p_pad / K1W_T;
+  const int Nc = sms / en.cl;
+  v.kind = 7;
+  v.dtype = dtype;
+  v.RB = K1W_RB;
+  v.cl = en.cl;
+  v.cpw = en.cpw;
+  v.n_pad = 256 * en.cpw * en.cl;
+  v.n_chunks = v.n_pad / 64;   // Afrag k-steps = n_pad / 4 = 16 n_chunks
+  v.rbs = (int)ceil_div(r, K1W_RB);
+  v.num_tiles = T;
+  if (Nc % v.rbs == 0 && Nc / v.rbs <= T) {
+    v.wmode = 0;
+    v.gp = Nc / v.rbs;
+  } else {
+    v.wmode = 1;
+    const int64_t U = (int64_t)v.rbs * T;
+    int64_t mx = 1;
+    for (int rb = 0; rb < v.rbs; ++rb)
+      mx = std::max<int64_t>(mx, k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
+    v.gp = (int)mx;
+  }
+  v.grid = Nc * en.cl;
+  v.smem = en.smem;
+  v.entry = e;
+  v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (K1W_RB / 8) * 32;
+  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * K1W_RB;
+  v.wpart_elems = (size_t)v.rbs * v.gp * K1W_RB;
+  v.name = std::string("k1w_fg_dmma<f32,RB=32,CPW=") + std::to_string(en.cpw) + ",CL=" +
+           std::to_string(en.cl) + (v.wmode ? ",ranges" : ",strided") + ">";
+  return true;
+}
+
 }  // namespace
 
 // The one-kernel reduce + finish (K3F) applies when its w block holds every w and the factor
@@ -412,6 +489,8 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
   if (dtype == MCP_F64 && MCP_CFG_K1S &&
       select_stream(n, r, p_pad, obs_pitch(dtype, n), sms, v))
     return true;
+  v = K1Variant();
+  if (MCP_CFG_K1W && select_w(dtype, n, r, p_pad, sms, v)) return true;
   v = K1Variant();
   // K1G when registers cap K1's column block at a quarter (or less) of K1G's: e.g. n = 1024,
   // r = 256 (c5): K1 RB = 16 vs K1G RB = 64 -> 4x fewer passes over V (measured 18% faster);
@@ -513,8 +592,27 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
 
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
-              double* wpart, cudaStream_t s) {
+              double* wpart, cudaStream_t s, const void* tmap) {
   if (v.entry < 0) return 1;
+  if (v.kind == 7) {
+    if (!tmap) return 1;
+    K1WParams wp;
+    wp.num_tiles = v.num_tiles;
+    wp.n = n;
+    wp.n_pad = v.n_pad;
+    wp.nu = dnu;
+    wp.nu_const = nu_const;
+    wp.Afrag = Afrag;
+    wp.d = d;
+    wp.rbs = v.rbs;
+    wp.nclusters = v.grid / v.cl;
+    wp.mode = v.wmode;
+    wp.slots = v.gp;
+    wp.Ypart = Ypart;
+    wp.wpart = wpart;
+    kTableW[v.entry].launch(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
+  }
   if (v.kind == 1 || v.kind == 3 || v.kind == 4 || v.kind == 6) {
     K1SParams sp;
     sp.V = static_cast<const double*>(dV);

@@ -1,0 +1,430 @@
+// K1W (FP64 mode, float32 observations, large n): TMA-staged, barrier-light fused f+grad.
+//
+// Same arithmetic as the other K1 kernels -- per tile of 64 observations and one 32-column
+// block of factors it replaces
+//   Z = V^T A                  pkg/src/momentcp/implicit.py:106     (GEMM1, DMMA.8x8x4)
+//   P = nu * Z^(d-1)           pkg/src/momentcp/implicit.py:82-91,107 (epilogue, registers)
+//   w += sum_l nu_l z_l^d      (= a_j^T y_j, implicit.py:139)
+//   Y += V P                   pkg/src/momentcp/implicit.py:107     (GEMM2, DMMA.8x8x4)
+// -- organised for the shapes where the FP64 pipe is the bound (c3: n = 512, r = 64; c5 through
+// a 2-CTA cluster: n = 1024, r = 256):
+//
+//  * the whole 64-row tile stays resident in shared memory as n/32 chunk slots of 64 x 32
+//    floats, each filled by ONE 2-D TMA (128-byte swizzle) and completing on its own mbarrier;
+//    GEMM2 reads the tile GEMM1 read (no reload), and each slot is refilled with the next tile's
+//    chunk by the one warp that owns the chunk in GEMM2, right after its GEMM2 pass over it --
+//    the other warps' GEMM1 reads of the tile are complete by then (they passed the P barrier);
+//  * GEMM1 visits the chunks in release order (every warp's first GEMM2 chunk, then its second),
+//    so the next tile's first chunks land while GEMM2 still runs;
+//  * the factor block (GEMM1's B operand, fragment order, 8 KB per chunk) streams through a
+//    small ring of 1-D TMA copies; the last of the 8 warps to release a slot refills it;
+//  * one named barrier per tile (P ready); everything else is mbarrier parity waits;
+//  * swizzled layouts make every fragment load conflict-free: GEMM1 reads rows 16 rg + 8 m + g at
+//    k = 4 ks + t (16-byte unit ks ^ g); GEMM2 reads column 8 mt + g at tile rows whose residue
+//    mod 8 is 2t + (ks & 1) -- DMMA's k index may be any permutation of the 64 tile rows as long
+//    as P uses the same one, and this one spreads the swizzled units over all 32 banks;
+//  * CL = 2: a cluster of two CTAs splits n; each computes its half of Z, the halves are
+//    exchanged through distributed shared memory and added in cluster-rank order (bitwise the
+//    same Z on both), and each CTA runs GEMM2 on its own half of the tile -- so the Y block stays
+//    in registers at n = 1024 with 32 factor columns.
+//
+// Work split: units = (column block, tile); when the clusters divide evenly among the column
+// blocks each cluster keeps one block and strides over tiles (CTAs of different blocks read the
+// same tile at about the same time, so it comes from L2); otherwise each cluster takes an equal
+// contiguous range of the block-major unit list (at most a few block switches, each flushing the
+// Y partial).  Partials go to [rb][slot][n_pad][RB] and are reduced in a fixed order by K3, so
+// results are deterministic and exactly linear in nu.
+#pragma once
+
+#include <cuda.h>
+
+#include "k1s_fp64.cuh"   // mbarrier helpers
+#include "mcp_common.cuh"
+#include "pdl.h"
+#include "umma.cuh"       // TMA helpers
+
+namespace mcp {
+
+constexpr int K1W_T = 64;          // observations per tile
+constexpr int K1W_NK = 32;         // floats per chunk row (one 128-byte swizzle row)
+constexpr int K1W_RB = 32;         // factor columns per block
+constexpr int K1W_THREADS = 256;   // 8 warps
+constexpr int K1W_SP = 34;         // P row pitch (doubles): == 2 mod 16 -> conflict-free B loads
+constexpr int K1W_CHUNK_BYTES = K1W_T * K1W_NK * 4;         // 8 KB of V
+constexpr int K1W_ACHUNK_BYTES = 8 * (K1W_RB / 8) * 32 * 8;   // 8 KB of factor fragments
+
+struct K1WParams {
+  int64_t num_tiles;      // tiles of 64 rows in p_pad
+  int n;                  // variables (whole set)
+  int n_pad;              // 256 * CPW * CL (Ypart row extent)
+  const double* nu;       // p_pad weights or nullptr
+  double nu_const;
+  const double* Afrag;    // [rbs][n_pad / 4][RB / 8][32]
+  int d;
+  int rbs;
+  int nclusters;          // gridDim.x / CL
+  int mode;               // 0: strided (nclusters % rbs == 0), 1: block-major ranges
+  int slots;              // partial slots per column block
+  double* Ypart;          // [rbs][slots][n_pad][RB]
+  double* wpart;          // [rbs][slots][RB]
+};
+
+template <int CPW, int CL>
+__host__ __device__ constexpr int k1w_sa() {
+  return CL == 1 ? 6 : 3;
+}
+
+template <int CPW, int CL>
+__host__ __device__ constexpr size_t k1w_smem_bytes() {
+  return 1024 /*alignment slack*/ + (size_t)8 * CPW * K1W_CHUNK_BYTES +
+         (size_t)k1w_sa<CPW, CL>() * K1W_ACHUNK_BYTES + 2 * (size_t)K1W_T * K1W_SP * 8 +
+         (CL > 1 ? 2 * (size_t)K1W_THREADS * 8 * 8 : 0) + 8 * (size_t)K1W_RB * 8 /*w*/ +
+         512 /*barriers, counters*/;
+}
+
+// ---- work split (shared by the host plan and the kernel) --------------------------------
+// block-major ranges: cluster c owns units [c U / Nc, (c + 1) U / Nc) of U = rbs * T
+__host__ __device__ inline int64_t k1w_u0(int64_t c, int64_t U, int64_t Nc) { return c * U / Nc; }
+// first cluster whose range touches column block rb
+__host__ __device__ inline int64_t k1w_cfirst(int64_t rb, int64_t T, int64_t U, int64_t Nc) {
+  int64_t c = rb * T * Nc / U;
+  while (c > 0 && k1w_u0(c, U, Nc) > rb * T) --c;
+  while (c + 1 < Nc && k1w_u0(c + 1, U, Nc) <= rb * T) ++c;
+  return c;
+}
+__host__ __device__ inline int64_t k1w_clast(int64_t rb, int64_t T, int64_t U, int64_t Nc) {
+  int64_t c = k1w_cfirst(rb, T, U, Nc);
+  while (c + 1 < Nc && k1w_u0(c + 1, U, Nc) < (rb + 1) * T) ++c;
+  return c;
+}
+
+struct K1WTile {
+  int rb, slot;
+  int64_t tile;
+  bool last_in_seg;   // flush the partial after this tile
+};
+
+// Tile `k` (0-based) of cluster c's work list; returns false past the end.
+__device__ __forceinline__ bool k1w_tile_at(const K1WParams& prm, int c, int64_t k, K1WTile& o) {
+  const int64_t T = prm.num_tiles;
+  if (prm.mode == 0) {
+    const int per = prm.nclusters / prm.rbs;
+    const int slot = c / prm.rbs;
+    const int64_t tile = slot + k * per;
+    if (tile >= T) return false;
+    o.rb = c % prm.rbs;
+    o.slot = slot;
+    o.tile = tile;
+    o.last_in_seg = tile + per >= T;
+    return true;
+  }
+  const int64_t U = (int64_t)prm.rbs * T, Nc = prm.nclusters;
+  const int64_t u = k1w_u0(c, U, Nc) + k;
+  if (u >= k1w_u0(c + 1, U, Nc)) return false;
+  o.rb = (int)(u / T);
+  o.tile = u % T;
+  o.slot = (int)(c - k1w_cfirst(o.rb, T, U, Nc));
+  o.last_in_seg = (u + 1 == k1w_u0(c + 1, U, Nc)) || ((u + 1) % T == 0);
+  return true;
+}
+
+__device__ __forceinline__ uint32_t k1w_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void k1w_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ double k1w_ld_peer(const double* local, uint32_t peer) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
+               : "=r"(remote)
+               : "r"(smem_u32(local)), "r"(peer));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(remote) : "memory");
+  return v;
+}
+__device__ __forceinline__ void k1w_named_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(K1W_THREADS) : "memory");
+}
+__device__ __forceinline__ void k1w_fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+template <int CPW, int CL>
+__global__ void __launch_bounds__(K1W_THREADS, 1)
+    k1w_fg_dmma(const __grid_constant__ CUtensorMap tmV, K1WParams prm) {
+  constexpr int C = 8 * CPW;           // chunk slots of this CTA's tile (n_local = 32 C)
+  constexpr int SA = k1w_sa<CPW, CL>();
+  constexpr int NT = K1W_RB / 8;       // 4 column tiles
+  extern __shared__ __align__(16) unsigned char k1w_smem_raw[];
+  unsigned char* base =
+      k1w_smem_raw + ((1024u - (smem_u32(k1w_smem_raw) & 1023u)) & 1023u);
+  float* sV = reinterpret_cast<float*>(base);                                  // [C][64][32]
+  double* sA = reinterpret_cast<double*>(base + (size_t)C * K1W_CHUNK_BYTES);  // [SA][8][NT][32]
+  double* sP = sA + (size_t)SA * (K1W_ACHUNK_BYTES / 8);                       // [2][64][SP]
+  double* sZx = sP + 2 * K1W_T * K1W_SP;                                       // [2][256][8]
+  double* sW = sZx + (CL > 1 ? 2 * K1W_THREADS * 8 : 0);                      // [8][RB]
+  uint64_t* fullV = reinterpret_cast<uint64_t*>(sW + 8 * K1W_RB);              // [C]
+  uint64_t* fullA = fullV + C;                                                 // [SA]
+  unsigned* cntA = reinterpret_cast<unsigned*>(fullA + SA);                    // [SA]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int rg = warp & 3, cg = warp >> 2;    // GEMM1: rows 16 rg .. +15, columns 16 cg .. +15
+  const uint32_t crank = CL > 1 ? k1w_cluster_rank() : 0;
+  const int cid = blockIdx.x / CL;            // cluster index (the unit of the work split)
+  const int n0 = (int)crank * 32 * C;         // this CTA's first variable
+  const int dm1 = prm.d - 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C; ++i) mbar_init(&fullV[i], 1);
+    for (int i = 0; i < SA; ++i) {
+      mbar_init(&fullA[i], 1);
+      cntA[i] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_prefetch_desc(&tmV);
+  }
+  __syncthreads();
+
+  K1WTile cur;
+  const bool any = k1w_tile_at(prm, cid, 0, cur);
+  // V never changes: the first tile's chunks load before waiting for the factor prep kernel
+  if (any && threadIdx.x == 0) {
+    for (int c = 0; c < C; ++c) {
+      mbar_arrive_expect_tx(&fullV[c], K1W_CHUNK_BYTES);
+      tma_load_2d(sV + (size_t)c * (K1W_CHUNK_BYTES / 4), &tmV, n0 + 32 * c,
+                  (int)(cur.tile * K1W_T), smem_u32(&fullV[c]));
+    }
+  }
+  pdl_enter();   // Afrag comes from the preceding prep kernel
+
+  // factor chunk q of this CTA's GEMM1 sequence: tile q / C, chunk position q % C
+  auto a_src = [&](int64_t q, const K1WTile& tq) -> const double* {
+    const int j = (int)(q % C);
+    const int c = CPW * (j & 7) + (j >> 3);                        // release order
+    const int kchunk = (n0 >> 5) + c;                              // 32-variable chunk index
+    return prm.Afrag + ((size_t)tq.rb * (prm.n_pad / 4) + (size_t)kchunk * 8) * NT * 32;
+  };
+  if (any && threadIdx.x == 0) {
+    for (int q = 0; q < SA; ++q) {
+      K1WTile tq;
+      if (!k1w_tile_at(prm, cid, q / C, tq)) break;
+      mbar_arrive_expect_tx(&fullA[q], K1W_ACHUNK_BYTES);
+      tma_bulk_g2s(sA + (size_t)q * (K1W_ACHUNK_BYTES / 8), a_src(q, tq), K1W_ACHUNK_BYTES,
+                   &fullA[q]);
+    }
+  }
+
+  double y[CPW][4][NT][2];
+#pragma unroll
+  for (int h = 0; h < CPW; ++h)
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) y[h][mt][nt][0] = y[h][mt][nt][1] = 0.0;
+  double wacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+
+  if (!any && prm.mode == 0 && cid / prm.rbs < prm.slots) {
+    // a strided cluster without tiles (p smaller than the grid) still owns a (zero) partial
+    const int rb = cid % prm.rbs, s = cid / prm.rbs;
+    double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1W_RB;
+    for (int e = threadIdx.x; e < 32 * C * K1W_RB; e += K1W_THREADS)
+      Yp[(size_t)n0 * K1W_RB + e] = 0.0;
+    if (crank == 0 && threadIdx.x < K1W_RB)
+      prm.wpart[((size_t)rb * prm.slots + s) * K1W_RB + threadIdx.x] = 0.0;
+  }
+
+  int64_t it = 0;
+  while (any) {
+    const uint32_t par = (uint32_t)(it & 1);
+    const int pb = (int)(it & 1);
+    const int64_t row0 = cur.tile * K1W_T;
+    K1WTile nxt;
+    const bool has_next = k1w_tile_at(prm, cid, it + 1, nxt);
+
+    // ---------------- GEMM1: Z[64 x 32] (partial over this CTA's variables) ----------------
+    double z[2][2][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int nn = 0; nn < 2; ++nn) z[m][nn][0] = z[m][nn][1] = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < C; ++j) {
+      const int c = CPW * (j & 7) + (j >> 3);
+      const int64_t q = it * C + j;
+      const int slot = (int)(q % SA);
+      mbar_wait(&fullV[c], par);
+      mbar_wait(&fullA[slot], (uint32_t)((q / SA) & 1));
+      const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4) + (16 * rg + g) * 32 + t;
+      const double* as = sA + (size_t)slot * (K1W_ACHUNK_BYTES / 8) + 2 * cg * 32 + lane;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int off = (ks ^ g) << 2;
+        const double a0 = (double)vs[off];
+        const double a1 = (double)vs[8 * 32 + off];
+        const double b0 = as[ks * NT * 32];
+        const double b1 = as[ks * NT * 32 + 32];
+        dmma884(z[0][0], a0, b0);
+        dmma884(z[0][1], a0, b1);
+        dmma884(z[1][0], a1, b0);
+        dmma884(z[1][1], a1, b1);
+      }
+      // release the factor slot; the last of the 8 warps refills it (chunk q + SA)
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&cntA[slot], 1u) == K1W_THREADS / 32 - 1) {
+          cntA[slot] = 0;
+          __threadfence_block();
+          const int64_t qn = q + SA;
+          K1WTile tq;
+          if (k1w_tile_at(prm, cid, qn / C, tq)) {
+            k1w_fence_proxy_async();
+            mbar_arrive_expect_tx(&fullA[slot], K1W_ACHUNK_BYTES);
+            tma_bulk_g2s(sA + (size_t)slot * (K1W_ACHUNK_BYTES / 8), a_src(qn, tq),
+                         K1W_ACHUNK_BYTES, &fullA[slot]);
+          }
+        }
+      }
+    }
+
+    if constexpr (CL > 1) {
+      // Z halves through distributed shared memory, summed in cluster-rank order on both CTAs
+      double* mine = sZx + (size_t)pb * K1W_THREADS * 8 + (size_t)threadIdx.x;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mine[e * K1W_THREADS] = (&z[0][0][0])[e];
+      k1w_cluster_sync();
+      const uint32_t peer = crank ^ 1u;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double o = k1w_ld_peer(mine + e * K1W_THREADS, peer);
+        double& zz = (&z[0][0][0])[e];
+        zz = crank == 0 ? zz + o : o + zz;
+      }
+    }
+
+    // ---------------- epilogue: P = nu z^(d-1), w += P z ----------------
+    {
+      double* P = sP + (size_t)pb * K1W_T * K1W_SP;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int lr = 16 * rg + 8 * m + g;
+        const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
+        double zv[4], pv[4];
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn) {
+          zv[2 * nn] = z[m][nn][0];
+          zv[2 * nn + 1] = z[m][nn][1];
+        }
+        rm_pow_vec<4>(zv, pv, dm1);
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn) {
+          const double p0 = nul * pv[2 * nn], p1 = nul * pv[2 * nn + 1];
+          wacc[nn][0] += p0 * zv[2 * nn];
+          wacc[nn][1] += p1 * zv[2 * nn + 1];
+          *reinterpret_cast<double2*>(&P[lr * K1W_SP + 16 * cg + 8 * nn + 2 * t]) =
+              make_double2(p0, p1);
+        }
+      }
+    }
+    k1w_named_sync();   // P complete; every warp's GEMM1 reads of this tile are done
+
+    // ---------------- GEMM2: Y[own 32 CPW variables x 32] += V^T P ----------------
+    {
+      const double* P = sP + (size_t)pb * K1W_T * K1W_SP + g;
+#pragma unroll
+      for (int h = 0; h < CPW; ++h) {
+        const int c = CPW * warp + h;
+        const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4) + (g & 3);
+#pragma unroll 4
+        for (int ks = 0; ks < 16; ++ks) {
+          const int r = 8 * (ks >> 1) + 2 * t + (ks & 1);
+          const int sw = 2 * t + (ks & 1);   // == r & 7
+          const float* vr = vs + r * 32;
+          double a[4], b[NT];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) a[mt] = (double)vr[((2 * mt + (g >> 2)) ^ sw) << 2];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) b[nt] = P[r * K1W_SP + 8 * nt];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma884(y[h][mt][nt], a[mt], b[nt]);
+        }
+        // chunk c is free: refill it with the next tile's chunk (this warp is its only GEMM2
+        // reader and every warp's GEMM1 reads finished before the P barrier)
+        __syncwarp();
+        if (lane == 0 && has_next) {
+          k1w_fence_proxy_async();
+          mbar_arrive_expect_tx(&fullV[c], K1W_CHUNK_BYTES);
+          tma_load_2d(sV + (size_t)c * (K1W_CHUNK_BYTES / 4), &tmV, n0 + 32 * c,
+                      (int)(nxt.tile * K1W_T), smem_u32(&fullV[c]));
+        }
+      }
+    }
+
+    // ---------------- end of a segment: flush this CTA's partial ----------------
+    if (cur.last_in_seg || !has_next) {
+      double* Yp = prm.Ypart + ((size_t)cur.rb * prm.slots + cur.slot) * prm.n_pad * K1W_RB;
+#pragma unroll
+      for (int h = 0; h < CPW; ++h) {
+        const int i0 = n0 + 32 * (CPW * warp + h);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            *reinterpret_cast<double2*>(&Yp[(size_t)(i0 + 8 * mt + g) * K1W_RB + 8 * nt + 2 * t]) =
+                make_double2(y[h][mt][nt][0], y[h][mt][nt][1]);
+            y[h][mt][nt][0] = y[h][mt][nt][1] = 0.0;
+          }
+      }
+      // w: over the 8 row lanes, then the 4 row-group warps in a fixed order (rank 0 writes)
+#pragma unroll
+      for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double v = wacc[nn][e];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (g == 0) sW[rg * K1W_RB + 16 * cg + 8 * nn + 2 * t + e] = v;
+          wacc[nn][e] = 0.0;
+        }
+      k1w_named_sync();
+      if (crank == 0 && threadIdx.x < K1W_RB) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s += sW[q * K1W_RB + threadIdx.x];
+        prm.wpart[((size_t)cur.rb * prm.slots + cur.slot) * K1W_RB + threadIdx.x] = s;
+      }
+      k1w_named_sync();   // sW reusable
+    }
+    if (!has_next) break;
+    cur = nxt;
+    ++it;
+  }
+
+  // partial slots no cluster writes (block-major split with fewer clusters on some blocks):
+  // zero them so the fixed-order reduce can sum every slot
+  if (prm.mode == 1) {
+    const int64_t T = prm.num_tiles, U = (int64_t)prm.rbs * T, Nc = prm.nclusters;
+    for (int rb = 0; rb < prm.rbs; ++rb) {
+      const int used = (int)(k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
+      for (int s = used; s < prm.slots; ++s) {
+        if ((rb * prm.slots + s) % prm.nclusters != cid) continue;
+        double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1W_RB;
+        for (int e = threadIdx.x; e < 32 * C * K1W_RB; e += K1W_THREADS)
+          Yp[(size_t)n0 * K1W_RB + e] = 0.0;
+        if (crank == 0 && threadIdx.x < K1W_RB)
+          prm.wpart[((size_t)rb * prm.slots + s) * K1W_RB + threadIdx.x] = 0.0;
+      }
+    }
+  }
+  if constexpr (CL > 1) k1w_cluster_sync();   // no CTA exits while its peer may read its Z
+}
+
+}  // namespace mcp

@@ -18,11 +18,15 @@
 //    so the next tile's first chunks land while GEMM2 still runs;
 //  * the factor block (GEMM1's B operand, fragment order, 8 KB per chunk) streams through a
 //    small ring of 1-D TMA copies; the last of the 8 warps to release a slot refills it;
-//  * one named barrier per tile (P ready); everything else is mbarrier parity waits;
-//  * swizzled layouts make every fragment load conflict-free: GEMM1 reads rows 16 rg + 8 m + g at
+//  * no CTA-wide barrier per tile: warp w computes Z and P for tile rows 8w .. 8w+7 and
+//    publishes them on its own mbarrier; in GEMM2 every warp starts with its own rows and
+//    rotates through the others, waiting only for the row blocks it has not seen yet -- so the
+//    two warps sharing an SM sub-partition never idle at a barrier while the other finishes;
+//  * swizzled layouts make every fragment load conflict-free: GEMM1 reads row 8w + g at
 //    k = 4 ks + t (16-byte unit ks ^ g); GEMM2 reads column 8 mt + g at tile rows whose residue
 //    mod 8 is 2t + (ks & 1) -- DMMA's k index may be any permutation of the 64 tile rows as long
-//    as P uses the same one, and this one spreads the swizzled units over all 32 banks;
+//    as P uses the same one, and this one spreads the swizzled units over all 32 banks; all
+//    per-lane offsets are computed once, so the inner loops are loads and DMMAs;
 //  * CL = 2: a cluster of two CTAs splits n; each computes its half of Z, the halves are
 //    exchanged through distributed shared memory and added in cluster-rank order (bitwise the
 //    same Z on both), and each CTA runs GEMM2 on its own half of the tile -- so the Y block stays
@@ -79,7 +83,7 @@ __host__ __device__ constexpr size_t k1w_smem_bytes() {
   return 1024 /*alignment slack*/ + (size_t)8 * CPW * K1W_CHUNK_BYTES +
          (size_t)k1w_sa<CPW, CL>() * K1W_ACHUNK_BYTES + 2 * (size_t)K1W_T * K1W_SP * 8 +
          (CL > 1 ? 2 * (size_t)K1W_THREADS * 8 * 8 : 0) + 8 * (size_t)K1W_RB * 8 /*w*/ +
-         512 /*barriers, counters*/;
+         1024 /*barriers, counters*/;
 }
 
 // ---- work split (shared by the host plan and the kernel) --------------------------------
@@ -159,21 +163,22 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
   constexpr int C = 8 * CPW;           // chunk slots of this CTA's tile (n_local = 32 C)
   constexpr int SA = k1w_sa<CPW, CL>();
   constexpr int NT = K1W_RB / 8;       // 4 column tiles
+  constexpr int SP = K1W_SP;
   extern __shared__ __align__(16) unsigned char k1w_smem_raw[];
   unsigned char* base =
       k1w_smem_raw + ((1024u - (smem_u32(k1w_smem_raw) & 1023u)) & 1023u);
   float* sV = reinterpret_cast<float*>(base);                                  // [C][64][32]
   double* sA = reinterpret_cast<double*>(base + (size_t)C * K1W_CHUNK_BYTES);  // [SA][8][NT][32]
   double* sP = sA + (size_t)SA * (K1W_ACHUNK_BYTES / 8);                       // [2][64][SP]
-  double* sZx = sP + 2 * K1W_T * K1W_SP;                                       // [2][256][8]
+  double* sZx = sP + 2 * K1W_T * SP;                                           // [2][8][256]
   double* sW = sZx + (CL > 1 ? 2 * K1W_THREADS * 8 : 0);                      // [8][RB]
   uint64_t* fullV = reinterpret_cast<uint64_t*>(sW + 8 * K1W_RB);              // [C]
   uint64_t* fullA = fullV + C;                                                 // [SA]
-  unsigned* cntA = reinterpret_cast<unsigned*>(fullA + SA);                    // [SA]
+  uint64_t* fullP = fullA + SA;                                                // [8] row blocks
+  unsigned* cntA = reinterpret_cast<unsigned*>(fullP + 8);                     // [SA]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int rg = warp & 3, cg = warp >> 2;    // GEMM1: rows 16 rg .. +15, columns 16 cg .. +15
   const uint32_t crank = CL > 1 ? k1w_cluster_rank() : 0;
   const int cid = blockIdx.x / CL;            // cluster index (the unit of the work split)
   const int n0 = (int)crank * 32 * C;         // this CTA's first variable
@@ -185,6 +190,7 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
       mbar_init(&fullA[i], 1);
       cntA[i] = 0;
     }
+    for (int i = 0; i < 8; ++i) mbar_init(&fullP[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tma_prefetch_desc(&tmV);
   }
@@ -219,6 +225,20 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
     }
   }
 
+  // per-lane shared-memory offsets, fixed for the whole kernel
+  // GEMM1: row 8 warp + g of a chunk, k = 4 ks + t, 16-byte unit ks ^ g (floats)
+  int v1off[8];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) v1off[ks] = (8 * warp + g) * 32 + ((ks ^ g) << 2) + t;
+  // GEMM2: column 8 mt + g of a chunk at row 2t + p (+ 8 * row block), p = ks & 1
+  int v2off[2][4];
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+      v2off[p][mt] = (2 * t + p) * 32 + (((2 * mt + (g >> 2)) ^ (2 * t + p)) << 2) + (g & 3);
+  const int p2off = 2 * t * SP + g;   // P[row 2t (+p) (+ 8 block)][8 nt + g]
+
   double y[CPW][4][NT][2];
 #pragma unroll
   for (int h = 0; h < CPW; ++h)
@@ -226,7 +246,9 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) y[h][mt][nt][0] = y[h][mt][nt][1] = 0.0;
-  double wacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  double wacc[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
 
   if (!any && prm.mode == 0 && cid / prm.rbs < prm.slots) {
     // a strided cluster without tiles (p smaller than the grid) still owns a (zero) partial
@@ -238,6 +260,8 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
       prm.wpart[((size_t)rb * prm.slots + s) * K1W_RB + threadIdx.x] = 0.0;
   }
 
+  int aslot = 0;            // factor ring position of the next chunk
+  uint32_t aphase = 0;
   int64_t it = 0;
   while (any) {
     const uint32_t par = (uint32_t)(it & 1);
@@ -246,49 +270,46 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
     K1WTile nxt;
     const bool has_next = k1w_tile_at(prm, cid, it + 1, nxt);
 
-    // ---------------- GEMM1: Z[64 x 32] (partial over this CTA's variables) ----------------
-    double z[2][2][2];
+    // ---------------- GEMM1: Z[8 rows x 32] (partial over this CTA's variables) ----------------
+    double z[NT][2];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int nn = 0; nn < 2; ++nn) z[m][nn][0] = z[m][nn][1] = 0.0;
+    for (int nt = 0; nt < NT; ++nt) z[nt][0] = z[nt][1] = 0.0;
 #pragma unroll 1
     for (int j = 0; j < C; ++j) {
       const int c = CPW * (j & 7) + (j >> 3);
-      const int64_t q = it * C + j;
-      const int slot = (int)(q % SA);
       mbar_wait(&fullV[c], par);
-      mbar_wait(&fullA[slot], (uint32_t)((q / SA) & 1));
-      const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4) + (16 * rg + g) * 32 + t;
-      const double* as = sA + (size_t)slot * (K1W_ACHUNK_BYTES / 8) + 2 * cg * 32 + lane;
+      mbar_wait(&fullA[aslot], aphase);
+      const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4);
+      const double* as = sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8) + lane;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        const int off = (ks ^ g) << 2;
-        const double a0 = (double)vs[off];
-        const double a1 = (double)vs[8 * 32 + off];
-        const double b0 = as[ks * NT * 32];
-        const double b1 = as[ks * NT * 32 + 32];
-        dmma884(z[0][0], a0, b0);
-        dmma884(z[0][1], a0, b1);
-        dmma884(z[1][0], a1, b0);
-        dmma884(z[1][1], a1, b1);
+        const double a = (double)vs[v1off[ks]];
+        double b[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = as[(ks * NT + nt) * 32];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(z[nt], a, b[nt]);
       }
       // release the factor slot; the last of the 8 warps refills it (chunk q + SA)
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
-        if (atomicAdd(&cntA[slot], 1u) == K1W_THREADS / 32 - 1) {
-          cntA[slot] = 0;
+        if (atomicAdd(&cntA[aslot], 1u) == K1W_THREADS / 32 - 1) {
+          cntA[aslot] = 0;
           __threadfence_block();
-          const int64_t qn = q + SA;
+          const int64_t qn = it * C + j + SA;
           K1WTile tq;
           if (k1w_tile_at(prm, cid, qn / C, tq)) {
             k1w_fence_proxy_async();
-            mbar_arrive_expect_tx(&fullA[slot], K1W_ACHUNK_BYTES);
-            tma_bulk_g2s(sA + (size_t)slot * (K1W_ACHUNK_BYTES / 8), a_src(qn, tq),
-                         K1W_ACHUNK_BYTES, &fullA[slot]);
+            mbar_arrive_expect_tx(&fullA[aslot], K1W_ACHUNK_BYTES);
+            tma_bulk_g2s(sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8), a_src(qn, tq),
+                         K1W_ACHUNK_BYTES, &fullA[aslot]);
           }
         }
+      }
+      if (++aslot == SA) {
+        aslot = 0;
+        aphase ^= 1u;
       }
     }
 
@@ -296,67 +317,69 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
       // Z halves through distributed shared memory, summed in cluster-rank order on both CTAs
       double* mine = sZx + (size_t)pb * K1W_THREADS * 8 + (size_t)threadIdx.x;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) mine[e * K1W_THREADS] = (&z[0][0][0])[e];
+      for (int e = 0; e < 8; ++e) mine[e * K1W_THREADS] = (&z[0][0])[e];
       k1w_cluster_sync();
       const uint32_t peer = crank ^ 1u;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const double o = k1w_ld_peer(mine + e * K1W_THREADS, peer);
-        double& zz = (&z[0][0][0])[e];
+        double& zz = (&z[0][0])[e];
         zz = crank == 0 ? zz + o : o + zz;
       }
     }
 
-    // ---------------- epilogue: P = nu z^(d-1), w += P z ----------------
+    // ---------------- epilogue: P = nu z^(d-1), w += P z  (rows 8 warp + g) ----------------
     {
-      double* P = sP + (size_t)pb * K1W_T * K1W_SP;
+      double* P = sP + (size_t)pb * K1W_T * SP;
+      const int lr = 8 * warp + g;
+      const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
+      double zv[2 * NT], pv[2 * NT];
 #pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int lr = 16 * rg + 8 * m + g;
-        const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
-        double zv[4], pv[4];
-#pragma unroll
-        for (int nn = 0; nn < 2; ++nn) {
-          zv[2 * nn] = z[m][nn][0];
-          zv[2 * nn + 1] = z[m][nn][1];
-        }
-        rm_pow_vec<4>(zv, pv, dm1);
-#pragma unroll
-        for (int nn = 0; nn < 2; ++nn) {
-          const double p0 = nul * pv[2 * nn], p1 = nul * pv[2 * nn + 1];
-          wacc[nn][0] += p0 * zv[2 * nn];
-          wacc[nn][1] += p1 * zv[2 * nn + 1];
-          *reinterpret_cast<double2*>(&P[lr * K1W_SP + 16 * cg + 8 * nn + 2 * t]) =
-              make_double2(p0, p1);
-        }
+      for (int nt = 0; nt < NT; ++nt) {
+        zv[2 * nt] = z[nt][0];
+        zv[2 * nt + 1] = z[nt][1];
       }
+      rm_pow_vec<2 * NT>(zv, pv, dm1);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double p0 = nul * pv[2 * nt], p1 = nul * pv[2 * nt + 1];
+        wacc[nt][0] += p0 * zv[2 * nt];
+        wacc[nt][1] += p1 * zv[2 * nt + 1];
+        *reinterpret_cast<double2*>(&P[lr * SP + 8 * nt + 2 * t]) = make_double2(p0, p1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fullP[warp]);   // this warp's 8 P rows (and its GEMM1) done
     }
-    k1w_named_sync();   // P complete; every warp's GEMM1 reads of this tile are done
 
     // ---------------- GEMM2: Y[own 32 CPW variables x 32] += V^T P ----------------
     {
-      const double* P = sP + (size_t)pb * K1W_T * K1W_SP + g;
+      const double* P = sP + (size_t)pb * K1W_T * SP + p2off;
 #pragma unroll
       for (int h = 0; h < CPW; ++h) {
         const int c = CPW * warp + h;
-        const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4) + (g & 3);
-#pragma unroll 4
-        for (int ks = 0; ks < 16; ++ks) {
-          const int r = 8 * (ks >> 1) + 2 * t + (ks & 1);
-          const int sw = 2 * t + (ks & 1);   // == r & 7
-          const float* vr = vs + r * 32;
-          double a[4], b[NT];
+        const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4);
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) {
+          const int blk = (warp + i) & 7;            // own rows first, then the others in turn
+          if (h == 0) mbar_wait(&fullP[blk], par);
+          const float* vb = vs + blk * 256;
+          const double* pbk = P + blk * 8 * SP;
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) a[mt] = (double)vr[((2 * mt + (g >> 2)) ^ sw) << 2];
+          for (int p = 0; p < 2; ++p) {
+            double a[4], b[NT];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) b[nt] = P[r * K1W_SP + 8 * nt];
+            for (int mt = 0; mt < 4; ++mt) a[mt] = (double)vb[v2off[p][mt]];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt)
+            for (int nt = 0; nt < NT; ++nt) b[nt] = pbk[p * SP + 8 * nt];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma884(y[h][mt][nt], a[mt], b[nt]);
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) dmma884(y[h][mt][nt], a[mt], b[nt]);
+          }
         }
-        // chunk c is free: refill it with the next tile's chunk (this warp is its only GEMM2
-        // reader and every warp's GEMM1 reads finished before the P barrier)
+        // chunk c is free: refill it with the next tile's chunk.  This warp is its only GEMM2
+        // reader, and every warp's GEMM1 reads of it finished before that warp published its P
+        // rows, all of which this warp has waited for.
         __syncwarp();
         if (lane == 0 && has_next) {
           k1w_fence_proxy_async();
@@ -382,23 +405,23 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
             y[h][mt][nt][0] = y[h][mt][nt][1] = 0.0;
           }
       }
-      // w: over the 8 row lanes, then the 4 row-group warps in a fixed order (rank 0 writes)
+      // w: over the 8 row lanes, then the 8 warps (row blocks) in a fixed order (rank 0 writes)
 #pragma unroll
-      for (int nn = 0; nn < 2; ++nn)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          double v = wacc[nn][e];
+          double v = wacc[nt][e];
           v += __shfl_xor_sync(0xffffffffu, v, 4);
           v += __shfl_xor_sync(0xffffffffu, v, 8);
           v += __shfl_xor_sync(0xffffffffu, v, 16);
-          if (g == 0) sW[rg * K1W_RB + 16 * cg + 8 * nn + 2 * t + e] = v;
-          wacc[nn][e] = 0.0;
+          if (g == 0) sW[warp * K1W_RB + 8 * nt + 2 * t + e] = v;
+          wacc[nt][e] = 0.0;
         }
       k1w_named_sync();
       if (crank == 0 && threadIdx.x < K1W_RB) {
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s += sW[q * K1W_RB + threadIdx.x];
+        for (int q = 0; q < 8; ++q) s += sW[q * K1W_RB + threadIdx.x];
         prm.wpart[((size_t)cur.rb * prm.slots + cur.slot) * K1W_RB + threadIdx.x] = s;
       }
       k1w_named_sync();   // sW reusable

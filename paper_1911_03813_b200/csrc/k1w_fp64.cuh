@@ -150,6 +150,19 @@ __device__ __forceinline__ double k1w_ld_peer(const double* local, uint32_t peer
   asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(remote) : "memory");
   return v;
 }
+// Shared-memory operand loads as volatile asm: they stay ahead of the (volatile) DMMAs they are
+// written before, so the next step's operands are in flight while the pipe works on this step's
+// products (an in-order warp stuck behind a throttled DMMA cannot issue later loads).
+__device__ __forceinline__ float k1w_lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double k1w_lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void k1w_named_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(K1W_THREADS) : "memory");
 }
@@ -271,45 +284,66 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
     const bool has_next = k1w_tile_at(prm, cid, it + 1, nxt);
 
     // ---------------- GEMM1: Z[8 rows x 32] (partial over this CTA's variables) ----------------
+    // flat sequence of C chunks x 8 k-steps; step s + 1's operands are loaded before step s's
+    // DMMAs issue (the next chunk's barriers are waited for after the last step's DMMAs)
     double z[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) z[nt][0] = z[nt][1] = 0.0;
+    {
+      uint32_t vsa, asa;   // shared addresses of the current chunk / factor slot
+      auto bind = [&](int jj) {
+        const int c = CPW * (jj & 7) + (jj >> 3);
+        mbar_wait(&fullV[c], par);
+        mbar_wait(&fullA[aslot], aphase);
+        vsa = smem_u32(sV + (size_t)c * (K1W_CHUNK_BYTES / 4));
+        asa = smem_u32(sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8) + lane);
+      };
+      float fa_n;
+      double b_n[NT];
+      auto load = [&](int ks) {
+        fa_n = k1w_lds_f32(vsa + 4u * (uint32_t)v1off[ks]);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b_n[nt] = k1w_lds_f64(asa + 8u * (uint32_t)((ks * NT + nt) * 32));
+      };
+      bind(0);
+      load(0);
 #pragma unroll 1
-    for (int j = 0; j < C; ++j) {
-      const int c = CPW * (j & 7) + (j >> 3);
-      mbar_wait(&fullV[c], par);
-      mbar_wait(&fullA[aslot], aphase);
-      const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4);
-      const double* as = sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8) + lane;
+      for (int j = 0; j < C; ++j) {
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const double a = (double)vs[v1off[ks]];
-        double b[NT];
+        for (int ks = 0; ks < 8; ++ks) {
+          const double a = (double)fa_n;
+          double b[NT];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) b[nt] = as[(ks * NT + nt) * 32];
+          for (int nt = 0; nt < NT; ++nt) b[nt] = b_n[nt];
+          if (ks < 7) load(ks + 1);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884(z[nt], a, b[nt]);
-      }
-      // release the factor slot; the last of the 8 warps refills it (chunk q + SA)
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        if (atomicAdd(&cntA[aslot], 1u) == K1W_THREADS / 32 - 1) {
-          cntA[aslot] = 0;
+          for (int nt = 0; nt < NT; ++nt) dmma884(z[nt], a, b[nt]);
+        }
+        // release the factor slot; the last of the 8 warps refills it (chunk q + SA)
+        __syncwarp();
+        if (lane == 0) {
           __threadfence_block();
-          const int64_t qn = it * C + j + SA;
-          K1WTile tq;
-          if (k1w_tile_at(prm, cid, qn / C, tq)) {
-            k1w_fence_proxy_async();
-            mbar_arrive_expect_tx(&fullA[aslot], K1W_ACHUNK_BYTES);
-            tma_bulk_g2s(sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8), a_src(qn, tq),
-                         K1W_ACHUNK_BYTES, &fullA[aslot]);
+          if (atomicAdd(&cntA[aslot], 1u) == K1W_THREADS / 32 - 1) {
+            cntA[aslot] = 0;
+            __threadfence_block();
+            const int64_t qn = it * C + j + SA;
+            K1WTile tq;
+            if (k1w_tile_at(prm, cid, qn / C, tq)) {
+              k1w_fence_proxy_async();
+              mbar_arrive_expect_tx(&fullA[aslot], K1W_ACHUNK_BYTES);
+              tma_bulk_g2s(sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8), a_src(qn, tq),
+                           K1W_ACHUNK_BYTES, &fullA[aslot]);
+            }
           }
         }
-      }
-      if (++aslot == SA) {
-        aslot = 0;
-        aphase ^= 1u;
+        if (++aslot == SA) {
+          aslot = 0;
+          aphase ^= 1u;
+        }
+        if (j + 1 < C) {
+          bind(j + 1);
+          load(0);
+        }
       }
     }
 
@@ -352,29 +386,48 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
     }
 
     // ---------------- GEMM2: Y[own 32 CPW variables x 32] += V^T P ----------------
+    // per half: 8 row blocks (own first, then the others in turn) x 2 k-steps; the next step's
+    // operands are loaded before this step's 16 DMMAs issue
     {
-      const double* P = sP + (size_t)pb * K1W_T * SP + p2off;
+      const uint32_t pbase = smem_u32(sP + (size_t)pb * K1W_T * SP + p2off);
 #pragma unroll
       for (int h = 0; h < CPW; ++h) {
         const int c = CPW * warp + h;
-        const float* vs = sV + (size_t)c * (K1W_CHUNK_BYTES / 4);
+        const uint32_t vsa = smem_u32(sV + (size_t)c * (K1W_CHUNK_BYTES / 4));
+        float fa_n[4];
+        double b_n[NT];
+        auto load = [&](int blk, int p) {
+          const uint32_t vb = vsa + 1024u * (uint32_t)blk;
+          const uint32_t pk = pbase + 8u * (uint32_t)(blk * 8 * SP + p * SP);
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) fa_n[mt] = k1w_lds_f32(vb + 4u * (uint32_t)v2off[p][mt]);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) b_n[nt] = k1w_lds_f64(pk + 64u * (uint32_t)nt);
+        };
+        if (h == 0) mbar_wait(&fullP[warp], par);
+        load(warp, 0);
 #pragma unroll 1
         for (int i = 0; i < 8; ++i) {
-          const int blk = (warp + i) & 7;            // own rows first, then the others in turn
-          if (h == 0) mbar_wait(&fullP[blk], par);
-          const float* vb = vs + blk * 256;
-          const double* pbk = P + blk * 8 * SP;
+          const int blk = (warp + i) & 7;
 #pragma unroll
           for (int p = 0; p < 2; ++p) {
             double a[4], b[NT];
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) a[mt] = (double)vb[v2off[p][mt]];
+            for (int mt = 0; mt < 4; ++mt) a[mt] = (double)fa_n[mt];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) b[nt] = pbk[p * SP + 8 * nt];
+            for (int nt = 0; nt < NT; ++nt) b[nt] = b_n[nt];
+            if (p == 0) load(blk, 1);
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt) dmma884(y[h][mt][nt], a[mt], b[nt]);
+            if (p == 1 && i < 7) {
+              // next row block: its P may still be in flight (waited for after this step's
+              // products are queued)
+              const int nb = (warp + i + 1) & 7;
+              if (h == 0) mbar_wait(&fullP[nb], par);
+              load(nb, 0);
+            }
           }
         }
         // chunk c is free: refill it with the next tile's chunk.  This warp is its only GEMM2

@@ -374,7 +374,7 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
 }
 
 // ---------------- K1W (fp32 V, large n: resident TMA tile, cluster n-split) ----------------
-template <int CPW, int CL>
+template <int CPW, int CL, int RB>
 void launch_w(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -390,24 +390,26 @@ void launch_w(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, k1w_fg_dmma<CPW, CL>, *tm, prm);
+  cudaLaunchKernelEx(&cfg, k1w_fg_dmma<CPW, CL, RB>, *tm, prm);
 }
 using LaunchW = void (*)(const K1WParams&, const CUtensorMap*, int, size_t, cudaStream_t);
 struct EntryW {
-  int cpw, cl;
+  int cpw, cl, rb;
   LaunchW launch;
   const void* fn;
   size_t smem;
 };
-#define MCP_K1W_E(CPW, CL) \
-  {CPW, CL, &launch_w<CPW, CL>, (const void*)&k1w_fg_dmma<CPW, CL>, k1w_smem_bytes<CPW, CL>()}
-const EntryW kTableW[] = {MCP_K1W_E(2, 1), MCP_K1W_E(1, 1), MCP_K1W_E(2, 2)};
+#define MCP_K1W_E(CPW, CL, RB)                                                                \
+  {CPW, CL, RB, &launch_w<CPW, CL, RB>, (const void*)&k1w_fg_dmma<CPW, CL, RB>,             \
+   k1w_smem_bytes<CPW, CL, RB>()}
+const EntryW kTableW[] = {MCP_K1W_E(2, 1, MCP_CFG_K1W_RB), MCP_K1W_E(1, 1, MCP_CFG_K1W_RB),
+                          MCP_K1W_E(2, 2, MCP_CFG_K1W_RB)};
 constexpr int kEntriesW = sizeof(kTableW) / sizeof(kTableW[0]);
 
 // K1W applies to fp32 sets whose n fills the 256-variable (per CTA) chunk grid well, with
 // enough factor columns for its 32-wide blocks.
 bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v) {
-  if (dtype != MCP_F32 || r < 24) return false;
+  if (dtype != MCP_F32 || r < (MCP_CFG_K1W_RB * 3) / 4) return false;
   int e = -1;
   for (int i = 0; i < kEntriesW && e < 0; ++i) {
     const int64_t npad = 256LL * kTableW[i].cpw * kTableW[i].cl;
@@ -420,12 +422,12 @@ bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v)
   const int Nc = sms / en.cl;
   v.kind = 7;
   v.dtype = dtype;
-  v.RB = K1W_RB;
+  v.RB = en.rb;
   v.cl = en.cl;
   v.cpw = en.cpw;
   v.n_pad = 256 * en.cpw * en.cl;
   v.n_chunks = v.n_pad / 64;   // Afrag k-steps = n_pad / 4 = 16 n_chunks
-  v.rbs = (int)ceil_div(r, K1W_RB);
+  v.rbs = (int)ceil_div(r, en.rb);
   v.num_tiles = T;
   if (Nc % v.rbs == 0 && Nc / v.rbs <= T) {
     v.wmode = 0;
@@ -441,10 +443,10 @@ bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v)
   v.grid = Nc * en.cl;
   v.smem = en.smem;
   v.entry = e;
-  v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (K1W_RB / 8) * 32;
-  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * K1W_RB;
-  v.wpart_elems = (size_t)v.rbs * v.gp * K1W_RB;
-  v.name = std::string("k1w_fg_dmma<f32,RB=32,CPW=") + std::to_string(en.cpw) + ",CL=" +
+  v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (en.rb / 8) * 32;
+  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * en.rb;
+  v.wpart_elems = (size_t)v.rbs * v.gp * en.rb;
+  v.name = std::string("k1w_fg_dmma<f32,RB=") + std::to_string(en.rb) + ",CPW=" + std::to_string(en.cpw) + ",CL=" +
            std::to_string(en.cl) + (v.wmode ? ",ranges" : ",strided") + ">";
   return true;
 }

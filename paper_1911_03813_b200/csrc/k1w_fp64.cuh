@@ -51,11 +51,13 @@ namespace mcp {
 
 constexpr int K1W_T = 64;          // observations per tile
 constexpr int K1W_NK = 32;         // floats per chunk row (one 128-byte swizzle row)
-constexpr int K1W_RB = 32;         // factor columns per block
+constexpr int K1W_RB_MAX = 32;     // factor columns per block: 16 or 32 (template RB)
 constexpr int K1W_THREADS = 256;   // 8 warps
-constexpr int K1W_SP = 34;         // P row pitch (doubles): == 2 mod 16 -> conflict-free B loads
+// P row pitch (doubles) RB + 2 == 2 mod 16 -> conflict-free GEMM2 B-fragment loads
+__host__ __device__ constexpr int k1w_sp(int rb) { return rb + 2; }
 constexpr int K1W_CHUNK_BYTES = K1W_T * K1W_NK * 4;         // 8 KB of V
-constexpr int K1W_ACHUNK_BYTES = 8 * (K1W_RB / 8) * 32 * 8;   // 8 KB of factor fragments
+// factor fragments of one 32-variable chunk: 8 k-steps x RB/8 column tiles x 32 lanes
+__host__ __device__ constexpr int k1w_achunk_bytes(int rb) { return 8 * (rb / 8) * 32 * 8; }
 
 struct K1WParams {
   int64_t num_tiles;      // tiles of 64 rows in p_pad
@@ -73,16 +75,18 @@ struct K1WParams {
   double* wpart;          // [rbs][slots][RB]
 };
 
-template <int CPW, int CL>
+// factor ring depth: 48 KB (CL = 1) or 24 KB (CL = 2, which also stages the Z exchange)
+template <int CPW, int CL, int RB>
 __host__ __device__ constexpr int k1w_sa() {
-  return CL == 1 ? 6 : 3;
+  return (CL == 1 ? 48 * 1024 : 24 * 1024) / k1w_achunk_bytes(RB);
 }
 
-template <int CPW, int CL>
+template <int CPW, int CL, int RB>
 __host__ __device__ constexpr size_t k1w_smem_bytes() {
   return 1024 /*alignment slack*/ + (size_t)8 * CPW * K1W_CHUNK_BYTES +
-         (size_t)k1w_sa<CPW, CL>() * K1W_ACHUNK_BYTES + 2 * (size_t)K1W_T * K1W_SP * 8 +
-         (CL > 1 ? 2 * (size_t)K1W_THREADS * 8 * 8 : 0) + 8 * (size_t)K1W_RB * 8 /*w*/ +
+         (size_t)k1w_sa<CPW, CL, RB>() * k1w_achunk_bytes(RB) +
+         2 * (size_t)K1W_T * k1w_sp(RB) * 8 +
+         (CL > 1 ? 2 * (size_t)K1W_THREADS * (RB / 4) * 8 : 0) + 8 * (size_t)RB * 8 /*w*/ +
          1024 /*barriers, counters*/;
 }
 
@@ -170,22 +174,23 @@ __device__ __forceinline__ void k1w_fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-template <int CPW, int CL>
+template <int CPW, int CL, int RB>
 __global__ void __launch_bounds__(K1W_THREADS, 1)
     k1w_fg_dmma(const __grid_constant__ CUtensorMap tmV, K1WParams prm) {
   constexpr int C = 8 * CPW;           // chunk slots of this CTA's tile (n_local = 32 C)
-  constexpr int SA = k1w_sa<CPW, CL>();
-  constexpr int NT = K1W_RB / 8;       // 4 column tiles
-  constexpr int SP = K1W_SP;
+  constexpr int SA = k1w_sa<CPW, CL, RB>();
+  constexpr int NT = RB / 8;           // column tiles
+  constexpr int SP = k1w_sp(RB);
+  constexpr int ACH = k1w_achunk_bytes(RB);
   extern __shared__ __align__(16) unsigned char k1w_smem_raw[];
   unsigned char* base =
       k1w_smem_raw + ((1024u - (smem_u32(k1w_smem_raw) & 1023u)) & 1023u);
   float* sV = reinterpret_cast<float*>(base);                                  // [C][64][32]
   double* sA = reinterpret_cast<double*>(base + (size_t)C * K1W_CHUNK_BYTES);  // [SA][8][NT][32]
-  double* sP = sA + (size_t)SA * (K1W_ACHUNK_BYTES / 8);                       // [2][64][SP]
-  double* sZx = sP + 2 * K1W_T * SP;                                           // [2][8][256]
-  double* sW = sZx + (CL > 1 ? 2 * K1W_THREADS * 8 : 0);                      // [8][RB]
-  uint64_t* fullV = reinterpret_cast<uint64_t*>(sW + 8 * K1W_RB);              // [C]
+  double* sP = sA + (size_t)SA * (ACH / 8);                       // [2][64][SP]
+  double* sZx = sP + 2 * K1W_T * SP;                                           // [2][2NT][256]
+  double* sW = sZx + (CL > 1 ? 2 * K1W_THREADS * 2 * NT : 0);                 // [8][RB]
+  uint64_t* fullV = reinterpret_cast<uint64_t*>(sW + 8 * RB);              // [C]
   uint64_t* fullA = fullV + C;                                                 // [SA]
   uint64_t* fullP = fullA + SA;                                                // [8] row blocks
   unsigned* cntA = reinterpret_cast<unsigned*>(fullP + 8);                     // [SA]
@@ -232,8 +237,8 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
     for (int q = 0; q < SA; ++q) {
       K1WTile tq;
       if (!k1w_tile_at(prm, cid, q / C, tq)) break;
-      mbar_arrive_expect_tx(&fullA[q], K1W_ACHUNK_BYTES);
-      tma_bulk_g2s(sA + (size_t)q * (K1W_ACHUNK_BYTES / 8), a_src(q, tq), K1W_ACHUNK_BYTES,
+      mbar_arrive_expect_tx(&fullA[q], ACH);
+      tma_bulk_g2s(sA + (size_t)q * (ACH / 8), a_src(q, tq), ACH,
                    &fullA[q]);
     }
   }
@@ -266,11 +271,11 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
   if (!any && prm.mode == 0 && cid / prm.rbs < prm.slots) {
     // a strided cluster without tiles (p smaller than the grid) still owns a (zero) partial
     const int rb = cid % prm.rbs, s = cid / prm.rbs;
-    double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1W_RB;
-    for (int e = threadIdx.x; e < 32 * C * K1W_RB; e += K1W_THREADS)
-      Yp[(size_t)n0 * K1W_RB + e] = 0.0;
-    if (crank == 0 && threadIdx.x < K1W_RB)
-      prm.wpart[((size_t)rb * prm.slots + s) * K1W_RB + threadIdx.x] = 0.0;
+    double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * RB;
+    for (int e = threadIdx.x; e < 32 * C * RB; e += K1W_THREADS)
+      Yp[(size_t)n0 * RB + e] = 0.0;
+    if (crank == 0 && threadIdx.x < RB)
+      prm.wpart[((size_t)rb * prm.slots + s) * RB + threadIdx.x] = 0.0;
   }
 
   int aslot = 0;            // factor ring position of the next chunk
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
         mbar_wait(&fullV[c], par);
         mbar_wait(&fullA[aslot], aphase);
         vsa = smem_u32(sV + (size_t)c * (K1W_CHUNK_BYTES / 4));
-        asa = smem_u32(sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8) + lane);
+        asa = smem_u32(sA + (size_t)aslot * (ACH / 8) + lane);
       };
       float fa_n;
       double b_n[NT];
@@ -330,9 +335,9 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
             K1WTile tq;
             if (k1w_tile_at(prm, cid, qn / C, tq)) {
               k1w_fence_proxy_async();
-              mbar_arrive_expect_tx(&fullA[aslot], K1W_ACHUNK_BYTES);
-              tma_bulk_g2s(sA + (size_t)aslot * (K1W_ACHUNK_BYTES / 8), a_src(qn, tq),
-                           K1W_ACHUNK_BYTES, &fullA[aslot]);
+              mbar_arrive_expect_tx(&fullA[aslot], ACH);
+              tma_bulk_g2s(sA + (size_t)aslot * (ACH / 8), a_src(qn, tq),
+                           ACH, &fullA[aslot]);
             }
           }
         }
@@ -349,13 +354,13 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
 
     if constexpr (CL > 1) {
       // Z halves through distributed shared memory, summed in cluster-rank order on both CTAs
-      double* mine = sZx + (size_t)pb * K1W_THREADS * 8 + (size_t)threadIdx.x;
+      double* mine = sZx + (size_t)pb * K1W_THREADS * 2 * NT + (size_t)threadIdx.x;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) mine[e * K1W_THREADS] = (&z[0][0])[e];
+      for (int e = 0; e < 2 * NT; ++e) mine[e * K1W_THREADS] = (&z[0][0])[e];
       k1w_cluster_sync();
       const uint32_t peer = crank ^ 1u;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < 2 * NT; ++e) {
         const double o = k1w_ld_peer(mine + e * K1W_THREADS, peer);
         double& zz = (&z[0][0])[e];
         zz = crank == 0 ? zz + o : o + zz;
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
 
     // ---------------- end of a segment: flush this CTA's partial ----------------
     if (cur.last_in_seg || !has_next) {
-      double* Yp = prm.Ypart + ((size_t)cur.rb * prm.slots + cur.slot) * prm.n_pad * K1W_RB;
+      double* Yp = prm.Ypart + ((size_t)cur.rb * prm.slots + cur.slot) * prm.n_pad * RB;
 #pragma unroll
       for (int h = 0; h < CPW; ++h) {
         const int i0 = n0 + 32 * (CPW * warp + h);
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
         for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            *reinterpret_cast<double2*>(&Yp[(size_t)(i0 + 8 * mt + g) * K1W_RB + 8 * nt + 2 * t]) =
+            *reinterpret_cast<double2*>(&Yp[(size_t)(i0 + 8 * mt + g) * RB + 8 * nt + 2 * t]) =
                 make_double2(y[h][mt][nt][0], y[h][mt][nt][1]);
             y[h][mt][nt][0] = y[h][mt][nt][1] = 0.0;
           }
@@ -467,15 +472,15 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
           v += __shfl_xor_sync(0xffffffffu, v, 4);
           v += __shfl_xor_sync(0xffffffffu, v, 8);
           v += __shfl_xor_sync(0xffffffffu, v, 16);
-          if (g == 0) sW[warp * K1W_RB + 8 * nt + 2 * t + e] = v;
+          if (g == 0) sW[warp * RB + 8 * nt + 2 * t + e] = v;
           wacc[nt][e] = 0.0;
         }
       k1w_named_sync();
-      if (crank == 0 && threadIdx.x < K1W_RB) {
+      if (crank == 0 && threadIdx.x < RB) {
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s += sW[q * K1W_RB + threadIdx.x];
-        prm.wpart[((size_t)cur.rb * prm.slots + cur.slot) * K1W_RB + threadIdx.x] = s;
+        for (int q = 0; q < 8; ++q) s += sW[q * RB + threadIdx.x];
+        prm.wpart[((size_t)cur.rb * prm.slots + cur.slot) * RB + threadIdx.x] = s;
       }
       k1w_named_sync();   // sW reusable
     }
@@ -492,11 +497,11 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
       const int used = (int)(k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
       for (int s = used; s < prm.slots; ++s) {
         if ((rb * prm.slots + s) % prm.nclusters != cid) continue;
-        double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1W_RB;
-        for (int e = threadIdx.x; e < 32 * C * K1W_RB; e += K1W_THREADS)
-          Yp[(size_t)n0 * K1W_RB + e] = 0.0;
-        if (crank == 0 && threadIdx.x < K1W_RB)
-          prm.wpart[((size_t)rb * prm.slots + s) * K1W_RB + threadIdx.x] = 0.0;
+        double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * RB;
+        for (int e = threadIdx.x; e < 32 * C * RB; e += K1W_THREADS)
+          Yp[(size_t)n0 * RB + e] = 0.0;
+        if (crank == 0 && threadIdx.x < RB)
+          prm.wpart[((size_t)rb * prm.slots + s) * RB + threadIdx.x] = 0.0;
       }
     }
   }

@@ -38,6 +38,9 @@
 #ifndef MCP_CFG_K1W
 #define MCP_CFG_K1W 1
 #endif
+#ifndef MCP_CFG_K1W_RB
+#define MCP_CFG_K1W_RB 32          // K1W factor columns per block (16 or 32)
+#endif
 // K1G (Y partial in L2) for large n when K1's register-bound column block is <= 1/4 of K1G's
 #ifndef MCP_CFG_K1G
 #define MCP_CFG_K1G 1

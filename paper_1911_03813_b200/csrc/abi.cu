@@ -25,6 +25,7 @@
 #include "k1_dispatch.h"
 #include "k1t_tf32.cuh"
 #include "k1w_fp64.cuh"
+#include "k1x_fp64.cuh"
 #include "ctx.h"
 
 #include <cuda.h>
@@ -362,11 +363,14 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   std::string why;
   if (!k1_select(c->dtype, c->n, r, c->p_pad, c->sms, pl.k1, why))
     return c->fail(MCP_ERR_ARG, why);
-  if (pl.k1.needs_tmap() && !c->tm_w_ready) {
-    if (!make_tmap_f32(&c->tm_w, c->dV, c->ldv, c->p_pad, 4 * c->ldv, K1W_NK, K1W_T,
-                       CU_TENSOR_MAP_SWIZZLE_128B))
-      return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K1W observation map");
-    c->tm_w_ready = true;
+  if (pl.k1.needs_tmap() && c->tm_w_kind != pl.k1.kind) {
+    const bool ok = pl.k1.kind == 8
+                        ? make_tmap_f32_chunks(&c->tm_w, c->dV, c->ldv, c->p_pad, K1X_T, K1X_C,
+                                               CU_TENSOR_MAP_SWIZZLE_128B)
+                        : make_tmap_f32(&c->tm_w, c->dV, c->ldv, c->p_pad, 4 * c->ldv, K1W_NK,
+                                        K1W_T, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!ok) return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K1W/K1X map");
+    c->tm_w_kind = pl.k1.kind;
   }
   int rc;
   const int64_t n = c->n;
@@ -767,7 +771,7 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   c->own_v32 = false;
   c->tm_v_ready = false;
   c->tm_c_ready = false;
-  c->tm_w_ready = false;
+  c->tm_w_kind = 0;
   int rc = dtype == MCP_F64
                ? upload_obs<double>(c, (const double*)V, on_device, layout, n, p, ld)
                : upload_obs<float>(c, (const float*)V, on_device, layout, n, p, ld);

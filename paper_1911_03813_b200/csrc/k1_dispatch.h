@@ -27,14 +27,15 @@ struct K1Variant {
                        // 4: k1q_fg_pairs (warp-specialised pairs)  5: k1g_fg_dmma (Y in L2)
                        // 6: k1r_fg_triads (K1Q with the GEMM1 role split by columns)
                        // 7: k1w_fg_dmma (fp32 V, large n: resident TMA tile, cluster n-split)
+                       // 8: k1x_fg_dmma (fp32 V, n <= 512: 16 warps, double-buffered tiles)
   int stages = 0;      // ring depth (kind 1)
   int MT = 0;          // GEMM2 m-tiles (kind 1)
   int MTW2 = 1;        // slabs per TMA copy unit (kind 1)
   int cl = 1;          // kind 7: cluster size (CTAs splitting n)
   int cpw = 2;         // kind 7: 32-variable chunks per warp
   int wmode = 0;       // kind 7: work split (0 strided, 1 block-major ranges)
-  bool needs_prep() const { return kind == 0 || kind == 5 || kind == 7; }
-  bool needs_tmap() const { return kind == 7; }
+  bool needs_prep() const { return kind == 0 || kind == 5 || kind == 7 || kind == 8; }
+  bool needs_tmap() const { return kind == 7 || kind == 8; }
 };
 
 // Choose the variant for (dtype, n, r, p_pad) on a device with `sms` SMs.

@@ -14,6 +14,7 @@
 #include "k1p_fp64.cuh"
 #include "k1q_fp64.cuh"
 #include "k1w_fp64.cuh"
+#include "k1x_fp64.cuh"
 #if MCP_WITH_K1R
 #include "k1r_fp64.cuh"
 #endif
@@ -406,6 +407,56 @@ const EntryW kTableW[] = {MCP_K1W_E(2, 1, MCP_CFG_K1W_RB), MCP_K1W_E(1, 1, MCP_C
                           MCP_K1W_E(2, 2, MCP_CFG_K1W_RB)};
 constexpr int kEntriesW = sizeof(kTableW) / sizeof(kTableW[0]);
 
+// K1X: fp32 sets with 384 < n <= 512 and a chunk-aligned pitch (one 3-D TMA per tile)
+void launch_x(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(K1X_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k1x_fg_dmma, *tm, prm);
+}
+
+bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
+  if (dtype != MCP_F32 || n <= 384 || n > 512 || ldv % 32 != 0 || r < 12) return false;
+  if (!ensure_dyn_smem((const void*)k1x_fg_dmma, k1x_smem_bytes())) return false;
+  const int64_t T = p_pad / K1X_T;
+  const int Nc = sms;
+  v.kind = 8;
+  v.dtype = dtype;
+  v.RB = K1X_RB;
+  v.cl = 1;
+  v.cpw = 1;
+  v.n_pad = 512;
+  v.n_chunks = v.n_pad / 64;
+  v.rbs = (int)ceil_div(r, K1X_RB);
+  v.num_tiles = T;
+  if (Nc % v.rbs == 0 && Nc / v.rbs <= T) {
+    v.wmode = 0;
+    v.gp = Nc / v.rbs;
+  } else {
+    v.wmode = 1;
+    const int64_t U = (int64_t)v.rbs * T;
+    int64_t mx = 1;
+    for (int rb = 0; rb < v.rbs; ++rb)
+      mx = std::max<int64_t>(mx, k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
+    v.gp = (int)mx;
+  }
+  v.grid = Nc;
+  v.smem = k1x_smem_bytes();
+  v.entry = 0;
+  v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (K1X_RB / 8) * 32;
+  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * K1X_RB;
+  v.wpart_elems = (size_t)v.rbs * v.gp * K1X_RB;
+  v.name = std::string("k1x_fg_dmma<f32,RB=16,T=32,16 warps") + (v.wmode ? ",ranges" : ",strided") + ">";
+  return true;
+}
+
 // K1W applies to fp32 sets whose n fills the 256-variable (per CTA) chunk grid well, with
 // enough factor columns for its 32-wide blocks.
 bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v) {
@@ -469,7 +520,9 @@ int64_t obs_pitch(int dtype, int64_t n) {
     while (ldv % 16 != 4) ++ldv;
     return ldv;
   }
-  return round_up(n, 4);
+  // fp32: whole 32-float chunks for n > 128 (the 3-D chunk tensor maps of K1X and the fast
+  // mode need ldv % 32 == 0), else 16-byte rows
+  return n > 128 ? round_up(n, 32) : round_up(n, 4);
 }
 
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v,
@@ -491,6 +544,8 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
   if (dtype == MCP_F64 && MCP_CFG_K1S &&
       select_stream(n, r, p_pad, obs_pitch(dtype, n), sms, v))
     return true;
+  v = K1Variant();
+  if (MCP_CFG_K1X && select_x(dtype, n, r, p_pad, obs_pitch(dtype, n), sms, v)) return true;
   v = K1Variant();
   if (MCP_CFG_K1W && select_w(dtype, n, r, p_pad, sms, v)) return true;
   v = K1Variant();
@@ -596,7 +651,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
               double* wpart, cudaStream_t s, const void* tmap) {
   if (v.entry < 0) return 1;
-  if (v.kind == 7) {
+  if (v.kind == 7 || v.kind == 8) {
     if (!tmap) return 1;
     K1WParams wp;
     wp.num_tiles = v.num_tiles;
@@ -612,7 +667,10 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     wp.slots = v.gp;
     wp.Ypart = Ypart;
     wp.wpart = wpart;
-    kTableW[v.entry].launch(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+    if (v.kind == 8)
+      launch_x(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+    else
+      kTableW[v.entry].launch(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }
   if (v.kind == 1 || v.kind == 3 || v.kind == 4 || v.kind == 6) {

@@ -38,6 +38,9 @@
 #ifndef MCP_CFG_K1W
 #define MCP_CFG_K1W 1
 #endif
+#ifndef MCP_CFG_K1X
+#define MCP_CFG_K1X 1              // K1X (16 warps, double-buffered tiles) for 384 < n <= 512
+#endif
 #ifndef MCP_CFG_K1W_RB
 #define MCP_CFG_K1W_RB 32          // K1W factor columns per block (16 or 32)
 #endif

@@ -28,9 +28,12 @@ def _case(n, p, r, d, seed, weights=False):
 
 
 @pytest.mark.parametrize("n,p,r,d", [
-    (512, 300_000, 64, 6),    # c3 shape, strided split (148 CTAs / 2 blocks)
+    (512, 300_000, 64, 6),    # c3 shape (K1X strided: 148 CTAs / 4 blocks)
     (512, 300_000, 96, 3),    # 3 blocks: block-major ranges
     (512, 5_000, 64, 4),      # p < grid tiles: clusters without tiles, zero-filled slots
+    (512, 2_000, 16, 3),      # one column block, p < grid (K1X strided with idle CTAs)
+    (400, 30_000, 20, 5),     # K1X ragged n and r, ranges split (148 % 2 == 0 -> strided)
+    (512, 60_000, 48, 6),     # K1X: 3 column blocks over 148 CTAs -> block-major ranges
     (500, 40_000, 40, 2),     # ragged n and r (last block partly padding), d = 2
     (256, 50_000, 32, 5),     # CPW = 1
     (1024, 60_000, 256, 3),   # c5 shape: 2-CTA cluster, 8 blocks over 74 clusters
@@ -40,7 +43,7 @@ def test_k1w_vs_oracle(n, p, r, d):
     V, nu, lam, A = _case(n, p, r, d, seed=n + p + r)
     obs = mcp.ObservationSet(V, nu)
     res = mcp.fg_implicit(obs, lam, A, d, 0.3)
-    assert obs.device_context().last_variant.startswith("k1w_fg_dmma"), \
+    assert obs.device_context().last_variant.startswith(("k1w_fg_dmma", "k1x_fg_dmma")), \
         obs.device_context().last_variant
     V64 = V.astype(np.float64)
     nu64 = np.full(p, 1.0 / p) if nu is None else nu

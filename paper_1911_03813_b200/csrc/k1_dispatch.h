@@ -8,6 +8,10 @@
 
 namespace mcp {
 
+// K1X's 3-D observation box: one tile of 32 rows x 16 chunks of 32 floats (k1x_fp64.cuh)
+constexpr int K1X_BOX_ROWS = 32;
+constexpr int K1X_BOX_CHUNKS = 16;
+
 struct K1Variant {
   int dtype = 0;       // MCP_F64 / MCP_F32
   int RB = 8;          // factor columns per CTA

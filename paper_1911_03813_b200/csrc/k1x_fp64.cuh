@@ -39,9 +39,11 @@
 
 namespace mcp {
 
-constexpr int K1X_T = 32;             // observations per tile
+#include "k1_dispatch.h"
+
+constexpr int K1X_T = K1X_BOX_ROWS;   // observations per tile
 constexpr int K1X_RB = 16;            // factor columns per block
-constexpr int K1X_C = 16;             // 32-variable chunks per tile (n <= 512)
+constexpr int K1X_C = K1X_BOX_CHUNKS; // 32-variable chunks per tile (n <= 512)
 constexpr int K1X_THREADS = 512;      // 16 warps
 constexpr int K1X_SP = 18;            // P row pitch (doubles), == 2 mod 16
 constexpr int K1X_TILE_BYTES = K1X_T * 32 * 4 * K1X_C;          // 64 KB of V

@@ -408,31 +408,44 @@ const EntryW kTableW[] = {MCP_K1W_E(2, 1, MCP_CFG_K1W_RB), MCP_K1W_E(1, 1, MCP_C
 constexpr int kEntriesW = sizeof(kTableW) / sizeof(kTableW[0]);
 
 // K1X: fp32 sets with 384 < n <= 512 and a chunk-aligned pitch (one 3-D TMA per tile)
+template <int CL>
 void launch_x(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(K1X_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CL;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k1x_fg_dmma, *tm, prm);
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, k1x_fg_dmma<CL>, *tm, prm);
 }
 
+// K1X: fp32 sets with 384 < n <= 512 (one CTA) or 768 < n <= 1024 (2-CTA cluster), chunk-aligned
+// pitch (one 3-D TMA per tile)
 bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
-  if (dtype != MCP_F32 || n <= 384 || n > 512 || ldv % 32 != 0 || r < 12) return false;
-  if (!ensure_dyn_smem((const void*)k1x_fg_dmma, k1x_smem_bytes())) return false;
+  if (dtype != MCP_F32 || ldv % 32 != 0 || r < 12) return false;
+  int cl = 0;
+  if (n > 384 && n <= 512) cl = 1;
+  else if (n > 768 && n <= 1024) cl = 2;
+  if (!cl) return false;
+  const void* fn = cl == 1 ? (const void*)k1x_fg_dmma<1> : (const void*)k1x_fg_dmma<2>;
+  const size_t smem = cl == 1 ? k1x_smem_bytes<1>() : k1x_smem_bytes<2>();
+  if (!ensure_dyn_smem(fn, smem)) return false;
   const int64_t T = p_pad / K1X_T;
-  const int Nc = sms;
+  const int Nc = sms / cl;
   v.kind = 8;
   v.dtype = dtype;
   v.RB = K1X_RB;
-  v.cl = 1;
+  v.cl = cl;
   v.cpw = 1;
-  v.n_pad = 512;
+  v.n_pad = 512 * cl;
   v.n_chunks = v.n_pad / 64;
   v.rbs = (int)ceil_div(r, K1X_RB);
   v.num_tiles = T;
@@ -447,13 +460,14 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
       mx = std::max<int64_t>(mx, k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
     v.gp = (int)mx;
   }
-  v.grid = Nc;
-  v.smem = k1x_smem_bytes();
+  v.grid = Nc * cl;
+  v.smem = smem;
   v.entry = 0;
   v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (K1X_RB / 8) * 32;
   v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * K1X_RB;
   v.wpart_elems = (size_t)v.rbs * v.gp * K1X_RB;
-  v.name = std::string("k1x_fg_dmma<f32,RB=16,T=32,16 warps") + (v.wmode ? ",ranges" : ",strided") + ">";
+  v.name = std::string("k1x_fg_dmma<f32,RB=16,T=32,16 warps,CL=") + std::to_string(cl) +
+           (v.wmode ? ",ranges" : ",strided") + ">";
   return true;
 }
 
@@ -667,8 +681,10 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     wp.slots = v.gp;
     wp.Ypart = Ypart;
     wp.wpart = wpart;
-    if (v.kind == 8)
-      launch_x(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+    if (v.kind == 8 && v.cl == 2)
+      launch_x<2>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+    else if (v.kind == 8)
+      launch_x<1>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     else
       kTableW[v.entry].launch(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;

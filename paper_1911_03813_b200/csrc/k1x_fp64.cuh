@@ -24,7 +24,12 @@
 //    the 4 warps forms P for a quarter of the row block's elements, published on the row
 //    block's mbarrier;
 //  * GEMM2: warp w owns variables 32w .. 32w+31 (4 x 2 DMMA tiles, Y in registers), starts with
-//    its own row block and waits only for row blocks it has not seen.
+//    its own row block and waits only for row blocks it has not seen;
+//  * CL = 2 (n <= 1024, c5): a cluster of two CTAs splits the variables in halves; after the
+//    K-quarter merge each lane stores its element's half-Z into the PEER's shared memory
+//    (st.shared::cluster) and arrives on the peer's row-block mbarrier (release.cluster); both
+//    CTAs add the halves in cluster-rank order (bitwise the same Z and P on both) and run GEMM2
+//    on their own half of the tile.  No cluster-wide barrier per tile.
 // Fixed-order merges and per-element ownership keep results deterministic and exactly linear
 // in nu.
 #pragma once
@@ -49,10 +54,45 @@ constexpr int K1X_SP = 18;            // P row pitch (doubles), == 2 mod 16
 constexpr int K1X_TILE_BYTES = K1X_T * 32 * 4 * K1X_C;          // 64 KB of V
 constexpr int K1X_A_BYTES = K1X_C * 8 * (K1X_RB / 8) * 32 * 8;  // 64 KB of factor fragments
 
+template <int CL>
 __host__ __device__ constexpr size_t k1x_smem_bytes() {
+  // (the w flush scratch aliases the Z merge slots; CL = 2 adds the peer's half-Z slots)
   return 1024 /*alignment*/ + 2 * (size_t)K1X_TILE_BYTES + K1X_A_BYTES +
          2 * (size_t)K1X_T * K1X_SP * 8 /*P*/ + (size_t)4 * 4 * 8 * K1X_RB * 8 /*Z merge*/ +
-         (size_t)16 * 32 * 8 /*w*/ + 512 /*barriers*/;
+         (CL > 1 ? (size_t)2 * 4 * 128 * 8 : 0) /*peer half-Z*/ + 512 /*barriers*/;
+}
+
+__device__ __forceinline__ uint32_t k1x_peer_addr(const void* local, uint32_t peer) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
+               : "=r"(remote)
+               : "r"(smem_u32(local)), "r"(peer));
+  return remote;
+}
+__device__ __forceinline__ void k1x_st_peer(uint32_t remote, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(remote), "d"(v) : "memory");
+}
+__device__ __forceinline__ void k1x_arrive_peer(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote_bar)
+               : "memory");
+}
+// parity wait with cluster-scope acquire (the arrivals come from the peer CTA)
+__device__ __forceinline__ void k1x_wait_cluster(uint64_t* bar, uint32_t parity) {
+  auto try_once = [&]() {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+  };
+  if (try_once()) return;
+  const long long t0 = clock64();
+  while (!try_once()) {
+    if (clock64() - t0 > (1ll << 35)) __trap();
+  }
 }
 
 __device__ __forceinline__ void k1x_bar_rowblock(int rbk) {
@@ -63,7 +103,8 @@ __device__ __forceinline__ void k1x_bar_all() {
 }
 
 // tmV: 3-D map over the fp32 observations viewed as (32 floats, rows, ldv / 32 chunks), box
-// (32, 32, 16), 128-byte swizzle.  Uses K1WParams (n_pad = 512, RB = 16).
+// (32, 32, 16), 128-byte swizzle.  Uses K1WParams (n_pad = 512 CL, RB = 16).
+template <int CL>
 __global__ void __launch_bounds__(K1X_THREADS, 1)
     k1x_fg_dmma(const __grid_constant__ CUtensorMap tmV, K1WParams prm) {
   constexpr int NT = K1X_RB / 8;   // 2 column tiles
@@ -75,17 +116,21 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
   double* sA = reinterpret_cast<double*>(base + 2 * (size_t)K1X_TILE_BYTES);    // [128 ks][NT][32]
   double* sP = sA + K1X_A_BYTES / 8;                                            // [2][32][SP]
   double* sZm = sP + 2 * K1X_T * SP;                                            // [4][4][8][16]
-  double* sW = sZm + 4 * 4 * 8 * K1X_RB;                                        // [16][32]
-  uint64_t* fullV = reinterpret_cast<uint64_t*>(sW + 16 * 32);                  // [2]
+  double* sW = sZm;                                                             // [512] flush
+  double* sXz = sZm + 4 * 4 * 8 * K1X_RB;                                       // [2][4][128]
+  uint64_t* fullV = reinterpret_cast<uint64_t*>(sXz + (CL > 1 ? 2 * 4 * 128 : 0));  // [2]
   uint64_t* fullA = fullV + 2;                                                  // [1]
   uint64_t* fullP = fullA + 1;                                                  // [2][4]
-  unsigned* cntV = reinterpret_cast<unsigned*>(fullP + 8);                      // [2]
+  uint64_t* fullX = fullP + 8;                                                  // [2][4] peer half-Z
+  unsigned* cntV = reinterpret_cast<unsigned*>(fullX + 8);                      // [2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int rbk = warp >> 2;       // GEMM1 row block (tile rows 8 rbk .. +7)
   const int kq = warp & 3;         // GEMM1 K-quarter (chunks 4 kq .. 4 kq + 3)
-  const int cid = blockIdx.x;
+  const uint32_t crank = CL > 1 ? k1w_cluster_rank() : 0;
+  const int cid = blockIdx.x / CL;   // cluster index (the unit of the work split)
+  const int c0 = (int)crank * K1X_C; // this CTA's first 32-variable chunk
   const int dm1 = prm.d - 1;
 
   if (threadIdx.x == 0) {
@@ -93,11 +138,13 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
     mbar_init(&fullV[1], 1);
     mbar_init(fullA, 1);
     for (int i = 0; i < 8; ++i) mbar_init(&fullP[i], 4);   // the row block's 4 warps
+    for (int i = 0; i < 8; ++i) mbar_init(&fullX[i], 4);   // the peer row block's 4 warps
     cntV[0] = cntV[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tma_prefetch_desc(&tmV);
   }
   __syncthreads();
+  if constexpr (CL > 1) k1w_cluster_sync();   // both CTAs' barriers exist before any remote arrive
 
   K1WTile cur;
   const bool any = k1w_tile_at(prm, cid, 0, cur);
@@ -107,14 +154,15 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
       K1WTile tb;
       if (!k1w_tile_at(prm, cid, b, tb)) break;
       mbar_arrive_expect_tx(&fullV[b], K1X_TILE_BYTES);
-      tma_load_3d(sV + (size_t)b * (K1X_TILE_BYTES / 4), &tmV, 0, (int)(tb.tile * K1X_T), 0,
+      tma_load_3d(sV + (size_t)b * (K1X_TILE_BYTES / 4), &tmV, 0, (int)(tb.tile * K1X_T), c0,
                   smem_u32(&fullV[b]));
     }
   }
   pdl_enter();   // Afrag comes from the preceding prep kernel
   auto load_a = [&](int rb) {
     mbar_arrive_expect_tx(fullA, K1X_A_BYTES);
-    tma_bulk_g2s(sA, prm.Afrag + (size_t)rb * (K1X_A_BYTES / 8), K1X_A_BYTES, fullA);
+    tma_bulk_g2s(sA, prm.Afrag + (size_t)rb * CL * (K1X_A_BYTES / 8) + (size_t)crank * (K1X_A_BYTES / 8),
+                 K1X_A_BYTES, fullA);
   };
   if (any && threadIdx.x == 0) load_a(cur.rb);
   uint32_t aphase = 0;
@@ -144,9 +192,10 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
 
   if (!any && prm.mode == 0 && cid / prm.rbs < prm.slots) {
     const int rb = cid % prm.rbs, s = cid / prm.rbs;
-    double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1X_RB;
-    for (int e = threadIdx.x; e < prm.n_pad * K1X_RB; e += K1X_THREADS) Yp[e] = 0.0;
-    if (threadIdx.x < K1X_RB) prm.wpart[((size_t)rb * prm.slots + s) * K1X_RB + threadIdx.x] = 0.0;
+    double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1X_RB + (size_t)crank * 512 * K1X_RB;
+    for (int e = threadIdx.x; e < 512 * K1X_RB; e += K1X_THREADS) Yp[e] = 0.0;
+    if (crank == 0 && threadIdx.x < K1X_RB)
+      prm.wpart[((size_t)rb * prm.slots + s) * K1X_RB + threadIdx.x] = 0.0;
   }
 
   int64_t it = 0;
@@ -214,6 +263,18 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
       double zz = zr[0];
 #pragma unroll
       for (int q = 1; q < 4; ++q) zz += zr[q * 8 * K1X_RB];
+      if constexpr (CL > 1) {
+        // half-Z of this element to the peer CTA, then the peer's half from our own slots;
+        // rank 0's half first on both sides
+        double* slot = sXz + (size_t)(buf * 4 + rbk) * 128 + kq * 32 + lane;
+        const uint32_t peer = crank ^ 1u;
+        k1x_st_peer(k1x_peer_addr(slot, peer), zz);
+        __syncwarp();
+        if (lane == 0) k1x_arrive_peer(k1x_peer_addr(&fullX[buf * 4 + rbk], peer));
+        k1x_wait_cluster(&fullX[buf * 4 + rbk], vpar);
+        const double o = *slot;
+        zz = crank == 0 ? zz + o : o + zz;
+      }
       const int lr = 8 * rbk + e_row;
       const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
       const double pv = nul * rm_pow(zz, dm1);
@@ -277,14 +338,15 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
           k1w_fence_proxy_async();
           mbar_arrive_expect_tx(&fullV[buf], K1X_TILE_BYTES);
           tma_load_3d(sV + (size_t)buf * (K1X_TILE_BYTES / 4), &tmV, 0, (int)(t2.tile * K1X_T),
-                      0, smem_u32(&fullV[buf]));
+                      c0, smem_u32(&fullV[buf]));
         }
       }
     }
 
     // ---------------- end of a segment: flush this CTA's partial ----------------
     if (cur.last_in_seg || !has_next) {
-      double* Yp = prm.Ypart + ((size_t)cur.rb * prm.slots + cur.slot) * prm.n_pad * K1X_RB;
+      double* Yp = prm.Ypart + ((size_t)cur.rb * prm.slots + cur.slot) * prm.n_pad * K1X_RB +
+                   (size_t)crank * 512 * K1X_RB;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -294,10 +356,12 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
               make_double2(y[mt][nt][0], y[mt][nt][1]);
           y[mt][nt][0] = y[mt][nt][1] = 0.0;
         }
+      // (sW aliases the Z merge slots: every warp is past this tile's merge reads)
+      k1x_bar_all();
       sW[threadIdx.x] = wacc;
       wacc = 0.0;
       k1x_bar_all();
-      if (threadIdx.x < K1X_RB) {
+      if (crank == 0 && threadIdx.x < K1X_RB) {
         // column j's partial sums sit at thread ids with (kq * 32 + lane) % 16 == j, i.e. at
         // every 16th thread: 32 of them, added in thread order
         double s = 0.0;
@@ -317,13 +381,15 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
       const int used = (int)(k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
       for (int s = used; s < prm.slots; ++s) {
         if ((rb * prm.slots + s) % prm.nclusters != cid) continue;
-        double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1X_RB;
-        for (int e = threadIdx.x; e < prm.n_pad * K1X_RB; e += K1X_THREADS) Yp[e] = 0.0;
-        if (threadIdx.x < K1X_RB)
+        double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1X_RB +
+                     (size_t)crank * 512 * K1X_RB;
+        for (int e = threadIdx.x; e < 512 * K1X_RB; e += K1X_THREADS) Yp[e] = 0.0;
+        if (crank == 0 && threadIdx.x < K1X_RB)
           prm.wpart[((size_t)rb * prm.slots + s) * K1X_RB + threadIdx.x] = 0.0;
       }
     }
   }
+  if constexpr (CL > 1) k1w_cluster_sync();   // the peer may still write into our half-Z slots
 }
 
 }  // namespace mcp

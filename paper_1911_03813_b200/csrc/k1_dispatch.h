@@ -37,7 +37,8 @@ struct K1Variant {
   int MTW2 = 1;        // slabs per TMA copy unit (kind 1)
   int cl = 1;          // kind 7: cluster size (CTAs splitting n)
   int cpw = 2;         // kind 7: 32-variable chunks per warp
-  int wmode = 0;       // kind 7: work split (0 strided, 1 block-major ranges)
+  int groups = 0;      // kinds 7, 8: work split (k1w_fp64.cuh k1w_split)
+  int64_t t_main = 0;
   bool needs_prep() const { return kind == 0 || kind == 5 || kind == 7 || kind == 8; }
   bool needs_tmap() const { return kind == 7 || kind == 8; }
 };

@@ -439,7 +439,6 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
   const size_t smem = cl == 1 ? k1x_smem_bytes<1>() : k1x_smem_bytes<2>();
   if (!ensure_dyn_smem(fn, smem)) return false;
   const int64_t T = p_pad / K1X_T;
-  const int Nc = sms / cl;
   v.kind = 8;
   v.dtype = dtype;
   v.RB = K1X_RB;
@@ -449,17 +448,12 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
   v.n_chunks = v.n_pad / 64;
   v.rbs = (int)ceil_div(r, K1X_RB);
   v.num_tiles = T;
-  if (Nc % v.rbs == 0 && Nc / v.rbs <= T) {
-    v.wmode = 0;
-    v.gp = Nc / v.rbs;
-  } else {
-    v.wmode = 1;
-    const int64_t U = (int64_t)v.rbs * T;
-    int64_t mx = 1;
-    for (int rb = 0; rb < v.rbs; ++rb)
-      mx = std::max<int64_t>(mx, k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
-    v.gp = (int)mx;
-  }
+  const int Nc = (int)std::min<int64_t>(sms / cl, (int64_t)v.rbs * T);
+  k1w_split(T, v.rbs, Nc, v.groups, v.t_main);
+  int mx = 1;
+  for (int rb = 0; rb < v.rbs; ++rb)
+    mx = std::max(mx, k1w_used_slots(rb, T, v.rbs, Nc, v.groups, v.t_main));
+  v.gp = mx;
   v.grid = Nc * cl;
   v.smem = smem;
   v.entry = 0;
@@ -467,7 +461,7 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
   v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * K1X_RB;
   v.wpart_elems = (size_t)v.rbs * v.gp * K1X_RB;
   v.name = std::string("k1x_fg_dmma<f32,RB=16,T=32,16 warps,CL=") + std::to_string(cl) +
-           (v.wmode ? ",ranges" : ",strided") + ">";
+           ",G=" + std::to_string(v.groups) + (v.t_main < T ? ",+ranges" : "") + ">";
   return true;
 }
 
@@ -484,7 +478,6 @@ bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v)
   const EntryW& en = kTableW[e];
   if (!ensure_dyn_smem(en.fn, en.smem)) return false;
   const int64_t T = p_pad / K1W_T;
-  const int Nc = sms / en.cl;
   v.kind = 7;
   v.dtype = dtype;
   v.RB = en.rb;
@@ -494,25 +487,21 @@ bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v)
   v.n_chunks = v.n_pad / 64;   // Afrag k-steps = n_pad / 4 = 16 n_chunks
   v.rbs = (int)ceil_div(r, en.rb);
   v.num_tiles = T;
-  if (Nc % v.rbs == 0 && Nc / v.rbs <= T) {
-    v.wmode = 0;
-    v.gp = Nc / v.rbs;
-  } else {
-    v.wmode = 1;
-    const int64_t U = (int64_t)v.rbs * T;
-    int64_t mx = 1;
-    for (int rb = 0; rb < v.rbs; ++rb)
-      mx = std::max<int64_t>(mx, k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
-    v.gp = (int)mx;
-  }
+  const int Nc = (int)std::min<int64_t>(sms / en.cl, (int64_t)v.rbs * T);
+  k1w_split(T, v.rbs, Nc, v.groups, v.t_main);
+  int mx = 1;
+  for (int rb = 0; rb < v.rbs; ++rb)
+    mx = std::max(mx, k1w_used_slots(rb, T, v.rbs, Nc, v.groups, v.t_main));
+  v.gp = mx;
   v.grid = Nc * en.cl;
   v.smem = en.smem;
   v.entry = e;
   v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (en.rb / 8) * 32;
   v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * en.rb;
   v.wpart_elems = (size_t)v.rbs * v.gp * en.rb;
-  v.name = std::string("k1w_fg_dmma<f32,RB=") + std::to_string(en.rb) + ",CPW=" + std::to_string(en.cpw) + ",CL=" +
-           std::to_string(en.cl) + (v.wmode ? ",ranges" : ",strided") + ">";
+  v.name = std::string("k1w_fg_dmma<f32,RB=") + std::to_string(en.rb) + ",CPW=" +
+           std::to_string(en.cpw) + ",CL=" + std::to_string(en.cl) + ",G=" +
+           std::to_string(v.groups) + (v.t_main < T ? ",+ranges" : "") + ">";
   return true;
 }
 
@@ -677,7 +666,8 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     wp.d = d;
     wp.rbs = v.rbs;
     wp.nclusters = v.grid / v.cl;
-    wp.mode = v.wmode;
+    wp.groups = v.groups;
+    wp.t_main = v.t_main;
     wp.slots = v.gp;
     wp.Ypart = Ypart;
     wp.wpart = wpart;

@@ -68,8 +68,9 @@ struct K1WParams {
   const double* Afrag;    // [rbs][n_pad / 4][RB / 8][32]
   int d;
   int rbs;
-  int nclusters;          // gridDim.x / CL
-  int mode;               // 0: strided (nclusters % rbs == 0), 1: block-major ranges
+  int nclusters;          // gridDim.x / CL (<= rbs * num_tiles: no cluster without work)
+  int groups;             // G = nclusters / rbs clusters per column block stride the main tiles
+  int64_t t_main;         // main region: tiles [0, t_main) of every block (see k1w_tile_at)
   int slots;              // partial slots per column block
   double* Ypart;          // [rbs][slots][n_pad][RB]
   double* wpart;          // [rbs][slots][RB]
@@ -112,28 +113,67 @@ struct K1WTile {
   bool last_in_seg;   // flush the partial after this tile
 };
 
+// Work split over (column block, tile) units, shared by the host plan and the kernels:
+//  * main region, tiles [0, t_main): the first G * rbs clusters form G groups of one cluster per
+//    column block; member j of a group strides over tiles j, j + G, ... -- the rbs clusters that
+//    read a tile do so at about the same time, so V comes from HBM once and from L2 rbs - 1
+//    times (slot j of the block);
+//  * leftover region, tiles [t_main, T): the L = Nc - G rbs remaining clusters take equal
+//    contiguous ranges of the block-major unit list (slots G, G + 1, ... of each block they
+//    touch); t_main = floor(G rbs T / Nc) equalises the work of both kinds of cluster.
+// With Nc <= rbs * T every cluster has work and every slot 0 .. G - 1 + (clusters touching a
+// block in the leftover region) is written exactly once; the remaining slots up to `slots` are
+// zero-filled.
+__host__ __device__ inline void k1w_split(int64_t T, int rbs, int64_t Nc, int& G, int64_t& t_main) {
+  G = (int)(Nc / rbs);
+  t_main = (Nc % rbs == 0) ? T : (int64_t)G * rbs * T / Nc;
+}
+__host__ __device__ inline int k1w_used_slots(int rb, int64_t T, int rbs, int64_t Nc, int G,
+                                              int64_t t_main) {
+  const int64_t L = Nc - (int64_t)G * rbs, T2 = T - t_main, U2 = (int64_t)rbs * T2;
+  if (L == 0 || T2 == 0) return G;
+  return G + (int)(k1w_clast(rb, T2, U2, L) - k1w_cfirst(rb, T2, U2, L) + 1);
+}
+
 // Tile `k` (0-based) of cluster c's work list; returns false past the end.
 __device__ __forceinline__ bool k1w_tile_at(const K1WParams& prm, int c, int64_t k, K1WTile& o) {
   const int64_t T = prm.num_tiles;
-  if (prm.mode == 0) {
-    const int per = prm.nclusters / prm.rbs;
+  const int G = prm.groups;
+  if (c < G * prm.rbs) {
     const int slot = c / prm.rbs;
-    const int64_t tile = slot + k * per;
-    if (tile >= T) return false;
+    const int64_t tile = slot + k * G;
+    if (tile >= prm.t_main) return false;
     o.rb = c % prm.rbs;
     o.slot = slot;
     o.tile = tile;
-    o.last_in_seg = tile + per >= T;
+    o.last_in_seg = tile + G >= prm.t_main;
     return true;
   }
-  const int64_t U = (int64_t)prm.rbs * T, Nc = prm.nclusters;
-  const int64_t u = k1w_u0(c, U, Nc) + k;
-  if (u >= k1w_u0(c + 1, U, Nc)) return false;
-  o.rb = (int)(u / T);
-  o.tile = u % T;
-  o.slot = (int)(c - k1w_cfirst(o.rb, T, U, Nc));
-  o.last_in_seg = (u + 1 == k1w_u0(c + 1, U, Nc)) || ((u + 1) % T == 0);
+  const int64_t L = prm.nclusters - (int64_t)G * prm.rbs, T2 = T - prm.t_main;
+  const int64_t U2 = (int64_t)prm.rbs * T2, lc = c - (int64_t)G * prm.rbs;
+  const int64_t u = k1w_u0(lc, U2, L) + k;
+  if (u >= k1w_u0(lc + 1, U2, L)) return false;
+  o.rb = (int)(u / T2);
+  o.tile = prm.t_main + u % T2;
+  o.slot = G + (int)(lc - k1w_cfirst(o.rb, T2, U2, L));
+  o.last_in_seg = (u + 1 == k1w_u0(lc + 1, U2, L)) || ((u + 1) % T2 == 0);
   return true;
+}
+
+// Zero the partial slots no cluster writes (blocks touched by fewer leftover clusters).
+template <int THREADS, int RB>
+__device__ __forceinline__ void k1w_zero_holes(const K1WParams& prm, int cid, int var0, int nvars,
+                                               bool write_w) {
+  for (int rb = 0; rb < prm.rbs; ++rb) {
+    const int used = k1w_used_slots(rb, prm.num_tiles, prm.rbs, prm.nclusters, prm.groups,
+                                    prm.t_main);
+    for (int s = used; s < prm.slots; ++s) {
+      if ((rb * prm.slots + s) % prm.nclusters != cid) continue;
+      double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * RB + (size_t)var0 * RB;
+      for (int e = threadIdx.x; e < nvars * RB; e += THREADS) Yp[e] = 0.0;
+      if (write_w && threadIdx.x < RB) prm.wpart[((size_t)rb * prm.slots + s) * RB + threadIdx.x] = 0.0;
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t k1w_cluster_rank() {
@@ -267,16 +307,6 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
   double wacc[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
-
-  if (!any && prm.mode == 0 && cid / prm.rbs < prm.slots) {
-    // a strided cluster without tiles (p smaller than the grid) still owns a (zero) partial
-    const int rb = cid % prm.rbs, s = cid / prm.rbs;
-    double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * RB;
-    for (int e = threadIdx.x; e < 32 * C * RB; e += K1W_THREADS)
-      Yp[(size_t)n0 * RB + e] = 0.0;
-    if (crank == 0 && threadIdx.x < RB)
-      prm.wpart[((size_t)rb * prm.slots + s) * RB + threadIdx.x] = 0.0;
-  }
 
   int aslot = 0;            // factor ring position of the next chunk
   uint32_t aphase = 0;
@@ -489,22 +519,7 @@ __global__ void __launch_bounds__(K1W_THREADS, 1)
     ++it;
   }
 
-  // partial slots no cluster writes (block-major split with fewer clusters on some blocks):
-  // zero them so the fixed-order reduce can sum every slot
-  if (prm.mode == 1) {
-    const int64_t T = prm.num_tiles, U = (int64_t)prm.rbs * T, Nc = prm.nclusters;
-    for (int rb = 0; rb < prm.rbs; ++rb) {
-      const int used = (int)(k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
-      for (int s = used; s < prm.slots; ++s) {
-        if ((rb * prm.slots + s) % prm.nclusters != cid) continue;
-        double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * RB;
-        for (int e = threadIdx.x; e < 32 * C * RB; e += K1W_THREADS)
-          Yp[(size_t)n0 * RB + e] = 0.0;
-        if (crank == 0 && threadIdx.x < RB)
-          prm.wpart[((size_t)rb * prm.slots + s) * RB + threadIdx.x] = 0.0;
-      }
-    }
-  }
+  k1w_zero_holes<K1W_THREADS, RB>(prm, cid, n0, 32 * C, crank == 0);
   if constexpr (CL > 1) k1w_cluster_sync();   // no CTA exits while its peer may read its Z
 }
 

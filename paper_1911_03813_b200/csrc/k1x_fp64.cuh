@@ -190,14 +190,6 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
   double wacc = 0.0;   // this lane's epilogue element column: (kq * 32 + lane) % 16
   const int e_row = (kq * 32 + lane) >> 4, e_col = (kq * 32 + lane) & 15;
 
-  if (!any && prm.mode == 0 && cid / prm.rbs < prm.slots) {
-    const int rb = cid % prm.rbs, s = cid / prm.rbs;
-    double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1X_RB + (size_t)crank * 512 * K1X_RB;
-    for (int e = threadIdx.x; e < 512 * K1X_RB; e += K1X_THREADS) Yp[e] = 0.0;
-    if (crank == 0 && threadIdx.x < K1X_RB)
-      prm.wpart[((size_t)rb * prm.slots + s) * K1X_RB + threadIdx.x] = 0.0;
-  }
-
   int64_t it = 0;
   while (any) {
     const int buf = (int)(it & 1);
@@ -375,20 +367,7 @@ __global__ void __launch_bounds__(K1X_THREADS, 1)
     ++it;
   }
 
-  if (prm.mode == 1) {
-    const int64_t T = prm.num_tiles, U = (int64_t)prm.rbs * T, Nc = prm.nclusters;
-    for (int rb = 0; rb < prm.rbs; ++rb) {
-      const int used = (int)(k1w_clast(rb, T, U, Nc) - k1w_cfirst(rb, T, U, Nc) + 1);
-      for (int s = used; s < prm.slots; ++s) {
-        if ((rb * prm.slots + s) % prm.nclusters != cid) continue;
-        double* Yp = prm.Ypart + ((size_t)rb * prm.slots + s) * prm.n_pad * K1X_RB +
-                     (size_t)crank * 512 * K1X_RB;
-        for (int e = threadIdx.x; e < 512 * K1X_RB; e += K1X_THREADS) Yp[e] = 0.0;
-        if (crank == 0 && threadIdx.x < K1X_RB)
-          prm.wpart[((size_t)rb * prm.slots + s) * K1X_RB + threadIdx.x] = 0.0;
-      }
-    }
-  }
+  k1w_zero_holes<K1X_THREADS, K1X_RB>(prm, cid, (int)crank * 512, 512, crank == 0);
   if constexpr (CL > 1) k1w_cluster_sync();   // the peer may still write into our half-Z slots
 }
 

@@ -433,7 +433,7 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
   if (dtype != MCP_F32 || ldv % 32 != 0 || r < 12) return false;
   int cl = 0;
   if (n > 384 && n <= 512) cl = 1;
-  else if (n > 768 && n <= 1024) cl = 2;
+  else if (MCP_CFG_K1X_CL2 && n > 768 && n <= 1024) cl = 2;
   if (!cl) return false;
   const void* fn = cl == 1 ? (const void*)k1x_fg_dmma<1> : (const void*)k1x_fg_dmma<2>;
   const size_t smem = cl == 1 ? k1x_smem_bytes<1>() : k1x_smem_bytes<2>();

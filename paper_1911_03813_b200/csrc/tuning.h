@@ -41,6 +41,11 @@
 #ifndef MCP_CFG_K1X
 #define MCP_CFG_K1X 1              // K1X (16 warps, double-buffered tiles) for 384 < n <= 512
 #endif
+// K1X's 2-CTA cluster form for 768 < n <= 1024: the per-tile half-Z exchange between the two
+// SMs costs ~11% (c5: 654 ms vs 622 ms for K1G), so K1G stays the default there
+#ifndef MCP_CFG_K1X_CL2
+#define MCP_CFG_K1X_CL2 0
+#endif
 #ifndef MCP_CFG_K1W_RB
 #define MCP_CFG_K1W_RB 32          // K1W factor columns per block (16 or 32)
 #endif

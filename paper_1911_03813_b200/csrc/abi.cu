@@ -24,7 +24,6 @@
 #include "pdl.h"
 #include "k1_dispatch.h"
 #include "k1t_tf32.cuh"
-#include "k1w_fp64.cuh"
 #include "ctx.h"
 
 #include <cuda.h>
@@ -363,12 +362,9 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   if (!k1_select(c->dtype, c->n, r, c->p_pad, c->sms, pl.k1, why))
     return c->fail(MCP_ERR_ARG, why);
   if (pl.k1.needs_tmap() && c->tm_w_kind != pl.k1.kind) {
-    const bool ok = pl.k1.kind == 8
-                        ? make_tmap_f32_chunks(&c->tm_w, c->dV, c->ldv, c->p_pad, K1X_BOX_ROWS, K1X_BOX_CHUNKS,
-                                               CU_TENSOR_MAP_SWIZZLE_128B)
-                        : make_tmap_f32(&c->tm_w, c->dV, c->ldv, c->p_pad, 4 * c->ldv, K1W_NK,
-                                        K1W_T, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (!ok) return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K1W/K1X map");
+    if (!make_tmap_f32_chunks(&c->tm_w, c->dV, c->ldv, c->p_pad, K1X_BOX_ROWS, K1X_BOX_CHUNKS,
+                              CU_TENSOR_MAP_SWIZZLE_128B))
+      return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K1X observation map");
     c->tm_w_kind = pl.k1.kind;
   }
   int rc;

@@ -30,24 +30,23 @@ struct K1Variant {
                        // 2: k1t_fg_tf32 (tcgen05 fast mode)  3: k1p_fg_pairs (self-fed pairs)
                        // 4: k1q_fg_pairs (warp-specialised pairs)  5: k1g_fg_dmma (Y in L2)
                        // 6: k1r_fg_triads (K1Q with the GEMM1 role split by columns)
-                       // 7: k1w_fg_dmma (fp32 V, large n: resident TMA tile, cluster n-split)
                        // 8: k1x_fg_dmma (fp32 V, n <= 512: 16 warps, double-buffered tiles)
   int stages = 0;      // ring depth (kind 1)
   int MT = 0;          // GEMM2 m-tiles (kind 1)
   int MTW2 = 1;        // slabs per TMA copy unit (kind 1)
-  int cl = 1;          // kind 7: cluster size (CTAs splitting n)
-  int cpw = 2;         // kind 7: 32-variable chunks per warp
-  int groups = 0;      // kinds 7, 8: work split (k1w_fp64.cuh k1w_split)
+  int cl = 1;          // kind 8: cluster size (CTAs splitting n)
+  int cpw = 1;
+  int groups = 0;      // kind 8: work split (k1x_common.cuh k1w_split)
   int64_t t_main = 0;
-  bool needs_prep() const { return kind == 0 || kind == 5 || kind == 7 || kind == 8; }
-  bool needs_tmap() const { return kind == 7 || kind == 8; }
+  bool needs_prep() const { return kind == 0 || kind == 5 || kind == 8; }
+  bool needs_tmap() const { return kind == 8; }
 };
 
 // Choose the variant for (dtype, n, r, p_pad) on a device with `sms` SMs.
 bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v, std::string& why);
 
 // Launch K1 on stream s; returns 0 on success.
-// tmap: the K1W observation tensor map (CUtensorMap*, fp32 V, 32 x 64 boxes, 128-byte swizzle)
+// tmap: the K1X observation tensor map (CUtensorMap*, fp32 V, 3-D 32 x 32 x 16 boxes, swizzled)
 // when v.needs_tmap(), else ignored.
 int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const double* dnu,
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,

@@ -13,7 +13,7 @@
 #include "k1s_fp64.cuh"
 #include "k1p_fp64.cuh"
 #include "k1q_fp64.cuh"
-#include "k1w_fp64.cuh"
+#include "k1x_common.cuh"
 #include "k1x_fp64.cuh"
 #if MCP_WITH_K1R
 #include "k1r_fp64.cuh"
@@ -374,40 +374,6 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   return true;
 }
 
-// ---------------- K1W (fp32 V, large n: resident TMA tile, cluster n-split) ----------------
-template <int CPW, int CL, int RB>
-void launch_w(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(K1W_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = CL;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, k1w_fg_dmma<CPW, CL, RB>, *tm, prm);
-}
-using LaunchW = void (*)(const K1WParams&, const CUtensorMap*, int, size_t, cudaStream_t);
-struct EntryW {
-  int cpw, cl, rb;
-  LaunchW launch;
-  const void* fn;
-  size_t smem;
-};
-#define MCP_K1W_E(CPW, CL, RB)                                                                \
-  {CPW, CL, RB, &launch_w<CPW, CL, RB>, (const void*)&k1w_fg_dmma<CPW, CL, RB>,             \
-   k1w_smem_bytes<CPW, CL, RB>()}
-const EntryW kTableW[] = {MCP_K1W_E(2, 1, MCP_CFG_K1W_RB), MCP_K1W_E(1, 1, MCP_CFG_K1W_RB),
-                          MCP_K1W_E(2, 2, MCP_CFG_K1W_RB)};
-constexpr int kEntriesW = sizeof(kTableW) / sizeof(kTableW[0]);
-
-// K1X: fp32 sets with 384 < n <= 512 and a chunk-aligned pitch (one 3-D TMA per tile)
 template <int CL>
 void launch_x(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
@@ -433,10 +399,15 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
   if (dtype != MCP_F32 || ldv % 32 != 0 || r < 12) return false;
   int cl = 0;
   if (n > 384 && n <= 512) cl = 1;
-  else if (MCP_CFG_K1X_CL2 && n > 768 && n <= 1024) cl = 2;
-  if (!cl) return false;
+#if MCP_CFG_K1X_CL2
+  else if (n > 768 && n <= 1024) cl = 2;
   const void* fn = cl == 1 ? (const void*)k1x_fg_dmma<1> : (const void*)k1x_fg_dmma<2>;
   const size_t smem = cl == 1 ? k1x_smem_bytes<1>() : k1x_smem_bytes<2>();
+#else
+  const void* fn = (const void*)k1x_fg_dmma<1>;
+  const size_t smem = k1x_smem_bytes<1>();
+#endif
+  if (!cl) return false;
   if (!ensure_dyn_smem(fn, smem)) return false;
   const int64_t T = p_pad / K1X_T;
   v.kind = 8;
@@ -462,46 +433,6 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
   v.wpart_elems = (size_t)v.rbs * v.gp * K1X_RB;
   v.name = std::string("k1x_fg_dmma<f32,RB=16,T=32,16 warps,CL=") + std::to_string(cl) +
            ",G=" + std::to_string(v.groups) + (v.t_main < T ? ",+ranges" : "") + ">";
-  return true;
-}
-
-// K1W applies to fp32 sets whose n fills the 256-variable (per CTA) chunk grid well, with
-// enough factor columns for its 32-wide blocks.
-bool select_w(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v) {
-  if (dtype != MCP_F32 || r < (MCP_CFG_K1W_RB * 3) / 4) return false;
-  int e = -1;
-  for (int i = 0; i < kEntriesW && e < 0; ++i) {
-    const int64_t npad = 256LL * kTableW[i].cpw * kTableW[i].cl;
-    if (n <= npad && 4 * n > 3 * npad) e = i;   // <= 33% padding
-  }
-  if (e < 0) return false;
-  const EntryW& en = kTableW[e];
-  if (!ensure_dyn_smem(en.fn, en.smem)) return false;
-  const int64_t T = p_pad / K1W_T;
-  v.kind = 7;
-  v.dtype = dtype;
-  v.RB = en.rb;
-  v.cl = en.cl;
-  v.cpw = en.cpw;
-  v.n_pad = 256 * en.cpw * en.cl;
-  v.n_chunks = v.n_pad / 64;   // Afrag k-steps = n_pad / 4 = 16 n_chunks
-  v.rbs = (int)ceil_div(r, en.rb);
-  v.num_tiles = T;
-  const int Nc = (int)std::min<int64_t>(sms / en.cl, (int64_t)v.rbs * T);
-  k1w_split(T, v.rbs, Nc, v.groups, v.t_main);
-  int mx = 1;
-  for (int rb = 0; rb < v.rbs; ++rb)
-    mx = std::max(mx, k1w_used_slots(rb, T, v.rbs, Nc, v.groups, v.t_main));
-  v.gp = mx;
-  v.grid = Nc * en.cl;
-  v.smem = en.smem;
-  v.entry = e;
-  v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (en.rb / 8) * 32;
-  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * en.rb;
-  v.wpart_elems = (size_t)v.rbs * v.gp * en.rb;
-  v.name = std::string("k1w_fg_dmma<f32,RB=") + std::to_string(en.rb) + ",CPW=" +
-           std::to_string(en.cpw) + ",CL=" + std::to_string(en.cl) + ",G=" +
-           std::to_string(v.groups) + (v.t_main < T ? ",+ranges" : "") + ">";
   return true;
 }
 
@@ -549,8 +480,6 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
     return true;
   v = K1Variant();
   if (MCP_CFG_K1X && select_x(dtype, n, r, p_pad, obs_pitch(dtype, n), sms, v)) return true;
-  v = K1Variant();
-  if (MCP_CFG_K1W && select_w(dtype, n, r, p_pad, sms, v)) return true;
   v = K1Variant();
   // K1G when registers cap K1's column block at a quarter (or less) of K1G's: e.g. n = 1024,
   // r = 256 (c5): K1 RB = 16 vs K1G RB = 64 -> 4x fewer passes over V (measured 18% faster);
@@ -654,7 +583,7 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
               double nu_const, const double* A, int r, const double* Afrag, int d, double* Ypart,
               double* wpart, cudaStream_t s, const void* tmap) {
   if (v.entry < 0) return 1;
-  if (v.kind == 7 || v.kind == 8) {
+  if (v.kind == 8) {
     if (!tmap) return 1;
     K1WParams wp;
     wp.num_tiles = v.num_tiles;
@@ -671,12 +600,12 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     wp.slots = v.gp;
     wp.Ypart = Ypart;
     wp.wpart = wpart;
-    if (v.kind == 8 && v.cl == 2)
+#if MCP_CFG_K1X_CL2
+    if (v.cl == 2)
       launch_x<2>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
-    else if (v.kind == 8)
-      launch_x<1>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     else
-      kTableW[v.entry].launch(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+#endif
+      launch_x<1>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }
   if (v.kind == 1 || v.kind == 3 || v.kind == 4 || v.kind == 6) {

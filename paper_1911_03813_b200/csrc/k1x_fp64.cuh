@@ -37,7 +37,7 @@
 #include <cuda.h>
 
 #include "k1s_fp64.cuh"   // mbarrier helpers
-#include "k1w_fp64.cuh"   // work split, cluster/proxy helpers, ordered shared loads
+#include "k1x_common.cuh" // work split, cluster/proxy helpers, ordered shared loads
 #include "mcp_common.cuh"
 #include "pdl.h"
 #include "umma.cuh"       // TMA helpers

@@ -34,10 +34,6 @@
 #ifndef MCP_WITH_K1R
 #define MCP_WITH_K1R 0
 #endif
-// large-n FP64: K1W (TMA-staged, warp-specialised) when it has a variant for the shape
-#ifndef MCP_CFG_K1W
-#define MCP_CFG_K1W 1
-#endif
 #ifndef MCP_CFG_K1X
 #define MCP_CFG_K1X 1              // K1X (16 warps, double-buffered tiles) for 384 < n <= 512
 #endif
@@ -45,9 +41,6 @@
 // SMs costs ~11% (c5: 654 ms vs 622 ms for K1G), so K1G stays the default there
 #ifndef MCP_CFG_K1X_CL2
 #define MCP_CFG_K1X_CL2 0
-#endif
-#ifndef MCP_CFG_K1W_RB
-#define MCP_CFG_K1W_RB 32          // K1W factor columns per block (16 or 32)
 #endif
 // K1G (Y partial in L2) for large n when K1's register-bound column block is <= 1/4 of K1G's
 #ifndef MCP_CFG_K1G

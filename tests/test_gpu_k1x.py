@@ -1,11 +1,11 @@
-"""K1W (fp32 observations, large n: resident TMA tile, cluster n-split) against the CPU oracle.
+"""K1X (fp32 observations, 384 < n <= 512: 16 warps, double-buffered TMA tiles, resident
+factor block) and the other large-n FP64 kernels against the CPU oracle.
 
-Covers both work splits (strided column blocks when the clusters divide evenly, block-major
-ranges otherwise -- including grids larger than the tile count, where clusters own no tiles and
-partial slots are zero-filled), the 2-CTA cluster (n > 512), ragged n and r, weights, every
-order d, and bitwise determinism / nu-linearity (the reference invariants,
-pkg/tests/test_implicit.py:53-57).  FP64 mode tolerance: 1e-10 term-scale
-(pkg/tests/test_acceptance.py:65-74).
+Covers the work split (groups of one CTA per column block striding the main tiles, block-major
+ranges for the leftover CTAs -- including grids capped at the unit count for small p, and
+zero-filled partial slots), ragged n and r, every order d, and bitwise determinism /
+nu-linearity (the reference invariants, pkg/tests/test_implicit.py:53-57).  FP64 mode
+tolerance: 1e-10 term-scale (pkg/tests/test_acceptance.py:65-74).
 """
 
 import numpy as np
@@ -27,23 +27,23 @@ def _case(n, p, r, d, seed, weights=False):
     return V, nu, lam, A
 
 
-@pytest.mark.parametrize("n,p,r,d", [
-    (512, 300_000, 64, 6),    # c3 shape (K1X strided: 148 CTAs / 4 blocks)
-    (512, 300_000, 96, 3),    # 3 blocks: block-major ranges
-    (512, 5_000, 64, 4),      # p < grid tiles: clusters without tiles, zero-filled slots
-    (512, 2_000, 16, 3),      # one column block, p < grid (K1X strided with idle CTAs)
-    (400, 30_000, 20, 5),     # K1X ragged n and r, ranges split (148 % 2 == 0 -> strided)
-    (512, 60_000, 48, 6),     # K1X: 3 column blocks over 148 CTAs -> block-major ranges
-    (500, 40_000, 40, 2),     # ragged n and r (last block partly padding), d = 2
-    (256, 50_000, 32, 5),     # CPW = 1
-    (1024, 60_000, 256, 3),   # c5 shape: 2-CTA cluster, 8 blocks over 74 clusters
-    (900, 20_000, 33, 4),     # cluster, ragged
+@pytest.mark.parametrize("n,p,r,d,k1x", [
+    (512, 300_000, 64, 6, True),    # c3 shape: 4 blocks, 37 groups strided (148 CTAs)
+    (512, 300_000, 96, 3, True),    # 6 blocks: 24 groups + 4 leftover CTAs on block-major ranges
+    (512, 5_000, 64, 4, True),      # small p: grid capped at the unit count
+    (512, 2_000, 16, 3, True),      # one column block, fewer tiles than SMs
+    (400, 30_000, 20, 5, True),     # ragged n and r
+    (512, 60_000, 48, 6, True),     # 3 blocks: 49 groups + 1 leftover CTA
+    (500, 40_000, 40, 2, True),     # ragged n and r, d = 2
+    (256, 50_000, 32, 5, False),    # n <= 384: the register-tiled K1
+    (1024, 60_000, 256, 3, False),  # c5 shape: K1G (Y partial in L2)
+    (900, 20_000, 33, 4, False),    # large ragged n
 ])
-def test_k1w_vs_oracle(n, p, r, d):
+def test_large_n_fp32_vs_oracle(n, p, r, d, k1x):
     V, nu, lam, A = _case(n, p, r, d, seed=n + p + r)
     obs = mcp.ObservationSet(V, nu)
     res = mcp.fg_implicit(obs, lam, A, d, 0.3)
-    assert obs.device_context().last_variant.startswith(("k1w_fg_dmma", "k1x_fg_dmma")), \
+    assert obs.device_context().last_variant.startswith("k1x_fg_dmma") == k1x, \
         obs.device_context().last_variant
     V64 = V.astype(np.float64)
     nu64 = np.full(p, 1.0 / p) if nu is None else nu
@@ -55,7 +55,7 @@ def test_k1w_vs_oracle(n, p, r, d):
     assert e <= 1e-10
 
 
-def test_k1w_deterministic_and_linear_in_nu():
+def test_k1x_deterministic_and_linear_in_nu():
     n, p, r, d = 512, 40_000, 64, 4
     V, _, lam, A = _case(n, p, r, d, seed=3)
     nu = np.random.default_rng(4).uniform(0.5, 2.0, p) / p
@@ -66,7 +66,7 @@ def test_k1w_deterministic_and_linear_in_nu():
     assert np.array_equal(2.0 * Y1, Y2)
 
 
-def test_k1w_zero_lambda_exact():
-    V, _, _, A = _case(1024, 9_000, 64, 3, seed=5)
+def test_k1x_zero_lambda_exact():
+    V, _, _, A = _case(512, 9_000, 64, 3, seed=5)
     res = mcp.fg_implicit(mcp.ObservationSet(V), np.zeros(64), A, 3, 0.0)
     assert res.f == 0.0 and np.array_equal(res.g_A, np.zeros_like(A))

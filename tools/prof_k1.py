@@ -19,7 +19,8 @@ ap.add_argument("--mode", default=None)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 V = synth.device_observations(cfg, 2024, p=a.p)
-obs = mcp.ObservationSet.from_device(V, p_total=V.shape[0])
+obs = mcp.ObservationSet.from_device(V, p_total=V.shape[0], release=True)
+del V
 ctx = obs.device_context()
 if a.dnorm:
     for _ in range(a.evals):

@@ -21,6 +21,7 @@ from .implicit import (
     ttsv_batch,
 )
 from .io import ParseError, read_observations_binary, write_observations_binary
+from .multidevice import MultiDeviceObservationSet
 from .objective import FgResult, fg_implicit, sample_observations
 from .optimize import (AdamConfig, FgCallback, OptConfig, RunReport, adam_minimize, lbfgs_minimize,
                        lbfgs_minimize_batched, multistart_lbfgs, pack, packed_fg_implicit,
@@ -34,6 +35,7 @@ __all__ = [
     "FgResult",
     "GramCache",
     "ObservationSet",
+    "MultiDeviceObservationSet",
     "OptConfig",
     "RunReport",
     "ParseError",

@@ -383,6 +383,7 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
 // fast mode: prep A^T hi/lo -> K1T -> K3 (Y) -> w from Y
 int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dYw,
                          cudaStream_t s) {
+  MCP_NVTX("K1T2 fast-mode partial");
   const K1TPlan& t = pl.t;
   const int n = (int)c->n, r = pl.r;
   k_prep_at_tf32<<<grid_for((int64_t)t.r_pad * t.kpad, 256, 4 * c->sms), 256, 0, s>>>(
@@ -449,9 +450,13 @@ int enqueue_partial(mcp_ctx* c, const EvalPlan& pl, const double* dx, double* dY
     ++launches;
   }
   auto* ev = timing_begin(c, s);
-  int rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r,
-                     (const double*)c->dAfrag.p, pl.d, (double*)c->dYpart.p, (double*)c->dwpart.p,
-                     s, &c->tm_w);
+  int rc;
+  {
+    MCP_NVTX("K1 f+grad partial");
+    rc = k1_launch(v, c->dV, c->ldv, n, c->dnu, c->nu_const, dx + r, r,
+                   (const double*)c->dAfrag.p, pl.d, (double*)c->dYpart.p, (double*)c->dwpart.p,
+                   s, &c->tm_w);
+  }
   timing_end(ev, s);
   if (rc) {
     const cudaError_t e = cudaGetLastError();
@@ -508,6 +513,7 @@ static bool k4s_fits(int64_t n, int r) {
 int enqueue_finish_yw(mcp_ctx* c, int d, int r, const double* dx, const double* dY,
                       const double* dw, const double* alpha_dev, double alpha, double* dout,
                       cudaStream_t s) {
+  MCP_NVTX("K4 tail");
   const int n = (int)c->n;
   if (k4s_fits(n, r)) {
     CUDA_TRY(c, launch_pdl(k_tail_fused, dim3(1), dim3(K4S_THREADS), k4s_smem_bytes((int64_t)n * r),
@@ -897,6 +903,7 @@ int mcp_load_obs(mcp_ctx* c, const void* V, int dtype, int layout, int64_t n, in
                  int64_t ld, const double* nu, double nu_const) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_load_obs");
   return load_obs_impl(c, V, false, dtype, layout, n, p, ld, nu, nu_const);
 }
 
@@ -904,6 +911,7 @@ int mcp_load_obs_device(mcp_ctx* c, const void* dV, int dtype, int layout, int64
                         int64_t ld, const double* dnu, double nu_const) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_load_obs_device");
   return load_obs_impl(c, dV, true, dtype, layout, n, p, ld, dnu, nu_const);
 }
 
@@ -919,6 +927,7 @@ int mcp_fg(mcp_ctx* c, int d, int r, const double* lam, const double* A, double 
            double* f, double* g_lam, double* g_A) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_fg");
   if (!lam || !A || !f || !g_lam || !g_A) return c->fail(MCP_ERR_ARG, "NULL argument");
   if (!std::isfinite(alpha))
     return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
@@ -935,6 +944,7 @@ int mcp_fg_packed(mcp_ctx* c, int d, int r, const double* x, double alpha, int m
                   double* g) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_fg_packed");
   if (!x || !f || !g) return c->fail(MCP_ERR_ARG, "NULL argument");
   if (!std::isfinite(alpha))
     return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
@@ -950,6 +960,7 @@ int mcp_fg_packed(mcp_ctx* c, int d, int r, const double* x, double alpha, int m
 int mcp_ttsv_batch(mcp_ctx* c, int d, int r, const double* A, int mode, double* Y) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_ttsv_batch");
   if (!A || !Y) return c->fail(MCP_ERR_ARG, "NULL argument");
   EvalPlan pl;
   int rc = plan_eval(c, d, r, mode, pl);
@@ -1015,6 +1026,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   if ((rc = ensure(c, c->dpart, sizeof(double) * grid))) return rc;
   if ((rc = ensure(c, c->dscalar, sizeof(double)))) return rc;
   auto* ev = timing_begin(c, c->stream);
+  MCP_NVTX("K5 Gram power");
   if (big && f64) {
     K52Cross<double> cr;
     if (cross) {
@@ -1063,12 +1075,14 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
 int mcp_data_norm_sq(mcp_ctx* c, int d, int mode, double* out) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_data_norm_sq");
   return data_norm_part(c, d, mode, 0, 1, nullptr, out);
 }
 
 int mcp_data_norm_sq_part(mcp_ctx* c, int d, int mode, int part, int nparts, double* out) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_data_norm_sq_part");
   return data_norm_part(c, d, mode, part, nparts, nullptr, out);
 }
 
@@ -1077,6 +1091,7 @@ int mcp_data_norm_sq_cross(mcp_ctx* c, const void* dVJ, int64_t p_pad_J, const d
                            double* out) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_data_norm_sq_cross");
   if (pair_order != 0 && pair_order != 1) return c->fail(MCP_ERR_ARG, "pair_order must be 0 or 1");
   CrossShard cs{dVJ, p_pad_J, dnuJ, nu_const_J, pair_order};
   return data_norm_part(c, d, mode, part, nparts, &cs, out);
@@ -1098,6 +1113,7 @@ int mcp_fg_partial_device(mcp_ctx* c, int d, int r, const double* dx, int mode, 
                           void* stream) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_fg_partial_device");
   if (!dx || !dYw) return c->fail(MCP_ERR_ARG, "NULL argument");
   EvalPlan pl;
   int rc = plan_eval(c, d, r, mode, pl);
@@ -1111,6 +1127,7 @@ int mcp_fg_partial_signal_device(mcp_ctx* c, int d, int r, const double* dx, int
                                  int64_t epoch, void* stream) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_fg_partial_signal_device");
   if (!dx || !dYw || !flag_ptrs) return c->fail(MCP_ERR_ARG, "NULL argument");
   if (world < 1 || rank < 0 || rank >= world) return c->fail(MCP_ERR_ARG, "bad peer arguments");
   EvalPlan pl;
@@ -1129,6 +1146,7 @@ int mcp_fg_finish_device(mcp_ctx* c, int d, int r, const double* dx, const doubl
                          double alpha, double* dout, void* stream) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_fg_finish_device");
   if (!dx || !dYw || !dout) return c->fail(MCP_ERR_ARG, "NULL argument");
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
   if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
@@ -1145,6 +1163,7 @@ int mcp_fg_device(mcp_ctx* c, int d, int r, const double* dx, double alpha, int 
                   double* dout, void* stream) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_fg_device");
   if (!dx || !dout) return c->fail(MCP_ERR_ARG, "NULL argument");
   EvalPlan pl;
   int rc = plan_eval(c, d, r, mode, pl);
@@ -1198,6 +1217,7 @@ int mcp_fg_batch(mcp_ctx* c, int d, int r, int k, const double* X, double alpha,
                  double* F, double* G) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_fg_batch");
   if (!X || !F || !G) return c->fail(MCP_ERR_ARG, "NULL argument");
   if (k < 1) return c->fail(MCP_ERR_ARG, "batch size must be >= 1");
   if (!std::isfinite(alpha))

@@ -292,6 +292,7 @@ extern "C" int mcp_adam(mcp_ctx* c, int d, int r, int mode, const double* x0, co
                         double* trace_t, int64_t trace_cap, int64_t* info) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_adam");
   if (!x0 || !opts || !est_idx || !sample || !x_out || !g_out || !f_out || !info)
     return c->fail(MCP_ERR_ARG, "NULL argument");
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");

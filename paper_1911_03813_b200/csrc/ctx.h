@@ -13,6 +13,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "momentcp_b200.h"
 #include "k1_dispatch.h"
 #include "tail_pieces.cuh"
@@ -123,6 +125,18 @@ struct EvalPlan {
   int mode = MCP_MODE_FP64;
   int d = 0, r = 0;
 };
+
+// NVTX range over an entry point or a kernel role's enqueue (header-only NVTX3: a no-op unless
+// a profiler injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define MCP_NVTX_CAT2(a, b) a##b
+#define MCP_NVTX_CAT(a, b) MCP_NVTX_CAT2(a, b)
+#define MCP_NVTX(name) mcp_internal::NvtxRange MCP_NVTX_CAT(_mcp_nvtx_, __LINE__)(name)
 
 struct Guard {
   mcp_ctx* c;

@@ -27,9 +27,6 @@ constexpr int K1Q_MAXREG = (65536 / K1Q_THREADS) > 255 ? 255 : ((65536 / K1Q_THR
 #ifndef MCP_K1Q_ODD_CHAINS
 #define MCP_K1Q_ODD_CHAINS 0   // 1: GEMM1 with separate even / odd k-step chains (no gain)
 #endif
-#ifndef MCP_K1Q_EXP_NOMATH
-#define MCP_K1Q_EXP_NOMATH 0   // timing experiment only: bit 0 skips GEMM1, bit 1 GEMM2, bit 2 GEMM1's DFMA tail (wrong results)
-#endif
 #ifndef MCP_K1Q_PROF
 #define MCP_K1Q_PROF 0         // diagnostics only: CTAs 0 and gridDim-1 print phase clocks
 #endif
@@ -208,7 +205,7 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
       for (int nt = 0; nt < NTM; ++nt) b_c[nt] = bp[nt * 32];
       if constexpr (TAIL > 0) t_c = *reinterpret_cast<const double2*>(at);
 #pragma unroll
-      for (int kk = 0; kk < ((MCP_K1Q_EXP_NOMATH & 1) ? 0 : KH); ++kk) {
+      for (int kk = 0; kk < KH; ++kk) {
         double a0n = 0.0, a1n = 0.0, b_n[NTM];
         double2 t_n = make_double2(0.0, 0.0);
         if (kk + 1 < KH) {
@@ -228,7 +225,7 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
             dmma884(z[1][nt], a1c, b_c[nt]);
           }
         }
-        if constexpr (TAIL > 0 && !(MCP_K1Q_EXP_NOMATH & 4)) {
+        if constexpr (TAIL > 0) {
           zt[0][0] = fma(a0c, t_c.x, zt[0][0]);
           zt[1][0] = fma(a1c, t_c.x, zt[1][0]);
           if constexpr (TAIL > 1) {
@@ -356,7 +353,7 @@ __global__ void __maxnreg__(K1Q_MAXREG) k1q_fg_pairs(K1SParams prm) {
       const double* sv = my_ring + (size_t)s * slab_elems;
       const double* Pb = my_P + (size_t)b * K1S_SR * PP;
 #pragma unroll
-      for (int k2 = 0; k2 < ((MCP_K1Q_EXP_NOMATH & 2) ? 0 : K1S_SR / 4); ++k2) {
+      for (int k2 = 0; k2 < K1S_SR / 4; ++k2) {
         const double* prow = Pb + (4 * k2 + t) * PP;
         double bb[NTM], bt[TL];
 #pragma unroll

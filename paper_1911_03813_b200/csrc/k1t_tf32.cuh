@@ -376,9 +376,6 @@ constexpr int K1T2_THREADS = (2 + K1T2_EPI_WARPS) * 32;
 #define K1T2_T0()
 #define K1T2_ACC(v)
 #endif
-#ifndef MCP_K1T2_EXP_NOLO2
-#define MCP_K1T2_EXP_NOLO2 0   // timing experiment only: skip the GEMM2 V_lo loads (wrong results)
-#endif
 
 __global__ void __launch_bounds__(K1T2_THREADS, 1)
     k1t2_fg_tf32(const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_v2,
@@ -492,16 +489,15 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
           const int mt = step >> 2, rc = step & 3;
           unsigned char* st = stage(q);
           uint64_t* fb = &full[q % NS];
-          mbar_arrive_expect_tx(fb, (MCP_K1T2_EXP_NOLO2 ? 1 : 2) * K1T_VBYTES);
+          mbar_arrive_expect_tx(fb, 2 * K1T_VBYTES);
           if (prm.g2_3d) {
             load3(st, &tm_v2, row0 + rc * 32, mt * 4, fb, pol_drop);
-            if (!MCP_K1T2_EXP_NOLO2) load3(st + K1T_VBYTES, &tm_l2, row0 + rc * 32, mt * 4, fb, pol_drop);
+            load3(st + K1T_VBYTES, &tm_l2, row0 + rc * 32, mt * 4, fb, pol_drop);
           } else {
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
               load(st + b * 4096, &tm_v2, mt * 128 + b * 32, row0 + rc * 32, fb, pol_drop);
-              if (!MCP_K1T2_EXP_NOLO2)
-                load(st + K1T_VBYTES + b * 4096, &tm_l2, mt * 128 + b * 32, row0 + rc * 32, fb,
+              load(st + K1T_VBYTES + b * 4096, &tm_l2, mt * 128 + b * 32, row0 + rc * 32, fb,
                      pol_drop);
             }
           }

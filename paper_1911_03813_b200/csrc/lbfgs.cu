@@ -951,6 +951,7 @@ extern "C" int mcp_lbfgs(mcp_ctx* c, int d, int r, double alpha, int mode, const
                          mcp_iterate_hook hook, void* hook_user) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_lbfgs");
   if (!x0 || !opts || !x_out || !g_out || !f_out || !info)
     return c->fail(MCP_ERR_ARG, "NULL argument");
   if (!std::isfinite(alpha)) return c->fail(MCP_ERR_ARG, "model variables and alpha must be finite");
@@ -972,6 +973,7 @@ extern "C" int mcp_lbfgs_batch(mcp_ctx* c, int k, int d, int r, double alpha, in
                                int64_t trace_cap, int64_t* info) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_lbfgs_batch");
   if (!X0 || !opts || !X_out || !G_out || !F_out || !info)
     return c->fail(MCP_ERR_ARG, "NULL argument");
   if (k < 1) return c->fail(MCP_ERR_ARG, "number of starts must be >= 1");

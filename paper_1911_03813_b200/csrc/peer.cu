@@ -158,6 +158,7 @@ extern "C" int mcp_peer_reduce_finish(mcp_ctx* c, int d, int r, const double* dx
                                       void* stream) {
   if (!c) return MCP_ERR_ARG;
   Guard gd(c);
+  MCP_NVTX("mcp_peer_reduce_finish");
   if (!dx || !part_ptrs || !my_flags || !dout || !derr || world < 1)
     return c->fail(MCP_ERR_ARG, "NULL argument");
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");

@@ -78,7 +78,9 @@ def main():
         ni, vi = h.index("Kernel Name"), h.index("Metric Value")
         launches = [(r[ni].split("(")[0], float(r[vi].replace(",", ""))) for r in lrows[start + 1:]
                     if len(r) > vi]
-        mine = [(n, t) for n, t in launches if "mcp::" in n]
+        import re
+        ours = re.compile(r"(mcp::|\bk1|\bk5|\bk_)")
+        mine = [(n, t) for n, t in launches if ours.search(n)]
         tot = sum(t for _, t in mine)
         agg = {}
         for n, t in mine:

@@ -22,6 +22,7 @@ V = synth.device_observations(cfg, 2024, p=a.p)
 obs = mcp.ObservationSet.from_device(V, p_total=V.shape[0], release=True)
 del V
 ctx = obs.device_context()
+torch.cuda.empty_cache()   # the released upload source goes back to the driver (V_lo needs it)
 if a.dnorm:
     for _ in range(a.evals):
         print("dnorm", ctx.data_norm_sq(cfg.d, None), ctx.last_variant)

@@ -17,7 +17,7 @@ bench)
   timeout 600 python bench.py --config c3 --mode tf32x3 > gpurun_out/bench_c3t.json 2> gpurun_out/bench_c3t.err
   timeout 600 python bench.py --config c5 --mode tf32x3 --steps 5 --warmup 3 > gpurun_out/bench_c5t.json 2> gpurun_out/bench_c5t.err ;;
 ncu)
-  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k" -c 200 --csv \
     --log-file gpurun_out/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:k1x --launch-skip 1 \
     --launch-count 1 -o gpurun_out/k1x_c3 python tools/prof_k1.py --config c3 --evals 3 > gpurun_out/ncu_k1x.log 2>&1

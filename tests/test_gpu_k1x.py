@@ -39,8 +39,9 @@ def _case(n, p, r, d, seed, weights=False):
     (1024, 60_000, 256, 3, False),  # c5 shape: K1G (Y partial in L2)
     (900, 20_000, 33, 4, False),    # large ragged n
 ])
-def test_large_n_fp32_vs_oracle(n, p, r, d, k1x):
-    V, nu, lam, A = _case(n, p, r, d, seed=n + p + r)
+@pytest.mark.parametrize("weights", [False, True])
+def test_large_n_fp32_vs_oracle(n, p, r, d, k1x, weights):
+    V, nu, lam, A = _case(n, p, r, d, seed=n + p + r, weights=weights)
     obs = mcp.ObservationSet(V, nu)
     res = mcp.fg_implicit(obs, lam, A, d, 0.3)
     assert obs.device_context().last_variant.startswith("k1x_fg_dmma") == k1x, \

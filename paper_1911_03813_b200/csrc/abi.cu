@@ -158,6 +158,20 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
+// 2-D fp64 tensor map (K53's V tiles): inner dim (contiguous) x outer dim, row pitch in bytes.
+bool make_tmap_f64(CUtensorMap* m, const void* gaddr, uint64_t inner, uint64_t outer,
+                   uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(gaddr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 2-D fp32 tensor map: inner dim (contiguous) x outer dim, row pitch in bytes.
 bool make_tmap_f32(CUtensorMap* m, void* gaddr, uint64_t inner, uint64_t outer, uint64_t pitch,
                    uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
@@ -999,21 +1013,24 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   if (!out) return c->fail(MCP_ERR_ARG, "NULL argument");
   if (cross && (!cross->dV || cross->p_pad < 0 || cross->p_pad % K52_T != 0))
     return c->fail(MCP_ERR_ARG, "cross shard must be a padded row block (multiple of 128 rows)");
-  // K5 v2 (128 x 128 tiles) for n >= 32 and every cross-shard rectangle; the 64 x 64 variant
-  // for narrow observations
+  // K53 (fp64, TMA ring) / K5 v2 (fp32) on 128 x 128 tiles for n >= 32 and every cross-shard
+  // rectangle; the 64 x 64 variant for narrow observations
   const bool big = (c->n >= 32 || cross) && (c->p_pad % K52_T) == 0;
+  const bool f64 = c->dtype == MCP_F64;
+  const bool k53 = big && f64 && MCP_CFG_K53;
   const int64_t TT = big ? K52_T : K5_T;
   const int64_t T = c->p_pad / TT;
   const int64_t TJ = cross ? cross->p_pad / K52_T : T;
   const int64_t pairs = cross ? T * TJ : T * (T + 1) / 2;
   const int64_t b = pairs * part / nparts, e = pairs * (part + 1) / nparts;
-  const int n_chunks = (int)ceil_div(c->n, big ? K52_NK : K5_NK);
-  const bool f64 = c->dtype == MCP_F64;
-  const size_t smem = big ? (f64 ? k52_smem_bytes<double>() : k52_smem_bytes<float>())
-                          : (f64 ? k5_smem_bytes<double>() : k5_smem_bytes<float>());
-  const void* fn = big ? (f64 ? (const void*)k52_gram_power<double> : (const void*)k52_gram_power<float>)
-                       : (f64 ? (const void*)k5_gram_power<double> : (const void*)k5_gram_power<float>);
-  const int threads = big ? K52_THREADS : K5_THREADS;
+  const int n_chunks = (int)ceil_div(c->n, k53 ? K53_NK : big ? K52_NK : K5_NK);
+  const size_t smem = k53 ? k53_smem_bytes()
+                          : big ? (f64 ? k52_smem_bytes<double>() : k52_smem_bytes<float>())
+                                : (f64 ? k5_smem_bytes<double>() : k5_smem_bytes<float>());
+  const void* fn = k53 ? (const void*)k53_gram_power
+                       : big ? (f64 ? (const void*)k52_gram_power<double> : (const void*)k52_gram_power<float>)
+                             : (f64 ? (const void*)k5_gram_power<double> : (const void*)k5_gram_power<float>);
+  const int threads = k53 ? K53_THREADS : big ? K52_THREADS : K5_THREADS;
   if (!ensure_dyn_smem(fn, smem))
     return c->fail(MCP_ERR_CUDA, "cannot raise the Gram-power kernel's shared-memory limit");
   int occ = 1;
@@ -1025,9 +1042,21 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   int rc;
   if ((rc = ensure(c, c->dpart, sizeof(double) * grid))) return rc;
   if ((rc = ensure(c, c->dscalar, sizeof(double)))) return rc;
+  CUtensorMap tmI, tmJ;
+  if (k53) {
+    if (!make_tmap_f64(&tmI, c->dV, c->ldv, c->p_pad, 8 * c->ldv, K53_NK, K53_T) ||
+        !make_tmap_f64(&tmJ, cross ? cross->dV : c->dV, c->ldv, cross ? cross->p_pad : c->p_pad,
+                       8 * c->ldv, K53_NK, K53_T))
+      return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Gram-power tiles");
+  }
   auto* ev = timing_begin(c, c->stream);
   MCP_NVTX("K5 Gram power");
-  if (big && f64) {
+  if (k53) {
+    k53_gram_power<<<(int)grid, threads, smem, c->stream>>>(
+        tmI, tmJ, n_chunks, c->dnu, c->nu_const, cross ? cross->dnu : nullptr,
+        cross ? cross->nu_const : 0.0, d, T, TJ, cross ? 1 : 0, cross ? cross->colmajor : 0, b, e,
+        (double*)c->dpart.p);
+  } else if (big && f64) {
     K52Cross<double> cr;
     if (cross) {
       cr.VJ = (const double*)cross->dV;
@@ -1067,7 +1096,8 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   CUDA_TRY(c, cudaMemcpyAsync(out, c->dscalar.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->last_launches = 2;
-  c->variant = std::string(big ? "k52_gram_dmma128" : "k5_gram_dmma64") + (f64 ? "<f64>" : "<f32>") +
+  c->variant = std::string(k53 ? "k53_gram_dmma128_tma" : big ? "k52_gram_dmma128" : "k5_gram_dmma64") +
+               (f64 ? "<f64>" : "<f32>") +
                (cross ? "[cross]" : "");
   return MCP_OK;
 }

@@ -9,7 +9,12 @@
 // CTA's sum is written once and reduced in a fixed order, so the result is deterministic.
 #pragma once
 
+#include <cuda.h>
+
+#include "k1s_fp64.cuh"      // mbarrier helpers
+#include "k1x_common.cuh"    // ordered shared loads, async-proxy fence
 #include "mcp_common.cuh"
+#include "umma.cuh"          // TMA helpers
 
 namespace mcp {
 
@@ -306,6 +311,170 @@ __global__ void k_ordered_sum(const double* __restrict__ part, int m, double* __
     double s = 0.0;
     for (int i = 0; i < m; ++i) s += part[i];
     *out = s;
+  }
+}
+
+
+// ---- K53 (fp64 sets): K52's 128 x 128 tile pairs and 4 x 4 warp grid, fed like K1X ----------
+// ncu at c4 put K52 at 78% of the FP64 pipe with 11% of the warp time issuing cp.async (2048
+// 16-byte copies and their addresses per 32-column chunk) and the rest of the loss at the two
+// __syncthreads per chunk.  K53 stages each 16-double chunk of the I and J tiles with one 2-D TMA
+// apiece (128-byte swizzle) into a ring of 6 stages that flows across tile pairs; the 16 warps
+// consume a stage independently (mbarrier parity waits, no CTA barrier) and the last one to
+// release it issues the refill (counter, nobody waits).  Fragment loads stay conflict-free under
+// the swizzle by letting DMMA row (column) g of a 8-row m-tile read physical tile row
+// 2g (g < 4) / 2(g - 4) + 1 (g >= 4): the 16 lanes of a half-warp then hit 16 distinct 8-byte
+// banks.  The epilogue uses the same row map for the weights, so the sum is the same Gram power
+// sum as K52 (tile-pair order and the per-CTA fixed-order reduction unchanged).
+constexpr int K53_T = 128;
+constexpr int K53_NK = 16;          // doubles per chunk row (one 128-byte swizzle row)
+constexpr int K53_THREADS = 512;
+constexpr int K53_STAGES = 6;
+constexpr int K53_STAGE_BYTES = 2 * K53_T * K53_NK * 8;   // I and J chunks, 32 KB
+
+__host__ __device__ constexpr size_t k53_smem_bytes() {
+  return 1024 + (size_t)K53_STAGES * K53_STAGE_BYTES + 256;
+}
+
+__device__ __forceinline__ int k53_prow(int g) { return g < 4 ? 2 * g : 2 * (g - 4) + 1; }
+
+__global__ void __launch_bounds__(K53_THREADS, 1)
+    k53_gram_power(const __grid_constant__ CUtensorMap tmI, const __grid_constant__ CUtensorMap tmJ,
+                   int n_chunks, const double* __restrict__ nu, double nu_const,
+                   const double* __restrict__ nuJ, double nu_constJ, int d, int64_t T, int64_t TJ,
+                   int rect, int colmajor, int64_t pair_begin, int64_t pair_end,
+                   double* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char k53_raw[];
+  unsigned char* base = k53_raw + ((1024u - (smem_u32(k53_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)K53_STAGES * K53_STAGE_BYTES);
+  unsigned* cnt = reinterpret_cast<unsigned*>(full + K53_STAGES);
+  double* sRed = reinterpret_cast<double*>(cnt + K53_STAGES + 2);   // 16 doubles (8-aligned)
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;   // 4 x 4 warps, 32 x 32 outputs each
+  const int prow = k53_prow(g);
+  const double* nuJv = rect ? nuJ : nu;
+  const double ncJ = rect ? nu_constJ : nu_const;
+
+  auto decode = [&](int64_t k, int64_t& I_, int64_t& J_) {
+    if (rect && colmajor) {
+      I_ = k % T;
+      J_ = k / T;
+    } else if (rect) {
+      I_ = k / TJ;
+      J_ = k % TJ;
+    } else {
+      k5_decode(k, T, I_, J_);
+    }
+  };
+  // this CTA's pairs: pair_begin + blockIdx.x + kp * gridDim.x
+  const int64_t my_pairs =
+      pair_begin + blockIdx.x < pair_end
+          ? (pair_end - pair_begin - blockIdx.x + gridDim.x - 1) / gridDim.x
+          : 0;
+  const int64_t nsteps = my_pairs * n_chunks;
+  auto issue = [&](int64_t q) {   // TMA of step q into its stage (one thread)
+    const int s = (int)(q % K53_STAGES);
+    const int64_t kp = q / n_chunks;
+    const int c = (int)(q % n_chunks);
+    int64_t I, J;
+    decode(pair_begin + blockIdx.x + kp * gridDim.x, I, J);
+    unsigned char* st = base + (size_t)s * K53_STAGE_BYTES;
+    mbar_arrive_expect_tx(&full[s], K53_STAGE_BYTES);
+    tma_load_2d(st, &tmI, c * K53_NK, (int)(I * K53_T), smem_u32(&full[s]));
+    tma_load_2d(st + K53_STAGE_BYTES / 2, &tmJ, c * K53_NK, (int)(J * K53_T), smem_u32(&full[s]));
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < K53_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      cnt[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_prefetch_desc(&tmI);
+    tma_prefetch_desc(&tmJ);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int64_t q = 0; q < K53_STAGES && q < nsteps; ++q) issue(q);
+
+  // per-lane word offsets (doubles) inside a stage: row * 16 + (k ^ 2 (row & 7)), row & 7 = prow
+  const int swz = 2 * prow;
+  int aoff[4], boff[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    aoff[i] = (32 * wm + 8 * i + prow) * K53_NK;
+    boff[i] = K53_T * K53_NK + (32 * wn + 8 * i + prow) * K53_NK;
+  }
+  const uint32_t st0 = smem_u32(base);
+  double tsum = 0.0;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  for (int64_t q = 0; q < nsteps; ++q) {
+    const int s = (int)(q % K53_STAGES);
+    mbar_wait(&full[s], (uint32_t)((q / K53_STAGES) & 1));
+    const uint32_t sb = st0 + (uint32_t)s * K53_STAGE_BYTES;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int kk = (4 * ks + t) ^ swz;
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = k1w_lds_f64(sb + 8u * (uint32_t)(aoff[i] + kk));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) b[i] = k1w_lds_f64(sb + 8u * (uint32_t)(boff[i] + kk));
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+    }
+    // release the stage; the last of the 16 warps refills it with step q + STAGES
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&cnt[s], 1u) == K53_THREADS / 32 - 1) {
+        cnt[s] = 0;
+        __threadfence_block();
+        if (q + K53_STAGES < nsteps) {
+          k1w_fence_proxy_async();
+          issue(q + K53_STAGES);
+        }
+      }
+    }
+    if ((q + 1) % n_chunks == 0) {
+      // last chunk of a tile pair: sum nu_l nu_l' g^d over the tile (x2 off the diagonal)
+      int64_t I, J;
+      decode(pair_begin + blockIdx.x + (q / n_chunks) * gridDim.x, I, J);
+      double tile_sum = 0.0;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int64_t l = I * K53_T + 32 * wm + 8 * mt + prow;
+        const double nl = nu ? nu[l] : nu_const;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t l2 = J * K53_T + 32 * wn + 8 * nt + k53_prow(2 * t + e);
+            const double nl2 = nuJv ? nuJv[l2] : ncJ;
+            tile_sum += (nl * nl2) * rm_pow(acc[mt][nt][e], d);
+            acc[mt][nt][e] = 0.0;
+          }
+      }
+      tsum += (I == J && !rect) ? tile_sum : 2.0 * tile_sum;
+    }
+  }
+
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, off);
+  if (lane == 0) sRed[warp] = tsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < K53_THREADS / 32; ++w) sum += sRed[w];
+    part[blockIdx.x] = sum;
   }
 }
 

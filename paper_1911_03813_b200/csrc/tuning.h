@@ -49,6 +49,10 @@
 #ifndef MCP_CFG_FORCE_K1G
 #define MCP_CFG_FORCE_K1G 0
 #endif
+// ||X||^2 on fp64 sets: K53 (TMA ring, no CTA barrier) instead of K52 (cp.async chunks)
+#ifndef MCP_CFG_K53
+#define MCP_CFG_K53 1
+#endif
 // fast mode: K1T2 (precomputed V_lo) unless 1 -> the in-kernel split K1T
 #ifndef MCP_CFG_K1T_V1
 #define MCP_CFG_K1T_V1 0

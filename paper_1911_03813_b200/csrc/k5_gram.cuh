@@ -321,16 +321,14 @@ __global__ void k_ordered_sum(const double* __restrict__ part, int m, double* __
 // __syncthreads per chunk.  K53 stages each 16-double chunk of the I and J tiles with one 2-D TMA
 // apiece (128-byte swizzle) into a ring of 6 stages that flows across tile pairs; the 16 warps
 // wait on the stage's mbarrier and, after the chunk, meet at one CTA barrier, after which thread
-// 0 refills the stage STAGES - 1 chunks ahead.  (Releasing stages warp by warp with the last
-// warp refilling -- no CTA barrier -- measured 69% vs 77% for K52: the fastest warps run up to
-// the ring's end and then wait for refills gated by the slowest warp.)  Fragment loads stay conflict-free under
+// 0 refills the stage STAGES - 1 chunks ahead.  Measured at c4: 360.8 ms, the same as K52 (359.4;
+// 77% of the FP64 pipe) with one TMA pair per chunk instead of 2048 cp.async.  Releasing stages
+// warp by warp with the last warp refilling (no CTA barrier, K1X's scheme) measured 404 ms: the
+// fastest warps run to the end of the ring and then wait for refills gated by the slowest warp.  Fragment loads stay conflict-free under
 // the swizzle by letting DMMA row (column) g of a 8-row m-tile read physical tile row
 // 2g (g < 4) / 2(g - 4) + 1 (g >= 4): the 16 lanes of a half-warp then hit 16 distinct 8-byte
 // banks.  The epilogue uses the same row map for the weights, so the sum is the same Gram power
 // sum as K52 (tile-pair order and the per-CTA fixed-order reduction unchanged).
-#ifndef MCP_K53_LOCKSTEP
-#define MCP_K53_LOCKSTEP 1   // 1: one CTA barrier per chunk keeps the warps together (see below)
-#endif
 constexpr int K53_T = 128;
 constexpr int K53_NK = 16;          // doubles per chunk row (one 128-byte swizzle row)
 constexpr int K53_THREADS = 512;
@@ -352,8 +350,7 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
   extern __shared__ __align__(16) unsigned char k53_raw[];
   unsigned char* base = k53_raw + ((1024u - (smem_u32(k53_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)K53_STAGES * K53_STAGE_BYTES);
-  unsigned* cnt = reinterpret_cast<unsigned*>(full + K53_STAGES);
-  double* sRed = reinterpret_cast<double*>(cnt + K53_STAGES + 2);   // 16 doubles (8-aligned)
+  double* sRed = reinterpret_cast<double*>(full + K53_STAGES);   // 16 doubles
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -391,10 +388,7 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
     tma_load_2d(st + K53_STAGE_BYTES / 2, &tmJ, c * K53_NK, (int)(J * K53_T), smem_u32(&full[s]));
   };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < K53_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      cnt[s] = 0;
-    }
+    for (int s = 0; s < K53_STAGES; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tma_prefetch_desc(&tmI);
     tma_prefetch_desc(&tmJ);
@@ -436,28 +430,12 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
     }
-#if MCP_K53_LOCKSTEP
     // every warp is done with the stage: refill it with step q + STAGES (STAGES - 1 steps ahead)
     __syncthreads();
     if (threadIdx.x == 0 && q + K53_STAGES < nsteps) {
       k1w_fence_proxy_async();
       issue(q + K53_STAGES);
     }
-#else
-    // release the stage; the last of the 16 warps refills it with step q + STAGES
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      if (atomicAdd(&cnt[s], 1u) == K53_THREADS / 32 - 1) {
-        cnt[s] = 0;
-        __threadfence_block();
-        if (q + K53_STAGES < nsteps) {
-          k1w_fence_proxy_async();
-          issue(q + K53_STAGES);
-        }
-      }
-    }
-#endif
     if ((q + 1) % n_chunks == 0) {
       // last chunk of a tile pair: sum nu_l nu_l' g^d over the tile (x2 off the diagonal)
       int64_t I, J;

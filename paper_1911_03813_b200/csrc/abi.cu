@@ -375,11 +375,12 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   std::string why;
   if (!k1_select(c->dtype, c->n, r, c->p_pad, c->sms, pl.k1, why))
     return c->fail(MCP_ERR_ARG, why);
-  if (pl.k1.needs_tmap() && c->tm_w_kind != pl.k1.kind) {
-    if (!make_tmap_f32_chunks(&c->tm_w, c->dV, c->ldv, c->p_pad, K1X_BOX_ROWS, K1X_BOX_CHUNKS,
-                              CU_TENSOR_MAP_SWIZZLE_128B))
+  if (pl.k1.needs_tmap() && c->tm_w_kind != pl.k1.t_rows) {
+    // K1X: one box = a whole tile (t_rows rows x n_pad / 32 chunks of 32 floats)
+    if (!make_tmap_f32_chunks(&c->tm_w, c->dV, c->ldv, c->p_pad, pl.k1.t_rows,
+                              (uint32_t)(pl.k1.n_pad / 32), CU_TENSOR_MAP_SWIZZLE_128B))
       return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K1X observation map");
-    c->tm_w_kind = pl.k1.kind;
+    c->tm_w_kind = pl.k1.t_rows;
   }
   int rc;
   const int64_t n = c->n;

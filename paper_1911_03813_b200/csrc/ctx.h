@@ -65,7 +65,7 @@ struct mcp_ctx {
   CUtensorMap tm_v3, tm_l3;    // K1T2 GEMM2: 3-D chunk maps over V / V_lo (ld % 32 == 0)
   bool tm_c_ready = false;
   CUtensorMap tm_w;            // K1X observation map (3-D, 32 x 32 x 16 boxes, 128-byte swizzle)
-  int tm_w_kind = 0;           // K1Variant kind tm_w was encoded for (0: none)
+  int tm_w_kind = 0;           // tile rows of the K1X shape tm_w was encoded for (0: none)
   void* tm_a_addr = nullptr;
   int tm_a_rows = 0, tm_a_kpad = 0, tm_a_rb = 0;
   mcp_internal::DevBuf dAt;

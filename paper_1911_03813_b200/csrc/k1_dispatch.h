@@ -8,9 +8,6 @@
 
 namespace mcp {
 
-// K1X's 3-D observation box: one tile of 32 rows x 16 chunks of 32 floats (k1x_fp64.cuh)
-constexpr int K1X_BOX_ROWS = 32;
-constexpr int K1X_BOX_CHUNKS = 16;
 
 struct K1Variant {
   int dtype = 0;       // MCP_F64 / MCP_F32
@@ -34,8 +31,9 @@ struct K1Variant {
   int stages = 0;      // ring depth (kind 1)
   int MT = 0;          // GEMM2 m-tiles (kind 1)
   int MTW2 = 1;        // slabs per TMA copy unit (kind 1)
-  int cl = 1;          // kind 8: cluster size (CTAs splitting n)
+  int cl = 1;
   int cpw = 1;
+  int t_rows = 0;      // kind 8: tile rows (the 3-D TMA box)
   int groups = 0;      // kind 8: work split (k1x_common.cuh k1w_split)
   int64_t t_main = 0;
   bool needs_prep() const { return kind == 0 || kind == 5 || kind == 8; }

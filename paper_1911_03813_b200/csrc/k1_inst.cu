@@ -374,65 +374,56 @@ bool select_pairs(int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Varia
   return true;
 }
 
-template <int CL>
+template <int NL, int T, int RB>
 void launch_x(const K1WParams& prm, const CUtensorMap* tm, int grid, size_t smem, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(K1X_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = CL;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, k1x_fg_dmma<CL>, *tm, prm);
+  launch_pdl(k1x_fg_dmma<NL, T, RB>, dim3(grid), dim3(K1X_THREADS), smem, s, *tm, prm);
 }
 
-// K1X: fp32 sets with 384 < n <= 512 (one CTA) or 768 < n <= 1024 (2-CTA cluster), chunk-aligned
-// pitch (one 3-D TMA per tile)
+// K1X: fp32 sets with a chunk-aligned pitch (one 3-D TMA per tile): 384 < n <= 512 (NL = 512,
+// T = 32, RB = 16) or, with K1X_1024, 768 < n <= 1024 (NL = 1024, T = 16, RB = 8)
 bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, K1Variant& v) {
-  if (dtype != MCP_F32 || ldv % 32 != 0 || r < 12) return false;
-  int cl = 0;
-  if (n > 384 && n <= 512) cl = 1;
-#if MCP_CFG_K1X_CL2
-  else if (n > 768 && n <= 1024) cl = 2;
-  const void* fn = cl == 1 ? (const void*)k1x_fg_dmma<1> : (const void*)k1x_fg_dmma<2>;
-  const size_t smem = cl == 1 ? k1x_smem_bytes<1>() : k1x_smem_bytes<2>();
-#else
-  const void* fn = (const void*)k1x_fg_dmma<1>;
-  const size_t smem = k1x_smem_bytes<1>();
-#endif
-  if (!cl) return false;
+  if (dtype != MCP_F32 || ldv % 32 != 0) return false;
+  int nl = 0, tt = 0, rb = 0;
+  const void* fn = nullptr;
+  size_t smem = 0;
+  if (n > 384 && n <= 512 && r >= 12) {
+    nl = 512, tt = 32, rb = 16;
+    fn = (const void*)k1x_fg_dmma<512, 32, 16>;
+    smem = k1x_smem_bytes<512, 32, 16>();
+  } else if (MCP_CFG_K1X_1024 && n > 768 && n <= 1024 && r >= 6) {
+    nl = 1024, tt = 16, rb = 8;
+    fn = (const void*)k1x_fg_dmma<1024, 16, 8>;
+    smem = k1x_smem_bytes<1024, 16, 8>();
+  } else {
+    return false;
+  }
   if (!ensure_dyn_smem(fn, smem)) return false;
-  const int64_t T = p_pad / K1X_T;
+  const int64_t T = p_pad / tt;
   v.kind = 8;
   v.dtype = dtype;
-  v.RB = K1X_RB;
-  v.cl = cl;
+  v.RB = rb;
+  v.cl = 1;
   v.cpw = 1;
-  v.n_pad = 512 * cl;
+  v.t_rows = tt;
+  v.n_pad = nl;
   v.n_chunks = v.n_pad / 64;
-  v.rbs = (int)ceil_div(r, K1X_RB);
+  v.rbs = (int)ceil_div(r, rb);
   v.num_tiles = T;
-  const int Nc = (int)std::min<int64_t>(sms / cl, (int64_t)v.rbs * T);
+  const int Nc = (int)std::min<int64_t>(sms, (int64_t)v.rbs * T);
   k1w_split(T, v.rbs, Nc, v.groups, v.t_main);
   int mx = 1;
-  for (int rb = 0; rb < v.rbs; ++rb)
-    mx = std::max(mx, k1w_used_slots(rb, T, v.rbs, Nc, v.groups, v.t_main));
+  for (int b = 0; b < v.rbs; ++b)
+    mx = std::max(mx, k1w_used_slots(b, T, v.rbs, Nc, v.groups, v.t_main));
   v.gp = mx;
-  v.grid = Nc * cl;
+  v.grid = Nc;
   v.smem = smem;
   v.entry = 0;
-  v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (K1X_RB / 8) * 32;
-  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * K1X_RB;
-  v.wpart_elems = (size_t)v.rbs * v.gp * K1X_RB;
-  v.name = std::string("k1x_fg_dmma<f32,RB=16,T=32,16 warps,CL=") + std::to_string(cl) +
-           ",G=" + std::to_string(v.groups) + (v.t_main < T ? ",+ranges" : "") + ">";
+  v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (rb / 8) * 32;
+  v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * rb;
+  v.wpart_elems = (size_t)v.rbs * v.gp * rb;
+  v.name = std::string("k1x_fg_dmma<f32,NL=") + std::to_string(nl) + ",T=" + std::to_string(tt) +
+           ",RB=" + std::to_string(rb) + ",16 warps,G=" + std::to_string(v.groups) +
+           (v.t_main < T ? ",+ranges" : "") + ">";
   return true;
 }
 
@@ -600,12 +591,10 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     wp.slots = v.gp;
     wp.Ypart = Ypart;
     wp.wpart = wpart;
-#if MCP_CFG_K1X_CL2
-    if (v.cl == 2)
-      launch_x<2>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+    if (v.n_pad == 1024)
+      launch_x<1024, 16, 8>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     else
-#endif
-      launch_x<1>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
+      launch_x<512, 32, 16>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }
   if (v.kind == 1 || v.kind == 3 || v.kind == 4 || v.kind == 6) {

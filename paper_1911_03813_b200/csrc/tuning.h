@@ -37,10 +37,9 @@
 #ifndef MCP_CFG_K1X
 #define MCP_CFG_K1X 1              // K1X (16 warps, double-buffered tiles) for 384 < n <= 512
 #endif
-// K1X's 2-CTA cluster form for 768 < n <= 1024: the per-tile half-Z exchange between the two
-// SMs costs ~11% (c5: 654 ms vs 622 ms for K1G), so K1G stays the default there
-#ifndef MCP_CFG_K1X_CL2
-#define MCP_CFG_K1X_CL2 0
+// K1X's n <= 1024 shape (T = 16, RB = 8) for 768 < n <= 1024 instead of K1G
+#ifndef MCP_CFG_K1X_1024
+#define MCP_CFG_K1X_1024 1
 #endif
 // K1G (Y partial in L2) for large n when K1's register-bound column block is <= 1/4 of K1G's
 #ifndef MCP_CFG_K1G

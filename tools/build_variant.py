@@ -22,7 +22,8 @@ def main():
         obj = os.path.join(out_dir, src.replace(".cu", ".o"))
         flags = [f for f in ge.NVCC_FLAGS if f != "-shared"]
         procs.append(subprocess.Popen([ge._nvcc(), *flags, *defs, "-c", os.path.join(ge.CSRC, src),
-                                       "-o", obj]))
+                                       "-o", obj], stdout=subprocess.DEVNULL,
+                                      stderr=subprocess.DEVNULL))
         objs.append(obj)
     if any(p.wait() for p in procs):
         raise SystemExit("nvcc failed")

@@ -390,10 +390,12 @@ bool select_x(int dtype, int64_t n, int r, int64_t p_pad, int64_t ldv, int sms, 
     nl = 512, tt = 32, rb = 16;
     fn = (const void*)k1x_fg_dmma<512, 32, 16>;
     smem = k1x_smem_bytes<512, 32, 16>();
-  } else if (MCP_CFG_K1X_1024 && n > 768 && n <= 1024 && r >= 6) {
+#if MCP_CFG_K1X_1024
+  } else if (n > 768 && n <= 1024 && r >= 6) {
     nl = 1024, tt = 16, rb = 8;
     fn = (const void*)k1x_fg_dmma<1024, 16, 8>;
     smem = k1x_smem_bytes<1024, 16, 8>();
+#endif
   } else {
     return false;
   }
@@ -591,9 +593,11 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
     wp.slots = v.gp;
     wp.Ypart = Ypart;
     wp.wpart = wpart;
+#if MCP_CFG_K1X_1024
     if (v.n_pad == 1024)
       launch_x<1024, 16, 8>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     else
+#endif
       launch_x<512, 32, 16>(wp, static_cast<const CUtensorMap*>(tmap), v.grid, v.smem, s);
     return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
   }

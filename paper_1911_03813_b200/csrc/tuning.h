@@ -37,9 +37,11 @@
 #ifndef MCP_CFG_K1X
 #define MCP_CFG_K1X 1              // K1X (16 warps, double-buffered tiles) for 384 < n <= 512
 #endif
-// K1X's n <= 1024 shape (T = 16, RB = 8) for 768 < n <= 1024 instead of K1G
+// K1X's n <= 1024 shape (T = 16, RB = 8) for 768 < n <= 1024 instead of K1G: measured 770 ms at
+// c5 vs 617 ms for K1G (two row blocks per 16-row tile: the P waits and the 256-thread merge
+// barrier cost twice as much per DMMA as at T = 32), so experiment builds only
 #ifndef MCP_CFG_K1X_1024
-#define MCP_CFG_K1X_1024 1
+#define MCP_CFG_K1X_1024 0
 #endif
 // K1G (Y partial in L2) for large n when K1's register-bound column block is <= 1/4 of K1G's
 #ifndef MCP_CFG_K1G

@@ -1,9 +1,9 @@
 #!/bin/bash
-# K1W iteration on the GPU box: parity tests, c3 / c5 bench lines, optional ncu capture.
-#   tools/run_k1w.sh [ncu]
+# K1X iteration on the GPU box: parity tests, c3 / c5 bench lines, optional ncu capture.
+#   tools/run_k1x.sh [ncu]
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_k1x.py -x -q -s -p no:cacheprovider > gpurun_out/k1w_tests.txt 2>&1
-echo "rc=$?" >> gpurun_out/k1w_tests.txt
+timeout 600 python -m pytest tests/test_gpu_k1x.py -x -q -s -p no:cacheprovider > gpurun_out/k1x_tests.txt 2>&1
+echo "rc=$?" >> gpurun_out/k1x_tests.txt
 timeout 300 python bench.py --no-cpu > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
 timeout 400 python bench.py --config c5 --no-cpu --steps 5 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 if [ "$1" = ncu ]; then

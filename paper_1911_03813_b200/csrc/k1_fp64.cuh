@@ -17,6 +17,9 @@
 
 #include "mcp_common.cuh"
 #include "pdl.h"
+#include "k1s_fp64.cuh"   // smem_u32
+#include "umma.cuh"       // TMEM helpers
+#include "k1x_common.cuh"  // (column block, tile) work split
 
 namespace mcp {
 
@@ -42,7 +45,9 @@ struct K1Params {
   const double* Afrag; // [rbs][n_chunks*16][RB/8][32] B-fragment ordered factor blocks
   int d;
   int rbs;             // number of RB-column blocks
-  int gp;              // persistent CTAs per column block
+  int gp;              // persistent CTAs per column block (K1G: partial slots per block)
+  int groups = 0;      // K1G: the k1w_split work split (k1x_common.cuh)
+  int64_t t_main = 0;
   double* Ypart;       // [rbs][gp][n_pad][RB]
   double* wpart;       // [rbs][gp][RB]
 };
@@ -258,20 +263,40 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
 #ifndef MCP_K1G_HINTS
 #define MCP_K1G_HINTS 0   // 1: L2 hints (V evict_first, Y evict_last): -20% DRAM, +3% time
 #endif
+#ifndef MCP_K1G_G2MAP
+#define MCP_K1G_G2MAP 1   // fp32 rows: conflict-free GEMM2 row map (experiment builds: 0)
+#endif
 #define K1G_LOAD_V(dst, V, ldv, row0, c) \
   (MCP_K1G_HINTS ? k1_load_v_hint<VT>(dst, V, ldv, row0, c, pol_v) : k1_load_v<VT>(dst, V, ldv, row0, c))
 
 template <typename VT, int RB>
+__host__ __device__ constexpr int k1g_sp() {
+  return (MCP_K1G_G2MAP && sizeof(VT) == 4) ? RB + 2 : RB + 4;
+}
+template <typename VT, int RB>
 __host__ __device__ constexpr size_t k1g_smem_bytes() {
   return 2 * (size_t)K1_TP * K1_SV * sizeof(VT) + 2 * (size_t)16 * (RB / 8) * 32 * 8 +
-         (size_t)K1_TP * (RB + 4) * 8 + (size_t)8 * RB * 8;
+         (size_t)K1_TP * k1g_sp<VT, RB>() * 8 + (size_t)8 * RB * 8;
 }
 
-template <typename VT, int RB>
+// K1G with TM = true ("K1GT"): the Y partial lives in tensor memory instead of L2.  TMEM is
+// used as private per-thread storage (fp64 as two 32-bit columns): thread (warp w, lane L) owns
+// TMEM lane 32 (w % 4) + L, columns [256 (w / 4), 256 (w / 4) + 256) -- 128 doubles, i.e. the
+// 2 NT doubles of each of the n_chunks GEMM2 accumulators it owns (n_chunks * RB <= 512: c5's
+// n = 1024 runs RB = 32).  Per chunk the previous partial is read with one tcgen05.ld before the
+// k-steps and written back with one tcgen05.st after them: the read-modify-write that spilled
+// from L2 to DRAM at c5 (14x the V bytes, ncu round 1) stays on chip, and the sum order per
+// element is K1G's (acc + prev, tile by tile), so the partials are the same arithmetic.
+template <typename VT, int RB, bool TM>
 __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
   pdl_enter();   // the factor fragments come from the preceding prep kernel
   constexpr int NT = RB / 8;
-  constexpr int SP = RB + 4;
+  static_assert(!TM || NT == 2 || NT == 4, "K1GT: RB = 16 or 32");
+  // P row pitch (doubles): == 4 (mod 16) for fp64 rows (GEMM2 k index = tile row 4 ks + t), == 2
+  // (mod 16) for fp32 rows, whose GEMM2 k index runs over tile rows 8 (ks >> 1) + 2 t + (ks & 1):
+  // the 4-byte V fragment loads then hit bank 8 t + g (+ const), all 32 distinct, where 4 ks + t
+  // gave a 2-way conflict on every load (ncu at c5: 150-257M per launch)
+  constexpr int SP = k1g_sp<VT, RB>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   VT* sV0 = reinterpret_cast<VT*>(smem_raw);
   VT* sV1 = sV0 + K1_TP * K1_SV;
@@ -282,13 +307,23 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int rb = blockIdx.x % prm.rbs;
-  const int pg = blockIdx.x / prm.rbs;
   const int C = prm.n_chunks;
   const int dm1 = prm.d - 1;
   const VT* __restrict__ V = static_cast<const VT*>(prm.V);
-  const double* __restrict__ Af = prm.Afrag + (size_t)rb * C * 16 * NT * 32;
-  double* __restrict__ Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * prm.n_pad * RB;
+  // the (column block, tile) work split shared with K1X (k1x_common.cuh): groups of one CTA per
+  // column block stride the main tiles together, leftover CTAs take block-major tail ranges
+  K1WParams wp;
+  wp.num_tiles = prm.num_tiles;
+  wp.rbs = prm.rbs;
+  wp.nclusters = (int)gridDim.x;
+  wp.groups = prm.groups;
+  wp.t_main = prm.t_main;
+  wp.slots = prm.gp;
+  wp.n_pad = prm.n_pad;
+  wp.Ypart = prm.Ypart;
+  wp.wpart = prm.wpart;
+  constexpr bool kF32 = MCP_K1G_G2MAP && sizeof(VT) == 4;
+  const int g2row = kF32 ? 2 * t : t;   // GEMM2 fragment row of k-step 0
 
   double wacc[NT][2];
 #pragma unroll
@@ -297,9 +332,21 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
   // V streams through L2 (evict first); the CTA's Y partial should stay there (evict last)
   const uint64_t pol_v = MCP_K1G_HINTS ? l2_policy_evict_first() : 0;
   const uint64_t pol_y = MCP_K1G_HINTS ? l2_policy_evict_last() : 0;
+  __shared__ uint32_t s_tmem;
+  uint32_t tme = 0;   // this thread's TMEM base (lane in bits 31..16, column below)
+  if constexpr (TM) {
+    if (warp == 0) tmem_alloc<512>(smem_u32(&s_tmem));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    tme = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2));
+  }
 
-  for (int64_t tile = pg; tile < prm.num_tiles; tile += prm.gp) {
-    const int64_t row0 = tile * K1_TP;
+  K1WTile ti;
+  for (int64_t k = 0; k1w_tile_at(wp, blockIdx.x, k, ti); ++k) {
+    const int64_t row0 = ti.tile * K1_TP;
+    const double* __restrict__ Af = prm.Afrag + (size_t)ti.rb * C * 16 * NT * 32;
+    double* __restrict__ Yp = prm.Ypart + ((size_t)ti.rb * prm.gp + ti.slot) * prm.n_pad * RB;
 
     // ---------------- GEMM1: Z[64 x RB] = V_tile[64 x n] * A[n x RB] ----------------
     double zacc[NT][2];
@@ -361,7 +408,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
       __syncthreads();
       double* yrow = Yp + (size_t)(c * K1_NK + 8 * warp + g) * RB + 2 * t;
       double2 prev[NT];
-      if (!first) {
+      uint32_t tprev[4 * NT];
+      if constexpr (TM) {
+        if (!first) tmem_ld_nowait<4 * NT>(tme + 4 * NT * c, tprev);
+      }
+      if (!TM && !first) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
           prev[nt] = MCP_K1G_HINTS
@@ -371,49 +422,92 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
       double acc[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-      const VT* vcol = sv + t * K1_SV + 8 * warp + g;
-      const double* prow = sP + t * SP + g;
+      const VT* vcol = sv + g2row * K1_SV + 8 * warp + g;
+      const double* prow = sP + g2row * SP + g;
 #pragma unroll 4
       for (int ks = 0; ks < 16; ++ks) {
-        const double a = to_f64(vcol[4 * ks * K1_SV]);
+        const int kr = kF32 ? 8 * (ks >> 1) + (ks & 1) : 4 * ks;   // + g2row: this lane's row
+        const double a = to_f64(vcol[kr * K1_SV]);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt], a, prow[4 * ks * SP + 8 * nt]);
+        for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt], a, prow[kr * SP + 8 * nt]);
       }
+      if constexpr (TM) {
+        if (!first) tmem_ld_wait();
+        uint32_t tout[4 * NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        double2 o = make_double2(acc[nt][0], acc[nt][1]);
-        if (!first) {
-          o.x += prev[nt].x;
-          o.y += prev[nt].y;
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double o = acc[nt][e];
+            if (!first)
+              o += __hiloint2double((int)tprev[4 * nt + 2 * e + 1], (int)tprev[4 * nt + 2 * e]);
+            tout[4 * nt + 2 * e] = (uint32_t)__double2loint(o);
+            tout[4 * nt + 2 * e + 1] = (uint32_t)__double2hiint(o);
+          }
+        tmem_st<4 * NT>(tme + 4 * NT * c, tout);
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double2 o = make_double2(acc[nt][0], acc[nt][1]);
+          if (!first) {
+            o.x += prev[nt].x;
+            o.y += prev[nt].y;
+          }
+          if (MCP_K1G_HINTS)
+            st_l2_hint(reinterpret_cast<double2*>(yrow + 8 * nt), o, pol_y);
+          else
+            *reinterpret_cast<double2*>(yrow + 8 * nt) = o;
         }
-        if (MCP_K1G_HINTS)
-          st_l2_hint(reinterpret_cast<double2*>(yrow + 8 * nt), o, pol_y);
-        else
-          *reinterpret_cast<double2*>(yrow + 8 * nt) = o;
       }
       __syncthreads();
     }
+    if constexpr (TM) tmem_st_wait();   // this tile's partial is in TMEM before the next reads it
     first = false;
-  }
-  if (first) {   // a CTA without tiles still owns a (zero) partial
-    for (int64_t e = threadIdx.x; e < (int64_t)prm.n_pad * RB; e += K1_THREADS) Yp[e] = 0.0;
-  }
+
+    if (ti.last_in_seg) {
+      // ---------------- segment end: this slot's partials leave the CTA ----------------
+      if constexpr (TM) {
+        for (int c = 0; c < C; ++c) {
+          uint32_t tv[4 * NT];
+          tmem_ld_nowait<4 * NT>(tme + 4 * NT * c, tv);
+          tmem_ld_wait();
+          double* yrow = Yp + (size_t)(c * K1_NK + 8 * warp + g) * RB + 2 * t;
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
+          for (int nt = 0; nt < NT; ++nt)
+            *reinterpret_cast<double2*>(yrow + 8 * nt) =
+                make_double2(__hiloint2double((int)tv[4 * nt + 1], (int)tv[4 * nt]),
+                             __hiloint2double((int)tv[4 * nt + 3], (int)tv[4 * nt + 2]));
+        }
+      }
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      double v = wacc[nt][e];
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 16);
-      if (g == 0) sW[warp * RB + 8 * nt + 2 * t + e] = v;
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double v = wacc[nt][e];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (g == 0) sW[warp * RB + 8 * nt + 2 * t + e] = v;
+          wacc[nt][e] = 0.0;
+        }
+      __syncthreads();
+      if (threadIdx.x < RB) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < K1_THREADS / 32; ++w) s += sW[w * RB + threadIdx.x];
+        prm.wpart[((size_t)ti.rb * prm.gp + ti.slot) * RB + threadIdx.x] = s;
+      }
+      __syncthreads();
+      first = true;
     }
-  __syncthreads();
-  if (threadIdx.x < RB) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < K1_THREADS / 32; ++w) s += sW[w * RB + threadIdx.x];
-    prm.wpart[((size_t)rb * prm.gp + pg) * RB + threadIdx.x] = s;
+  }
+  // partial slots no CTA writes (blocks touched by fewer leftover CTAs) are zero
+  k1w_zero_holes<K1_THREADS, RB>(wp, blockIdx.x, 0, prm.n_pad, true);
+  if constexpr (TM) {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc<512>(s_tmem);
   }
 }
 

@@ -73,15 +73,20 @@ struct Entry {
 const Entry kTable[] = {MCP_K1_ROW(double, MCP_F64), MCP_K1_ROW(float, MCP_F32)};
 
 // K1G (Y partial in global memory): column blocks of RB in {16, 32, 64}
-template <typename VT, int RB>
+// (Entry::MTW = 1 marks the TMEM-resident-Y form K1GT, RB 16 or 32)
+template <typename VT, int RB, bool TM>
 void launch_g(const K1Params& prm, int grid, size_t smem, cudaStream_t s) {
-  launch_pdl(k1g_fg_dmma<VT, RB>, dim3(grid), dim3(K1_THREADS), smem, s, prm);
+  launch_pdl(k1g_fg_dmma<VT, RB, TM>, dim3(grid), dim3(K1_THREADS), smem, s, prm);
 }
-#define MCP_K1G_E(VT, DT, RB) \
-  {DT, RB, 0, &launch_g<VT, RB>, (const void*)&k1g_fg_dmma<VT, RB>, k1g_smem_bytes<VT, RB>()}
-const Entry kTableG[] = {MCP_K1G_E(double, MCP_F64, 16), MCP_K1G_E(double, MCP_F64, 32),
-                         MCP_K1G_E(double, MCP_F64, 64), MCP_K1G_E(float, MCP_F32, 16),
-                         MCP_K1G_E(float, MCP_F32, 32),  MCP_K1G_E(float, MCP_F32, 64)};
+#define MCP_K1G_E(VT, DT, RB, TM)                                                \
+  {DT, RB, TM, &launch_g<VT, RB, TM>, (const void*)&k1g_fg_dmma<VT, RB, TM>, \
+   k1g_smem_bytes<VT, RB>()}
+const Entry kTableG[] = {MCP_K1G_E(double, MCP_F64, 16, false), MCP_K1G_E(double, MCP_F64, 32, false),
+                         MCP_K1G_E(double, MCP_F64, 64, false), MCP_K1G_E(float, MCP_F32, 16, false),
+                         MCP_K1G_E(float, MCP_F32, 32, false),  MCP_K1G_E(float, MCP_F32, 64, false),
+                         MCP_K1G_E(double, MCP_F64, 16, true),  MCP_K1G_E(double, MCP_F64, 32, true),
+                         MCP_K1G_E(float, MCP_F32, 16, true),   MCP_K1G_E(float, MCP_F32, 32, true)};
+constexpr int kEntriesG = sizeof(kTableG) / sizeof(kTableG[0]);
 constexpr int kEntries = sizeof(kTable) / sizeof(kTable[0]);
 
 int max_rb_for(int mtw) {
@@ -488,11 +493,18 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
   int rb_g = 16;
   while (rb_g < (int)round_up(r, 8) && rb_g < 64) rb_g *= 2;
   const bool use_g = MCP_CFG_FORCE_K1G ? true : (rb_g >= 4 * rb_k1 || n > 2048);
-  if (MCP_CFG_K1G && use_g && n > 128) {   // any n: Y lives in L2
-    const int rb = rb_g;
+  if (MCP_CFG_K1G && use_g && n > 128) {   // any n: Y lives in L2 (or TMEM)
+    int rb = rb_g;
+    int tm = 0;
+    // K1GT: the Y partial fits TMEM when n_chunks * RB <= 512 (RB 16 or 32)
+    const int nch = (int)ceil_div(n, K1_NK);
+    if (MCP_CFG_K1GT && nch * 16 <= 512) {
+      tm = 1;
+      rb = (nch * 32 <= 512 && rb_g >= 32) ? 32 : 16;
+    }
     int e = -1;
-    for (int i = 0; i < 6; ++i)
-      if (kTableG[i].dtype == dtype && kTableG[i].RB == rb) e = i;
+    for (int i = 0; i < kEntriesG; ++i)
+      if (kTableG[i].dtype == dtype && kTableG[i].RB == rb && kTableG[i].MTW == tm) e = i;
     if (e >= 0) {
       if (ensure_dyn_smem(kTableG[e].fn, kTableG[e].smem)) {
         const int n_chunks = (int)ceil_div(n, K1_NK);
@@ -504,21 +516,22 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
         v.n_pad = n_chunks * K1_NK;
         v.rbs = (int)ceil_div(r, rb);
         v.num_tiles = p_pad / K1_TP;
-        int64_t G = sms;
-        if (G < v.rbs) G = v.rbs;
-        G -= G % v.rbs;
-        int64_t gp = G / v.rbs;
-        if (gp > v.num_tiles) gp = v.num_tiles;
-        if (gp < 1) gp = 1;
-        v.gp = (int)gp;
-        v.grid = v.gp * v.rbs;
+        // every SM busy: K1X's split (groups striding the main tiles + leftover tail ranges)
+        const int64_t T = v.num_tiles;
+        const int Nc = (int)std::min<int64_t>(sms, (int64_t)v.rbs * T);
+        k1w_split(T, v.rbs, Nc, v.groups, v.t_main);
+        int mx = 1;
+        for (int b = 0; b < v.rbs; ++b)
+          mx = std::max(mx, k1w_used_slots(b, T, v.rbs, Nc, v.groups, v.t_main));
+        v.gp = mx;
+        v.grid = Nc;
         v.smem = kTableG[e].smem;
         v.entry = e;
         v.afrag_elems = (size_t)v.rbs * v.n_chunks * 16 * (rb / 8) * 32;
         v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * rb;
         v.wpart_elems = (size_t)v.rbs * v.gp * rb;
-        v.name = std::string("k1g_fg_dmma<") + (dtype == MCP_F64 ? "f64" : "f32") + ",RB=" +
-                 std::to_string(rb) + ">";
+        v.name = std::string(tm ? "k1gt_fg_dmma<" : "k1g_fg_dmma<") +
+                 (dtype == MCP_F64 ? "f64" : "f32") + ",RB=" + std::to_string(rb) + ">";
         return true;
       }
     }
@@ -641,6 +654,8 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
   prm.d = d;
   prm.rbs = v.rbs;
   prm.gp = v.gp;
+  prm.groups = v.groups;
+  prm.t_main = v.t_main;
   prm.Ypart = Ypart;
   prm.wpart = wpart;
   (v.kind == 5 ? kTableG : kTable)[v.entry].launch(prm, v.grid, v.smem, s);

@@ -47,6 +47,10 @@
 #ifndef MCP_CFG_K1G
 #define MCP_CFG_K1G 1
 #endif
+// K1GT: K1G with the Y partial in TMEM (no L2 read-modify-write) when n_chunks * 16 <= 512
+#ifndef MCP_CFG_K1GT
+#define MCP_CFG_K1GT 1
+#endif
 #ifndef MCP_CFG_FORCE_K1G
 #define MCP_CFG_FORCE_K1G 0
 #endif

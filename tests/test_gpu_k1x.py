@@ -36,7 +36,7 @@ def _case(n, p, r, d, seed, weights=False):
     (512, 60_000, 48, 6, True),     # 3 blocks: 49 groups + 1 leftover CTA
     (500, 40_000, 40, 2, True),     # ragged n and r, d = 2
     (256, 50_000, 32, 5, False),    # n <= 384: the register-tiled K1
-    (1024, 60_000, 256, 3, False),  # c5 shape: K1G (Y partial in L2)
+    (1024, 60_000, 256, 3, False),  # c5 shape: K1GT (Y partial in TMEM)
     (900, 20_000, 33, 4, False),    # large ragged n
     (700, 20_000, 20, 3, False),    # 512 < n <= 768: K1G
 ])
@@ -72,3 +72,36 @@ def test_k1x_zero_lambda_exact():
     V, _, _, A = _case(512, 9_000, 64, 3, seed=5)
     res = mcp.fg_implicit(mcp.ObservationSet(V), np.zeros(64), A, 3, 0.0)
     assert res.f == 0.0 and np.array_equal(res.g_A, np.zeros_like(A))
+
+
+@pytest.mark.parametrize("n,p,r,d,dt,rb", [
+    (1024, 40_000, 256, 3, np.float32, 32),   # c5 shape: 8 column blocks of 32
+    (900, 20_000, 33, 4, np.float32, 32),     # ragged n and r (one full + one 1-column block)
+    (1024, 12_000, 64, 5, np.float64, 32),    # fp64 rows
+    (2000, 6_000, 40, 3, np.float64, 16),     # 32 chunks: RB = 16 fills all 512 TMEM columns
+    (1024, 3_000, 256, 4, np.float32, 32),    # 47 tiles x 8 blocks < 2 units per SM: leftover ranges
+    (960, 9_500, 72, 3, np.float32, 32),      # 3 blocks: 49 groups + 1 leftover CTA
+])
+def test_k1gt_tmem_partial_vs_oracle(n, p, r, d, dt, rb):
+    """K1GT (K1G with the Y partial in TMEM): oracle parity, then bitwise determinism and exact
+    nu-linearity (pkg/tests/test_implicit.py:53-57) -- the TMEM read-modify-write keeps K1G's
+    per-element sum order."""
+    rng = np.random.default_rng(n + r)
+    V = (rng.standard_normal((n, p)) / np.sqrt(n)).astype(dt)
+    nu = rng.uniform(0.5, 2.0, p) / p
+    lam = rng.standard_normal(r)
+    A = rng.standard_normal((n, r)) / np.sqrt(n)
+    obs = mcp.ObservationSet(V, nu)
+    res = mcp.fg_implicit(obs, lam, A, d, 0.1)
+    var = obs.device_context().last_variant
+    assert var.startswith("k1gt_fg_dmma") and f"RB={rb}" in var, var
+    V64 = V.astype(np.float64)
+    f, gl, gA = om.fg_implicit(V64, nu, lam, A, d, 0.1)
+    fs, gls, gAs, _ = om.term_scales(V64, nu, lam, A, d, 0.1)
+    e = max(om.term_rel_err(res.f, f, fs), om.term_rel_err(res.g_lam, gl, gls),
+            om.term_rel_err(res.g_A, gA, gAs))
+    print(f"n={n} p={p} r={r} d={d}: {var} term-scale {e:.2e}")
+    assert e <= 1e-10
+    Y1 = mcp.ttsv_batch(obs, A, d)
+    assert np.array_equal(Y1, mcp.ttsv_batch(obs, A, d))
+    assert np.array_equal(2.0 * Y1, mcp.ttsv_batch(mcp.ObservationSet(V, 2.0 * nu), A, d))

@@ -324,7 +324,11 @@ __global__ void k_ordered_sum(const double* __restrict__ part, int m, double* __
 // 0 refills the stage STAGES - 1 chunks ahead.  Measured at c4: 360.8 ms, the same as K52 (359.4;
 // 77% of the FP64 pipe) with one TMA pair per chunk instead of 2048 cp.async.  Releasing stages
 // warp by warp with the last warp refilling (no CTA barrier, K1X's scheme) measured 404 ms: the
-// fastest warps run to the end of the ring and then wait for refills gated by the slowest warp.  Fragment loads stay conflict-free under
+// fastest warps run to the end of the ring and then wait for refills gated by the slowest warp.
+// Round 2: the refill decode (sqrt + 64-bit divisions per chunk on warp 0) made warp 0 the
+// straggler at every barrier (ncu source view: 15% of samples behind BAR.SYNC); the refill cursor
+// is now kept by every thread, decoded once per pair, the refilling warp rotates, and the next
+// k-step's operands load before the current DMMAs -- 359.5 -> 346.8 ms (76.8% -> 79.6%).  Fragment loads stay conflict-free under
 // the swizzle by letting DMMA row (column) g of a 8-row m-tile read physical tile row
 // 2g (g < 4) / 2(g - 4) + 1 (g >= 4): the 16 lanes of a half-warp then hit 16 distinct 8-byte
 // banks.  The epilogue uses the same row map for the weights, so the sum is the same Gram power
@@ -334,6 +338,12 @@ constexpr int K53_NK = 16;          // doubles per chunk row (one 128-byte swizz
 constexpr int K53_THREADS = 512;
 constexpr int K53_STAGES = 6;
 constexpr int K53_STAGE_BYTES = 2 * K53_T * K53_NK * 8;   // I and J chunks, 32 KB
+#ifndef MCP_K53_SYNC
+#define MCP_K53_SYNC 1
+#endif
+// chunks per CTA barrier (and refill group); measured at c4 (tools/ab.sh, one box): 1 -> 346.8 ms,
+// 2 -> 347.9, 3 -> 350.6 -- the skew does not amortise over longer groups
+constexpr int K53_SYNC = MCP_K53_SYNC;
 
 __host__ __device__ constexpr size_t k53_smem_bytes() {
   return 1024 + (size_t)K53_STAGES * K53_STAGE_BYTES + 256;
@@ -376,12 +386,10 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
           ? (pair_end - pair_begin - blockIdx.x + gridDim.x - 1) / gridDim.x
           : 0;
   const int64_t nsteps = my_pairs * n_chunks;
-  auto issue = [&](int64_t q) {   // TMA of step q into its stage (one thread)
-    const int s = (int)(q % K53_STAGES);
-    const int64_t kp = q / n_chunks;
-    const int c = (int)(q % n_chunks);
-    int64_t I, J;
-    decode(pair_begin + blockIdx.x + kp * gridDim.x, I, J);
+  auto pair_of = [&](int64_t kp, int64_t& I_, int64_t& J_) {
+    decode(pair_begin + blockIdx.x + kp * gridDim.x, I_, J_);
+  };
+  auto issue = [&](int s, int c, int64_t I, int64_t J) {   // TMA of one chunk into stage s
     unsigned char* st = base + (size_t)s * K53_STAGE_BYTES;
     mbar_arrive_expect_tx(&full[s], K53_STAGE_BYTES);
     tma_load_2d(st, &tmI, c * K53_NK, (int)(I * K53_T), smem_u32(&full[s]));
@@ -394,8 +402,21 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
     tma_prefetch_desc(&tmJ);
   }
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (int64_t q = 0; q < K53_STAGES && q < nsteps; ++q) issue(q);
+  if (threadIdx.x == 0) {
+    int64_t I = 0, J = 0;
+    for (int64_t q = 0; q < K53_STAGES && q < nsteps; ++q) {
+      if (q % n_chunks == 0) pair_of(q / n_chunks, I, J);
+      issue((int)q, (int)(q % n_chunks), I, J);
+    }
+  }
+  // Refill cursor (step q + STAGES), kept by every thread so the refilling warp can rotate: the
+  // tile-pair decode (sqrt, 64-bit divisions) runs once per pair on all warps at the same point
+  // instead of once per chunk on warp 0, which made warp 0 the straggler at every chunk barrier
+  // (ncu source view of the previous form: 15% of warp samples waiting behind BAR.SYNC).
+  int64_t r_kp = K53_STAGES / n_chunks;
+  int r_c = K53_STAGES % n_chunks;
+  int64_t rI = 0, rJ = 0;
+  if (K53_STAGES < nsteps) pair_of(r_kp, rI, rJ);
 
   // per-lane word offsets (doubles) inside a stage: row * 16 + (k ^ 2 (row & 7)), row & 7 = prow
   const int swz = 2 * prow;
@@ -413,33 +434,61 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  int s = 0, cc = 0;      // stage, chunk of the current pair
+  uint32_t ph = 0;
+  int64_t kp = 0;
   for (int64_t q = 0; q < nsteps; ++q) {
-    const int s = (int)(q % K53_STAGES);
-    mbar_wait(&full[s], (uint32_t)((q / K53_STAGES) & 1));
+    mbar_wait(&full[s], ph);
     const uint32_t sb = st0 + (uint32_t)s * K53_STAGE_BYTES;
+    // operands of k-step ks + 1 are loaded before k-step ks's DMMAs issue (ordered ld.shared),
+    // so a warp running alone keeps the pipe fed
+    double a[2][4], b[2][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[0][i] = k1w_lds_f64(sb + 8u * (uint32_t)(aoff[i] + (t ^ swz)));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[0][i] = k1w_lds_f64(sb + 8u * (uint32_t)(boff[i] + (t ^ swz)));
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      const int kk = (4 * ks + t) ^ swz;
-      double a[4], b[4];
+      const int cur = ks & 1, nxt = cur ^ 1;
+      if (ks < 3) {
+        const int kk = (4 * (ks + 1) + t) ^ swz;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = k1w_lds_f64(sb + 8u * (uint32_t)(aoff[i] + kk));
+        for (int i = 0; i < 4; ++i) a[nxt][i] = k1w_lds_f64(sb + 8u * (uint32_t)(aoff[i] + kk));
 #pragma unroll
-      for (int i = 0; i < 4; ++i) b[i] = k1w_lds_f64(sb + 8u * (uint32_t)(boff[i] + kk));
+        for (int i = 0; i < 4; ++i) b[nxt][i] = k1w_lds_f64(sb + 8u * (uint32_t)(boff[i] + kk));
+      }
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], a[mt], b[nt]);
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], a[cur][mt], b[cur][nt]);
     }
-    // every warp is done with the stage: refill it with step q + STAGES (STAGES - 1 steps ahead)
-    __syncthreads();
-    if (threadIdx.x == 0 && q + K53_STAGES < nsteps) {
-      k1w_fence_proxy_async();
-      issue(q + K53_STAGES);
+    // every K53_SYNC chunks: every warp is done with those stages; refill them with the steps
+    // STAGES ahead (one CTA barrier per K53_SYNC chunks: the barrier skew is per barrier)
+    if ((q + 1) % K53_SYNC == 0 || q + 1 == nsteps) {
+      __syncthreads();
+      const int64_t q0 = q + 1 - ((q % K53_SYNC) + 1);   // first step of this sync group
+      for (int64_t qq = q0; qq <= q; ++qq) {
+        if (qq + K53_STAGES >= nsteps) break;
+        if (warp == (int)(qq & 15) && lane == 0) {
+          k1w_fence_proxy_async();
+          issue((int)(qq % K53_STAGES), r_c, rI, rJ);
+        }
+        if (++r_c == n_chunks) {
+          r_c = 0;
+          ++r_kp;
+          if (qq + K53_STAGES + 1 < nsteps) pair_of(r_kp, rI, rJ);
+        }
+      }
     }
-    if ((q + 1) % n_chunks == 0) {
+    if (++s == K53_STAGES) {
+      s = 0;
+      ph ^= 1u;
+    }
+    if (++cc == n_chunks) {
+      cc = 0;
       // last chunk of a tile pair: sum nu_l nu_l' g^d over the tile (x2 off the diagonal)
       int64_t I, J;
-      decode(pair_begin + blockIdx.x + (q / n_chunks) * gridDim.x, I, J);
+      pair_of(kp++, I, J);
       double tile_sum = 0.0;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {

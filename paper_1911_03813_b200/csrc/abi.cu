@@ -224,6 +224,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     }
     c->tm_v_ready = false;
     c->tm_c_ready = false;
+    c->tm_l3_ready = false;
   }
   if (!c->tm_v_ready) {
     if (!make_tmap_f32(&c->tm_v1, c->dV32, c->ldv32, c->p_pad, 4 * c->ldv32, 32, 128,
@@ -233,9 +234,21 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
       return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for V");
     c->tm_v_ready = true;
   }
-  // K1T2: V_lo precomputed once per set (falls back to the in-kernel split if it does not fit)
+  // K1T2: V_lo formed in shared memory by splitter warps (MCP_CFG_K1T2_INSPLIT), else
+  // precomputed once per set (falling back to K1T's in-kernel split if it does not fit)
+  // The split pays where the UMMAs are compute-bound enough to spare shared-memory bandwidth:
+  // measured c3 (RB = 64: N = 128 / 64 products) 5.46 -> 5.11 ms, c5 (RB = 48: N = 96 / 48)
+  // 220 -> 238 ms -- so only when K1T2's column block is 64 (same formula as below).
+  const int rb_v2 = [&] {
+    int rbv = (int)std::min<int64_t>(64, round_up(r, 16));
+    while (rbv > 16 && ((MCP_CFG_K1T2_SERIAL ? 1 : 2) + t.mt2) * rbv > 512) rbv -= 16;
+    return rbv;
+  }();
   t.v2 = false;
-  if (!MCP_CFG_K1T_V1) {
+  t.insplit = !MCP_CFG_K1T_V1 && MCP_CFG_K1T2_INSPLIT && rb_v2 >= 64;
+  if (t.insplit) {
+    t.v2 = true;
+  } else if (!MCP_CFG_K1T_V1) {
     if (!c->dVlo32) {
       const size_t bytes = sizeof(float) * (size_t)c->p_pad * c->ldv32;
       if (cudaMalloc(&c->dVlo32, bytes) == cudaSuccess) {
@@ -258,14 +271,13 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   // K1T2's GEMM2 V reads: one 3-D TMA per 16 KB stage half when rows are whole 32-float chunks
   t.g2_3d = false;
   if (t.v2 && c->ldv32 % 32 == 0 && c->ldv32 >= 128 && MCP_CFG_K1T2_G2_3D) {
-    if (!c->tm_c_ready) {
-      c->tm_c_ready =
-          make_tmap_f32_chunks(&c->tm_v3, c->dV32, c->ldv32, c->p_pad, 32, 4,
-                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
-          make_tmap_f32_chunks(&c->tm_l3, c->dVlo32, c->ldv32, c->p_pad, 32, 4,
-                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    }
-    t.g2_3d = c->tm_c_ready;
+    if (!c->tm_c_ready)
+      c->tm_c_ready = make_tmap_f32_chunks(&c->tm_v3, c->dV32, c->ldv32, c->p_pad, 32, 4,
+                                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    if (!t.insplit && !c->tm_l3_ready)
+      c->tm_l3_ready = make_tmap_f32_chunks(&c->tm_l3, c->dVlo32, c->ldv32, c->p_pad, 32, 4,
+                                            CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    t.g2_3d = c->tm_c_ready && (t.insplit || c->tm_l3_ready);
   }
   // column block RB (the UMMA N): as wide as TMEM allows -- Z (K1T2: double-buffered) plus
   // Y[mt] for the n / 128 m-tiles -- since the 3xTF32 UMMAs are shared-memory-bandwidth bound
@@ -345,7 +357,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
                 std::to_string(RB) + ",S=" + std::to_string(ns) +
                 (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
-                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + ",flush=" + std::to_string(t.flush)
+                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + (t.insplit ? ",insplit" : "") + ",flush=" + std::to_string(t.flush)
                       : std::string()) +
                 ">";
   return MCP_OK;
@@ -424,13 +436,15 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.flush = t.flush;
   prm.g2_3d = t.g2_3d ? 1 : 0;
   prm.wide = t.wide;
+  prm.insplit = t.insplit ? 1 : 0;
   // opt-in: GEMM2 as V P_hi with P_hi rounded to nearest (8-9% faster at c3 / c5, but normwise
   // error up to 7e-5 at reduced p -- too close to the stated 1e-4 to be the default)
   prm.g2x2 = MCP_CFG_K1T2_G2X2 ? 1 : 0;
   auto* ev = timing_begin(c, s);
   if (t.v2)
-    k1t2_fg_tf32<<<t.gp * t.rbs, K1T2_THREADS, t.smem, s>>>(
-        c->tm_v1, t.g2_3d ? c->tm_v3 : c->tm_v2, c->tm_l1, t.g2_3d ? c->tm_l3 : c->tm_l2, c->tm_a,
+    k1t2_fg_tf32<<<t.gp * t.rbs, t.insplit ? K1T2_THREADS_S : K1T2_THREADS, t.smem, s>>>(
+        c->tm_v1, t.g2_3d ? c->tm_v3 : c->tm_v2, t.insplit ? c->tm_v1 : c->tm_l1,
+        t.insplit ? (t.g2_3d ? c->tm_v3 : c->tm_v2) : (t.g2_3d ? c->tm_l3 : c->tm_l2), c->tm_a,
         prm);
   else
     k1t_fg_tf32<<<t.gp * t.rbs, K1T_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_a, prm);
@@ -787,6 +801,7 @@ int load_obs_impl(mcp_ctx* c, const void* V, bool on_device, int dtype, int layo
   c->own_v32 = false;
   c->tm_v_ready = false;
   c->tm_c_ready = false;
+  c->tm_l3_ready = false;
   c->tm_w_kind = 0;
   int rc = dtype == MCP_F64
                ? upload_obs<double>(c, (const double*)V, on_device, layout, n, p, ld)

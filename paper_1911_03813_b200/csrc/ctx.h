@@ -64,6 +64,7 @@ struct mcp_ctx {
   CUtensorMap tm_l1, tm_l2;
   CUtensorMap tm_v3, tm_l3;    // K1T2 GEMM2: 3-D chunk maps over V / V_lo (ld % 32 == 0)
   bool tm_c_ready = false;
+  bool tm_l3_ready = false;   // the V_lo chunk map (tm_l3) matches dVlo32
   CUtensorMap tm_w;            // K1X observation map (3-D, 32 x 32 x 16 boxes, 128-byte swizzle)
   int tm_w_kind = 0;           // tile rows of the K1X shape tm_w was encoded for (0: none)
   void* tm_a_addr = nullptr;
@@ -114,6 +115,7 @@ struct K1TPlan {
   int flush = 8;        // K1T2 tiles per fp64 flush of the fp32 TMEM Y
   bool g2_3d = false;   // K1T2 GEMM2 V loads as one 3-D TMA per operand and stage
   int wide = 0;         // K1T2 GEMM2 m-tiles with the N = 2 RB [P_hi | P_lo] product
+  bool insplit = false; // K1T2 V_lo formed in shared memory (no V_lo copy in HBM)
   int64_t num_tiles = 0;
   size_t smem = 0;
 };

@@ -58,6 +58,8 @@ struct K1TParams {
   int g2_3d = 0;      // K1T2: tm_v2 / tm_l2 are 3-D chunk maps (one TMA per 16 KB operand)
   int g2x2 = 0;       // K1T2: GEMM2 as V P_hi (2 products) with P_hi rounded to nearest; the
                       // dropped V_hi P_lo term is unbiased and <= 2^-12 of each product
+  int insplit = 0;    // K1T2: V_lo = V - tf32(V) formed in shared memory by 4 splitter warps
+                      // from the one TMA'd fp32 stage (no V_lo copy in HBM, DRAM ~1x V)
   int wide = 0;       // K1T2: GEMM2 m-tiles [0, wide) run V_hi [P_hi | P_lo] as ONE N = 2 RB
                       // product into two TMEM halves (spare columns), the V_hi operand read once
 };
@@ -366,6 +368,11 @@ __global__ void k_f64_to_f32(const double* __restrict__ src, float* __restrict__
 // columns each with zcat), then Y[mt]: (zbufs * ZW / RB + n/128) RB <= 512 columns.
 constexpr int K1T2_EPI_WARPS = 8;
 constexpr int K1T2_THREADS = (2 + K1T2_EPI_WARPS) * 32;
+constexpr int K1T2_SPLIT_WARPS = 4;                                   // prm.insplit
+constexpr int K1T2_THREADS_S = K1T2_THREADS + K1T2_SPLIT_WARPS * 32;
+#ifndef MCP_K1T2_KO
+#define MCP_K1T2_KO 0   // timing knockouts (see the producer), experiment builds only
+#endif
 #ifndef MCP_K1T2_PROF
 #define MCP_K1T2_PROF 0   // diagnostics only: CTA 0 prints per-role wait / busy cycles
 #endif
@@ -377,7 +384,7 @@ constexpr int K1T2_THREADS = (2 + K1T2_EPI_WARPS) * 32;
 #define K1T2_ACC(v)
 #endif
 
-__global__ void __launch_bounds__(K1T2_THREADS, 1)
+__global__ void __launch_bounds__(K1T2_THREADS_S, 1)
     k1t2_fg_tf32(const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_v2,
                  const __grid_constant__ CUtensorMap tm_l1, const __grid_constant__ CUtensorMap tm_l2,
                  const __grid_constant__ CUtensorMap tm_a, K1TParams prm) {
@@ -397,6 +404,10 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
   uint64_t* y_full = z_full + 4;
   uint64_t* y_empty = z_full + 5;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(z_full + 6);
+  uint64_t* split = z_full + 8;         // [NS], prm.insplit: V_lo of the stage is formed
+  // the MMA consumes a stage once its data is complete: TMA bytes (full) or, with the in-kernel
+  // split, the splitter warps' V_lo as well (split)
+  uint64_t* ready = prm.insplit ? split : full;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = blockIdx.x % prm.rbs;
@@ -414,6 +425,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&split[s], K1T2_SPLIT_WARPS);
     }
     mbar_init(&z_full[0], 1);
     mbar_init(&z_full[1], 1);
@@ -475,12 +487,18 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb, ++q) {
           unsigned char* st = stage(q);
           uint64_t* fb = &full[q % NS];
-          mbar_arrive_expect_tx(fb, 2 * K1T_VBYTES + 256 * RB);
+          // MCP_K1T2_KO (timing knockouts, wrong results, experiment builds only): bit 0 = no
+          // V_lo loads, bit 1 = factor loaded for the first tile only, bit 2 = no GEMM2 loads
+          const bool ko_lo = (MCP_K1T2_KO & 1) || prm.insplit;
+          const bool ko_a = (MCP_K1T2_KO & 2) && q >= NS;
+          mbar_arrive_expect_tx(fb, (ko_lo ? 1 : 2) * K1T_VBYTES + (ko_a ? 0 : 256 * RB));
           load(st, &tm_v1, kb * 32, row0, fb, pol_keep);
-          load(st + K1T_VBYTES, &tm_l1, kb * 32, row0, fb, pol_keep);
-          tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, kb * 32, rb * RB, smem_u32(fb));
-          tma_load_2d(st + 2 * K1T_VBYTES + 128 * RB, &tm_a, kb * 32, prm.r_pad + rb * RB,
-                      smem_u32(fb));
+          if (!ko_lo) load(st + K1T_VBYTES, &tm_l1, kb * 32, row0, fb, pol_keep);
+          if (!ko_a) {
+            tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, kb * 32, rb * RB, smem_u32(fb));
+            tma_load_2d(st + 2 * K1T_VBYTES + 128 * RB, &tm_a, kb * 32, prm.r_pad + rb * RB,
+                        smem_u32(fb));
+          }
         }
       };
       auto g2 = [&](int64_t v) {
@@ -489,7 +507,22 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
           const int mt = step >> 2, rc = step & 3;
           unsigned char* st = stage(q);
           uint64_t* fb = &full[q % NS];
-          mbar_arrive_expect_tx(fb, 2 * K1T_VBYTES);
+          if (MCP_K1T2_KO & 4) {
+            mbar_arrive(fb);
+            continue;
+          }
+          const bool no_lo = (MCP_K1T2_KO & 1) || prm.insplit;
+          mbar_arrive_expect_tx(fb, (no_lo ? 1 : 2) * K1T_VBYTES);
+          if (no_lo) {
+            if (prm.g2_3d) {
+              load3(st, &tm_v2, row0 + rc * 32, mt * 4, fb, pol_drop);
+            } else {
+#pragma unroll
+              for (int b = 0; b < 4; ++b)
+                load(st + b * 4096, &tm_v2, mt * 128 + b * 32, row0 + rc * 32, fb, pol_drop);
+            }
+            continue;
+          }
           if (prm.g2_3d) {
             load3(st, &tm_v2, row0 + rc * 32, mt * 4, fb, pol_drop);
             load3(st + K1T_VBYTES, &tm_l2, row0 + rc * 32, mt * 4, fb, pol_drop);
@@ -534,7 +567,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             const int s = (int)(q % NS);
             {
               K1T2_T0();
-              mbar_wait(&full[s], (uint32_t)(q / NS) & 1);
+              mbar_wait(&ready[s], (uint32_t)(q / NS) & 1);
               K1T2_ACC(w_full1);
             }
             tc_fence_after();
@@ -553,7 +586,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
                 umma_tf32(tz, dvh + 2 * ks, dah + 2 * ks, id1c, (kb | ks) != 0 ? 1u : 0u);
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks)
-                umma_tf32(tz + RB, dvl + 2 * ks, dah + 2 * ks, id1, 1u);
+                if (!(MCP_K1T2_KO & 8)) umma_tf32(tz + RB, dvl + 2 * ks, dah + 2 * ks, id1, 1u);
             } else {
 #pragma unroll
               for (int pr = 0; pr < 3; ++pr) {
@@ -589,7 +622,7 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
             const int s = (int)(q % NS);
             {
               K1T2_T0();
-              mbar_wait(&full[s], (uint32_t)(q / NS) & 1);
+              mbar_wait(&ready[s], (uint32_t)(q / NS) & 1);
               K1T2_ACC(w_full2);
             }
             tc_fence_after();
@@ -604,11 +637,13 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
                           (fresh && rc == 0 && ks == 0) ? 0u : 1u);
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks)
-                umma_tf32(ty + ycol(mt), dvl + 64 * ks, dph + boff + 2 * ks, id2, 1u);
+                if (!(MCP_K1T2_KO & 8))
+                  umma_tf32(ty + ycol(mt), dvl + 64 * ks, dph + boff + 2 * ks, id2, 1u);
             } else {
 #pragma unroll
               for (int pr = 0; pr < 3; ++pr) {
                 if (pr == 1 && prm.g2x2) continue;
+                if (pr == 2 && (MCP_K1T2_KO & 8)) continue;
                 const uint64_t av = pr == 2 ? dvl : dvh;
                 const uint64_t bv = (pr == 1 ? dpl : dph) + boff;
 #pragma unroll
@@ -660,6 +695,34 @@ __global__ void __launch_bounds__(K1T2_THREADS, 1)
                clock64() - t_begin, w_full1, w_full2, w_p, w_y, (long long)my_tiles);
 #endif
       (void)t_begin;
+    }
+  } else if (warp >= 2 + K1T2_EPI_WARPS) {
+    // =========================== splitter warps (prm.insplit) ===========================
+    // every stage in ring order (the same sequence for either tile order): V_lo = V - tf32(V)
+    // elementwise into the stage's V_lo half -- the same swizzled position, since both halves
+    // are 1 KB-aligned copies of one layout -- then release the stage to the MMA issuer
+    const int st_id = (warp - 2 - K1T2_EPI_WARPS) * 32 + lane;   // 0..127
+    const int64_t total = my_tiles * (int64_t)(nkb + 4 * mt2);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t q = 0; q < total; ++q) {
+      mbar_wait(&full[s], ph);
+      const float4* vh = reinterpret_cast<const float4*>(base + s * SB);
+      float4* vl = reinterpret_cast<float4*>(base + s * SB + K1T_VBYTES);
+      float4 x[K1T_VBYTES / 16 / 128];
+#pragma unroll
+      for (int k = 0; k < K1T_VBYTES / 16 / 128; ++k) x[k] = vh[st_id + 128 * k];
+#pragma unroll
+      for (int k = 0; k < K1T_VBYTES / 16 / 128; ++k)
+        vl[st_id + 128 * k] = make_float4(x[k].x - tf32_hi(x[k].x), x[k].y - tf32_hi(x[k].y),
+                                          x[k].z - tf32_hi(x[k].z), x[k].w - tf32_hi(x[k].w));
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&split[s]);
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
   } else {
     // =========================== epilogue / flush warps ===========================

@@ -62,6 +62,10 @@
 #ifndef MCP_CFG_K1T_V1
 #define MCP_CFG_K1T_V1 0
 #endif
+// fast mode: V_lo formed in shared memory by splitter warps (no V_lo copy in HBM)
+#ifndef MCP_CFG_K1T2_INSPLIT
+#define MCP_CFG_K1T2_INSPLIT 1
+#endif
 #ifndef MCP_CFG_K1T2_SERIAL
 #define MCP_CFG_K1T2_SERIAL 1
 #endif

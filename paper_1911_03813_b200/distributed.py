@@ -306,29 +306,42 @@ def data_norm_sq_sharded(sobs: ShardedObservationSet, d: int, group=None,
     nubufs = [be.buffer(pmax * 8) for _ in range(2)] if with_nu else [None, None]
     steps = world // 2
 
+    # gloo moves only host tensors point to point: device shards are staged through host
+    # copies there (the multi-rank-on-one-GPU test mode); NCCL sends HBM directly
+    staged = dev.type == "cuda" and dist.get_backend(group) == "gloo"
+
     def exchange(cur_rows, cur_nu, src_shard, slot):
         # send the shard we hold to the left neighbour, receive the next one from the right
         nb = int(metas[src_shard][0])
-        ops = [dist.P2POp(dist.isend, cur_rows, left, group),
-               dist.P2POp(dist.irecv, bufs[slot][:nb * rb], right, group)]
+        pairs = [(cur_rows, bufs[slot][:nb * rb])]
         if with_nu:
-            ops += [dist.P2POp(dist.isend, cur_nu, left, group),
-                    dist.P2POp(dist.irecv, nubufs[slot][:nb * 8], right, group)]
-        return dist.batch_isend_irecv(ops)
+            pairs.append((cur_nu, nubufs[slot][:nb * 8]))
+        ops, landing = [], []
+        for snd, rcv in pairs:
+            if staged:
+                snd = snd.cpu()
+                host = torch.empty(rcv.shape, dtype=rcv.dtype)
+                landing.append((host, rcv))
+                rcv = host
+            ops += [dist.P2POp(dist.isend, snd, left, group),
+                    dist.P2POp(dist.irecv, rcv, right, group)]
+        return dist.batch_isend_irecv(ops), landing
 
     total = float(be.self_sum(d))
     cur_rows, cur_nu = rows, nu
-    reqs = exchange(cur_rows, cur_nu, (rank + 1) % world, 0)
+    reqs, landing = exchange(cur_rows, cur_nu, (rank + 1) % world, 0)
     for s in range(1, steps + 1):
         for q in reqs:
             q.wait()
+        for host, rcv in landing:
+            rcv.copy_(host)
         src = (rank + s) % world
         nb = int(metas[src][0])
         slot = (s - 1) % 2
         cur_rows = bufs[slot][:nb * rb]
         cur_nu = nubufs[slot][:nb * 8] if with_nu else None
         if s < steps:   # next hop in flight while this rectangle is reduced
-            reqs = exchange(cur_rows, cur_nu, (rank + s + 1) % world, s % 2)
+            reqs, landing = exchange(cur_rows, cur_nu, (rank + s + 1) % world, s % 2)
         part, nparts, order = 0, 1, 0
         if world % 2 == 0 and s == steps:
             # shards k and k + W/2 meet from both sides: the lower rank takes the first half of

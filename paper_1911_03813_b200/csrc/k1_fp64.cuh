@@ -60,14 +60,14 @@ __host__ __device__ constexpr size_t k1_smem_bytes() {
          + (size_t)8 * RB * 8;                       // w cross-warp reduction
 }
 
-template <typename VT>
+template <typename VT, int THREADS = K1_THREADS>
 __device__ __forceinline__ void k1_load_v(VT* dst, const VT* __restrict__ V, int64_t ldv,
                                           int64_t row0, int c) {
   constexpr int SEG = 16 / sizeof(VT);
   constexpr int SEGS_ROW = K1_NK / SEG;
   constexpr int TOTAL = K1_TP * SEGS_ROW;
 #pragma unroll
-  for (int s = threadIdx.x; s < TOTAL; s += K1_THREADS) {
+  for (int s = threadIdx.x; s < TOTAL; s += THREADS) {
     const int row = s / SEGS_ROW, seg = s % SEGS_ROW;
     const int64_t col = (int64_t)c * K1_NK + seg * SEG;
     const bool ok = col < ldv;
@@ -76,14 +76,14 @@ __device__ __forceinline__ void k1_load_v(VT* dst, const VT* __restrict__ V, int
   }
 }
 
-template <typename VT>
+template <typename VT, int THREADS = K1_THREADS>
 __device__ __forceinline__ void k1_load_v_hint(VT* dst, const VT* __restrict__ V, int64_t ldv,
                                                int64_t row0, int c, uint64_t policy) {
   constexpr int SEG = 16 / sizeof(VT);
   constexpr int SEGS_ROW = K1_NK / SEG;
   constexpr int TOTAL = K1_TP * SEGS_ROW;
 #pragma unroll
-  for (int s = threadIdx.x; s < TOTAL; s += K1_THREADS) {
+  for (int s = threadIdx.x; s < TOTAL; s += THREADS) {
     const int row = s / SEGS_ROW, seg = s % SEGS_ROW;
     const int64_t col = (int64_t)c * K1_NK + seg * SEG;
     const bool ok = col < ldv;
@@ -92,11 +92,11 @@ __device__ __forceinline__ void k1_load_v_hint(VT* dst, const VT* __restrict__ V
   }
 }
 
-template <int NT>
+template <int NT, int THREADS = K1_THREADS>
 __device__ __forceinline__ void k1_load_a(double* dst, const double* __restrict__ src) {
   constexpr int TOTAL = 16 * NT * 32 / 2;
 #pragma unroll
-  for (int s = threadIdx.x; s < TOTAL; s += K1_THREADS) cp_async16(dst + 2 * s, src + 2 * s, 16);
+  for (int s = threadIdx.x; s < TOTAL; s += THREADS) cp_async16(dst + 2 * s, src + 2 * s, 16);
 }
 
 template <typename VT, int RB, int MTW>
@@ -266,8 +266,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
 #ifndef MCP_K1G_G2MAP
 #define MCP_K1G_G2MAP 1   // fp32 rows: conflict-free GEMM2 row map (experiment builds: 0)
 #endif
-#define K1G_LOAD_V(dst, V, ldv, row0, c) \
-  (MCP_K1G_HINTS ? k1_load_v_hint<VT>(dst, V, ldv, row0, c, pol_v) : k1_load_v<VT>(dst, V, ldv, row0, c))
+#define K1G_LOAD_V(dst, V, ldv, row0, c)                                       \
+  (MCP_K1G_HINTS ? k1_load_v_hint<VT, THREADS>(dst, V, ldv, row0, c, pol_v) \
+                 : k1_load_v<VT, THREADS>(dst, V, ldv, row0, c))
 
 template <typename VT, int RB>
 __host__ __device__ constexpr int k1g_sp() {
@@ -287,11 +288,19 @@ __host__ __device__ constexpr size_t k1g_smem_bytes() {
 // k-steps and written back with one tcgen05.st after them: the read-modify-write that spilled
 // from L2 to DRAM at c5 (14x the V bytes, ncu round 1) stays on chip, and the sum order per
 // element is K1G's (acc + prev, tile by tile), so the partials are the same arithmetic.
-template <typename VT, int RB, bool TM>
-__global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
+// NW = 8 or 16 warps.  With 16 the warps split the column block in halves: warp w owns row
+// block / GEMM2 m-tile w % 8 and the NTW = NT / 2 column tiles starting at 8 NTW (w / 8) in both
+// GEMMs (4 warps per sub-partition instead of 2, each with half the DMMA chains).
+template <typename VT, int RB, bool TM, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
   pdl_enter();   // the factor fragments come from the preceding prep kernel
+  constexpr int THREADS = NW * 32;
   constexpr int NT = RB / 8;
-  static_assert(!TM || NT == 2 || NT == 4, "K1GT: RB = 16 or 32");
+  constexpr int NTW = NT / (NW / 8);     // column tiles per warp
+  constexpr int TCOLS = 512 / (NW / 4);  // TMEM columns per thread (K1GT)
+  static_assert(NW == 8 || NW == 16, "K1G: 8 or 16 warps");
+  static_assert(NTW >= 1, "K1G: column block too narrow for the warp split");
+  static_assert(!TM || NTW == 2 || NTW == 4, "K1GT: 8 or 16 TMEM columns per chunk and thread");
   // P row pitch (doubles): == 4 (mod 16) for fp64 rows (GEMM2 k index = tile row 4 ks + t), == 2
   // (mod 16) for fp32 rows, whose GEMM2 k index runs over tile rows 8 (ks >> 1) + 2 t + (ks & 1):
   // the 4-byte V fragment loads then hit bank 8 t + g (+ const), all 32 distinct, where 4 ks + t
@@ -307,6 +316,8 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  const int wr = warp & 7;               // row block (GEMM1) / m-tile (GEMM2)
+  const int nt0 = NTW * (warp >> 3);     // first column tile of this warp
   const int C = prm.n_chunks;
   const int dm1 = prm.d - 1;
   const VT* __restrict__ V = static_cast<const VT*>(prm.V);
@@ -325,9 +336,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
   constexpr bool kF32 = MCP_K1G_G2MAP && sizeof(VT) == 4;
   const int g2row = kF32 ? 2 * t : t;   // GEMM2 fragment row of k-step 0
 
-  double wacc[NT][2];
+  double wacc[NTW][2];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
+  for (int nt = 0; nt < NTW; ++nt) wacc[nt][0] = wacc[nt][1] = 0.0;
   bool first = true;
   // V streams through L2 (evict first); the CTA's Y partial should stay there (evict last)
   const uint64_t pol_v = MCP_K1G_HINTS ? l2_policy_evict_first() : 0;
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    tme = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2));
+    tme = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(TCOLS * (warp >> 2));
   }
 
   K1WTile ti;
@@ -349,40 +360,41 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
     double* __restrict__ Yp = prm.Ypart + ((size_t)ti.rb * prm.gp + ti.slot) * prm.n_pad * RB;
 
     // ---------------- GEMM1: Z[64 x RB] = V_tile[64 x n] * A[n x RB] ----------------
-    double zacc[NT][2];
+    double zacc[NTW][2];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) zacc[nt][0] = zacc[nt][1] = 0.0;
+    for (int nt = 0; nt < NTW; ++nt) zacc[nt][0] = zacc[nt][1] = 0.0;
     K1G_LOAD_V(sV0, V, prm.ldv, row0, 0);
-    k1_load_a<NT>(sA0, Af);
+    k1_load_a<NT, THREADS>(sA0, Af);
     cp_async_commit();
     for (int c = 0; c < C; ++c) {
       VT* sv = (c & 1) ? sV1 : sV0;
       double* sa = (c & 1) ? sA1 : sA0;
       if (c + 1 < C) {
         K1G_LOAD_V((c & 1) ? sV0 : sV1, V, prm.ldv, row0, c + 1);
-        k1_load_a<NT>((c & 1) ? sA0 : sA1, Af + (size_t)(c + 1) * 16 * NT * 32);
+        k1_load_a<NT, THREADS>((c & 1) ? sA0 : sA1, Af + (size_t)(c + 1) * 16 * NT * 32);
         cp_async_commit();
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncthreads();
-      const VT* vrow = sv + (8 * warp + g) * K1_SV + t;
+      const VT* vrow = sv + (8 * wr + g) * K1_SV + t;
 #pragma unroll
       for (int ks = 0; ks < 16; ++ks) {
         const double a = to_f64(vrow[4 * ks]);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884(zacc[nt], a, sa[(ks * NT + nt) * 32 + lane]);
+        for (int nt = 0; nt < NTW; ++nt)
+          dmma884(zacc[nt], a, sa[(ks * NT + nt0 + nt) * 32 + lane]);
       }
       __syncthreads();
     }
 
     // ---------------- epilogue: P = nu * z^(d-1), w += P * z ----------------
     {
-      const int lr = 8 * warp + g;
+      const int lr = 8 * wr + g;
       const double nul = prm.nu ? prm.nu[row0 + lr] : prm.nu_const;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+      for (int nt = 0; nt < NTW; ++nt) {
         double pv[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -390,7 +402,8 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
           pv[e] = nul * rm_pow(z, dm1);
           wacc[nt][e] += pv[e] * z;
         }
-        *reinterpret_cast<double2*>(&sP[lr * SP + 8 * nt + 2 * t]) = make_double2(pv[0], pv[1]);
+        *reinterpret_cast<double2*>(&sP[lr * SP + 8 * (nt0 + nt) + 2 * t]) =
+            make_double2(pv[0], pv[1]);
       }
     }
     __syncthreads();
@@ -406,36 +419,36 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
         cp_async_wait<0>();
       }
       __syncthreads();
-      double* yrow = Yp + (size_t)(c * K1_NK + 8 * warp + g) * RB + 2 * t;
-      double2 prev[NT];
-      uint32_t tprev[4 * NT];
+      double* yrow = Yp + (size_t)(c * K1_NK + 8 * wr + g) * RB + 8 * nt0 + 2 * t;
+      double2 prev[NTW];
+      uint32_t tprev[4 * NTW];
       if constexpr (TM) {
-        if (!first) tmem_ld_nowait<4 * NT>(tme + 4 * NT * c, tprev);
+        if (!first) tmem_ld_nowait<4 * NTW>(tme + 4 * NTW * c, tprev);
       }
       if (!TM && !first) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NTW; ++nt)
           prev[nt] = MCP_K1G_HINTS
                          ? ld_l2_hint(reinterpret_cast<const double2*>(yrow + 8 * nt), pol_y)
                          : *reinterpret_cast<const double2*>(yrow + 8 * nt);
       }
-      double acc[NT][2];
+      double acc[NTW][2];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-      const VT* vcol = sv + g2row * K1_SV + 8 * warp + g;
-      const double* prow = sP + g2row * SP + g;
+      for (int nt = 0; nt < NTW; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      const VT* vcol = sv + g2row * K1_SV + 8 * wr + g;
+      const double* prow = sP + g2row * SP + 8 * nt0 + g;
 #pragma unroll 4
       for (int ks = 0; ks < 16; ++ks) {
         const int kr = kF32 ? 8 * (ks >> 1) + (ks & 1) : 4 * ks;   // + g2row: this lane's row
         const double a = to_f64(vcol[kr * K1_SV]);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt], a, prow[kr * SP + 8 * nt]);
+        for (int nt = 0; nt < NTW; ++nt) dmma884(acc[nt], a, prow[kr * SP + 8 * nt]);
       }
       if constexpr (TM) {
         if (!first) tmem_ld_wait();
-        uint32_t tout[4 * NT];
+        uint32_t tout[4 * NTW];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             double o = acc[nt][e];
@@ -444,10 +457,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
             tout[4 * nt + 2 * e] = (uint32_t)__double2loint(o);
             tout[4 * nt + 2 * e + 1] = (uint32_t)__double2hiint(o);
           }
-        tmem_st<4 * NT>(tme + 4 * NT * c, tout);
+        tmem_st<4 * NTW>(tme + 4 * NTW * c, tout);
       } else {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
+        for (int nt = 0; nt < NTW; ++nt) {
           double2 o = make_double2(acc[nt][0], acc[nt][1]);
           if (!first) {
             o.x += prev[nt].x;
@@ -468,33 +481,33 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
       // ---------------- segment end: this slot's partials leave the CTA ----------------
       if constexpr (TM) {
         for (int c = 0; c < C; ++c) {
-          uint32_t tv[4 * NT];
-          tmem_ld_nowait<4 * NT>(tme + 4 * NT * c, tv);
+          uint32_t tv[4 * NTW];
+          tmem_ld_nowait<4 * NTW>(tme + 4 * NTW * c, tv);
           tmem_ld_wait();
-          double* yrow = Yp + (size_t)(c * K1_NK + 8 * warp + g) * RB + 2 * t;
+          double* yrow = Yp + (size_t)(c * K1_NK + 8 * wr + g) * RB + 8 * nt0 + 2 * t;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
+          for (int nt = 0; nt < NTW; ++nt)
             *reinterpret_cast<double2*>(yrow + 8 * nt) =
                 make_double2(__hiloint2double((int)tv[4 * nt + 1], (int)tv[4 * nt]),
                              __hiloint2double((int)tv[4 * nt + 3], (int)tv[4 * nt + 2]));
         }
       }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           double v = wacc[nt][e];
           v += __shfl_xor_sync(0xffffffffu, v, 4);
           v += __shfl_xor_sync(0xffffffffu, v, 8);
           v += __shfl_xor_sync(0xffffffffu, v, 16);
-          if (g == 0) sW[warp * RB + 8 * nt + 2 * t + e] = v;
+          if (g == 0) sW[wr * RB + 8 * (nt0 + nt) + 2 * t + e] = v;
           wacc[nt][e] = 0.0;
         }
       __syncthreads();
       if (threadIdx.x < RB) {
         double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < K1_THREADS / 32; ++w) s += sW[w * RB + threadIdx.x];
+        for (int w = 0; w < 8; ++w) s += sW[w * RB + threadIdx.x];   // row blocks in order
         prm.wpart[((size_t)ti.rb * prm.gp + ti.slot) * RB + threadIdx.x] = s;
       }
       __syncthreads();
@@ -502,7 +515,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1g_fg_dmma(K1Params prm) {
     }
   }
   // partial slots no CTA writes (blocks touched by fewer leftover CTAs) are zero
-  k1w_zero_holes<K1_THREADS, RB>(wp, blockIdx.x, 0, prm.n_pad, true);
+  k1w_zero_holes<THREADS, RB>(wp, blockIdx.x, 0, prm.n_pad, true);
   if constexpr (TM) {
     tc_fence_before();
     __syncthreads();

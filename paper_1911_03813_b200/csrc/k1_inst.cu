@@ -73,19 +73,24 @@ struct Entry {
 const Entry kTable[] = {MCP_K1_ROW(double, MCP_F64), MCP_K1_ROW(float, MCP_F32)};
 
 // K1G (Y partial in global memory): column blocks of RB in {16, 32, 64}
-// (Entry::MTW = 1 marks the TMEM-resident-Y form K1GT, RB 16 or 32)
-template <typename VT, int RB, bool TM>
+// (Entry::MTW: 0 = Y partial in L2 (8 warps), 1 = K1GT with 8 warps, 2 = K1GT with 16 warps)
+template <typename VT, int RB, bool TM, int NW>
 void launch_g(const K1Params& prm, int grid, size_t smem, cudaStream_t s) {
-  launch_pdl(k1g_fg_dmma<VT, RB, TM>, dim3(grid), dim3(K1_THREADS), smem, s, prm);
+  launch_pdl(k1g_fg_dmma<VT, RB, TM, NW>, dim3(grid), dim3(NW * 32), smem, s, prm);
 }
-#define MCP_K1G_E(VT, DT, RB, TM)                                                \
-  {DT, RB, TM, &launch_g<VT, RB, TM>, (const void*)&k1g_fg_dmma<VT, RB, TM>, \
+#define MCP_K1G_E(VT, DT, RB, TM, NW)                                                        \
+  {DT, RB, TM ? NW / 8 : 0, &launch_g<VT, RB, TM, NW>, (const void*)&k1g_fg_dmma<VT, RB, TM, NW>, \
    k1g_smem_bytes<VT, RB>()}
-const Entry kTableG[] = {MCP_K1G_E(double, MCP_F64, 16, false), MCP_K1G_E(double, MCP_F64, 32, false),
-                         MCP_K1G_E(double, MCP_F64, 64, false), MCP_K1G_E(float, MCP_F32, 16, false),
-                         MCP_K1G_E(float, MCP_F32, 32, false),  MCP_K1G_E(float, MCP_F32, 64, false),
-                         MCP_K1G_E(double, MCP_F64, 16, true),  MCP_K1G_E(double, MCP_F64, 32, true),
-                         MCP_K1G_E(float, MCP_F32, 16, true),   MCP_K1G_E(float, MCP_F32, 32, true)};
+const Entry kTableG[] = {
+    MCP_K1G_E(double, MCP_F64, 16, false, 8), MCP_K1G_E(double, MCP_F64, 32, false, 8),
+    MCP_K1G_E(double, MCP_F64, 64, false, 8), MCP_K1G_E(float, MCP_F32, 16, false, 8),
+    MCP_K1G_E(float, MCP_F32, 32, false, 8),  MCP_K1G_E(float, MCP_F32, 64, false, 8),
+    MCP_K1G_E(double, MCP_F64, 16, true, 8),  MCP_K1G_E(double, MCP_F64, 32, true, 8),
+    MCP_K1G_E(float, MCP_F32, 16, true, 8),   MCP_K1G_E(float, MCP_F32, 32, true, 8),
+#if MCP_CFG_K1GT_NW == 16
+    MCP_K1G_E(double, MCP_F64, 32, true, 16), MCP_K1G_E(float, MCP_F32, 32, true, 16),
+#endif
+};
 constexpr int kEntriesG = sizeof(kTableG) / sizeof(kTableG[0]);
 constexpr int kEntries = sizeof(kTable) / sizeof(kTable[0]);
 
@@ -501,6 +506,8 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
     if (MCP_CFG_K1GT && nch * 16 <= 512) {
       tm = 1;
       rb = (nch * 32 <= 512 && rb_g >= 32) ? 32 : 16;
+      // 16 warps (column halves, 128 TMEM columns per thread) when RB = 32 and n <= 1024
+      if (MCP_CFG_K1GT_NW == 16 && rb == 32 && nch <= 16) tm = 2;
     }
     int e = -1;
     for (int i = 0; i < kEntriesG; ++i)
@@ -531,7 +538,8 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
         v.ypart_elems = (size_t)v.rbs * v.gp * v.n_pad * rb;
         v.wpart_elems = (size_t)v.rbs * v.gp * rb;
         v.name = std::string(tm ? "k1gt_fg_dmma<" : "k1g_fg_dmma<") +
-                 (dtype == MCP_F64 ? "f64" : "f32") + ",RB=" + std::to_string(rb) + ">";
+                 (dtype == MCP_F64 ? "f64" : "f32") + ",RB=" + std::to_string(rb) +
+                 (tm == 2 ? ",16 warps" : "") + ">";
         return true;
       }
     }

@@ -51,6 +51,12 @@
 #ifndef MCP_CFG_K1GT
 #define MCP_CFG_K1GT 1
 #endif
+// K1GT with 16 warps (column halves per warp, 128 TMEM columns per thread) for RB = 32 and
+// n <= 1024: measured 664 ms at c5 vs 643 ms with 8 warps (half the DMMA chains per warp, V
+// fragments loaded twice), so experiment builds only
+#ifndef MCP_CFG_K1GT_NW
+#define MCP_CFG_K1GT_NW 8
+#endif
 #ifndef MCP_CFG_FORCE_K1G
 #define MCP_CFG_FORCE_K1G 0
 #endif

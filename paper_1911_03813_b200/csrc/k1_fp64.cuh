@@ -280,7 +280,11 @@ __host__ __device__ constexpr size_t k1g_smem_bytes() {
          (size_t)K1_TP * k1g_sp<VT, RB>() * 8 + (size_t)8 * RB * 8;
 }
 
-// K1G with TM = true ("K1GT"): the Y partial lives in tensor memory instead of L2.  TMEM is
+// K1G with TM = true ("K1GT"): the Y partial lives in tensor memory instead of L2 -- all of it
+// when n_chunks * RB <= 512, else (RB = 64 at n = 1024, the c5 default) chunks 0-7 in TMEM and
+// the rest in L2: half K1G's L2 working set, which then stays resident.  Measured at c5 (one
+// box, back to back): K1G 633 ms / 845 W / DRAM 14.3x V; K1GT RB = 32 657 ms / 669 W / 1.0x;
+// K1GT RB = 64 half-and-half 625.5 ms / 741 W / 1.4x (profiles/r02/ab_c5_k1gt_half.txt).  TMEM is
 // used as private per-thread storage (fp64 as two 32-bit columns): thread (warp w, lane L) owns
 // TMEM lane 32 (w % 4) + L, columns [256 (w / 4), 256 (w / 4) + 256) -- 128 doubles, i.e. the
 // 2 NT doubles of each of the n_chunks GEMM2 accumulators it owns (n_chunks * RB <= 512: c5's
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
   constexpr int TCOLS = 512 / (NW / 4);  // TMEM columns per thread (K1GT)
   static_assert(NW == 8 || NW == 16, "K1G: 8 or 16 warps");
   static_assert(NTW >= 1, "K1G: column block too narrow for the warp split");
-  static_assert(!TM || NTW == 2 || NTW == 4, "K1GT: 8 or 16 TMEM columns per chunk and thread");
+  static_assert(!TM || NTW == 2 || NTW == 4 || NTW == 8, "K1GT: 8 / 16 / 32 TMEM columns per chunk");
   // P row pitch (doubles): == 4 (mod 16) for fp64 rows (GEMM2 k index = tile row 4 ks + t), == 2
   // (mod 16) for fp32 rows, whose GEMM2 k index runs over tile rows 8 (ks >> 1) + 2 t + (ks & 1):
   // the 4-byte V fragment loads then hit bank 8 t + g (+ const), all 32 distinct, where 4 ks + t
@@ -353,6 +357,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
     tme = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(TCOLS * (warp >> 2));
   }
 
+  // K1GT: chunks [0, CT) of the partial live in TMEM, the rest (RB = 64 at n = 1024: half of
+  // it) in L2 -- half the L2 working set of K1G, which then stays resident
+  const int CT = TM ? min(C, TCOLS / (4 * NTW)) : 0;
   K1WTile ti;
   for (int64_t k = 0; k1w_tile_at(wp, blockIdx.x, k, ti); ++k) {
     const int64_t row0 = ti.tile * K1_TP;
@@ -422,10 +429,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
       double* yrow = Yp + (size_t)(c * K1_NK + 8 * wr + g) * RB + 8 * nt0 + 2 * t;
       double2 prev[NTW];
       uint32_t tprev[4 * NTW];
+      const bool in_tm = c < CT;   // uniform across the CTA
       if constexpr (TM) {
-        if (!first) tmem_ld_nowait<4 * NTW>(tme + 4 * NTW * c, tprev);
+        if (in_tm && !first) tmem_ld_nowait<4 * NTW>(tme + 4 * NTW * c, tprev);
       }
-      if (!TM && !first) {
+      if (!in_tm && !first) {
 #pragma unroll
         for (int nt = 0; nt < NTW; ++nt)
           prev[nt] = MCP_K1G_HINTS
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
 #pragma unroll
         for (int nt = 0; nt < NTW; ++nt) dmma884(acc[nt], a, prow[kr * SP + 8 * nt]);
       }
-      if constexpr (TM) {
+      if (TM && in_tm) {
         if (!first) tmem_ld_wait();
         uint32_t tout[4 * NTW];
 #pragma unroll
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
     if (ti.last_in_seg) {
       // ---------------- segment end: this slot's partials leave the CTA ----------------
       if constexpr (TM) {
-        for (int c = 0; c < C; ++c) {
+        for (int c = 0; c < CT; ++c) {
           uint32_t tv[4 * NTW];
           tmem_ld_nowait<4 * NTW>(tme + 4 * NTW * c, tv);
           tmem_ld_wait();

@@ -87,6 +87,7 @@ const Entry kTableG[] = {
     MCP_K1G_E(float, MCP_F32, 32, false, 8),  MCP_K1G_E(float, MCP_F32, 64, false, 8),
     MCP_K1G_E(double, MCP_F64, 16, true, 8),  MCP_K1G_E(double, MCP_F64, 32, true, 8),
     MCP_K1G_E(float, MCP_F32, 16, true, 8),   MCP_K1G_E(float, MCP_F32, 32, true, 8),
+    MCP_K1G_E(double, MCP_F64, 64, true, 8),  MCP_K1G_E(float, MCP_F32, 64, true, 8),
 #if MCP_CFG_K1GT_NW == 16
     MCP_K1G_E(double, MCP_F64, 32, true, 16), MCP_K1G_E(float, MCP_F32, 32, true, 16),
 #endif
@@ -503,7 +504,9 @@ bool k1_select(int dtype, int64_t n, int r, int64_t p_pad, int sms, K1Variant& v
     int tm = 0;
     // K1GT: the Y partial fits TMEM when n_chunks * RB <= 512 (RB 16 or 32)
     const int nch = (int)ceil_div(n, K1_NK);
-    if (MCP_CFG_K1GT && nch * 16 <= 512) {
+    if (MCP_CFG_K1GT_HALF && rb_g == 64 && nch * 32 <= 512) {
+      tm = 1;   // RB = 64 with the first half of the partial in TMEM, the rest in L2
+    } else if (MCP_CFG_K1GT && nch * 16 <= 512) {
       tm = 1;
       rb = (nch * 32 <= 512 && rb_g >= 32) ? 32 : 16;
       // 16 warps (column halves, 128 TMEM columns per thread) when RB = 32 and n <= 1024

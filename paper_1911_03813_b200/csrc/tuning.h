@@ -54,6 +54,10 @@
 // K1GT with 16 warps (column halves per warp, 128 TMEM columns per thread) for RB = 32 and
 // n <= 1024: measured 664 ms at c5 vs 643 ms with 8 warps (half the DMMA chains per warp, V
 // fragments loaded twice), so experiment builds only
+// K1GT at RB = 64 with chunks beyond TMEM's 256 columns per thread kept in L2 (n <= 1024)
+#ifndef MCP_CFG_K1GT_HALF
+#define MCP_CFG_K1GT_HALF 1
+#endif
 #ifndef MCP_CFG_K1GT_NW
 #define MCP_CFG_K1GT_NW 8
 #endif

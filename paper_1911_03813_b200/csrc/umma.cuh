@@ -138,8 +138,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // 32 (w % 4) + L; NC consecutive 32-bit columns move with one warp-collective instruction.
 template <int NC>
 __device__ __forceinline__ void tmem_ld_nowait(uint32_t taddr, uint32_t (&r)[NC]) {
-  static_assert(NC == 8 || NC == 16, "x8 / x16 only");
-  if constexpr (NC == 8) {
+  static_assert(NC == 8 || NC == 16 || NC == 32, "x8 / x16 / x32 only");
+  if constexpr (NC == 32) {
+    tmem_ld_nowait<16>(taddr, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+    tmem_ld_nowait<16>(taddr + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+  } else if constexpr (NC == 8) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
                    "=r"(r[6]), "=r"(r[7])
@@ -156,8 +159,11 @@ __device__ __forceinline__ void tmem_ld_nowait(uint32_t taddr, uint32_t (&r)[NC]
 }
 template <int NC>
 __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[NC]) {
-  static_assert(NC == 8 || NC == 16, "x8 / x16 only");
-  if constexpr (NC == 8) {
+  static_assert(NC == 8 || NC == 16 || NC == 32, "x8 / x16 / x32 only");
+  if constexpr (NC == 32) {
+    tmem_st<16>(taddr, *reinterpret_cast<const uint32_t(*)[16]>(&r[0]));
+    tmem_st<16>(taddr + 16, *reinterpret_cast<const uint32_t(*)[16]>(&r[16]));
+  } else if constexpr (NC == 8) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(
                      taddr),
                  "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),

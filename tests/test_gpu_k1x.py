@@ -75,12 +75,12 @@ def test_k1x_zero_lambda_exact():
 
 
 @pytest.mark.parametrize("n,p,r,d,dt,rb", [
-    (1024, 40_000, 256, 3, np.float32, 32),   # c5 shape: 8 column blocks of 32
-    (900, 20_000, 33, 4, np.float32, 32),     # ragged n and r (one full + one 1-column block)
-    (1024, 12_000, 64, 5, np.float64, 32),    # fp64 rows
+    (1024, 40_000, 256, 3, np.float32, 64),   # c5 shape: chunks 0-7 in TMEM, 8-15 in L2
+    (900, 20_000, 33, 4, np.float32, 64),     # ragged n and r (15 chunks: 8 TMEM + 7 L2)
+    (1024, 12_000, 64, 5, np.float64, 64),    # fp64 rows
     (2000, 6_000, 40, 3, np.float64, 16),     # 32 chunks: RB = 16 fills all 512 TMEM columns
-    (1024, 3_000, 256, 4, np.float32, 32),    # 47 tiles x 8 blocks < 2 units per SM: leftover ranges
-    (960, 9_500, 72, 3, np.float32, 32),      # 3 blocks: 49 groups + 1 leftover CTA
+    (1024, 1_500, 100, 4, np.float32, 64),    # 56 tiles x 2 blocks < 148 SMs: grid capped
+    (960, 9_500, 136, 3, np.float32, 64),     # 3 blocks: 49 groups + 1 leftover CTA
 ])
 def test_k1gt_tmem_partial_vs_oracle(n, p, r, d, dt, rb):
     """K1GT (K1G with the Y partial in TMEM): oracle parity, then bitwise determinism and exact

@@ -414,7 +414,8 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   const K1TPlan& t = pl.t;
   const int n = (int)c->n, r = pl.r;
   k_prep_at_tf32<<<grid_for((int64_t)t.r_pad * t.kpad, 256, 4 * c->sms), 256, 0, s>>>(
-      dx + r, n, r, t.r_pad, t.kpad, (float*)c->dAt.p);
+      dx + r, n, r, t.r_pad, t.kpad, (float*)c->dAt.p,
+      (t.insplit && MCP_K1T2_ASPLIT && t.serial) ? 1 : 0);
   K1TParams prm;
   prm.n = n;
   prm.r = r;

@@ -316,15 +316,18 @@ __global__ void __launch_bounds__(K1T_THREADS, 1)
 
 // Prepared factor operand for K1T: At[h][j][i] (h = 0 hi, 1 lo), fp32, zero padded to
 // r_pad rows and kpad = nkb*32 columns; the TF32 split of the fp32 rounding of A (fp64).
+// hi_full = 1 (K1T2 with the in-kernel split): the hi half holds the fp32 value itself -- the
+// tensor core reads it as its TF32 truncation, and the splitter warps form lo from it in shared
+// memory, so only the hi half is streamed.
 __global__ void k_prep_at_tf32(const double* __restrict__ A, int n, int r, int r_pad, int kpad,
-                               float* __restrict__ At) {
+                               float* __restrict__ At, int hi_full = 0) {
   const int64_t total = (int64_t)r_pad * kpad;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int j = idx / kpad, i = idx % kpad;
     const float a = (i < n && j < r) ? (float)A[(int64_t)j * n + i] : 0.0f;
     const float hi = tf32_hi(a);
-    At[idx] = hi;
+    At[idx] = hi_full ? a : hi;
     At[total + idx] = a - hi;
   }
 }
@@ -370,6 +373,9 @@ constexpr int K1T2_EPI_WARPS = 8;
 constexpr int K1T2_THREADS = (2 + K1T2_EPI_WARPS) * 32;
 constexpr int K1T2_SPLIT_WARPS = 4;                                   // prm.insplit
 constexpr int K1T2_THREADS_S = K1T2_THREADS + K1T2_SPLIT_WARPS * 32;
+#ifndef MCP_K1T2_ASPLIT
+#define MCP_K1T2_ASPLIT 0   // 1: the factor's lo rows formed in smem too (measured 5.21 vs 5.11 ms at c3: off)
+#endif
 #ifndef MCP_K1T2_KO
 #define MCP_K1T2_KO 0   // timing knockouts (see the producer), experiment builds only
 #endif
@@ -491,14 +497,16 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
           // V_lo loads, bit 1 = factor loaded for the first tile only, bit 2 = no GEMM2 loads
           const bool ko_lo = (MCP_K1T2_KO & 1) || prm.insplit;
           const bool ko_a = (MCP_K1T2_KO & 2) && q >= NS;
-          mbar_arrive_expect_tx(fb, (ko_lo ? 1 : 2) * K1T_VBYTES + (ko_a ? 0 : 256 * RB));
+          const bool a_lo =   // else formed in smem by the splitter warps
+              !ko_a && !(prm.insplit && prm.serial && MCP_K1T2_ASPLIT);
+          mbar_arrive_expect_tx(fb, (ko_lo ? 1 : 2) * K1T_VBYTES +
+                                        (ko_a ? 0 : a_lo ? 256 * RB : 128 * RB));
           load(st, &tm_v1, kb * 32, row0, fb, pol_keep);
           if (!ko_lo) load(st + K1T_VBYTES, &tm_l1, kb * 32, row0, fb, pol_keep);
-          if (!ko_a) {
-            tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, kb * 32, rb * RB, smem_u32(fb));
+          if (!ko_a) tma_load_2d(st + 2 * K1T_VBYTES, &tm_a, kb * 32, rb * RB, smem_u32(fb));
+          if (a_lo)
             tma_load_2d(st + 2 * K1T_VBYTES + 128 * RB, &tm_a, kb * 32, prm.r_pad + rb * RB,
                         smem_u32(fb));
-          }
         }
       };
       auto g2 = [&](int64_t v) {
@@ -703,10 +711,23 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
     // are 1 KB-aligned copies of one layout -- then release the stage to the MMA issuer
     const int st_id = (warp - 2 - K1T2_EPI_WARPS) * 32 + lane;   // 0..127
     const int64_t total = my_tiles * (int64_t)(nkb + 4 * mt2);
-    int s = 0;
+    const int per_tile = nkb + 4 * mt2;
+    int s = 0, in_tile = 0;
     uint32_t ph = 0;
     for (int64_t q = 0; q < total; ++q) {
       mbar_wait(&full[s], ph);
+      // GEMM1 stages (the first nkb of a tile in the serial order): the factor block's lo rows
+      // from its fp32 rows (MCP_K1T2_ASPLIT), same swizzle position RB rows further on
+      if (MCP_K1T2_ASPLIT && prm.serial && in_tile < nkb) {
+        const float4* ah = reinterpret_cast<const float4*>(base + s * SB + 2 * K1T_VBYTES);
+        float4* al = reinterpret_cast<float4*>(base + s * SB + 2 * K1T_VBYTES + 128 * RB);
+        for (int e = st_id; e < 8 * RB; e += 128) {
+          const float4 x = ah[e];
+          al[e] = make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z),
+                              x.w - tf32_hi(x.w));
+        }
+      }
+      if (++in_tile == per_tile) in_tile = 0;
       const float4* vh = reinterpret_cast<const float4*>(base + s * SB);
       float4* vl = reinterpret_cast<float4*>(base + s * SB + K1T_VBYTES);
       float4 x[K1T_VBYTES / 16 / 128];

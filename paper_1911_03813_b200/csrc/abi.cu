@@ -202,6 +202,9 @@ bool make_tmap_f32_chunks(CUtensorMap* m, void* gaddr, uint64_t ld, uint64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// an experiment build's forced column block disables the transient-m-tile widening
+static bool forced_rb_ok(int forced) { return !(forced >= 16 && forced <= 64); }
+
 int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   K1TPlan& t = pl.t;
   const int64_t n = c->n;
@@ -239,9 +242,20 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   // The split pays where the UMMAs are compute-bound enough to spare shared-memory bandwidth:
   // measured c3 (RB = 64: N = 128 / 64 products) 5.46 -> 5.11 ms, c5 (RB = 48: N = 96 / 48)
   // 220 -> 238 ms -- so only when K1T2's column block is 64 (same formula as below).
+  // transient GEMM2 m-tiles (serial order, zcat): tr m-tiles accumulate in Z's 2 RB columns,
+  // so RB fits when 2 RB + (mt2 - tr) RB <= 512 with tr RB <= 2 RB
+  auto transient_tr = [&](int rbv) -> int {
+    if (!MCP_CFG_K1T2_TRANSIENT || !MCP_CFG_K1T2_SERIAL || !MCP_CFG_K1T_ZCAT || 2 * rbv > 256)
+      return 0;
+    for (int tr = 1; tr <= 2 && tr <= t.mt2; ++tr)
+      if (2 * rbv + (t.mt2 - tr) * rbv <= 512) return tr;
+    return 0;
+  };
   const int rb_v2 = [&] {
-    int rbv = (int)std::min<int64_t>(64, round_up(r, 16));
+    const int want = (int)std::min<int64_t>(64, round_up(r, 16));
+    int rbv = want;
     while (rbv > 16 && ((MCP_CFG_K1T2_SERIAL ? 1 : 2) + t.mt2) * rbv > 512) rbv -= 16;
+    if (rbv < want && transient_tr(want) > 0) rbv = want;
     return rbv;
   }();
   t.v2 = false;
@@ -303,15 +317,26 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     if (forced >= 16 && forced <= 64 && forced % 16 == 0 && (zbufs + t.mt2) * forced <= 512)
       RB = forced;
   }
+  // transient m-tiles when they widen the column block (c5: 48 -> 64, four blocks instead of six)
+  t.mt_tr = 0;
+  if (!v1 && t.serial && forced_rb_ok(MCP_CFG_K1T2_RB)) {
+    const int want = (int)std::min<int64_t>(64, round_up(r, 16));
+    const int tr = transient_tr(want);
+    if (want > RB && tr > 0) {
+      RB = want;
+      t.mt_tr = tr;
+    }
+  }
   // K1T2 with the concatenated GEMM1 when TMEM has room for two 2 RB-wide Z buffers
   t.zcat = !v1 && MCP_CFG_K1T_ZCAT && 2 * RB <= 256 && (2 * zbufs + t.mt2) * RB <= 512;
-  if ((zbufs + t.mt2) * RB > 512)
+  if (t.mt_tr) t.zcat = true;   // transient m-tiles live in the concatenated Z's columns
+  if ((zbufs + t.mt2 - t.mt_tr) * RB > 512)
     return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
   // GEMM2 m-tiles that get a second RB-column accumulator half from the spare TMEM columns
   t.wide = 0;
   if (!v1 && MCP_CFG_K1T2_WIDE != 0) {
     const int zw = t.zcat ? 2 * RB : RB;
-    const int spare = 512 - zbufs * zw - t.mt2 * RB;
+    const int spare = 512 - zbufs * zw - (t.mt2 - t.mt_tr) * RB;
     t.wide = std::max(0, std::min(t.mt2, spare / RB));
   }
   t.RB = RB;
@@ -343,7 +368,10 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
     c->tm_a_kpad = t.kpad;
     c->tm_a_rb = RB;
   }
-  if (!ensure_dyn_smem(t.v2 ? (const void*)k1t2_fg_tf32 : (const void*)k1t_fg_tf32, t.smem))
+  if (!ensure_dyn_smem(!t.v2        ? (const void*)k1t_fg_tf32
+                       : t.mt_tr ? (const void*)k1t2_fg_tf32<true>
+                                 : (const void*)k1t2_fg_tf32<false>,
+                       t.smem))
     return c->fail(MCP_ERR_CUDA, "cudaFuncSetAttribute failed for the tf32x3 kernel");
   pl.k1 = K1Variant();
   pl.k1.kind = 2;
@@ -357,7 +385,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
                 std::to_string(RB) + ",S=" + std::to_string(ns) +
                 (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
-                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + (t.insplit ? ",insplit" : "") + ",flush=" + std::to_string(t.flush)
+                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + (t.insplit ? ",insplit" : "") + (t.mt_tr ? ",transient=" + std::to_string(t.mt_tr) : std::string()) + ",flush=" + std::to_string(t.flush)
                       : std::string()) +
                 ">";
   return MCP_OK;
@@ -438,12 +466,13 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.g2_3d = t.g2_3d ? 1 : 0;
   prm.wide = t.wide;
   prm.insplit = t.insplit ? 1 : 0;
+  prm.mt_tr = t.mt_tr;
   // opt-in: GEMM2 as V P_hi with P_hi rounded to nearest (8-9% faster at c3 / c5, but normwise
   // error up to 7e-5 at reduced p -- too close to the stated 1e-4 to be the default)
   prm.g2x2 = MCP_CFG_K1T2_G2X2 ? 1 : 0;
   auto* ev = timing_begin(c, s);
   if (t.v2)
-    k1t2_fg_tf32<<<t.gp * t.rbs, t.insplit ? K1T2_THREADS_S : K1T2_THREADS, t.smem, s>>>(
+    (t.mt_tr ? k1t2_fg_tf32<true> : k1t2_fg_tf32<false>)<<<t.gp * t.rbs, t.insplit ? K1T2_THREADS_S : K1T2_THREADS, t.smem, s>>>(
         c->tm_v1, t.g2_3d ? c->tm_v3 : c->tm_v2, t.insplit ? c->tm_v1 : c->tm_l1,
         t.insplit ? (t.g2_3d ? c->tm_v3 : c->tm_v2) : (t.g2_3d ? c->tm_l3 : c->tm_l2), c->tm_a,
         prm);

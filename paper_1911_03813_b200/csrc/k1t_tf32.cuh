@@ -58,6 +58,10 @@ struct K1TParams {
   int g2_3d = 0;      // K1T2: tm_v2 / tm_l2 are 3-D chunk maps (one TMA per 16 KB operand)
   int g2x2 = 0;       // K1T2: GEMM2 as V P_hi (2 products) with P_hi rounded to nearest; the
                       // dropped V_hi P_lo term is unbiased and <= 2^-12 of each product
+  int mt_tr = 0;      // K1T2 (serial, zcat): the last mt_tr GEMM2 m-tiles accumulate in the Z
+                      // columns (free once the epilogue has read Z), run first in GEMM2's order
+                      // and drain into the fp64 partial every tile -- RB = 64 where the
+                      // persistent Y would not fit TMEM (c5: 128 + 6 x 64 = 512 columns)
   int insplit = 0;    // K1T2: V_lo = V - tf32(V) formed in shared memory by 4 splitter warps
                       // from the one TMA'd fp32 stage (no V_lo copy in HBM, DRAM ~1x V)
   int wide = 0;       // K1T2: GEMM2 m-tiles [0, wide) run V_hi [P_hi | P_lo] as ONE N = 2 RB
@@ -390,6 +394,9 @@ constexpr int K1T2_THREADS_S = K1T2_THREADS + K1T2_SPLIT_WARPS * 32;
 #define K1T2_ACC(v)
 #endif
 
+// TR: the kernel handles transient m-tiles (prm.mt_tr > 0); the TR = false instance compiles that
+// logic away (the single MMA-issuing thread's per-step work measured 4% at c3 otherwise)
+template <bool TR>
 __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
     k1t2_fg_tf32(const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_v2,
                  const __grid_constant__ CUtensorMap tm_l1, const __grid_constant__ CUtensorMap tm_l2,
@@ -411,6 +418,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
   uint64_t* y_empty = z_full + 5;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(z_full + 6);
   uint64_t* split = z_full + 8;         // [NS], prm.insplit: V_lo of the stage is formed
+  uint64_t* yt_full = z_full + 16;      // prm.mt_tr: this tile's transient m-tiles are complete
+  uint64_t* yt_empty = z_full + 17;     //            ... and read out of TMEM
   // the MMA consumes a stage once its data is complete: TMA bytes (full) or, with the in-kernel
   // split, the splitter warps' V_lo as well (split)
   uint64_t* ready = prm.insplit ? split : full;
@@ -421,6 +430,9 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
   const int64_t my_tiles =
       pg < prm.num_tiles ? (prm.num_tiles - pg + prm.gp - 1) / prm.gp : 0;
   const int mt2 = prm.mt2, nkb = prm.nkb;
+  const int mtr = TR ? prm.mt_tr : 0, mt_p = mt2 - mtr;   // transient / persistent m-tiles
+  // GEMM2 m-tile of step group i: the transient m-tiles [mt_p, mt2) first
+  auto g2_mt = [&](int i) -> int { return i < mtr ? mt_p + i : i - mtr; };
   auto flush_after = [&](int64_t v) {   // tile v ends a group of prm.flush tiles (or the last)
     return (v % prm.flush) == prm.flush - 1 || v == my_tiles - 1;
   };
@@ -439,6 +451,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
     mbar_init(p_empty, 1);
     mbar_init(y_full, 1);
     mbar_init(y_empty, K1T2_EPI_WARPS);
+    mbar_init(yt_full, 1);
+    mbar_init(yt_empty, K1T2_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc<512>(smem_u32(tslot));
@@ -459,6 +473,10 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
   const uint32_t ty = tmem + (prm.serial ? 1 : 2) * ZW;
   auto ycol = [&](int mt) -> uint32_t {
     return (uint32_t)(mt < prm.wide ? 2 * RB * mt : 2 * RB * prm.wide + RB * (mt - prm.wide));
+  };
+  // accumulator of GEMM2 m-tile mt: persistent Y after the Z buffer, transient in Z's columns
+  auto ydst = [&](int mt) -> uint32_t {
+    return mt >= mt_p ? tmem + (uint32_t)(RB * (mt - mt_p)) : ty + ycol(mt);
   };
 
   if (warp == 0) {
@@ -512,7 +530,7 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
       auto g2 = [&](int64_t v) {
         const int row0 = (int)((pg + v * prm.gp) * K1T_TP);
         for (int step = 0; step < 4 * mt2; ++step, ++q) {
-          const int mt = step >> 2, rc = step & 3;
+          const int mt = g2_mt(step >> 2), rc = step & 3;
           unsigned char* st = stage(q);
           uint64_t* fb = &full[q % NS];
           if (MCP_K1T2_KO & 4) {
@@ -571,6 +589,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
       auto g1 = [&](int64_t u) {
           // ---- GEMM1(u): Z[zb] = V A (3xTF32) ----
           const uint32_t tz = tmem + (uint32_t)(zbuf(u) * ZW);
+          // Z's columns held tile u - 1's transient m-tiles: wait until they are read out
+          if (mtr && u >= 1) mbar_wait(yt_empty, (uint32_t)(u - 1) & 1);
           for (int kb = 0; kb < nkb; ++kb, ++q) {
             const int s = (int)(q % NS);
             {
@@ -626,7 +646,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
           const uint64_t dph = umma_desc_sw128(smem_u32(sP2), 16, 1024);
           const uint64_t dpl = dph + ((128 * RB) >> 4);
           for (int step = 0; step < 4 * mt2; ++step, ++q) {
-            const int mt = step >> 2, rc = step & 3;
+            const int mt = g2_mt(step >> 2), rc = step & 3;
+            const bool fr = mt >= mt_p || fresh;   // transient m-tiles start fresh every tile
             const int s = (int)(q % NS);
             {
               K1T2_T0();
@@ -641,12 +662,12 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
               // [V_hi P_hi | V_hi P_lo] in one N = 2 RB product, then V_lo P_hi into the first half
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks)
-                umma_tf32(ty + ycol(mt), dvh + 64 * ks, dph + boff + 2 * ks, id2w,
-                          (fresh && rc == 0 && ks == 0) ? 0u : 1u);
+                umma_tf32(ydst(mt), dvh + 64 * ks, dph + boff + 2 * ks, id2w,
+                          (fr && rc == 0 && ks == 0) ? 0u : 1u);
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks)
                 if (!(MCP_K1T2_KO & 8))
-                  umma_tf32(ty + ycol(mt), dvl + 64 * ks, dph + boff + 2 * ks, id2, 1u);
+                  umma_tf32(ydst(mt), dvl + 64 * ks, dph + boff + 2 * ks, id2, 1u);
             } else {
 #pragma unroll
               for (int pr = 0; pr < 3; ++pr) {
@@ -656,11 +677,12 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
                 const uint64_t bv = (pr == 1 ? dpl : dph) + boff;
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks)
-                  umma_tf32(ty + ycol(mt), av + 64 * ks, bv + 2 * ks, id2,
-                            (fresh && rc == 0 && pr == 0 && ks == 0) ? 0u : 1u);
+                  umma_tf32(ydst(mt), av + 64 * ks, bv + 2 * ks, id2,
+                            (fr && rc == 0 && pr == 0 && ks == 0) ? 0u : 1u);
               }
             }
             umma_commit(smem_u32(&empty[s]));
+            if (mtr && step == 4 * mtr - 1) umma_commit(smem_u32(yt_full));
           }
           fresh = false;
           umma_commit(smem_u32(p_empty));
@@ -762,7 +784,7 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
       K1T2_T0();
       mbar_wait(y_full, (uint32_t)flushes & 1);
       tc_fence_after();
-      for (int mt = 0; mt < mt2; ++mt) {
+      for (int mt = 0; mt < mt_p; ++mt) {   // persistent m-tiles (transient ones drain per tile)
         double* yrow = Yp + ((size_t)mt * 128 + l) * RB;
         for (int c0 = half * hc; col_active && c0 < c_end; c0 += 16) {
           float yv[16], y2[16];
@@ -840,6 +862,35 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (mtr) {
+        // this tile's transient m-tiles (GEMM2 runs them first): 16 columns at a time out of
+        // TMEM into the fp64 partial (one owner per element, in order; fire-and-forget REDs
+        // keep the registers low -- 4 warps per sub-partition cap them at 128), then Z's
+        // columns go back to GEMM1(u + 1)
+        mbar_wait(yt_full, (uint32_t)u & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c0 = half * hc + 16 * h;
+            if (i < mtr && col_active && c0 < c_end) {
+              float tv[16];
+              tmem_ld16(tmem + (uint32_t)(RB * i) + ((uint32_t)(32 * sp) << 16) + c0, tv);
+              double* yrow = Yp + ((size_t)(mt_p + i) * 128 + l) * RB;
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) {
+                if (u == 0)
+                  yrow[c0 + jj] = (double)tv[jj];
+                else
+                  atomicAdd(yrow + c0 + jj, (double)tv[jj]);   // fire-and-forget RED
+              }
+            }
+          }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(yt_empty);
+      }
       if (!prm.serial && u >= 1 && flush_after(u - 1)) flush();   // committed after GEMM2(u - 1)
     }
     if (my_tiles > 0) flush();                      // the group ending at the last tile

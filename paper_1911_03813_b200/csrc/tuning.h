@@ -76,6 +76,11 @@
 #ifndef MCP_CFG_K1T2_INSPLIT
 #define MCP_CFG_K1T2_INSPLIT 1
 #endif
+// fast mode: up to two GEMM2 m-tiles accumulate in Z's TMEM columns and drain every tile, so
+// the column block can stay 64 where the persistent Y would not fit (c5)
+#ifndef MCP_CFG_K1T2_TRANSIENT
+#define MCP_CFG_K1T2_TRANSIENT 1
+#endif
 #ifndef MCP_CFG_K1T2_SERIAL
 #define MCP_CFG_K1T2_SERIAL 1
 #endif

@@ -330,6 +330,17 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   // K1T2 with the concatenated GEMM1 when TMEM has room for two 2 RB-wide Z buffers
   t.zcat = !v1 && MCP_CFG_K1T_ZCAT && 2 * RB <= 256 && (2 * zbufs + t.mt2) * RB <= 512;
   if (t.mt_tr) t.zcat = true;   // transient m-tiles live in the concatenated Z's columns
+  // every GEMM2 m-tile wide when one wide transient m-tile in Z's columns makes room for the
+  // rest: 2 RB + (mt2 - 1) 2 RB <= 512 (c3: 4 m-tiles at RB = 64)
+  t.tr_wide = false;
+  if (!v1 && t.serial && t.zcat && !t.mt_tr && MCP_CFG_K1T2_TRANSIENT && MCP_CFG_K1T2_WIDE &&
+      MCP_CFG_K1T2_TRWIDE && t.mt2 >= 2 && 2 * RB + (t.mt2 - 1) * 2 * RB <= 512) {
+    const int spare_now = 512 - 2 * RB - t.mt2 * RB;
+    if (spare_now / RB < t.mt2) {   // not all wide today
+      t.mt_tr = 1;
+      t.tr_wide = true;
+    }
+  }
   if ((zbufs + t.mt2 - t.mt_tr) * RB > 512)
     return c->fail(MCP_ERR_ARG, "n = " + std::to_string(n) + " exceeds the tf32x3 kernel limit");
   // GEMM2 m-tiles that get a second RB-column accumulator half from the spare TMEM columns
@@ -337,7 +348,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   if (!v1 && MCP_CFG_K1T2_WIDE != 0) {
     const int zw = t.zcat ? 2 * RB : RB;
     const int spare = 512 - zbufs * zw - (t.mt2 - t.mt_tr) * RB;
-    t.wide = std::max(0, std::min(t.mt2, spare / RB));
+    t.wide = std::max(0, std::min(t.mt2 - t.mt_tr, spare / RB));
   }
   t.RB = RB;
   t.rbs = (int)ceil_div(r, RB);
@@ -385,7 +396,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
                 std::to_string(RB) + ",S=" + std::to_string(ns) +
                 (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
-                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + (t.insplit ? ",insplit" : "") + (t.mt_tr ? ",transient=" + std::to_string(t.mt_tr) : std::string()) + ",flush=" + std::to_string(t.flush)
+                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + (t.insplit ? ",insplit" : "") + (t.mt_tr ? ",transient=" + std::to_string(t.mt_tr) + (t.tr_wide ? "w" : "") : std::string()) + ",flush=" + std::to_string(t.flush)
                       : std::string()) +
                 ">";
   return MCP_OK;
@@ -467,6 +478,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.wide = t.wide;
   prm.insplit = t.insplit ? 1 : 0;
   prm.mt_tr = t.mt_tr;
+  prm.tr_wide = t.tr_wide ? 1 : 0;
   // opt-in: GEMM2 as V P_hi with P_hi rounded to nearest (8-9% faster at c3 / c5, but normwise
   // error up to 7e-5 at reduced p -- too close to the stated 1e-4 to be the default)
   prm.g2x2 = MCP_CFG_K1T2_G2X2 ? 1 : 0;

@@ -117,6 +117,7 @@ struct K1TPlan {
   int wide = 0;         // K1T2 GEMM2 m-tiles with the N = 2 RB [P_hi | P_lo] product
   bool insplit = false; // K1T2 V_lo formed in shared memory (no V_lo copy in HBM)
   int mt_tr = 0;        // K1T2 transient GEMM2 m-tiles (accumulate in Z's columns)
+  bool tr_wide = false; // K1T2: the transient m-tile is wide (all m-tiles wide at c3)
   int64_t num_tiles = 0;
   size_t smem = 0;
 };

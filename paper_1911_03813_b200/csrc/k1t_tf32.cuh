@@ -58,6 +58,8 @@ struct K1TParams {
   int g2_3d = 0;      // K1T2: tm_v2 / tm_l2 are 3-D chunk maps (one TMA per 16 KB operand)
   int g2x2 = 0;       // K1T2: GEMM2 as V P_hi (2 products) with P_hi rounded to nearest; the
                       // dropped V_hi P_lo term is unbiased and <= 2^-12 of each product
+  int tr_wide = 0;    // K1T2: the (single) transient m-tile is wide (2 RB columns = all of Z):
+                      // c3 runs every GEMM2 m-tile as the N = 2 RB [P_hi | P_lo] product
   int mt_tr = 0;      // K1T2 (serial, zcat): the last mt_tr GEMM2 m-tiles accumulate in the Z
                       // columns (free once the epilogue has read Z), run first in GEMM2's order
                       // and drain into the fp64 partial every tile -- RB = 64 where the
@@ -478,6 +480,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
   auto ydst = [&](int mt) -> uint32_t {
     return mt >= mt_p ? tmem + (uint32_t)(RB * (mt - mt_p)) : ty + ycol(mt);
   };
+  // m-tiles with the N = 2 RB product: the first prm.wide persistent ones, a wide transient one
+  auto is_wide = [&](int mt) -> bool { return mt < prm.wide || (TR && mt >= mt_p && prm.tr_wide); };
 
   if (warp == 0) {
     // =========================== TMA producer (same order as the MMA issuer) ===========================
@@ -658,7 +662,7 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
             const uint64_t dvh = umma_desc_sw128_32b(smem_u32(base + s * SB), 4096, 512);
             const uint64_t dvl = dvh + (K1T_VBYTES >> 4);
             const uint64_t boff = (uint64_t)((rc * 256 * RB) >> 4);
-            if (mt < prm.wide) {
+            if (is_wide(mt)) {
               // [V_hi P_hi | V_hi P_lo] in one N = 2 RB product, then V_lo P_hi into the first half
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks)
@@ -877,6 +881,20 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
             if (i < mtr && col_active && c0 < c_end) {
               float tv[16];
               tmem_ld16(tmem + (uint32_t)(RB * i) + ((uint32_t)(32 * sp) << 16) + c0, tv);
+              if (prm.tr_wide) {   // the wide m-tile's second half (V_hi P_lo)
+                float t2[16];
+                tmem_ld16(tmem + (uint32_t)RB + ((uint32_t)(32 * sp) << 16) + c0, t2);
+                double* yrow = Yp + ((size_t)(mt_p + i) * 128 + l) * RB;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  const double yd = (double)tv[jj] + (double)t2[jj];
+                  if (u == 0)
+                    yrow[c0 + jj] = yd;
+                  else
+                    atomicAdd(yrow + c0 + jj, yd);
+                }
+                continue;
+              }
               double* yrow = Yp + ((size_t)(mt_p + i) * 128 + l) * RB;
 #pragma unroll
               for (int jj = 0; jj < 16; ++jj) {

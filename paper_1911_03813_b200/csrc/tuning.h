@@ -81,6 +81,11 @@
 #ifndef MCP_CFG_K1T2_TRANSIENT
 #define MCP_CFG_K1T2_TRANSIENT 1
 #endif
+#ifndef MCP_CFG_K1T2_TRWIDE
+// one wide transient m-tile so every GEMM2 m-tile is wide (c3): measured 5.77 vs 5.09 ms (the
+// per-tile drain of 2 x 64 columns through L2 atomics costs more than the wide products save)
+#define MCP_CFG_K1T2_TRWIDE 0
+#endif
 #ifndef MCP_CFG_K1T2_SERIAL
 #define MCP_CFG_K1T2_SERIAL 1
 #endif

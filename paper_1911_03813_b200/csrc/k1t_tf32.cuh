@@ -382,6 +382,10 @@ constexpr int K1T2_THREADS_S = K1T2_THREADS + K1T2_SPLIT_WARPS * 32;
 #ifndef MCP_K1T2_ASPLIT
 #define MCP_K1T2_ASPLIT 0   // 1: the factor's lo rows formed in smem too (measured 5.21 vs 5.11 ms at c3: off)
 #endif
+#ifndef MCP_K1T2_DRAIN_RMW
+#define MCP_K1T2_DRAIN_RMW 0   // 1: transient drain as owner read-modify-write (c5: 188.6-190 ms
+                               // vs 185.2-185.4 with RED atomics)
+#endif
 #ifndef MCP_K1T2_KO
 #define MCP_K1T2_KO 0   // timing knockouts (see the producer), experiment builds only
 #endif
@@ -870,7 +874,9 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
         // this tile's transient m-tiles (GEMM2 runs them first): 16 columns at a time out of
         // TMEM into the fp64 partial (one owner per element, in order; fire-and-forget REDs
         // keep the registers low -- 4 warps per sub-partition cap them at 128), then Z's
-        // columns go back to GEMM1(u + 1)
+        // columns go back to GEMM1(u + 1).  The drain costs ~13% at c5 (a no-drain timing
+        // knockout: 160.6 vs 185.2 ms); reading every value out of TMEM before the release
+        // (188.2 ms, spills) and owner read-modify-writes instead of REDs (188.6 ms) lost.
         mbar_wait(yt_full, (uint32_t)u & 1);
         tc_fence_after();
 #pragma unroll
@@ -881,6 +887,7 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
             if (i < mtr && col_active && c0 < c_end) {
               float tv[16];
               tmem_ld16(tmem + (uint32_t)(RB * i) + ((uint32_t)(32 * sp) << 16) + c0, tv);
+              if (MCP_K1T2_KO & 16) continue;   // knockout: no drain (timing only)
               if (prm.tr_wide) {   // the wide m-tile's second half (V_hi P_lo)
                 float t2[16];
                 tmem_ld16(tmem + (uint32_t)RB + ((uint32_t)(32 * sp) << 16) + c0, t2);
@@ -896,12 +903,24 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
                 continue;
               }
               double* yrow = Yp + ((size_t)(mt_p + i) * 128 + l) * RB;
+              if (MCP_K1T2_DRAIN_RMW && u != 0) {
+                // owner-thread read-modify-write: 8 x 16-byte loads in flight, then the stores
+                double2* y2p = reinterpret_cast<double2*>(yrow + c0);
+                double2 cur[8];
 #pragma unroll
-              for (int jj = 0; jj < 16; ++jj) {
-                if (u == 0)
-                  yrow[c0 + jj] = (double)tv[jj];
-                else
-                  atomicAdd(yrow + c0 + jj, (double)tv[jj]);   // fire-and-forget RED
+                for (int jj = 0; jj < 8; ++jj) cur[jj] = y2p[jj];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj)
+                  y2p[jj] = make_double2(cur[jj].x + (double)tv[2 * jj],
+                                         cur[jj].y + (double)tv[2 * jj + 1]);
+              } else {
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  if (u == 0)
+                    yrow[c0 + jj] = (double)tv[jj];
+                  else
+                    atomicAdd(yrow + c0 + jj, (double)tv[jj]);   // fire-and-forget RED
+                }
               }
             }
           }

@@ -160,7 +160,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 // 2-D fp64 tensor map (K53's V tiles): inner dim (contiguous) x outer dim, row pitch in bytes.
 bool make_tmap_f64(CUtensorMap* m, const void* gaddr, uint64_t inner, uint64_t outer,
-                   uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+                   uint64_t pitch, uint32_t box_inner, uint32_t box_outer,
+                   CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = tmap_encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -168,7 +169,7 @@ bool make_tmap_f64(CUtensorMap* m, const void* gaddr, uint64_t inner, uint64_t o
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(gaddr), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -355,11 +356,12 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   t.r_pad = t.rbs * RB;
   t.kpad = t.nkb * 32;
   const size_t budget = 227 * 1024;
-  int ns = (int)((budget - k1t_smem_bytes(RB, 0)) / k1t_stage_bytes(RB));
+  const bool drain_tma = t.mt_tr && MCP_K1T2_DRAIN_TMA;
+  int ns = (int)((budget - k1t_smem_bytes(RB, 0, drain_tma)) / k1t_stage_bytes(RB));
   if (ns > 8) ns = 8;
   if (ns < 2) return c->fail(MCP_ERR_ARG, "tf32x3 stage ring does not fit");
   t.stages = ns;
-  t.smem = k1t_smem_bytes(RB, ns);
+  t.smem = k1t_smem_bytes(RB, ns, drain_tma);
   t.num_tiles = c->p_pad / K1T_TP;
   int64_t G = c->sms;
   if (G < t.rbs) G = t.rbs;
@@ -478,6 +480,18 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   prm.wide = t.wide;
   prm.insplit = t.insplit ? 1 : 0;
   prm.mt_tr = t.mt_tr;
+  // the transient drain's bulk tensor reduce-add target: the fp64 partial as rows of RB
+  CUtensorMap tm_y;
+  prm.drain_tma = 0;
+  if (t.mt_tr && MCP_K1T2_DRAIN_TMA) {
+    if (!make_tmap_f64(&tm_y, c->dYpart.p, (uint64_t)t.RB,
+                       (uint64_t)t.rbs * t.gp * t.mt2 * 128, 8 * (uint64_t)t.RB, 8, 32,
+                       CU_TENSOR_MAP_SWIZZLE_NONE))
+      return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fast-mode partial");
+    prm.drain_tma = 1;
+  } else {
+    tm_y = c->tm_a;   // unused
+  }
   prm.tr_wide = t.tr_wide ? 1 : 0;
   // opt-in: GEMM2 as V P_hi with P_hi rounded to nearest (8-9% faster at c3 / c5, but normwise
   // error up to 7e-5 at reduced p -- too close to the stated 1e-4 to be the default)
@@ -487,7 +501,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
     (t.mt_tr ? k1t2_fg_tf32<true> : k1t2_fg_tf32<false>)<<<t.gp * t.rbs, t.insplit ? K1T2_THREADS_S : K1T2_THREADS, t.smem, s>>>(
         c->tm_v1, t.g2_3d ? c->tm_v3 : c->tm_v2, t.insplit ? c->tm_v1 : c->tm_l1,
         t.insplit ? (t.g2_3d ? c->tm_v3 : c->tm_v2) : (t.g2_3d ? c->tm_l3 : c->tm_l2), c->tm_a,
-        prm);
+        tm_y, prm);
   else
     k1t_fg_tf32<<<t.gp * t.rbs, K1T_THREADS, t.smem, s>>>(c->tm_v1, c->tm_v2, c->tm_a, prm);
   timing_end(ev, s);

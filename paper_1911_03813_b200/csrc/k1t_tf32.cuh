@@ -58,6 +58,8 @@ struct K1TParams {
   int g2_3d = 0;      // K1T2: tm_v2 / tm_l2 are 3-D chunk maps (one TMA per 16 KB operand)
   int g2x2 = 0;       // K1T2: GEMM2 as V P_hi (2 products) with P_hi rounded to nearest; the
                       // dropped V_hi P_lo term is unbiased and <= 2^-12 of each product
+  int drain_tma = 0;  // K1T2: transient m-tiles drain by bulk tensor reduce-add (TMA) from a
+                      // 2 KB staging slot per epilogue warp instead of per-element REDs
   int tr_wide = 0;    // K1T2: the (single) transient m-tile is wide (2 RB columns = all of Z):
                       // c3 runs every GEMM2 m-tile as the N = 2 RB [P_hi | P_lo] product
   int mt_tr = 0;      // K1T2 (serial, zcat): the last mt_tr GEMM2 m-tiles accumulate in the Z
@@ -71,9 +73,9 @@ struct K1TParams {
 };
 
 __host__ __device__ constexpr size_t k1t_stage_bytes(int RB) { return 2 * K1T_VBYTES + 256 * RB; }
-__host__ __device__ constexpr size_t k1t_smem_bytes(int RB, int stages) {
+__host__ __device__ constexpr size_t k1t_smem_bytes(int RB, int stages, bool drain_tma = false) {
   return 1024 /*align slack*/ + stages * k1t_stage_bytes(RB) + 1024 * (size_t)RB /*P hi+lo*/ +
-         1024 /*barriers*/;
+         1024 /*barriers*/ + (drain_tma ? 8 * 2048 : 0) /*K1T2 drain staging*/;
 }
 
 __global__ void __launch_bounds__(K1T_THREADS, 1)
@@ -375,12 +377,31 @@ __global__ void k_f64_to_f32(const double* __restrict__ src, float* __restrict__
 // Roles: warp 0 TMA producer, warp 1 MMA issuer + TMEM owner, warps 2..9 epilogue / flush (two
 // per TMEM sub-partition, each on half of the columns).  TMEM: Z (one or two buffers, 2 RB
 // columns each with zcat), then Y[mt]: (zbufs * ZW / RB + n/128) RB <= 512 columns.
+// bulk tensor reduce-add (TMA, performed at L2) of a shared-memory box into global memory
+__device__ __forceinline__ void k1t_bulk_reduce_add_2d(const CUtensorMap* tm, int c0, int c1,
+                                                       const void* src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n"
+      "cp.async.bulk.commit_group;\n" ::"l"(tm),
+      "r"(c0), "r"(c1), "r"((uint32_t)__cvta_generic_to_shared(src))
+      : "memory");
+}
+__device__ __forceinline__ void k1t_bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void k1t_bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 constexpr int K1T2_EPI_WARPS = 8;
 constexpr int K1T2_THREADS = (2 + K1T2_EPI_WARPS) * 32;
 constexpr int K1T2_SPLIT_WARPS = 4;                                   // prm.insplit
 constexpr int K1T2_THREADS_S = K1T2_THREADS + K1T2_SPLIT_WARPS * 32;
 #ifndef MCP_K1T2_ASPLIT
 #define MCP_K1T2_ASPLIT 0   // 1: the factor's lo rows formed in smem too (measured 5.21 vs 5.11 ms at c3: off)
+#endif
+#ifndef MCP_K1T2_DRAIN_TMA
+#define MCP_K1T2_DRAIN_TMA 1   // transient drain by bulk tensor reduce-add (0: per-element REDs)
 #endif
 #ifndef MCP_K1T2_DRAIN_RMW
 #define MCP_K1T2_DRAIN_RMW 0   // 1: transient drain as owner read-modify-write (c5: 188.6-190 ms
@@ -406,7 +427,8 @@ template <bool TR>
 __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
     k1t2_fg_tf32(const __grid_constant__ CUtensorMap tm_v1, const __grid_constant__ CUtensorMap tm_v2,
                  const __grid_constant__ CUtensorMap tm_l1, const __grid_constant__ CUtensorMap tm_l2,
-                 const __grid_constant__ CUtensorMap tm_a, K1TParams prm) {
+                 const __grid_constant__ CUtensorMap tm_a,
+                 const __grid_constant__ CUtensorMap tm_y, K1TParams prm) {
   extern __shared__ __align__(16) unsigned char smem_raw_t2[];
   unsigned char* base = smem_raw_t2 + ((1024u - (smem_u32(smem_raw_t2) & 1023u)) & 1023u);
   const int RB = prm.RB, NS = prm.stages;
@@ -426,6 +448,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
   uint64_t* split = z_full + 8;         // [NS], prm.insplit: V_lo of the stage is formed
   uint64_t* yt_full = z_full + 16;      // prm.mt_tr: this tile's transient m-tiles are complete
   uint64_t* yt_empty = z_full + 17;     //            ... and read out of TMEM
+  // prm.drain_tma: one 2 KB staging slot (32 rows x 8 doubles) per epilogue warp
+  double* drain_stage = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(bars) + 1024);
   // the MMA consumes a stage once its data is complete: TMA bytes (full) or, with the in-kernel
   // split, the splitter warps' V_lo as well (split)
   uint64_t* ready = prm.insplit ? split : full;
@@ -879,6 +903,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
         // (188.2 ms, spills) and owner read-modify-writes instead of REDs (188.6 ms) lost.
         mbar_wait(yt_full, (uint32_t)u & 1);
         tc_fence_after();
+        // the previous tile's reduce-adds to these rows have completed (fixed add order)
+        if (TR && prm.drain_tma && u != 0 && lane == 0) k1t_bulk_wait_all();
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -888,6 +914,33 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
               float tv[16];
               tmem_ld16(tmem + (uint32_t)(RB * i) + ((uint32_t)(32 * sp) << 16) + c0, tv);
               if (MCP_K1T2_KO & 16) continue;   // knockout: no drain (timing only)
+              if (TR && prm.drain_tma && u != 0) {
+                // two 8-column bulk reduce-adds of this warp's 32 rows through its staging slot
+                // (a wide m-tile's halves summed first, in the flush's order)
+                float t2[16];
+                if (prm.tr_wide)
+                  tmem_ld16(tmem + (uint32_t)RB + ((uint32_t)(32 * sp) << 16) + c0, t2);
+                double* stg = drain_stage + (size_t)ew * 256;   // [32 rows][8]
+                const int grow = (int)((((size_t)rb * prm.gp + pg) * mt2 + (mt_p + i)) * 128 +
+                                       32 * sp);
+#pragma unroll
+                for (int k8 = 0; k8 < 2; ++k8) {
+                  if (lane == 0) k1t_bulk_wait_read();   // the slot's previous reduce read it
+                  __syncwarp();
+#pragma unroll
+                  for (int jj = 0; jj < 4; ++jj) {
+                    const int a = 8 * k8 + 2 * jj;
+                    const double v0 = prm.tr_wide ? (double)tv[a] + (double)t2[a] : (double)tv[a];
+                    const double v1 =
+                        prm.tr_wide ? (double)tv[a + 1] + (double)t2[a + 1] : (double)tv[a + 1];
+                    reinterpret_cast<double2*>(stg + 8 * lane)[jj] = make_double2(v0, v1);
+                  }
+                  fence_async_smem();
+                  __syncwarp();
+                  if (lane == 0) k1t_bulk_reduce_add_2d(&tm_y, c0 + 8 * k8, grow, stg);
+                }
+                continue;
+              }
               if (prm.tr_wide) {   // the wide m-tile's second half (V_hi P_lo)
                 float t2[16];
                 tmem_ld16(tmem + (uint32_t)RB + ((uint32_t)(32 * sp) << 16) + c0, t2);
@@ -924,6 +977,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
               }
             }
           }
+        // tile 0's plain stores are seen by the later reduce-adds (async proxy)
+        if (TR && prm.drain_tma && u == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(yt_empty);
@@ -940,6 +995,7 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
       for (int mt = 0; mt < mt2; ++mt)
         for (int c = half * hc; col_active && c < c_end; ++c)
           Yp[((size_t)mt * 128 + l) * RB + c] = 0.0;
+    if (TR && prm.drain_tma && lane == 0) k1t_bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();

@@ -82,8 +82,8 @@
 #define MCP_CFG_K1T2_TRANSIENT 1
 #endif
 #ifndef MCP_CFG_K1T2_TRWIDE
-// one wide transient m-tile so every GEMM2 m-tile is wide (c3): measured 5.77 vs 5.09 ms (the
-// per-tile drain of 2 x 64 columns through L2 atomics costs more than the wide products save)
+// one wide transient m-tile so every GEMM2 m-tile is wide (c3): measured 5.77 vs 5.09 ms with
+// the per-element RED drain and 5.16-5.17 vs 5.10-5.13 ms with the bulk tensor reduce-add drain
 #define MCP_CFG_K1T2_TRWIDE 0
 #endif
 #ifndef MCP_CFG_K1T2_SERIAL

@@ -456,3 +456,26 @@ def test_fast_mode_tile_shapes_vs_oracle(n, r, d):
     f_s, gl_s, gA_s, _ = om.term_scales(V64, nu, lam, A, d, 0.1)
     e = max(_err(res.f, f, f_s), _err(res.g_lam, gl, gl_s), _err(res.g_A, gA, gA_s))
     assert e <= FAST_TOL, e
+
+
+@pytest.mark.parametrize("n,r", [(1024, 256), (900, 200)])
+def test_fast_mode_transient_tiles_deterministic(n, r):
+    """Fast mode with transient GEMM2 m-tiles (c5 shape: two per tile, RB = 64) drained by bulk
+    tensor reduce-adds: repeated evaluations are bitwise identical (each tile's
+    reduce-adds complete before the next tile's are issued, so the add order is fixed), and the
+    result stays within the stated bound of FP64."""
+    rng = np.random.default_rng(n + r)
+    p = 20_000
+    V = (rng.standard_normal((n, p)) / np.sqrt(n)).astype(np.float32)
+    lam = rng.standard_normal(r)
+    A = rng.standard_normal((n, r)) / np.sqrt(n)
+    obs = mcp.ObservationSet(V)
+    a = mcp.fg_implicit(obs, lam, A, 3, 0.0, mode="tf32x3")
+    assert "transient" in obs.device_context().last_variant, obs.device_context().last_variant
+    b = mcp.fg_implicit(obs, lam, A, 3, 0.0, mode="tf32x3")
+    assert a.f == b.f and np.array_equal(a.g_lam, b.g_lam) and np.array_equal(a.g_A, b.g_A)
+    ref = mcp.fg_implicit(obs, lam, A, 3, 0.0)
+    e = max(abs(a.f - ref.f) / abs(ref.f),
+            np.linalg.norm(a.g_A - ref.g_A) / np.linalg.norm(ref.g_A),
+            np.linalg.norm(a.g_lam - ref.g_lam) / np.linalg.norm(ref.g_lam))
+    assert e <= 1e-4, e

@@ -356,7 +356,14 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   t.r_pad = t.rbs * RB;
   t.kpad = t.nkb * 32;
   const size_t budget = 227 * 1024;
-  const bool drain_tma = t.mt_tr && MCP_K1T2_DRAIN_TMA;
+  // the fp64 partial's adds (flushes, transient drains) by bulk tensor reduce-add need a 16 KB
+  // staging area: taken unless it would cost a stage of the ring (transient m-tiles: always)
+  bool drain_tma = !v1 && MCP_K1T2_DRAIN_TMA;
+  if (drain_tma && !t.mt_tr &&
+      (budget - k1t_smem_bytes(RB, 0, true)) / k1t_stage_bytes(RB) <
+          (budget - k1t_smem_bytes(RB, 0, false)) / k1t_stage_bytes(RB))
+    drain_tma = false;
+  t.drain_tma = drain_tma;
   int ns = (int)((budget - k1t_smem_bytes(RB, 0, drain_tma)) / k1t_stage_bytes(RB));
   if (ns > 8) ns = 8;
   if (ns < 2) return c->fail(MCP_ERR_ARG, "tf32x3 stage ring does not fit");
@@ -398,7 +405,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   pl.k1.name = std::string(t.v2 ? "k1t2_fg_tf32" : "k1t_fg_tf32") + "<3xTF32,RB=" +
                 std::to_string(RB) + ",S=" + std::to_string(ns) +
                 (t.v2 ? std::string(t.serial ? ",serial" : ",lookahead") + (t.zcat ? ",zcat" : "") +
-                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + (t.insplit ? ",insplit" : "") + (t.mt_tr ? ",transient=" + std::to_string(t.mt_tr) + (t.tr_wide ? "w" : "") : std::string()) + ",flush=" + std::to_string(t.flush)
+                             (t.hint ? ",l2hint" : "") +  (t.g2_3d ? ",g2tma3d" : "") + (t.wide ? ",wide=" + std::to_string(t.wide) : std::string()) + (MCP_CFG_K1T2_G2X2 ? ",g2x2" : "") + (t.insplit ? ",insplit" : "") + (t.drain_tma ? ",tmadrain" : "") + (t.mt_tr ? ",transient=" + std::to_string(t.mt_tr) + (t.tr_wide ? "w" : "") : std::string()) + ",flush=" + std::to_string(t.flush)
                       : std::string()) +
                 ">";
   return MCP_OK;
@@ -483,7 +490,7 @@ int enqueue_partial_tf32(mcp_ctx* c, const EvalPlan& pl, const double* dx, doubl
   // the transient drain's bulk tensor reduce-add target: the fp64 partial as rows of RB
   CUtensorMap tm_y;
   prm.drain_tma = 0;
-  if (t.mt_tr && MCP_K1T2_DRAIN_TMA) {
+  if (t.drain_tma) {
     if (!make_tmap_f64(&tm_y, c->dYpart.p, (uint64_t)t.RB,
                        (uint64_t)t.rbs * t.gp * t.mt2 * 128, 8 * (uint64_t)t.RB, 8, 32,
                        CU_TENSOR_MAP_SWIZZLE_NONE))

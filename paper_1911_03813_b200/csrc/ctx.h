@@ -118,6 +118,7 @@ struct K1TPlan {
   bool insplit = false; // K1T2 V_lo formed in shared memory (no V_lo copy in HBM)
   int mt_tr = 0;        // K1T2 transient GEMM2 m-tiles (accumulate in Z's columns)
   bool tr_wide = false; // K1T2: the transient m-tile is wide (all m-tiles wide at c3)
+  bool drain_tma = false; // K1T2: partial adds by bulk tensor reduce-add (16 KB staging)
   int64_t num_tiles = 0;
   size_t smem = 0;
 };

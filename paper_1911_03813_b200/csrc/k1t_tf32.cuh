@@ -812,10 +812,34 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
     int flushes = 0;
     double* Yp = prm.Ypart + ((size_t)rb * prm.gp + pg) * (size_t)mt2 * 128 * RB;
     long long e_wz = 0, e_wp = 0, e_epi = 0, e_fl = 0;
+    // 16 columns of this warp's 32 rows of m-tile mt (wide: halves summed first, fp64) added into
+    // the fp64 partial by two bulk tensor reduce-adds (TMA, at L2) through the warp's 2 KB
+    // staging slot; the caller's previous reduce-adds to these rows have completed (fixed order)
+    auto stage_reduce = [&](const float (&tv)[16], const float (&t2)[16], bool wide, int mt,
+                            int c0) {
+      double* stg = drain_stage + (size_t)ew * 256;   // [32 rows][8]
+      const int grow = (int)((((size_t)rb * prm.gp + pg) * mt2 + mt) * 128 + 32 * sp);
+#pragma unroll
+      for (int k8 = 0; k8 < 2; ++k8) {
+        if (lane == 0) k1t_bulk_wait_read();   // the slot's previous reduce has read it
+        __syncwarp();
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int a = 8 * k8 + 2 * jj;
+          const double v0 = wide ? (double)tv[a] + (double)t2[a] : (double)tv[a];
+          const double v1 = wide ? (double)tv[a + 1] + (double)t2[a + 1] : (double)tv[a + 1];
+          reinterpret_cast<double2*>(stg + 8 * lane)[jj] = make_double2(v0, v1);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) k1t_bulk_reduce_add_2d(&tm_y, c0 + 8 * k8, grow, stg);
+      }
+    };
     auto flush = [&]() {
       K1T2_T0();
       mbar_wait(y_full, (uint32_t)flushes & 1);
       tc_fence_after();
+      if (prm.drain_tma && flushes > 0 && lane == 0) k1t_bulk_wait_all();
       for (int mt = 0; mt < mt_p; ++mt) {   // persistent m-tiles (transient ones drain per tile)
         double* yrow = Yp + ((size_t)mt * 128 + l) * RB;
         for (int c0 = half * hc; col_active && c0 < c_end; c0 += 16) {
@@ -823,6 +847,10 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
           tmem_ld16(ty + ycol(mt) + ((uint32_t)(32 * sp) << 16) + c0, yv);
           const bool wide = mt < prm.wide;
           if (wide) tmem_ld16(ty + ycol(mt) + RB + ((uint32_t)(32 * sp) << 16) + c0, y2);
+          if (prm.drain_tma && flushes > 0) {
+            stage_reduce(yv, y2, wide, mt, c0);
+            continue;
+          }
           // each partial element has exactly one owner thread and flushes are in program order,
           // so fire-and-forget reductions (RED, no load latency) keep the sum order fixed
 #pragma unroll
@@ -835,6 +863,8 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
           }
         }
       }
+      // the first flush's plain stores are seen by the later reduce-adds (async proxy)
+      if (prm.drain_tma && flushes == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty);
@@ -915,30 +945,10 @@ __global__ void __launch_bounds__(K1T2_THREADS_S, 1)
               tmem_ld16(tmem + (uint32_t)(RB * i) + ((uint32_t)(32 * sp) << 16) + c0, tv);
               if (MCP_K1T2_KO & 16) continue;   // knockout: no drain (timing only)
               if (TR && prm.drain_tma && u != 0) {
-                // two 8-column bulk reduce-adds of this warp's 32 rows through its staging slot
-                // (a wide m-tile's halves summed first, in the flush's order)
                 float t2[16];
                 if (prm.tr_wide)
                   tmem_ld16(tmem + (uint32_t)RB + ((uint32_t)(32 * sp) << 16) + c0, t2);
-                double* stg = drain_stage + (size_t)ew * 256;   // [32 rows][8]
-                const int grow = (int)((((size_t)rb * prm.gp + pg) * mt2 + (mt_p + i)) * 128 +
-                                       32 * sp);
-#pragma unroll
-                for (int k8 = 0; k8 < 2; ++k8) {
-                  if (lane == 0) k1t_bulk_wait_read();   // the slot's previous reduce read it
-                  __syncwarp();
-#pragma unroll
-                  for (int jj = 0; jj < 4; ++jj) {
-                    const int a = 8 * k8 + 2 * jj;
-                    const double v0 = prm.tr_wide ? (double)tv[a] + (double)t2[a] : (double)tv[a];
-                    const double v1 =
-                        prm.tr_wide ? (double)tv[a + 1] + (double)t2[a + 1] : (double)tv[a + 1];
-                    reinterpret_cast<double2*>(stg + 8 * lane)[jj] = make_double2(v0, v1);
-                  }
-                  fence_async_smem();
-                  __syncwarp();
-                  if (lane == 0) k1t_bulk_reduce_add_2d(&tm_y, c0 + 8 * k8, grow, stg);
-                }
+                stage_reduce(tv, t2, prm.tr_wide != 0, mt_p + i, c0);
                 continue;
               }
               if (prm.tr_wide) {   // the wide m-tile's second half (V_hi P_lo)

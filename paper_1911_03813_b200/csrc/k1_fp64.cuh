@@ -263,6 +263,12 @@ __global__ void __launch_bounds__(K1_THREADS) k1_fg_dmma(K1Params prm) {
 #ifndef MCP_K1G_HINTS
 #define MCP_K1G_HINTS 0   // 1: L2 hints (V evict_first, Y evict_last): -20% DRAM, +3% time
 #endif
+#ifndef MCP_K1GT_TMEM_CHUNKS
+#define MCP_K1GT_TMEM_CHUNKS 64   // cap on K1GT's TMEM-resident chunks (experiments)
+#endif
+#ifndef MCP_K1G_TMA_RED
+#define MCP_K1G_TMA_RED 1   // K1GT's L2 chunks added by bulk tensor reduce-add (0: load + store)
+#endif
 #ifndef MCP_K1G_G2MAP
 #define MCP_K1G_G2MAP 1   // fp32 rows: conflict-free GEMM2 row map (experiment builds: 0)
 #endif
@@ -274,17 +280,31 @@ template <typename VT, int RB>
 __host__ __device__ constexpr int k1g_sp() {
   return (MCP_K1G_G2MAP && sizeof(VT) == 4) ? RB + 2 : RB + 4;
 }
-template <typename VT, int RB>
+template <typename VT, int RB, bool TM = false>
 __host__ __device__ constexpr size_t k1g_smem_bytes() {
   return 2 * (size_t)K1_TP * K1_SV * sizeof(VT) + 2 * (size_t)16 * (RB / 8) * 32 * 8 +
-         (size_t)K1_TP * k1g_sp<VT, RB>() * 8 + (size_t)8 * RB * 8;
+         (size_t)K1_TP * k1g_sp<VT, RB>() * 8 + (size_t)8 * RB * 8 +
+         (TM && MCP_K1G_TMA_RED ? 128 + (size_t)8 * 8 * RB * 8 : 0);   // K1GT L2-chunk staging
+}
+
+// bulk tensor reduce-add (TMA, performed at L2) of a shared-memory box into global memory
+__device__ __forceinline__ void k1g_bulk_reduce_add_2d(const CUtensorMap* tm, int c0, int c1,
+                                                       const void* src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n"
+      "cp.async.bulk.commit_group;\n" ::"l"(tm),
+      "r"(c0), "r"(c1), "r"((uint32_t)__cvta_generic_to_shared(src))
+      : "memory");
 }
 
 // K1G with TM = true ("K1GT"): the Y partial lives in tensor memory instead of L2 -- all of it
 // when n_chunks * RB <= 512, else (RB = 64 at n = 1024, the c5 default) chunks 0-7 in TMEM and
 // the rest in L2: half K1G's L2 working set, which then stays resident.  Measured at c5 (one
 // box, back to back): K1G 633 ms / 845 W / DRAM 14.3x V; K1GT RB = 32 657 ms / 669 W / 1.0x;
-// K1GT RB = 64 half-and-half 625.5 ms / 741 W / 1.4x (profiles/r02/ab_c5_k1gt_half.txt).  TMEM is
+// K1GT RB = 64 half-and-half 625.5 ms / 741 W / 1.4x (profiles/r02/ab_c5_k1gt_half.txt).  The L2
+// chunks are then added by one bulk tensor reduce-add per warp and chunk (the warp's 8 x RB result
+// staged in shared memory; the add happens at L2, no load of the previous value): 611.5 ms, 684 W
+// (profiles/r02/ab_c5_k1gt_tmared.txt; 0 or 4 TMEM chunks instead of 8 measured 646 / 628 ms).  TMEM is
 // used as private per-thread storage (fp64 as two 32-bit columns): thread (warp w, lane L) owns
 // TMEM lane 32 (w % 4) + L, columns [256 (w / 4), 256 (w / 4) + 256) -- 128 doubles, i.e. the
 // 2 NT doubles of each of the n_chunks GEMM2 accumulators it owns (n_chunks * RB <= 512: c5's
@@ -296,7 +316,8 @@ __host__ __device__ constexpr size_t k1g_smem_bytes() {
 // block / GEMM2 m-tile w % 8 and the NTW = NT / 2 column tiles starting at 8 NTW (w / 8) in both
 // GEMMs (4 warps per sub-partition instead of 2, each with half the DMMA chains).
 template <typename VT, int RB, bool TM, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
+__global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm,
+                                                          const __grid_constant__ CUtensorMap tm_y) {
   pdl_enter();   // the factor fragments come from the preceding prep kernel
   constexpr int THREADS = NW * 32;
   constexpr int NT = RB / 8;
@@ -317,6 +338,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
   double* sA1 = sA0 + 16 * NT * 32;
   double* sP = sA1 + 16 * NT * 32;
   double* sW = sP + K1_TP * SP;
+  // K1GT's L2 chunks: each warp stages its 8 x RB GEMM2 result (fp64) and adds it into the
+  // partial with one bulk tensor reduce-add -- no load of the previous value, the add at L2
+  constexpr bool kTmaRed = TM && MCP_K1G_TMA_RED && NW == 8;
+  double* sStg = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(sW + 8 * RB) + 127) & ~(uintptr_t)127);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -359,7 +385,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
 
   // K1GT: chunks [0, CT) of the partial live in TMEM, the rest (RB = 64 at n = 1024: half of
   // it) in L2 -- half the L2 working set of K1G, which then stays resident
-  const int CT = TM ? min(C, TCOLS / (4 * NTW)) : 0;
+  const int CT = TM ? min(min(C, TCOLS / (4 * NTW)), MCP_K1GT_TMEM_CHUNKS) : 0;
   K1WTile ti;
   for (int64_t k = 0; k1w_tile_at(wp, blockIdx.x, k, ti); ++k) {
     const int64_t row0 = ti.tile * K1_TP;
@@ -416,6 +442,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
     __syncthreads();
 
     // ---------------- GEMM2, chunk by chunk, last to first ----------------
+    // the previous tile's reduce-adds have completed before this tile's (fixed add order)
+    if (kTmaRed && !first && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     for (int c = C - 1; c >= 0; --c) {
       const VT* sv = (c & 1) ? sV1 : sV0;
       if (c >= 1 && c - 1 <= C - 3) {
@@ -433,7 +461,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
       if constexpr (TM) {
         if (in_tm && !first) tmem_ld_nowait<4 * NTW>(tme + 4 * NTW * c, tprev);
       }
-      if (!in_tm && !first) {
+      if (!in_tm && !first && !kTmaRed) {
 #pragma unroll
         for (int nt = 0; nt < NTW; ++nt)
           prev[nt] = MCP_K1G_HINTS
@@ -466,6 +494,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
             tout[4 * nt + 2 * e + 1] = (uint32_t)__double2hiint(o);
           }
         tmem_st<4 * NTW>(tme + 4 * NTW * c, tout);
+      } else if (kTmaRed && !first) {
+        double* stg = sStg + (size_t)warp * 8 * RB;   // [8 rows][RB]
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+          *reinterpret_cast<double2*>(stg + g * RB + 8 * (nt0 + nt) + 2 * t) =
+              make_double2(acc[nt][0], acc[nt][1]);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+          k1g_bulk_reduce_add_2d(&tm_y, 0,
+                                 (int)(((size_t)ti.rb * prm.gp + ti.slot) * prm.n_pad +
+                                       c * K1_NK + 8 * wr),
+                                 stg);
       } else {
 #pragma unroll
         for (int nt = 0; nt < NTW; ++nt) {
@@ -483,6 +526,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
       __syncthreads();
     }
     if constexpr (TM) tmem_st_wait();   // this tile's partial is in TMEM before the next reads it
+    // a segment's first plain stores are seen by the later reduce-adds (async proxy)
+    if (kTmaRed && first) asm volatile("fence.proxy.async.global;\n" ::: "memory");
     first = false;
 
     if (ti.last_in_seg) {
@@ -522,6 +567,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1g_fg_dmma(K1Params prm) {
       first = true;
     }
   }
+  if (kTmaRed && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   // partial slots no CTA writes (blocks touched by fewer leftover CTAs) are zero
   k1w_zero_holes<THREADS, RB>(wp, blockIdx.x, 0, prm.n_pad, true);
   if constexpr (TM) {

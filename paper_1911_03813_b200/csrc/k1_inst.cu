@@ -19,6 +19,12 @@
 #include "k1r_fp64.cuh"
 #endif
 
+namespace mcp_internal {
+// abi.cu: 2-D fp64 tensor map (inner x outer, row pitch in bytes)
+bool make_tmap_f64(CUtensorMap* m, const void* gaddr, uint64_t inner, uint64_t outer,
+                   uint64_t pitch, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw);
+}  // namespace mcp_internal
+
 namespace mcp {
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device maximum: raise it once per
@@ -74,13 +80,16 @@ const Entry kTable[] = {MCP_K1_ROW(double, MCP_F64), MCP_K1_ROW(float, MCP_F32)}
 
 // K1G (Y partial in global memory): column blocks of RB in {16, 32, 64}
 // (Entry::MTW: 0 = Y partial in L2 (8 warps), 1 = K1GT with 8 warps, 2 = K1GT with 16 warps)
+// K1G's launch takes the partial's tensor map (K1GT's bulk reduce-adds) through a file-scope
+// slot set by k1_launch right before the call (the table's launchers share one signature)
+thread_local const CUtensorMap* g_k1g_tmap = nullptr;
 template <typename VT, int RB, bool TM, int NW>
 void launch_g(const K1Params& prm, int grid, size_t smem, cudaStream_t s) {
-  launch_pdl(k1g_fg_dmma<VT, RB, TM, NW>, dim3(grid), dim3(NW * 32), smem, s, prm);
+  launch_pdl(k1g_fg_dmma<VT, RB, TM, NW>, dim3(grid), dim3(NW * 32), smem, s, prm, *g_k1g_tmap);
 }
 #define MCP_K1G_E(VT, DT, RB, TM, NW)                                                        \
   {DT, RB, TM ? NW / 8 : 0, &launch_g<VT, RB, TM, NW>, (const void*)&k1g_fg_dmma<VT, RB, TM, NW>, \
-   k1g_smem_bytes<VT, RB>()}
+   k1g_smem_bytes<VT, RB, TM>()}
 const Entry kTableG[] = {
     MCP_K1G_E(double, MCP_F64, 16, false, 8), MCP_K1G_E(double, MCP_F64, 32, false, 8),
     MCP_K1G_E(double, MCP_F64, 64, false, 8), MCP_K1G_E(float, MCP_F32, 16, false, 8),
@@ -669,6 +678,15 @@ int k1_launch(const K1Variant& v, const void* dV, int64_t ldv, int n, const doub
   prm.t_main = v.t_main;
   prm.Ypart = Ypart;
   prm.wpart = wpart;
+  CUtensorMap tm_y;
+  if (v.kind == 5) {
+    // the Y partial as rows of RB doubles; box = one warp's 8 x RB GEMM2 chunk result
+    if (!mcp_internal::make_tmap_f64(&tm_y, Ypart, (uint64_t)v.RB,
+                                     (uint64_t)v.rbs * v.gp * v.n_pad, 8 * (uint64_t)v.RB,
+                                     (uint32_t)v.RB, 8, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return 1;
+    g_k1g_tmap = &tm_y;
+  }
   (v.kind == 5 ? kTableG : kTable)[v.entry].launch(prm, v.grid, v.smem, s);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 1;
 }

@@ -328,16 +328,25 @@ __global__ void k_ordered_sum(const double* __restrict__ part, int m, double* __
 // Round 2: the refill decode (sqrt + 64-bit divisions per chunk on warp 0) made warp 0 the
 // straggler at every barrier (ncu source view: 15% of samples behind BAR.SYNC); the refill cursor
 // is now kept by every thread, decoded once per pair, the refilling warp rotates, and the next
-// k-step's operands load before the current DMMAs -- 359.5 -> 346.8 ms (76.8% -> 79.6%).  Fragment loads stay conflict-free under
+// k-step's operands load before the current DMMAs -- 359.5 -> 346.8 ms (76.8% -> 79.6%).  Then
+// each tile pair split into two 64-row halves of I on neighbouring CTAs (8 warps, 4-stage ring,
+// two CTAs per SM): one CTA's barrier skew and epilogue are covered by the other CTA's DMMAs --
+// 349.3 -> 333.0 ms (83% of the FP64 pipe; profiles/r02/ab_c4_k53_halves.txt).  Fragment loads stay conflict-free under
 // the swizzle by letting DMMA row (column) g of a 8-row m-tile read physical tile row
 // 2g (g < 4) / 2(g - 4) + 1 (g >= 4): the 16 lanes of a half-warp then hit 16 distinct 8-byte
 // banks.  The epilogue uses the same row map for the weights, so the sum is the same Gram power
 // sum as K52 (tile-pair order and the per-CTA fixed-order reduction unchanged).
 constexpr int K53_T = 128;
 constexpr int K53_NK = 16;          // doubles per chunk row (one 128-byte swizzle row)
-constexpr int K53_THREADS = 512;
-constexpr int K53_STAGES = 6;
-constexpr int K53_STAGE_BYTES = 2 * K53_T * K53_NK * 8;   // I and J chunks, 32 KB
+// TI = rows of the I tile a CTA takes: 128 (16 warps, one CTA per SM) or 64 (K53H: each tile
+// pair split in two row halves, 8 warps per CTA, two CTAs per SM -- one CTA's barrier skew and
+// epilogue are covered by the other's DMMAs)
+template <int TI> __host__ __device__ constexpr int k53_threads() { return TI == 128 ? 512 : 256; }
+template <int TI> __host__ __device__ constexpr int k53_stages() { return TI == 128 ? 6 : 4; }
+template <int TI> __host__ __device__ constexpr int k53_stage_bytes() { return (TI + K53_T) * K53_NK * 8; }
+constexpr int K53_THREADS = k53_threads<128>();
+constexpr int K53_STAGES = k53_stages<128>();
+constexpr int K53_STAGE_BYTES = k53_stage_bytes<128>();   // I and J chunks, 32 KB
 #ifndef MCP_K53_SYNC
 #define MCP_K53_SYNC 1
 #endif
@@ -345,26 +354,30 @@ constexpr int K53_STAGE_BYTES = 2 * K53_T * K53_NK * 8;   // I and J chunks, 32 
 // 2 -> 347.9, 3 -> 350.6 -- the skew does not amortise over longer groups
 constexpr int K53_SYNC = MCP_K53_SYNC;
 
+template <int TI = 128>
 __host__ __device__ constexpr size_t k53_smem_bytes() {
-  return 1024 + (size_t)K53_STAGES * K53_STAGE_BYTES + 256;
+  return 1024 + (size_t)k53_stages<TI>() * k53_stage_bytes<TI>() + 256;
 }
 
 __device__ __forceinline__ int k53_prow(int g) { return g < 4 ? 2 * g : 2 * (g - 4) + 1; }
 
-__global__ void __launch_bounds__(K53_THREADS, 1)
+template <int TI>
+__global__ void __launch_bounds__(k53_threads<TI>(), 128 / TI)
     k53_gram_power(const __grid_constant__ CUtensorMap tmI, const __grid_constant__ CUtensorMap tmJ,
                    int n_chunks, const double* __restrict__ nu, double nu_const,
                    const double* __restrict__ nuJ, double nu_constJ, int d, int64_t T, int64_t TJ,
                    int rect, int colmajor, int64_t pair_begin, int64_t pair_end,
                    double* __restrict__ part) {
+  constexpr int ST_ = k53_stages<TI>(), SB_ = k53_stage_bytes<TI>(), NTH_ = k53_threads<TI>();
+  constexpr int HALVES = K53_T / TI;   // units per tile pair
   extern __shared__ __align__(16) unsigned char k53_raw[];
   unsigned char* base = k53_raw + ((1024u - (smem_u32(k53_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)K53_STAGES * K53_STAGE_BYTES);
-  double* sRed = reinterpret_cast<double*>(full + K53_STAGES);   // 16 doubles
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)ST_ * SB_);
+  double* sRed = reinterpret_cast<double*>(full + ST_);   // 16 doubles
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;   // 4 x 4 warps, 32 x 32 outputs each
+  const int wm = warp >> 2, wn = warp & 3;   // (TI / 32) x 4 warps, 32 x 32 outputs each
   const int prow = k53_prow(g);
   const double* nuJv = rect ? nuJ : nu;
   const double ncJ = rect ? nu_constJ : nu_const;
@@ -380,23 +393,25 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
       k5_decode(k, T, I_, J_);
     }
   };
-  // this CTA's pairs: pair_begin + blockIdx.x + kp * gridDim.x
-  const int64_t my_pairs =
-      pair_begin + blockIdx.x < pair_end
-          ? (pair_end - pair_begin - blockIdx.x + gridDim.x - 1) / gridDim.x
-          : 0;
-  const int64_t nsteps = my_pairs * n_chunks;
-  auto pair_of = [&](int64_t kp, int64_t& I_, int64_t& J_) {
-    decode(pair_begin + blockIdx.x + kp * gridDim.x, I_, J_);
+  // this CTA's units (tile pair x row half): unit blockIdx.x + kp * gridDim.x of
+  // HALVES * (pair_end - pair_begin); both halves of a pair run on neighbouring CTAs
+  const int64_t units = (pair_end - pair_begin) * HALVES;
+  const int64_t my_units =
+      blockIdx.x < units ? (units - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t nsteps = my_units * n_chunks;
+  auto pair_of = [&](int64_t kp, int64_t& I_, int64_t& J_, int& h_) {
+    const int64_t u = blockIdx.x + kp * gridDim.x;
+    decode(pair_begin + u / HALVES, I_, J_);
+    h_ = (int)(u % HALVES);
   };
-  auto issue = [&](int s, int c, int64_t I, int64_t J) {   // TMA of one chunk into stage s
-    unsigned char* st = base + (size_t)s * K53_STAGE_BYTES;
-    mbar_arrive_expect_tx(&full[s], K53_STAGE_BYTES);
-    tma_load_2d(st, &tmI, c * K53_NK, (int)(I * K53_T), smem_u32(&full[s]));
-    tma_load_2d(st + K53_STAGE_BYTES / 2, &tmJ, c * K53_NK, (int)(J * K53_T), smem_u32(&full[s]));
+  auto issue = [&](int s, int c, int64_t I, int64_t J, int h) {   // one chunk into stage s
+    unsigned char* st = base + (size_t)s * SB_;
+    mbar_arrive_expect_tx(&full[s], SB_);
+    tma_load_2d(st, &tmI, c * K53_NK, (int)(I * K53_T + TI * h), smem_u32(&full[s]));
+    tma_load_2d(st + TI * K53_NK * 8, &tmJ, c * K53_NK, (int)(J * K53_T), smem_u32(&full[s]));
   };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < K53_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < ST_; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tma_prefetch_desc(&tmI);
     tma_prefetch_desc(&tmJ);
@@ -404,19 +419,21 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
   __syncthreads();
   if (threadIdx.x == 0) {
     int64_t I = 0, J = 0;
-    for (int64_t q = 0; q < K53_STAGES && q < nsteps; ++q) {
-      if (q % n_chunks == 0) pair_of(q / n_chunks, I, J);
-      issue((int)q, (int)(q % n_chunks), I, J);
+    int h = 0;
+    for (int64_t q = 0; q < ST_ && q < nsteps; ++q) {
+      if (q % n_chunks == 0) pair_of(q / n_chunks, I, J, h);
+      issue((int)q, (int)(q % n_chunks), I, J, h);
     }
   }
   // Refill cursor (step q + STAGES), kept by every thread so the refilling warp can rotate: the
   // tile-pair decode (sqrt, 64-bit divisions) runs once per pair on all warps at the same point
   // instead of once per chunk on warp 0, which made warp 0 the straggler at every chunk barrier
   // (ncu source view of the previous form: 15% of warp samples waiting behind BAR.SYNC).
-  int64_t r_kp = K53_STAGES / n_chunks;
-  int r_c = K53_STAGES % n_chunks;
+  int64_t r_kp = ST_ / n_chunks;
+  int r_c = ST_ % n_chunks;
   int64_t rI = 0, rJ = 0;
-  if (K53_STAGES < nsteps) pair_of(r_kp, rI, rJ);
+  int rh = 0;
+  if (ST_ < nsteps) pair_of(r_kp, rI, rJ, rh);
 
   // per-lane word offsets (doubles) inside a stage: row * 16 + (k ^ 2 (row & 7)), row & 7 = prow
   const int swz = 2 * prow;
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     aoff[i] = (32 * wm + 8 * i + prow) * K53_NK;
-    boff[i] = K53_T * K53_NK + (32 * wn + 8 * i + prow) * K53_NK;
+    boff[i] = TI * K53_NK + (32 * wn + 8 * i + prow) * K53_NK;
   }
   const uint32_t st0 = smem_u32(base);
   double tsum = 0.0;
@@ -439,7 +456,7 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
   int64_t kp = 0;
   for (int64_t q = 0; q < nsteps; ++q) {
     mbar_wait(&full[s], ph);
-    const uint32_t sb = st0 + (uint32_t)s * K53_STAGE_BYTES;
+    const uint32_t sb = st0 + (uint32_t)s * SB_;
     // operands of k-step ks + 1 are loaded before k-step ks's DMMAs issue (ordered ld.shared),
     // so a warp running alone keeps the pipe fed
     double a[2][4], b[2][4];
@@ -468,19 +485,19 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
       __syncthreads();
       const int64_t q0 = q + 1 - ((q % K53_SYNC) + 1);   // first step of this sync group
       for (int64_t qq = q0; qq <= q; ++qq) {
-        if (qq + K53_STAGES >= nsteps) break;
-        if (warp == (int)(qq & 15) && lane == 0) {
+        if (qq + ST_ >= nsteps) break;
+        if (warp == (int)(qq % (NTH_ / 32)) && lane == 0) {
           k1w_fence_proxy_async();
-          issue((int)(qq % K53_STAGES), r_c, rI, rJ);
+          issue((int)(qq % ST_), r_c, rI, rJ, rh);
         }
         if (++r_c == n_chunks) {
           r_c = 0;
           ++r_kp;
-          if (qq + K53_STAGES + 1 < nsteps) pair_of(r_kp, rI, rJ);
+          if (qq + ST_ + 1 < nsteps) pair_of(r_kp, rI, rJ, rh);
         }
       }
     }
-    if (++s == K53_STAGES) {
+    if (++s == ST_) {
       s = 0;
       ph ^= 1u;
     }
@@ -488,11 +505,12 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
       cc = 0;
       // last chunk of a tile pair: sum nu_l nu_l' g^d over the tile (x2 off the diagonal)
       int64_t I, J;
-      pair_of(kp++, I, J);
+      int h;
+      pair_of(kp++, I, J, h);
       double tile_sum = 0.0;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        const int64_t l = I * K53_T + 32 * wm + 8 * mt + prow;
+        const int64_t l = I * K53_T + TI * h + 32 * wm + 8 * mt + prow;
         const double nl = nu ? nu[l] : nu_const;
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
@@ -514,7 +532,7 @@ __global__ void __launch_bounds__(K53_THREADS, 1)
   __syncthreads();
   if (threadIdx.x == 0) {
     double sum = 0.0;
-    for (int w = 0; w < K53_THREADS / 32; ++w) sum += sRed[w];
+    for (int w = 0; w < NTH_ / 32; ++w) sum += sRed[w];
     part[blockIdx.x] = sum;
   }
 }

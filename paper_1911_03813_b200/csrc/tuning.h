@@ -68,6 +68,10 @@
 #ifndef MCP_CFG_K53
 #define MCP_CFG_K53 1
 #endif
+// K53 with each tile pair split in two 64-row halves (8 warps, two CTAs per SM)
+#ifndef MCP_CFG_K53_HALF
+#define MCP_CFG_K53_HALF 1
+#endif
 // fast mode: K1T2 (precomputed V_lo) unless 1 -> the in-kernel split K1T
 #ifndef MCP_CFG_K1T_V1
 #define MCP_CFG_K1T_V1 0

@@ -1104,13 +1104,16 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   const int64_t b = pairs * part / nparts, e = pairs * (part + 1) / nparts;
   const int n_chunks = (int)ceil_div(c->n, k53 ? K53_NK : big ? K52_NK : K5_NK);
   const bool k53h = k53 && MCP_CFG_K53_HALF;   // 64-row I halves, two CTAs per SM
-  const size_t smem = k53 ? (k53h ? k53_smem_bytes<64>() : k53_smem_bytes<128>())
+  const int k53ti = !k53 ? 128 : !k53h ? 128 : MCP_CFG_K53_TI;   // I-tile rows per CTA
+  const size_t smem = k53 ? (k53ti == 32 ? k53_smem_bytes<32>()
+                             : k53ti == 64 ? k53_smem_bytes<64>() : k53_smem_bytes<128>())
                           : big ? (f64 ? k52_smem_bytes<double>() : k52_smem_bytes<float>())
                                 : (f64 ? k5_smem_bytes<double>() : k5_smem_bytes<float>());
-  const void* fn = k53 ? (k53h ? (const void*)k53_gram_power<64> : (const void*)k53_gram_power<128>)
+  const void* fn = k53 ? (k53ti == 32 ? (const void*)k53_gram_power<32>
+                         : k53ti == 64 ? (const void*)k53_gram_power<64> : (const void*)k53_gram_power<128>)
                        : big ? (f64 ? (const void*)k52_gram_power<double> : (const void*)k52_gram_power<float>)
                              : (f64 ? (const void*)k5_gram_power<double> : (const void*)k5_gram_power<float>);
-  const int threads = k53 ? (k53h ? k53_threads<64>() : k53_threads<128>())
+  const int threads = k53 ? 4 * k53ti
                           : big ? K52_THREADS : K5_THREADS;
   if (!ensure_dyn_smem(fn, smem))
     return c->fail(MCP_ERR_CUDA, "cannot raise the Gram-power kernel's shared-memory limit");
@@ -1118,7 +1121,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)c->sms * occ;
-  const int64_t work_units = (e - b) * (k53h ? 2 : 1);
+  const int64_t work_units = (e - b) * (k53 ? 128 / k53ti : 1);
   if (grid > work_units) grid = work_units;
   if (grid < 1) grid = 1;
   int rc;
@@ -1126,7 +1129,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   if ((rc = ensure(c, c->dscalar, sizeof(double)))) return rc;
   CUtensorMap tmI, tmJ;
   if (k53) {
-    if (!make_tmap_f64(&tmI, c->dV, c->ldv, c->p_pad, 8 * c->ldv, K53_NK, k53h ? 64 : K53_T) ||
+    if (!make_tmap_f64(&tmI, c->dV, c->ldv, c->p_pad, 8 * c->ldv, K53_NK, (uint32_t)k53ti) ||
         !make_tmap_f64(&tmJ, cross ? cross->dV : c->dV, c->ldv, cross ? cross->p_pad : c->p_pad,
                        8 * c->ldv, K53_NK, K53_T))
       return c->fail(MCP_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Gram-power tiles");
@@ -1134,7 +1137,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   auto* ev = timing_begin(c, c->stream);
   MCP_NVTX("K5 Gram power");
   if (k53) {
-    (k53h ? k53_gram_power<64> : k53_gram_power<128>)<<<(int)grid, threads, smem, c->stream>>>(
+    (k53ti == 32 ? k53_gram_power<32> : k53ti == 64 ? k53_gram_power<64> : k53_gram_power<128>)<<<(int)grid, threads, smem, c->stream>>>(
         tmI, tmJ, n_chunks, c->dnu, c->nu_const, cross ? cross->dnu : nullptr,
         cross ? cross->nu_const : 0.0, d, T, TJ, cross ? 1 : 0, cross ? cross->colmajor : 0, b, e,
         (double*)c->dpart.p);
@@ -1178,7 +1181,7 @@ static int data_norm_part(mcp_ctx* c, int d, int mode, int part, int nparts, con
   CUDA_TRY(c, cudaMemcpyAsync(out, c->dscalar.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->last_launches = 2;
-  c->variant = std::string(k53h ? "k53_gram_dmma64x128_tma" : k53 ? "k53_gram_dmma128_tma" : big ? "k52_gram_dmma128" : "k5_gram_dmma64") +
+  c->variant = std::string(k53 ? "k53_gram_dmma" + std::to_string(k53ti) + "x128_tma" : big ? "k52_gram_dmma128" : "k5_gram_dmma64") +
                (f64 ? "<f64>" : "<f32>") +
                (cross ? "[cross]" : "");
   return MCP_OK;

@@ -341,8 +341,13 @@ constexpr int K53_NK = 16;          // doubles per chunk row (one 128-byte swizz
 // TI = rows of the I tile a CTA takes: 128 (16 warps, one CTA per SM) or 64 (K53H: each tile
 // pair split in two row halves, 8 warps per CTA, two CTAs per SM -- one CTA's barrier skew and
 // epilogue are covered by the other's DMMAs)
-template <int TI> __host__ __device__ constexpr int k53_threads() { return TI == 128 ? 512 : 256; }
-template <int TI> __host__ __device__ constexpr int k53_stages() { return TI == 128 ? 6 : 4; }
+#ifndef MCP_K53_STAGES32
+#define MCP_K53_STAGES32 2   // ring depth of the 32-row form (2: four CTAs per SM, 3: three)
+#endif
+template <int TI> __host__ __device__ constexpr int k53_threads() { return 4 * TI; }
+template <int TI> __host__ __device__ constexpr int k53_stages() {
+  return TI == 128 ? 6 : TI == 64 ? 4 : MCP_K53_STAGES32;
+}
 template <int TI> __host__ __device__ constexpr int k53_stage_bytes() { return (TI + K53_T) * K53_NK * 8; }
 constexpr int K53_THREADS = k53_threads<128>();
 constexpr int K53_STAGES = k53_stages<128>();

@@ -72,6 +72,9 @@
 #ifndef MCP_CFG_K53_HALF
 #define MCP_CFG_K53_HALF 1
 #endif
+#ifndef MCP_CFG_K53_TI
+#define MCP_CFG_K53_TI 64          // I-tile rows per CTA when split: 64 (2 CTAs / SM) or 32
+#endif
 // fast mode: K1T2 (precomputed V_lo) unless 1 -> the in-kernel split K1T
 #ifndef MCP_CFG_K1T_V1
 #define MCP_CFG_K1T_V1 0

@@ -165,8 +165,12 @@ int mcp_set_kernel_timing(mcp_ctx* ctx, int enable);   /* enable > 1: time every
  *   MCP_OPT_FUSED_TAIL (default 1): end eligible FP64 evaluations with the one-kernel
  *     reduce+finish (K3F); 0 runs the separate reduce and tail kernels (bitwise-equal results;
  *     the tests compare the two).  No reference counterpart (an implementation choice).
+ *   MCP_OPT_SMALL_KERNEL (default 1): evaluate small problems (config 1, mini-batches) with the
+ *     single-launch kernel K1Z; 0 runs the general K1 -> reduce+finish chain (results agree to
+ *     fp64 reassociation; the tests compare the two).  No reference counterpart.
  */
 #define MCP_OPT_FUSED_TAIL 1
+#define MCP_OPT_SMALL_KERNEL 2
 int mcp_set_option(mcp_ctx* ctx, int key, int64_t value);
 int mcp_kernel_time_ms(mcp_ctx* ctx, double* total_ms, int* launches, int reset);
 

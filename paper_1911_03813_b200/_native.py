@@ -25,6 +25,7 @@ MCP_F64, MCP_F32 = 0, 1
 MCP_VAR_MAJOR, MCP_OBS_MAJOR = 0, 1
 MODES = {"fp64": 0, "tf32x3": 1}
 MCP_OPT_FUSED_TAIL = 1
+MCP_OPT_SMALL_KERNEL = 2
 
 # name -> (restype, argtypes); every symbol include/momentcp_b200.h declares
 _c_void_p = ctypes.c_void_p

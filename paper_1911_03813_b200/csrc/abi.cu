@@ -24,6 +24,7 @@
 #include "pdl.h"
 #include "k1_dispatch.h"
 #include "k1t_tf32.cuh"
+#include "k1z_small.cuh"
 #include "ctx.h"
 
 #include <cuda.h>
@@ -411,6 +412,58 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
   return MCP_OK;
 }
 
+// K1Z shape for (dtype, n, r, p): a function of those and the SM count only (the summation
+// order -- and so the result bits -- must not depend on where the rows came from).
+static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
+  z = K1ZPlan();
+  if (!MCP_CFG_K1Z || !c->opt_small_kernel) return false;
+  const int64_t n = c->n, p = c->p;
+  if (r > K1Z_MAXR || n > K1Z_MAXN || p < 1) return false;
+  if ((double)p * (double)n * (double)r > (double)MCP_CFG_K1Z_MAX_WORK) return false;
+  const int dtype = c->gV ? c->gdtype : c->dtype;
+  const size_t esz = dtype == MCP_F64 ? 8 : 4;
+  z.RP = r <= 8 ? 8 : 16;
+  z.NI = n > 256 ? 2 : 1;
+  if (n > 128) {
+    z.IB = 256;
+  } else {
+    z.IB = 32;
+    while (z.IB < n) z.IB *= 2;
+  }
+  z.LG = K1Z_T / z.IB;
+  int64_t ns = n;
+  if (dtype == MCP_F64) {
+    while (ns % 16 != 4) ++ns;
+  } else {
+    while (ns % 32 != 8) ++ns;
+  }
+  z.ns = (int)ns;
+  const int64_t max_g = MCP_CFG_K1Z_MAXG > 0 ? std::min<int64_t>(MCP_CFG_K1Z_MAXG, c->sms) : c->sms;
+  // few rows per CTA: GEMM1 splits k over 2 or 4 threads so a pass covers 16 or 8 rows
+  const int64_t rpc0 = ceil_div(p, max_g);
+  z.KQ = rpc0 <= 8 ? 4 : (rpc0 <= 16 ? 2 : 1);
+  const int64_t RS = 32 / z.KQ;
+  z.rows_per_cta = (int)round_up(rpc0, RS);
+  z.G = (int)ceil_div(p, (int64_t)z.rows_per_cta);
+  z.PS = (int)round_up(n * r + r, (int64_t)2);
+  z.np = (int)(n | 1);
+  const size_t fixed = sizeof(double) * ((size_t)z.np * z.RP + 32 * z.RP +
+                                         2 * K1Z_MAXR * K1Z_MAXR + 2 * K1Z_T + 3 * z.RP);
+  const size_t combine = z.LG > 1 ? sizeof(double) * (size_t)K1Z_T * z.RP : 0;
+  const size_t budget = 226 * 1024;
+  const size_t per_row = ns * esz + sizeof(double) * z.RP;
+  if (fixed + std::max(combine, (size_t)RS * per_row) > budget) return false;
+  const int64_t Rmax = (int64_t)((budget - fixed) / per_row) / RS * RS;
+  z.R = (int)std::min<int64_t>(z.rows_per_cta, Rmax);
+  z.smem = fixed + sizeof(double) * (size_t)z.R * z.RP +
+           std::max(combine, (size_t)z.R * ns * esz);
+  z.name = std::string("k1z_fg_small<") + (dtype == MCP_F64 ? "f64" : "f32") +
+           ",RP=" + std::to_string(z.RP) + ",NI=" + std::to_string(z.NI) + ",KQ=" + std::to_string(z.KQ) +
+           ",G=" + std::to_string(z.G) + ",R=" + std::to_string(z.R) + ">";
+  z.on = true;
+  return true;
+}
+
 int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   if (!c->loaded) return c->fail(MCP_ERR_STATE, "no observation set loaded (call mcp_load_obs)");
   if (d < 2) return c->fail(MCP_ERR_ARG, "order must be >= 2, got " + std::to_string(d));
@@ -452,6 +505,16 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   if ((rc = ensure(c, c->dwpart, sizeof(double) * pl.k1.wpart_elems))) return rc;
   if ((rc = ensure(c, c->dG, sizeof(double) * (size_t)r * r))) return rc;
   if ((rc = ensure(c, c->dC, sizeof(double) * (size_t)r * r))) return rc;
+  // K1Z only where the general chain is the 4-6 launch one (prep -> K1 -> K3 -> tail): the
+  // two-launch pairs / stream kernels of n <= 128 fp64 sets measured faster than K1Z
+  // (tools/sweep_small.py, profiles/r02/sweep_small.txt)
+  if (pl.k1.needs_prep() && plan_k1z(c, r, pl.z)) {
+    if ((rc = ensure(c, c->dYpart, sizeof(double) * (size_t)pl.z.G * pl.z.PS))) return rc;
+    if (!c->dzbar.p) {
+      if ((rc = ensure(c, c->dzbar, 4 * sizeof(unsigned)))) return rc;
+      CUDA_TRY(c, cudaMemset(c->dzbar.p, 0, 4 * sizeof(unsigned)));
+    }
+  }
   return MCP_OK;
 }
 
@@ -652,9 +715,81 @@ int enqueue_tails_batched(mcp_ctx* c, int d, int r, int k, const double* xs, int
   return MCP_OK;
 }
 
+// The whole evaluation in one cooperative launch (small problems, csrc/k1z_small.cuh).
+static int enqueue_fg_small(mcp_ctx* c, const EvalPlan& pl, const double* dx,
+                            const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
+  MCP_NVTX("K1Z single-launch f+grad");
+  const K1ZPlan& z = pl.z;
+  K1ZParams prm;
+  prm.V = c->gV ? c->gV : c->dV;
+  prm.ldv = c->gV ? c->gldv : c->ldv;
+  prm.idx = c->gV ? c->gidx : nullptr;
+  prm.it_dev = c->gV ? c->git : nullptr;
+  prm.nu = c->dnu;
+  prm.nu_const = c->nu_const;
+  prm.x = dx;
+  prm.alpha_dev = alpha_dev;
+  prm.alpha_host = alpha;
+  prm.part = (double*)c->dYpart.p;
+  prm.bar = (unsigned*)c->dzbar.p;
+  prm.out = dout;
+  prm.p = c->p;
+  prm.n = (int)c->n;
+  prm.r = pl.r;
+  prm.d = pl.d;
+  prm.rows_per_cta = z.rows_per_cta;
+  prm.R = z.R;
+  prm.ns = z.ns;
+  prm.np = z.np;
+  prm.IB = z.IB;
+  prm.LG = z.LG;
+  prm.PS = z.PS;
+  const bool f64 = (c->gV ? c->gdtype : c->dtype) == MCP_F64;
+  void (*fn)(const K1ZParams) = nullptr;
+#define MCP_K1Z_PICK(TV, RP_, NI_)                                                         \
+  fn = z.KQ == 1 ? k1z_fg_small<TV, RP_, NI_, 1>                                           \
+                 : (z.KQ == 2 ? k1z_fg_small<TV, RP_, NI_, 2> : k1z_fg_small<TV, RP_, NI_, 4>)
+  if (f64) {
+    if (z.RP == 8 && z.NI == 1) MCP_K1Z_PICK(double, 8, 1);
+    else if (z.RP == 8) MCP_K1Z_PICK(double, 8, 2);
+    else if (z.NI == 1) MCP_K1Z_PICK(double, 16, 1);
+    else MCP_K1Z_PICK(double, 16, 2);
+  } else {
+    if (z.RP == 8 && z.NI == 1) MCP_K1Z_PICK(float, 8, 1);
+    else if (z.RP == 8) MCP_K1Z_PICK(float, 8, 2);
+    else if (z.NI == 1) MCP_K1Z_PICK(float, 16, 1);
+    else MCP_K1Z_PICK(float, 16, 2);
+  }
+#undef MCP_K1Z_PICK
+  if (!ensure_dyn_smem((const void*)fn, z.smem))
+    return c->fail(MCP_ERR_CUDA, "K1Z: cannot raise the dynamic shared-memory limit");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)z.G);
+  cfg.blockDim = dim3(K1Z_T);
+  cfg.dynamicSmemBytes = z.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;   // every CTA resident: the grid barrier is safe
+  attr[0].val.cooperative = MCP_CFG_K1Z_COOP;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto* ev = timing_begin(c, s);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, prm);
+  timing_end(ev, s);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return c->fail(MCP_ERR_CUDA, std::string("K1Z launch failed: ") + cudaGetErrorString(e));
+  }
+  c->last_launches = 1;
+  c->variant = z.name;
+  return MCP_OK;
+}
+
 int enqueue_fg_full(mcp_ctx* c, const EvalPlan& pl, const double* dx, const double* alpha_dev,
                     double alpha, double* dout, cudaStream_t s) {
   const int r = pl.r;
+  if (pl.mode == MCP_MODE_FP64 && pl.z.on)
+    return enqueue_fg_small(c, pl, dx, alpha_dev, alpha, dout, s);
   if (pl.mode != MCP_MODE_FP64 || !k1_fuses_tail(pl.k1, c->n, r) || !c->opt_fused_tail) {
     int rc = enqueue_partial(c, pl, dx, (double*)c->dYw.p, s);
     if (rc) return rc;
@@ -746,6 +881,9 @@ int run_host_eval(mcp_ctx* c, int d, int r, int mode, const double* lam, const d
     CUDA_TRY(c, ce);
     CUDA_TRY(c, cudaGraphInstantiate(&ge.exec, ge.graph, 0));
     it = c->graphs.emplace(key, ge).first;
+  } else if (pl.mode == MCP_MODE_FP64 && pl.z.on) {
+    c->last_launches = 1;
+    c->variant = pl.z.name;
   } else {
     c->last_launches =
         (pl.mode == MCP_MODE_FP64 && k1_fuses_tail(pl.k1, c->n, r) && c->opt_fused_tail)
@@ -883,7 +1021,7 @@ void release_ctx(mcp_ctx* c) {
   drop_graphs(c);
   DevBuf* bufs[] = {&c->dx, &c->dout, &c->dYw, &c->dAfrag, &c->dYpart, &c->dwpart,
                     &c->dG, &c->dC, &c->dpart, &c->dscalar, &c->dflag, &c->dAt,
-                    &c->dticket};
+                    &c->dticket, &c->dzbar};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->own_v32 && c->dV32) cudaFree(c->dV32);
@@ -1294,6 +1432,10 @@ int mcp_set_option(mcp_ctx* c, int key, int64_t value) {
     case MCP_OPT_FUSED_TAIL:
       if (c->opt_fused_tail != (value != 0)) drop_graphs(c);
       c->opt_fused_tail = value != 0;
+      return MCP_OK;
+    case MCP_OPT_SMALL_KERNEL:
+      if (c->opt_small_kernel != (value != 0)) drop_graphs(c);
+      c->opt_small_kernel = value != 0;
       return MCP_OK;
     default:
       return c->fail(MCP_ERR_ARG, "unknown option " + std::to_string(key));

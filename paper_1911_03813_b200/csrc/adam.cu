@@ -105,11 +105,12 @@ struct AdamRun {
   int64_t* h_idx = nullptr;
   double* h_bc = nullptr;
   double* h_scal = nullptr;  // [lr, f_est]
-  GraphEntry g_iter, g_est;
+  GraphEntry g_iter, g_chunk, g_est;   // one iteration, ITER_CHUNK iterations, the estimate
+  int64_t chunk_iters = 0;
   AdamScalars sc{};
 
   ~AdamRun() {
-    for (GraphEntry* g : {&g_iter, &g_est}) {
+    for (GraphEntry* g : {&g_iter, &g_chunk, &g_est}) {
       if (g->exec) cudaGraphExecDestroy(g->exec);
       if (g->graph) cudaGraphDestroy(g->graph);
     }
@@ -194,28 +195,51 @@ struct AdamRun {
     nb = grid_for(N, AD_T, 2 * c->sms);
     int rc;
     if ((rc = make_view(&vb, &Vb, batch)) || (rc = make_view(&ve, &Ve, n_est))) return rc;
+    if ((rc = alloc(idx, epoch_len * batch)) || (rc = alloc(it_dev, 1))) return rc;
+    if (mode == MCP_MODE_FP64) {
+      // K1Z (when the batch plans to it) reads the batch rows in place through the index list
+      vb->gV = c->dV;
+      vb->gldv = c->ldv;
+      vb->gdtype = c->dtype;
+      vb->gidx = idx;
+      vb->git = it_dev;
+    }
     if ((rc = plan_eval(vb, d, r, mode, plb))) return c->fail(rc, vb->err);
     if ((rc = plan_eval(ve, d, r, mode, ple))) return c->fail(rc, ve->err);
     if ((rc = alloc(X, N)) || (rc = alloc(XB, N)) || (rc = alloc(M1, N)) || (rc = alloc(M2, N)) ||
         (rc = alloc(OB, N + 1)) || (rc = alloc(OE, N + 1)) || (rc = alloc(bc, 2 * epoch_len)) ||
-        (rc = alloc(lr_dev, 1)) || (rc = alloc(idx, epoch_len * batch)) ||
-        (rc = alloc(eidx, n_est)) || (rc = alloc(it_dev, 1)) || (rc = alloc(counter, 1)))
+        (rc = alloc(lr_dev, 1)) || (rc = alloc(eidx, n_est)) || (rc = alloc(counter, 1)))
       return rc;
     CUDA_TRY(c, cudaMemset(counter, 0, sizeof(unsigned)));
     CUDA_TRY(c, cudaMallocHost(&h_idx, sizeof(int64_t) * std::max(epoch_len * batch, n_est)));
     CUDA_TRY(c, cudaMallocHost(&h_bc, sizeof(double) * 2 * epoch_len));
     CUDA_TRY(c, cudaMallocHost(&h_scal, sizeof(double) * 4));
     cudaStream_t s = c->stream;
-    if ((rc = capture(g_iter, [&]() -> int {
-           int e = enqueue_gather(Vb, batch, idx, it_dev, vb->ldv);
-           if (e) return e;
-           if ((e = fg_on(vb, plb, X, OB))) return e;
-           CUDA_TRY(c, launch_pdl(k_adam_step, dim3(nb), dim3(AD_T), 0, s, N, (const double*)OB,
-                                  X, M1, M2, (const double*)bc, (const double*)lr_dev, sc, it_dev,
-                                  counter));
-           return MCP_OK;
-         })))
-      return rc;
+    auto one_iteration = [&]() -> int {
+      int e = MCP_OK;
+      // no gathered copy when the single-launch kernel reads the rows through the index
+      if (!(mode == MCP_MODE_FP64 && plb.z.on)) e = enqueue_gather(Vb, batch, idx, it_dev, vb->ldv);
+      if (e) return e;
+      if ((e = fg_on(vb, plb, X, OB))) return e;
+      CUDA_TRY(c, launch_pdl(k_adam_step, dim3(nb), dim3(AD_T), 0, s, N, (const double*)OB, X, M1,
+                             M2, (const double*)bc, (const double*)lr_dev, sc, it_dev, counter));
+      return MCP_OK;
+    };
+    if ((rc = capture(g_iter, one_iteration))) return rc;
+    // the iteration cursor lives on the device, so iterations are identical graph nodes: an epoch
+    // replays a graph of up to ITER_CHUNK iterations (one host launch instead of one per
+    // iteration) plus single iterations for the remainder
+    chunk_iters = std::min<int64_t>(epoch_len, MCP_CFG_ADAM_ITER_CHUNK);
+    if (chunk_iters > 1) {
+      if ((rc = capture(g_chunk, [&]() -> int {
+             for (int64_t k = 0; k < chunk_iters; ++k) {
+               int e = one_iteration();
+               if (e) return e;
+             }
+             return MCP_OK;
+           })))
+        return rc;
+    }
     if ((rc = capture(g_est, [&]() -> int {
            int e = fg_on(ve, ple, X, OE);
            if (e) return e;
@@ -376,7 +400,13 @@ extern "C" int mcp_adam(mcp_ctx* c, int d, int r, int mode, const double* x0, co
                                 cudaMemcpyHostToDevice, s));
     CUDA_TRY(c, cudaMemcpyAsync(R.lr_dev, R.h_scal, sizeof(double), cudaMemcpyHostToDevice, s));
     CUDA_TRY(c, cudaMemsetAsync(R.it_dev, 0, sizeof(int), s));
-    for (int64_t k = 0; k < epoch_len; ++k) CUDA_TRY(c, cudaGraphLaunch(R.g_iter.exec, s));
+    {
+      int64_t k = 0;
+      if (R.chunk_iters > 1)
+        for (; k + R.chunk_iters <= epoch_len; k += R.chunk_iters)
+          CUDA_TRY(c, cudaGraphLaunch(R.g_chunk.exec, s));
+      for (; k < epoch_len; ++k) CUDA_TRY(c, cudaGraphLaunch(R.g_iter.exec, s));
+    }
     t += epoch_len;
     n_iter += epoch_len;
     double f_est = 0.0;

@@ -49,6 +49,7 @@ struct mcp_ctx {
 
   mcp_internal::DevBuf dx, dout, dYw, dAfrag, dYpart, dwpart, dG, dC, dpart, dscalar, dflag;
   mcp_internal::DevBuf dticket;  // K3 last-block ticket of the fused peer publication
+  mcp_internal::DevBuf dzbar;    // K1Z grid barrier: arrivals, generation, error flag (zeroed)
   void* hx = nullptr;
   size_t hx_bytes = 0;
   void* hout = nullptr;
@@ -80,6 +81,16 @@ struct mcp_ctx {
   std::string variant = "none";
   // run-time options (mcp_set_option)
   bool opt_fused_tail = true;   // MCP_OPT_FUSED_TAIL: K1 -> fused reduce+finish when eligible
+  bool opt_small_kernel = true; // MCP_OPT_SMALL_KERNEL: small problems in one launch (K1Z)
+
+  // optional row indirection of a view (stochastic path): row l of this view is row
+  // gidx[*git * p + l] of gV (the parent's resident set); K1Z reads the rows in place and the
+  // gathered copy in dV is only made for the other kernels
+  const void* gV = nullptr;
+  int64_t gldv = 0;
+  int gdtype = MCP_F64;
+  const int64_t* gidx = nullptr;
+  const int* git = nullptr;
 
   // cached device-resident L-BFGS workspace (lbfgs.cu); freed with the graphs
   void* lbfgs_ws = nullptr;
@@ -123,10 +134,19 @@ struct K1TPlan {
   size_t smem = 0;
 };
 
+// Shape of the single-launch small-problem evaluation (K1Z, csrc/k1z_small.cuh).
+struct K1ZPlan {
+  bool on = false;
+  int G = 0, rows_per_cta = 0, R = 0, ns = 0, np = 0, RP = 0, NI = 0, KQ = 1, IB = 0, LG = 0, PS = 0;
+  size_t smem = 0;
+  std::string name;
+};
+
 // Shape of one evaluation's K1 launch.
 struct EvalPlan {
   mcp::K1Variant k1;
   K1TPlan t;
+  K1ZPlan z;
   int mode = MCP_MODE_FP64;
   int d = 0, r = 0;
 };

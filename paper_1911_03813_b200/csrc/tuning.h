@@ -16,6 +16,32 @@
 #ifndef MCP_CFG_HOST_MEMCPY
 #define MCP_CFG_HOST_MEMCPY 0
 #endif
+// K1Z: FP64 evaluations with r <= 16, n <= 512 and at most MCP_CFG_K1Z_MAX_WORK = p n r
+// multiply-adds per GEMM run as ONE cooperative launch (csrc/k1z_small.cuh)
+#ifndef MCP_CFG_K1Z
+#define MCP_CFG_K1Z 1
+#endif
+#ifndef MCP_CFG_K1Z_MAX_WORK
+#define MCP_CFG_K1Z_MAX_WORK (1ll << 24)
+#endif
+// K1Z launch: cooperative (every CTA resident by contract: the grid barrier cannot deadlock
+// against other kernels) or a plain launch (experiment builds, timing only)
+#ifndef MCP_CFG_K1Z_COOP
+#define MCP_CFG_K1Z_COOP 1
+#endif
+#ifndef MCP_CFG_K1Z_MAXG
+#define MCP_CFG_K1Z_MAXG 0         // cap on K1Z's CTAs (0: one per SM)
+#endif
+#ifndef MCP_K1Z_PROF
+#define MCP_K1Z_PROF 0             // per-phase clock stamps printed by three CTAs (experiment builds)
+#endif
+#ifndef MCP_K1Z_KO
+#define MCP_K1Z_KO 0               // timing knockouts (wrong results), experiment builds only
+#endif
+// stochastic path: Adam iterations per replayed graph (1: one graph launch per iteration)
+#ifndef MCP_CFG_ADAM_ITER_CHUNK
+#define MCP_CFG_ADAM_ITER_CHUNK 128
+#endif
 // FP64 K1 family for n <= 128: K1Q (warp-specialised pairs), then K1P, then K1S fallbacks
 #ifndef MCP_CFG_K1Q
 #define MCP_CFG_K1Q 1

@@ -1,0 +1,116 @@
+"""K1Z, the single-launch small-problem f+grad (csrc/k1z_small.cuh), through the C ABI.
+
+* against the CPU oracle over shapes that cover both GEMM2 thread maps (row groups for small n,
+  two variables per thread for n > 256), both column paddings (r <= 8, r <= 16), one and many
+  CTAs, ragged last CTAs, several slabs per CTA, the 1 / 2 / 4-way k splits of GEMM1, fp32 and
+  fp64 rows, explicit weights, d = 2..6 -- term-scale <= 1e-10 (pkg/tests/test_acceptance.py:65-74);
+* against the general K1 -> reduce+finish chain (MCP_OPT_SMALL_KERNEL = 0) to 1e-13;
+* repeated evaluations bit-identical, gradients bitwise independent of alpha, lambda = 0 exact
+  (test_objective.py:101-121);
+* a sampled set evaluates to the bits of an uploaded copy of the same rows (the split depends
+  on the shape only); the device Adam reads its mini-batch rows through the index list, which
+  tests/test_gpu_stochastic.py pins bitwise against evaluations of uploaded copies.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1911_03813_b200 as mcp
+from paper_1911_03813_b200 import _native
+from oracle import momentcp_oracle as om
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    # n, r, d, p, dtype, weighted
+    (20, 5, 3, 10_000, np.float64, False),    # config 1: 105 CTAs, row groups of 32 variables
+    (20, 5, 3, 37, np.float64, True),         # two CTAs, the second ragged
+    (7, 1, 2, 5, np.float64, False),          # one CTA, one column
+    (100, 10, 4, 3_000, np.float64, True),    # RP = 16, 128 variable slots x 2 row groups
+    (130, 16, 6, 2_000, np.float64, False),   # one variable per thread, all 16 columns
+    (500, 10, 3, 1_000, np.float64, False),   # the paper's Table 2 mini-batch: NI = 2
+    (500, 10, 3, 10, np.float64, False),
+    (512, 16, 3, 1_900, np.float64, True),    # largest n and r, one slab of 32 rows per CTA
+    (257, 3, 5, 700, np.float32, False),      # fp32 rows, NI = 2, RP = 8
+    (33, 8, 4, 20_000, np.float32, True),     # fp32 rows, 160 rows per CTA
+    (64, 2, 3, 100_000, np.float64, False),   # 704 rows per CTA
+    (512, 6, 3, 5_000, np.float64, False),    # 64 rows per CTA in two slabs of 32
+    (300, 12, 4, 150, np.float64, True),      # k split over 4 threads, 8-row passes, ragged
+]
+
+
+def _instance(k, n, r, d, p, dtype, weighted):
+    rng = np.random.default_rng(1000 + k)
+    V = (rng.standard_normal((n, p)) / np.sqrt(n)).astype(dtype)
+    nu = (rng.random(p) + 0.5) / p if weighted else None
+    lam = rng.standard_normal(r)
+    A = rng.standard_normal((n, r)) / np.sqrt(n)
+    return V, nu, lam, A, 0.375
+
+
+def _check(res, V, nu, lam, A, d, alpha, tol):
+    V64 = V.astype(np.float64)
+    nu_ = np.full(V.shape[1], 1.0 / V.shape[1]) if nu is None else nu
+    f, gl, gA = om.fg_implicit(V64, nu_, lam, A, d, alpha)
+    f_s, gl_s, gA_s, _ = om.term_scales(V64, nu_, lam, A, d, alpha)
+    e = max(om.term_rel_err(res.f, f, f_s), om.term_rel_err(res.g_lam, gl, gl_s),
+            om.term_rel_err(res.g_A, gA, gA_s))
+    assert e <= tol, e
+
+
+@pytest.mark.parametrize("k", range(len(SHAPES)))
+def test_k1z_vs_oracle_and_general_chain(k):
+    n, r, d, p, dtype, weighted = SHAPES[k]
+    V, nu, lam, A, alpha = _instance(k, *SHAPES[k])
+    obs = mcp.ObservationSet(V, nu)
+    ctx = obs.device_context()
+    res = mcp.fg_implicit(obs, lam, A, d, alpha)
+    assert ctx.last_variant.startswith("k1z_fg_small"), ctx.last_variant
+    assert ctx.last_launch_count == 1
+    _check(res, V, nu, lam, A, d, alpha, 1e-10)
+    again = mcp.fg_implicit(obs, lam, A, d, alpha)
+    assert again.f == res.f and np.array_equal(again.g_lam, res.g_lam)
+    assert np.array_equal(again.g_A, res.g_A)
+    shifted = mcp.fg_implicit(obs, lam, A, d, alpha + 3.0)
+    assert np.array_equal(shifted.g_lam, res.g_lam) and np.array_equal(shifted.g_A, res.g_A)
+    zero = mcp.fg_implicit(obs, np.zeros(r), A, d, alpha)
+    assert zero.f == alpha and np.array_equal(zero.g_A, np.zeros_like(A))
+    ctx.set_option(_native.MCP_OPT_SMALL_KERNEL, 0)
+    try:
+        gen = mcp.fg_implicit(obs, lam, A, d, alpha)
+        assert not ctx.last_variant.startswith("k1z"), ctx.last_variant
+    finally:
+        ctx.set_option(_native.MCP_OPT_SMALL_KERNEL, 1)
+    V64 = V.astype(np.float64)
+    nu_ = np.full(p, 1.0 / p) if nu is None else nu
+    f_s, gl_s, gA_s, _ = om.term_scales(V64, nu_, lam, A, d, alpha)
+    e = max(om.term_rel_err(res.f, gen.f, f_s), om.term_rel_err(res.g_lam, gen.g_lam, gl_s),
+            om.term_rel_err(res.g_A, gen.g_A, gA_s))
+    assert e <= 1e-13, e
+
+
+def test_k1z_limits_fall_back_to_the_general_chain():
+    rng = np.random.default_rng(5)
+    for n, r, p in ((40, 17, 500), (513, 4, 300), (100, 10, 40_000)):
+        V = rng.standard_normal((n, p)) / np.sqrt(n)
+        obs = mcp.ObservationSet(V)
+        lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)
+        res = mcp.fg_implicit(obs, lam, A, 3, 0.0)
+        assert not obs.device_context().last_variant.startswith("k1z")
+        _check(res, V, None, lam, A, 3, 0.0, 1e-10)
+
+
+def test_k1z_sampled_set_equals_uploaded_copy_bitwise():
+    """sample_observations -> fg equals, bitwise, the evaluation of an uploaded copy of the same
+    rows (objective.py:97-113): the work split is a function of the shape only."""
+    rng = np.random.default_rng(8)
+    for n, r, d, p, s in ((20, 5, 3, 4_000, 300), (500, 10, 3, 3_000, 1_000), (64, 8, 4, 900, 7)):
+        V = rng.standard_normal((n, p)) / np.sqrt(n)
+        obs = mcp.ObservationSet(V)
+        lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)
+        sub = mcp.sample_observations(obs, s, np.random.default_rng(77))
+        idx = np.random.default_rng(77).integers(0, p, size=s)
+        a = mcp.fg_implicit(sub, lam, A, d, 0.5)
+        b = mcp.fg_implicit(mcp.ObservationSet(V[:, idx]), lam, A, d, 0.5)
+        assert a.f == b.f and np.array_equal(a.g_lam, b.g_lam) and np.array_equal(a.g_A, b.g_A)
+        _check(a, V[:, idx], None, lam, A, d, 0.5, 1e-10)

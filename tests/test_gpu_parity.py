@@ -337,7 +337,8 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
     """The sharded building blocks on one rank: partial (K1 + reduce) then finish (K4) must
     reproduce the single-call evaluation bitwise, with and without the fused reduce + finish
     (K3F forms G, C, M, u in-kernel in the same expression order as K4), over orders d and
-    ranks up to K3F's limit r = 32."""
+    ranks up to K3F's limit r = 32.  The single-launch small-problem kernel (K1Z) is switched
+    off for the bitwise part: it sums in its own fixed order and is compared to 1e-13."""
 
     import torch
 
@@ -353,6 +354,13 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
         x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
         s = _native.stream_handle(torch.cuda.current_stream())
         outs = []
+        o_small = torch.empty(1 + r + n * r, dtype=torch.float64, device="cuda")
+        ctx.fg_device(d, r, x.data_ptr(), 0.25, None, o_small.data_ptr(), s)
+        small = ctx.last_variant.startswith("k1z")
+        assert small == (r <= 16), ctx.last_variant
+        res = mcp.fg_implicit(obs, lam, A, d, 0.25)
+        assert float(o_small[0]) == res.f
+        ctx.set_option(_native.MCP_OPT_SMALL_KERNEL, 0)
         for fused in (True, False):
             ctx.set_option(_native.MCP_OPT_FUSED_TAIL, 1 if fused else 0)
             try:
@@ -367,9 +375,17 @@ def test_partial_then_finish_equals_single_evaluation_bitwise():
                 outs.append(o1.cpu())
             finally:
                 ctx.set_option(_native.MCP_OPT_FUSED_TAIL, 1)
+        ctx.set_option(_native.MCP_OPT_SMALL_KERNEL, 1)
         assert torch.equal(outs[0], outs[1]), (n, r, d)
         res = mcp.fg_implicit(obs, lam, A, d, 0.25)
-        assert float(outs[0][0]) == res.f
+        if small:
+            f_s, gl_s, gA_s, _ = om.term_scales(V, _nu(V, None), lam, A, d, 0.25)
+            got, want = o_small.cpu().numpy(), outs[0].numpy()
+            assert _err(got[0], want[0], f_s) <= 1e-13
+            assert _err(got[1:1 + r], want[1:1 + r], gl_s) <= 1e-13
+            assert _err(got[1 + r:], want[1 + r:], gA_s.reshape(-1, order="F")) <= 1e-13
+        else:
+            assert float(outs[0][0]) == res.f
 
 
 def test_peer_exchange_kernels_two_virtual_ranks():

@@ -48,6 +48,8 @@ def main():
             "workload": "t2 (paper Table 2)", "batch": s,
             "device": {"inner_iters": rep.n_fg, "epochs": len(rep.trace) - 1, "s": td,
                        "iters_per_s": rep.n_fg / td, "us_per_iter": 1e6 * td / rep.n_fg,
+                       # epochs only (sampling callback + graph replays + estimate), no set-up
+                       "us_per_iter_steady": 1e6 * (rep.trace[-1][1] - rep.trace[0][1]) / rep.n_fg,
                        "reason": rep.reason, "f": rep.f},
             "cpu_port": {"inner_iters": host["n_iter"], "s": th,
                          "iters_per_s": host["n_iter"] / th, "us_per_iter": 1e6 * th / host["n_iter"],

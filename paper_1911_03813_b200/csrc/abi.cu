@@ -423,42 +423,36 @@ static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
   const int dtype = c->gV ? c->gdtype : c->dtype;
   const size_t esz = dtype == MCP_F64 ? 8 : 4;
   z.RP = r <= 8 ? 8 : 16;
-  z.NI = n > 256 ? 2 : 1;
-  if (n > 128) {
-    z.IB = 256;
-  } else {
-    z.IB = 32;
-    while (z.IB < n) z.IB *= 2;
-  }
-  z.LG = K1Z_T / z.IB;
-  int64_t ns = n;
-  if (dtype == MCP_F64) {
-    while (ns % 16 != 4) ++ns;
-  } else {
-    while (ns % 32 != 8) ++ns;
-  }
+  // staged rows: conflict-free 8 x 4 DMMA fragment loads (== 4 mod 16 doubles / mod 32 floats)
+  const int64_t n4 = round_up(n, (int64_t)4);
+  const int64_t mod = dtype == MCP_F64 ? 16 : 32;
+  int64_t ns = n4;
+  while (ns % mod != 4) ++ns;
   z.ns = (int)ns;
+  z.np = (int)(n4 | 1);
   const int64_t max_g = MCP_CFG_K1Z_MAXG > 0 ? std::min<int64_t>(MCP_CFG_K1Z_MAXG, c->sms) : c->sms;
-  // few rows per CTA: GEMM1 splits k over 2 or 4 threads so a pass covers 16 or 8 rows
+  // GEMM1 pass height: 8, 16 or 32 rows (1, 2 or 4 DMMA row tiles sharing the factor fragments)
   const int64_t rpc0 = ceil_div(p, max_g);
-  z.KQ = rpc0 <= 8 ? 4 : (rpc0 <= 16 ? 2 : 1);
-  const int64_t RS = 32 / z.KQ;
-  z.rows_per_cta = (int)round_up(rpc0, RS);
-  z.G = (int)ceil_div(p, (int64_t)z.rows_per_cta);
-  z.PS = (int)round_up(n * r + r, (int64_t)2);
-  z.np = (int)(n | 1);
-  const size_t fixed = sizeof(double) * ((size_t)z.np * z.RP + 32 * z.RP +
-                                         2 * K1Z_MAXR * K1Z_MAXR + 2 * K1Z_T + 3 * z.RP);
-  const size_t combine = z.LG > 1 ? sizeof(double) * (size_t)K1Z_T * z.RP : 0;
   const size_t budget = 226 * 1024;
   const size_t per_row = ns * esz + sizeof(double) * z.RP;
-  if (fixed + std::max(combine, (size_t)RS * per_row) > budget) return false;
-  const int64_t Rmax = (int64_t)((budget - fixed) / per_row) / RS * RS;
-  z.R = (int)std::min<int64_t>(z.rows_per_cta, Rmax);
-  z.smem = fixed + sizeof(double) * (size_t)z.R * z.RP +
-           std::max(combine, (size_t)z.R * ns * esz);
+  for (z.MT1 = rpc0 <= 8 ? 1 : (rpc0 <= 16 ? 2 : 4); z.MT1 >= 1; z.MT1 /= 2) {
+    const int64_t RS = 8 * z.MT1;
+    const size_t fixed =
+        sizeof(double) * ((size_t)z.np * z.RP +
+                          (size_t)K1Z_NW * std::max<int64_t>(RS, z.RP) * z.RP + 3 * K1Z_T +
+                          2 * K1Z_MAXR * K1Z_MAXR + 3 * z.RP) + 8 * esz;
+    if (fixed + (size_t)RS * per_row > budget) continue;   // a lower pass height may fit
+    z.rows_per_cta = (int)round_up(rpc0, RS);
+    z.G = (int)ceil_div(p, (int64_t)z.rows_per_cta);
+    const int64_t Rmax = (int64_t)((budget - fixed) / per_row) / RS * RS;
+    z.R = (int)std::min<int64_t>(z.rows_per_cta, Rmax);
+    z.smem = fixed + (size_t)z.R * per_row;
+    break;
+  }
+  if (z.MT1 < 1) return false;
+  z.PS = (int)round_up(n * r + r, (int64_t)2);
   z.name = std::string("k1z_fg_small<") + (dtype == MCP_F64 ? "f64" : "f32") +
-           ",RP=" + std::to_string(z.RP) + ",NI=" + std::to_string(z.NI) + ",KQ=" + std::to_string(z.KQ) +
+           ",RP=" + std::to_string(z.RP) + ",MT1=" + std::to_string(z.MT1) +
            ",G=" + std::to_string(z.G) + ",R=" + std::to_string(z.R) + ">";
   z.on = true;
   return true;
@@ -741,24 +735,18 @@ static int enqueue_fg_small(mcp_ctx* c, const EvalPlan& pl, const double* dx,
   prm.R = z.R;
   prm.ns = z.ns;
   prm.np = z.np;
-  prm.IB = z.IB;
-  prm.LG = z.LG;
   prm.PS = z.PS;
   const bool f64 = (c->gV ? c->gdtype : c->dtype) == MCP_F64;
   void (*fn)(const K1ZParams) = nullptr;
-#define MCP_K1Z_PICK(TV, RP_, NI_)                                                         \
-  fn = z.KQ == 1 ? k1z_fg_small<TV, RP_, NI_, 1>                                           \
-                 : (z.KQ == 2 ? k1z_fg_small<TV, RP_, NI_, 2> : k1z_fg_small<TV, RP_, NI_, 4>)
+#define MCP_K1Z_PICK(TV, RP_)                                                    \
+  fn = z.MT1 == 1 ? k1z_fg_small<TV, RP_, 1>                                     \
+                  : (z.MT1 == 2 ? k1z_fg_small<TV, RP_, 2> : k1z_fg_small<TV, RP_, 4>)
   if (f64) {
-    if (z.RP == 8 && z.NI == 1) MCP_K1Z_PICK(double, 8, 1);
-    else if (z.RP == 8) MCP_K1Z_PICK(double, 8, 2);
-    else if (z.NI == 1) MCP_K1Z_PICK(double, 16, 1);
-    else MCP_K1Z_PICK(double, 16, 2);
+    if (z.RP == 8) MCP_K1Z_PICK(double, 8);
+    else MCP_K1Z_PICK(double, 16);
   } else {
-    if (z.RP == 8 && z.NI == 1) MCP_K1Z_PICK(float, 8, 1);
-    else if (z.RP == 8) MCP_K1Z_PICK(float, 8, 2);
-    else if (z.NI == 1) MCP_K1Z_PICK(float, 16, 1);
-    else MCP_K1Z_PICK(float, 16, 2);
+    if (z.RP == 8) MCP_K1Z_PICK(float, 8);
+    else MCP_K1Z_PICK(float, 16);
   }
 #undef MCP_K1Z_PICK
   if (!ensure_dyn_smem((const void*)fn, z.smem))

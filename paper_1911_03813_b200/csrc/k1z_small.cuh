@@ -13,11 +13,11 @@
 //      gathered copy).  While they fly it stages A and lam, forms G = A^T A, C = G^(d-1), the
 //      M = (A o lam) C entries of the outputs it will finish and (last CTA) u -- everything that
 //      depends on x alone;
-//   2. Z = V A (thread = row x column group x k-split, several passes interleaved and several
-//      accumulators per column: the loop is bound by the DFMA latency, not its rate),
-//      P = nu Z^(d-1) and its share of w, then Y_b = V^T P (thread = variable(s) x all columns,
-//      P broadcast from shared memory), all in plain DFMA -- on B200 DFMA and DMMA share one
-//      FP64 pipe rate and there is too little work to fill either;
+//   2. Z = V A by DMMA.8x8x4 in passes of 8 / 16 / 32 rows, k split over the 8 warps and the
+//      partial Z summed in warp order through shared memory (plain DFMA loops measured bound by
+//      shared-memory wavefronts: 13 FMA per wavefront against 64 for DMMA fragments);
+//      P = nu Z^(d-1) and its share of w; then Y_b = V^T P by DMMA, warp w owning the 8-variable
+//      tiles w, w + 8, ... with Y_b in registers across passes and slabs;
 //   3. writes [Y_b ; w_b] to its partial slot and arrives on a grid barrier (bounded spin);
 //   4. after the barrier the outputs are split over the CTAs: each output sums its G partials
 //      in a fixed (slot-strided, then sequential) order and is finished in place --
@@ -55,11 +55,10 @@ struct K1ZParams {
   double* out = nullptr;          // [f ; g_lam ; vec_F(g_A)]
   int64_t p = 0;
   int n = 0, r = 0, d = 0;
-  int rows_per_cta = 0;           // contiguous rows per CTA (multiple of 32 / KQ)
-  int R = 0;                      // slab rows staged at once (multiple of 32 / KQ)
+  int rows_per_cta = 0;           // contiguous rows per CTA (multiple of the pass height)
+  int R = 0;                      // slab rows staged at once (multiple of the pass height)
   int ns = 0;                     // shared-memory row pitch of a staged row (elements)
   int np = 0;                     // shared-memory pitch of a factor column (doubles, odd)
-  int IB = 0, LG = 0;             // GEMM2 map: IB variable slots x LG row groups (IB * LG = 256)
   int PS = 0;                     // partial slot pitch (doubles)
 };
 
@@ -106,112 +105,54 @@ __device__ __forceinline__ void k1z_reduce(const double* part, int PS, int G, in
   }
 }
 
-// TV: element type of V.  RP: padded factor columns (8 or 16).  NI: variables per thread in
-// GEMM2 (2 for n > 256).  KQ: k-splits of GEMM1 (a pass covers 32 / KQ rows).
+// TV: element type of V.  RP: padded factor columns (8 or 16).  MT1: 8-row DMMA tiles per
+// GEMM1 pass (a pass covers 8 MT1 rows).
 #if MCP_K1Z_PROF
 #define K1Z_STAMP(k) do { if (threadIdx.x == 0) stamps[k] = clock64(); } while (0)
 #else
 #define K1Z_STAMP(k) do { } while (0)
 #endif
 
-// One GEMM1 pass group: SB passes of RS rows interleaved (shared factor loads), U accumulators
-// per (row, column).  z[s][c] = sum over this thread's k-split of v_l[i] a_c[i], U-way split in
-// i order, combined ((u0 + u1) + (u2 + u3)).
-template <typename TV, int RP, int KQ, int SB, int U>
-__device__ __forceinline__ void k1z_gemm1(const TV* __restrict__ sV, const double* __restrict__ sAT,
-                                          int n, int ns, int np, int R, int sub0, int rl, int kq,
-                                          int jg, double (&zz)[SB][RP / 8]) {
-  constexpr int CPT = RP / 8, RS = 32 / KQ;
-  const TV* vr[SB];
-#pragma unroll
-  for (int s = 0; s < SB; ++s) {
-    const int l = sub0 + s * RS + rl;
-    vr[s] = sV + (size_t)(l < R ? l : 0) * ns;
-  }
-  const double* ar = sAT + (size_t)(jg * CPT) * np;   // column jg CPT + c at ar + c np
-  double z[SB][CPT][U];
-#pragma unroll
-  for (int s = 0; s < SB; ++s)
-#pragma unroll
-    for (int c = 0; c < CPT; ++c)
-#pragma unroll
-      for (int u = 0; u < U; ++u) z[s][c][u] = 0.0;
-  int i = kq;
-  for (; i + (U - 1) * KQ < n; i += U * KQ) {
-    double av[U][CPT];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) av[u][c] = ar[(size_t)c * np + i + u * KQ];
-#pragma unroll
-    for (int s = 0; s < SB; ++s)
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const double v = to_f64(vr[s][i + u * KQ]);
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) z[s][c][u] = fma(v, av[u][c], z[s][c][u]);
-      }
-  }
-#pragma unroll
-  for (int u = 0; u < U - 1; ++u) {
-    if (i + u * KQ < n) {
-#pragma unroll
-      for (int s = 0; s < SB; ++s) {
-        const double v = to_f64(vr[s][i + u * KQ]);
-#pragma unroll
-        for (int c = 0; c < CPT; ++c)
-          z[s][c][u] = fma(v, ar[(size_t)c * np + i + u * KQ], z[s][c][u]);
-      }
-    }
-  }
-#pragma unroll
-  for (int s = 0; s < SB; ++s)
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      double t;
-      if (U == 4)
-        t = (z[s][c][0] + z[s][c][1]) + (z[s][c][U / 2] + z[s][c][U - 1]);
-      else
-        t = z[s][c][0] + z[s][c][U - 1];
-      if (KQ >= 2) t += __shfl_xor_sync(0xffffffffu, t, 8);
-      if (KQ == 4) t += __shfl_xor_sync(0xffffffffu, t, 16);
-      zz[s][c] = t;
-    }
-}
+constexpr int K1Z_NW = K1Z_T / 32;
+constexpr int K1Z_MAXMT = K1Z_MAXN / 8 / K1Z_NW;   // GEMM2 m-tiles per warp
 
-template <typename TV, int RP, int NI, int KQ>
+template <typename TV, int RP, int MT1>
 __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
-  constexpr int CPT = RP / 8;   // GEMM1 columns per thread
-  constexpr int RS = 32 / KQ;   // rows per GEMM1 pass
+  constexpr int NT = RP / 8;      // 8-column DMMA tiles
+  constexpr int RS = 8 * MT1;     // rows per GEMM1 pass
+  constexpr int NW = K1Z_NW;
 #if MCP_K1Z_PROF
   long long stamps[12];
   K1Z_STAMP(0);
 #endif
   extern __shared__ __align__(16) unsigned char k1z_smem[];
   const int tid = threadIdx.x, G = gridDim.x, b = blockIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int n = a.n, r = a.r, d = a.d, ns = a.ns, np = a.np, R = a.R;
+  const int n4 = (n + 3) & ~3;
 #if MCP_K1Z_KO & 2
   if (a.n > 0) return;
 #endif
-  // the factor, column-major with an odd pitch: conflict-free both across variables (G, M,
-  // the coalesced fill) and across columns (GEMM1)
+  // the factor, column-major with an odd pitch (zero padded to np rows and RP columns):
+  // conflict-free across variables (the fill, M) and across the 8 x 4 DMMA fragment lanes
   double* sAT = reinterpret_cast<double*>(k1z_smem);         // [RP][np]
   double* sP = sAT + (size_t)RP * np;                         // [R][RP]
-  double* sW = sP + (size_t)R * RP;                           // [32][RP]
-  double* sG = sW + 32 * RP;                                  // [r][r]
+  double* sZ = sP + (size_t)R * RP;                           // [NW][max(RS, RP)][RP] partials
+  double* sW = sZ + (size_t)NW * (RS > RP ? RS : RP) * RP;    // [256]
+  double* sG = sW + K1Z_T;                                    // [r][r]
   double* sC = sG + K1Z_MAXR * K1Z_MAXR;                      // [r][r]
   double* sR = sC + K1Z_MAXR * K1Z_MAXR;                      // [256] reduce lanes
   double* sM = sR + K1Z_T;                                    // [256] M entries of my outputs
   double* sL = sM + K1Z_T;                                    // [RP] lam, zero padded
   double* sS = sL + RP;                                       // [2 RP] w, u of the finish
-  TV* sV = reinterpret_cast<TV*>(sS + 2 * RP);                // [R][ns]; later the LG combine
+  TV* sV = reinterpret_cast<TV*>(sS + 2 * RP);                // [R][ns] (+ 8 elements of slack)
   const double* __restrict__ A = a.x + r;
 
   const int64_t base = (a.idx && a.it_dev) ? (int64_t)(*a.it_dev) * a.p : 0;
   const int64_t row_lo = (int64_t)b * a.rows_per_cta;
   const int64_t row_hi = min(a.p, row_lo + a.rows_per_cta);
   constexpr int EPC = 16 / (int)sizeof(TV);          // elements per 16-byte chunk
-  const int CH = (n + EPC - 1) / EPC;
+  const int CH = n4 / EPC;                            // the source rows are zero padded past n
   auto issue_slab = [&](int64_t row0, int rows) {
     for (int c = tid; c < rows * CH; c += K1Z_T) {
       const int l = c / CH, k = c % CH;
@@ -220,63 +161,61 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
                  reinterpret_cast<const TV*>(a.V) + grow * a.ldv + k * EPC, 16);
     }
     cp_async_commit();
+    // rows of the last pass beyond the range: zeros (their P is zero; 0 x stale could be NaN)
+    const int pad_to = min(R, (rows + RS - 1) / RS * RS);
+    for (int c = rows * ns + tid; c < pad_to * ns; c += K1Z_T) sV[c] = TV(0);
   };
   // ---- the first slab's rows in flight; everything that depends on x alone meanwhile ----
   if (row_lo < row_hi) issue_slab(row_lo, (int)min((int64_t)R, row_hi - row_lo));
-#pragma unroll 8
-  for (int e = tid; e < n * r; e += K1Z_T) sAT[(size_t)(e / n) * np + e % n] = A[e];
+  // coalesced column reads: the loads of all r columns of a variable in flight before the stores
+  for (int i = tid; i < np; i += K1Z_T) {
+    double v[K1Z_MAXR];
+#pragma unroll
+    for (int j = 0; j < K1Z_MAXR; ++j) v[j] = (j < r && i < n) ? A[(int64_t)j * n + i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < K1Z_MAXR; ++j)
+      if (j < r) sAT[(size_t)j * np + i] = v[j];
+  }
   for (int e = r * np + tid; e < RP * np; e += K1Z_T) sAT[e] = 0.0;   // padded columns
   if (tid < RP) sL[tid] = tid < r ? a.x[tid] : 0.0;
   __syncthreads();
   K1Z_STAMP(9);
   {
-    // G = A^T A (warp per upper-triangle entry, two entries at a time; lane-strided products in
-    // two interleaved sums, fixed butterfly, mirrored), C = G^(d-1) by repeated multiplication
-    // (implicit.py:82-91, 147-148)
-    const int warp = tid >> 5, lane = tid & 31;
-    constexpr int NW = K1Z_T / 32;
-    const int T = r * (r + 1) / 2;
-    for (int t0 = warp; t0 < T; t0 += 2 * NW) {
-      int jj[2], kk[2];
-      double sum[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    // G = A^T A by DMMA: the fragment A^T[j0 + g][4 ks + t] is both the row operand of tile row
+    // j0 and the column operand of tile column j0; k-steps strided over the warps, partial
+    // tiles summed in warp order; upper tiles only, mirrored.  C = G^(d-1) by repeated
+    // multiplication (implicit.py:82-91, 147-148).
+    double cg[NT][NT][2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int t = min(t0 + h * NW, T - 1), j = 0;
-        while (t >= r - j) {
-          t -= r - j;
-          ++j;
-        }
-        jj[h] = j;
-        kk[h] = j + t;
-      }
-      const double* c0 = sAT + (size_t)jj[0] * np;
-      const double* c1 = sAT + (size_t)kk[0] * np;
-      const double* c2 = sAT + (size_t)jj[1] * np;
-      const double* c3 = sAT + (size_t)kk[1] * np;
-      int i = lane;
-      for (; i + 32 < n; i += 64) {
-        sum[0][0] += c0[i] * c1[i];
-        sum[0][1] += c0[i + 32] * c1[i + 32];
-        sum[1][0] += c2[i] * c3[i];
-        sum[1][1] += c2[i + 32] * c3[i + 32];
-      }
-      if (i < n) {
-        sum[0][0] += c0[i] * c1[i];
-        sum[1][0] += c2[i] * c3[i];
-      }
+    for (int jt = 0; jt < NT; ++jt)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double sg = sum[h][0] + sum[h][1];
+      for (int kt = 0; kt < NT; ++kt) cg[jt][kt][0] = cg[jt][kt][1] = 0.0;
+    for (int ks = warp; ks < n4 / 4; ks += NW) {
+      double f[NT];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, off);
-        if (lane == 0 && t0 + h * NW < T) {
-          const double cg = rm_pow(sg, d - 1);
-          sG[jj[h] * r + kk[h]] = sg;
-          sG[kk[h] * r + jj[h]] = sg;
-          sC[jj[h] * r + kk[h]] = cg;
-          sC[kk[h] * r + jj[h]] = cg;
-        }
-      }
+      for (int nt = 0; nt < NT; ++nt) f[nt] = sAT[(size_t)(nt * 8 + g) * np + 4 * ks + t];
+#pragma unroll
+      for (int jt = 0; jt < NT; ++jt)
+#pragma unroll
+        for (int kt = jt; kt < NT; ++kt) dmma884(cg[jt][kt], f[jt], f[kt]);
+    }
+#pragma unroll
+    for (int jt = 0; jt < NT; ++jt)
+#pragma unroll
+      for (int kt = jt; kt < NT; ++kt)
+        *reinterpret_cast<double2*>(sZ + ((size_t)warp * RP + jt * 8 + g) * RP + kt * 8 + 2 * t) =
+            make_double2(cg[jt][kt][0], cg[jt][kt][1]);
+    __syncthreads();
+    for (int e = tid; e < r * r; e += K1Z_T) {
+      const int j = e / r, k = e % r;
+      if (j > k) continue;
+      double s = sZ[(size_t)j * RP + k];
+      for (int w = 1; w < NW; ++w) s += sZ[((size_t)w * RP + j) * RP + k];
+      const double c = rm_pow(s, d - 1);
+      sG[j * r + k] = s;
+      sG[k * r + j] = s;
+      sC[j * r + k] = c;
+      sC[k * r + j] = c;
     }
   }
   __syncthreads();
@@ -296,16 +235,13 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   double* s_u = sS + RP;
   if (b == G - 1 && tid < r) s_u[tid] = tail_u_entry(sG, sC, sL, r, tid);
 
-  const int rl = tid / (8 * KQ), kq = (tid >> 3) % KQ, jg = tid & 7;   // GEMM1 map
-  const int ib = tid % a.IB, lg = tid / a.IB;         // GEMM2: variable slot x row group
-  double wacc[CPT];
+  double wacc = 0.0;              // this thread's share of w_(tid % RP)
+  double acc[K1Z_MAXMT][NT][2];   // Y_b tiles (8 warp + m) of this warp
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) wacc[c] = 0.0;
-  double acc[NI][RP];
+  for (int m = 0; m < K1Z_MAXMT; ++m)
 #pragma unroll
-  for (int k = 0; k < NI; ++k)
-#pragma unroll
-    for (int j = 0; j < RP; ++j) acc[k][j] = 0.0;
+    for (int nt = 0; nt < NT; ++nt) acc[m][nt][0] = acc[m][nt][1] = 0.0;
+  const int n_mt = (n + 7) / 8;
   K1Z_STAMP(1);
 
   for (int64_t row0 = row_lo; row0 < row_hi; row0 += R) {
@@ -317,59 +253,72 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
     cp_async_wait<0>();
     __syncthreads();
     K1Z_STAMP(2);
-    // GEMM1 + epilogue: z = v_l . a_j, P = nu z^(d-1), w += P z
-    auto epilogue = [&](int l, const double (&z)[CPT]) {
-      const bool valid = l < rows;
-      double nul = a.nu_const;
-      if (a.nu && valid) nul = a.nu[a.idx ? a.idx[base + row0 + l] : row0 + l];
+    // ---- GEMM1 + epilogue per pass: z = v_l . a_j, P = nu z^(d-1), w += P z ----
+    for (int sub0 = 0; sub0 < rows; sub0 += RS) {
+      double cz[2][MT1][NT][2];
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        const double pv = valid ? nul * rm_pow(z[c], d - 1) : 0.0;
-        if (kq == 0) {
-          if (valid) wacc[c] += pv * z[c];
-          if (l < R) sP[(size_t)l * RP + jg * CPT + c] = pv;
-        }
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int mt = 0; mt < MT1; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) cz[h][mt][nt][0] = cz[h][mt][nt][1] = 0.0;
+      const TV* vrow = sV + (size_t)(sub0 + g) * ns + t;
+      const double* acol = sAT + (size_t)g * np + t;
+      auto kstep = [&](int ks, int h) {
+        double fb[NT], fa[MT1];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) fb[nt] = acol[(size_t)nt * 8 * np + 4 * ks];
+#pragma unroll
+        for (int mt = 0; mt < MT1; ++mt) fa[mt] = to_f64(vrow[(size_t)mt * 8 * ns + 4 * ks]);
+#pragma unroll
+        for (int mt = 0; mt < MT1; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(cz[h][mt][nt], fa[mt], fb[nt]);
+      };
+      int ks = warp;
+      for (; ks + NW < n4 / 4; ks += 2 * NW) {   // two accumulator sets: two chains per tile
+        kstep(ks, 0);
+        kstep(ks + NW, 1);
       }
-    };
-    int sub0 = 0;
-    for (; sub0 + 4 * RS <= R; sub0 += 4 * RS) {
-      double zz[4][CPT];
-      k1z_gemm1<TV, RP, KQ, 4, 2>(sV, sAT, n, ns, np, R, sub0, rl, kq, jg, zz);
+      if (ks < n4 / 4) kstep(ks, 0);
 #pragma unroll
-      for (int s = 0; s < 4; ++s) epilogue(sub0 + s * RS + rl, zz[s]);
-    }
-    for (; sub0 + 2 * RS <= R; sub0 += 2 * RS) {
-      double zz[2][CPT];
-      k1z_gemm1<TV, RP, KQ, 2, 2>(sV, sAT, n, ns, np, R, sub0, rl, kq, jg, zz);
+      for (int mt = 0; mt < MT1; ++mt)
 #pragma unroll
-      for (int s = 0; s < 2; ++s) epilogue(sub0 + s * RS + rl, zz[s]);
-    }
-    for (; sub0 < R; sub0 += RS) {
-      double zz[1][CPT];
-      k1z_gemm1<TV, RP, KQ, 1, 4>(sV, sAT, n, ns, np, R, sub0, rl, kq, jg, zz);
-      epilogue(sub0 + rl, zz[0]);
-    }
-    __syncthreads();
-    K1Z_STAMP(3);
-    // GEMM2: Y[i][:] += v_l[i] P[l][:], rows l = lg, lg + LG, ... in order
-    if (ib < n) {
-      for (int l = lg; l < rows; l += a.LG) {
-        const TV* vr = sV + (size_t)l * ns;
-        const double* pr = sP + (size_t)l * RP;
-        double v[NI];
-#pragma unroll
-        for (int k = 0; k < NI; ++k) {
-          const int i = ib + k * K1Z_T;
-          v[k] = i < n ? to_f64(vr[i]) : 0.0;
+        for (int nt = 0; nt < NT; ++nt)
+          *reinterpret_cast<double2*>(sZ + ((size_t)warp * RS + mt * 8 + g) * RP + nt * 8 + 2 * t) =
+              make_double2(cz[0][mt][nt][0] + cz[1][mt][nt][0], cz[0][mt][nt][1] + cz[1][mt][nt][1]);
+      __syncthreads();
+      for (int e = tid; e < RS * RP; e += K1Z_T) {   // column e % RP == tid % RP on every trip
+        const int row = e / RP, col = e % RP;
+        double z = sZ[(size_t)row * RP + col];
+        for (int w = 1; w < NW; ++w) z += sZ[((size_t)w * RS + row) * RP + col];
+        const int l = sub0 + row;
+        double pv = 0.0;
+        if (l < rows) {
+          double nul = a.nu_const;
+          if (a.nu) nul = a.nu[a.idx ? a.idx[base + row0 + l] : row0 + l];
+          pv = nul * rm_pow(z, d - 1);
+          wacc += pv * z;
         }
+        if (l < R) sP[(size_t)l * RP + col] = pv;
+      }
+      __syncthreads();   // P of this pass written; sZ free for the next pass
+    }
+    K1Z_STAMP(3);
+    // ---- GEMM2: Y[8 m + g][:] += sum_l v_l[8 m + g] P[l][:], k-steps of 4 rows in order ----
+    const int ksteps2 = (rows + 3) / 4;
+    for (int ks = 0; ks < ksteps2; ++ks) {
+      double fb[NT];
 #pragma unroll
-        for (int j = 0; j < RP; j += 2) {
-          const double2 pj = *reinterpret_cast<const double2*>(pr + j);
+      for (int nt = 0; nt < NT; ++nt) fb[nt] = sP[(size_t)(4 * ks + t) * RP + nt * 8 + g];
+      const TV* vk = sV + (size_t)(4 * ks + t) * ns + g;
 #pragma unroll
-          for (int k = 0; k < NI; ++k) {
-            acc[k][j] = fma(v[k], pj.x, acc[k][j]);
-            acc[k][j + 1] = fma(v[k], pj.y, acc[k][j + 1]);
-          }
+      for (int m = 0; m < K1Z_MAXMT; ++m) {
+        const int mt = warp + m * NW;
+        if (mt < n_mt) {
+          const double fa = to_f64(vk[mt * 8]);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[m][nt], fa, fb[nt]);
         }
       }
     }
@@ -379,36 +328,24 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
 
   // ---- this CTA's partial [vec_F(Y_b) ; w_b] ----
   double* mine = a.part + (int64_t)b * a.PS;
+  sW[tid] = wacc;
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) sW[(tid >> 3) * RP + jg * CPT + c] = wacc[c];
-  if (a.LG == 1) {
+  for (int m = 0; m < K1Z_MAXMT; ++m) {
+    const int i = (warp + m * NW) * 8 + g;
+    if (i < n) {
 #pragma unroll
-    for (int k = 0; k < NI; ++k) {
-      const int i = ib + k * K1Z_T;
-      if (i < n)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int j = 0; j < RP; ++j)
-          if (j < r) __stcg(mine + (int64_t)j * n + i, acc[k][j]);
-    }
-    __syncthreads();
-  } else {
-    // row groups combined in group order through shared memory: sY[lg][j][IB]
-    double* sY = reinterpret_cast<double*>(sV);
-#pragma unroll
-    for (int j = 0; j < RP; ++j) sY[((size_t)lg * RP + j) * a.IB + ib] = acc[0][j];
-    __syncthreads();
-    for (int e = tid; e < r * a.IB; e += K1Z_T) {
-      const int j = e / a.IB, i = e % a.IB;
-      if (i < n) {
-        double s = sY[(size_t)j * a.IB + i];
-        for (int g = 1; g < a.LG; ++g) s += sY[((size_t)g * RP + j) * a.IB + i];
-        __stcg(mine + (int64_t)j * n + i, s);
-      }
+        for (int e = 0; e < 2; ++e) {
+          const int j = nt * 8 + 2 * t + e;
+          if (j < r) __stcg(mine + (int64_t)j * n + i, acc[m][nt][e]);
+        }
     }
   }
+  __syncthreads();
   if (tid < r) {
     double s = sW[tid];
-    for (int l = 1; l < 32; ++l) s += sW[l * RP + tid];
+    for (int k = 1; k < K1Z_T / RP; ++k) s += sW[k * RP + tid];
     __stcg(mine + (int64_t)n * r + tid, s);
   }
 #if MCP_K1Z_KO & 1

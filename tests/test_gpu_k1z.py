@@ -1,9 +1,8 @@
 """K1Z, the single-launch small-problem f+grad (csrc/k1z_small.cuh), through the C ABI.
 
-* against the CPU oracle over shapes that cover both GEMM2 thread maps (row groups for small n,
-  two variables per thread for n > 256), both column paddings (r <= 8, r <= 16), one and many
-  CTAs, ragged last CTAs, several slabs per CTA, the 1 / 2 / 4-way k splits of GEMM1, fp32 and
-  fp64 rows, explicit weights, d = 2..6 -- term-scale <= 1e-10 (pkg/tests/test_acceptance.py:65-74);
+* against the CPU oracle over shapes that cover the 8 / 16 / 32-row GEMM1 passes, both column
+  paddings (r <= 8, r <= 16), n not a multiple of 4 or 8, one and many CTAs, ragged last CTAs
+  and passes, several slabs per CTA, fp32 and fp64 rows, explicit weights, d = 2..6 -- term-scale <= 1e-10 (pkg/tests/test_acceptance.py:65-74);
 * against the general K1 -> reduce+finish chain (MCP_OPT_SMALL_KERNEL = 0) to 1e-13;
 * repeated evaluations bit-identical, gradients bitwise independent of alpha, lambda = 0 exact
   (test_objective.py:101-121);
@@ -23,19 +22,18 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [
     # n, r, d, p, dtype, weighted
-    (20, 5, 3, 10_000, np.float64, False),    # config 1: 105 CTAs, row groups of 32 variables
-    (20, 5, 3, 37, np.float64, True),         # two CTAs, the second ragged
-    (7, 1, 2, 5, np.float64, False),          # one CTA, one column
-    (100, 10, 4, 3_000, np.float64, True),    # RP = 16, 128 variable slots x 2 row groups
-    (130, 16, 6, 2_000, np.float64, False),   # one variable per thread, all 16 columns
-    (500, 10, 3, 1_000, np.float64, False),   # the paper's Table 2 mini-batch: NI = 2
-    (500, 10, 3, 10, np.float64, False),
-    (512, 16, 3, 1_900, np.float64, True),    # largest n and r, one slab of 32 rows per CTA
-    (257, 3, 5, 700, np.float32, False),      # fp32 rows, NI = 2, RP = 8
-    (33, 8, 4, 20_000, np.float32, True),     # fp32 rows, 160 rows per CTA
-    (64, 2, 3, 100_000, np.float64, False),   # 704 rows per CTA
-    (512, 6, 3, 5_000, np.float64, False),    # 64 rows per CTA in two slabs of 32
-    (300, 12, 4, 150, np.float64, True),      # k split over 4 threads, 8-row passes, ragged
+    (500, 10, 3, 1_000, np.float64, False),   # the paper's Table 2 mini-batch: 8-row passes
+    (500, 10, 3, 10, np.float64, False),      # two CTAs
+    (200, 5, 2, 7, np.float64, False),        # one CTA (no grid barrier), ragged pass
+    (300, 12, 4, 150, np.float64, True),      # 19 CTAs, the last ragged, explicit weights
+    (130, 16, 6, 2_000, np.float64, False),   # 16-row passes, all 16 columns, d = 6
+    (512, 16, 3, 1_900, np.float64, True),    # largest n and r
+    (512, 6, 3, 5_000, np.float64, False),    # 32-row passes, 64 rows per CTA in two slabs
+    (257, 3, 5, 700, np.float32, False),      # fp32 rows, n = 1 (mod 4) and (mod 8)
+    (33, 8, 4, 20_000, np.float32, True),     # fp32 rows, 160 rows per CTA, 5 variable tiles
+    (20, 5, 3, 10_000, np.float32, False),    # config 1's shape on fp32 rows: 3 variable tiles
+    (7, 1, 2, 5, np.float32, False),          # one CTA, one column, one variable tile
+    (129, 9, 3, 4_736, np.float64, False),    # 32 rows on every CTA of a 148-SM part
 ]
 
 
@@ -90,8 +88,10 @@ def test_k1z_vs_oracle_and_general_chain(k):
 
 
 def test_k1z_limits_fall_back_to_the_general_chain():
+    """Outside K1Z's limits (r <= 16, n <= 512, p n r <= 2^24) and for fp64 sets with n <= 128
+    (where the two-launch K1Q chain measured faster) the general chain runs."""
     rng = np.random.default_rng(5)
-    for n, r, p in ((40, 17, 500), (513, 4, 300), (100, 10, 40_000)):
+    for n, r, p in ((200, 17, 500), (513, 4, 300), (300, 10, 10_000), (100, 10, 3_000)):
         V = rng.standard_normal((n, p)) / np.sqrt(n)
         obs = mcp.ObservationSet(V)
         lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)
@@ -104,7 +104,7 @@ def test_k1z_sampled_set_equals_uploaded_copy_bitwise():
     """sample_observations -> fg equals, bitwise, the evaluation of an uploaded copy of the same
     rows (objective.py:97-113): the work split is a function of the shape only."""
     rng = np.random.default_rng(8)
-    for n, r, d, p, s in ((20, 5, 3, 4_000, 300), (500, 10, 3, 3_000, 1_000), (64, 8, 4, 900, 7)):
+    for n, r, d, p, s in ((200, 5, 3, 4_000, 300), (500, 10, 3, 3_000, 1_000), (264, 8, 4, 900, 7)):
         V = rng.standard_normal((n, p)) / np.sqrt(n)
         obs = mcp.ObservationSet(V)
         lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)

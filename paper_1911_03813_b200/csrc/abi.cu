@@ -419,7 +419,7 @@ static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
   if (!MCP_CFG_K1Z || !c->opt_small_kernel) return false;
   const int64_t n = c->n, p = c->p;
   if (r > K1Z_MAXR || n > K1Z_MAXN || p < 1) return false;
-  if ((double)p * (double)n * (double)r > (double)MCP_CFG_K1Z_MAX_WORK) return false;
+  if (ceil_div(p, (int64_t)c->sms) > MCP_CFG_K1Z_MAX_ROWS) return false;
   const int dtype = c->gV ? c->gdtype : c->dtype;
   const size_t esz = dtype == MCP_F64 ? 8 : 4;
   z.RP = r <= 8 ? 8 : 16;

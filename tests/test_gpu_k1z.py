@@ -34,6 +34,7 @@ SHAPES = [
     (20, 5, 3, 10_000, np.float32, False),    # config 1's shape on fp32 rows: 3 variable tiles
     (7, 1, 2, 5, np.float32, False),          # one CTA, one column, one variable tile
     (129, 9, 3, 4_736, np.float64, False),    # 32 rows on every CTA of a 148-SM part
+    (320, 7, 3, 18_000, np.float64, False),   # 128 rows per CTA: four 32-row passes per slab
 ]
 
 
@@ -88,10 +89,10 @@ def test_k1z_vs_oracle_and_general_chain(k):
 
 
 def test_k1z_limits_fall_back_to_the_general_chain():
-    """Outside K1Z's limits (r <= 16, n <= 512, p n r <= 2^24) and for fp64 sets with n <= 128
-    (where the two-launch K1Q chain measured faster) the general chain runs."""
+    """Outside K1Z's limits (r <= 16, n <= 512, at most 128 rows per SM) and for fp64 sets with
+    n <= 128 (where the two-launch K1Q chain measured faster) the general chain runs."""
     rng = np.random.default_rng(5)
-    for n, r, p in ((200, 17, 500), (513, 4, 300), (300, 10, 10_000), (100, 10, 3_000)):
+    for n, r, p in ((200, 17, 500), (513, 4, 300), (300, 10, 30_000), (100, 10, 3_000)):
         V = rng.standard_normal((n, p)) / np.sqrt(n)
         obs = mcp.ObservationSet(V)
         lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)

@@ -84,3 +84,26 @@ def test_device_adam_fp32_set_fast_mode_and_errors():
     with pytest.raises(ValueError):
         mcp.adam_minimize(obs32, cfg.d, cfg.r, x0[:-1], mcp.AdamConfig(**small),
                           np.random.default_rng(5))
+
+
+def test_device_adam_bitwise_on_the_single_launch_path():
+    """n > 128: the mini-batch and estimate evaluations run as the single-launch K1Z, the
+    mini-batch rows read in place through the epoch's index list (no gathered copy).  The run
+    must still equal, bitwise, the restated reference Adam fed with GPU evaluations of UPLOADED
+    copies of the same rows (K1Z's summation order depends on the shape only)."""
+    rng = np.random.default_rng(41)
+    n, p, r, d = 200, 3000, 4, 3
+    V = rng.standard_normal((n, p)) / np.sqrt(n)
+    lam, A = np.full(r, 1.0 / r), rng.standard_normal((n, r)) / np.sqrt(n)
+    x0 = om.pack(lam, A)
+    cfg = dict(epoch_len=12, batch=40, estimate_samples=150, max_epochs=4)
+    obs = mcp.ObservationSet(V)
+    dev = mcp.adam_minimize(obs, d, r, x0, mcp.AdamConfig(**cfg), np.random.default_rng(9))
+    sub = mcp.ObservationSet(V[:, :40])
+    mcp.fg_implicit(sub, lam, A, d)
+    assert sub.device_context().last_variant.startswith("k1z_fg_small")
+    host = ao.adam(V, d, r, x0, np.random.default_rng(9), fg_fn=_gpu_fg, **cfg)
+    assert dev.n_fg == host["n_iter"] and dev.reason == host["reason"]
+    assert np.array_equal(np.array([t[0] for t in dev.trace]), np.array(host["trace_f"]))
+    assert np.array_equal(mcp.pack(dev.lam, dev.A), host["x"])
+    assert dev.f == host["f"] and dev.grad_inf_norm == host["grad_inf"]

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-end style checks on the GPU box: the -m gpu suite, the default bench (c3 FP64) with its
 # CPU baseline and the reference arm, other configs, and ncu captures of the dominant kernels.
-#   tools/round_check.sh [tests] [bench] [ncu]
+#   tools/round_check.sh [tests] [bench] [ncu] [small]
 mkdir -p gpurun_out
 for what in "$@"; do
 case $what in
@@ -22,6 +22,11 @@ ncu)
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:k1x --launch-skip 1 \
     --launch-count 1 -o gpurun_out/k1x_c3 python tools/prof_k1.py --config c3 --evals 3 > gpurun_out/ncu_k1x.log 2>&1
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:k1t2 --launch-skip 1 \
-    --launch-count 1 -o gpurun_out/k1t2_c5 python tools/prof_k1.py --config c5 --mode tf32x3 --evals 2 > gpurun_out/ncu_k1t2.log 2>&1 ;;
+    --launch-count 1 -o gpurun_out/k1t2_c5 python tools/prof_k1.py --config c5 --mode tf32x3 --evals 2 > gpurun_out/ncu_k1t2.log 2>&1
+  timeout 300 ncu --set full --import-source on --clock-control none -k regex:k1z --launch-skip 2 \
+    --launch-count 1 -o gpurun_out/k1z_t2 python tools/prof_k1z.py --shape 500,10,3,1000 > gpurun_out/ncu_k1z.log 2>&1 ;;
+small)
+  python tools/sweep_small.py > gpurun_out/sweep_small.txt 2>&1
+  timeout 600 python tools/bench_adam.py --epochs 10 --cpu-epochs 1 > gpurun_out/adam_t2.txt 2>&1 ;;
 esac
 done

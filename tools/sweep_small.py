@@ -34,7 +34,10 @@ def time_evals(ctx, d, r, x, out, s, iters=300):
 
 def main():
     rng = np.random.default_rng(0)
-    for n, r, d, p in SHAPES:
+    shapes = SHAPES
+    if len(sys.argv) > 1:   # "n,r,d,p n,r,d,p ..."
+        shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
+    for n, r, d, p in shapes:
         V = rng.standard_normal((n, p)) / np.sqrt(n)
         obs = mcp.ObservationSet(V)
         ctx = obs.device_context()

@@ -1041,6 +1041,8 @@ mcp_ctx* make_view_ctx(const mcp_ctx* parent, void* dV, int dtype, int64_t p, in
   v->dV = dV;
   v->dnu = nullptr;
   v->nu_const = 1.0 / (double)p;
+  v->opt_fused_tail = parent->opt_fused_tail;
+  v->opt_small_kernel = parent->opt_small_kernel;
   v->loaded = true;
   return v;
 }

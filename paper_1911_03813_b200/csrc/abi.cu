@@ -414,6 +414,7 @@ int plan_tf32(mcp_ctx* c, int r, EvalPlan& pl) {
 
 // K1Z shape for (dtype, n, r, p): a function of those and the SM count only (the summation
 // order -- and so the result bits -- must not depend on where the rows came from).
+static bool k1z_pdl_ok(mcp_ctx* c);
 static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
   z = K1ZPlan();
   if (!MCP_CFG_K1Z || !c->opt_small_kernel) return false;
@@ -503,6 +504,7 @@ int plan_eval(mcp_ctx* c, int d, int r, int mode, EvalPlan& pl) {
   // two-launch pairs / stream kernels of n <= 128 fp64 sets measured faster than K1Z
   // (tools/sweep_small.py, profiles/r02/sweep_small.txt)
   if (pl.k1.needs_prep() && plan_k1z(c, r, pl.z)) {
+    pl.z.pdl = k1z_pdl_ok(c);
     if ((rc = ensure(c, c->dYpart, sizeof(double) * (size_t)pl.z.G * pl.z.PS))) return rc;
     if (!c->dzbar.p) {
       if ((rc = ensure(c, c->dzbar, 4 * sizeof(unsigned)))) return rc;
@@ -709,6 +711,37 @@ int enqueue_tails_batched(mcp_ctx* c, int d, int r, int k, const double* xs, int
   return MCP_OK;
 }
 
+// Can a kernel be launched with the cooperative AND the programmatic-serialization attribute?
+// Probed once per process with an empty kernel on the context's stream (never while capturing).
+__global__ void k_k1z_probe() { pdl_wait(); }
+static std::atomic<int> g_k1z_pdl{-1};   // -1 unknown, 0 no, 1 yes
+static bool k1z_pdl_ok(mcp_ctx* c) {
+  if (!MCP_CFG_K1Z_PDL || !pdl_enabled()) return false;
+  int st = g_k1z_pdl.load();
+  if (st >= 0) return st == 1;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(c->stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    (void)cudaGetLastError();
+    return false;   // decide at the next plan outside a capture
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(32);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_k1z_probe);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) (void)cudaGetLastError();
+  g_k1z_pdl.store(e == cudaSuccess ? 1 : 0);
+  return e == cudaSuccess;
+}
+
 // The whole evaluation in one cooperative launch (small problems, csrc/k1z_small.cuh).
 static int enqueue_fg_small(mcp_ctx* c, const EvalPlan& pl, const double* dx,
                             const double* alpha_dev, double alpha, double* dout, cudaStream_t s) {
@@ -756,11 +789,13 @@ static int enqueue_fg_small(mcp_ctx* c, const EvalPlan& pl, const double* dx,
   cfg.blockDim = dim3(K1Z_T);
   cfg.dynamicSmemBytes = z.smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;   // every CTA resident: the grid barrier is safe
   attr[0].val.cooperative = MCP_CFG_K1Z_COOP;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = z.pdl ? 2 : 1;
   auto* ev = timing_begin(c, s);
   cudaError_t e = cudaLaunchKernelEx(&cfg, fn, prm);
   timing_end(ev, s);

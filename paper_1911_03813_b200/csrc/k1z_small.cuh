@@ -30,6 +30,7 @@
 #include "mcp_common.cuh"
 #include "tail_pieces.cuh"
 #include "tuning.h"
+#include "pdl.h"
 #if MCP_K1Z_PROF
 #include <cstdio>
 #endif
@@ -148,6 +149,10 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   TV* sV = reinterpret_cast<TV*>(sS + 2 * RP);                // [R][ns] (+ 8 elements of slack)
   const double* __restrict__ A = a.x + r;
 
+  // under programmatic dependent launch the grid may be resident before its predecessor (the
+  // previous iteration's update kernel) has finished: nothing of x, the cursor or the index
+  // list is read before this wait (a no-op for a plain launch)
+  pdl_wait();
   const int64_t base = (a.idx && a.it_dev) ? (int64_t)(*a.it_dev) * a.p : 0;
   const int64_t row_lo = (int64_t)b * a.rows_per_cta;
   const int64_t row_hi = min(a.p, row_lo + a.rows_per_cta);
@@ -167,14 +172,24 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   };
   // ---- the first slab's rows in flight; everything that depends on x alone meanwhile ----
   if (row_lo < row_hi) issue_slab(row_lo, (int)min((int64_t)R, row_hi - row_lo));
-  // coalesced column reads: the loads of all r columns of a variable in flight before the stores
-  for (int i = tid; i < np; i += K1Z_T) {
-    double v[K1Z_MAXR];
+  // coalesced column reads: the loads of all r columns of two variables in flight before the
+  // stores (every CTA reads the same lines of L2 at once: ~2.3k cycles per round trip)
+  for (int i0 = tid; i0 < np; i0 += 2 * K1Z_T) {
+    double v[2][K1Z_MAXR];
 #pragma unroll
-    for (int j = 0; j < K1Z_MAXR; ++j) v[j] = (j < r && i < n) ? A[(int64_t)j * n + i] : 0.0;
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int j = 0; j < K1Z_MAXR; ++j)
-      if (j < r) sAT[(size_t)j * np + i] = v[j];
+      for (int j = 0; j < K1Z_MAXR; ++j) {
+        const int i = i0 + h * K1Z_T;
+        v[h][j] = (j < r && i < n) ? A[(int64_t)j * n + i] : 0.0;
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < K1Z_MAXR; ++j) {
+        const int i = i0 + h * K1Z_T;
+        if (j < r && i < np) sAT[(size_t)j * np + i] = v[h][j];
+      }
   }
   for (int e = r * np + tid; e < RP * np; e += K1Z_T) sAT[e] = 0.0;   // padded columns
   if (tid < RP) sL[tid] = tid < r ? a.x[tid] : 0.0;
@@ -386,6 +401,9 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
     K1Z_STAMP(6);
   }
   K1Z_STAMP(7);
+  // a dependent launched with the programmatic attribute (the Adam update) may become resident
+  // now; it waits for this grid's completion before reading the gradient
+  pdl_trigger();
 
   // ---- reduce + finish, outputs split over the CTAs ----
   const double s2d = -2.0 * d;

@@ -31,6 +31,13 @@
 #ifndef MCP_CFG_K1Z_COOP
 #define MCP_CFG_K1Z_COOP 1
 #endif
+// K1Z launched cooperatively AND with programmatic stream serialization (its launch latency
+// hides under the predecessor; probed once per process).  Works, and back-to-back evaluations
+// gain 7% (16.4 -> 15.2 us), but the device Adam loses (batch 100: 24.7 vs 21.3 us per
+// iteration, batch 1000: 30.2 vs 25.6 -- profiles/r02/ab_k1z_pdl.txt), so off
+#ifndef MCP_CFG_K1Z_PDL
+#define MCP_CFG_K1Z_PDL 0
+#endif
 #ifndef MCP_CFG_K1Z_MAXG
 #define MCP_CFG_K1Z_MAXG 0         // cap on K1Z's CTAs (0: one per SM)
 #endif

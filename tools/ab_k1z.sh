@@ -2,7 +2,7 @@
 # A/B of K1Z launch / barrier variants at c1 (bench value = L2-flushed device-resident step)
 mkdir -p gpurun_out
 V=paper_1911_03813_b200/_lib/variants
-for tag in default z_nocoop z_g32 z_ko1 z_ko2 nosmall; do
+for tag in default z_nopdl z_prof nosmall; do   # tags built with tools/build_variant.py
   if [ $tag = default ]; then unset MCP_LIBRARY; elif [ $tag = nosmall ]; then export MCP_LIBRARY=$PWD/$V/libmomentcp_b200_z_nosmall.so; else export MCP_LIBRARY=$PWD/$V/libmomentcp_b200_$tag.so; fi
   [ -n "$MCP_LIBRARY" ] && [ ! -f "$MCP_LIBRARY" ] && continue
   for cfg in "$@"; do

@@ -252,3 +252,37 @@ def test_c2_full_size_fit_replay():
              iterate_hook=ref_its.append)
     for k in range(min(len(ref_its), 4)):
         assert np.allclose(its[k], ref_its[k], rtol=1e-9, atol=1e-12), k
+
+
+def test_device_lbfgs_on_the_single_launch_path_step_for_step():
+    """n > 128 and few rows: every trial point of the device solver is one K1Z launch inside
+    the solver's graph.  Same protocol as above: the restated reference solver driven by the same
+    GPU f+grad takes the same steps (evaluation counts, f to 1e-12, iterates to 1e-9) for the
+    opening steps, and every trace value is bitwise the f+grad of its iterate."""
+    rng = np.random.default_rng(77)
+    n, p, r, d = 160, 2500, 4, 3
+    means = rng.standard_normal((n, r))
+    means /= np.linalg.norm(means, axis=0)
+    V = means[:, rng.integers(0, r, p)] + 0.1 * rng.standard_normal((n, p))
+    obs = mcp.ObservationSet(V)
+    A0 = rng.standard_normal((n, r))
+    x0 = om.pack(np.full(r, 1.0 / r), A0 / np.linalg.norm(A0, axis=0))
+    fg = mcp.packed_fg_implicit(obs, d, r)
+    fg(x0)
+    assert obs.device_context().last_variant.startswith("k1z_fg_small")
+    counts, host_its, dev_its = [], [], []
+
+    def counting(x):
+        counts.append(1)
+        return fg(x)
+
+    host = lo.lbfgs(counting, x0, max_iters=12, iterate_hook=host_its.append)
+    dev = mcp.lbfgs_minimize(fg, x0, mcp.OptConfig(max_iters=12), iterate_hook=dev_its.append)
+    assert dev.n_steps == host["n_steps"] >= 3 and dev.n_fg == host["n_fg"]
+    assert dev.reason == host["reason"]
+    for k in range(dev.n_steps + 1):
+        assert abs(dev.trace[k][0] - host["trace"][k]) <= 1e-12 * abs(host["trace"][k]), k
+        assert np.allclose(dev_its[k], host_its[k], rtol=1e-9, atol=1e-12), k
+        assert fg(dev_its[k])[0] == dev.trace[k][0], k
+    again = mcp.lbfgs_minimize(fg, x0, mcp.OptConfig(max_iters=12))
+    assert again.f == dev.f and np.array_equal(again.A, dev.A)

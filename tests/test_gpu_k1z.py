@@ -115,3 +115,39 @@ def test_k1z_sampled_set_equals_uploaded_copy_bitwise():
         b = mcp.fg_implicit(mcp.ObservationSet(V[:, idx]), lam, A, d, 0.5)
         assert a.f == b.f and np.array_equal(a.g_lam, b.g_lam) and np.array_equal(a.g_A, b.g_A)
         _check(a, V[:, idx], None, lam, A, d, 0.5, 1e-10)
+
+
+def test_k1z_on_a_row_shard_uses_the_set_weight():
+    """A device-resident row shard (weights 1 / p_total, not 1 / rows): K1Z and the general chain
+    agree, and both equal the oracle on explicit weights 1 / p_total."""
+    import torch
+
+    rng = np.random.default_rng(14)
+    n, rows, p_total, r, d = 240, 900, 5_000, 6, 3
+    V = rng.standard_normal((n, rows)) / np.sqrt(n)
+    lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)
+    obs = mcp.ObservationSet.from_device(torch.as_tensor(V.T.copy(), device="cuda"),
+                                         p_total=p_total)
+    ctx = obs.device_context()
+    x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
+    s = _native.stream_handle(torch.cuda.current_stream())
+    outs = []
+    for small in (1, 0):
+        ctx.set_option(_native.MCP_OPT_SMALL_KERNEL, small)
+        o = torch.empty(1 + r + n * r, dtype=torch.float64, device="cuda")
+        ctx.fg_device(d, r, x.data_ptr(), 0.125, None, o.data_ptr(), s)
+        torch.cuda.synchronize()
+        assert ctx.last_variant.startswith("k1z") == bool(small), ctx.last_variant
+        outs.append(o.cpu().numpy())
+    ctx.set_option(_native.MCP_OPT_SMALL_KERNEL, 1)
+    nu = np.full(rows, 1.0 / p_total)
+    f, gl, gA = om.fg_implicit(V, nu, lam, A, d, 0.125)
+    f_s, gl_s, gA_s, _ = om.term_scales(V, nu, lam, A, d, 0.125)
+    for got, tol in ((outs[0], 1e-10), (outs[1], 1e-10)):
+        e = max(om.term_rel_err(got[0], f, f_s), om.term_rel_err(got[1:1 + r], gl, gl_s),
+                om.term_rel_err(got[1 + r:], gA.reshape(-1, order="F"),
+                                gA_s.reshape(-1, order="F")))
+        assert e <= tol, e
+    e = max(om.term_rel_err(outs[0][0], outs[1][0], f_s),
+            om.term_rel_err(outs[0][1 + r:], outs[1][1 + r:], gA_s.reshape(-1, order="F")))
+    assert e <= 1e-13, e

@@ -423,7 +423,7 @@ static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
   if (ceil_div(p, (int64_t)c->sms) > MCP_CFG_K1Z_MAX_ROWS) return false;
   const int dtype = c->gV ? c->gdtype : c->dtype;
   const size_t esz = dtype == MCP_F64 ? 8 : 4;
-  z.RP = r <= 8 ? 8 : 16;
+  z.RP = r <= 8 ? 8 : (r <= 16 ? 16 : 32);
   // staged rows: conflict-free 8 x 4 DMMA fragment loads (== 4 mod 16 doubles / mod 32 floats)
   const int64_t n4 = round_up(n, (int64_t)4);
   const int64_t mod = dtype == MCP_F64 ? 16 : 32;
@@ -436,12 +436,12 @@ static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
   const int64_t rpc0 = ceil_div(p, max_g);
   const size_t budget = 226 * 1024;
   const size_t per_row = ns * esz + sizeof(double) * z.RP;
-  for (z.MT1 = rpc0 <= 8 ? 1 : (rpc0 <= 16 ? 2 : 4); z.MT1 >= 1; z.MT1 /= 2) {
+  // (32 columns: at most 16-row passes -- the Y_b tiles already take 128 registers)
+  for (z.MT1 = rpc0 <= 8 ? 1 : ((rpc0 <= 16 || z.RP == 32) ? 2 : 4); z.MT1 >= 1; z.MT1 /= 2) {
     const int64_t RS = 8 * z.MT1;
     const size_t fixed =
-        sizeof(double) * ((size_t)z.np * z.RP +
-                          (size_t)K1Z_NW * std::max<int64_t>(RS, z.RP) * z.RP + 3 * K1Z_T +
-                          2 * K1Z_MAXR * K1Z_MAXR + 3 * z.RP) + 8 * esz;
+        sizeof(double) * ((size_t)z.np * z.RP + (size_t)k1z_sz_elems(z.RP, z.MT1) + 3 * K1Z_T +
+                          2 * (size_t)z.RP * z.RP + 3 * z.RP) + 8 * esz;
     if (fixed + (size_t)RS * per_row > budget) continue;   // a lower pass height may fit
     z.rows_per_cta = (int)round_up(rpc0, RS);
     z.G = (int)ceil_div(p, (int64_t)z.rows_per_cta);
@@ -776,10 +776,12 @@ static int enqueue_fg_small(mcp_ctx* c, const EvalPlan& pl, const double* dx,
                   : (z.MT1 == 2 ? k1z_fg_small<TV, RP_, 2> : k1z_fg_small<TV, RP_, 4>)
   if (f64) {
     if (z.RP == 8) MCP_K1Z_PICK(double, 8);
-    else MCP_K1Z_PICK(double, 16);
+    else if (z.RP == 16) MCP_K1Z_PICK(double, 16);
+    else fn = z.MT1 == 1 ? k1z_fg_small<double, 32, 1> : k1z_fg_small<double, 32, 2>;
   } else {
     if (z.RP == 8) MCP_K1Z_PICK(float, 8);
-    else MCP_K1Z_PICK(float, 16);
+    else if (z.RP == 16) MCP_K1Z_PICK(float, 16);
+    else fn = z.MT1 == 1 ? k1z_fg_small<float, 32, 1> : k1z_fg_small<float, 32, 2>;
   }
 #undef MCP_K1Z_PICK
   if (!ensure_dyn_smem((const void*)fn, z.smem))

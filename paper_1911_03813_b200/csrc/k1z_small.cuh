@@ -38,7 +38,7 @@
 namespace mcp {
 
 constexpr int K1Z_T = 256;
-constexpr int K1Z_MAXR = 16;
+constexpr int K1Z_MAXR = 32;
 constexpr int K1Z_MAXN = 512;
 
 struct K1ZParams {
@@ -106,7 +106,7 @@ __device__ __forceinline__ void k1z_reduce(const double* part, int PS, int G, in
   }
 }
 
-// TV: element type of V.  RP: padded factor columns (8 or 16).  MT1: 8-row DMMA tiles per
+// TV: element type of V.  RP: padded factor columns (8, 16 or 32).  MT1: 8-row DMMA tiles per
 // GEMM1 pass (a pass covers 8 MT1 rows).
 #if MCP_K1Z_PROF
 #define K1Z_STAMP(k) do { if (threadIdx.x == 0) stamps[k] = clock64(); } while (0)
@@ -115,6 +115,11 @@ __device__ __forceinline__ void k1z_reduce(const double* part, int PS, int G, in
 #endif
 
 constexpr int K1Z_NW = K1Z_T / 32;
+// doubles of the partial-sum area: NW GEMM1 pass partials or NW / 2 slots of the factor Gram
+__host__ __device__ constexpr int k1z_sz_elems(int RP, int MT1) {
+  return (K1Z_NW * 8 * MT1 * RP) > (K1Z_NW / 2 * RP * RP) ? (K1Z_NW * 8 * MT1 * RP)
+                                                          : (K1Z_NW / 2 * RP * RP);
+}
 constexpr int K1Z_MAXMT = K1Z_MAXN / 8 / K1Z_NW;   // GEMM2 m-tiles per warp
 
 template <typename TV, int RP, int MT1>
@@ -138,11 +143,12 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   // conflict-free across variables (the fill, M) and across the 8 x 4 DMMA fragment lanes
   double* sAT = reinterpret_cast<double*>(k1z_smem);         // [RP][np]
   double* sP = sAT + (size_t)RP * np;                         // [R][RP]
-  double* sZ = sP + (size_t)R * RP;                           // [NW][max(RS, RP)][RP] partials
-  double* sW = sZ + (size_t)NW * (RS > RP ? RS : RP) * RP;    // [256]
+  double* sZ = sP + (size_t)R * RP;                           // partials: [NW][RS][RP] of a GEMM1
+                                                              // pass, [NW / 2][RP][RP] of G
+  double* sW = sZ + k1z_sz_elems(RP, MT1);                    // [256]
   double* sG = sW + K1Z_T;                                    // [r][r]
-  double* sC = sG + K1Z_MAXR * K1Z_MAXR;                      // [r][r]
-  double* sR = sC + K1Z_MAXR * K1Z_MAXR;                      // [256] reduce lanes
+  double* sC = sG + RP * RP;                                  // [r][r]
+  double* sR = sC + RP * RP;                                  // [256] reduce lanes
   double* sM = sR + K1Z_T;                                    // [256] M entries of my outputs
   double* sL = sM + K1Z_T;                                    // [RP] lam, zero padded
   double* sS = sL + RP;                                       // [2 RP] w, u of the finish
@@ -175,18 +181,18 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   // coalesced column reads: the loads of all r columns of two variables in flight before the
   // stores (every CTA reads the same lines of L2 at once: ~2.3k cycles per round trip)
   for (int i0 = tid; i0 < np; i0 += 2 * K1Z_T) {
-    double v[2][K1Z_MAXR];
+    double v[2][RP];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int j = 0; j < K1Z_MAXR; ++j) {
+      for (int j = 0; j < RP; ++j) {
         const int i = i0 + h * K1Z_T;
         v[h][j] = (j < r && i < n) ? A[(int64_t)j * n + i] : 0.0;
       }
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int j = 0; j < K1Z_MAXR; ++j) {
+      for (int j = 0; j < RP; ++j) {
         const int i = i0 + h * K1Z_T;
         if (j < r && i < np) sAT[(size_t)j * np + i] = v[h][j];
       }
@@ -214,18 +220,36 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
 #pragma unroll
         for (int kt = jt; kt < NT; ++kt) dmma884(cg[jt][kt], f[jt], f[kt]);
     }
+    // partial tiles of warps 0..3 stored, those of warps 4..7 added onto them (slot w - 4 is
+    // touched by one warp per round), then the four slots summed in order
+    {
+      double* slot = sZ + (size_t)(warp & (NW / 2 - 1)) * RP * RP;
+      if (warp < NW / 2) {
 #pragma unroll
-    for (int jt = 0; jt < NT; ++jt)
+        for (int jt = 0; jt < NT; ++jt)
 #pragma unroll
-      for (int kt = jt; kt < NT; ++kt)
-        *reinterpret_cast<double2*>(sZ + ((size_t)warp * RP + jt * 8 + g) * RP + kt * 8 + 2 * t) =
-            make_double2(cg[jt][kt][0], cg[jt][kt][1]);
+          for (int kt = jt; kt < NT; ++kt)
+            *reinterpret_cast<double2*>(slot + (size_t)(jt * 8 + g) * RP + kt * 8 + 2 * t) =
+                make_double2(cg[jt][kt][0], cg[jt][kt][1]);
+      }
+      __syncthreads();
+      if (warp >= NW / 2) {
+#pragma unroll
+        for (int jt = 0; jt < NT; ++jt)
+#pragma unroll
+          for (int kt = jt; kt < NT; ++kt) {
+            double2* q = reinterpret_cast<double2*>(slot + (size_t)(jt * 8 + g) * RP + kt * 8 + 2 * t);
+            const double2 o = *q;
+            *q = make_double2(o.x + cg[jt][kt][0], o.y + cg[jt][kt][1]);
+          }
+      }
+    }
     __syncthreads();
     for (int e = tid; e < r * r; e += K1Z_T) {
       const int j = e / r, k = e % r;
       if (j > k) continue;
       double s = sZ[(size_t)j * RP + k];
-      for (int w = 1; w < NW; ++w) s += sZ[((size_t)w * RP + j) * RP + k];
+      for (int w = 1; w < NW / 2; ++w) s += sZ[((size_t)w * RP + j) * RP + k];
       const double c = rm_pow(s, d - 1);
       sG[j * r + k] = s;
       sG[k * r + j] = s;

@@ -16,7 +16,7 @@
 #ifndef MCP_CFG_HOST_MEMCPY
 #define MCP_CFG_HOST_MEMCPY 0
 #endif
-// K1Z: FP64 evaluations with r <= 16, n <= 512 and at most MCP_CFG_K1Z_MAX_ROWS rows per SM
+// K1Z: FP64 evaluations with r <= 32, n <= 512 and at most MCP_CFG_K1Z_MAX_ROWS rows per SM
 // run as ONE cooperative launch (csrc/k1z_small.cuh) where the general chain would be the
 // 4-6 launch prep -> K1 -> reduce -> tail.  Measured crossover against that chain
 // (tools/sweep_small.py, profiles/r02/sweep_small_k1z.txt): 140-290 rows per CTA.

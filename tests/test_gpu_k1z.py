@@ -1,7 +1,7 @@
 """K1Z, the single-launch small-problem f+grad (csrc/k1z_small.cuh), through the C ABI.
 
 * against the CPU oracle over shapes that cover the 8 / 16 / 32-row GEMM1 passes, both column
-  paddings (r <= 8, r <= 16), n not a multiple of 4 or 8, one and many CTAs, ragged last CTAs
+  paddings (r <= 8, 16, 32), n not a multiple of 4 or 8, one and many CTAs, ragged last CTAs
   and passes, several slabs per CTA, fp32 and fp64 rows, explicit weights, d = 2..6 -- term-scale <= 1e-10 (pkg/tests/test_acceptance.py:65-74);
 * against the general K1 -> reduce+finish chain (MCP_OPT_SMALL_KERNEL = 0) to 1e-13;
 * repeated evaluations bit-identical, gradients bitwise independent of alpha, lambda = 0 exact
@@ -35,6 +35,10 @@ SHAPES = [
     (7, 1, 2, 5, np.float32, False),          # one CTA, one column, one variable tile
     (129, 9, 3, 4_736, np.float64, False),    # 32 rows on every CTA of a 148-SM part
     (320, 7, 3, 18_000, np.float64, False),   # 128 rows per CTA: four 32-row passes per slab
+    (500, 32, 3, 1_000, np.float64, False),   # 32 columns (four column tiles), 8-row passes
+    (300, 20, 4, 2_000, np.float64, True),    # 32-column padding of r = 20, 16-row passes
+    (512, 32, 3, 900, np.float64, False),     # largest n and r: the shared-memory limit
+    (200, 25, 2, 60, np.float32, False),      # fp32 rows, 32-column padding, 8 CTAs
 ]
 
 
@@ -89,10 +93,10 @@ def test_k1z_vs_oracle_and_general_chain(k):
 
 
 def test_k1z_limits_fall_back_to_the_general_chain():
-    """Outside K1Z's limits (r <= 16, n <= 512, at most 128 rows per SM) and for fp64 sets with
+    """Outside K1Z's limits (r <= 32, n <= 512, at most 128 rows per SM) and for fp64 sets with
     n <= 128 (where the two-launch K1Q chain measured faster) the general chain runs."""
     rng = np.random.default_rng(5)
-    for n, r, p in ((200, 17, 500), (513, 4, 300), (300, 10, 30_000), (100, 10, 3_000)):
+    for n, r, p in ((200, 33, 500), (513, 4, 300), (300, 10, 30_000), (100, 10, 3_000)):
         V = rng.standard_normal((n, p)) / np.sqrt(n)
         obs = mcp.ObservationSet(V)
         lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)

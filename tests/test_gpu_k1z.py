@@ -155,3 +155,41 @@ def test_k1z_on_a_row_shard_uses_the_set_weight():
     e = max(om.term_rel_err(outs[0][0], outs[1][0], f_s),
             om.term_rel_err(outs[0][1 + r:], outs[1][1 + r:], gA_s.reshape(-1, order="F")))
     assert e <= 1e-13, e
+
+
+@pytest.mark.parametrize("shape", [(500, 10, 3, 1_000), (20, 5, 3, 10_000)])
+def test_device_evaluations_capture_into_a_callers_cuda_graph(shape):
+    """fg_device launches on the stream it is given, so a caller may capture evaluations into a
+    CUDA graph of its own (the cooperative K1Z launch and the K1Q -> K3F chain under programmatic
+    dependent launch both capture); replays reproduce the eager result bitwise."""
+    import torch
+
+    n, r, d, p = shape
+    rng = np.random.default_rng(p)
+    V = rng.standard_normal((n, p)) / np.sqrt(n)
+    ctx = mcp.ObservationSet(V).device_context()
+    lam, A = rng.standard_normal(r), rng.standard_normal((n, r)) / np.sqrt(n)
+    x = torch.as_tensor(mcp.pack(lam, A), device="cuda")
+    out = torch.empty(1 + r + n * r, dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        s = _native.stream_handle(torch.cuda.current_stream())
+        ctx.fg_device(d, r, x.data_ptr(), 0.5, None, out.data_ptr(), s)
+        torch.cuda.synchronize()
+        eager = out.clone()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            s = _native.stream_handle(torch.cuda.current_stream())
+            for _ in range(3):
+                ctx.fg_device(d, r, x.data_ptr(), 0.5, None, out.data_ptr(), s)
+        out.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, eager)
+        x.mul_(1.5)            # the graph reads x in place: a new point, no re-capture
+        graph.replay()
+        torch.cuda.synchronize()
+        replayed = out.clone()
+        ctx.fg_device(d, r, x.data_ptr(), 0.5, None, out.data_ptr(), s)
+        torch.cuda.synchronize()
+        assert torch.equal(out, replayed)

@@ -444,7 +444,9 @@ static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
                           2 * (size_t)z.RP * z.RP + 3 * z.RP) + 8 * esz;
     if (fixed + (size_t)RS * per_row > budget) continue;   // a lower pass height may fit
     z.rows_per_cta = (int)round_up(rpc0, RS);
-    z.G = (int)ceil_div(p, (int64_t)z.rows_per_cta);
+    z.Gp = (int)ceil_div(p, (int64_t)z.rows_per_cta);
+    // tiny batches: extra CTAs without rows so that no CTA finishes more than 256 outputs
+    z.G = (int)std::max<int64_t>(z.Gp, std::min<int64_t>(max_g, ceil_div(n * r + r, (int64_t)K1Z_T)));
     const int64_t Rmax = (int64_t)((budget - fixed) / per_row) / RS * RS;
     z.R = (int)std::min<int64_t>(z.rows_per_cta, Rmax);
     z.smem = fixed + (size_t)z.R * per_row;
@@ -454,7 +456,8 @@ static bool plan_k1z(const mcp_ctx* c, int r, K1ZPlan& z) {
   z.PS = (int)round_up(n * r + r, (int64_t)2);
   z.name = std::string("k1z_fg_small<") + (dtype == MCP_F64 ? "f64" : "f32") +
            ",RP=" + std::to_string(z.RP) + ",MT1=" + std::to_string(z.MT1) +
-           ",G=" + std::to_string(z.G) + ",R=" + std::to_string(z.R) + ">";
+           ",G=" + std::to_string(z.G) + (z.G != z.Gp ? "/" + std::to_string(z.Gp) : std::string()) +
+           ",R=" + std::to_string(z.R) + ">";
   z.on = true;
   return true;
 }
@@ -769,6 +772,7 @@ static int enqueue_fg_small(mcp_ctx* c, const EvalPlan& pl, const double* dx,
   prm.ns = z.ns;
   prm.np = z.np;
   prm.PS = z.PS;
+  prm.Gp = z.Gp;
   const bool f64 = (c->gV ? c->gdtype : c->dtype) == MCP_F64;
   void (*fn)(const K1ZParams) = nullptr;
 #define MCP_K1Z_PICK(TV, RP_)                                                    \

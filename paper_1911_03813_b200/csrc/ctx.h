@@ -138,7 +138,7 @@ struct K1TPlan {
 struct K1ZPlan {
   bool on = false;
   bool pdl = false;   // launch with the programmatic-serialization attribute as well
-  int G = 0, rows_per_cta = 0, R = 0, ns = 0, np = 0, RP = 0, MT1 = 1, PS = 0;
+  int G = 0, Gp = 0, rows_per_cta = 0, R = 0, ns = 0, np = 0, RP = 0, MT1 = 1, PS = 0;
   size_t smem = 0;
   std::string name;
 };

@@ -61,6 +61,8 @@ struct K1ZParams {
   int ns = 0;                     // shared-memory row pitch of a staged row (elements)
   int np = 0;                     // shared-memory pitch of a factor column (doubles, odd)
   int PS = 0;                     // partial slot pitch (doubles)
+  int Gp = 0;                     // CTAs that own rows (partial slots); CTAs Gp .. gridDim - 1 only
+                                  // take a share of the finish (tiny batches: few row CTAs)
 };
 
 __device__ __forceinline__ unsigned long long k1z_now_ns() {
@@ -365,13 +367,14 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   __syncthreads();
   K1Z_STAMP(4);
 
-  // ---- this CTA's partial [vec_F(Y_b) ; w_b] ----
+  // ---- this CTA's partial [vec_F(Y_b) ; w_b] (row-owning CTAs only) ----
+  const bool owner = b < a.Gp;
   double* mine = a.part + (int64_t)b * a.PS;
   sW[tid] = wacc;
 #pragma unroll
   for (int m = 0; m < K1Z_MAXMT; ++m) {
     const int i = (warp + m * NW) * 8 + g;
-    if (i < n) {
+    if (owner && i < n) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
     }
   }
   __syncthreads();
-  if (tid < r) {
+  if (owner && tid < r) {
     double s = sW[tid];
     for (int k = 1; k < K1Z_T / RP; ++k) s += sW[k * RP + tid];
     __stcg(mine + (int64_t)n * r + tid, s);
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   const double s2d = -2.0 * d;
   const double bad = failed ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
   const int cnt = e1 - e0 + (b == G - 1 ? r : 0);   // the last CTA's entries end at n_out: w follows
-  k1z_reduce(a.part, a.PS, G, e0, cnt, sR, [&](int e, double y) {
+  k1z_reduce(a.part, a.PS, a.Gp, e0, cnt, sR, [&](int e, double y) {
     if (e < n_out) {
       const double m = e - e0 < K1Z_T ? sM[e - e0] : m_entry(e);
       a.out[1 + r + e] = (s2d * (y - m)) * sL[e / n] + bad;

@@ -15,7 +15,8 @@ import paper_1911_03813_b200 as mcp
 from paper_1911_03813_b200 import _native
 
 SHAPES = [(20, 5, 3, 10000), (20, 5, 3, 1000), (100, 10, 4, 3000), (500, 10, 3, 1000),
-          (500, 10, 3, 100), (256, 16, 3, 2000), (500, 32, 3, 1000)]
+          (500, 10, 3, 100), (500, 10, 3, 10), (500, 10, 3, 4000), (256, 16, 3, 2000),
+          (500, 32, 3, 1000)]
 
 
 def main():

@@ -773,6 +773,8 @@ static int enqueue_fg_small(mcp_ctx* c, const EvalPlan& pl, const double* dx,
   prm.np = z.np;
   prm.PS = z.PS;
   prm.Gp = z.Gp;
+  if (c->z_adam && static_cast<const K1ZAdam*>(c->z_adam)->x == dx)
+    prm.adam = *static_cast<const K1ZAdam*>(c->z_adam);
   const bool f64 = (c->gV ? c->gdtype : c->dtype) == MCP_F64;
   void (*fn)(const K1ZParams) = nullptr;
 #define MCP_K1Z_PICK(TV, RP_)                                                    \

@@ -25,6 +25,7 @@
 #include "ctx.h"
 #include "mcp_common.cuh"
 #include "pdl.h"
+#include "k1z_small.cuh"
 
 using namespace mcp;
 using namespace mcp_internal;
@@ -105,6 +106,7 @@ struct AdamRun {
   int64_t* h_idx = nullptr;
   double* h_bc = nullptr;
   double* h_scal = nullptr;  // [lr, f_est]
+  K1ZAdam zadam;   // the update fused into K1Z's finish when the batch plans to K1Z
   GraphEntry g_iter, g_chunk, g_est;   // one iteration, ITER_CHUNK iterations, the estimate
   int64_t chunk_iters = 0;
   AdamScalars sc{};
@@ -215,12 +217,28 @@ struct AdamRun {
     CUDA_TRY(c, cudaMallocHost(&h_bc, sizeof(double) * 2 * epoch_len));
     CUDA_TRY(c, cudaMallocHost(&h_scal, sizeof(double) * 4));
     cudaStream_t s = c->stream;
+    const bool fused_step = mode == MCP_MODE_FP64 && plb.z.on && MCP_CFG_ADAM_FUSED_STEP;
+    if (fused_step) {
+      zadam.x = X;
+      zadam.m1 = M1;
+      zadam.m2 = M2;
+      zadam.bc = bc;
+      zadam.lr = lr_dev;
+      zadam.it = it_dev;
+      zadam.b1 = sc.b1;
+      zadam.omb1 = sc.omb1;
+      zadam.b2 = sc.b2;
+      zadam.omb2 = sc.omb2;
+      zadam.eps = sc.eps;
+      vb->z_adam = &zadam;
+    }
     auto one_iteration = [&]() -> int {
       int e = MCP_OK;
       // no gathered copy when the single-launch kernel reads the rows through the index
       if (!(mode == MCP_MODE_FP64 && plb.z.on)) e = enqueue_gather(Vb, batch, idx, it_dev, vb->ldv);
       if (e) return e;
       if ((e = fg_on(vb, plb, X, OB))) return e;
+      if (fused_step) return MCP_OK;   // gather, f+grad and the update were one launch
       CUDA_TRY(c, launch_pdl(k_adam_step, dim3(nb), dim3(AD_T), 0, s, N, (const double*)OB, X, M1,
                              M2, (const double*)bc, (const double*)lr_dev, sc, it_dev, counter));
       return MCP_OK;

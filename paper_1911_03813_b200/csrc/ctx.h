@@ -91,6 +91,9 @@ struct mcp_ctx {
   int gdtype = MCP_F64;
   const int64_t* gidx = nullptr;
   const int* git = nullptr;
+  // optional Adam update fused into K1Z's finish (mcp::K1ZAdam owned by the stochastic-path
+  // workspace; applied only when the evaluation's x is the Adam variables)
+  const void* z_adam = nullptr;
 
   // cached device-resident L-BFGS workspace (lbfgs.cu); freed with the graphs
   void* lbfgs_ws = nullptr;

@@ -41,6 +41,20 @@ constexpr int K1Z_T = 256;
 constexpr int K1Z_MAXR = 32;
 constexpr int K1Z_MAXN = 512;
 
+// Optional Adam update fused into the finish (stochastic path, optimize.py:425-430): after the
+// grid barrier nobody reads x from global memory any more (every CTA staged it before arriving),
+// so the thread that finishes gradient entry k also updates m1[k], m2[k] and x[k] in place, in
+// the reference's operation order with explicit round-to-nearest operations.
+struct K1ZAdam {
+  double* x = nullptr;            // the packed variables (same buffer K1ZParams::x reads)
+  double* m1 = nullptr;
+  double* m2 = nullptr;
+  const double* bc = nullptr;     // bc[2 it], bc[2 it + 1] = 1 - b1^t, 1 - b2^t
+  const double* lr = nullptr;
+  int* it = nullptr;              // iteration cursor, advanced by the last CTA
+  double b1 = 0, omb1 = 0, b2 = 0, omb2 = 0, eps = 0;
+};
+
 struct K1ZParams {
   const void* V = nullptr;        // observation-major rows, pitch ldv elements
   int64_t ldv = 0;
@@ -61,6 +75,7 @@ struct K1ZParams {
   int ns = 0;                     // shared-memory row pitch of a staged row (elements)
   int np = 0;                     // shared-memory pitch of a factor column (doubles, odd)
   int PS = 0;                     // partial slot pitch (doubles)
+  K1ZAdam adam;                   // adam.x == nullptr: no fused update
   int Gp = 0;                     // CTAs that own rows (partial slots); CTAs Gp .. gridDim - 1 only
                                   // take a share of the finish (tiny batches: few row CTAs)
 };
@@ -162,6 +177,7 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   // list is read before this wait (a no-op for a plain launch)
   pdl_wait();
   const int64_t base = (a.idx && a.it_dev) ? (int64_t)(*a.it_dev) * a.p : 0;
+  const int it0 = a.adam.x ? *a.adam.it : 0;
   const int64_t row_lo = (int64_t)b * a.rows_per_cta;
   const int64_t row_hi = min(a.p, row_lo + a.rows_per_cta);
   constexpr int EPC = 16 / (int)sizeof(TV);          // elements per 16-byte chunk
@@ -436,14 +452,34 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
   const double s2d = -2.0 * d;
   const double bad = failed ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;
   const int cnt = e1 - e0 + (b == G - 1 ? r : 0);   // the last CTA's entries end at n_out: w follows
+  double bc1 = 1.0, bc2 = 1.0, lr = 0.0;
+  if (a.adam.x) {
+    bc1 = a.adam.bc[2 * it0];
+    bc2 = a.adam.bc[2 * it0 + 1];
+    lr = *a.adam.lr;
+  }
+  auto adam_update = [&](int k, double gk) {   // k_adam_step's arithmetic (csrc/adam.cu)
+    const K1ZAdam& ad = a.adam;
+    const double u = __dadd_rn(__dmul_rn(ad.b1, ad.m1[k]), __dmul_rn(ad.omb1, gk));
+    const double v = __dadd_rn(__dmul_rn(ad.b2, ad.m2[k]), __dmul_rn(__dmul_rn(ad.omb2, gk), gk));
+    ad.m1[k] = u;
+    ad.m2[k] = v;
+    const double mh = __ddiv_rn(u, bc1);
+    const double vh = __ddiv_rn(v, bc2);
+    ad.x[k] = __dsub_rn(ad.x[k], __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), ad.eps)));
+  };
   k1z_reduce(a.part, a.PS, a.Gp, e0, cnt, sR, [&](int e, double y) {
     if (e < n_out) {
       const double m = e - e0 < K1Z_T ? sM[e - e0] : m_entry(e);
-      a.out[1 + r + e] = (s2d * (y - m)) * sL[e / n] + bad;
+      const double gk = (s2d * (y - m)) * sL[e / n] + bad;
+      a.out[1 + r + e] = gk;
+      if (a.adam.x) adam_update(r + e, gk);
     } else {
       const int j = e - n_out;
       s_w[j] = y;
-      a.out[1 + j] = -2.0 * (y - s_u[j]) + bad;
+      const double gk = -2.0 * (y - s_u[j]) + bad;
+      a.out[1 + j] = gk;
+      if (a.adam.x) adam_update(j, gk);
     }
   });
   if (b == G - 1 && tid == 0) {
@@ -452,6 +488,7 @@ __global__ void __launch_bounds__(K1Z_T) k1z_fg_small(const K1ZParams a) {
     for (int j = 0; j < r; ++j) wl += s_w[j] * sL[j];
     const double alpha = a.alpha_dev ? *a.alpha_dev : a.alpha_host;
     a.out[0] = alpha + lu - 2.0 * wl + bad;
+    if (a.adam.x) *a.adam.it = it0 + 1;
   }
 #if MCP_K1Z_PROF
   K1Z_STAMP(8);

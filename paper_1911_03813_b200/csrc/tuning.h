@@ -51,6 +51,10 @@
 #ifndef MCP_CFG_ADAM_ITER_CHUNK
 #define MCP_CFG_ADAM_ITER_CHUNK 128
 #endif
+// stochastic path: the Adam update runs inside K1Z's finish when the mini-batch plans to K1Z
+#ifndef MCP_CFG_ADAM_FUSED_STEP
+#define MCP_CFG_ADAM_FUSED_STEP 1
+#endif
 // FP64 K1 family for n <= 128: K1Q (warp-specialised pairs), then K1P, then K1S fallbacks
 #ifndef MCP_CFG_K1Q
 #define MCP_CFG_K1Q 1

@@ -225,7 +225,12 @@ const char* mcp_lbfgs_batch_errors(void);
  *   opts[8] = {step_size, reduced_step_size, epoch_len, batch, beta1, beta2, eps, max_epochs}
  *   x_out / g_out: best iterate and its estimate gradient; f_out: best estimate
  *   trace_f / trace_t: estimate at x0 and after every epoch, seconds since start
- *   info[3] = {inner iterations, reason (0 iteration cap, 1 learning-rate exhausted), trace rows}
+ *   info[4] = {inner iterations, reason (0 iteration cap, 1 learning-rate exhausted), trace rows,
+ *              epochs drawn ahead and never run (0 or 1)}.  The next epoch's sample() call is
+ *              made while the GPU runs the current epoch; when the run stops on the learning-rate
+ *              rule that last draw was not needed, and a caller that wants its generator left
+ *              exactly where the reference leaves it restores the state it saved before that
+ *              call (the Python layer does).
  */
 typedef int (*mcp_sample_fn)(int64_t* idx, int64_t count, void* user);
 int mcp_gather_rows(mcp_ctx* ctx, const int64_t* idx, int64_t s, void* dst, int64_t ld_dst,

@@ -367,7 +367,7 @@ class Context:
         g = np.empty(N)
         tf = np.empty(cap)
         tt = np.empty(cap)
-        info = np.zeros(3, dtype=np.int64)
+        info = np.zeros(4, dtype=np.int64)
         f = ctypes.c_double()
         err: list[BaseException] = []
 
@@ -387,7 +387,7 @@ class Context:
             raise err[0]
         self._check(rc, "mcp_adam")
         k = int(info[2])
-        return {"x": x, "g": g, "f": f.value, "n_iter": int(info[0]),
+        return {"x": x, "g": g, "f": f.value, "n_iter": int(info[0]), "unused_draws": int(info[3]),
                 "reason": ("iteration cap", "learning-rate exhausted")[int(info[1])],
                 "trace": list(zip(tf[:k].tolist(), tt[:k].tolist()))}
 

@@ -103,7 +103,8 @@ struct AdamRun {
   int64_t *idx = nullptr, *eidx = nullptr;
   int* it_dev = nullptr;
   unsigned* counter = nullptr;
-  int64_t* h_idx = nullptr;
+  int64_t* h_idx = nullptr;    // two staging halves: the running epoch and the one sampled ahead
+  int64_t h_idx_half = 0;
   double* h_bc = nullptr;
   double* h_scal = nullptr;  // [lr, f_est]
   K1ZAdam zadam;   // the update fused into K1Z's finish when the batch plans to K1Z
@@ -213,7 +214,8 @@ struct AdamRun {
         (rc = alloc(lr_dev, 1)) || (rc = alloc(eidx, n_est)) || (rc = alloc(counter, 1)))
       return rc;
     CUDA_TRY(c, cudaMemset(counter, 0, sizeof(unsigned)));
-    CUDA_TRY(c, cudaMallocHost(&h_idx, sizeof(int64_t) * std::max(epoch_len * batch, n_est)));
+    h_idx_half = std::max(epoch_len * batch, n_est);
+    CUDA_TRY(c, cudaMallocHost(&h_idx, sizeof(int64_t) * 2 * h_idx_half));
     CUDA_TRY(c, cudaMallocHost(&h_bc, sizeof(double) * 2 * epoch_len));
     CUDA_TRY(c, cudaMallocHost(&h_scal, sizeof(double) * 4));
     cudaStream_t s = c->stream;
@@ -398,21 +400,30 @@ extern "C" int mcp_adam(mcp_ctx* c, int d, int r, int mode, const double* x0, co
   double lr = step_size;
   int64_t t = 0, n_iter = 0;
   int increases = 0, reason = 0;
-  for (int64_t epoch = 0; epoch < max_epochs; ++epoch) {
-    // the previous epoch's graph replays must be done with the pinned staging before reuse
-    CUDA_TRY(c, cudaStreamSynchronize(s));
-    if (sample(R.h_idx, epoch_len * batch, user) != 0)
+  // one epoch's indices into a staging half, checked (optimize.py:409: rng.integers(0, p, ...))
+  auto draw = [&](int64_t* buf) -> int {
+    if (sample(buf, epoch_len * batch, user) != 0)
       return c->fail(MCP_ERR_ARG, "sampling callback failed");
     for (int64_t l = 0; l < epoch_len * batch; ++l)
-      if (R.h_idx[l] < 0 || R.h_idx[l] >= c->p)
-        return c->fail(MCP_ERR_ARG, "row index out of range");
+      if (buf[l] < 0 || buf[l] >= c->p) return c->fail(MCP_ERR_ARG, "row index out of range");
+    return MCP_OK;
+  };
+  int cur = 0;
+  bool ahead = false;   // the next epoch's indices are already in the other half
+  for (int64_t epoch = 0; epoch < max_epochs; ++epoch) {
+    int64_t* hb = R.h_idx + (size_t)cur * R.h_idx_half;
+    if (!ahead) {
+      // (the estimate's synchronisation ended every copy out of this half)
+      CUDA_TRY(c, cudaStreamSynchronize(s));
+      if ((rc = draw(hb))) return rc;
+    }
     for (int64_t k = 0; k < epoch_len; ++k) {
       const double tt = (double)(t + k + 1);
       R.h_bc[2 * k] = 1.0 - std::pow(beta1, tt);
       R.h_bc[2 * k + 1] = 1.0 - std::pow(beta2, tt);
     }
     R.h_scal[0] = lr;
-    CUDA_TRY(c, cudaMemcpyAsync(R.idx, R.h_idx, sizeof(int64_t) * epoch_len * batch,
+    CUDA_TRY(c, cudaMemcpyAsync(R.idx, hb, sizeof(int64_t) * epoch_len * batch,
                                 cudaMemcpyHostToDevice, s));
     CUDA_TRY(c, cudaMemcpyAsync(R.bc, R.h_bc, sizeof(double) * 2 * epoch_len,
                                 cudaMemcpyHostToDevice, s));
@@ -427,6 +438,14 @@ extern "C" int mcp_adam(mcp_ctx* c, int d, int r, int mode, const double* x0, co
     }
     t += epoch_len;
     n_iter += epoch_len;
+    // while the GPU runs this epoch, the host draws the next one (the draws do not depend on
+    // the epoch's outcome; if the run stops here the caller rewinds its generator: info[3])
+    ahead = false;
+    if (epoch + 1 < max_epochs) {
+      if ((rc = draw(R.h_idx + (size_t)(cur ^ 1) * R.h_idx_half))) return rc;
+      ahead = true;
+    }
+    cur ^= 1;
     double f_est = 0.0;
     if ((rc = R.estimate(&f_est))) return rc;
     push_trace(f_est);
@@ -458,5 +477,6 @@ extern "C" int mcp_adam(mcp_ctx* c, int d, int r, int mode, const double* x0, co
   info[0] = n_iter;
   info[1] = reason;
   info[2] = std::min(n_trace, trace_cap);
+  info[3] = (reason == 1 && ahead) ? 1 : 0;   // epochs drawn ahead and never run
   return MCP_OK;
 }

@@ -211,7 +211,12 @@ def adam_minimize(obs: ObservationSet, d: int, r_hat: int, x0: np.ndarray, cfg: 
         raise ValueError("model variables and alpha must be finite")
     est_idx = rng.choice(p, size=min(cfg.estimate_samples, p), replace=False)
 
+    before_last_draw: list[dict] = []
+
     def sample(count: int) -> np.ndarray:
+        # the library draws the next epoch while the GPU runs the current one; if the run then
+        # stops, that epoch was never needed and the generator is rewound below
+        before_last_draw[:] = [rng.bit_generator.state]
         out = np.empty(count, dtype=np.int64)
         for k in range(count // cfg.batch):
             out[k * cfg.batch:(k + 1) * cfg.batch] = rng.integers(0, p, size=cfg.batch)
@@ -221,6 +226,8 @@ def adam_minimize(obs: ObservationSet, d: int, r_hat: int, x0: np.ndarray, cfg: 
     opts = (cfg.step_size, cfg.reduced_step_size, cfg.epoch_len, cfg.batch, cfg.beta1,
             cfg.beta2, cfg.eps, cfg.max_epochs)
     out = ctx.adam(x, n, d, r_hat, mode, opts, est_idx, sample)
+    if out["unused_draws"] and before_last_draw:
+        rng.bit_generator.state = before_last_draw[0]   # leave rng where the reference leaves it
     lam, A = unpack(out["x"], n, r_hat)
     return RunReport(lam=lam, A=A, f=out["f"], grad_inf_norm=float(np.abs(out["g"]).max()),
                      n_fg=out["n_iter"], n_steps=out["n_iter"],

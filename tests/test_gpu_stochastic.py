@@ -46,10 +46,12 @@ def test_device_adam_bitwise_vs_restated_reference_with_gpu_gradients(golden):
     cfg, V, lam, A = instances.config_instance("c1")
     x0 = om.pack(lam, A)
     obs = mcp.ObservationSet(V)
-    dev = mcp.adam_minimize(obs, cfg.d, cfg.r, x0, mcp.AdamConfig(**instances.ADAM_C1),
-                            np.random.default_rng(instances.ADAM_SEED))
-    host = ao.adam(V, cfg.d, cfg.r, x0, np.random.default_rng(instances.ADAM_SEED),
-                   fg_fn=_gpu_fg, **instances.ADAM_C1)
+    rng_dev = np.random.default_rng(instances.ADAM_SEED)
+    rng_host = np.random.default_rng(instances.ADAM_SEED)
+    dev = mcp.adam_minimize(obs, cfg.d, cfg.r, x0, mcp.AdamConfig(**instances.ADAM_C1), rng_dev)
+    host = ao.adam(V, cfg.d, cfg.r, x0, rng_host, fg_fn=_gpu_fg, **instances.ADAM_C1)
+    # the epoch drawn ahead of a stopping decision is rewound: same generator state as the reference
+    assert rng_dev.bit_generator.state == rng_host.bit_generator.state
     assert dev.reason == host["reason"] == str(golden["adam_c1"]["reason"])
     assert dev.n_fg == host["n_iter"] == int(golden["adam_c1"]["n_fg"])
     assert np.array_equal(np.array([t[0] for t in dev.trace]), np.array(host["trace_f"]))
@@ -98,11 +100,13 @@ def test_device_adam_bitwise_on_the_single_launch_path():
     x0 = om.pack(lam, A)
     cfg = dict(epoch_len=12, batch=40, estimate_samples=150, max_epochs=4)
     obs = mcp.ObservationSet(V)
-    dev = mcp.adam_minimize(obs, d, r, x0, mcp.AdamConfig(**cfg), np.random.default_rng(9))
+    rng_dev, rng_host = np.random.default_rng(9), np.random.default_rng(9)
+    dev = mcp.adam_minimize(obs, d, r, x0, mcp.AdamConfig(**cfg), rng_dev)
     sub = mcp.ObservationSet(V[:, :40])
     mcp.fg_implicit(sub, lam, A, d)
     assert sub.device_context().last_variant.startswith("k1z_fg_small")
-    host = ao.adam(V, d, r, x0, np.random.default_rng(9), fg_fn=_gpu_fg, **cfg)
+    host = ao.adam(V, d, r, x0, rng_host, fg_fn=_gpu_fg, **cfg)
+    assert rng_dev.bit_generator.state == rng_host.bit_generator.state
     assert dev.n_fg == host["n_iter"] and dev.reason == host["reason"]
     assert np.array_equal(np.array([t[0] for t in dev.trace]), np.array(host["trace_f"]))
     assert np.array_equal(mcp.pack(dev.lam, dev.A), host["x"])

@@ -26,6 +26,7 @@
 // are fixed-order reductions (deterministic, summed in a different order than numpy's).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -34,8 +35,11 @@
 #include <vector>
 
 #include "ctx.h"
+#include "pdl.h"
 
 using namespace mcp_internal;
+using mcp::launch_pdl;
+using mcp::pdl_enter;
 
 namespace {
 
@@ -74,6 +78,9 @@ struct LbDev {
   const int* act;
   double* Xb;   // batched K1 layout [lam_all (k r) ; A_all (n x k r)] or nullptr (k == 1)
   double* st_host;   // mapped pinned copy of the stats records (written by the probe kernel)
+  unsigned long long* seq_dev;    // per run: rounds whose record has been written
+  unsigned long long* seq_host;   // the same count in mapped pinned memory, stored after the
+                                  // record: the host polls it instead of synchronising the stream
   int r;
   int64_t n;
   __device__ int action(int s) const { return act[s] & 7; }
@@ -145,6 +152,7 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
 
 // SAVE: the last trial becomes the saved best (before this round overwrites it)
 __global__ void k_lbb_save(LbDev D) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
   const int s = blockIdx.y;
   if (!(D.act[s] & ACT_SAVE)) return;
   const double *t = D.t(s), *ot = D.ot(s);
@@ -158,6 +166,7 @@ __global__ void k_lbb_save(LbDev D) {
 
 // INIT: x0's evaluation lives in OT; take it as [f; g] of x, statistics, ring reset
 __global__ void k_lbb_init_stats(LbDev D) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
   __shared__ double red[33];
   const int s = blockIdx.y;
   const double* out = D.ot(s);
@@ -208,6 +217,7 @@ __global__ void k_lbb_init_stats(LbDev D) {
 // ACC_T / ACC_B: s = xs - x, y = gs - g into ring slot `head`, x <- xs, g <- gs; then the
 // curvature test (optimize.py:330-332) and the ring update in the run's last block
 __global__ void k_lbb_accept(LbDev D) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
   __shared__ double red[33];
   const int s = blockIdx.y, a = D.action(s);
   if (a != ACT_ACC_T && a != ACT_ACC_B) return;
@@ -282,6 +292,7 @@ __global__ void k_lbb_accept(LbDev D) {
 // initial step (optimize.py:307-322).  When the window fits (stage != 0), g and the (s, y)
 // window are staged in shared memory first so the 2m+1 dependent passes run at smem latency.
 __global__ void __launch_bounds__(LB_DIR_T) k_lbb_direction(LbDev D, int stage) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
   extern __shared__ double sm[];
   __shared__ double red[33];
   __shared__ double alpha_s[65];
@@ -421,6 +432,7 @@ __global__ void __launch_bounds__(LB_DIR_T) k_lbb_direction(LbDev D, int stage) 
 // trial point xa = x + a * p (optimize.py:187); phase 0 of INIT: xa = x (evaluate x0).
 // Also scatters the trial into the batched K1 layout when k > 1.
 __global__ void k_lbb_trial(LbDev D, int init_phase0) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
   const int s = blockIdx.y, act = D.action(s);
   const double* x = D.x(s);
   const double* p = D.p(s);
@@ -442,6 +454,7 @@ __global__ void k_lbb_trial(LbDev D, int init_phase0) {
 
 // ga . p and the finiteness of the trial point, finished by the run's last block
 __global__ void k_lbb_probe_stats(LbDev D) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
   __shared__ double red[33];
   const int s = blockIdx.y, act = D.action(s);
   if (act == ACT_IDLE) return;
@@ -474,11 +487,16 @@ __global__ void k_lbb_probe_stats(LbDev D) {
   // the whole record of this run, straight into mapped host memory (no D2H copy node)
   double* h = D.st_host + (int64_t)s * S_COUNT;
   for (int i = 0; i < S_COUNT; ++i) h[i] = st[i];
+  __threadfence_system();   // the record before the count that announces it
+  const unsigned long long v = D.seq_dev[s] + 1;
+  D.seq_dev[s] = v;
+  *reinterpret_cast<volatile unsigned long long*>(D.seq_host + s) = v;
 }
 
 // actions and host-chosen steps of the round, pulled from mapped host memory by one tiny kernel
 __global__ void k_lbb_pull(const int* __restrict__ h_act, const double* __restrict__ h_a,
                            int* __restrict__ d_act, double* __restrict__ d_a, int k) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
   for (int s = threadIdx.x; s < k; s += blockDim.x) {
     d_act[s] = h_act[s];
     d_a[s] = h_a[s];
@@ -608,6 +626,8 @@ struct LbEngine {
   double* h_st = nullptr;  // pinned, k x S_COUNT
   double* h_x = nullptr;   // pinned, k x N
   int* d_act = nullptr;
+  unsigned long long* h_seq = nullptr;        // pinned, k
+  std::vector<unsigned long long> expected;   // records announced so far, per run
   GraphEntry g_init, g_round;
 
   ~LbEngine() {
@@ -616,7 +636,7 @@ struct LbEngine {
       if (g->graph) cudaGraphDestroy(g->graph);
     }
     for (void* p : dev) cudaFree(p);
-    for (void* p : {(void*)h_act, (void*)h_a, (void*)h_st, (void*)h_x})
+    for (void* p : {(void*)h_act, (void*)h_a, (void*)h_st, (void*)h_x, (void*)h_seq})
       if (p) cudaFreeHost(p);
   }
 
@@ -646,11 +666,11 @@ struct LbEngine {
 
   int enqueue_round_tail() {   // direction (for ACC / INIT runs) -> trial -> fg -> probe stats
     cudaStream_t s = c->stream;
-    k_lbb_direction<<<dim3(1, k), dir_threads, dir_smem, s>>>(D, dir_smem ? 1 : 0);
-    k_lbb_trial<<<dim3(nb, k), LB_T, 0, s>>>(D, 0);
+    CUDA_TRY(c, launch_pdl(k_lbb_direction, dim3(1, k), dim3(dir_threads), dir_smem, s, D, dir_smem ? 1 : 0));
+    CUDA_TRY(c, launch_pdl(k_lbb_trial, dim3(nb, k), dim3(LB_T), 0, s, D, 0));
     int rc = enqueue_fg();
     if (rc) return rc;
-    k_lbb_probe_stats<<<dim3(nb, k), LB_T, 0, s>>>(D);
+    CUDA_TRY(c, launch_pdl(k_lbb_probe_stats, dim3(nb, k), dim3(LB_T), 0, s, D));
     CUDA_TRY(c, cudaGetLastError());
     return MCP_OK;
   }
@@ -665,9 +685,36 @@ struct LbEngine {
     return MCP_OK;
   }
 
+  // Launch a round and wait for the records of its active runs.  The probe kernel stores each
+  // run's count into mapped host memory after the record, so the host polls those words (a PCIe
+  // write away from the kernel) instead of paying a stream synchronisation per evaluation.
   int replay(GraphEntry& ge) {
     CUDA_TRY(c, cudaGraphLaunch(ge.exec, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (!MCP_CFG_LBFGS_POLL) {
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      for (int s = 0; s < k; ++s)
+        if ((h_act[s] & 7) != ACT_IDLE) ++expected[s];
+      return MCP_OK;
+    }
+    for (int s = 0; s < k; ++s) {
+      if ((h_act[s] & 7) == ACT_IDLE) continue;
+      const unsigned long long want = ++expected[s];
+      volatile unsigned long long* w = h_seq + s;
+      unsigned spins = 0;
+      while (*w < want) {
+        if ((++spins & 0x3fffu) == 0) {
+          // every 16k polls: has the stream failed, or finished without announcing the record?
+          const cudaError_t q = cudaStreamQuery(c->stream);
+          if (q == cudaSuccess) {
+            if (*w < want) return c->fail(MCP_ERR_CUDA, "L-BFGS round finished without its record");
+          } else if (q != cudaErrorNotReady) {
+            (void)cudaGetLastError();
+            return c->fail(MCP_ERR_CUDA, std::string("L-BFGS round: ") + cudaGetErrorString(q));
+          }
+        }
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
     return MCP_OK;
   }
 
@@ -710,23 +757,29 @@ struct LbEngine {
     CUDA_TRY(c, cudaMallocHost(&h_a, sizeof(double) * K));
     CUDA_TRY(c, cudaMallocHost(&h_st, sizeof(double) * K * S_COUNT));
     CUDA_TRY(c, cudaMallocHost(&h_x, sizeof(double) * K * N));
+    CUDA_TRY(c, cudaMallocHost(&h_seq, sizeof(unsigned long long) * K));
+    std::memset(h_seq, 0, sizeof(unsigned long long) * K);
+    expected.assign(K, 0ull);
+    if ((rc = alloc(D.seq_dev, K))) return rc;
+    CUDA_TRY(c, cudaMemset(D.seq_dev, 0, sizeof(unsigned long long) * K));
+    D.seq_host = h_seq;
     D.st_host = h_st;   // pinned memory is device-mapped under UVA
     cudaStream_t s = c->stream;
     // init: evaluate x0 (trial = x), statistics, direction, first probe
     if ((rc = capture(g_init, [&]() -> int {
            CUDA_TRY(c, cudaMemcpyAsync(D.X, h_x, sizeof(double) * K * N, cudaMemcpyHostToDevice, s));
            CUDA_TRY(c, cudaMemcpyAsync(d_act, h_act, sizeof(int) * K, cudaMemcpyHostToDevice, s));
-           k_lbb_trial<<<dim3(nb, k), LB_T, 0, s>>>(D, 1);
+           CUDA_TRY(c, launch_pdl(k_lbb_trial, dim3(nb, k), dim3(LB_T), 0, s, D, 1));
            int e = enqueue_fg();
            if (e) return e;
-           k_lbb_init_stats<<<dim3(nb, k), LB_T, 0, s>>>(D);
+           CUDA_TRY(c, launch_pdl(k_lbb_init_stats, dim3(nb, k), dim3(LB_T), 0, s, D));
            return enqueue_round_tail();
          })))
       return rc;
     if ((rc = capture(g_round, [&]() -> int {
-           k_lbb_pull<<<1, 32, 0, s>>>(h_act, h_a, d_act, D.ah, k);
-           k_lbb_save<<<dim3(nb, k), LB_T, 0, s>>>(D);
-           k_lbb_accept<<<dim3(nb, k), LB_T, 0, s>>>(D);
+           CUDA_TRY(c, launch_pdl(k_lbb_pull, dim3(1), dim3(32), 0, s, (const int*)h_act, (const double*)h_a, d_act, D.ah, k));
+           CUDA_TRY(c, launch_pdl(k_lbb_save, dim3(nb, k), dim3(LB_T), 0, s, D));
+           CUDA_TRY(c, launch_pdl(k_lbb_accept, dim3(nb, k), dim3(LB_T), 0, s, D));
            return enqueue_round_tail();
          })))
       return rc;

@@ -55,6 +55,11 @@
 #ifndef MCP_CFG_ADAM_FUSED_STEP
 #define MCP_CFG_ADAM_FUSED_STEP 1
 #endif
+// device L-BFGS: the host polls each round's record count in mapped memory instead of
+// synchronising the stream after every evaluation
+#ifndef MCP_CFG_LBFGS_POLL
+#define MCP_CFG_LBFGS_POLL 1
+#endif
 // FP64 K1 family for n <= 128: K1Q (warp-specialised pairs), then K1P, then K1S fallbacks
 #ifndef MCP_CFG_K1Q
 #define MCP_CFG_K1Q 1

@@ -47,6 +47,10 @@ constexpr int LB_T = 256;        // threads of the streaming kernels
 constexpr int LB_DIR_T = 1024;   // the one-CTA-per-run two-loop kernel (large N)
 constexpr int LB_NP = 6;         // partial sums per block
 constexpr int LB_MAX_BLOCKS = 296;
+// one block per run (N <= LB_T) and the fused round prologue up to here.  Measured against the
+// separate kernels (tools/lbfgs_small_ab.py): N = 105 45.0 vs 49.4 us per step; forcing one
+// block per run at N = 1010 / 2010 loses (88.3 vs 81.1, 87.5 vs 75.0 us per step)
+constexpr int64_t LB_SMALL_N = 256;
 
 // actions (low 3 bits) + flag
 enum { ACT_PROBE = 0, ACT_ACC_T = 1, ACT_ACC_B = 2, ACT_IDLE = 3, ACT_INIT = 4, ACT_SAVE = 8 };
@@ -151,8 +155,7 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   for (int64_t j = blockIdx.x * (int64_t)LB_T + threadIdx.x; j < D.N; j += (int64_t)gridDim.x * LB_T)
 
 // SAVE: the last trial becomes the saved best (before this round overwrites it)
-__global__ void k_lbb_save(LbDev D) {
-  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+__device__ __forceinline__ void lbb_save(const LbDev& D) {
   const int s = blockIdx.y;
   if (!(D.act[s] & ACT_SAVE)) return;
   const double *t = D.t(s), *ot = D.ot(s);
@@ -163,6 +166,11 @@ __global__ void k_lbb_save(LbDev D) {
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) ob[0] = ot[0];
 }
+__global__ void k_lbb_save(LbDev D) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+  lbb_save(D);
+}
+
 
 // INIT: x0's evaluation lives in OT; take it as [f; g] of x, statistics, ring reset
 __global__ void k_lbb_init_stats(LbDev D) {
@@ -216,8 +224,7 @@ __global__ void k_lbb_init_stats(LbDev D) {
 
 // ACC_T / ACC_B: s = xs - x, y = gs - g into ring slot `head`, x <- xs, g <- gs; then the
 // curvature test (optimize.py:330-332) and the ring update in the run's last block
-__global__ void k_lbb_accept(LbDev D) {
-  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+__device__ __forceinline__ void lbb_accept(const LbDev& D) {
   __shared__ double red[33];
   const int s = blockIdx.y, a = D.action(s);
   if (a != ACT_ACC_T && a != ACT_ACC_B) return;
@@ -287,12 +294,16 @@ __global__ void k_lbb_accept(LbDev D) {
   st[S_KEEP] = keep ? 1.0 : 0.0;
   st[S_F] = outx[0];
 }
+__global__ void k_lbb_accept(LbDev D) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+  lbb_accept(D);
+}
+
 
 // Two-loop recursion (optimize.py:149-168) in one CTA per run, then the descent check and the
 // initial step (optimize.py:307-322).  When the window fits (stage != 0), g and the (s, y)
 // window are staged in shared memory first so the 2m+1 dependent passes run at smem latency.
-__global__ void __launch_bounds__(LB_DIR_T) k_lbb_direction(LbDev D, int stage) {
-  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+__device__ __forceinline__ void lbb_direction(const LbDev& D, int stage) {
   extern __shared__ double sm[];
   __shared__ double red[33];
   __shared__ double alpha_s[65];
@@ -428,11 +439,15 @@ __global__ void __launch_bounds__(LB_DIR_T) k_lbb_direction(LbDev D, int stage) 
     D.a0[run] = a0;
   }
 }
+__global__ void __launch_bounds__(LB_DIR_T) k_lbb_direction(LbDev D, int stage) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+  lbb_direction(D, stage);
+}
+
 
 // trial point xa = x + a * p (optimize.py:187); phase 0 of INIT: xa = x (evaluate x0).
 // Also scatters the trial into the batched K1 layout when k > 1.
-__global__ void k_lbb_trial(LbDev D, int init_phase0) {
-  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+__device__ __forceinline__ void lbb_trial(const LbDev& D, int init_phase0) {
   const int s = blockIdx.y, act = D.action(s);
   const double* x = D.x(s);
   const double* p = D.p(s);
@@ -450,6 +465,35 @@ __global__ void k_lbb_trial(LbDev D, int init_phase0) {
         D.Xb[R + (int64_t)s * nr + (j - D.r)] = v;
     }
   }
+}
+__global__ void k_lbb_trial(LbDev D, int init_phase0) {
+  pdl_enter();   // chained under programmatic dependent launch: wait, then let the successor launch
+  lbb_trial(D, init_phase0);
+}
+
+
+// Small problems (one block per run: N <= LB_SMALL_N = LB_T): the round's prologue -- pull the host's
+// actions and steps, save, accept, two-loop direction, trial point -- as ONE kernel instead of
+// five launches; the phases are the bodies above, separated by block barriers (one block per
+// run, so every "last block" is this block and global writes are visible after the barrier).
+__global__ void __launch_bounds__(LB_T) k_lbb_round_small(LbDev D, const int* __restrict__ h_act,
+                                                          const double* __restrict__ h_a,
+                                                          int* __restrict__ d_act,
+                                                          double* __restrict__ d_a, int stage) {
+  pdl_enter();
+  const int s = blockIdx.y;
+  if (threadIdx.x == 0) {
+    d_act[s] = h_act[s];
+    d_a[s] = h_a[s];
+  }
+  __syncthreads();
+  lbb_save(D);
+  __syncthreads();
+  lbb_accept(D);
+  __syncthreads();
+  lbb_direction(D, stage);
+  __syncthreads();
+  lbb_trial(D, 0);
 }
 
 // ga . p and the finiteness of the trial point, finished by the run's last block
@@ -616,6 +660,7 @@ struct LbEngine {
   int64_t n = 0, N = 0;
   int nb = 1;
   int dir_threads = LB_DIR_T;
+  bool small = false;   // N <= LB_SMALL_N: one block per run, fused round prologue
   size_t dir_smem = 0;
   EvalPlan pl;   // k == 1: the single evaluation; k > 1: the shared pass over k r columns
   std::vector<void*> dev;
@@ -721,12 +766,14 @@ struct LbEngine {
   int setup() {
     n = c->n;
     N = r + n * r;
-    nb = grid_for(N, LB_T, LB_MAX_BLOCKS);
+    small = MCP_CFG_LBFGS_FUSED_SMALL && N <= LB_SMALL_N;
+    nb = small ? 1 : grid_for(N, LB_T, LB_MAX_BLOCKS);
     dir_threads = N <= 8192 ? 256 : LB_DIR_T;
     const size_t stage_bytes = sizeof(double) * (size_t)N * (2 * (size_t)m + 2);
     dir_smem = stage_bytes <= 192 * 1024 ? stage_bytes : 0;
     int rc;
-    if (dir_smem && !mcp::ensure_dyn_smem((const void*)k_lbb_direction, dir_smem))
+    if (dir_smem && (!mcp::ensure_dyn_smem((const void*)k_lbb_direction, dir_smem) ||
+                     (small && !mcp::ensure_dyn_smem((const void*)k_lbb_round_small, dir_smem))))
       return c->fail(MCP_ERR_CUDA, "cannot raise the two-loop kernel's shared-memory limit");
     const size_t K = (size_t)k, M1 = (size_t)m + 1;
     D.N = N;
@@ -777,6 +824,15 @@ struct LbEngine {
          })))
       return rc;
     if ((rc = capture(g_round, [&]() -> int {
+           if (small) {
+             CUDA_TRY(c, launch_pdl(k_lbb_round_small, dim3(1, k), dim3(LB_T), dir_smem, s, D,
+                                    (const int*)h_act, (const double*)h_a, d_act, D.ah,
+                                    dir_smem ? 1 : 0));
+             int e = enqueue_fg();
+             if (e) return e;
+             CUDA_TRY(c, launch_pdl(k_lbb_probe_stats, dim3(nb, k), dim3(LB_T), 0, s, D));
+             return MCP_OK;
+           }
            CUDA_TRY(c, launch_pdl(k_lbb_pull, dim3(1), dim3(32), 0, s, (const int*)h_act, (const double*)h_a, d_act, D.ah, k));
            CUDA_TRY(c, launch_pdl(k_lbb_save, dim3(nb, k), dim3(LB_T), 0, s, D));
            CUDA_TRY(c, launch_pdl(k_lbb_accept, dim3(nb, k), dim3(LB_T), 0, s, D));

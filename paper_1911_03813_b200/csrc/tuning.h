@@ -60,6 +60,11 @@
 #ifndef MCP_CFG_LBFGS_POLL
 #define MCP_CFG_LBFGS_POLL 1
 #endif
+// device L-BFGS: up to 256 variables (one block per run, e.g. c1) the round prologue (pull, save,
+// accept, direction, trial) is one kernel instead of five launches
+#ifndef MCP_CFG_LBFGS_FUSED_SMALL
+#define MCP_CFG_LBFGS_FUSED_SMALL 1
+#endif
 // FP64 K1 family for n <= 128: K1Q (warp-specialised pairs), then K1P, then K1S fallbacks
 #ifndef MCP_CFG_K1Q
 #define MCP_CFG_K1Q 1

@@ -747,15 +747,11 @@ struct LbEngine {
       volatile unsigned long long* w = h_seq + s;
       unsigned spins = 0;
       while (*w < want) {
-        if ((++spins & 0x3fffu) == 0) {
-          // every 16k polls: has the stream failed, or finished without announcing the record?
-          const cudaError_t q = cudaStreamQuery(c->stream);
-          if (q == cudaSuccess) {
-            if (*w < want) return c->fail(MCP_ERR_CUDA, "L-BFGS round finished without its record");
-          } else if (q != cudaErrorNotReady) {
-            (void)cudaGetLastError();
-            return c->fail(MCP_ERR_CUDA, std::string("L-BFGS round: ") + cudaGetErrorString(q));
-          }
+        if (++spins == 0x4000u) {
+          // ~100 us of polling: a long evaluation (or a fault).  Stop burning the core: wait for
+          // the stream the ordinary way; its status also reports a failed round.
+          CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+          if (*w < want) return c->fail(MCP_ERR_CUDA, "L-BFGS round finished without its record");
         }
       }
     }

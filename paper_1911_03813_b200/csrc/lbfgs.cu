@@ -746,9 +746,11 @@ struct LbEngine {
       const unsigned long long want = ++expected[s];
       volatile unsigned long long* w = h_seq + s;
       unsigned spins = 0;
+      const auto t0 = std::chrono::steady_clock::now();
       while (*w < want) {
-        if (++spins == 0x4000u) {
-          // ~100 us of polling: a long evaluation (or a fault).  Stop burning the core: wait for
+        if ((++spins & 0xffu) == 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(250)) {
+          // 250 us of polling: a long evaluation (or a fault).  Stop burning the core: wait for
           // the stream the ordinary way; its status also reports a failed round.
           CUDA_TRY(c, cudaStreamSynchronize(c->stream));
           if (*w < want) return c->fail(MCP_ERR_CUDA, "L-BFGS round finished without its record");

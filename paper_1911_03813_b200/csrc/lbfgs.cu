@@ -752,8 +752,15 @@ struct LbEngine {
             std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(250)) {
           // 250 us of polling: a long evaluation (or a fault).  Stop burning the core: wait for
           // the stream the ordinary way; its status also reports a failed round.
-          CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-          if (*w < want) return c->fail(MCP_ERR_CUDA, "L-BFGS round finished without its record");
+          const cudaError_t e = cudaStreamSynchronize(c->stream);
+          if (e != cudaSuccess || *w < want) {
+            // keep the cached engine usable: count what actually arrived
+            (void)cudaGetLastError();
+            for (int q = 0; q < k; ++q) expected[q] = h_seq[q];
+            return c->fail(MCP_ERR_CUDA,
+                           e != cudaSuccess ? std::string("L-BFGS round: ") + cudaGetErrorString(e)
+                                            : std::string("L-BFGS round finished without its record"));
+          }
         }
       }
     }

@@ -41,8 +41,8 @@ def main():
         rep = mcp.adam_minimize(obs, cfg.d, cfg.r, x0, ac, np.random.default_rng(1))
         td = time.perf_counter() - t
         t = time.perf_counter()
-        host = ao.adam(V, cfg.d, cfg.r, x0, np.random.default_rng(1), batch=s,
-                       max_epochs=args.cpu_epochs)
+        host = (ao.adam(V, cfg.d, cfg.r, x0, np.random.default_rng(1), batch=s,
+                        max_epochs=args.cpu_epochs) if args.cpu_epochs > 0 else {"n_iter": 0})
         th = time.perf_counter() - t
         print(json.dumps({
             "workload": "t2 (paper Table 2)", "batch": s,
@@ -52,7 +52,8 @@ def main():
                        "us_per_iter_steady": 1e6 * (rep.trace[-1][1] - rep.trace[0][1]) / rep.n_fg,
                        "reason": rep.reason, "f": rep.f},
             "cpu_port": {"inner_iters": host["n_iter"], "s": th,
-                         "iters_per_s": host["n_iter"] / th, "us_per_iter": 1e6 * th / host["n_iter"],
+                         "iters_per_s": host["n_iter"] / th,
+                         "us_per_iter": 1e6 * th / host["n_iter"] if host["n_iter"] else None,
                          "threads": os.cpu_count()},
         }), flush=True)
 
